@@ -1,0 +1,142 @@
+"""O.3 — forward of a set of tree nodes.  Test infrastructure only.
+
+Model: decoder-only, pre-RMSNorm, rotary positions, gated-SiLU MLP, untied
+head ("pre-RMS-norm, rotary positions, gated-SiLU MLP, untied
+output head"), optional Qwen QKV bias.
+
+Tree decoding: "Multiple branching token paths are flattened and evaluated in
+one forward pass.  Positional encodings and attention masks are modified to
+preserve tree structure dependency" (§2.2).  Reading R9: a node's
+position is P + depth; its keys are the committed prefix [0, P) followed by
+its ancestors root..self in depth order (the ancestor-closure mask,
+SPEC.md:70).  The committed prefix holds the *target's* K/V and is read by
+both draft and target (shared KV-cache); every forwarded
+node writes its own K/V into its tree slot — draft values during drafting,
+which the target overwrites during verification (Fig. 3 right).
+
+Layer math for each layer, processed over all nodes before the next layer:
+    h  = rmsnorm(x) * g_attn
+    q,k,v = W_q h (+b_q), W_k h (+b_k), W_v h (+b_v);  RoPE(q, k) at pos
+    store k, v in the node's tree slot
+    per head: a = softmax_{keys}(q.k / sqrt(d_h));  o = sum a v   (GQA: kv head = hq // (n_h/n_kv))
+    x += W_o concat(o) ;  h2 = rmsnorm(x) * g_mlp ;  x += W_d (silu(W_g h2) * (W_u h2))
+Final: logits = Head (rmsnorm(x) * g_final).
+
+mode "exact": float64 throughout.  mode "bf16": additionally rounds to bf16
+(RNE) at the GPU's named rounding points (reading R3): h, h2 and the final
+normed vector; q, k, v after bias and RoPE; the attention output; the
+SiLU-mul activation.  Logits, scores, softmax and the residual stream are
+never rounded.  Every node's arithmetic is a per-row op sequence identical to
+what an autoregressive forward would do at that position, so chain ==
+sequential and path replay hold bitwise.
+"""
+import numpy as np
+
+from synth.configs import ModelConfig
+from synth.weights import tensor_specs, gen_tensor_bits
+from .numerics import bf16_bits_to_f64, round_bf16, rmsnorm, silu, rope_rotate_half
+from .quant import substitute_matrix
+
+LAYER_MATS = ("wq", "wk", "wv", "wo", "wg", "wu", "wd")
+
+
+class TargetWeights:
+    """The target's bf16 weights as float64 arrays (all values exactly bf16)."""
+
+    def __init__(self, cfg: ModelConfig, seed: int, layers=None):
+        self.cfg = cfg
+        self.layers = [dict() for _ in range(cfg.n_layers)]
+        want = set(range(cfg.n_layers)) if layers is None else set(layers)
+        for tid, name, shape, kind, sigma in tensor_specs(cfg):
+            if name.startswith("l"):
+                l = int(name[1:name.index(".")])
+                if l not in want:
+                    continue
+                self.layers[l][name.split(".", 1)[1]] = bf16_bits_to_f64(
+                    gen_tensor_bits(seed, tid, shape, kind, sigma))
+            else:
+                setattr(self, name, bf16_bits_to_f64(gen_tensor_bits(seed, tid, shape, kind, sigma)))
+
+
+def draft_layers(target: TargetWeights, n_resident: int, bits=4, group=64):
+    """Draft model view (SPEC.md:214-222 build_draft_view):
+    layers [0, n_resident) are Shared (the target's own dict); the rest are
+    Substitute: every linear matrix replaced by its dequantized low-bit copy,
+    norms and biases kept (reading R6)."""
+    out = []
+    for l, lw in enumerate(target.layers):
+        if l < n_resident:
+            out.append(lw)
+        else:
+            sub = dict(lw)
+            for m in LAYER_MATS:
+                sub[m] = substitute_matrix(lw[m], bits, group)
+            out.append(sub)
+    return out
+
+
+class KVCache:
+    """Shared KV-cache: committed region [0, P) plus per-node tree slots."""
+
+    def __init__(self, cfg: ModelConfig, max_nodes: int):
+        L, C, nkv, d = cfg.n_layers, cfg.max_context, cfg.n_kv_heads, cfg.head_dim
+        self.cfg = cfg
+        self.K = np.zeros((L, C, nkv, d))
+        self.V = np.zeros((L, C, nkv, d))
+        self.tK = np.zeros((L, max_nodes, nkv, d))
+        self.tV = np.zeros((L, max_nodes, nkv, d))
+        self.P = 0
+
+
+def forward_nodes(cfg: ModelConfig, layers, target: TargetWeights, kv: KVCache,
+                  tokens, slots, positions, ancestors, mode="exact", return_hidden=False):
+    """Forward the given nodes through `layers` (a list of per-layer weight dicts).
+
+    tokens[i], slots[i] (tree slot written), positions[i], ancestors[i] (tree
+    slots root..self).  Returns logits [n, V] (and the final normed hidden)."""
+    R = round_bf16 if mode == "bf16" else (lambda a: a)
+    n = len(tokens)
+    H, nh, nkv, d = cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+    grp = nh // nkv
+    P = kv.P
+    x = [target.embed[int(t)].copy() for t in tokens]
+    inv_sqrt_d = 1.0 / np.sqrt(d)
+    for l, lw in enumerate(layers):
+        qs = []
+        for i in range(n):
+            h = R(rmsnorm(x[i], lw["attn_norm"], cfg.rms_eps))
+            q = lw["wq"] @ h
+            k = lw["wk"] @ h
+            v = lw["wv"] @ h
+            if cfg.qkv_bias:
+                q = q + lw["bq"]
+                k = k + lw["bk"]
+                v = v + lw["bv"]
+            q = q.reshape(nh, d)
+            k = k.reshape(nkv, d)
+            q = np.stack([rope_rotate_half(q[j], positions[i], cfg.rope_theta, d) for j in range(nh)])
+            k = np.stack([rope_rotate_half(k[j], positions[i], cfg.rope_theta, d) for j in range(nkv)])
+            qs.append(R(q))
+            kv.tK[l, slots[i]] = R(k)
+            kv.tV[l, slots[i]] = R(v.reshape(nkv, d))
+        for i in range(n):
+            anc = list(ancestors[i])
+            o = np.empty((nh, d))
+            for hq in range(nh):
+                g = hq // grp
+                Kall = np.concatenate([kv.K[l, :P, g], kv.tK[l, anc, g]])
+                Vall = np.concatenate([kv.V[l, :P, g], kv.tV[l, anc, g]])
+                s = (Kall @ qs[i][hq]) * inv_sqrt_d
+                e = np.exp(s - s.max())
+                p = e / e.sum()
+                o[hq] = p @ Vall
+            o = R(o.reshape(-1))
+            x[i] = x[i] + lw["wo"] @ o
+            h2 = R(rmsnorm(x[i], lw["mlp_norm"], cfg.rms_eps))
+            a = R(silu(lw["wg"] @ h2) * (lw["wu"] @ h2))
+            x[i] = x[i] + lw["wd"] @ a
+    hf = [R(rmsnorm(x[i], target.final_norm, cfg.rms_eps)) for i in range(n)]
+    logits = np.stack([target.head @ hf[i] for i in range(n)])
+    if return_hidden:
+        return logits, np.stack(hf)
+    return logits
