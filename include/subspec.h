@@ -1,0 +1,168 @@
+/*
+ * subspec.h — C-ABI of libsubspec: one SubSpec tree-speculative decode step on a B200.
+ *
+ * Method: Substitute Speculative Decoding (arXiv 2509.18344, §4).  The draft model
+ * reuses the target's GPU-resident layers ("GPU-Resident Layer Sharing"),
+ * replaces every offloaded layer with a low-bit quantized substitute that stays on the GPU
+ * ("Quantized Substitute Weights"; 4-bit, group 64) and shares
+ * the target's KV-cache ("Shared KV-Cache").  It grows a context-aware dynamic
+ * draft tree of depth D with top-k expansion over sharpened cumulative scores (
+ * k = 6, D = 48, T = 0.2).  The target verifies all 1 + kD nodes in one pass
+ * with its offloaded layers streamed from pinned host memory, and the
+ * longest root path matching the target's greedy choices is accepted and committed (greedy
+ * verification).  The committed output equals greedy AR decoding of the
+ * target ("lossless").  Step order follows Eq. 2.
+ *
+ * Conventions:
+ *  - Every function returns ss_status; on error ss_last_error(ctx) describes it.  After any CUDA
+ *    error the context is poisoned: every later call returns SS_ERR_CUDA; only ss_destroy is valid.
+ *  - Ownership: the library never retains a caller pointer after a call returns, except the
+ *    device arena and streams given to ss_create, which the caller keeps alive until ss_destroy.
+ *    Every device allocation of the context is carved from that arena, so arena_bytes is the
+ *    emulated VRAM cap (CUDA context memory is excluded).  The context owns its
+ *    pinned host store (cudaHostAlloc, portable) for offloaded layers.
+ *  - Host pointers: all array arguments below are HOST pointers unless named dev_*; they are
+ *    read/written only during the call.  Calls that return host data synchronise the compute
+ *    stream before returning.
+ *  - Call order: create -> load_weights -> build_substitutes -> prefill ->
+ *    (draft_tree -> verify_tree -> accept_and_commit)*  [or ss_step / ss_generate].  Any other
+ *    order returns SS_ERR_STRUCTURE.  One context per session; no concurrent calls on a context.
+ *  - Capacity: before drafting, D is clamped to D_eff = min(D, floor((max_context - P - 1)/k));
+ *    D_eff = 0 runs an AR step (tree = root only).  SS_ERR_CAPACITY only when P + 1 > max_context,
+ *    detected before any write.
+ *  - Layouts: token ids int32; all weights bf16 [out x in] row-major in the generator's index
+ *    space.
+ */
+#ifndef SUBSPEC_H
+#define SUBSPEC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SS_OK = 0,
+  SS_ERR_INVALID = 1,   /* bad argument, non-finite input, unsupported config */
+  SS_ERR_CAPACITY = 2,  /* context would exceed max_context (checked before any write) */
+  SS_ERR_STRUCTURE = 3, /* call out of order, malformed tree */
+  SS_ERR_BUDGET = 4,    /* arena (VRAM cap) below the minimum footprint */
+  SS_ERR_CUDA = 5       /* CUDA failure; context poisoned */
+} ss_status;
+
+/* Decoder-only model shape (Llama/Qwen family).  hidden, ffn, qkv rows and vocab
+ * must be multiples of 128; head_dim is 64 or 128; n_heads % n_kv_heads == 0. */
+typedef struct {
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, max_context;
+  float rope_theta, rms_eps;
+  int32_t qkv_bias;
+} ss_model_config;
+
+/* Sizes the context provisions buffers for (all >= the values later used). */
+typedef struct {
+  int32_t max_depth;    /* D_max (48) */
+  int32_t max_top_k;    /* k_max (<= 32) */
+  int32_t max_chunk;    /* prefill chunk (256) */
+} ss_limits;
+
+/* Substitute quantization: bits = 4, group_size = 64 are supported. */
+typedef struct { int32_t bits, group_size; } ss_quant_spec;
+
+/* Draft tree parameters: depth D, top-k, sharpening temperature. */
+typedef struct { int32_t depth, top_k; float sharpen_t; } ss_draft_params;
+
+typedef struct {
+  int64_t steps, tokens_emitted, prefill_tokens, gpu_launches;
+  double draft_ms, verify_ms, accept_ms;      /* device time (CUDA events), cumulative */
+  double stream_bytes, stream_busy_ms;        /* host->device layer streaming (copy stream) */
+  int64_t arena_used, arena_cap, ring_bytes, host_pinned_bytes, substitute_bytes;
+  int32_t n_resident, n_offloaded, committed_len, last_d_eff;
+} ss_stats;
+
+typedef struct ss_ctx ss_ctx;
+
+/* Create a context on `device`.  dev_arena/arena_bytes: caller-owned device block (torch), the
+ * VRAM cap.  compute_stream/copy_stream: cudaStream_t handles (may be the same only if
+ * streaming is never needed).  Errors: INVALID (shape), BUDGET (arena too small for fixed parts). */
+ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device, void* dev_arena,
+                    size_t arena_bytes, void* compute_stream, void* copy_stream, ss_ctx** out);
+
+/* Generate the target's bf16 weights with the counter-based generator (seed) on the device and
+ * place them: layers [0, n_resident) resident in the arena, the rest offloaded to the pinned host
+ * store in device layout (App. H P:540 "All decoder layers ... offloaded" is
+ * n_resident = 0).  n_resident = -1: the planner's maximum resident prefix under the cap
+ * (SPEC.md:205-213).  Embedding, final norm and head are always resident. */
+ss_status ss_load_weights(ss_ctx* ctx, uint64_t seed, int32_t n_resident);
+
+/* Build the 4-bit group-64 substitute of every offloaded layer: stream it host->device through
+ * the staging ring and quantize on the device (K1).  Norms/biases are shared. */
+ss_status ss_build_substitutes(ss_ctx* ctx, const ss_quant_spec* q);
+
+/* Start a new session (committed length 0) and prefill `prompt` (n tokens, host) through the
+ * target in chunks of `chunk` tokens.  *out_first_token = greedy token at the
+ * last prompt position, which becomes the root of the first draft tree. */
+ss_status ss_prefill(ss_ctx* ctx, const int32_t* prompt, int32_t n, int32_t chunk, int32_t* out_first_token);
+
+/* Draft pass loop (K2-K5): grow the tree from the current root (the last emitted token; or
+ * root_token >= 0 to override).  Optional host outputs, each [1 + k*D_eff]: tokens, parents,
+ * depths, cumulative log-scores (NULL to skip). *opt_n_nodes receives 1 + k*D_eff. */
+ss_status ss_draft_tree(ss_ctx* ctx, int32_t root_token, const ss_draft_params* p, int32_t* opt_tokens,
+                        int32_t* opt_parents, int32_t* opt_depths, float* opt_scores, int32_t* opt_n_nodes);
+
+/* Verification (K6-K8): one target pass over every node; offloaded layers streamed from the
+ * pinned host store (K7).  Optional host outputs [n_nodes]: target argmax per node and the
+ * top-1/top-2 logit gap (near-tie flags). */
+ss_status ss_verify_tree(ss_ctx* ctx, int32_t* opt_argmax, float* opt_gap);
+
+/* Greedy acceptance + KV commit/compaction (K9).  out_tokens (capacity D+1) receives the
+ * accepted draft tokens followed by the bonus token; *out_n in [1, D+1].  opt_path receives the
+ * committed tree slots (root first, capacity D+1). */
+ss_status ss_accept_and_commit(ss_ctx* ctx, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path);
+
+/* draft_tree + verify_tree + accept_and_commit without host round trips except the emitted tokens. */
+ss_status ss_step(ss_ctx* ctx, const ss_draft_params* p, int32_t* out_tokens, int32_t* out_n);
+
+/* Convenience loop: prefill then steps until max_new tokens (first token included) are emitted.
+ * p->depth = 0 gives plain AR decoding through the same target path.  out_tokens capacity
+ * max_new; opt_tau_hist capacity D+2 (histogram of tokens per step). */
+ss_status ss_generate(ss_ctx* ctx, const int32_t* prompt, int32_t n, int32_t max_new, int32_t chunk,
+                      const ss_draft_params* p, int32_t* out_tokens, int32_t* out_n, int32_t* opt_tau_hist);
+
+ss_status ss_get_stats(ss_ctx* ctx, ss_stats* out);
+ss_status ss_reset_stats(ss_ctx* ctx);
+const char* ss_last_error(ss_ctx* ctx);
+void ss_destroy(ss_ctx* ctx);
+
+/* ---- debug / parity entry points (tests only) ------------------------------------------- */
+/* Device generator for one tensor id (natural row-major bf16 bits) -> host out[rows*cols]. */
+ss_status ss_debug_gen_tensor(ss_ctx* ctx, uint64_t seed, int32_t tid, int64_t rows, int64_t cols,
+                              int32_t kind /*0 mat, 1 gain, 2 bias*/, double sigma, uint16_t* out);
+/* Target bf16 matrix of (layer, group) in fused natural row order -> host [N x K].
+ * groups: 0 qkv [q;k;v], 1 o, 2 gate_up (rows interleaved per 64: gate 64, up 64, ...), 3 down. */
+ss_status ss_debug_read_group(ss_ctx* ctx, int32_t layer, int32_t group, uint16_t* out);
+/* Substitute of an offloaded (layer, group) in canonical form: codes [N x K] u8, s,z [N x K/64] bf16 bits. */
+ss_status ss_debug_get_substitute(ss_ctx* ctx, int32_t layer, int32_t group, uint8_t* codes, uint16_t* s,
+                                  uint16_t* z);
+/* Run the draft GEMV (K2: substitute if offloaded, bf16 if resident) or the target GEMM (K6) of
+ * (layer, group) on host activations x [M x K] (bf16 bits) -> host y [M x N] fp32 (fused row order). */
+ss_status ss_debug_matmul(ss_ctx* ctx, int32_t which /*0 draft K2, 1 target K6*/, int32_t layer, int32_t group,
+                          const uint16_t* x, int32_t M, float* y);
+/* Teacher-forced forward of a depth-major tree (tokens/parents, n nodes) at the current committed
+ * length: which = 0 draft (depth by depth, as the draft loop), 1 target (one pass).  Writes the
+ * tree KV (draft or target values) but commits nothing.  out_logits [n x V] fp32 (host). */
+ss_status ss_debug_forward(ss_ctx* ctx, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
+                           float* out_logits);
+/* Replace the device tree by a given depth-major tree (root first) for verify/accept tests. */
+ss_status ss_debug_set_tree(ss_ctx* ctx, const int32_t* tokens, const int32_t* parents, int32_t n, int32_t top_k);
+/* Committed K/V rows [pos0, pos0+n) of a layer -> host [n_kv x n x head_dim] bf16 bits each. */
+ss_status ss_debug_read_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
+/* Time one launch of the draft dequant-GEMV of (layer, group) with M tokens: average device ms of
+ * `iters` back-to-back launches (CUDA events on the compute stream). */
+ss_status ss_debug_time_matmul(ss_ctx* ctx, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
+                               float* out_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUBSPEC_H */

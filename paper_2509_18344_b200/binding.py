@@ -1,0 +1,272 @@
+"""Thin ctypes binding of libsubspec (include/subspec.h).  Argument marshalling only: every
+step of the decode path runs in the library's CUDA kernels.  PyTorch provides the device arena
+(the emulated VRAM cap) and the two CUDA streams; nothing else.
+
+There is no CPU fallback: if libsubspec.so is missing or no CUDA device is present, construction
+raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from .build import LIB
+
+c_int32, c_int64, c_float, c_double, c_void_p, c_size_t, c_uint64 = (
+    ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t,
+    ctypes.c_uint64)
+
+STATUS = {0: "SS_OK", 1: "SS_ERR_INVALID", 2: "SS_ERR_CAPACITY", 3: "SS_ERR_STRUCTURE", 4: "SS_ERR_BUDGET",
+          5: "SS_ERR_CUDA"}
+
+
+class ModelConfigC(ctypes.Structure):
+    _fields_ = [("n_layers", c_int32), ("hidden", c_int32), ("n_heads", c_int32), ("n_kv_heads", c_int32),
+                ("head_dim", c_int32), ("ffn", c_int32), ("vocab", c_int32), ("max_context", c_int32),
+                ("rope_theta", c_float), ("rms_eps", c_float), ("qkv_bias", c_int32)]
+
+
+class LimitsC(ctypes.Structure):
+    _fields_ = [("max_depth", c_int32), ("max_top_k", c_int32), ("max_chunk", c_int32)]
+
+
+class QuantSpecC(ctypes.Structure):
+    _fields_ = [("bits", c_int32), ("group_size", c_int32)]
+
+
+class DraftParamsC(ctypes.Structure):
+    _fields_ = [("depth", c_int32), ("top_k", c_int32), ("sharpen_t", c_float)]
+
+
+class StatsC(ctypes.Structure):
+    _fields_ = [("steps", c_int64), ("tokens_emitted", c_int64), ("prefill_tokens", c_int64),
+                ("gpu_launches", c_int64), ("draft_ms", c_double), ("verify_ms", c_double),
+                ("accept_ms", c_double), ("stream_bytes", c_double), ("stream_busy_ms", c_double),
+                ("arena_used", c_int64), ("arena_cap", c_int64), ("ring_bytes", c_int64),
+                ("host_pinned_bytes", c_int64), ("substitute_bytes", c_int64), ("n_resident", c_int32),
+                ("n_offloaded", c_int32), ("committed_len", c_int32), ("last_d_eff", c_int32)]
+
+
+P = ctypes.POINTER
+_FUNCS = {
+    "ss_create": [P(ModelConfigC), P(LimitsC), ctypes.c_int, c_void_p, c_size_t, c_void_p, c_void_p, P(c_void_p)],
+    "ss_load_weights": [c_void_p, c_uint64, c_int32],
+    "ss_build_substitutes": [c_void_p, P(QuantSpecC)],
+    "ss_prefill": [c_void_p, c_void_p, c_int32, c_int32, P(c_int32)],
+    "ss_draft_tree": [c_void_p, c_int32, P(DraftParamsC), c_void_p, c_void_p, c_void_p, c_void_p, P(c_int32)],
+    "ss_verify_tree": [c_void_p, c_void_p, c_void_p],
+    "ss_accept_and_commit": [c_void_p, c_void_p, P(c_int32), c_void_p],
+    "ss_step": [c_void_p, P(DraftParamsC), c_void_p, P(c_int32)],
+    "ss_generate": [c_void_p, c_void_p, c_int32, c_int32, c_int32, P(DraftParamsC), c_void_p, P(c_int32), c_void_p],
+    "ss_get_stats": [c_void_p, P(StatsC)],
+    "ss_reset_stats": [c_void_p],
+    "ss_debug_gen_tensor": [c_void_p, c_uint64, c_int32, c_int64, c_int64, c_int32, c_double, c_void_p],
+    "ss_debug_read_group": [c_void_p, c_int32, c_int32, c_void_p],
+    "ss_debug_get_substitute": [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p],
+    "ss_debug_matmul": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p],
+    "ss_debug_forward": [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p],
+    "ss_debug_set_tree": [c_void_p, c_void_p, c_void_p, c_int32, c_int32],
+    "ss_debug_read_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
+    "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
+}
+EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy"]
+
+_lib = None
+
+
+def load_library(path=LIB):
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libsubspec.so not built ({path}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    for name, args in _FUNCS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.ss_last_error.argtypes = [c_void_p]
+    lib.ss_last_error.restype = ctypes.c_char_p
+    lib.ss_destroy.argtypes = [c_void_p]
+    lib.ss_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+class SubSpecError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    return a.ctypes.data_as(c_void_p) if a is not None else None
+
+
+def model_config_c(cfg):
+    return ModelConfigC(cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn, cfg.vocab,
+                        cfg.max_context, cfg.rope_theta, cfg.rms_eps, int(cfg.qkv_bias))
+
+
+class SubSpec:
+    """One decode session on one GPU: the C-ABI context plus its torch-owned arena and streams."""
+
+    def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("SubSpec needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.cfg = cfg
+        self.device = device
+        self.limits = LimitsC(max_depth, max_top_k, max_chunk)
+        self.arena = torch.empty(int(arena_bytes), dtype=torch.uint8, device=f"cuda:{device}")
+        self.compute_stream = torch.cuda.Stream(device=device)
+        self.copy_stream = torch.cuda.Stream(device=device)
+        torch.cuda.synchronize(device)
+        ctx = c_void_p()
+        st = self.lib.ss_create(ctypes.byref(model_config_c(cfg)), ctypes.byref(self.limits), device,
+                                c_void_p(self.arena.data_ptr()), c_size_t(int(arena_bytes)),
+                                c_void_p(self.compute_stream.cuda_stream), c_void_p(self.copy_stream.cuda_stream),
+                                ctypes.byref(ctx))
+        if st:
+            raise SubSpecError(st, "ss_create failed")
+        self.ctx = ctx
+
+    def _check(self, st):
+        if st:
+            raise SubSpecError(st, self.lib.ss_last_error(self.ctx).decode())
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.ss_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- the method ---------------------------------------------------------------------
+    def load_weights(self, seed, n_resident=0):
+        self._check(self.lib.ss_load_weights(self.ctx, c_uint64(seed), n_resident))
+
+    def build_substitutes(self, bits=4, group=64):
+        self._check(self.lib.ss_build_substitutes(self.ctx, ctypes.byref(QuantSpecC(bits, group))))
+
+    def prefill(self, prompt, chunk=256):
+        p = np.ascontiguousarray(prompt, dtype=np.int32)
+        out = c_int32()
+        self._check(self.lib.ss_prefill(self.ctx, _ptr(p), len(p), chunk, ctypes.byref(out)))
+        return out.value
+
+    def draft_tree(self, depth, top_k, sharpen_t, root_token=-1, want_tree=True):
+        n_max = 1 + top_k * depth
+        arrs = [np.zeros(n_max, np.int32), np.zeros(n_max, np.int32), np.zeros(n_max, np.int32),
+                np.zeros(n_max, np.float32)] if want_tree else [None] * 4
+        n = c_int32()
+        self._check(self.lib.ss_draft_tree(self.ctx, root_token, ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)),
+                                           *[_ptr(a) for a in arrs], ctypes.byref(n)))
+        if not want_tree:
+            return n.value
+        return {"tokens": arrs[0][:n.value], "parents": arrs[1][:n.value], "depths": arrs[2][:n.value],
+                "scores": arrs[3][:n.value]}
+
+    def verify_tree(self, n_nodes=None, want=True):
+        if not want:
+            self._check(self.lib.ss_verify_tree(self.ctx, None, None))
+            return None
+        am = np.zeros(n_nodes, np.int32)
+        gap = np.zeros(n_nodes, np.float32)
+        self._check(self.lib.ss_verify_tree(self.ctx, _ptr(am), _ptr(gap)))
+        return am, gap
+
+    def accept_and_commit(self, cap):
+        toks = np.zeros(cap, np.int32)
+        path = np.zeros(cap, np.int32)
+        n = c_int32()
+        self._check(self.lib.ss_accept_and_commit(self.ctx, _ptr(toks), ctypes.byref(n), _ptr(path)))
+        return toks[:n.value].tolist(), path[:n.value].tolist()
+
+    def step(self, depth, top_k, sharpen_t):
+        toks = np.zeros(depth + 1, np.int32)
+        n = c_int32()
+        self._check(self.lib.ss_step(self.ctx, ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)), _ptr(toks),
+                                     ctypes.byref(n)))
+        return toks[:n.value].tolist()
+
+    def generate(self, prompt, max_new, depth, top_k, sharpen_t, chunk=256):
+        p = np.ascontiguousarray(prompt, dtype=np.int32)
+        out = np.zeros(max_new, np.int32)
+        hist = np.zeros(depth + 2, np.int32)
+        n = c_int32()
+        self._check(self.lib.ss_generate(self.ctx, _ptr(p), len(p), max_new, chunk,
+                                         ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)), _ptr(out),
+                                         ctypes.byref(n), _ptr(hist)))
+        return out[:n.value].tolist(), hist
+
+    def stats(self):
+        s = StatsC()
+        self._check(self.lib.ss_get_stats(self.ctx, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in StatsC._fields_}
+
+    def reset_stats(self):
+        self._check(self.lib.ss_reset_stats(self.ctx))
+
+    # ---- debug / parity -----------------------------------------------------------------
+    def debug_gen_tensor(self, seed, tid, shape, kind, sigma):
+        rows, cols = (shape[0], shape[1]) if len(shape) == 2 else (1, shape[0])
+        out = np.zeros(rows * cols, np.uint16)
+        self._check(self.lib.ss_debug_gen_tensor(self.ctx, c_uint64(seed), tid, rows, cols,
+                                                 {"mat": 0, "gain": 1, "bias": 2}[kind], sigma, _ptr(out)))
+        return out.reshape(shape)
+
+    def group_shape(self, group):
+        c = self.cfg
+        return [(c.qkv_rows, c.hidden), (c.hidden, c.q_dim), (2 * c.ffn, c.hidden), (c.hidden, c.ffn)][group]
+
+    def debug_read_group(self, layer, group):
+        N, K = self.group_shape(group)
+        out = np.zeros(N * K, np.uint16)
+        self._check(self.lib.ss_debug_read_group(self.ctx, layer, group, _ptr(out)))
+        return out.reshape(N, K)
+
+    def debug_get_substitute(self, layer, group):
+        N, K = self.group_shape(group)
+        codes = np.zeros(N * K, np.uint8)
+        s = np.zeros(N * K // 64, np.uint16)
+        z = np.zeros(N * K // 64, np.uint16)
+        self._check(self.lib.ss_debug_get_substitute(self.ctx, layer, group, _ptr(codes), _ptr(s), _ptr(z)))
+        return codes.reshape(N, K), s.reshape(N, K // 64), z.reshape(N, K // 64)
+
+    def debug_matmul(self, which, layer, group, x_bits):
+        N, K = self.group_shape(group)
+        x = np.ascontiguousarray(x_bits, dtype=np.uint16)
+        M = x.shape[0]
+        y = np.zeros(M * N, np.float32)
+        self._check(self.lib.ss_debug_matmul(self.ctx, which, layer, group, _ptr(x), M, _ptr(y)))
+        return y.reshape(M, N)
+
+    def debug_forward(self, which, tokens, parents):
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        p = np.ascontiguousarray(parents, dtype=np.int32)
+        out = np.zeros(len(t) * self.cfg.vocab, np.float32)
+        self._check(self.lib.ss_debug_forward(self.ctx, which, _ptr(t), _ptr(p), len(t), _ptr(out)))
+        return out.reshape(len(t), self.cfg.vocab)
+
+    def debug_set_tree(self, tokens, parents, top_k):
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        p = np.ascontiguousarray(parents, dtype=np.int32)
+        self._check(self.lib.ss_debug_set_tree(self.ctx, _ptr(t), _ptr(p), len(t), top_k))
+
+    def debug_read_kv(self, layer, pos0, n):
+        c = self.cfg
+        k = np.zeros(c.n_kv_heads * n * c.head_dim, np.uint16)
+        v = np.zeros_like(k)
+        self._check(self.lib.ss_debug_read_kv(self.ctx, layer, pos0, n, _ptr(k), _ptr(v)))
+        return k.reshape(c.n_kv_heads, n, c.head_dim), v.reshape(c.n_kv_heads, n, c.head_dim)
+
+    def debug_time_matmul(self, layer, group, M, iters=20):
+        ms = c_float()
+        self._check(self.lib.ss_debug_time_matmul(self.ctx, 0, layer, group, M, iters, ctypes.byref(ms)))
+        return ms.value

@@ -1,0 +1,155 @@
+// Shared device helpers for libsubspec (sm_100a).  No method arithmetic lives here.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#define SS_DEV __device__ __forceinline__
+#define SS_HD __host__ __device__ __forceinline__
+
+namespace ss {
+
+constexpr int kTileRows = 128;      // weight rows per tile (one head at d_h = 128)
+constexpr int kChunkK = 128;        // K elements per tile-chunk
+constexpr int kQ4CodeBytes = 8192;  // 128 x 128 x 4 bit
+constexpr int kQ4MetaBytes = 1024;  // 128 rows x 2 groups x (s,z) bf16
+constexpr int kQ4TileBytes = kQ4CodeBytes + kQ4MetaBytes;   // 9216
+constexpr int kBF16TileBytes = kTileRows * kChunkK * 2;     // 32768
+constexpr int kXChunkBytesPerNT = 8 * kChunkK * 2;          // 2048: 8 tokens x 128 k bf16
+
+// ---------------------------------------------------------------------------
+// Weight "tiled fragment" layout.
+// Matrix W [N x K] (N % 128 == 0, K % 128 == 0) is stored as tile-chunks
+// (r = n/128, c = k/128), index tc = r * (K/128) + c, each contiguous.
+// Inside a tile-chunk warp w (0..7) owns rows 16w..16w+15; lane = g*4 + t4
+// owns rows 16w+g (h=0) and 16w+g+8 (h=1) and k = 32*t4 .. 32*t4+31.
+// ---------------------------------------------------------------------------
+SS_HD uint64_t bf16_tiled_offset(int64_t n, int64_t k, int64_t K) {   // in bytes
+  int64_t tc = (n >> 7) * (K >> 7) + (k >> 7);
+  int nn = int(n & 127), kk = int(k & 127);
+  int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
+  int t4 = kk >> 5, i = kk & 31, q = i >> 3, e = i & 7;
+  int lane = g * 4 + t4;
+  return uint64_t(tc) * kBF16TileBytes + uint64_t((((w * 2 + h) * 4 + q) * 32 + lane) * 16 + e * 2);
+}
+
+// Q4: codes at (((w*2+h)*32 + lane)*16 + byte); a lane's 32 codes i = 0..31 sit in
+// 4 words (word = i/8); code c = i%8 of a word lives in nibble slot (c%2)*4 + c/2,
+// so (word >> 4p) & 0x000F000F yields the bf16x2 pair (c_2p, c_2p+1).
+SS_HD uint64_t q4_tile_base(int64_t n, int64_t k, int64_t K) {
+  return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ4TileBytes;
+}
+SS_HD void q4_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
+  int nn = int(n & 127), kk = int(k & 127);
+  int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
+  int t4 = kk >> 5, i = kk & 31, word = i >> 3, c = i & 7;
+  int lane = g * 4 + t4;
+  int slot = (c & 1) * 4 + (c >> 1);
+  uint64_t wordoff = q4_tile_base(n, k, K) + uint64_t(((w * 2 + h) * 32 + lane) * 16 + word * 4);
+  *byte_off = wordoff + (slot >> 1);
+  *shift = (slot & 1) * 4;
+}
+SS_HD uint64_t q4_meta_offset(int64_t n, int64_t k, int64_t K) {     // bytes; 4 B (s lo16, z hi16)
+  int nn = int(n & 127), kk = int(k & 127);
+  int w = nn >> 4, rr = nn & 15, grp = kk >> 6;
+  return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((w * 2 + grp) * 16 + rr) * 4);
+}
+
+// ---------------------------------------------------------------------------
+// FragX activation layout: X [Mpad x K] bf16, Mpad % 8 == 0, NT = Mpad/8.
+// Chunk c (128 k) of all NT n-tiles is contiguous (NT * 2 KB).
+// offset(m,k) = ((((c*NT + nt)*8 + s)*4 + t4)*8 + g)*4 + j   (elements)
+// with kk = k%128, t4 = kk/32, s = (kk%32)/4, j = kk%4, nt = m/8, g = m%8.
+// ---------------------------------------------------------------------------
+SS_HD int64_t fragx_offset(int64_t m, int64_t k, int NT) {
+  int64_t c = k >> 7;
+  int kk = int(k & 127), t4 = kk >> 5, s = (kk & 31) >> 2, j = kk & 3;
+  int nt = int(m >> 3), g = int(m & 7);
+  return ((((c * NT + nt) * 8 + s) * 4 + t4) * 8 + g) * 4 + j;
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+SS_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SS_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+SS_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+SS_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+SS_DEV void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+SS_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+SS_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared, completion counted on an mbarrier (TMA engine; SASS UBLKCP)
+SS_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+SS_DEV void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+SS_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+SS_DEV void mma_bf16_16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                           uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// (word >> 4p) & 0x000F000F | 0x43004300 gives bf16x2 (128 + c_lo, 128 + c_hi); subtracting 128
+// is exact; one fma.rn.bf16x2 then gives RNE_bf16(code*s + z) (single rounding).
+SS_DEV uint32_t dq_pair(uint32_t word, int p, uint32_t s2, uint32_t z2) {
+  uint32_t v = ((word >> (4 * p)) & 0x000F000Fu) | 0x43004300u;
+  __nv_bfloat162 bv = *reinterpret_cast<__nv_bfloat162*>(&v);
+  const uint32_t k128 = 0x43004300u;
+  __nv_bfloat162 c = __hsub2(bv, *reinterpret_cast<const __nv_bfloat162*>(&k128));
+  __nv_bfloat162 r = __hfma2(c, *reinterpret_cast<__nv_bfloat162*>(&s2), *reinterpret_cast<__nv_bfloat162*>(&z2));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+SS_DEV float bf2f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
+SS_DEV uint16_t f2bf(float f) {   // RNE (finite inputs)
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+SS_DEV float warp_sum(float v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+SS_DEV float warp_max(float v) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace ss

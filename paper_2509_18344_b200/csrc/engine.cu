@@ -1,0 +1,1355 @@
+// libsubspec engine: context, capped arena, placement, pinned host store, K7 layer streaming,
+// draft loop (CUDA graph + PDL), verification, acceptance, and the C-ABI (include/subspec.h).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "subspec.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace ss;
+
+namespace {
+
+constexpr uint64_t kTidMul = 0xD1B54A32D192ED03ull;
+uint64_t splitmix64_host(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t tensor_key(uint64_t seed, uint64_t tid) { return splitmix64_host(seed ^ (tid * kTidMul)); }
+float scale_c32(double sigma) { return float((sigma * std::sqrt(12.0)) / 262144.0); }
+
+struct Arena {
+  uint8_t* base = nullptr;
+  size_t cap = 0, used = 0;
+  void* alloc(size_t bytes, size_t align = 256) {
+    size_t off = (used + align - 1) / align * align;
+    if (off + bytes > cap) return nullptr;
+    used = off + bytes;
+    return base + off;
+  }
+};
+
+struct LayerW {
+  uint16_t* attn_norm = nullptr;
+  uint16_t* mlp_norm = nullptr;
+  uint16_t* bias = nullptr;
+  bool resident = false;
+  uint8_t* bf16[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint8_t* q4[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t host_off[4] = {0, 0, 0, 0};
+};
+
+struct StreamItem {
+  int64_t seq;
+  int layer, group;
+  size_t off, bytes;
+  int ev;
+  bool consumed;
+};
+
+enum State { ST_CREATED = 0, ST_LOADED = 1, ST_READY = 2, ST_SESSION = 3, ST_DRAFTED = 4, ST_VERIFIED = 5 };
+
+}  // namespace
+
+struct ss_ctx {
+  ss_model_config cfg{};
+  ss_limits lim{};
+  int device = 0;
+  cudaStream_t cs = nullptr, xs = nullptr;
+  Arena ar;
+  std::string err;
+  bool poisoned = false;
+  int state = ST_CREATED;
+  int H = 0, F = 0, qd = 0, kvd = 0, qkv_rows = 0, L = 0, V = 0, d = 0, nh = 0, nkv = 0, C = 0;
+  int gN[4] = {0}, gK[4] = {0};
+  // weights
+  uint16_t* embed = nullptr;
+  uint8_t* head = nullptr;
+  uint16_t* final_norm = nullptr;
+  std::vector<LayerW> lw;
+  int n_resident = 0;
+  uint64_t seed = 0;
+  uint8_t* host = nullptr;
+  size_t host_bytes = 0;
+  bool substitutes_built = false;
+  // kv + tree
+  uint16_t *kc = nullptr, *vc = nullptr, *kt = nullptr, *vt = nullptr;
+  int64_t kc_layer = 0, kt_layer = 0;
+  int max_nodes = 0, anc_stride = 0;
+  int *tok = nullptr, *parent = nullptr, *depth = nullptr, *anc = nullptr;
+  float* score = nullptr;
+  int *committed_len = nullptr, *root_tok = nullptr, *tokbuf = nullptr;
+  int P = 0, n_nodes = 0, cur_k = 0, cur_deff = 0;
+  // activations
+  float* x = nullptr;
+  uint16_t *hfrag = nullptr, *attnfrag = nullptr, *actfrag = nullptr, *qbuf = nullptr;
+  float* logits = nullptr;
+  int mpad_max = 0;
+  float2* rope = nullptr;
+  // gemv scratch
+  float* gv_part = nullptr;
+  int* gv_cnt = nullptr;
+  int gv_grid = 148;
+  size_t gv_part_floats = 0;
+  // attention scratch
+  float *at_o = nullptr, *at_ml = nullptr;
+  int at_seg_max = 0;
+  int split_draft = 64, split_target = 128;
+  // topk scratch
+  float *tk_max = nullptr, *tk_sum = nullptr, *tk_val = nullptr;
+  int* tk_idx = nullptr;
+  // verify
+  float *am_val = nullptr, *am_sec = nullptr, *gap = nullptr;
+  int *am_idx = nullptr, *argmax = nullptr;
+  int vtiles = 0;
+  // accept
+  int *out_tokens = nullptr, *out_n = nullptr, *out_path = nullptr, *commit_meta = nullptr;
+  int* h_out = nullptr;   // pinned: [0] n, [1..] tokens
+  // streaming ring (K7)
+  uint8_t* ring = nullptr;
+  size_t ring_bytes = 0, ring_head = 0;
+  std::deque<StreamItem> inflight;
+  int64_t next_issue = 0, next_consume = 0;
+  std::vector<std::pair<int, int>> cycle;
+  std::vector<cudaEvent_t> ev_copied, ev_consumed, ev_t0, ev_t1;
+  std::vector<bool> ev_pending;
+  std::deque<int> timing_queue;
+  int ev_pool = 0;
+  // graphs
+  std::map<std::tuple<int, int, uint32_t>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int, uint32_t>, int64_t> graph_launches;
+  bool use_graphs = true, use_pdl = true;
+  // stats
+  ss_stats st{};
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  int64_t launches = 0;
+  bool capturing = false;
+};
+
+// ------------------------------------------------------------------------------------------
+namespace {
+
+ss_status fail(ss_ctx* c, ss_status s, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (s == SS_ERR_CUDA) c->poisoned = true;
+  }
+  return s;
+}
+
+#define CK(call)                                                                               \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return fail(c, SS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+ss_status check_launch(ss_ctx* c, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, SS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return SS_OK;
+}
+
+size_t q4_bytes(int N, int K) { return size_t(N / 128) * (K / 128) * kQ4TileBytes; }
+size_t bf16_bytes(int N, int K) { return size_t(N) * K * 2; }
+
+int gemv_nt(int M) { return M <= 8 ? 1 : (M <= 16 ? 2 : 4); }
+int gemm_nt(int M) { return ((M + 127) / 128) * 16; }
+
+// ---------------------------------- K7 streaming ------------------------------------------
+ss_status pump(ss_ctx* c) {
+  if (c->cycle.empty()) return SS_OK;
+  const int n_items = int(c->cycle.size());
+  while (true) {
+    const int64_t seq = c->next_issue;
+    // never run more than one cycle ahead of consumption
+    if (seq >= c->next_consume + n_items) return SS_OK;
+    const auto [l, g] = c->cycle[seq % n_items];
+    const size_t B = bf16_bytes(c->gN[g], c->gK[g]);
+    size_t off = c->ring_head;
+    if (off + B > c->ring_bytes) off = 0;
+    const int ev = int(seq % c->ev_pool);
+    for (size_t i = 0; i < c->inflight.size(); ++i)
+      if (c->inflight[i].ev == ev) {   // event slot still owned by an old item
+        if (!c->inflight[i].consumed) return SS_OK;
+        // consumed long ago (the pool is 4 cycles deep): order the copy stream after it and drop it
+        CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[ev], 0));
+        c->inflight.erase(c->inflight.begin() + i);
+        break;
+      }
+    // regions of older items that the new copy overwrites must have been consumed
+    std::vector<size_t> dead;
+    for (size_t i = 0; i < c->inflight.size(); ++i) {
+      const auto& it = c->inflight[i];
+      const bool overlap = it.off < off + B && off < it.off + it.bytes;
+      if (overlap) {
+        if (!it.consumed) return SS_OK;
+        dead.push_back(i);
+      }
+    }
+    if (c->ev_pending[ev]) {   // timing of a previous copy with this slot not yet harvested
+      CK(cudaEventSynchronize(c->ev_t1[ev]));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev_t0[ev], c->ev_t1[ev]));
+      c->st.stream_busy_ms += ms;
+      c->ev_pending[ev] = false;
+    }
+    for (size_t i : dead) CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[c->inflight[i].ev], 0));
+    for (size_t k = dead.size(); k-- > 0;) c->inflight.erase(c->inflight.begin() + dead[k]);
+    CK(cudaEventRecord(c->ev_t0[ev], c->xs));
+    CK(cudaMemcpyAsync(c->ring + off, c->host + c->lw[l].host_off[g], B, cudaMemcpyHostToDevice, c->xs));
+    CK(cudaEventRecord(c->ev_t1[ev], c->xs));
+    CK(cudaEventRecord(c->ev_copied[ev], c->xs));
+    c->ev_pending[ev] = true;
+    c->timing_queue.push_back(ev);
+    c->st.stream_bytes += double(B);
+    c->inflight.push_back({seq, l, g, off, B, ev, false});
+    c->ring_head = off + B;
+    c->next_issue = seq + 1;
+  }
+}
+
+void harvest_timing(ss_ctx* c) {
+  while (!c->timing_queue.empty()) {
+    const int ev = c->timing_queue.front();
+    if (!c->ev_pending[ev]) {
+      c->timing_queue.pop_front();
+      continue;
+    }
+    if (cudaEventQuery(c->ev_t1[ev]) != cudaSuccess) break;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev_t0[ev], c->ev_t1[ev]) == cudaSuccess) c->st.stream_busy_ms += ms;
+    c->ev_pending[ev] = false;
+    c->timing_queue.pop_front();
+  }
+  cudaGetLastError();
+}
+
+// returns the staged weights of the next item in the cycle (must be (l, g)); compute waits on its copy
+ss_status consume_begin(ss_ctx* c, int l, int g, const uint8_t** w, int* ev_out) {
+  ss_status s = pump(c);
+  if (s != SS_OK) return s;
+  const int64_t seq = c->next_consume;
+  const int n_items = int(c->cycle.size());
+  if (c->cycle[seq % n_items] != std::make_pair(l, g)) return fail(c, SS_ERR_STRUCTURE, "stream order mismatch");
+  for (auto& it : c->inflight)
+    if (it.seq == seq) {
+      CK(cudaStreamWaitEvent(c->cs, c->ev_copied[it.ev], 0));
+      *w = c->ring + it.off;
+      *ev_out = it.ev;
+      return SS_OK;
+    }
+  return fail(c, SS_ERR_BUDGET, "staging ring cannot hold the next layer group");
+}
+ss_status consume_end(ss_ctx* c, int ev) {
+  CK(cudaEventRecord(c->ev_consumed[ev], c->cs));
+  for (auto& it : c->inflight)
+    if (it.ev == ev) it.consumed = true;
+  c->next_consume++;
+  return pump(c);
+}
+
+// ----------------------------------- passes -------------------------------------------------
+struct PassOut {
+  bool logits = false;        // draft: logits to c->logits [M x V]
+  bool argmax = false;        // target: per-node argmax + gap
+};
+
+ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M, const EpiParams& epi) {
+  const int N = c->gN[g], K = c->gK[g];
+  const LayerW& w = c->lw[l];
+  if (!target) {
+    GemvParams p{};
+    p.W = w.resident ? w.bf16[g] : w.q4[g];
+    p.X = X;
+    p.N = N;
+    p.K = K;
+    p.NT = gemv_nt(M);
+    p.partials = c->gv_part;
+    p.counters = c->gv_cnt;
+    p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+    p.epi = epi;
+    launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
+    c->launches++;
+    return check_launch(c, "gemv");
+  }
+  GemmParams p{};
+  p.X = X;
+  p.N = N;
+  p.K = K;
+  p.NT = gemm_nt(M);
+  p.epi = epi;
+  if (w.resident) {
+    p.W = w.bf16[g];
+    launch_gemm(p, c->use_pdl, c->cs);
+    c->launches++;
+    return check_launch(c, "gemm");
+  }
+  const uint8_t* wp = nullptr;
+  int ev = -1;
+  ss_status s = consume_begin(c, l, g, &wp, &ev);
+  if (s != SS_OK) return s;
+  p.W = wp;
+  launch_gemm(p, false, c->cs);   // follows a cross-stream event wait: plain serialisation
+  c->launches++;
+  s = check_launch(c, "gemm");
+  if (s != SS_OK) return s;
+  return consume_end(c, ev);
+}
+
+EpiParams base_epi(ss_ctx* c, int M) {
+  EpiParams e{};
+  e.M = M;
+  e.committed_len = c->committed_len;
+  e.depth = c->depth;
+  e.rope = c->rope;
+  e.q_dim = c->qd;
+  e.kv_dim = c->kvd;
+  e.head_dim = c->d;
+  e.max_nodes = c->max_nodes;
+  e.x = c->x;
+  e.ldx = c->H;
+  e.ffn = c->F;
+  return e;
+}
+
+// Forward M nodes [node_base, node_base + M) through the draft (GEMV path) or the target (GEMM
+// path, streamed).  Tree slots of these nodes receive their K/V.
+ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassOut& out) {
+  const int NT = target ? gemm_nt(M) : gemv_nt(M);
+  const float eps = c->cfg.rms_eps;
+  ss_status s;
+  launch_embed_rmsnorm(c->tok, node_base, M, c->embed, c->x, c->H, c->lw[0].attn_norm, eps, c->hfrag, NT,
+                       c->use_pdl, c->cs);
+  c->launches++;
+  if ((s = check_launch(c, "embed_rmsnorm")) != SS_OK) return s;
+  for (int l = 0; l < c->L; ++l) {
+    EpiParams e = base_epi(c, M);
+    e.kind = EPI_QKV;
+    e.bias = c->lw[l].bias;
+    e.q_out = c->qbuf;
+    e.k_tree = c->kt + l * c->kt_layer;
+    e.v_tree = c->vt + l * c->kt_layer;
+    e.node_base = node_base;
+    if ((s = matmul(c, target, l, 0, c->hfrag, M, e)) != SS_OK) return s;
+    AttnParams a{};
+    a.q = c->qbuf;
+    a.k_cache = c->kc + l * c->kc_layer;
+    a.v_cache = c->vc + l * c->kc_layer;
+    a.k_tree = c->kt + l * c->kt_layer;
+    a.v_tree = c->vt + l * c->kt_layer;
+    a.committed_len = c->committed_len;
+    a.anc = c->anc;
+    a.depth = c->depth;
+    a.anc_stride = c->anc_stride;
+    a.max_ctx = c->C;
+    a.max_nodes = c->max_nodes;
+    a.n_q = M;
+    a.node_base = node_base;
+    a.n_heads = c->nh;
+    a.n_kv = c->nkv;
+    a.head_dim = c->d;
+    a.split = target ? c->split_target : c->split_draft;
+    a.n_seg_max = c->at_seg_max;
+    a.part_o = c->at_o;
+    a.part_ml = c->at_ml;
+    a.out_fragx = c->attnfrag;
+    a.out_nt = NT;
+    // logical keys of a node: P + depth + 1 <= max_context.  The draft loop is replayed from a CUDA
+    // graph while P grows, so its grid is sized for max_context.
+    launch_attention(a, target ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
+    c->launches += 2;
+    if ((s = check_launch(c, "attention")) != SS_OK) return s;
+    e = base_epi(c, M);
+    e.kind = EPI_RESID;
+    if ((s = matmul(c, target, l, 1, c->attnfrag, M, e)) != SS_OK) return s;
+    launch_rmsnorm(c->x, M, c->H, c->lw[l].mlp_norm, eps, c->hfrag, NT, c->use_pdl, c->cs);
+    c->launches++;
+    if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
+    e = base_epi(c, M);
+    e.kind = EPI_SILU;
+    e.act = c->actfrag;
+    e.act_nt = NT;
+    if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
+    e = base_epi(c, M);
+    e.kind = EPI_RESID;
+    if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
+    const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
+    if (!target || out.argmax) {
+      launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, NT, c->use_pdl, c->cs);
+      c->launches++;
+      if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
+    } else if (l + 1 < c->L) {
+      launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, NT, c->use_pdl, c->cs);
+      c->launches++;
+      if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
+    }
+  }
+  if (out.argmax) {
+    GemmParams p{};
+    p.W = c->head;
+    p.X = c->hfrag;
+    p.N = c->V;
+    p.K = c->H;
+    p.NT = NT;
+    p.epi = base_epi(c, M);
+    p.epi.kind = EPI_ARGMAX;
+    p.epi.am_val = c->am_val;
+    p.epi.am_idx = c->am_idx;
+    p.epi.am_second = c->am_sec;
+    p.epi.am_tiles = c->vtiles;
+    launch_gemm(p, c->use_pdl, c->cs);
+    launch_argmax_merge(c->am_val, c->am_idx, c->am_sec, M, c->vtiles, c->argmax, c->gap, c->use_pdl, c->cs);
+    c->launches += 2;
+    return check_launch(c, "verify head");
+  }
+  if (out.logits) {
+    // head over the final normed rows (GEMV, <= 32 rows at a time)
+    for (int r0 = 0; r0 < M && !target; r0 += 32) {
+      const int m = std::min(32, M - r0);
+      GemvParams p{};
+      p.W = c->head;
+      p.X = c->hfrag;
+      p.N = c->V;
+      p.K = c->H;
+      p.NT = gemv_nt(m);
+      p.partials = c->gv_part;
+      p.counters = c->gv_cnt;
+      p.max_seg = gemv_max_segments(c->V, c->H, c->gv_grid);
+      p.epi = base_epi(c, m);
+      p.epi.kind = EPI_LOGITS;
+      p.epi.out = c->logits;
+      p.epi.ldo = c->V;
+      launch_gemv(false, p, c->gv_grid, c->use_pdl, c->cs);
+      c->launches++;
+      if ((s = check_launch(c, "head gemv")) != SS_OK) return s;
+    }
+  }
+  return SS_OK;
+}
+
+ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
+  ss_status s;
+  launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, c->use_pdl, c->cs);
+  c->launches++;
+  if ((s = check_launch(c, "tree_init")) != SS_OK) return s;
+  for (int dd = 0; dd < D; ++dd) {
+    const int M = dd == 0 ? 1 : k;
+    const int base = dd == 0 ? 0 : 1 + (dd - 1) * k;
+    PassOut o;
+    o.logits = true;
+    if ((s = forward_pass(c, false, M, base, o)) != SS_OK) return s;
+    TopkParams t{};
+    t.logits = c->logits;
+    t.M = M;
+    t.V = c->V;
+    t.k = k;
+    t.inv_t = float(1.0 / double(T));
+    t.blocks_per_row = std::max(1, std::min(64, 296 / M));
+    t.blk_max = c->tk_max;
+    t.blk_sum = c->tk_sum;
+    t.blk_val = c->tk_val;
+    t.blk_idx = c->tk_idx;
+    t.tok = c->tok;
+    t.parent = c->parent;
+    t.depth = c->depth;
+    t.score = c->score;
+    t.anc = c->anc;
+    t.anc_stride = c->anc_stride;
+    t.node_base = base;
+    t.child_base = 1 + dd * k;
+    t.child_depth = dd + 1;
+    launch_topk(t, c->use_pdl, c->cs);
+    c->launches += 2;
+    if ((s = check_launch(c, "topk")) != SS_OK) return s;
+  }
+  return SS_OK;
+}
+
+ss_status run_draft(ss_ctx* c, int D, int k, float T) {
+  uint32_t tb;
+  std::memcpy(&tb, &T, 4);
+  const auto key = std::make_tuple(D, k, tb);
+  if (c->use_graphs) {
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      // first use: run eagerly (sets kernel attributes), then capture for later steps
+      const int64_t l0 = c->launches;
+      ss_status s = draft_loop(c, D, k, T);
+      if (s != SS_OK) return s;
+      const int64_t nl = c->launches - l0;
+      cudaGraph_t g = nullptr;
+      if (cudaStreamBeginCapture(c->cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        c->capturing = true;
+        const int64_t lsave = c->launches;
+        ss_status s2 = draft_loop(c, D, k, T);
+        c->launches = lsave;
+        c->capturing = false;
+        cudaError_t e = cudaStreamEndCapture(c->cs, &g);
+        cudaGraphExec_t ge = nullptr;
+        if (s2 == SS_OK && e == cudaSuccess && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess) {
+          c->graphs[key] = ge;
+          c->graph_launches[key] = nl;
+        } else {
+          c->use_graphs = false;
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        c->poisoned = false;
+        c->err.clear();
+      } else {
+        cudaGetLastError();
+        c->use_graphs = false;
+      }
+      return SS_OK;
+    }
+    CK(cudaGraphLaunch(it->second, c->cs));
+    c->launches += c->graph_launches[key];
+    return SS_OK;
+  }
+  return draft_loop(c, D, k, T);
+}
+
+ss_status do_verify(ss_ctx* c) {
+  PassOut o;
+  o.argmax = true;
+  return forward_pass(c, true, c->n_nodes, 0, o);
+}
+
+ss_status do_accept(ss_ctx* c, bool chain) {
+  AcceptParams a{};
+  a.argmax = c->argmax;
+  a.tok = c->tok;
+  a.parent = c->parent;
+  a.commit_meta = c->commit_meta;
+  a.n_nodes = c->n_nodes;
+  a.k = std::max(1, c->cur_k);
+  a.depth_max = c->cur_deff;
+  a.committed_len = c->committed_len;
+  a.root_tok = c->root_tok;
+  a.out_tokens = c->out_tokens;
+  a.out_n = c->out_n;
+  a.out_path = c->out_path;
+  a.k_cache = c->kc;
+  a.v_cache = c->vc;
+  a.k_tree = c->kt;
+  a.v_tree = c->vt;
+  a.cache_layer_stride = c->kc_layer;
+  a.tree_layer_stride = c->kt_layer;
+  a.n_layers = c->L;
+  a.n_kv = c->nkv;
+  a.head_dim = c->d;
+  a.max_ctx = c->C;
+  a.max_nodes = c->max_nodes;
+  a.chain = chain ? 1 : 0;
+  launch_accept_commit(a, c->use_pdl, c->cs);
+  c->launches += 2;
+  return check_launch(c, "accept_commit");
+}
+
+ss_status read_outputs(ss_ctx* c, int cap, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path) {
+  CK(cudaMemcpyAsync(c->h_out, c->out_n, 4, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaMemcpyAsync(c->h_out + 1, c->out_tokens, size_t(cap) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (opt_path) CK(cudaMemcpyAsync(c->h_out + 1 + cap, c->out_path, size_t(cap) * 4, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  const int n = c->h_out[0];
+  if (out_n) *out_n = n;
+  if (out_tokens) std::memcpy(out_tokens, c->h_out + 1, size_t(std::min(n, cap)) * 4);
+  if (opt_path) std::memcpy(opt_path, c->h_out + 1 + cap, size_t(std::min(n, cap)) * 4);
+  return SS_OK;
+}
+
+bool valid_cfg(const ss_model_config* m, const ss_limits* l) {
+  if (!m || !l) return false;
+  if (m->n_layers < 1 || m->hidden % 128 || m->ffn % 128 || m->vocab % 128 || m->n_heads < 1 || m->n_kv_heads < 1)
+    return false;
+  if (m->n_heads % m->n_kv_heads) return false;
+  if (m->head_dim != 64 && m->head_dim != 128) return false;
+  if (((m->n_heads + 2 * m->n_kv_heads) * m->head_dim) % 128) return false;
+  if ((m->n_heads * m->head_dim) % 128) return false;
+  if (m->max_context < 2 || m->max_context > 8192) return false;
+  if (m->n_heads / m->n_kv_heads > 16) return false;
+  if (l->max_depth < 0 || l->max_top_k < 1 || l->max_top_k > 32 || l->max_chunk < 1 || l->max_chunk > 1024) return false;
+  return true;
+}
+
+#define GUARD(c)                                                                 \
+  do {                                                                           \
+    if (!(c)) return SS_ERR_INVALID;                                             \
+    if ((c)->poisoned) return SS_ERR_CUDA;                                       \
+    cudaSetDevice((c)->device);                                                  \
+  } while (0)
+
+}  // namespace
+
+// ================================== C-ABI ===================================================
+extern "C" {
+
+ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device, void* dev_arena, size_t arena_bytes,
+                    void* compute_stream, void* copy_stream, ss_ctx** out) {
+  if (!out || !valid_cfg(cfg, lim) || !dev_arena) return SS_ERR_INVALID;
+  *out = nullptr;
+  ss_ctx* c = new ss_ctx();
+  c->cfg = *cfg;
+  c->lim = *lim;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return SS_ERR_CUDA;
+  }
+  c->cs = reinterpret_cast<cudaStream_t>(compute_stream);
+  c->xs = reinterpret_cast<cudaStream_t>(copy_stream);
+  c->ar.base = reinterpret_cast<uint8_t*>(dev_arena);
+  c->ar.cap = arena_bytes;
+  c->H = cfg->hidden;
+  c->F = cfg->ffn;
+  c->nh = cfg->n_heads;
+  c->nkv = cfg->n_kv_heads;
+  c->d = cfg->head_dim;
+  c->qd = c->nh * c->d;
+  c->kvd = c->nkv * c->d;
+  c->qkv_rows = c->qd + 2 * c->kvd;
+  c->L = cfg->n_layers;
+  c->V = cfg->vocab;
+  c->C = cfg->max_context;
+  c->gN[0] = c->qkv_rows; c->gK[0] = c->H;
+  c->gN[1] = c->H;        c->gK[1] = c->qd;
+  c->gN[2] = 2 * c->F;    c->gK[2] = c->H;
+  c->gN[3] = c->H;        c->gK[3] = c->F;
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  c->gv_grid = dev_sms;
+  const int k = lim->max_top_k, D = lim->max_depth;
+  c->max_nodes = std::max(1 + k * D, lim->max_chunk);
+  c->anc_stride = std::max(D + 1, lim->max_chunk);
+  c->mpad_max = std::max(32, ((c->max_nodes + 127) / 128) * 128);
+  Arena& a = c->ar;
+  auto A = [&](size_t bytes) { return a.alloc(bytes); };
+  bool ok = true;
+  auto chk = [&](void* p) { ok = ok && p != nullptr; return p; };
+  c->embed = (uint16_t*)chk(A(size_t(c->V) * c->H * 2));
+  c->head = (uint8_t*)chk(A(bf16_bytes(c->V, c->H)));
+  c->final_norm = (uint16_t*)chk(A(size_t(c->H) * 2));
+  c->lw.resize(c->L);
+  for (auto& w : c->lw) {
+    w.attn_norm = (uint16_t*)chk(A(size_t(c->H) * 2));
+    w.mlp_norm = (uint16_t*)chk(A(size_t(c->H) * 2));
+    if (cfg->qkv_bias) w.bias = (uint16_t*)chk(A(size_t(c->qkv_rows) * 2));
+  }
+  c->kc_layer = int64_t(c->nkv) * c->C * c->d;
+  c->kt_layer = int64_t(c->nkv) * c->max_nodes * c->d;
+  c->kc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
+  c->vc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
+  c->kt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
+  c->vt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
+  c->tok = (int*)chk(A(size_t(c->max_nodes) * 4));
+  c->parent = (int*)chk(A(size_t(c->max_nodes) * 4));
+  c->depth = (int*)chk(A(size_t(c->max_nodes) * 4));
+  c->score = (float*)chk(A(size_t(c->max_nodes) * 4));
+  c->anc = (int*)chk(A(size_t(c->max_nodes) * c->anc_stride * 4));
+  c->committed_len = (int*)chk(A(64));
+  c->root_tok = (int*)chk(A(64));
+  c->tokbuf = (int*)chk(A(size_t(lim->max_chunk) * 4));
+  const int fx_cols = std::max({c->H, c->qd, c->F});
+  c->x = (float*)chk(A(size_t(c->mpad_max) * c->H * 4));
+  c->hfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * fx_cols * 2));
+  c->attnfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * c->qd * 2));
+  c->actfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * c->F * 2));
+  c->qbuf = (uint16_t*)chk(A(size_t(c->max_nodes) * c->qd * 2));
+  c->logits = (float*)chk(A(size_t(32) * c->V * 4));
+  c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
+  // gemv partials: worst case over groups and the head at Mpad = 32
+  size_t gvf = 0;
+  int max_tiles = 0;
+  for (int g = 0; g < 5; ++g) {
+    const int N = g < 4 ? c->gN[g] : c->V, K = g < 4 ? c->gK[g] : c->H;
+    gvf = std::max(gvf, size_t(N / 128) * gemv_max_segments(N, K, c->gv_grid) * 128 * 32);
+    max_tiles = std::max(max_tiles, N / 128);
+  }
+  c->gv_part_floats = gvf;
+  c->gv_part = (float*)chk(A(gvf * 4));
+  c->gv_cnt = (int*)chk(A(size_t(max_tiles) * 4));
+  c->at_seg_max = (c->C + std::min(c->split_draft, c->split_target) - 1) / std::min(c->split_draft, c->split_target);
+  c->at_o = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d * 4));
+  c->at_ml = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * 2 * 4));
+  c->tk_max = (float*)chk(A(size_t(32) * 296 * 4));
+  c->tk_sum = (float*)chk(A(size_t(32) * 296 * 4));
+  c->tk_val = (float*)chk(A(size_t(32) * 296 * 32 * 4));
+  c->tk_idx = (int*)chk(A(size_t(32) * 296 * 32 * 4));
+  c->vtiles = c->V / 128;
+  c->am_val = (float*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
+  c->am_sec = (float*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
+  c->am_idx = (int*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
+  c->argmax = (int*)chk(A(size_t(c->max_nodes) * 4));
+  c->gap = (float*)chk(A(size_t(c->max_nodes) * 4));
+  c->out_tokens = (int*)chk(A(size_t(c->max_nodes + 1) * 4));
+  c->out_n = (int*)chk(A(64));
+  c->out_path = (int*)chk(A(size_t(c->max_nodes + 1) * 4));
+  c->commit_meta = (int*)chk(A(64));
+  if (!ok) {
+    delete c;
+    return SS_ERR_BUDGET;
+  }
+  // zero everything carved so far (padding rows of FragX buffers must be finite; counters 0)
+  if (cudaMemsetAsync(a.base, 0, a.used, c->cs) != cudaSuccess) {
+    delete c;
+    return SS_ERR_CUDA;
+  }
+  // RoPE table (cos, sin) of pos * theta^(-2j/d), computed in double
+  std::vector<float2> rope(size_t(c->C) * (c->d / 2));
+  for (int p = 0; p < c->C; ++p)
+    for (int j = 0; j < c->d / 2; ++j) {
+      const double ang = double(p) * std::pow(double(cfg->rope_theta), -2.0 * j / c->d);
+      rope[size_t(p) * (c->d / 2) + j] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+    }
+  cudaMemcpyAsync(c->rope, rope.data(), rope.size() * 8, cudaMemcpyHostToDevice, c->cs);
+  cudaStreamSynchronize(c->cs);
+  cudaHostAlloc(&c->h_out, size_t(2 * c->max_nodes + 8) * 4, cudaHostAllocPortable);
+  cudaEventCreate(&c->e0);
+  cudaEventCreate(&c->e1);
+  cudaEventCreate(&c->e2);
+  cudaEventCreate(&c->e3);
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess || !c->h_out) {
+    delete c;
+    return SS_ERR_CUDA;
+  }
+  c->st.arena_cap = int64_t(arena_bytes);
+  *out = c;
+  return SS_OK;
+}
+
+ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
+  GUARD(c);
+  if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "load_weights: already loaded");
+  c->seed = seed;
+  const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
+  const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += q4_bytes(c->gN[g], c->gK[g]); return s; }();
+  size_t max_group = 0;
+  for (int g = 0; g < 4; ++g) max_group = std::max(max_group, bf16_bytes(c->gN[g], c->gK[g]));
+  const size_t avail = c->ar.cap - c->ar.used - 4096 * 8;
+  auto need = [&](int nr) {
+    const int off = c->L - nr;
+    return size_t(nr) * layer_bf16 + size_t(off) * layer_q4 + (off > 0 ? 2 * max_group : max_group);
+  };
+  int nr = n_resident;
+  if (nr < 0) {
+    nr = 0;
+    while (nr < c->L && need(nr + 1) <= avail) ++nr;
+  }
+  if (nr > c->L) return fail(c, SS_ERR_INVALID, "n_resident > n_layers");
+  if (need(nr) > avail) return fail(c, SS_ERR_BUDGET, "arena below the minimum footprint for this placement");
+  c->n_resident = nr;
+  for (int l = 0; l < c->L; ++l) {
+    LayerW& w = c->lw[l];
+    w.resident = l < nr;
+    for (int g = 0; g < 4; ++g) {
+      if (w.resident)
+        w.bf16[g] = (uint8_t*)c->ar.alloc(bf16_bytes(c->gN[g], c->gK[g]), 1024);
+      else
+        w.q4[g] = (uint8_t*)c->ar.alloc(q4_bytes(c->gN[g], c->gK[g]), 1024);
+    }
+  }
+  c->ring_bytes = (c->ar.cap - c->ar.used - 4096) / 4096 * 4096;
+  c->ring = (uint8_t*)c->ar.alloc(c->ring_bytes, 4096);
+  if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
+  // pinned host store for offloaded layers (device layout)
+  c->host_bytes = size_t(c->L - nr) * layer_bf16;
+  if (c->host_bytes) {
+    if (cudaHostAlloc(&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess)
+      return fail(c, SS_ERR_CUDA, "cudaHostAlloc of the pinned host store failed");
+    size_t off = 0;
+    for (int l = nr; l < c->L; ++l)
+      for (int g = 0; g < 4; ++g) {
+        c->lw[l].host_off[g] = off;
+        off += bf16_bytes(c->gN[g], c->gK[g]);
+      }
+  }
+  // generation (tensor ids: SURVEY O.1 / synth/weights.py)
+  const double H = c->H;
+  launch_gen_natural(c->embed, tensor_key(seed, 0), uint64_t(c->V) * c->H, scale_c32(1.0), 0, c->cs);
+  launch_gen_tiled(c->head, tensor_key(seed, 2 + 16 * c->L), c->V, c->H, scale_c32(1.0 / std::sqrt(H)), 0, 0, c->cs);
+  launch_gen_natural(c->final_norm, tensor_key(seed, 1 + 16 * c->L), c->H, scale_c32(0.05), 1, c->cs);
+  for (int l = 0; l < c->L; ++l) {
+    LayerW& w = c->lw[l];
+    const uint64_t b = 1 + 16 * uint64_t(l);
+    launch_gen_natural(w.attn_norm, tensor_key(seed, b + 0), c->H, scale_c32(0.05), 1, c->cs);
+    launch_gen_natural(w.mlp_norm, tensor_key(seed, b + 8), c->H, scale_c32(0.05), 1, c->cs);
+    if (w.bias) {
+      launch_gen_natural(w.bias, tensor_key(seed, b + 2), c->qd, scale_c32(0.02), 0, c->cs);
+      launch_gen_natural(w.bias + c->qd, tensor_key(seed, b + 4), c->kvd, scale_c32(0.02), 0, c->cs);
+      launch_gen_natural(w.bias + c->qd + c->kvd, tensor_key(seed, b + 6), c->kvd, scale_c32(0.02), 0, c->cs);
+    }
+    for (int g = 0; g < 4; ++g) {
+      uint8_t* dst = w.resident ? w.bf16[g] : c->ring;
+      const int K = c->gK[g];
+      const float cin = scale_c32(1.0 / std::sqrt(double(K)));
+      if (g == 0) {
+        launch_gen_tiled(dst, tensor_key(seed, b + 1), c->qd, K, cin, 0, 0, c->cs);
+        launch_gen_tiled(dst, tensor_key(seed, b + 3), c->kvd, K, cin, 0, c->qd, c->cs);
+        launch_gen_tiled(dst, tensor_key(seed, b + 5), c->kvd, K, cin, 0, c->qd + c->kvd, c->cs);
+      } else if (g == 1) {
+        launch_gen_tiled(dst, tensor_key(seed, b + 7), c->H, K, cin, 0, 0, c->cs);
+      } else if (g == 2) {
+        launch_gen_tiled(dst, tensor_key(seed, b + 9), c->F, K, cin, 1, 0, c->cs);
+        launch_gen_tiled(dst, tensor_key(seed, b + 10), c->F, K, cin, 2, 0, c->cs);
+      } else {
+        launch_gen_tiled(dst, tensor_key(seed, b + 11), c->H, K, cin, 0, 0, c->cs);
+      }
+      if (!w.resident) {
+        CK(cudaMemcpyAsync(c->host + w.host_off[g], c->ring, bf16_bytes(c->gN[g], K), cudaMemcpyDeviceToHost, c->cs));
+        CK(cudaStreamSynchronize(c->cs));
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(c->cs));
+  ss_status s = check_launch(c, "load_weights");
+  if (s != SS_OK) return s;
+  // streaming cycle: offloaded layers in order, groups qkv, o, gate_up, down
+  c->cycle.clear();
+  for (int l = nr; l < c->L; ++l)
+    for (int g = 0; g < 4; ++g) c->cycle.emplace_back(l, g);
+  c->ev_pool = 4 * int(c->cycle.size()) + 64;
+  for (int i = 0; i < c->ev_pool; ++i) {
+    cudaEvent_t e1, e2, t0, t1;
+    cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e2, cudaEventDisableTiming);
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    c->ev_copied.push_back(e1);
+    c->ev_consumed.push_back(e2);
+    c->ev_t0.push_back(t0);
+    c->ev_t1.push_back(t1);
+  }
+  c->ev_pending.assign(c->ev_pool, false);
+  c->st.n_resident = nr;
+  c->st.n_offloaded = c->L - nr;
+  c->st.host_pinned_bytes = int64_t(c->host_bytes);
+  c->st.ring_bytes = int64_t(c->ring_bytes);
+  c->st.arena_used = int64_t(c->ar.used);
+  c->st.substitute_bytes = int64_t(size_t(c->L - nr) * layer_q4);
+  c->state = ST_LOADED;
+  return SS_OK;
+}
+
+ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
+  GUARD(c);
+  if (!q || q->bits != 4 || q->group_size != 64) return fail(c, SS_ERR_INVALID, "only 4-bit group-64 substitutes");
+  if (c->state != ST_LOADED) return fail(c, SS_ERR_STRUCTURE, "build_substitutes before load_weights");
+  for (int l = c->n_resident; l < c->L; ++l)
+    for (int g = 0; g < 4; ++g) {
+      const LayerW& w = c->lw[l];
+      CK(cudaMemcpyAsync(c->ring, c->host + w.host_off[g], bf16_bytes(c->gN[g], c->gK[g]), cudaMemcpyHostToDevice, c->cs));
+      launch_quantize_q4(c->ring, w.q4[g], c->gN[g], c->gK[g], c->cs);
+      CK(cudaStreamSynchronize(c->cs));
+    }
+  ss_status s = check_launch(c, "quantize");
+  if (s != SS_OK) return s;
+  c->substitutes_built = true;
+  c->state = ST_READY;
+  c->ring_head = 0;
+  return pump(c);   // start streaming the first verify's layers right away
+}
+
+ss_status ss_prefill(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t chunk, int32_t* out_first) {
+  GUARD(c);
+  if (c->state < ST_READY) return fail(c, SS_ERR_STRUCTURE, "prefill before build_substitutes");
+  if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "prefill inside a step");
+  if (!prompt || n < 1 || chunk < 1 || chunk > c->lim.max_chunk) return fail(c, SS_ERR_INVALID, "prefill: bad prompt/chunk");
+  if (n > c->C) return fail(c, SS_ERR_CAPACITY, "prompt longer than max_context");
+  for (int i = 0; i < n; ++i)
+    if (prompt[i] < 0 || prompt[i] >= c->V) return fail(c, SS_ERR_INVALID, "token id out of range");
+  CK(cudaMemsetAsync(c->committed_len, 0, 4, c->cs));
+  c->P = 0;
+  for (int c0 = 0; c0 < n; c0 += chunk) {
+    const int m = std::min(chunk, n - c0);
+    CK(cudaMemcpyAsync(c->tokbuf, prompt + c0, size_t(m) * 4, cudaMemcpyHostToDevice, c->cs));
+    launch_chain_init(c->tokbuf, m, c->tok, c->parent, c->depth, c->score, c->anc, c->anc_stride, c->cs);
+    c->n_nodes = m;
+    c->cur_k = 1;
+    c->cur_deff = 0;
+    ss_status s = do_verify(c);
+    if (s != SS_OK) return s;
+    if ((s = do_accept(c, true)) != SS_OK) return s;
+    c->P += m;
+    // the pageable prompt buffer is reused next chunk: make the H2D copy complete
+    CK(cudaStreamSynchronize(c->cs));
+  }
+  int32_t first = 0, nn = 0;
+  ss_status s = read_outputs(c, 1, &first, &nn, nullptr);
+  if (s != SS_OK) return s;
+  if (out_first) *out_first = first;
+  c->st.prefill_tokens += n;
+  c->st.committed_len = c->P;
+  c->state = ST_SESSION;
+  harvest_timing(c);
+  return SS_OK;
+}
+
+static ss_status draft_impl(ss_ctx* c, int32_t root_token, const ss_draft_params* p) {
+  if (!p || p->top_k < 1 || p->top_k > c->lim.max_top_k || p->depth < 0 || p->depth > c->lim.max_depth ||
+      !(p->sharpen_t > 0.f) || !std::isfinite(p->sharpen_t))
+    return fail(c, SS_ERR_INVALID, "draft params");
+  if (c->state != ST_SESSION) return fail(c, SS_ERR_STRUCTURE, "draft_tree needs a prefilled session (and no pending step)");
+  if (c->P + 1 > c->C) return fail(c, SS_ERR_CAPACITY, "context full");
+  if (root_token >= c->V) return fail(c, SS_ERR_INVALID, "root token out of range");
+  const int k = p->top_k;
+  const int deff = std::max(0, std::min(p->depth, (c->C - c->P - 1) / k));
+  if (root_token >= 0) CK(cudaMemcpyAsync(c->root_tok, &root_token, 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaEventRecord(c->e0, c->cs));
+  ss_status s;
+  if (deff == 0) {
+    launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, c->use_pdl, c->cs);
+    c->launches++;
+    s = check_launch(c, "tree_init");
+  } else {
+    s = run_draft(c, deff, k, p->sharpen_t);
+  }
+  if (s != SS_OK) return s;
+  CK(cudaEventRecord(c->e1, c->cs));
+  c->cur_k = k;
+  c->cur_deff = deff;
+  c->n_nodes = 1 + k * deff;
+  c->st.last_d_eff = deff;
+  c->state = ST_DRAFTED;
+  if (root_token >= 0) CK(cudaStreamSynchronize(c->cs));   // host int on the stack was the source
+  return SS_OK;
+}
+
+ss_status ss_draft_tree(ss_ctx* c, int32_t root_token, const ss_draft_params* p, int32_t* ot, int32_t* op, int32_t* od,
+                        float* os, int32_t* on) {
+  GUARD(c);
+  ss_status s = draft_impl(c, root_token, p);
+  if (s != SS_OK) return s;
+  const int n = c->n_nodes;
+  if (on) *on = n;
+  if (ot) CK(cudaMemcpyAsync(ot, c->tok, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (op) CK(cudaMemcpyAsync(op, c->parent, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (od) CK(cudaMemcpyAsync(od, c->depth, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (os) CK(cudaMemcpyAsync(os, c->score, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (ot || op || od || os) CK(cudaStreamSynchronize(c->cs));
+  return SS_OK;
+}
+
+static ss_status verify_impl(ss_ctx* c) {
+  if (c->state != ST_DRAFTED) return fail(c, SS_ERR_STRUCTURE, "verify_tree before draft_tree");
+  ss_status s = do_verify(c);
+  if (s != SS_OK) return s;
+  CK(cudaEventRecord(c->e2, c->cs));
+  c->state = ST_VERIFIED;
+  return SS_OK;
+}
+
+ss_status ss_verify_tree(ss_ctx* c, int32_t* opt_argmax, float* opt_gap) {
+  GUARD(c);
+  ss_status s = verify_impl(c);
+  if (s != SS_OK) return s;
+  if (opt_argmax) CK(cudaMemcpyAsync(opt_argmax, c->argmax, size_t(c->n_nodes) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (opt_gap) CK(cudaMemcpyAsync(opt_gap, c->gap, size_t(c->n_nodes) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (opt_argmax || opt_gap) CK(cudaStreamSynchronize(c->cs));
+  return SS_OK;
+}
+
+static ss_status accept_impl(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path) {
+  if (c->state != ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "accept before verify");
+  ss_status s = do_accept(c, false);
+  if (s != SS_OK) return s;
+  CK(cudaEventRecord(c->e3, c->cs));
+  int32_t n = 0;
+  const int cap = c->cur_deff + 1;
+  if ((s = read_outputs(c, cap, out_tokens, &n, opt_path)) != SS_OK) return s;
+  if (out_n) *out_n = n;
+  c->P += n;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, c->e0, c->e1) == cudaSuccess) c->st.draft_ms += ms;
+  if (cudaEventElapsedTime(&ms, c->e1, c->e2) == cudaSuccess) c->st.verify_ms += ms;
+  if (cudaEventElapsedTime(&ms, c->e2, c->e3) == cudaSuccess) c->st.accept_ms += ms;
+  cudaGetLastError();
+  c->st.steps++;
+  c->st.tokens_emitted += n;
+  c->st.committed_len = c->P;
+  c->st.gpu_launches = c->launches;
+  harvest_timing(c);
+  c->state = ST_SESSION;
+  return SS_OK;
+}
+
+ss_status ss_accept_and_commit(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path) {
+  GUARD(c);
+  return accept_impl(c, out_tokens, out_n, opt_path);
+}
+
+ss_status ss_step(ss_ctx* c, const ss_draft_params* p, int32_t* out_tokens, int32_t* out_n) {
+  GUARD(c);
+  ss_status s = draft_impl(c, -1, p);
+  if (s != SS_OK) return s;
+  if ((s = verify_impl(c)) != SS_OK) return s;
+  return accept_impl(c, out_tokens, out_n, nullptr);
+}
+
+ss_status ss_generate(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t max_new, int32_t chunk,
+                      const ss_draft_params* p, int32_t* out_tokens, int32_t* out_n, int32_t* tau_hist) {
+  GUARD(c);
+  if (!p || !out_tokens || max_new < 1) return fail(c, SS_ERR_INVALID, "generate args");
+  if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "generate inside a step");
+  int32_t first = 0;
+  ss_status s = ss_prefill(c, prompt, n, chunk, &first);
+  if (s != SS_OK) return s;
+  int produced = 0;
+  out_tokens[produced++] = first;
+  std::vector<int32_t> buf(size_t(c->lim.max_depth) + 2);
+  ss_draft_params q = *p;
+  const bool ar = p->depth == 0;
+  if (ar) {
+    q.depth = 0;
+    q.top_k = 1;
+  }
+  while (produced < max_new) {
+    if (c->P + 1 > c->C) break;
+    int32_t m = 0;
+    if ((s = ss_step(c, &q, buf.data(), &m)) != SS_OK) return s;
+    if (tau_hist && m >= 0 && m <= p->depth + 1) tau_hist[m]++;
+    for (int i = 0; i < m && produced < max_new; ++i) out_tokens[produced++] = buf[i];
+  }
+  if (out_n) *out_n = produced;
+  return SS_OK;
+}
+
+ss_status ss_get_stats(ss_ctx* c, ss_stats* out) {
+  if (!c || !out) return SS_ERR_INVALID;
+  harvest_timing(c);
+  c->st.gpu_launches = c->launches;
+  *out = c->st;
+  return SS_OK;
+}
+
+ss_status ss_reset_stats(ss_ctx* c) {
+  if (!c) return SS_ERR_INVALID;
+  harvest_timing(c);
+  const ss_stats keep = c->st;
+  c->st = ss_stats{};
+  c->st.arena_used = keep.arena_used;
+  c->st.arena_cap = keep.arena_cap;
+  c->st.ring_bytes = keep.ring_bytes;
+  c->st.host_pinned_bytes = keep.host_pinned_bytes;
+  c->st.substitute_bytes = keep.substitute_bytes;
+  c->st.n_resident = keep.n_resident;
+  c->st.n_offloaded = keep.n_offloaded;
+  c->st.committed_len = keep.committed_len;
+  c->launches = 0;
+  return SS_OK;
+}
+
+const char* ss_last_error(ss_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void ss_destroy(ss_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto e : c->ev_copied) cudaEventDestroy(e);
+  for (auto e : c->ev_consumed) cudaEventDestroy(e);
+  for (auto e : c->ev_t0) cudaEventDestroy(e);
+  for (auto e : c->ev_t1) cudaEventDestroy(e);
+  for (auto e : {c->e0, c->e1, c->e2, c->e3})
+    if (e) cudaEventDestroy(e);
+  if (c->host) cudaFreeHost(c->host);
+  if (c->h_out) cudaFreeHost(c->h_out);
+  cudaGetLastError();
+  delete c;
+}
+
+// ---------------------------------- debug ---------------------------------------------------
+ss_status ss_debug_gen_tensor(ss_ctx* c, uint64_t seed, int32_t tid, int64_t rows, int64_t cols, int32_t kind,
+                              double sigma, uint16_t* out) {
+  GUARD(c);
+  if (!out || rows < 1 || cols < 1) return fail(c, SS_ERR_INVALID, "gen_tensor args");
+  if (c->state != ST_CREATED && c->state < ST_READY) return fail(c, SS_ERR_STRUCTURE, "gen_tensor needs a free ring");
+  const size_t bytes = size_t(rows) * cols * 2;
+  uint8_t* buf = c->ring ? c->ring : c->ar.base + c->ar.used;
+  const size_t room = c->ring ? c->ring_bytes : c->ar.cap - c->ar.used;
+  if (bytes > room) return fail(c, SS_ERR_BUDGET, "gen_tensor: tensor larger than free arena");
+  if (c->ring && !c->inflight.empty()) {   // ring busy with prefetches: drain them first
+    CK(cudaStreamSynchronize(c->xs));
+    return fail(c, SS_ERR_STRUCTURE, "gen_tensor: ring in use by streaming");
+  }
+  launch_gen_natural(reinterpret_cast<uint16_t*>(buf), tensor_key(seed, uint64_t(tid)), uint64_t(rows) * cols,
+                     scale_c32(sigma), kind == 1, c->cs);
+  CK(cudaMemcpyAsync(out, buf, bytes, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  return check_launch(c, "gen_tensor");
+}
+
+static ss_status drain_stream(ss_ctx* c) {
+  CK(cudaStreamSynchronize(c->cs));
+  CK(cudaStreamSynchronize(c->xs));
+  return SS_OK;
+}
+
+ss_status ss_debug_read_group(ss_ctx* c, int32_t layer, int32_t group, uint16_t* out) {
+  GUARD(c);
+  if (c->state < ST_LOADED || layer < 0 || layer >= c->L || group < 0 || group > 3 || !out)
+    return fail(c, SS_ERR_INVALID, "read_group args");
+  const int N = c->gN[group], K = c->gK[group];
+  const LayerW& w = c->lw[layer];
+  ss_status s = drain_stream(c);
+  if (s != SS_OK) return s;
+  // tiled source: resident buffer, or the host store copied to the device
+  uint8_t* src = w.resident ? w.bf16[group] : nullptr;
+  std::vector<uint8_t> tmp;
+  if (!w.resident) {
+    tmp.resize(bf16_bytes(N, K));
+    std::memcpy(tmp.data(), c->host + w.host_off[group], tmp.size());
+  } else {
+    tmp.resize(bf16_bytes(N, K));
+    CK(cudaMemcpyAsync(tmp.data(), src, tmp.size(), cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaStreamSynchronize(c->cs));
+  }
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t k = 0; k < K; ++k)
+      std::memcpy(out + n * K + k, tmp.data() + bf16_tiled_offset(n, k, K), 2);
+  return SS_OK;
+}
+
+ss_status ss_debug_get_substitute(ss_ctx* c, int32_t layer, int32_t group, uint8_t* codes, uint16_t* s, uint16_t* z) {
+  GUARD(c);
+  if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || c->lw[layer].resident)
+    return fail(c, SS_ERR_INVALID, "get_substitute: not an offloaded layer (or substitutes not built)");
+  const int N = c->gN[group], K = c->gK[group];
+  std::vector<uint8_t> q(q4_bytes(N, K));
+  CK(cudaMemcpyAsync(q.data(), c->lw[layer].q4[group], q.size(), cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t k = 0; k < K; ++k) {
+      uint64_t off;
+      int sh;
+      q4_code_pos(n, k, K, &off, &sh);
+      if (codes) codes[n * K + k] = (q[off] >> sh) & 15;
+      if ((k & 63) == 0) {
+        uint32_t m;
+        std::memcpy(&m, q.data() + q4_meta_offset(n, k, K), 4);
+        if (s) s[n * (K / 64) + k / 64] = uint16_t(m & 0xFFFF);
+        if (z) z[n * (K / 64) + k / 64] = uint16_t(m >> 16);
+      }
+    }
+  return SS_OK;
+}
+
+ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group, const uint16_t* x, int32_t M, float* y) {
+  GUARD(c);
+  if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || !x || !y || M < 1)
+    return fail(c, SS_ERR_INVALID, "debug_matmul args");
+  if (which == 0 && M > 32) return fail(c, SS_ERR_INVALID, "draft GEMV: M <= 32");
+  if (which == 1 && M > c->mpad_max) return fail(c, SS_ERR_INVALID, "target GEMM: M too large");
+  const int N = c->gN[group], K = c->gK[group];
+  const int NT = which == 0 ? gemv_nt(M) : gemm_nt(M);
+  ss_status s = drain_stream(c);
+  if (s != SS_OK) return s;
+  // X -> FragX (host side), into hfrag/actfrag scratch
+  std::vector<uint16_t> fx(size_t(NT) * 8 * K, 0);
+  for (int m = 0; m < M; ++m)
+    for (int k = 0; k < K; ++k) fx[fragx_offset(m, k, NT)] = x[int64_t(m) * K + k];
+  uint16_t* X = K == c->F ? c->actfrag : c->hfrag;
+  CK(cudaMemcpyAsync(X, fx.data(), fx.size() * 2, cudaMemcpyHostToDevice, c->cs));
+  float* Y = c->at_o;   // debug output scratch: the attention partial buffer
+  if (size_t(M) * N > size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d)
+    return fail(c, SS_ERR_BUDGET, "debug_matmul: output too large");
+  EpiParams e = base_epi(c, M);
+  e.kind = EPI_STORE;
+  e.out = Y;
+  e.ldo = N;
+  const LayerW& w = c->lw[layer];
+  if (which == 0) {
+    GemvParams p{};
+    p.W = w.resident ? w.bf16[group] : w.q4[group];
+    p.X = X;
+    p.N = N;
+    p.K = K;
+    p.NT = NT;
+    p.partials = c->gv_part;
+    p.counters = c->gv_cnt;
+    p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+    p.epi = e;
+    launch_gemv(!w.resident, p, c->gv_grid, false, c->cs);
+  } else {
+    GemmParams p{};
+    p.X = X;
+    p.N = N;
+    p.K = K;
+    p.NT = NT;
+    p.epi = e;
+    if (w.resident) {
+      p.W = w.bf16[group];
+    } else {
+      return fail(c, SS_ERR_STRUCTURE, "debug target matmul on an offloaded layer: use a resident layer");
+    }
+    launch_gemm(p, false, c->cs);
+  }
+  CK(cudaMemcpyAsync(y, Y, size_t(M) * N * 4, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  return check_launch(c, "debug_matmul");
+}
+
+ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
+                               float* out_ms) {
+  GUARD(c);
+  if (c->state < ST_READY || which != 0 || layer < 0 || layer >= c->L || group < -1 || group > 3 || M < 1 || M > 32 ||
+      iters < 1 || !out_ms)
+    return fail(c, SS_ERR_INVALID, "time_matmul args");
+  const bool head = group == -1;
+  const int N = head ? c->V : c->gN[group], K = head ? c->H : c->gK[group];
+  const LayerW& w = c->lw[layer];
+  GemvParams p{};
+  p.W = head ? c->head : (w.resident ? w.bf16[group] : w.q4[group]);
+  p.X = K == c->F ? c->actfrag : c->hfrag;
+  p.N = N;
+  p.K = K;
+  p.NT = gemv_nt(M);
+  p.partials = c->gv_part;
+  p.counters = c->gv_cnt;
+  p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+  p.epi = base_epi(c, M);
+  p.epi.kind = EPI_STORE;
+  p.epi.out = c->logits;
+  p.epi.ldo = N;
+  p.epi.M = 0;   // time the GEMV with a no-op store
+  const bool q4 = !head && !w.resident;
+  launch_gemv(q4, p, c->gv_grid, c->use_pdl, c->cs);
+  CK(cudaEventRecord(c->e0, c->cs));
+  for (int i = 0; i < iters; ++i) launch_gemv(q4, p, c->gv_grid, c->use_pdl, c->cs);
+  CK(cudaEventRecord(c->e1, c->cs));
+  CK(cudaEventSynchronize(c->e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  *out_ms = ms / iters;
+  return check_launch(c, "time_matmul");
+}
+
+ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
+                           float* out_logits) {
+  GUARD(c);
+  if (c->state != ST_SESSION) return fail(c, SS_ERR_STRUCTURE, "debug_forward needs a session");
+  if (!tokens || !parents || n < 1 || n > c->max_nodes || !out_logits) return fail(c, SS_ERR_INVALID, "debug_forward args");
+  // depth-major tree check + host-side depths/ancestors
+  std::vector<int> dep(n), anc(size_t(n) * c->anc_stride, 0), par(parents, parents + n), tk(tokens, tokens + n);
+  for (int i = 0; i < n; ++i) {
+    if (i == 0 ? parents[0] != -1 : (parents[i] < 0 || parents[i] >= i)) return fail(c, SS_ERR_STRUCTURE, "tree not depth-major");
+    dep[i] = i == 0 ? 0 : dep[parents[i]] + 1;
+    if (i > 0 && dep[i] < dep[i - 1]) return fail(c, SS_ERR_STRUCTURE, "tree not depth-major");
+    if (dep[i] >= c->anc_stride) return fail(c, SS_ERR_CAPACITY, "tree too deep");
+    if (tokens[i] < 0 || tokens[i] >= c->V) return fail(c, SS_ERR_INVALID, "token id");
+    int a = i, dd = dep[i];
+    while (a >= 0) {
+      anc[size_t(i) * c->anc_stride + dd--] = a;
+      a = parents[a];
+    }
+  }
+  if (c->P + dep[n - 1] + 1 > c->C) return fail(c, SS_ERR_CAPACITY, "tree beyond max_context");
+  std::vector<float> sc(n, 0.f);
+  CK(cudaMemcpyAsync(c->tok, tk.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->parent, par.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->depth, dep.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->score, sc.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->anc, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  ss_status s;
+  if (which == 0) {
+    int i0 = 0;
+    while (i0 < n) {
+      int i1 = i0;
+      while (i1 < n && dep[i1] == dep[i0]) ++i1;
+      if (i1 - i0 > 32) return fail(c, SS_ERR_INVALID, "draft debug forward: <= 32 nodes per depth");
+      PassOut o;
+      o.logits = true;
+      if ((s = forward_pass(c, false, i1 - i0, i0, o)) != SS_OK) return s;
+      CK(cudaMemcpyAsync(out_logits + int64_t(i0) * c->V, c->logits, size_t(i1 - i0) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
+      CK(cudaStreamSynchronize(c->cs));
+      i0 = i1;
+    }
+  } else {
+    PassOut o;   // no head: we read logits via the GEMV head in 32-row groups below
+    c->n_nodes = n;
+    if ((s = forward_pass(c, true, n, 0, o)) != SS_OK) return s;
+    for (int r0 = 0; r0 < n; r0 += 32) {
+      const int m = std::min(32, n - r0);
+      launch_rmsnorm(c->x + int64_t(r0) * c->H, m, c->H, c->final_norm, c->cfg.rms_eps, c->hfrag, gemv_nt(m), false, c->cs);
+      GemvParams p{};
+      p.W = c->head;
+      p.X = c->hfrag;
+      p.N = c->V;
+      p.K = c->H;
+      p.NT = gemv_nt(m);
+      p.partials = c->gv_part;
+      p.counters = c->gv_cnt;
+      p.max_seg = gemv_max_segments(c->V, c->H, c->gv_grid);
+      p.epi = base_epi(c, m);
+      p.epi.kind = EPI_LOGITS;
+      p.epi.out = c->logits;
+      p.epi.ldo = c->V;
+      launch_gemv(false, p, c->gv_grid, false, c->cs);
+      CK(cudaMemcpyAsync(out_logits + int64_t(r0) * c->V, c->logits, size_t(m) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
+      CK(cudaStreamSynchronize(c->cs));
+    }
+  }
+  return check_launch(c, "debug_forward");
+}
+
+ss_status ss_debug_set_tree(ss_ctx* c, const int32_t* tokens, const int32_t* parents, int32_t n, int32_t top_k) {
+  GUARD(c);
+  if (c->state != ST_SESSION) return fail(c, SS_ERR_STRUCTURE, "set_tree needs a session");
+  if (!tokens || !parents || n < 1 || top_k < 1 || (n - 1) % top_k || n > c->max_nodes)
+    return fail(c, SS_ERR_INVALID, "set_tree args");
+  const int D = (n - 1) / top_k;
+  if (c->P + 1 + D > c->C) return fail(c, SS_ERR_CAPACITY, "tree beyond max_context");
+  std::vector<int> dep(n), anc(size_t(n) * c->anc_stride, 0);
+  for (int i = 0; i < n; ++i) {
+    const int want = i == 0 ? 0 : 1 + (i - 1) / top_k;
+    dep[i] = i == 0 ? 0 : dep[parents[i]] + 1;
+    if ((i == 0 && parents[0] != -1) || (i > 0 && (parents[i] < 0 || parents[i] >= i)) || dep[i] != want)
+      return fail(c, SS_ERR_STRUCTURE, "set_tree: not a depth-major k-ary tree");
+    int a = i, dd = dep[i];
+    while (a >= 0) {
+      anc[size_t(i) * c->anc_stride + dd--] = a;
+      a = parents[a];
+    }
+  }
+  std::vector<float> sc(n, 0.f);
+  CK(cudaMemcpyAsync(c->tok, tokens, size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->parent, parents, size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->depth, dep.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->score, sc.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->anc, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->root_tok, tokens, 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  c->n_nodes = n;
+  c->cur_k = top_k;
+  c->cur_deff = D;
+  CK(cudaEventRecord(c->e0, c->cs));
+  CK(cudaEventRecord(c->e1, c->cs));
+  c->state = ST_DRAFTED;
+  return SS_OK;
+}
+
+ss_status ss_debug_read_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v) {
+  GUARD(c);
+  if (layer < 0 || layer >= c->L || pos0 < 0 || n < 1 || pos0 + n > c->C || !k || !v)
+    return fail(c, SS_ERR_INVALID, "read_kv args");
+  CK(cudaStreamSynchronize(c->cs));
+  for (int h = 0; h < c->nkv; ++h) {
+    const int64_t src = layer * c->kc_layer + (int64_t(h) * c->C + pos0) * c->d;
+    CK(cudaMemcpyAsync(k + int64_t(h) * n * c->d, c->kc + src, size_t(n) * c->d * 2, cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaMemcpyAsync(v + int64_t(h) * n * c->d, c->vc + src, size_t(n) * c->d * 2, cudaMemcpyDeviceToHost, c->cs));
+  }
+  CK(cudaStreamSynchronize(c->cs));
+  return SS_OK;
+}
+
+}  // extern "C"

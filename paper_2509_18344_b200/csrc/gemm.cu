@@ -1,0 +1,124 @@
+// K6 — dense bf16 GEMM for verification / prefill (M = 1 + kD tree nodes, or a prefill chunk).
+// Y[M x N] = X[M x K] * W^T over staged (streamed) or resident bf16 weights,
+// fused epilogues incl. the K8 per-tile argmax for the head (logits never written to HBM).
+// Each output element reduces over K in a fixed order independent of M (no split-K), so the
+// target path is batch-invariant: a node's logits are bitwise those of an AR step.
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+constexpr int kGemmConsumerWarps = 8;
+constexpr int kGemmThreads = (kGemmConsumerWarps + 1) * 32;
+constexpr int kGemmTokNT = 16;                                // 128 tokens per CTA
+constexpr int kGemmXBytes = kGemmTokNT * kXChunkBytesPerNT;   // 32 KB
+constexpr int kGemmStageBytes = kBF16TileBytes + kGemmXBytes; // 64 KB
+constexpr int kGemmStages = 3;
+constexpr int kGemmSmem = kGemmStages * kGemmStageBytes + 2 * kGemmStages * 8 + 64;
+
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(const GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGemmStages * kGemmStageBytes);
+  uint64_t* empty = full + kGemmStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x, tt = blockIdx.y;
+  const int nC = p.K >> 7;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGemmStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kGemmConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const uint8_t* wbase = p.W + int64_t(r) * nC * kBF16TileBytes;
+  if (warp == kGemmConsumerWarps) {
+    if (lane == 0) {
+      const int pre = nC < kGemmStages ? nC : kGemmStages;
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], kGemmStageBytes);
+        bulk_g2s(ring + i * kGemmStageBytes, wbase + int64_t(i) * kBF16TileBytes, kBF16TileBytes, &full[i]);
+      }
+      griddep_wait();
+      for (int i = 0; i < pre; ++i)
+        bulk_g2s(ring + i * kGemmStageBytes + kBF16TileBytes,
+                 p.X + (int64_t(i) * p.NT + tt * kGemmTokNT) * 1024, kGemmXBytes, &full[i]);
+      for (int i = pre; i < nC; ++i) {
+        const int s = i % kGemmStages;
+        mbar_wait(&empty[s], uint32_t(i / kGemmStages - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], kGemmStageBytes);
+        bulk_g2s(ring + s * kGemmStageBytes, wbase + int64_t(i) * kBF16TileBytes, kBF16TileBytes, &full[s]);
+        bulk_g2s(ring + s * kGemmStageBytes + kBF16TileBytes, p.X + (int64_t(i) * p.NT + tt * kGemmTokNT) * 1024,
+                 kGemmXBytes, &full[s]);
+      }
+    }
+  } else {
+    griddep_wait();
+    const int g = lane >> 2, t4 = lane & 3;
+    float acc[kGemmTokNT][4];
+#pragma unroll
+    for (int j = 0; j < kGemmTokNT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int i = 0; i < nC; ++i) {
+      const int s = i % kGemmStages;
+      mbar_wait(&full[s], uint32_t(i / kGemmStages) & 1);
+      const uint8_t* wst = ring + s * kGemmStageBytes;
+      const uint8_t* xst = wst + kBF16TileBytes;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 r0 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 0) * 4 + q) * 32 + lane) * 16);
+        const uint4 r1 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 1) * 4 + q) * 32 + lane) * 16);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int st = 2 * q + hh;
+          const uint32_t a0 = hh ? r0.z : r0.x, a2 = hh ? r0.w : r0.y;
+          const uint32_t a1 = hh ? r1.z : r1.x, a3 = hh ? r1.w : r1.y;
+#pragma unroll
+          for (int j = 0; j < kGemmTokNT; ++j) {
+            const uint2 b = *reinterpret_cast<const uint2*>(xst + ((((j * 8 + st) * 4 + t4) * 8 + g) * 8));
+            mma_bf16_16816(acc[j], a0, a1, a2, a3, b.x, b.y);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // all stages consumed and no copies outstanding: reuse the ring as the output tile
+    asm volatile("bar.sync 1, %0;" ::"r"(kGemmConsumerWarps * 32) : "memory");
+    float* tile = reinterpret_cast<float*>(ring);
+    constexpr int ld = kGemmTokNT * 8 + 1;   // +1: conflict-free column scans in the argmax epilogue
+#pragma unroll
+    for (int j = 0; j < kGemmTokNT; ++j) {
+      const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
+      tile[n0 * ld + m] = acc[j][0];
+      tile[n0 * ld + m + 1] = acc[j][1];
+      tile[(n0 + 8) * ld + m] = acc[j][2];
+      tile[(n0 + 8) * ld + m + 1] = acc[j][3];
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kGemmConsumerWarps * 32) : "memory");
+    griddep_launch();
+    apply_epilogue(p.epi, tile, ld, r, tt * 128, 128, threadIdx.x, kGemmConsumerWarps * 32);
+  }
+}
+
+void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.N / 128, (p.NT * 8) / 128);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = kGemmSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, gemm_kernel, p);
+}
+
+}  // namespace ss

@@ -1,0 +1,162 @@
+// Weight generator (independent re-implementation of synth/weights.py),
+// K1 substitute quantizer (SURVEY O.2 / PAPER.md:133-136, :278) and layout debug readbacks.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+SS_DEV uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// element value for row-major index idx: Irwin-Hall(4) integer, one fp32 multiply, (gain: + 1.0f), RNE bf16
+SS_DEV uint16_t gen_value(uint64_t key, uint64_t idx, float c32, int gain) {
+  uint64_t r = splitmix64(key ^ idx);
+  int32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s += int32_t((r >> (16 * j)) & 0xFFFFu);
+  int32_t s2 = 2 * s - 4 * 65535;
+  float w = __fmul_rn(float(s2), c32);   // s2 exact in fp32 (|s2| < 2^18)
+  if (gain) w = __fadd_rn(1.0f, w);
+  return f2bf(w);
+}
+
+// natural row-major destination (embedding, norm gains, biases)
+__global__ void gen_natural_kernel(uint16_t* __restrict__ dst, uint64_t key, uint64_t count, float c32, int gain) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count; i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = gen_value(key, i, c32, gain);
+}
+
+// tiled destination: src [rows x K] row-major index space, dst row = map(src row)
+// map: 0 -> dst = row_off + r ; 1 -> gate rows (r/64)*128 + r%64 ; 2 -> up rows (r/64)*128 + 64 + r%64
+__global__ void gen_tiled_kernel(uint8_t* __restrict__ dst, uint64_t key, int64_t rows, int64_t K, float c32,
+                                 int map, int64_t row_off) {
+  int64_t n8 = rows * (K / 8);
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n8; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t r = t / (K / 8), k0 = (t % (K / 8)) * 8;
+    int64_t dr = map == 0 ? row_off + r : (map == 1 ? (r / 64) * 128 + (r % 64) : (r / 64) * 128 + 64 + (r % 64));
+    uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint16_t lo = gen_value(key, uint64_t(r * K + k0 + 2 * e), c32, 0);
+      uint16_t hi = gen_value(key, uint64_t(r * K + k0 + 2 * e + 1), c32, 0);
+      v[e] = uint32_t(lo) | (uint32_t(hi) << 16);
+    }
+    *reinterpret_cast<uint4*>(dst + bf16_tiled_offset(dr, k0, K)) = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st) {
+  int blocks = int((count + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gen_natural_kernel<<<blocks, 256, 0, st>>>(dst, key, count, c32, gain);
+}
+void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float c32, int map, int64_t row_off,
+                      cudaStream_t st) {
+  int64_t n8 = rows * (K / 8);
+  int blocks = int((n8 + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gen_tiled_kernel<<<blocks, 256, 0, st>>>(dst, key, rows, K, c32, map, row_off);
+}
+
+// ---------------------------------------------------------------------------
+// K1: RTN min/max 4-bit group-64 quantizer, bf16 tiled -> Q4 tiled.
+// One warp per (tile-chunk, 16-row block).  Lane (g, t4) holds rows 16w+g, 16w+g+8 and
+// k = 32 t4 .. 32 t4 + 31; a 64-group spans lanes t4 = {0,1} or {2,3} (partner = lane ^ 1).
+//   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / 15) ; z = m
+//   code = clamp(rint_even(fp32(x - z) / s), 0, 15)       (IEEE div.rn; built without fast-math)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) quantize_q4_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                          int64_t n_tc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t4 = lane & 3, g = lane >> 2;
+  for (int64_t tc = blockIdx.x; tc < n_tc; tc += gridDim.x) {
+    const uint8_t* s_tile = src + tc * kBF16TileBytes;
+    uint8_t* d_tile = dst + tc * kQ4TileBytes;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float x[32];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v = *reinterpret_cast<const uint4*>(s_tile + (((warp * 2 + h) * 4 + q) * 32 + lane) * 16);
+        uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x[q * 8 + 2 * e] = __uint_as_float(w4[e] << 16);
+          x[q * 8 + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
+        }
+      }
+      float mn = x[0], mx = x[0];
+#pragma unroll
+      for (int i = 1; i < 32; ++i) {
+        mn = fminf(mn, x[i]);
+        mx = fmaxf(mx, x[i]);
+      }
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      float sc;
+      if (mx == mn) {
+        sc = 1.0f;
+      } else {
+        sc = __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), 15.0f))) << 16);
+      }
+      const float z = mn;
+      uint32_t words[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float t = __fdiv_rn(__fsub_rn(x[i], z), sc);
+        float r = rintf(t);
+        r = fminf(fmaxf(r, 0.0f), 15.0f);
+        uint32_t code = uint32_t(r);
+        int c = i & 7, slot = (c & 1) * 4 + (c >> 1);
+        words[i >> 3] |= code << (4 * slot);
+      }
+      *reinterpret_cast<uint4*>(d_tile + ((warp * 2 + h) * 32 + lane) * 16) =
+          make_uint4(words[0], words[1], words[2], words[3]);
+      if ((t4 & 1) == 0) {
+        int grp = t4 >> 1, rr = g + 8 * h;
+        uint32_t meta = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
+        *reinterpret_cast<uint32_t*>(d_tile + kQ4CodeBytes + ((warp * 2 + grp) * 16 + rr) * 4) = meta;
+      }
+    }
+  }
+}
+
+void launch_quantize_q4(const uint8_t* src_bf16_tiled, uint8_t* dst_q4, int64_t N, int64_t K, cudaStream_t st) {
+  int64_t n_tc = (N / 128) * (K / 128);
+  int blocks = int(n_tc < 148 * 8 ? n_tc : 148 * 8);
+  quantize_q4_kernel<<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q4, n_tc);
+}
+
+// ---- debug readbacks --------------------------------------------------------
+__global__ void q4_to_canonical_kernel(const uint8_t* __restrict__ q4, uint8_t* codes, uint16_t* s, uint16_t* z,
+                                       int64_t N, int64_t K) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < N * K; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t n = t / K, k = t % K;
+    uint64_t off;
+    int sh;
+    q4_code_pos(n, k, K, &off, &sh);
+    codes[t] = (q4[off] >> sh) & 15;
+    if ((k & 63) == 0) {
+      uint32_t m = *reinterpret_cast<const uint32_t*>(q4 + q4_meta_offset(n, k, K));
+      s[n * (K / 64) + k / 64] = uint16_t(m & 0xFFFF);
+      z[n * (K / 64) + k / 64] = uint16_t(m >> 16);
+    }
+  }
+}
+__global__ void tiled_to_natural_kernel(const uint8_t* __restrict__ t, uint16_t* out, int64_t N, int64_t K) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < N * K; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = *reinterpret_cast<const uint16_t*>(t + bf16_tiled_offset(i / K, i % K, K));
+}
+void launch_q4_to_canonical(const uint8_t* q4, uint8_t* codes, uint16_t* s, uint16_t* z, int64_t N, int64_t K,
+                            cudaStream_t st) {
+  q4_to_canonical_kernel<<<1024, 256, 0, st>>>(q4, codes, s, z, N, K);
+}
+void launch_tiled_to_natural(const uint8_t* t, uint16_t* out, int64_t N, int64_t K, cudaStream_t st) {
+  tiled_to_natural_kernel<<<1024, 256, 0, st>>>(t, out, N, K);
+}
+
+}  // namespace ss

@@ -1,0 +1,151 @@
+// Internal launcher interface of libsubspec (not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ss {
+
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5 };
+
+// Epilogue parameters shared by the GEMV (draft, M <= 32) and GEMM (verify) kernels.
+struct EpiParams {
+  int kind;
+  int M;                         // valid tokens (rows of X)
+  // EPI_QKV
+  const uint16_t* bias;          // fused [q|k|v] bias (bf16) or nullptr
+  uint16_t* q_out;               // [M x q_dim] bf16 natural
+  uint16_t* k_tree;              // this layer's tree scratch K [n_kv][max_nodes][d]
+  uint16_t* v_tree;
+  int max_nodes, node_base;
+  const int* committed_len;      // device P
+  const int* depth;              // per-node depth (indexed node_base + m)
+  const float2* rope;            // [max_ctx][d/2] (cos, sin)
+  int q_dim, kv_dim, head_dim;
+  // EPI_RESID
+  float* x;                      // [M x ldx] fp32 residual stream
+  int ldx;
+  // EPI_SILU
+  uint16_t* act;                 // FragX [Mpad x F]
+  int act_nt, ffn;
+  // EPI_LOGITS / EPI_STORE
+  float* out;                    // [M x ldo]
+  int ldo;
+  // EPI_ARGMAX: per (token, row tile) partial (max, idx, second max)
+  float* am_val;                 // [M x n_tiles]
+  int* am_idx;
+  float* am_second;
+  int am_tiles;
+};
+
+struct GemvParams {
+  const uint8_t* W;              // tiled weights (Q4 or BF16)
+  const uint16_t* X;             // FragX [Mpad x K]
+  int N, K, NT;                  // NT = Mpad / 8
+  float* partials;               // [n_tiles][max_seg][128*Mpad]
+  int* counters;                 // [n_tiles], zero on entry, restored to zero on exit
+  int max_seg;
+  EpiParams epi;
+};
+
+int gemv_max_segments(int N, int K, int grid);
+void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
+
+struct GemmParams {
+  const uint8_t* W;              // tiled BF16 weights [N x K]
+  const uint16_t* X;             // FragX [Mpad x K], Mpad % 128 == 0
+  int N, K, NT;                  // NT = Mpad/8
+  EpiParams epi;
+};
+void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st);
+
+// generator / quantizer / readback
+void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st);
+void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float c32, int map, int64_t row_off,
+                      cudaStream_t st);
+void launch_quantize_q4(const uint8_t* src_bf16_tiled, uint8_t* dst_q4, int64_t N, int64_t K, cudaStream_t st);
+void launch_q4_to_canonical(const uint8_t* q4, uint8_t* codes, uint16_t* s, uint16_t* z, int64_t N, int64_t K,
+                            cudaStream_t st);
+void launch_tiled_to_natural(const uint8_t* t, uint16_t* out, int64_t N, int64_t K, cudaStream_t st);
+
+// small kernels (K4, K5, K8, K9)
+void launch_embed_rmsnorm(const int* tokens_dev, int tok_offset, int M, const uint16_t* embed, float* x, int H,
+                          const uint16_t* gain, float eps, uint16_t* h_fragx, int nt, bool pdl, cudaStream_t st);
+void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float eps, uint16_t* h_fragx, int nt,
+                    bool pdl, cudaStream_t st);
+
+struct AttnParams {
+  const uint16_t* q;             // [n_q x n_h*d] bf16
+  const uint16_t* k_cache;       // committed [n_kv][max_ctx][d]
+  const uint16_t* v_cache;
+  const uint16_t* k_tree;        // [n_kv][max_nodes][d]
+  const uint16_t* v_tree;
+  const int* committed_len;
+  const int* anc;                // [max_nodes][anc_stride] ancestor slots root..self
+  const int* depth;              // [max_nodes]
+  int anc_stride, max_ctx, max_nodes;
+  int n_q, node_base;            // query rows are nodes node_base .. node_base + n_q - 1
+  int n_heads, n_kv, head_dim;
+  int split;                     // prefix keys per segment
+  int n_seg_max;                 // segments allocated in the partial buffers
+  float* part_o;                 // [n_q * n_heads][n_seg_max][d]
+  float* part_ml;                // [n_q * n_heads][n_seg_max][2]
+  uint16_t* out_fragx;           // [Mpad x n_heads*d] FragX
+  int out_nt;
+};
+void launch_attention(const AttnParams& p, int max_prefix, bool pdl, cudaStream_t st);
+
+struct TopkParams {
+  const float* logits;           // [M x V]
+  int M, V, k;
+  float inv_t;                   // 1 / sharpen temperature
+  int blocks_per_row;
+  float* blk_max;                // [M][B]
+  float* blk_sum;                // [M][B]  sum exp((l - blk_max) * inv_t)
+  float* blk_val;                // [M][B][k]
+  int* blk_idx;
+  // tree state (device)
+  int* tok;                      // [max_nodes]
+  int* parent;
+  int* depth;
+  float* score;
+  int* anc;                      // [max_nodes][anc_stride]
+  int anc_stride;
+  int node_base;                 // frontier nodes node_base .. node_base + M - 1
+  int child_base;                // new nodes child_base .. child_base + k - 1
+  int child_depth;
+};
+void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st);
+
+void launch_argmax_merge(const float* am_val, const int* am_idx, const float* am_second, int M, int tiles,
+                         int* argmax, float* gap, bool pdl, cudaStream_t st);
+
+struct AcceptParams {
+  const int* argmax;             // [n_nodes]
+  const int* tok;
+  const int* parent;
+  int* commit_meta;              // [2]: base position, rows committed
+  int n_nodes, k, depth_max;
+  int* committed_len;            // in/out
+  int* root_tok;                 // out: bonus token = next root
+  int* out_tokens;               // [depth_max + 1] emitted tokens
+  int* out_n;                    // count
+  int* out_path;                 // [depth_max + 1]: root + accepted slots
+  // KV commit
+  uint16_t* k_cache;             // base of committed K for layer 0; layer stride below
+  uint16_t* v_cache;
+  const uint16_t* k_tree;
+  const uint16_t* v_tree;
+  int64_t cache_layer_stride, tree_layer_stride;   // elements
+  int n_layers, n_kv, head_dim, max_ctx, max_nodes;
+  int chain;                     // 1: commit all nodes (prefill chunk), ignore argmax
+};
+void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st);
+
+// tree init for a new step: root node (slot 0) with token *root_tok, depth 0
+void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,
+                      cudaStream_t st);
+// chain tree for prefill chunk: tokens copied from device buffer
+void launch_chain_init(const int* tokens, int n, int* tok, int* parent, int* depth, float* score, int* anc,
+                       int anc_stride, cudaStream_t st);
+
+}  // namespace ss

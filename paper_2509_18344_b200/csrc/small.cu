@@ -1,0 +1,584 @@
+// K3 tree attention, K4 RMSNorm/embedding, K5 sharpened top-k tree growth, K8 argmax merge,
+// K9 greedy acceptance + KV commit.  All reductions use fixed orders (bitwise reproducible).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ss {
+
+static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStream_t st, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+// block-wide fixed-order sum (256 threads)
+SS_DEV float block_sum_256(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x < 32) {
+    t = (l < 8) ? red[l] : 0.f;
+    t = warp_sum(t);
+    if (l == 0) red[8] = t;
+  }
+  __syncthreads();
+  return red[8];
+}
+
+// ---------------------------------------------------------------------------
+// K4: h = bf16(x * 1/sqrt(mean(x^2) + eps) * g) -> FragX.  Optionally x = embed[token] first.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const int* tokens, int tok_offset, const uint16_t* embed,
+                                                      float* x, int H, const uint16_t* gain, float eps,
+                                                      uint16_t* out, int nt) {
+  __shared__ float red[9];
+  const int m = blockIdx.x;
+  griddep_wait();
+  griddep_launch();
+  float* xr = x + int64_t(m) * H;
+  if (embed) {
+    const uint16_t* er = embed + int64_t(tokens[tok_offset + m]) * H;
+    for (int i = threadIdx.x; i < H; i += 256) xr[i] = bf2f(er[i]);
+    __syncthreads();
+  }
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < H; i += 256) ss += xr[i] * xr[i];
+  ss = block_sum_256(ss, red);
+  const float r = 1.0f / sqrtf(ss / float(H) + eps);
+  for (int i = threadIdx.x; i < H; i += 256) out[fragx_offset(m, i, nt)] = f2bf(xr[i] * r * bf2f(gain[i]));
+}
+
+void launch_embed_rmsnorm(const int* tokens_dev, int tok_offset, int M, const uint16_t* embed, float* x, int H,
+                          const uint16_t* gain, float eps, uint16_t* h_fragx, int nt, bool pdl, cudaStream_t st) {
+  void* args[] = {&tokens_dev, &tok_offset, &embed, &x, &H, &gain, &eps, &h_fragx, &nt};
+  launch_pdl((const void*)rmsnorm_kernel, dim3(M), dim3(256), 0, pdl, st, args);
+}
+void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float eps, uint16_t* h_fragx, int nt,
+                    bool pdl, cudaStream_t st) {
+  const int* tokens = nullptr;
+  int off = 0;
+  const uint16_t* embed = nullptr;
+  float* xx = const_cast<float*>(x);
+  void* args[] = {&tokens, &off, &embed, &xx, &H, &gain, &eps, &h_fragx, &nt};
+  launch_pdl((const void*)rmsnorm_kernel, dim3(M), dim3(256), 0, pdl, st, args);
+}
+
+// ---------------------------------------------------------------------------
+// K3: tree attention.  Row = (query node, head).  The keys of node i
+// form one LOGICAL sequence: committed prefix [0, P) followed by its ancestors root..i (tree
+// slots), i.e. exactly the keys an AR step at that position would see, in the same order.
+// Segment s covers logical keys [s*split, (s+1)*split); prefix keys of a segment are shared by
+// all rows and staged in shared memory, ancestor keys are read per row.  Partials (o, m, l) are
+// merged in segment order by attn_combine.  Because the blocking depends only on the logical key
+// index, a node's attention is bitwise identical whether computed in a tree (verify) or as an AR
+// step.
+// ---------------------------------------------------------------------------
+constexpr int kAttnQB = 8;   // query nodes per CTA
+
+template <int D>
+SS_DEV float dot_q_k(const float* qr, const uint16_t* kr16) {
+  const uint32_t* kr = reinterpret_cast<const uint32_t*>(kr16);
+  float a = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < D / 2; ++i) {
+    const uint32_t kk = kr[i];
+    a += qr[2 * i] * __uint_as_float(kk << 16);
+    a += qr[2 * i + 1] * __uint_as_float(kk & 0xFFFF0000u);
+  }
+  return a;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) attn_partial_kernel(const AttnParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  constexpr int KS = D + 2;                       // padded bf16 row stride (odd word stride)
+  const int kvh = blockIdx.x, seg = blockIdx.y, qb = blockIdx.z;
+  const int grp = p.n_heads / p.n_kv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_wait();
+  griddep_launch();
+  const int P = *p.committed_len;
+  const int q0 = qb * kAttnQB;
+  const int nq = min(kAttnQB, p.n_q - q0);
+  if (nq <= 0) return;
+  const int k0 = seg * p.split;
+  int maxdep = 0;
+  for (int qi = 0; qi < nq; ++qi) maxdep = max(maxdep, p.depth[p.node_base + q0 + qi]);
+  if (k0 >= P + maxdep + 1) return;               // no row has keys in this segment
+  const int nrows = nq * grp;
+  float* qs = reinterpret_cast<float*>(sm);       // [kAttnQB*grp][D]
+  uint16_t* Ks = reinterpret_cast<uint16_t*>(sm + kAttnQB * grp * D * 4);
+  uint16_t* Vs = Ks + p.split * KS;
+  for (int e = threadIdx.x; e < nrows * D; e += 256) {
+    const int row = e / D, i = e % D;
+    const int qi = row / grp, hq = kvh * grp + row % grp;
+    qs[e] = bf2f(p.q[(int64_t(q0 + qi) * p.n_heads + hq) * D + i]);
+  }
+  const int np = max(0, min(p.split, P - k0));    // shared prefix keys in this segment
+  {
+    const uint16_t* kc = p.k_cache + (int64_t(kvh) * p.max_ctx + k0) * D;
+    const uint16_t* vc = p.v_cache + (int64_t(kvh) * p.max_ctx + k0) * D;
+    for (int e = threadIdx.x; e < np * (D / 2); e += 256) {
+      const int j = e / (D / 2), i = e % (D / 2);
+      reinterpret_cast<uint32_t*>(Ks + j * KS)[i] = reinterpret_cast<const uint32_t*>(kc + int64_t(j) * D)[i];
+      reinterpret_cast<uint32_t*>(Vs + j * KS)[i] = reinterpret_cast<const uint32_t*>(vc + int64_t(j) * D)[i];
+    }
+  }
+  __syncthreads();
+  const float scale = rsqrtf(float(D));
+  constexpr int DPL = D / 32;                     // dims per lane
+  const uint16_t* kt = p.k_tree + int64_t(kvh) * p.max_nodes * D;
+  const uint16_t* vt = p.v_tree + int64_t(kvh) * p.max_nodes * D;
+  for (int row = warp; row < nrows; row += 8) {
+    const int qi = row / grp, hq = kvh * grp + row % grp;
+    const int node = p.node_base + q0 + qi;
+    const int nkeys = P + p.depth[node] + 1;      // logical keys of this node
+    const int nk = min(p.split, nkeys - k0);
+    if (nk <= 0) continue;
+    const int* an = p.anc + int64_t(node) * p.anc_stride;
+    const float* qr = qs + row * D;
+    float sc[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = lane + 32 * u;
+      sc[u] = -INFINITY;
+      if (j < nk) {
+        const uint16_t* kr = (j < np) ? (Ks + j * KS) : (kt + int64_t(an[k0 + j - P]) * D);
+        sc[u] = dot_q_k<D>(qr, kr) * scale;
+        mx = fmaxf(mx, sc[u]);
+      }
+    }
+    mx = warp_max(mx);
+    float l = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = lane + 32 * u;
+      sc[u] = (j < nk) ? expf(sc[u] - mx) : 0.f;
+      l += sc[u];
+    }
+    l = warp_sum(l);
+    float o[DPL];
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) o[t] = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jb = 32 * u;
+      if (jb >= nk) break;
+      const int cnt = min(32, nk - jb);
+      for (int jj = 0; jj < cnt; ++jj) {
+        const int j = jb + jj;
+        const float pj = __shfl_sync(0xffffffffu, sc[u], jj);
+        const uint16_t* vr = ((j < np) ? (Vs + j * KS) : (vt + int64_t(an[k0 + j - P]) * D)) + lane * DPL;
+#pragma unroll
+        for (int t = 0; t < DPL; ++t) o[t] += pj * bf2f(vr[t]);
+      }
+    }
+    const int64_t prow = int64_t(q0 + qi) * p.n_heads + hq;
+    float* po = p.part_o + (prow * p.n_seg_max + seg) * D;
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) po[lane * DPL + t] = o[t];
+    if (lane == 0) {
+      p.part_ml[(prow * p.n_seg_max + seg) * 2] = mx;
+      p.part_ml[(prow * p.n_seg_max + seg) * 2 + 1] = l;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
+  griddep_wait();
+  griddep_launch();
+  const int P = *p.committed_len;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * 8 + warp;
+  if (row >= int64_t(p.n_q) * p.n_heads) return;
+  const int qi = int(row / p.n_heads), hq = int(row % p.n_heads);
+  const int nkeys = P + p.depth[p.node_base + qi] + 1;
+  const int nseg = (nkeys + p.split - 1) / p.split;
+  const float* ml = p.part_ml + row * p.n_seg_max * 2;
+  float m = -INFINITY;
+  for (int s = 0; s < nseg; ++s) m = fmaxf(m, ml[2 * s]);
+  constexpr int DPL = D / 32;
+  float o[DPL];
+#pragma unroll
+  for (int t = 0; t < DPL; ++t) o[t] = 0.f;
+  float l = 0.f;
+  for (int s = 0; s < nseg; ++s) {
+    const float w = expf(ml[2 * s] - m);
+    l += w * ml[2 * s + 1];
+    const float* po = p.part_o + (row * p.n_seg_max + s) * D + lane * DPL;
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) o[t] += w * po[t];
+  }
+  const float inv = 1.0f / l;
+#pragma unroll
+  for (int t = 0; t < DPL; ++t)
+    p.out_fragx[fragx_offset(qi, int64_t(hq) * D + lane * DPL + t, p.out_nt)] = f2bf(o[t] * inv);
+}
+
+void launch_attention(const AttnParams& p, int max_prefix, bool pdl, cudaStream_t st) {
+  const int grp = p.n_heads / p.n_kv;
+  const int nseg = (max_prefix + p.split - 1) / p.split;   // max_prefix: max logical keys of any row
+  const size_t smem = size_t(kAttnQB) * grp * p.head_dim * 4 + size_t(2) * p.split * (p.head_dim + 2) * 2;
+  const dim3 grid(p.n_kv, nseg, (p.n_q + kAttnQB - 1) / kAttnQB);
+  AttnParams pp = p;
+  void* args[] = {&pp};
+  if (p.head_dim == 128) {
+    cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    launch_pdl((const void*)attn_partial_kernel<128>, grid, dim3(256), smem, pdl, st, args);
+    launch_pdl((const void*)attn_combine_kernel<128>, dim3((p.n_q * p.n_heads + 7) / 8), dim3(256), 0, pdl, st, args);
+  } else {
+    cudaFuncSetAttribute(attn_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    launch_pdl((const void*)attn_partial_kernel<64>, grid, dim3(256), smem, pdl, st, args);
+    launch_pdl((const void*)attn_combine_kernel<64>, dim3((p.n_q * p.n_heads + 7) / 8), dim3(256), 0, pdl, st, args);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: sharpened log-softmax scores and global top-k tree growth.
+// Stage A (grid M x B): per block max, sum exp((l - max)/T), and the block's top-k logits.
+// Stage B (1 CTA): lse per row, candidate score = parent + (l - max_m)/T - lse_m, global
+// top-k by (score desc, token asc, parent asc), canonical order (parent asc, token asc).
+// ---------------------------------------------------------------------------
+struct Cand {
+  float v;
+  int idx;
+};
+SS_DEV bool better(float va, int ia, float vb, int ib) { return va > vb || (va == vb && ia < ib); }
+
+__global__ void __launch_bounds__(256) topk_block_kernel(const TopkParams p) {
+  __shared__ float red[9];
+  __shared__ Cand wbest[8];
+  __shared__ int taken[32];
+  griddep_wait();
+  griddep_launch();
+  const int m = blockIdx.x, b = blockIdx.y, B = gridDim.y;
+  const int64_t v0 = int64_t(p.V) * b / B, v1 = int64_t(p.V) * (b + 1) / B;
+  const float* l = p.logits + int64_t(m) * p.V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // max
+  float mx = -INFINITY;
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += 256) mx = fmaxf(mx, l[v]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float s = 0.f;
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += 256) s += expf((l[v] - mx) * p.inv_t);
+  s = block_sum_256(s, red);
+  const int base = (m * B + b);
+  if (threadIdx.x == 0) {
+    p.blk_max[base] = mx;
+    p.blk_sum[base] = s;
+  }
+  // k rounds of block argmax with exclusion
+  for (int r = 0; r < p.k; ++r) {
+    float bv = -INFINITY;
+    int bi = INT32_MAX;
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += 256) {
+      bool tk = false;
+      for (int q = 0; q < r; ++q) tk |= (taken[q] == int(v));
+      if (!tk && better(l[v], int(v), bv, bi)) {
+        bv = l[v];
+        bi = int(v);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) wbest[warp] = {bv, bi};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Cand c = wbest[0];
+      for (int w = 1; w < 8; ++w)
+        if (better(wbest[w].v, wbest[w].idx, c.v, c.idx)) c = wbest[w];
+      taken[r] = c.idx;
+      p.blk_val[int64_t(base) * p.k + r] = c.v;
+      p.blk_idx[int64_t(base) * p.k + r] = c.idx;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int B = p.blocks_per_row;
+  float* lse = reinterpret_cast<float*>(sm);        // [M]
+  float* rmax = lse + 32;                           // [M]
+  float* sel_s = rmax + 32;                         // [k]
+  int* sel_t = reinterpret_cast<int*>(sel_s + 32);  // [k] token
+  int* sel_p = sel_t + 32;                          // [k] parent row m
+  __shared__ float wv[32];
+  __shared__ int wt[32], wp[32], wc[32];
+  griddep_wait();
+  griddep_launch();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < p.M) {
+    const int m = threadIdx.x;
+    float mx = -INFINITY;
+    for (int b = 0; b < B; ++b) mx = fmaxf(mx, p.blk_max[m * B + b]);
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += p.blk_sum[m * B + b] * expf((p.blk_max[m * B + b] - mx) * p.inv_t);
+    rmax[m] = mx;
+    lse[m] = logf(s);
+  }
+  __syncthreads();
+  const int ncand = p.M * B * p.k;
+  for (int r = 0; r < p.k; ++r) {
+    float bs = -INFINITY;
+    int bt = INT32_MAX, bp = INT32_MAX, bc = -1;
+    for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
+      const int m = c / (B * p.k);
+      const int tok = p.blk_idx[c];
+      bool tk = false;
+      for (int q = 0; q < r; ++q) tk |= (sel_t[q] == tok && sel_p[q] == m);
+      if (tk) continue;
+      const float lp = (p.blk_val[c] - rmax[m]) * p.inv_t - lse[m];
+      const float sc = p.score[p.node_base + m] + lp;
+      if (sc > bs || (sc == bs && (tok < bt || (tok == bt && m < bp)))) {
+        bs = sc;
+        bt = tok;
+        bp = m;
+        bc = c;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (os > bs || (os == bs && (ot < bt || (ot == bt && op < bp)))) {
+        bs = os;
+        bt = ot;
+        bp = op;
+        bc = oc;
+      }
+    }
+    if (lane == 0) {
+      wv[warp] = bs;
+      wt[warp] = bt;
+      wp[warp] = bp;
+      wc[warp] = bc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s = wv[0];
+      int t = wt[0], pp = wp[0];
+      for (int w = 1; w < int(blockDim.x >> 5); ++w)
+        if (wv[w] > s || (wv[w] == s && (wt[w] < t || (wt[w] == t && wp[w] < pp)))) {
+          s = wv[w];
+          t = wt[w];
+          pp = wp[w];
+        }
+      sel_s[r] = s;
+      sel_t[r] = t;
+      sel_p[r] = pp;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // canonical order: parent asc, token asc (insertion sort, k <= 32)
+    for (int i = 1; i < p.k; ++i) {
+      const float s = sel_s[i];
+      const int t = sel_t[i], pp = sel_p[i];
+      int j = i - 1;
+      while (j >= 0 && (sel_p[j] > pp || (sel_p[j] == pp && sel_t[j] > t))) {
+        sel_s[j + 1] = sel_s[j];
+        sel_t[j + 1] = sel_t[j];
+        sel_p[j + 1] = sel_p[j];
+        --j;
+      }
+      sel_s[j + 1] = s;
+      sel_t[j + 1] = t;
+      sel_p[j + 1] = pp;
+    }
+  }
+  __syncthreads();
+  for (int j = warp; j < p.k; j += blockDim.x >> 5) {
+    const int node = p.child_base + j, par = p.node_base + sel_p[j];
+    if (lane == 0) {
+      p.tok[node] = sel_t[j];
+      p.parent[node] = par;
+      p.depth[node] = p.child_depth;
+      p.score[node] = sel_s[j];
+    }
+    for (int a = lane; a < p.child_depth; a += 32)
+      p.anc[int64_t(node) * p.anc_stride + a] = p.anc[int64_t(par) * p.anc_stride + a];
+    if (lane == 0) p.anc[int64_t(node) * p.anc_stride + p.child_depth] = node;
+  }
+}
+
+void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
+  TopkParams pp = p;
+  void* args[] = {&pp};
+  launch_pdl((const void*)topk_block_kernel, dim3(p.M, p.blocks_per_row), dim3(256), 0, pdl, st, args);
+  launch_pdl((const void*)topk_select_kernel, dim3(1), dim3(1024), 32 * 4 * 5, pdl, st, args);
+}
+
+// ---------------------------------------------------------------------------
+// K8: merge per-tile (max, argmax, second) into per-node argmax (ties -> smallest id) and gap.
+// ---------------------------------------------------------------------------
+__global__ void argmax_merge_kernel(const float* am_val, const int* am_idx, const float* am_second, int M, int tiles,
+                                    int* argmax, float* gap) {
+  griddep_wait();
+  griddep_launch();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * 8 + warp;
+  if (m >= M) return;
+  float bv = -INFINITY, sv = -INFINITY;
+  int bi = INT32_MAX;
+  for (int t = lane; t < tiles; t += 32) {
+    const float v = am_val[int64_t(m) * tiles + t], s2 = am_second[int64_t(m) * tiles + t];
+    const int i = am_idx[int64_t(m) * tiles + t];
+    if (better(v, i, bv, bi)) {
+      sv = fmaxf(bv, s2);
+      bv = v;
+      bi = i;
+    } else {
+      sv = fmaxf(sv, v);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const float os = __shfl_xor_sync(0xffffffffu, sv, o);
+    if (better(ov, oi, bv, bi)) {
+      sv = fmaxf(bv, os);
+      bv = ov;
+      bi = oi;
+    } else {
+      sv = fmaxf(sv, ov);
+    }
+  }
+  if (lane == 0) {
+    argmax[m] = bi;
+    gap[m] = bv - sv;
+  }
+}
+void launch_argmax_merge(const float* am_val, const int* am_idx, const float* am_second, int M, int tiles,
+                         int* argmax, float* gap, bool pdl, cudaStream_t st) {
+  void* args[] = {&am_val, &am_idx, &am_second, &M, &tiles, &argmax, &gap};
+  launch_pdl((const void*)argmax_merge_kernel, dim3((M + 7) / 8), dim3(256), 0, pdl, st, args);
+}
+
+// ---------------------------------------------------------------------------
+// K9: greedy acceptance (one warp, ballot over the <= 32 children of each depth) and the
+// KV commit/compaction of root + accepted path into committed positions P..P+a.
+// ---------------------------------------------------------------------------
+__global__ void accept_kernel(const AcceptParams p) {
+  griddep_wait();
+  griddep_launch();
+  const int lane = threadIdx.x;
+  int n = 1, cur = 0;
+  if (p.chain) {
+    for (int i = lane; i < p.n_nodes; i += 32) p.out_path[i] = i;
+    n = p.n_nodes;
+    cur = p.n_nodes - 1;
+  } else {
+    if (lane == 0) p.out_path[0] = 0;
+    for (int d = 0; d < p.depth_max; ++d) {
+      const int y = p.argmax[cur];
+      const int c = 1 + d * p.k + lane;
+      const bool hit = lane < p.k && c < p.n_nodes && p.parent[c] == cur && p.tok[c] == y;
+      const unsigned b = __ballot_sync(0xffffffffu, hit);
+      if (b == 0) break;
+      cur = 1 + d * p.k + (__ffs(b) - 1);
+      if (lane == 0) {
+        p.out_path[n] = cur;
+        p.out_tokens[n - 1] = p.tok[cur];
+      }
+      ++n;
+    }
+  }
+  if (lane == 0) {
+    const int bonus = p.argmax[cur];
+    const int P = *p.committed_len;
+    if (p.chain) {
+      p.out_tokens[0] = bonus;
+      *p.out_n = 1;
+    } else {
+      p.out_tokens[n - 1] = bonus;
+      *p.out_n = n;
+    }
+    p.commit_meta[0] = P;   // base position
+    p.commit_meta[1] = n;   // rows committed (root + accepted)
+    *p.committed_len = P + n;
+    *p.root_tok = bonus;
+  }
+}
+
+__global__ void __launch_bounds__(256) commit_kernel(const AcceptParams p) {
+  griddep_wait();
+  griddep_launch();
+  const int l = blockIdx.x, h = blockIdx.y, which = blockIdx.z;
+  const int base = p.commit_meta[0], n = p.commit_meta[1];
+  uint16_t* cache = (which ? p.v_cache : p.k_cache) + l * p.cache_layer_stride + int64_t(h) * p.max_ctx * p.head_dim;
+  const uint16_t* tree = (which ? p.v_tree : p.k_tree) + l * p.tree_layer_stride + int64_t(h) * p.max_nodes * p.head_dim;
+  const int dw = p.head_dim / 2;
+  for (int e = threadIdx.x; e < n * dw; e += 256) {
+    const int j = e / dw, i = e % dw;
+    const int slot = p.out_path[j];
+    reinterpret_cast<uint32_t*>(cache + int64_t(base + j) * p.head_dim)[i] =
+        reinterpret_cast<const uint32_t*>(tree + int64_t(slot) * p.head_dim)[i];
+  }
+}
+
+void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st) {
+  AcceptParams pp = p;
+  void* args[] = {&pp};
+  launch_pdl((const void*)accept_kernel, dim3(1), dim3(32), 0, pdl, st, args);
+  launch_pdl((const void*)commit_kernel, dim3(p.n_layers, p.n_kv, 2), dim3(256), 0, pdl, st, args);
+}
+
+__global__ void tree_init_kernel(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc) {
+  griddep_wait();
+  griddep_launch();
+  tok[0] = *root_tok;
+  parent[0] = -1;
+  depth[0] = 0;
+  score[0] = 0.f;
+  anc[0] = 0;
+}
+void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,
+                      cudaStream_t st) {
+  void* args[] = {&root_tok, &tok, &parent, &depth, &score, &anc};
+  launch_pdl((const void*)tree_init_kernel, dim3(1), dim3(1), 0, pdl, st, args);
+}
+
+__global__ void chain_init_kernel(const int* tokens, int n, int* tok, int* parent, int* depth, float* score, int* anc,
+                                  int anc_stride) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    if (threadIdx.x == 0) {
+      tok[i] = tokens[i];
+      parent[i] = i - 1;
+      depth[i] = i;
+      score[i] = 0.f;
+    }
+    for (int j = threadIdx.x; j <= i; j += blockDim.x) anc[int64_t(i) * anc_stride + j] = j;
+  }
+}
+void launch_chain_init(const int* tokens, int n, int* tok, int* parent, int* depth, float* score, int* anc,
+                       int anc_stride, cudaStream_t st) {
+  chain_init_kernel<<<n < 256 ? n : 256, 128, 0, st>>>(tokens, n, tok, parent, depth, score, anc, anc_stride);
+}
+
+}  // namespace ss
