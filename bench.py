@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py — SubSpec tree-speculative decode on B200 (BASELINE.json metric: decode tokens/s and mean
+acceptance length at the VRAM cap; dequant-GEMM HBM GB/s).
+
+A "step" is one SubSpec decode step = D draft passes + one verification pass + acceptance/commit
+(Eq. 2, :86) on one synthetic MT-Bench-shaped request.  Default workload:
+BASELINE.json config 2 — Qwen2.5-7B shape, random-init bf16 target, 8 GiB emulated VRAM cap, all 28
+decoder layers offloaded with 4-bit/g64 substitutes, D = 48, k = 6, T = 0.2.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config qwen2.5-7b]
+
+Under torchrun each rank runs its own independent request on its own GPU (weak scaling, no
+data-path collective; torch.distributed only for the barrier and the max/sum of the timings).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth.configs import PRESETS, GIB  # noqa: E402
+from synth.prompts import mtbench_prompt  # noqa: E402
+
+SEED = 0x5EED
+TAU_FILE = os.path.join(ROOT, "profiles", "bench_tau.json")
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="qwen2.5-7b", choices=sorted(PRESETS))
+    ap.add_argument("--cap-gib", type=float, default=8.0)
+    ap.add_argument("--n-resident", type=int, default=0, help="0 = paper-faithful; -1 = planner max")
+    ap.add_argument("--depth", type=int, default=48)
+    ap.add_argument("--topk", type=int, default=6)
+    ap.add_argument("--temp", type=float, default=0.2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        return os.cpu_count()
+
+
+# ---------------------------------------------------------------------------------------------
+def oracle_step_seconds(cfg, depth, topk, nodes=6):
+    """Bounded sample of the oracle on the SAME shape: one decoder layer (target + 4-bit substitute)
+    plus the head, `nodes` draft and `nodes` target node-forwards, extrapolated to one full step of
+    (1 + k(D-1)) draft + (1 + kD) target node-forwards through all layers.  Returns (seconds/step, info)."""
+    from oracle.model import TargetWeights, draft_layers, KVCache, forward_nodes
+    from oracle.tree import tempered_log_softmax, select_topk
+    cfg1 = cfg.with_(n_layers=1)
+    t0 = time.time()
+    tw = TargetWeights(cfg1, SEED)
+    dl = draft_layers(tw, 0)
+    setup = time.time() - t0
+    kv = KVCache(cfg1, nodes + 1)
+    toks = list(range(1, nodes + 1))
+    slots = list(range(nodes))
+    anc = [[s] for s in slots]
+    pos = [0] * nodes
+    t0 = time.perf_counter()
+    forward_nodes(cfg1, dl, tw, kv, toks, slots, pos, anc)
+    t_draft_node = (time.perf_counter() - t0) / nodes
+    t0 = time.perf_counter()
+    logits = forward_nodes(cfg1, tw.layers, tw, kv, toks, slots, pos, anc)
+    t_target_node = (time.perf_counter() - t0) / nodes
+    h = np.ones(cfg.hidden)
+    t0 = time.perf_counter()
+    for _ in range(nodes):
+        tw.head @ h
+    t_head = (time.perf_counter() - t0) / nodes
+    t0 = time.perf_counter()
+    lp = np.stack([tempered_log_softmax(logits[i], 0.2) for i in range(min(topk, nodes))])
+    select_topk(list(range(len(lp))), [0.0] * len(lp), lp, topk)
+    t_select = time.perf_counter() - t0
+    L = cfg.n_layers
+    n_draft = 1 + topk * (depth - 1)
+    n_verify = 1 + topk * depth
+    step = (n_draft * ((t_draft_node - t_head) * L + t_head) + n_verify * ((t_target_node - t_head) * L + t_head)
+            + depth * t_select)
+    info = {"t_draft_node_1layer_s": t_draft_node, "t_target_node_1layer_s": t_target_node, "t_head_s": t_head,
+            "t_select_s": t_select, "setup_s": setup, "node_forwards": n_draft + n_verify}
+    return step, info
+
+
+def load_tau():
+    try:
+        return json.load(open(TAU_FILE))
+    except Exception:
+        return None
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = PRESETS[a.config]
+    tau_rec = load_tau()
+    tau = tau_rec["tau"] if tau_rec and tau_rec.get("config") == a.config else 1.0
+    times = []
+    info = None
+    for i in range(a.warmup + a.steps):
+        s, info = oracle_step_seconds(cfg, a.depth, a.topk)
+        if i >= a.warmup:
+            times.append(s)
+    step_s = statistics.mean(times)
+    value = tau / step_s
+    cores = blas_threads()
+    sample = (f"1 {cfg.name}-shape decoder layer (bf16 target + 4-bit substitute, fp64 NumPy oracle) + head, 6 draft "
+              f"and 6 target node-forwards per step, extrapolated to a D={a.depth},k={a.topk} step "
+              f"({info['node_forwards']} node-forwards x {cfg.n_layers} layers); tau={tau:.3f} "
+              f"({'from the deterministic GPU run, ' + TAU_FILE if tau_rec else 'assumed 1'})")
+    line = {"metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init weights, MT-Bench-shaped prompt)",
+            "config": workload_config(a, cfg), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "oracle_timing": info}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(a, cfg):
+    return {"workload": f"{cfg.name} SubSpec step, {a.cap_gib:g} GiB cap, n_resident={a.n_resident}, "
+                        f"4-bit g64 substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt",
+            "model_shape": cfg.name, "vram_cap_gib": a.cap_gib, "n_resident": a.n_resident, "depth": a.depth,
+            "top_k": a.topk, "sharpen_t": a.temp, "batch": 1, "max_context": cfg.max_context,
+            "l2": "inputs larger than L2 (>= 4.76 GB of draft weights per draft pass; 13 GB streamed per verify)",
+            "parallelism": f"requests partitioned, {a.gpus} GPU(s), no collective"}
+
+
+def k2_bytes(N, K, M):
+    # codes N*K/2 + meta N*K/64*4 + X M*K*2 + Y M*N*2
+    return N * K // 2 + N * K // 64 * 4 + M * K * 2 + M * N * 2
+
+
+def run_ours(a):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2509_18344_b200.binding import SubSpec
+    cfg = PRESETS[a.config]
+    D, k, T = a.depth, a.topk, a.temp
+    t_setup = time.time()
+    ss = SubSpec(cfg, int(a.cap_gib * GIB), device=local, max_depth=D, max_top_k=max(k, 6), max_chunk=256)
+    ss.load_weights(SEED, n_resident=a.n_resident)
+    ss.build_substitutes(4, 64)
+    prompt = mtbench_prompt(SEED, rank, cfg.vocab)
+    ss.prefill(prompt)
+    t_setup = time.time() - t_setup
+    for _ in range(a.warmup):
+        ss.step(D, k, T)
+    ss.reset_stats()
+    cs = ss.compute_stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0.record(cs)
+    emitted, taus = 0, []
+    for _ in range(a.steps):
+        t = ss.step(D, k, T)
+        emitted += len(t)
+        taus.append(len(t))
+    e1.record(cs)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = ss.stats()
+    # ---- dominant kernel: K2 dequant-GEMV, live sweep over every layer (weights from HBM) ----
+    M = k
+    groups = [ss.group_shape(g) for g in range(4)]
+    per_group = {}
+    for g, name in enumerate(("qkv", "o", "gate_up", "down")):
+        t = ss.debug_time_matmul(-1, g, M, iters=3)
+        per_group[name] = {"N": groups[g][0], "K": groups[g][1], "us": t * 1e3,
+                           "gbs": k2_bytes(*groups[g], M) / (t * 1e-3) / 1e9}
+    t_sweep = ss.debug_time_matmul(-1, -2, M, iters=3)       # avg per launch, 4 groups x L layers
+    bytes_layer = sum(k2_bytes(N, K, M) for N, K in groups)
+    k2_gbs = bytes_layer / (4 * t_sweep * 1e-3) / 1e9
+    t_head = ss.debug_time_matmul(0, -1, M, iters=5)
+    head_gbs = (cfg.vocab * cfg.hidden * 2 + M * cfg.hidden * 2 + M * cfg.vocab * 4) / (t_head * 1e-3) / 1e9
+    # ---- e2e through the C-ABI with host buffers: root token H2D, emitted tokens D2H ----
+    e2e = None
+    if not a.no_e2e:
+        root = int(ss.step(D, k, T)[-1])
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st0 = ss.stats()
+        t0 = time.perf_counter()
+        e2e_tok = 0
+        n_e2e = max(2, a.steps // 2)
+        for _ in range(n_e2e):
+            ss.draft_tree(D, k, T, root_token=root, want_tree=False)
+            ss.verify_tree(want=False)
+            toks, _ = ss.accept_and_commit(D + 1)
+            root = toks[-1]
+            e2e_tok += len(toks)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        st1 = ss.stats()
+        if dist:
+            t_ = torch.tensor([wall], device=f"cuda:{local}")
+            n_ = torch.tensor([float(e2e_tok)], device=f"cuda:{local}")
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            dist.all_reduce(n_)
+            wall, e2e_tok = float(t_), float(n_)
+        streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / n_e2e
+        e2e = {"value": e2e_tok / wall, "unit": "tokens/s", "h2d_bytes_per_step": int(4 + streamed),
+               "d2h_bytes_per_step": int(4 * (e2e_tok / max(1, n_e2e)) + 4),
+               "h2d_breakdown": {"root_token": 4, "streamed_layer_weights": int(streamed)}, "steps": n_e2e}
+    # host link measured in the same run: pinned H2D 1 GiB on the copy stream, best of 5
+    hbuf = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    dbuf = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{local}")
+    best = 1e9
+    with torch.cuda.stream(ss.copy_stream):
+        for _ in range(5):
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x0.record(ss.copy_stream)
+            dbuf.copy_(hbuf, non_blocking=True)
+            x1.record(ss.copy_stream)
+            x1.synchronize()
+            best = min(best, x0.elapsed_time(x1))
+    link_gbs = (1 << 30) / (best * 1e-3) / 1e9
+    del hbuf, dbuf
+    # ---- aggregate over ranks ----
+    tot_tokens, tmax = float(emitted), ms
+    if dist:
+        t_ = torch.tensor([ms], device=f"cuda:{local}")
+        n_ = torch.tensor([float(emitted)], device=f"cuda:{local}")
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        dist.all_reduce(n_)
+        tmax, tot_tokens = float(t_), float(n_)
+    value = tot_tokens / (tmax / 1e3)
+    tau = float(np.mean(taus))
+    steps_per_s = a.steps / (ms / 1e3)
+    peaks = measured_peaks()
+    hbm_peak = (peaks or {}).get("hbm_gbs") or 6650.0
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "k2_traffic.json"))).get("traffic_bytes_per_launch")
+    except Exception:
+        pass
+    stream_gbs = st["stream_bytes"] / (st["stream_busy_ms"] * 1e-3) / 1e9 if st["stream_busy_ms"] else None
+    line = {
+        "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded random-init bf16 weights of the named shape; MT-Bench-shaped prompts)",
+        "config": workload_config(a, cfg),
+        "tau_mean": tau, "tau_hist": np.bincount(taus, minlength=D + 2).tolist(), "steps_per_s": steps_per_s,
+        "tokens_per_s_at_paper_tau_27.08": 27.08 * steps_per_s,
+        "step_breakdown_ms": {"draft": st["draft_ms"] / a.steps, "verify": st["verify_ms"] / a.steps,
+                              "accept": st["accept_ms"] / a.steps},
+        "roofline": {"kernel": "K2 dequant-GEMV (4-bit g64 substitutes, M=k tokens), all layers x 4 groups",
+                     "bound": "hbm", "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
+                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                     "per_group": per_group, "head_bf16_gemv_gbs": head_gbs},
+        "streaming": {"bytes_per_step": st["stream_bytes"] / a.steps, "busy_gbs": stream_gbs,
+                      "host_link_gbs_measured": link_gbs, "frac": (stream_gbs / link_gbs) if stream_gbs else None,
+                      "duty_cycle": (st["stream_busy_ms"] / ms) if ms else None},
+        "memory": {"arena_used": st["arena_used"], "arena_cap": st["arena_cap"], "ring_bytes": st["ring_bytes"],
+                   "substitute_bytes": st["substitute_bytes"], "host_pinned_bytes": st["host_pinned_bytes"],
+                   "n_resident": st["n_resident"]},
+        "gpu_launches": int(st["gpu_launches"]),
+        "clocks": ck, "e2e": e2e, "setup_s": t_setup,
+    }
+    if rank == 0:
+        os.makedirs(os.path.dirname(TAU_FILE), exist_ok=True)
+        if world == 1:
+            try:
+                json.dump({"config": a.config, "tau": tau, "steps": a.steps, "note": "deterministic seeded workload"},
+                          open(TAU_FILE, "w"))
+            except Exception:
+                pass
+        if world == 1 and not a.no_cpu_baseline:
+            s, info = oracle_step_seconds(cfg, D, k)
+            line["cpu_baseline"] = {
+                "value": tau / s, "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
+                "sample": (f"1 {cfg.name}-shape decoder layer + head, 6 draft + 6 target node-forwards (fp64 NumPy "
+                           f"oracle), extrapolated to one D={D},k={k} step ({info['node_forwards']} node-forwards x "
+                           f"{cfg.n_layers} layers) at this run's tau={tau:.3f}"),
+                "seconds_per_step": s}
+        print(json.dumps(line), flush=True)
+    ss.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    a = args_()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,15 @@ ss_status ss_debug_read_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, 
 ss_status ss_debug_time_matmul(ss_ctx* ctx, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
                                float* out_ms);
 
+/* Time the draft forward of M frontier nodes (one draft pass incl. head, no top-k): average device ms
+ * over `iters` eager launches.  skip: bit mask of kernel classes left out (1 attention, 2 RMSNorm,
+ * 4 dequant-GEMVs, 8 head) — attribution only; results are not meaningful when skip != 0. */
+ss_status ss_debug_time_pass(ss_ctx* ctx, int32_t M, int32_t iters, int32_t skip, float* out_ms);
+/* One traced draft pass: each dequant-GEMV launch records 8 %globaltimer events (ns) into
+ * out[8*i .. 8*i+7] (entry, producer/consumer dependency release, first data, loop end, flush,
+ * kernel end, loop end max); *out_n = number of launches traced (<= cap). */
+ss_status ss_debug_trace_pass(ss_ctx* ctx, int32_t M, int64_t* out, int32_t cap, int32_t* out_n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,11 +15,12 @@ Per (row n, group g), with x the bf16 values (exact in fp32):
       = RNE_bf16( fp32( fp32(M - m) / 15 ) )  otherwise
     z = m
     code = clamp( rint_half_even( fp32( fp32(x - z) / s ) ), 0, 2^bits - 1 )
-    W_hat = RNE_bf16( exact(code * s + z) )   (one rounding)
+    W_hat = code * s + z                      (exact; reading R3: the affine dequantisation is
+                                               applied exactly, as fused low-bit GEMM kernels do
+                                               when they scale per group in fp32)
 """
 import numpy as np
 
-from .numerics import round_bf16
 
 
 def _f32_to_bf16_f32(x32):
@@ -54,14 +55,11 @@ def quantize(w, bits=4, group=64):
 
 
 def dequantize(codes, s, z, group=64):
-    """W_hat[n,k] = RNE_bf16(code*s + z), computed exactly in float64 then rounded once."""
+    """W_hat[n,k] = code*s + z, exact in float64 (a <=8-bit x 8-bit significand product plus an
+    8-bit-significand addend of nearby magnitude)."""
     N, K = codes.shape
     c = codes.astype(np.float64).reshape(N, K // group, group)
-    exact = c * s[..., None] + z[..., None]      # exact: 4-bit x 8-bit significands + 8-bit addend
-    out = np.zeros_like(exact)
-    nz = exact != 0
-    out[nz] = round_bf16(exact[nz])
-    return out.reshape(N, K)
+    return (c * s[..., None] + z[..., None]).reshape(N, K)
 
 
 def substitute_matrix(w, bits=4, group=64):

@@ -68,6 +68,8 @@ _FUNCS = {
     "ss_debug_set_tree": [c_void_p, c_void_p, c_void_p, c_int32, c_int32],
     "ss_debug_read_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
     "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
+    "ss_debug_time_pass": [c_void_p, c_int32, c_int32, c_int32, P(c_float)],
+    "ss_debug_trace_pass": [c_void_p, c_int32, c_void_p, c_int32, P(c_int32)],
 }
 EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy"]
 
@@ -265,6 +267,17 @@ class SubSpec:
         v = np.zeros_like(k)
         self._check(self.lib.ss_debug_read_kv(self.ctx, layer, pos0, n, _ptr(k), _ptr(v)))
         return k.reshape(c.n_kv_heads, n, c.head_dim), v.reshape(c.n_kv_heads, n, c.head_dim)
+
+    def debug_time_pass(self, M, iters=5, skip=0):
+        ms = c_float()
+        self._check(self.lib.ss_debug_time_pass(self.ctx, M, iters, skip, ctypes.byref(ms)))
+        return ms.value
+
+    def debug_trace_pass(self, M, cap=256):
+        out = np.zeros(cap * 8, np.int64)
+        n = c_int32()
+        self._check(self.lib.ss_debug_trace_pass(self.ctx, M, _ptr(out), cap, ctypes.byref(n)))
+        return out[: n.value * 8].reshape(n.value, 8)
 
     def debug_time_matmul(self, layer, group, M, iters=20):
         ms = c_float()

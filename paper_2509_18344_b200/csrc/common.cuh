@@ -21,51 +21,68 @@ constexpr int kXChunkBytesPerNT = 8 * kChunkK * 2;          // 2048: 8 tokens x 
 // Weight "tiled fragment" layout.
 // Matrix W [N x K] (N % 128 == 0, K % 128 == 0) is stored as tile-chunks
 // (r = n/128, c = k/128), index tc = r * (K/128) + c, each contiguous.
-// Inside a tile-chunk warp w (0..7) owns rows 16w..16w+15; lane = g*4 + t4
-// owns rows 16w+g (h=0) and 16w+g+8 (h=1) and k = 32*t4 .. 32*t4+31.
+// Inside a tile-chunk warp w (0..7) owns rows 16w..16w+15; lane = g*4 + t4 owns rows
+// 16w+g (h=0) and 16w+g+8 (h=1).  Within the chunk, k = 64*G + 16*t4 + i16 (G = 64-group,
+// i16 = 0..15), so every mma.m16n8k16 k-step st = 4*G + i16/4 stays inside one quant group.
 // ---------------------------------------------------------------------------
+struct KPos {
+  int G, t4, i16, st, j;
+};
+SS_HD KPos kpos(int64_t k) {
+  const int kk = int(k & 127);
+  KPos p;
+  p.G = kk >> 6;
+  p.t4 = (kk & 63) >> 4;
+  p.i16 = kk & 15;
+  p.st = 4 * p.G + (p.i16 >> 2);
+  p.j = p.i16 & 3;
+  return p;
+}
 SS_HD uint64_t bf16_tiled_offset(int64_t n, int64_t k, int64_t K) {   // in bytes
-  int64_t tc = (n >> 7) * (K >> 7) + (k >> 7);
-  int nn = int(n & 127), kk = int(k & 127);
-  int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
-  int t4 = kk >> 5, i = kk & 31, q = i >> 3, e = i & 7;
-  int lane = g * 4 + t4;
+  const int64_t tc = (n >> 7) * (K >> 7) + (k >> 7);
+  const int nn = int(n & 127);
+  const int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
+  const KPos p = kpos(k);
+  const int q = 2 * p.G + (p.i16 >> 3), e = p.i16 & 7;
+  const int lane = g * 4 + p.t4;
   return uint64_t(tc) * kBF16TileBytes + uint64_t((((w * 2 + h) * 4 + q) * 32 + lane) * 16 + e * 2);
 }
 
-// Q4: codes at (((w*2+h)*32 + lane)*16 + byte); a lane's 32 codes i = 0..31 sit in
-// 4 words (word = i/8); code c = i%8 of a word lives in nibble slot (c%2)*4 + c/2,
-// so (word >> 4p) & 0x000F000F yields the bf16x2 pair (c_2p, c_2p+1).
+// Q4: per (warp w, group G, lane) 16 bytes = [row g: word0, word1][row g+8: word0, word1];
+// word holds i16 = 8*word .. +7; code c8 = i16 % 8 lives in nibble slot (c8%2)*4 + c8/2, so
+// (word >> 4p) & 0x000F000F yields the bf16x2 pair (c_2p, c_2p+1).
+// Meta (4 B: s bf16 lo, z bf16 hi) at 8192 + ((w*2 + G)*16 + row_in_warp) * 4.
 SS_HD uint64_t q4_tile_base(int64_t n, int64_t k, int64_t K) {
   return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ4TileBytes;
 }
 SS_HD void q4_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
-  int nn = int(n & 127), kk = int(k & 127);
-  int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
-  int t4 = kk >> 5, i = kk & 31, word = i >> 3, c = i & 7;
-  int lane = g * 4 + t4;
-  int slot = (c & 1) * 4 + (c >> 1);
-  uint64_t wordoff = q4_tile_base(n, k, K) + uint64_t(((w * 2 + h) * 32 + lane) * 16 + word * 4);
+  const int nn = int(n & 127);
+  const int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
+  const KPos p = kpos(k);
+  const int lane = g * 4 + p.t4;
+  const int word = p.i16 >> 3, c8 = p.i16 & 7;
+  const int slot = (c8 & 1) * 4 + (c8 >> 1);
+  const uint64_t wordoff = q4_tile_base(n, k, K) + uint64_t(((w * 2 + p.G) * 32 + lane) * 16 + h * 8 + word * 4);
   *byte_off = wordoff + (slot >> 1);
   *shift = (slot & 1) * 4;
 }
 SS_HD uint64_t q4_meta_offset(int64_t n, int64_t k, int64_t K) {     // bytes; 4 B (s lo16, z hi16)
-  int nn = int(n & 127), kk = int(k & 127);
-  int w = nn >> 4, rr = nn & 15, grp = kk >> 6;
-  return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((w * 2 + grp) * 16 + rr) * 4);
+  const int nn = int(n & 127);
+  const int w = nn >> 4, rr = nn & 15;
+  return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((w * 2 + kpos(k).G) * 16 + rr) * 4);
 }
 
 // ---------------------------------------------------------------------------
 // FragX activation layout: X [Mpad x K] bf16, Mpad % 8 == 0, NT = Mpad/8.
-// Chunk c (128 k) of all NT n-tiles is contiguous (NT * 2 KB).
-// offset(m,k) = ((((c*NT + nt)*8 + s)*4 + t4)*8 + g)*4 + j   (elements)
-// with kk = k%128, t4 = kk/32, s = (kk%32)/4, j = kk%4, nt = m/8, g = m%8.
+// Chunk c (128 k) of all NT n-tiles is contiguous (NT * 2 KB); within it
+// offset(m,k) = ((((c*NT + nt)*8 + st)*4 + t4)*8 + g)*4 + j  with (st, t4, j) = kpos(k),
+// nt = m/8, g = m%8: the 8 bytes lane (g, t4) needs for k-step st are contiguous.
 // ---------------------------------------------------------------------------
 SS_HD int64_t fragx_offset(int64_t m, int64_t k, int NT) {
-  int64_t c = k >> 7;
-  int kk = int(k & 127), t4 = kk >> 5, s = (kk & 31) >> 2, j = kk & 3;
-  int nt = int(m >> 3), g = int(m & 7);
-  return ((((c * NT + nt) * 8 + s) * 4 + t4) * 8 + g) * 4 + j;
+  const int64_t c = k >> 7;
+  const KPos p = kpos(k);
+  const int nt = int(m >> 3), g = int(m & 7);
+  return ((((c * NT + nt) * 8 + p.st) * 4 + p.t4) * 8 + g) * 4 + p.j;
 }
 
 // ---------------------------------------------------------------------------
@@ -92,10 +109,16 @@ SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
+}
+// (x & 0x000F000F) | magic in ONE lop3 (C++ "(x & a) | b" becomes two LOP3s with immediates)
+SS_DEV uint32_t lop3_and_or(uint32_t x, uint32_t magic) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 0x000F000F, %2, 0xEA;" : "=r"(d) : "r"(x), "r"(magic));
+  return d;
 }
 // 1-D bulk async copy global -> shared, completion counted on an mbarrier (TMA engine; SASS UBLKCP)
 SS_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
@@ -125,17 +148,6 @@ SS_DEV void mma_bf16_16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// (word >> 4p) & 0x000F000F | 0x43004300 gives bf16x2 (128 + c_lo, 128 + c_hi); subtracting 128
-// is exact; one fma.rn.bf16x2 then gives RNE_bf16(code*s + z) (single rounding).
-SS_DEV uint32_t dq_pair(uint32_t word, int p, uint32_t s2, uint32_t z2) {
-  uint32_t v = ((word >> (4 * p)) & 0x000F000Fu) | 0x43004300u;
-  __nv_bfloat162 bv = *reinterpret_cast<__nv_bfloat162*>(&v);
-  const uint32_t k128 = 0x43004300u;
-  __nv_bfloat162 c = __hsub2(bv, *reinterpret_cast<const __nv_bfloat162*>(&k128));
-  __nv_bfloat162 r = __hfma2(c, *reinterpret_cast<__nv_bfloat162*>(&s2), *reinterpret_cast<__nv_bfloat162*>(&z2));
-  return *reinterpret_cast<uint32_t*>(&r);
 }
 
 SS_DEV float bf2f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }

@@ -93,7 +93,9 @@ struct ss_ctx {
   // activations
   float* x = nullptr;
   uint16_t *hfrag = nullptr, *attnfrag = nullptr, *actfrag = nullptr, *qbuf = nullptr;
+  float *hxs = nullptr, *attnxs = nullptr, *actxs = nullptr;   // group sums of the FragX inputs
   float* logits = nullptr;
+  unsigned long long* tracebuf = nullptr;   // debug: %globaltimer events [512][8]
   int mpad_max = 0;
   float2* rope = nullptr;
   // gemv scratch
@@ -103,8 +105,9 @@ struct ss_ctx {
   size_t gv_part_floats = 0;
   // attention scratch
   float *at_o = nullptr, *at_ml = nullptr;
+  int* at_cnt = nullptr;
   int at_seg_max = 0;
-  int split_draft = 64, split_target = 128;
+  int split_draft = 32, split_target = 128;
   // topk scratch
   float *tk_max = nullptr, *tk_sum = nullptr, *tk_val = nullptr;
   int* tk_idx = nullptr;
@@ -263,14 +266,21 @@ struct PassOut {
   bool logits = false;        // draft: logits to c->logits [M x V]
   bool argmax = false;        // target: per-node argmax + gap
 };
+// debug timing only (ss_debug_time_pass): skip kernel classes to attribute pass time
+int g_skip = 0;
+unsigned long long* g_trace = nullptr;   // device buffer [launch][8] for ss_debug_trace_pass
+int g_trace_n = 0, g_trace_cap = 0;
+enum { SKIP_ATTN = 1, SKIP_NORM = 2, SKIP_GEMV = 4, SKIP_HEAD = 8 };
 
 ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M, const EpiParams& epi) {
+  if (!target && (g_skip & SKIP_GEMV)) return SS_OK;
   const int N = c->gN[g], K = c->gK[g];
   const LayerW& w = c->lw[l];
   if (!target) {
     GemvParams p{};
     p.W = w.resident ? w.bf16[g] : w.q4[g];
     p.X = X;
+    p.XS = X == c->hfrag ? c->hxs : (X == c->attnfrag ? c->attnxs : c->actxs);
     p.N = N;
     p.K = K;
     p.NT = gemv_nt(M);
@@ -278,6 +288,7 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.counters = c->gv_cnt;
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = epi;
+    if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + 8 * (g_trace_n++);
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
     c->launches++;
     return check_launch(c, "gemv");
@@ -328,7 +339,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
   const int NT = target ? gemm_nt(M) : gemv_nt(M);
   const float eps = c->cfg.rms_eps;
   ss_status s;
-  launch_embed_rmsnorm(c->tok, node_base, M, c->embed, c->x, c->H, c->lw[0].attn_norm, eps, c->hfrag, NT,
+  launch_embed_rmsnorm(c->tok, node_base, M, c->embed, c->x, c->H, c->lw[0].attn_norm, eps, c->hfrag, c->hxs, NT,
                        c->use_pdl, c->cs);
   c->launches++;
   if ((s = check_launch(c, "embed_rmsnorm")) != SS_OK) return s;
@@ -362,34 +373,37 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     a.n_seg_max = c->at_seg_max;
     a.part_o = c->at_o;
     a.part_ml = c->at_ml;
+    a.counters = c->at_cnt;
     a.out_fragx = c->attnfrag;
+    a.out_xs = c->attnxs;
     a.out_nt = NT;
     // logical keys of a node: P + depth + 1 <= max_context.  The draft loop is replayed from a CUDA
     // graph while P grows, so its grid is sized for max_context.
-    launch_attention(a, target ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
+    if (!(g_skip & SKIP_ATTN)) launch_attention(a, target ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
     c->launches += 2;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
     e = base_epi(c, M);
     e.kind = EPI_RESID;
     if ((s = matmul(c, target, l, 1, c->attnfrag, M, e)) != SS_OK) return s;
-    launch_rmsnorm(c->x, M, c->H, c->lw[l].mlp_norm, eps, c->hfrag, NT, c->use_pdl, c->cs);
+    if (!(g_skip & SKIP_NORM)) launch_rmsnorm(c->x, M, c->H, c->lw[l].mlp_norm, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
     c->launches++;
     if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
     e = base_epi(c, M);
     e.kind = EPI_SILU;
     e.act = c->actfrag;
+    e.act_xs = c->actxs;
     e.act_nt = NT;
     if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
     e = base_epi(c, M);
     e.kind = EPI_RESID;
     if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
     const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
-    if (!target || out.argmax) {
-      launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, NT, c->use_pdl, c->cs);
+    if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
+      launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
       c->launches++;
       if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
     } else if (l + 1 < c->L) {
-      launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, NT, c->use_pdl, c->cs);
+      launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
       c->launches++;
       if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
     }
@@ -414,7 +428,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
   }
   if (out.logits) {
     // head over the final normed rows (GEMV, <= 32 rows at a time)
-    for (int r0 = 0; r0 < M && !target; r0 += 32) {
+    for (int r0 = 0; r0 < M && !target && !(g_skip & SKIP_HEAD); r0 += 32) {
       const int m = std::min(32, M - r0);
       GemvParams p{};
       p.W = c->head;
@@ -665,7 +679,11 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->attnfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * c->qd * 2));
   c->actfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * c->F * 2));
   c->qbuf = (uint16_t*)chk(A(size_t(c->max_nodes) * c->qd * 2));
+  c->hxs = (float*)chk(A(size_t(c->mpad_max) * (fx_cols / 64) * 4));
+  c->attnxs = (float*)chk(A(size_t(c->mpad_max) * (c->qd / 64) * 4));
+  c->actxs = (float*)chk(A(size_t(c->mpad_max) * (c->F / 64) * 4));
   c->logits = (float*)chk(A(size_t(32) * c->V * 4));
+  c->tracebuf = (unsigned long long*)chk(A(size_t(512) * 8 * 8));
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32
   size_t gvf = 0;
@@ -681,6 +699,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->at_seg_max = (c->C + std::min(c->split_draft, c->split_target) - 1) / std::min(c->split_draft, c->split_target);
   c->at_o = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d * 4));
   c->at_ml = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * 2 * 4));
+  c->at_cnt = (int*)chk(A(size_t(c->nkv) * ((c->max_nodes + 7) / 8) * 4));
   c->tk_max = (float*)chk(A(size_t(32) * 296 * 4));
   c->tk_sum = (float*)chk(A(size_t(32) * 296 * 4));
   c->tk_val = (float*)chk(A(size_t(32) * 296 * 32 * 4));
@@ -1068,6 +1087,12 @@ void ss_destroy(ss_ctx* c) {
 }
 
 // ---------------------------------- debug ---------------------------------------------------
+static ss_status drain_stream(ss_ctx* c) {
+  CK(cudaStreamSynchronize(c->cs));
+  CK(cudaStreamSynchronize(c->xs));
+  return SS_OK;
+}
+
 ss_status ss_debug_gen_tensor(ss_ctx* c, uint64_t seed, int32_t tid, int64_t rows, int64_t cols, int32_t kind,
                               double sigma, uint16_t* out) {
   GUARD(c);
@@ -1086,12 +1111,6 @@ ss_status ss_debug_gen_tensor(ss_ctx* c, uint64_t seed, int32_t tid, int64_t row
   CK(cudaMemcpyAsync(out, buf, bytes, cudaMemcpyDeviceToHost, c->cs));
   CK(cudaStreamSynchronize(c->cs));
   return check_launch(c, "gen_tensor");
-}
-
-static ss_status drain_stream(ss_ctx* c) {
-  CK(cudaStreamSynchronize(c->cs));
-  CK(cudaStreamSynchronize(c->xs));
-  return SS_OK;
 }
 
 ss_status ss_debug_read_group(ss_ctx* c, int32_t layer, int32_t group, uint16_t* out) {
@@ -1158,7 +1177,17 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
   for (int m = 0; m < M; ++m)
     for (int k = 0; k < K; ++k) fx[fragx_offset(m, k, NT)] = x[int64_t(m) * K + k];
   uint16_t* X = K == c->F ? c->actfrag : c->hfrag;
+  float* XS = K == c->F ? c->actxs : c->hxs;
+  std::vector<float> xs(size_t(K / 64) * NT * 8, 0.f);
+  for (int m = 0; m < M; ++m)
+    for (int k = 0; k < K; ++k) {
+      uint32_t b = uint32_t(x[int64_t(m) * K + k]) << 16;
+      float f;
+      std::memcpy(&f, &b, 4);
+      xs[size_t(k / 64) * NT * 8 + m] += f;
+    }
   CK(cudaMemcpyAsync(X, fx.data(), fx.size() * 2, cudaMemcpyHostToDevice, c->cs));
+  if (which == 0) CK(cudaMemcpyAsync(XS, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice, c->cs));
   float* Y = c->at_o;   // debug output scratch: the attention partial buffer
   if (size_t(M) * N > size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d)
     return fail(c, SS_ERR_BUDGET, "debug_matmul: output too large");
@@ -1171,6 +1200,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
     GemvParams p{};
     p.W = w.resident ? w.bf16[group] : w.q4[group];
     p.X = X;
+    p.XS = XS;
     p.N = N;
     p.K = K;
     p.NT = NT;
@@ -1201,36 +1231,120 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
 ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
                                float* out_ms) {
   GUARD(c);
-  if (c->state < ST_READY || which != 0 || layer < 0 || layer >= c->L || group < -1 || group > 3 || M < 1 || M > 32 ||
+  // layer >= 0: that layer only; layer == -1: every layer in turn (weights stream from HBM, not L2).
+  // group 0..3: that matrix group; -1: the bf16 head; -2: the four groups of each layer in pass order.
+  if (c->state < ST_READY || which != 0 || layer < -1 || layer >= c->L || group < -2 || group > 3 || M < 1 || M > 32 ||
       iters < 1 || !out_ms)
     return fail(c, SS_ERR_INVALID, "time_matmul args");
-  const bool head = group == -1;
-  const int N = head ? c->V : c->gN[group], K = head ? c->H : c->gK[group];
-  const LayerW& w = c->lw[layer];
-  GemvParams p{};
-  p.W = head ? c->head : (w.resident ? w.bf16[group] : w.q4[group]);
-  p.X = K == c->F ? c->actfrag : c->hfrag;
-  p.N = N;
-  p.K = K;
-  p.NT = gemv_nt(M);
-  p.partials = c->gv_part;
-  p.counters = c->gv_cnt;
-  p.max_seg = gemv_max_segments(N, K, c->gv_grid);
-  p.epi = base_epi(c, M);
-  p.epi.kind = EPI_STORE;
-  p.epi.out = c->logits;
-  p.epi.ldo = N;
-  p.epi.M = 0;   // time the GEMV with a no-op store
-  const bool q4 = !head && !w.resident;
-  launch_gemv(q4, p, c->gv_grid, c->use_pdl, c->cs);
+  std::vector<std::pair<int, int>> seq;
+  for (int l = (layer < 0 ? 0 : layer); l < (layer < 0 ? c->L : layer + 1); ++l) {
+    if (group == -2)
+      for (int g = 0; g < 4; ++g) seq.emplace_back(l, g);
+    else
+      seq.emplace_back(l, group);
+  }
+  if (group == -1) seq.assign(1, {0, -1});
+  auto launch = [&](int l, int g) {
+    const bool head = g == -1;
+    const int N = head ? c->V : c->gN[g], K = head ? c->H : c->gK[g];
+    const LayerW& w = c->lw[l];
+    GemvParams p{};
+    p.W = head ? c->head : (w.resident ? w.bf16[g] : w.q4[g]);
+    p.X = K == c->F ? c->actfrag : c->hfrag;
+    p.XS = K == c->F ? c->actxs : c->hxs;
+    p.N = N;
+    p.K = K;
+    p.NT = gemv_nt(M);
+    p.partials = c->gv_part;
+    p.counters = c->gv_cnt;
+    p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+    p.epi = base_epi(c, M);
+    p.epi.kind = EPI_STORE;
+    p.epi.out = c->at_o;
+    p.epi.ldo = N;
+    launch_gemv(!head && !w.resident, p, c->gv_grid, c->use_pdl, c->cs);
+  };
+  ss_status s = drain_stream(c);
+  if (s != SS_OK) return s;
+  for (auto& lg : seq) launch(lg.first, lg.second);   // warm-up (attributes, instruction cache)
   CK(cudaEventRecord(c->e0, c->cs));
-  for (int i = 0; i < iters; ++i) launch_gemv(q4, p, c->gv_grid, c->use_pdl, c->cs);
+  for (int i = 0; i < iters; ++i)
+    for (auto& lg : seq) launch(lg.first, lg.second);
   CK(cudaEventRecord(c->e1, c->cs));
   CK(cudaEventSynchronize(c->e1));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
-  *out_ms = ms / iters;
+  *out_ms = ms / float(iters * seq.size());
   return check_launch(c, "time_matmul");
+}
+
+ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, float* out_ms) {
+  GUARD(c);
+  if (c->state != ST_SESSION || M < 1 || M > std::min(32, c->max_nodes - 1) || iters < 1 || !out_ms)
+    return fail(c, SS_ERR_INVALID, "time_pass args");
+  // draft forward of M frontier nodes (slots 1..M, children of the root), repeated; tree metadata
+  // is set up host-side first.  Writes tree KV scratch only.
+  std::vector<int> tk(M + 1), par(M + 1), dep(M + 1), anc(size_t(M + 1) * c->anc_stride, 0);
+  std::vector<float> sc(M + 1, 0.f);
+  for (int i = 0; i <= M; ++i) {
+    tk[i] = (i * 7919) % c->V;
+    par[i] = i ? 0 : -1;
+    dep[i] = i ? 1 : 0;
+    anc[size_t(i) * c->anc_stride] = 0;
+    if (i) anc[size_t(i) * c->anc_stride + 1] = i;
+  }
+  CK(cudaMemcpyAsync(c->tok, tk.data(), tk.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->parent, par.data(), par.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->depth, dep.data(), dep.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->score, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaMemcpyAsync(c->anc, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  g_skip = skip;
+  PassOut o;
+  o.logits = true;
+  ss_status s = forward_pass(c, false, M, 1, o);   // warm-up
+  if (s == SS_OK) {
+    CK(cudaEventRecord(c->e0, c->cs));
+    for (int i = 0; i < iters && s == SS_OK; ++i) s = forward_pass(c, false, M, 1, o);
+    CK(cudaEventRecord(c->e1, c->cs));
+  }
+  g_skip = 0;
+  if (s != SS_OK) return s;
+  CK(cudaEventSynchronize(c->e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  *out_ms = ms / iters;
+  return check_launch(c, "time_pass");
+}
+
+ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, int32_t* out_n) {
+  GUARD(c);
+  if (c->state != ST_SESSION || !out || cap < 1 || !out_n) return fail(c, SS_ERR_INVALID, "trace_pass args");
+  // run one draft pass with %globaltimer events recorded in every dequant-GEMV launch
+  float ms = 0.f;
+  ss_status s = ss_debug_time_pass(c, M, 1, 0, &ms);   // sets up the frontier + warm-up
+  if (s != SS_OK) return s;
+  std::vector<unsigned long long> init(size_t(cap) * 8);
+  for (int i = 0; i < cap; ++i)
+    for (int j = 0; j < 8; ++j) init[size_t(i) * 8 + j] = (j == 0) ? ~0ull : 0ull;
+  if (cap > 512) cap = 512;
+  unsigned long long* buf = c->tracebuf;
+  CK(cudaMemcpyAsync(buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  g_trace = buf;
+  g_trace_n = 0;
+  g_trace_cap = cap;
+  PassOut o;
+  o.logits = true;
+  s = forward_pass(c, false, M, 1, o);
+  const int n = g_trace_n;
+  g_trace = nullptr;
+  if (s != SS_OK) return s;
+  CK(cudaMemcpyAsync(init.data(), buf, size_t(n) * 8 * 8, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  std::memcpy(out, init.data(), size_t(n) * 8 * 8);
+  *out_n = n;
+  return SS_OK;
 }
 
 ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
@@ -1280,7 +1394,7 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
     if ((s = forward_pass(c, true, n, 0, o)) != SS_OK) return s;
     for (int r0 = 0; r0 < n; r0 += 32) {
       const int m = std::min(32, n - r0);
-      launch_rmsnorm(c->x + int64_t(r0) * c->H, m, c->H, c->final_norm, c->cfg.rms_eps, c->hfrag, gemv_nt(m), false, c->cs);
+      launch_rmsnorm(c->x + int64_t(r0) * c->H, m, c->H, c->final_norm, c->cfg.rms_eps, c->hfrag, c->hxs, gemv_nt(m), false, c->cs);
       GemvParams p{};
       p.W = c->head;
       p.X = c->hfrag;

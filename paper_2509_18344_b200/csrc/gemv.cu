@@ -1,19 +1,24 @@
 // K2 — fused dequant-GEMV/GEMM for the draft (M = frontier tokens <= 32).
-// Y[M x N] = X[M x K] * W_hat^T with W_hat = RNE_bf16(code*s + z)
-// ("low-bit GEMM kernels"; 4 bit / group 64).
+// Y[M x N] = X[M x K] * W_hat^T with W_hat = code*s + z per 64-group
+// ("highly optimized low-bit GEMM kernels"; 4 bit / group 64, PAPER.md:278;
+// reading R3 in DESIGN.md: the affine dequantisation is applied exactly, in fp32).
 //
 // B200 design:
-//  * persistent grid (one CTA per SM); the (row-tile, k-chunk) space of 128x128 tile-chunks is
-//    split into equal contiguous ranges per CTA (Stream-K); because the weight layout is
-//    tile-chunk contiguous, a CTA streams ONE contiguous byte range;
-//  * a producer warp streams tile-chunks with cp.async.bulk (TMA engine) into an S-stage
-//    shared-memory ring guarded by mbarriers; the weight part of the first stages is issued
-//    BEFORE griddepcontrol.wait, overlapping the previous kernel (PDL);
-//  * 8 consumer warps dequantise 4-bit codes in registers (lop3 + sub + fma.bf16x2) straight
-//    into mma.m16n8k16 A fragments (weights as the 16-row A operand, tokens as N = 8..32);
-//  * row tiles split across CTAs are reduced deterministically by the last-arriving CTA in
-//    fixed slot order, which then runs the fused epilogue (bias+RoPE+KV write / residual /
-//    SiLU*mul / logits).
+//  * weights are tile-chunk contiguous (128 rows x 128 k, 9 KB for Q4): a CTA streams its work
+//    with cp.async.bulk (TMA engine) into an S-stage shared-memory ring guarded by mbarriers; the
+//    weight part of the first stages is issued BEFORE griddepcontrol.wait (PDL), overlapping the
+//    previous kernel's tail;
+//  * 8 consumer warps turn 4-bit codes into exact bf16 (128 + code) with ONE lop3 per pair and
+//    feed them straight into mma.m16n8k16 as the 16-row A operand (tokens are N = 8..32); every
+//    k-step stays inside one 64-group, a second MMA with an all-ones A gives the group sums of x,
+//    and y += s*sum((128+c)x) + (z - 128 s)*sum(x) applies the group scale/zero in fp32;
+//  * narrow matrices (qkv, o, down) use cluster split-K: the S CTAs of a cluster split a row
+//    tile's K and rank 0 reduces their partial tiles through distributed shared memory, in rank
+//    order, then runs the fused epilogue (bias+RoPE+KV write / residual / SiLU*mul / logits);
+//    persistent clusters loop over row tiles so that at most one CTA per SM is used and the next
+//    kernel can co-reside and prefetch;
+//  * the tall bf16 head uses Stream-K (equal contiguous ranges of the tile-chunk space per
+//    persistent CTA) with a fixed-order fixup by the last-arriving CTA.
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -25,86 +30,225 @@ constexpr int kGemvThreads = (kGemvConsumerWarps + 1) * 32;
 
 template <bool Q4, int NT>
 struct GemvCfg {
+  static constexpr int kCPS = Q4 ? 2 : 1;                       // tile-chunks per pipeline stage
   static constexpr int kWBytes = Q4 ? kQ4TileBytes : kBF16TileBytes;
   static constexpr int kXBytes = NT * kXChunkBytesPerNT;
-  static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kRingBudget = 88 * 1024;   // 2 CTAs/SM: this kernel + the next (PDL)
-  static constexpr int kStages = (kRingBudget / kStageBytes) < 2 ? 2 : (kRingBudget / kStageBytes > 8 ? 8 : kRingBudget / kStageBytes);
+  static constexpr int kSBytes = Q4 ? 2 * NT * 8 * 4 : 0;       // group sums of x: [2 groups][Mpad] fp32
+  static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
+  static constexpr int kMaxStages = 16;
   static constexpr int kTileFloats = kTileRows * NT * 8;
-  static constexpr int kSmem = kStages * kStageBytes + kTileFloats * 4 + 2 * kStages * 8 + 64;
+  // runtime stage count S: ring S*stage + out tile + 2*kMaxStages barriers
+  static constexpr int smem_for(int S) { return S * kStageBytes + kTileFloats * 4 + 2 * kMaxStages * 8 + 64; }
 };
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
 
 SS_HD int64_t owner_of(int64_t t, int64_t T, int G) { return ((t + 1) * G - 1) / T; }
 
 static int gemv_grid_for(int N, int K, int grid) {
   const int64_t T = int64_t(N / 128) * (K / 128);
-  return int(T < grid ? T : grid);   // every CTA gets >= 1 tile-chunk, so segment counts are exact
+  return int(T < grid ? T : grid);   // every Stream-K CTA gets >= 1 tile-chunk
 }
 
 int gemv_max_segments(int N, int K, int grid) {
-  int64_t nC = K / 128, T = int64_t(N / 128) * nC;
+  const int64_t nC = K / 128, T = int64_t(N / 128) * nC;
   grid = gemv_grid_for(N, K, grid);
   int mx = 1;
   for (int64_t r = 0; r < N / 128; ++r) {
-    int s = int(owner_of((r + 1) * nC - 1, T, grid) - owner_of(r * nC, T, grid) + 1);
+    const int s = int(owner_of((r + 1) * nC - 1, T, grid) - owner_of(r * nC, T, grid) + 1);
     if (s > mx) mx = s;
   }
   return mx;
 }
 
-SS_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+SS_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace events: 0 first CTA entry (min), 1 producer dep-wait done (CTA 0), 2 consumer dep-wait done
+// (CTA 0), 3 first stage arrived (CTA 0), 4 main loop done (CTA 0), 5 last flush start (CTA 0),
+// 6 kernel end (max over CTAs), 7 main loop done (max over CTAs)
+#define SS_TRACE_MIN(ev) do { if (p.trace) atomicMin(&p.trace[ev], gtime()); } while (0)
+#define SS_TRACE_MAX(ev) do { if (p.trace) atomicMax(&p.trace[ev], gtime()); } while (0)
+#define SS_TRACE_CTA0(ev) do { if (p.trace && blockIdx.x == 0) p.trace[ev] = gtime(); } while (0)
 
-template <bool Q4, int NT>
+SS_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+SS_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SS_DEV uint32_t cluster_nrank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+SS_DEV uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+SS_DEV uint32_t cluster_count_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+SS_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+SS_DEV float4 ld_dsmem_f32x4(const float* local, uint32_t rank) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+  return v;
+}
+
+// The tile-chunks a CTA processes, in streaming order (identical for producer and consumers).
+struct Work {
+  int r, c;          // current tile and chunk
+  int c_begin, c_end;
+  int r_step;
+  int64_t left;      // items remaining
+  SS_DEV int take(int cps) const {   // chunks of the current tile in the next stage
+    const int rem = c_end - c;
+    return rem < cps ? rem : cps;
+  }
+  SS_DEV void next(int nC, int n) {
+    c += n;
+    if (c == c_end) {
+      r += r_step;
+      c = c_begin;
+      if (r_step == 1 && c_end == nC) c = 0;   // Stream-K: later tiles start at chunk 0
+    }
+    left -= n;
+  }
+  SS_DEV int64_t stages(int nC, int cps) const {   // number of stages left (tile-aligned stages)
+    Work w = *this;
+    int64_t n = 0;
+    while (w.left > 0) {
+      w.next(nC, w.take(cps));
+      ++n;
+    }
+    return n;
+  }
+};
+
+template <bool kCluster>
+SS_DEV Work make_work(int N, int K, uint32_t crank, uint32_t csize) {
+  const int nC = K >> 7, n_tiles = N >> 7;
+  Work w;
+  if constexpr (kCluster) {
+    const int cid = int(cluster_id_x()), ncl = int(cluster_count_x());
+    w.c_begin = int(int64_t(crank) * nC / csize);
+    w.c_end = int(int64_t(crank + 1) * nC / csize);
+    w.r = cid;
+    w.c = w.c_begin;
+    w.r_step = ncl;
+    const int my_tiles = cid < n_tiles ? (n_tiles - cid + ncl - 1) / ncl : 0;
+    w.left = int64_t(my_tiles) * (w.c_end - w.c_begin);
+  } else {
+    const int64_t T = int64_t(n_tiles) * nC;
+    const int G = gridDim.x;
+    const int64_t lo = int64_t(blockIdx.x) * T / G, hi = int64_t(blockIdx.x + 1) * T / G;
+    w.r = int(lo / nC);
+    w.c = int(lo % nC);
+    w.c_begin = w.c;
+    w.c_end = nC;
+    w.r_step = 1;
+    w.left = hi - lo;
+  }
+  return w;
+}
+
+template <bool Q4, int NT, bool kCluster>
 __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams p) {
   using C = GemvCfg<Q4, NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
+  const int kStages = p.stages;
   uint8_t* ring = smem;
-  float* otile = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kTileFloats * 4);
-  uint64_t* empty = full + C::kStages;
-  int* flag = reinterpret_cast<int*>(empty + C::kStages);
+  float* otile = reinterpret_cast<float*>(smem + kStages * C::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + C::kTileFloats * 4);
+  uint64_t* empty = full + C::kMaxStages;
+  int* flag = reinterpret_cast<int*>(empty + C::kMaxStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SS_TRACE_MIN(0);
   const int nC = p.K >> 7;
   const int64_t T = int64_t(p.N >> 7) * nC;
-  const int G = gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * T / G, hi = int64_t(blockIdx.x + 1) * T / G;
   const int Mpad = NT * 8;
-
+  uint32_t crank = 0, csize = 1;
+  if constexpr (kCluster) {
+    crank = cluster_rank();
+    csize = cluster_nrank();
+  }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGemvConsumerWarps);
     }
     fence_barrier_init();
   }
   __syncthreads();
-  griddep_launch();   // all CTAs are resident (grid <= #SMs): let the next kernel prefetch now
+  griddep_launch();   // grid <= one CTA per SM: let the next kernel prefetch now
 
   if (warp == kGemvConsumerWarps) {
     // ------------------------------ producer -------------------------------
+    Work w = make_work<kCluster>(p.N, p.K, crank, csize);
+    const int64_t n_stage = w.stages(nC, C::kCPS);
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      const int64_t n = hi - lo;
-      const int pre = int(n < C::kStages ? n : C::kStages);
+      const int pre = int(n_stage < kStages ? n_stage : kStages);
+      Work wx = w;   // replayed below for the activation copies of the prefetched stages
+      auto issue_w = [&](int st, const Work& ww, int n) {
+        mbar_arrive_expect_tx(&full[st], uint32_t(n) * (C::kWBytes + C::kXBytes + C::kSBytes));
+        bulk_g2s_hint(ring + st * C::kStageBytes, p.W + (int64_t(ww.r) * nC + ww.c) * C::kWBytes,
+                      uint32_t(n) * C::kWBytes, &full[st], pol);
+      };
+      auto issue_x = [&](int st, const Work& ww, int n) {
+        uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
+        bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
+        if constexpr (Q4)
+          bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * NT * 8, uint32_t(n) * C::kSBytes, &full[st]);
+      };
       // weights do not depend on the previous kernel: issue before the grid-dependency wait
       for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], C::kStageBytes);
-        bulk_g2s_hint(ring + i * C::kStageBytes, p.W + (lo + i) * C::kWBytes, C::kWBytes, &full[i], pol);
+        const int n = w.take(C::kCPS);
+        issue_w(i, w, n);
+        w.next(nC, n);
       }
       griddep_wait();
+      SS_TRACE_CTA0(1);
       for (int i = 0; i < pre; ++i) {
-        const int c = int((lo + i) % nC);
-        bulk_g2s(ring + i * C::kStageBytes + C::kWBytes, p.X + int64_t(c) * NT * 1024, C::kXBytes, &full[i]);
+        const int n = wx.take(C::kCPS);
+        issue_x(i, wx, n);
+        wx.next(nC, n);
       }
-      for (int64_t i = pre; i < n; ++i) {
-        const int s = int(i % C::kStages);
-        const uint32_t ph = uint32_t((i / C::kStages) - 1) & 1;
-        mbar_wait(&empty[s], ph);
-        const int c = int((lo + i) % nC);
-        mbar_arrive_expect_tx(&full[s], C::kStageBytes);
-        bulk_g2s_hint(ring + s * C::kStageBytes, p.W + (lo + i) * C::kWBytes, C::kWBytes, &full[s], pol);
-        bulk_g2s(ring + s * C::kStageBytes + C::kWBytes, p.X + int64_t(c) * NT * 1024, C::kXBytes, &full[s]);
+      int st = pre % kStages;
+      uint32_t ph = pre / kStages;   // 0 or 1 (pre <= kStages)
+      for (int64_t i = pre; i < n_stage; ++i) {
+        mbar_wait(&empty[st], (ph - 1) & 1);
+        const int n = w.take(C::kCPS);
+        issue_w(st, w, n);
+        issue_x(st, w, n);
+        w.next(nC, n);
+        if (++st == kStages) {
+          st = 0;
+          ++ph;
+        }
+      }
+    }
+    if constexpr (kCluster) {
+      if (csize > 1) {   // take part in the cluster barriers of every tile's reduction
+        const int64_t per = int64_t(w.c_end - w.c_begin);
+        const int64_t tiles = per ? w.left / per : 0;
+        for (int64_t t = 0; t < tiles; ++t) {
+          cluster_sync_all();
+          cluster_sync_all();
+        }
       }
     }
     return;
@@ -112,147 +256,245 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
 
   // ------------------------------ consumers --------------------------------
   griddep_wait();
+  if (threadIdx.x == 0) SS_TRACE_CTA0(2);
   const int g = lane >> 2, t4 = lane & 3;
+  const int nthr = kGemvConsumerWarps * 32;
   float acc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
-  auto flush = [&](int64_t r, int64_t c_first, int64_t c_last) {
-    // c_first..c_last: chunks of row tile r handled by this CTA
-    const bool complete = (c_first == 0 && c_last == nC - 1);
-    float* dst;
-    int ld;
-    int64_t slot = 0, nseg = 1, first = 0;
-    if (complete) {
-      dst = otile;
-      ld = Mpad;
-    } else {
-      first = owner_of(r * nC, T, G);
-      nseg = owner_of((r + 1) * nC - 1, T, G) - first + 1;
-      slot = blockIdx.x - first;
-      dst = p.partials + (r * p.max_seg + slot) * int64_t(kTileRows * Mpad);
-      ld = Mpad;
-    }
+  auto stash = [&](float* dst) {   // accumulators -> [128 x Mpad] tile, then clear
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
-      dst[n0 * ld + m] = acc[j][0];
-      dst[n0 * ld + m + 1] = acc[j][1];
-      dst[(n0 + 8) * ld + m] = acc[j][2];
-      dst[(n0 + 8) * ld + m + 1] = acc[j][3];
+      *reinterpret_cast<float2*>(dst + n0 * Mpad + m) = make_float2(acc[j][0], acc[j][1]);
+      *reinterpret_cast<float2*>(dst + (n0 + 8) * Mpad + m) = make_float2(acc[j][2], acc[j][3]);
       acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     }
-    const int ctid = threadIdx.x, nthr = kGemvConsumerWarps * 32;
-    if (!complete) {
-      __threadfence();
-      named_bar(1, nthr);
-      if (ctid == 0) {
-        const int old = atomicAdd(&p.counters[r], 1);
-        *flag = (old == nseg - 1);
-      }
-      named_bar(1, nthr);
-      if (!*flag) return;
-      __threadfence();
-      const float* base = p.partials + r * p.max_seg * int64_t(kTileRows * Mpad);
-      for (int e = ctid; e < kTileRows * Mpad; e += nthr) {
-        float s = 0.f;
-        for (int q = 0; q < nseg; ++q) s += __ldcg(base + q * int64_t(kTileRows * Mpad) + e);
-        otile[e] = s;
-      }
-      if (ctid == 0) p.counters[r] = 0;
-    }
-    named_bar(1, nthr);
-    apply_epilogue(p.epi, otile, Mpad, int(r), 0, Mpad, ctid, nthr);
-    named_bar(1, nthr);
   };
 
-  int64_t cur_r = lo / nC, c_first = lo % nC;
-  for (int64_t i = lo; i < hi; ++i) {
-    const int64_t r = i / nC;
-    const int c = int(i % nC);
-    if (r != cur_r) {
-      flush(cur_r, c_first, nC - 1);
-      cur_r = r;
-      c_first = c;
-    }
-    const int s = int((i - lo) % C::kStages);
-    const uint32_t ph = uint32_t((i - lo) / C::kStages) & 1;
-    mbar_wait(&full[s], ph);
-    const uint8_t* wst = ring + s * C::kStageBytes;
-    const uint8_t* xst = wst + C::kWBytes;
-    if constexpr (Q4) {
-      const uint4 c0 = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + 0) * 32 + lane) * 16);
-      const uint4 c1 = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + 1) * 32 + lane) * 16);
-      const uint32_t m0 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + (t4 >> 1)) * 16 + g) * 4);
-      const uint32_t m1 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + (t4 >> 1)) * 16 + g + 8) * 4);
-      const uint32_t s0 = (m0 & 0xFFFFu) * 0x10001u, z0 = (m0 >> 16) * 0x10001u;
-      const uint32_t s1 = (m1 & 0xFFFFu) * 0x10001u, z1 = (m1 >> 16) * 0x10001u;
-      const uint32_t w0[4] = {c0.x, c0.y, c0.z, c0.w};
-      const uint32_t w1[4] = {c1.x, c1.y, c1.z, c1.w};
-#pragma unroll
-      for (int st = 0; st < 8; ++st) {
-        const int pp = 2 * (st & 1);
-        const uint32_t a0 = dq_pair(w0[st >> 1], pp, s0, z0);
-        const uint32_t a1 = dq_pair(w1[st >> 1], pp, s1, z1);
-        const uint32_t a2 = dq_pair(w0[st >> 1], pp + 1, s0, z0);
-        const uint32_t a3 = dq_pair(w1[st >> 1], pp + 1, s1, z1);
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const uint2 b = *reinterpret_cast<const uint2*>(xst + ((((j * 8 + st) * 4 + t4) * 8 + g) * 8));
-          mma_bf16_16816(acc[j], a0, a1, a2, a3, b.x, b.y);
+  auto flush = [&](int r, int c_first, int c_last) {
+    if constexpr (kCluster) {
+      stash(otile);
+      if (csize > 1) {
+        cluster_sync_all();                       // partial tiles of all ranks visible cluster-wide
+        if (crank == 0) {
+          for (int e = threadIdx.x * 4; e < kTileRows * Mpad; e += nthr * 4) {
+            float4 v = *reinterpret_cast<float4*>(otile + e);
+            for (uint32_t q = 1; q < csize; ++q) {
+              const float4 o = ld_dsmem_f32x4(otile + e, q);
+              v.x += o.x;
+              v.y += o.y;
+              v.z += o.z;
+              v.w += o.w;
+            }
+            *reinterpret_cast<float4*>(otile + e) = v;
+          }
         }
+        cluster_sync_all();                       // peers reuse/exit only after rank 0 read them
       }
+      if (crank == 0) {
+        named_bar(1, nthr);
+        apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr);
+        named_bar(1, nthr);
+      }
+      return;
     } else {
+      const bool complete = (c_first == 0 && c_last == nC - 1);
+      if (complete) {
+        stash(otile);
+      } else {
+        const int G = gridDim.x;
+        const int64_t first = owner_of(int64_t(r) * nC, T, G);
+        const int64_t nseg = owner_of(int64_t(r + 1) * nC - 1, T, G) - first + 1;
+        const int64_t slot = blockIdx.x - first;
+        stash(p.partials + (int64_t(r) * p.max_seg + slot) * int64_t(kTileRows * Mpad));
+        __threadfence();
+        named_bar(1, nthr);
+        if (threadIdx.x == 0) {
+          const int old = atomicAdd(&p.counters[r], 1);
+          *flag = (old == nseg - 1);
+        }
+        named_bar(1, nthr);
+        if (!*flag) return;
+        __threadfence();
+        const float* base = p.partials + int64_t(r) * p.max_seg * int64_t(kTileRows * Mpad);
+        for (int e = threadIdx.x; e < kTileRows * Mpad; e += nthr) {
+          float s = 0.f;
+          for (int q = 0; q < nseg; ++q) s += __ldcg(base + q * int64_t(kTileRows * Mpad) + e);
+          otile[e] = s;
+        }
+        if (threadIdx.x == 0) p.counters[r] = 0;
+      }
+      named_bar(1, nthr);
+      apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr);
+      named_bar(1, nthr);
+    }
+  };
+
+  Work w = make_work<kCluster>(p.N, p.K, crank, csize);
+  const int64_t n_items = w.left;
+  int cur_r = w.r, c_first = w.c, c_last = w.c;
+  int s = 0;
+  uint32_t ph = 0;
+  const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
+  while (w.left > 0) {
+    if (w.r != cur_r) {
+      flush(cur_r, c_first, c_last);
+      cur_r = w.r;
+      c_first = w.c;
+    }
+    const int nch = w.take(C::kCPS);
+    c_last = w.c + nch - 1;
+    mbar_wait(&full[s], ph);
+    if (threadIdx.x == 0 && w.left == n_items) SS_TRACE_CTA0(3);
+    const uint8_t* stage = ring + s * C::kStageBytes;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 r0 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 0) * 4 + q) * 32 + lane) * 16);
-        const uint4 r1 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 1) * 4 + q) * 32 + lane) * 16);
+    for (int ci = 0; ci < C::kCPS; ++ci) {
+      if (ci >= nch) break;
+      const uint8_t* wst = stage + ci * C::kWBytes;
+      const uint8_t* xst = stage + C::kCPS * C::kWBytes + ci * C::kXBytes + ((t4 * 8 + g) * 8);
+      if constexpr (Q4) {
+        const float* xsum = reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int st = 2 * q + hh;
-          const uint32_t a0 = hh ? r0.z : r0.x, a2 = hh ? r0.w : r0.y;
-          const uint32_t a1 = hh ? r1.z : r1.x, a3 = hh ? r1.w : r1.y;
+        for (int G = 0; G < 2; ++G) {
+          const uint4 cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);
+          const uint32_t m0 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g) * 4);
+          const uint32_t m1 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4);
+          float cg[NT][4];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) cg[j][0] = cg[j][1] = cg[j][2] = cg[j][3] = 0.f;
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int st = 4 * G + k4;
+            const uint32_t wg = (k4 < 2) ? cw.x : cw.y, wg8 = (k4 < 2) ? cw.z : cw.w;
+            const int pp = 2 * (k4 & 1);
+            const uint32_t a0 = lop3_and_or(wg >> (4 * pp), kMagic);
+            const uint32_t a1 = lop3_and_or(wg8 >> (4 * pp), kMagic);
+            const uint32_t a2 = lop3_and_or(wg >> (4 * pp + 4), kMagic);
+            const uint32_t a3 = lop3_and_or(wg8 >> (4 * pp + 4), kMagic);
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              const uint2 b = *reinterpret_cast<const uint2*>(xst + (j * 8 + st) * 256);
+              mma_bf16_16816(cg[j], a0, a1, a2, a3, b.x, b.y);
+            }
+          }
+          // y += s * sum((128 + c) x) + (z - 128 s) * sum(x)      (exact affine dequant, fp32)
+          const float s0 = __uint_as_float(m0 << 16), z0 = __uint_as_float(m0 & 0xFFFF0000u);
+          const float s1 = __uint_as_float(m1 << 16), z1 = __uint_as_float(m1 & 0xFFFF0000u);
+          const float zz0 = fmaf(-128.0f, s0, z0), zz1 = fmaf(-128.0f, s1, z1);   // exact
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
-            const uint2 b = *reinterpret_cast<const uint2*>(xst + ((((j * 8 + st) * 4 + t4) * 8 + g) * 8));
-            mma_bf16_16816(acc[j], a0, a1, a2, a3, b.x, b.y);
+            const float2 xs = *reinterpret_cast<const float2*>(xsum + G * NT * 8 + j * 8 + 2 * t4);
+            acc[j][0] = fmaf(s0, cg[j][0], fmaf(zz0, xs.x, acc[j][0]));
+            acc[j][1] = fmaf(s0, cg[j][1], fmaf(zz0, xs.y, acc[j][1]));
+            acc[j][2] = fmaf(s1, cg[j][2], fmaf(zz1, xs.x, acc[j][2]));
+            acc[j][3] = fmaf(s1, cg[j][3], fmaf(zz1, xs.y, acc[j][3]));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 r0 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 0) * 4 + q) * 32 + lane) * 16);
+          const uint4 r1 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 1) * 4 + q) * 32 + lane) * 16);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int st = 2 * q + hh;
+            const uint32_t a0 = hh ? r0.z : r0.x, a2 = hh ? r0.w : r0.y;
+            const uint32_t a1 = hh ? r1.z : r1.x, a3 = hh ? r1.w : r1.y;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              const uint2 b = *reinterpret_cast<const uint2*>(xst + (j * 8 + st) * 256);
+              mma_bf16_16816(acc[j], a0, a1, a2, a3, b.x, b.y);
+            }
           }
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == kStages) {
+      s = 0;
+      ph ^= 1;
+    }
+    w.next(nC, nch);
   }
-  if (hi > lo) flush(cur_r, c_first, (hi - 1) % nC);
+  if (threadIdx.x == 0) {
+    SS_TRACE_CTA0(4);
+    SS_TRACE_MAX(7);
+  }
+  if (n_items > 0) flush(cur_r, c_first, c_last);   // the last tile of this CTA
+  if (threadIdx.x == 0) SS_TRACE_MAX(6);
 }
 
-template <bool Q4, int NT>
-static void launch_t(const GemvParams& p, int grid, bool pdl, cudaStream_t st) {
+// split factor of the cluster mode: ~one CTA per SM, <= 8 (portable cluster), <= chunks
+int gemv_cluster_split(int N, int K, int sms) {
+  const int tiles = N / 128, nC = K / 128;
+  int S = (sms + tiles / 2) / tiles;
+  if (S < 1) S = 1;
+  if (S > 8) S = 8;
+  if (S > nC) S = nC;
+  return S;
+}
+bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
+
+template <bool Q4, int NT, bool kCluster>
+static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
   using C = GemvCfg<Q4, NT>;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(gemv_kernel<Q4, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    init = true;
+  static int stages = 0;
+  if (!stages) {
+    const int budget = env_int("SS_GEMV_RING_KB", 88) * 1024;
+    stages = budget / C::kStageBytes;
+    if (stages < 2) stages = 2;
+    if (stages > C::kMaxStages) stages = C::kMaxStages;
+    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(stages));
   }
+  GemvParams p = p0;
+  p.stages = stages;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemvThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.dynamicSmemBytes = C::smem_for(stages);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (kCluster) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = S;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT>, p);
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster>, p);
+}
+
+template <bool Q4, int NT>
+static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
+  if (gemv_use_cluster(p.N, p.K, sms)) {
+    const int S = gemv_cluster_split(p.N, p.K, sms);
+    const int tiles = p.N / 128;
+    static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
+    int ncl = sms * per_sm / S;
+    if (ncl > tiles) ncl = tiles;
+    if (ncl < 1) ncl = 1;
+    launch_t<Q4, NT, true>(p, ncl * S, S, pdl, st);
+  } else {
+    launch_t<Q4, NT, false>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);
+  }
 }
 
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st) {
-  grid = gemv_grid_for(p.N, p.K, grid);
   switch (p.NT) {
-    case 1: q4 ? launch_t<true, 1>(p, grid, pdl, st) : launch_t<false, 1>(p, grid, pdl, st); break;
-    case 2: q4 ? launch_t<true, 2>(p, grid, pdl, st) : launch_t<false, 2>(p, grid, pdl, st); break;
-    case 4: q4 ? launch_t<true, 4>(p, grid, pdl, st) : launch_t<false, 4>(p, grid, pdl, st); break;
+    case 1: q4 ? launch_mode<true, 1>(p, grid, pdl, st) : launch_mode<false, 1>(p, grid, pdl, st); break;
+    case 2: q4 ? launch_mode<true, 2>(p, grid, pdl, st) : launch_mode<false, 2>(p, grid, pdl, st); break;
+    case 4: q4 ? launch_mode<true, 4>(p, grid, pdl, st) : launch_mode<false, 4>(p, grid, pdl, st); break;
     default: break;
   }
 }

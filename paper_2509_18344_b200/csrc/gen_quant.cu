@@ -63,9 +63,9 @@ void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float
 }
 
 // ---------------------------------------------------------------------------
-// K1: RTN min/max 4-bit group-64 quantizer, bf16 tiled -> Q4 tiled.
-// One warp per (tile-chunk, 16-row block).  Lane (g, t4) holds rows 16w+g, 16w+g+8 and
-// k = 32 t4 .. 32 t4 + 31; a 64-group spans lanes t4 = {0,1} or {2,3} (partner = lane ^ 1).
+// K1: RTN min/max 4-bit group-64 quantizer, bf16 tiled -> Q4 tiled (SURVEY O.2).
+// One warp per (tile-chunk, 16-row block).  Lane (g, t4) holds rows 16w+g, 16w+g+8 and, for each
+// 64-group G of the chunk, k = 64G + 16 t4 .. +15; a group spans the 4 lanes t4 = 0..3 of a g.
 //   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / 15) ; z = m
 //   code = clamp(rint_even(fp32(x - z) / s), 0, 15)       (IEEE div.rn; built without fast-math)
 // ---------------------------------------------------------------------------
@@ -76,50 +76,52 @@ __global__ void __launch_bounds__(256) quantize_q4_kernel(const uint8_t* __restr
   for (int64_t tc = blockIdx.x; tc < n_tc; tc += gridDim.x) {
     const uint8_t* s_tile = src + tc * kBF16TileBytes;
     uint8_t* d_tile = dst + tc * kQ4TileBytes;
+    float x[2][32];   // [h][q*8 + e] with q = 2G + i16/8, e = i16 % 8
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float x[32];
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint4 v = *reinterpret_cast<const uint4*>(s_tile + (((warp * 2 + h) * 4 + q) * 32 + lane) * 16);
-        uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        const uint4 v = *reinterpret_cast<const uint4*>(s_tile + (((warp * 2 + h) * 4 + q) * 32 + lane) * 16);
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          x[q * 8 + 2 * e] = __uint_as_float(w4[e] << 16);
-          x[q * 8 + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
+          x[h][q * 8 + 2 * e] = __uint_as_float(w4[e] << 16);
+          x[h][q * 8 + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
         }
       }
-      float mn = x[0], mx = x[0];
 #pragma unroll
-      for (int i = 1; i < 32; ++i) {
-        mn = fminf(mn, x[i]);
-        mx = fmaxf(mx, x[i]);
-      }
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      float sc;
-      if (mx == mn) {
-        sc = 1.0f;
-      } else {
-        sc = __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), 15.0f))) << 16);
-      }
-      const float z = mn;
-      uint32_t words[4] = {0, 0, 0, 0};
+    for (int G = 0; G < 2; ++G) {
+      uint32_t words[2][2] = {{0, 0}, {0, 0}};
+      uint32_t meta[2];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float t = __fdiv_rn(__fsub_rn(x[i], z), sc);
-        float r = rintf(t);
-        r = fminf(fmaxf(r, 0.0f), 15.0f);
-        uint32_t code = uint32_t(r);
-        int c = i & 7, slot = (c & 1) * 4 + (c >> 1);
-        words[i >> 3] |= code << (4 * slot);
+      for (int h = 0; h < 2; ++h) {
+        const float* xv = &x[h][16 * G];   // i16 = 0..15
+        float mn = xv[0], mx = xv[0];
+#pragma unroll
+        for (int i = 1; i < 16; ++i) {
+          mn = fminf(mn, xv[i]);
+          mx = fmaxf(mx, xv[i]);
+        }
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), 15.0f))) << 16);
+        const float z = mn;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float t = __fdiv_rn(__fsub_rn(xv[i], z), sc);
+          const float r = fminf(fmaxf(rintf(t), 0.0f), 15.0f);
+          const int c8 = i & 7, slot = (c8 & 1) * 4 + (c8 >> 1);
+          words[h][i >> 3] |= uint32_t(r) << (4 * slot);
+        }
+        meta[h] = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
       }
-      *reinterpret_cast<uint4*>(d_tile + ((warp * 2 + h) * 32 + lane) * 16) =
-          make_uint4(words[0], words[1], words[2], words[3]);
-      if ((t4 & 1) == 0) {
-        int grp = t4 >> 1, rr = g + 8 * h;
-        uint32_t meta = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
-        *reinterpret_cast<uint32_t*>(d_tile + kQ4CodeBytes + ((warp * 2 + grp) * 16 + rr) * 4) = meta;
+      *reinterpret_cast<uint4*>(d_tile + ((warp * 2 + G) * 32 + lane) * 16) =
+          make_uint4(words[0][0], words[0][1], words[1][0], words[1][1]);
+      if (t4 == 0) {
+        *reinterpret_cast<uint32_t*>(d_tile + kQ4CodeBytes + ((warp * 2 + G) * 16 + g) * 4) = meta[0];
+        *reinterpret_cast<uint32_t*>(d_tile + kQ4CodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4) = meta[1];
       }
     }
   }

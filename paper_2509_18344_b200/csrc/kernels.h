@@ -26,6 +26,7 @@ struct EpiParams {
   int ldx;
   // EPI_SILU
   uint16_t* act;                 // FragX [Mpad x F]
+  float* act_xs;                 // group sums [F/64][Mpad] (sum of the bf16 activations)
   int act_nt, ffn;
   // EPI_LOGITS / EPI_STORE
   float* out;                    // [M x ldo]
@@ -40,10 +41,13 @@ struct EpiParams {
 struct GemvParams {
   const uint8_t* W;              // tiled weights (Q4 or BF16)
   const uint16_t* X;             // FragX [Mpad x K]
+  const float* XS;               // Q4 only: group sums of X, [K/64][Mpad] fp32 (sum of the bf16 values)
   int N, K, NT;                  // NT = Mpad / 8
   float* partials;               // [n_tiles][max_seg][128*Mpad]
   int* counters;                 // [n_tiles], zero on entry, restored to zero on exit
   int max_seg;
+  int stages;                    // ring depth (set by the launcher)
+  unsigned long long* trace;     // optional %globaltimer trace: [8] events of this launch (debug)
   EpiParams epi;
 };
 
@@ -69,9 +73,10 @@ void launch_tiled_to_natural(const uint8_t* t, uint16_t* out, int64_t N, int64_t
 
 // small kernels (K4, K5, K8, K9)
 void launch_embed_rmsnorm(const int* tokens_dev, int tok_offset, int M, const uint16_t* embed, float* x, int H,
-                          const uint16_t* gain, float eps, uint16_t* h_fragx, int nt, bool pdl, cudaStream_t st);
-void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float eps, uint16_t* h_fragx, int nt,
-                    bool pdl, cudaStream_t st);
+                          const uint16_t* gain, float eps, uint16_t* h_fragx, float* h_xs, int nt, bool pdl,
+                          cudaStream_t st);
+void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float eps, uint16_t* h_fragx, float* h_xs,
+                    int nt, bool pdl, cudaStream_t st);
 
 struct AttnParams {
   const uint16_t* q;             // [n_q x n_h*d] bf16
@@ -89,7 +94,10 @@ struct AttnParams {
   int n_seg_max;                 // segments allocated in the partial buffers
   float* part_o;                 // [n_q * n_heads][n_seg_max][d]
   float* part_ml;                // [n_q * n_heads][n_seg_max][2]
+  int* counters;                 // unused (reserved)
+  int single;                    // set by the launcher: all rows fit one segment
   uint16_t* out_fragx;           // [Mpad x n_heads*d] FragX
+  float* out_xs;                 // group sums [n_heads*d/64][Mpad]
   int out_nt;
 };
 void launch_attention(const AttnParams& p, int max_prefix, bool pdl, cudaStream_t st);

@@ -1,0 +1,21 @@
+"""Attribute one Qwen-7B-shape draft pass (M = 6) to kernel classes by skipping them."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from synth.configs import QWEN7B, GIB
+from synth.prompts import mtbench_prompt
+from paper_2509_18344_b200.binding import SubSpec
+ss = SubSpec(QWEN7B, 8 * GIB, max_depth=48, max_top_k=6)
+ss.load_weights(0x5EED, 0); ss.build_substitutes()
+ss.prefill(mtbench_prompt(0x5EED, 0, QWEN7B.vocab))
+for name, skip in (("full", 0), ("-attn", 1), ("-norm", 2), ("-gemv", 4), ("-head", 8), ("gemv+head only", 3), ("gemv only", 11), ("nothing", 15)):
+    print(f"{name:16s} {ss.debug_time_pass(6, 5, skip) * 1e3:9.1f} us/pass", flush=True)
+tr = ss.debug_trace_pass(6).astype("float64")
+t0 = tr[:, 0].min()
+names = ["qkv", "o", "gate_up", "down"]
+print("launch  entry  pdep  cdep  first  loop0  loopmax  end   (us, rel. to first entry)")
+prev_end = None
+for i, r in enumerate(tr[:12]):
+    rel = (r - t0) / 1e3
+    gap = "" if prev_end is None else f" gap_from_prev_end={rel[0] - prev_end:6.2f}"
+    print(f"{names[i % 4]:8s} " + " ".join(f"{v:6.2f}" for v in rel[[0, 1, 2, 3, 4, 7, 6]]) + gap)
+    prev_end = rel[6]
