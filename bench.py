@@ -198,6 +198,23 @@ def workload_config(a, cfg):
             "parallelism": f"requests partitioned, {a.gpus} GPU(s), no collective"}
 
 
+def aggregate_ranks(dist, ms, tokens, device="cpu"):
+    """Whole-job timing across ranks: max of the per-rank device times, sum of the tokens."""
+    if dist is None:
+        return ms, tokens
+    import torch
+    t = torch.tensor([float(ms)], device=device, dtype=torch.float64)
+    n = torch.tensor([float(tokens)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(n)
+    return float(t), float(n)
+
+
+def request_for_rank(rank, vocab):
+    """Requests are partitioned over ranks (BJ config 5): rank r decodes prompt r."""
+    return mtbench_prompt(SEED, rank, vocab)
+
+
 def k2_bytes(N, K, M):
     # SURVEY §8(d): codes N*K/2 + meta N*K/64*4 + X M*K*2 + Y M*N*2
     return N * K // 2 + N * K // 64 * 4 + M * K * 2 + M * N * 2
@@ -218,7 +235,7 @@ def run_ours(a):
     ss = SubSpec(cfg, int(a.cap_gib * GIB), device=local, max_depth=D, max_top_k=max(k, 6), max_chunk=256)
     ss.load_weights(SEED, n_resident=a.n_resident)
     ss.build_substitutes(4, 64)
-    prompt = mtbench_prompt(SEED, rank, cfg.vocab)
+    prompt = request_for_rank(rank, cfg.vocab)
     ss.prefill(prompt)
     t_setup = time.time() - t_setup
     for _ in range(a.warmup):
@@ -277,12 +294,7 @@ def run_ours(a):
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         st1 = ss.stats()
-        if dist:
-            t_ = torch.tensor([wall], device=f"cuda:{local}")
-            n_ = torch.tensor([float(e2e_tok)], device=f"cuda:{local}")
-            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
-            dist.all_reduce(n_)
-            wall, e2e_tok = float(t_), float(n_)
+        wall, e2e_tok = aggregate_ranks(dist, wall, e2e_tok, f"cuda:{local}")
         streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / n_e2e
         e2e = {"value": e2e_tok / wall, "unit": "tokens/s", "h2d_bytes_per_step": int(4 + streamed),
                "d2h_bytes_per_step": int(4 * (e2e_tok / max(1, n_e2e)) + 4),
@@ -302,13 +314,7 @@ def run_ours(a):
     link_gbs = (1 << 30) / (best * 1e-3) / 1e9
     del hbuf, dbuf
     # ---- aggregate over ranks ----
-    tot_tokens, tmax = float(emitted), ms
-    if dist:
-        t_ = torch.tensor([ms], device=f"cuda:{local}")
-        n_ = torch.tensor([float(emitted)], device=f"cuda:{local}")
-        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
-        dist.all_reduce(n_)
-        tmax, tot_tokens = float(t_), float(n_)
+    tmax, tot_tokens = aggregate_ranks(dist, ms, emitted, f"cuda:{local}")
     value = tot_tokens / (tmax / 1e3)
     tau = float(np.mean(taus))
     steps_per_s = a.steps / (ms / 1e3)

@@ -1350,8 +1350,10 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
 ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
                            float* out_logits) {
   GUARD(c);
-  if (c->state != ST_SESSION) return fail(c, SS_ERR_STRUCTURE, "debug_forward needs a session");
+  if (c->state != ST_SESSION && c->state != ST_DRAFTED)
+    return fail(c, SS_ERR_STRUCTURE, "debug_forward needs a session (or a drafted tree)");
   if (!tokens || !parents || n < 1 || n > c->max_nodes || !out_logits) return fail(c, SS_ERR_INVALID, "debug_forward args");
+  if (which == 1 && c->state == ST_DRAFTED) return fail(c, SS_ERR_STRUCTURE, "target debug_forward inside a step");
   // depth-major tree check + host-side depths/ancestors
   std::vector<int> dep(n), anc(size_t(n) * c->anc_stride, 0), par(parents, parents + n), tk(tokens, tokens + n);
   for (int i = 0; i < n; ++i) {
