@@ -38,6 +38,11 @@ SS_HD KPos kpos(int64_t k) {
   p.j = p.i16 & 3;
   return p;
 }
+// byte offset, inside a bf16 tile-chunk, of the 16-byte piece q (= 2*G + half) of (warp w, row half h,
+// lane): group-major, so each 64-k half of a tile-chunk (16 KB) is contiguous.
+SS_HD int bf16_piece_off(int w, int h, int q, int lane) {
+  return (((((q >> 1) * 8 + w) * 2 + h) * 2 + (q & 1)) * 32 + lane) * 16;
+}
 SS_HD uint64_t bf16_tiled_offset(int64_t n, int64_t k, int64_t K) {   // in bytes
   const int64_t tc = (n >> 7) * (K >> 7) + (k >> 7);
   const int nn = int(n & 127);
@@ -45,7 +50,7 @@ SS_HD uint64_t bf16_tiled_offset(int64_t n, int64_t k, int64_t K) {   // in byte
   const KPos p = kpos(k);
   const int q = 2 * p.G + (p.i16 >> 3), e = p.i16 & 7;
   const int lane = g * 4 + p.t4;
-  return uint64_t(tc) * kBF16TileBytes + uint64_t((((w * 2 + h) * 4 + q) * 32 + lane) * 16 + e * 2);
+  return uint64_t(tc) * kBF16TileBytes + uint64_t(bf16_piece_off(w, h, q, lane) + e * 2);
 }
 
 // Q4: per (warp w, group G, lane) 16 bytes = [row g: word0, word1][row g+8: word0, word1];
@@ -134,6 +139,10 @@ SS_DEV void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes, 
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// TMA-engine prefetch of a global range into L2 (no shared memory involved)
+SS_DEV void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 SS_DEV uint64_t policy_evict_first() {
   uint64_t p;

@@ -128,6 +128,18 @@ struct ss_ctx {
   std::vector<bool> ev_pending;
   std::deque<int> timing_queue;
   int ev_pool = 0;
+  // fused persistent draft pass (pass.cu)
+  bool use_fused = false;
+  bool l2_prefetch = true;
+  bool attn_v2 = true;
+  std::vector<PhaseDesc> phases;
+  PhaseDesc* d_phases = nullptr;
+  float *sumsq = nullptr, *pass_part = nullptr;
+  unsigned* pass_bar = nullptr;
+  int* attn_ctr = nullptr;
+  int* norm_ctr = nullptr;
+  bool fuse_norm = true;
+  int pass_grid = 0, pass_stages = 0;
   // graphs
   std::map<std::tuple<int, int, uint32_t>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, uint32_t>, int64_t> graph_launches;
@@ -272,6 +284,27 @@ unsigned long long* g_trace = nullptr;   // device buffer [launch][8] for ss_deb
 int g_trace_n = 0, g_trace_cap = 0;
 enum { SKIP_ATTN = 1, SKIP_NORM = 2, SKIP_GEMV = 4, SKIP_HEAD = 8 };
 
+// the draft's weight stream in pass order: qkv, o, gate_up, down of each layer, then the head
+static void next_weights(ss_ctx* c, int l, int g, const uint8_t** ptr, int64_t* bytes) {
+  int nl = l, ng = g + 1;
+  if (ng == 4) {
+    ng = 0;
+    ++nl;
+  }
+  if (nl >= c->L) {   // after the last layer: the head (prefetch its first part only)
+    *ptr = c->head;
+    *bytes = std::min<int64_t>(int64_t(64) << 20, int64_t(bf16_bytes(c->V, c->H)));
+    return;
+  }
+  const LayerW& w = c->lw[nl];
+  *ptr = w.resident ? w.bf16[ng] : w.q4[ng];
+  *bytes = int64_t(w.resident ? bf16_bytes(c->gN[ng], c->gK[ng]) : q4_bytes(c->gN[ng], c->gK[ng]));
+  if (ng == 0) {   // qkv is small: let it cover o as well (two kernels ahead)
+    const uint8_t* p2 = w.resident ? w.bf16[1] : w.q4[1];
+    if (p2 == *ptr + *bytes) *bytes += int64_t(w.resident ? bf16_bytes(c->gN[1], c->gK[1]) : q4_bytes(c->gN[1], c->gK[1]));
+  }
+}
+
 ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M, const EpiParams& epi) {
   if (!target && (g_skip & SKIP_GEMV)) return SS_OK;
   const int N = c->gN[g], K = c->gK[g];
@@ -288,6 +321,7 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.counters = c->gv_cnt;
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = epi;
+    if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + 8 * (g_trace_n++);
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
     c->launches++;
@@ -369,7 +403,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     a.n_heads = c->nh;
     a.n_kv = c->nkv;
     a.head_dim = c->d;
-    a.split = target ? c->split_target : c->split_draft;
+    a.split = c->attn_v2 ? 0 : (target ? c->split_target : c->split_draft);
     a.n_seg_max = c->at_seg_max;
     a.part_o = c->at_o;
     a.part_ml = c->at_ml;
@@ -380,13 +414,31 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     // logical keys of a node: P + depth + 1 <= max_context.  The draft loop is replayed from a CUDA
     // graph while P grows, so its grid is sized for max_context.
     if (!(g_skip & SKIP_ATTN)) launch_attention(a, target ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
-    c->launches += 2;
+    c->launches += c->attn_v2 ? 1 : 2;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
+    const bool fnorm = !target && c->fuse_norm && !(g_skip & SKIP_NORM) &&
+                       gemv_tiles_all_resident(c->gN[1], c->gK[1], c->gv_grid) &&
+                       gemv_tiles_all_resident(c->gN[3], c->gK[3], c->gv_grid);
+    auto resid_norm = [&](const uint16_t* gain) {
+      EpiParams r = base_epi(c, M);
+      r.kind = EPI_RESID_NORM;
+      r.sumsq = c->sumsq;
+      r.norm_gain = gain;
+      r.norm_out = c->hfrag;
+      r.norm_xs = c->hxs;
+      r.norm_ctr = c->norm_ctr;
+      r.n_tiles = c->H / 128;
+      r.eps = eps;
+      r.act_nt = NT;
+      return r;
+    };
     e = base_epi(c, M);
     e.kind = EPI_RESID;
+    if (fnorm) e = resid_norm(c->lw[l].mlp_norm);
     if ((s = matmul(c, target, l, 1, c->attnfrag, M, e)) != SS_OK) return s;
-    if (!(g_skip & SKIP_NORM)) launch_rmsnorm(c->x, M, c->H, c->lw[l].mlp_norm, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
-    c->launches++;
+    if (!fnorm && !(g_skip & SKIP_NORM))
+      launch_rmsnorm(c->x, M, c->H, c->lw[l].mlp_norm, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
+    c->launches += fnorm ? 0 : 1;
     if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
     e = base_epi(c, M);
     e.kind = EPI_SILU;
@@ -394,11 +446,13 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     e.act_xs = c->actxs;
     e.act_nt = NT;
     if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
+    const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
     e = base_epi(c, M);
     e.kind = EPI_RESID;
+    if (fnorm) e = resid_norm(nextg);
     if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
-    const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
-    if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
+    if (fnorm) {
+    } else if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
       launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
       c->launches++;
       if ((s = check_launch(c, "rmsnorm")) != SS_OK) return s;
@@ -489,6 +543,94 @@ ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
   return SS_OK;
 }
 
+// one launch of the persistent draft pass over frontier nodes [base, base + M)
+ss_status launch_fused_pass(ss_ctx* c, int M, int base, int child_base, int child_depth, int k, float T, int skip_topk,
+                            unsigned long long* trace) {
+  ss_status s;
+  PassParams p{};
+  p.ph = c->d_phases;
+  p.n_ph = int(c->phases.size());
+  p.M = M;
+  p.NT = gemv_nt(M);
+  p.node_base = base;
+  p.H = c->H;
+  p.eps = c->cfg.rms_eps;
+  p.x = c->x;
+  p.sumsq = c->sumsq;
+  p.tok = c->tok;
+  p.embed = c->embed;
+  p.partials = c->pass_part;
+  p.tile_ctr = c->gv_cnt;
+  p.max_seg = 1;
+  for (const auto& ph : c->phases)
+    if (ph.kind == PH_GEMV) p.max_seg = std::max(p.max_seg, pass_max_segments(ph.N, ph.K, c->pass_grid));
+  p.bar = c->pass_bar;
+  p.stages = c->pass_stages;
+  AttnParams& a = p.attn;
+  a.q = c->qbuf;
+  a.k_cache = c->kc;
+  a.v_cache = c->vc;
+  a.k_tree = c->kt;
+  a.v_tree = c->vt;
+  a.committed_len = c->committed_len;
+  a.anc = c->anc;
+  a.depth = c->depth;
+  a.anc_stride = c->anc_stride;
+  a.max_ctx = c->C;
+  a.max_nodes = c->max_nodes;
+  a.n_heads = c->nh;
+  a.n_kv = c->nkv;
+  a.head_dim = c->d;
+  a.split = c->split_draft;
+  a.n_seg_max = c->at_seg_max;
+  a.part_o = c->at_o;
+  a.part_ml = c->at_ml;
+  a.out_fragx = c->attnfrag;
+  a.out_xs = c->attnxs;
+  p.kc_layer = c->kc_layer;
+  p.kt_layer = c->kt_layer;
+  p.attn_ctr = c->attn_ctr;
+  TopkParams& t = p.topk;
+  t.logits = c->logits;
+  t.M = M;
+  t.V = c->V;
+  t.k = k;
+  t.inv_t = float(1.0 / double(T));
+  t.blocks_per_row = std::max(1, std::min(64, c->pass_grid / M));
+  t.blk_max = c->tk_max;
+  t.blk_sum = c->tk_sum;
+  t.blk_val = c->tk_val;
+  t.blk_idx = c->tk_idx;
+  t.tok = c->tok;
+  t.parent = c->parent;
+  t.depth = c->depth;
+  t.score = c->score;
+  t.anc = c->anc;
+  t.anc_stride = c->anc_stride;
+  t.node_base = base;
+  t.child_base = child_base;
+  t.child_depth = child_depth;
+  p.trace = trace;
+  p.skip_topk = skip_topk;
+  CK(cudaMemsetAsync(c->pass_bar, 0, 4, c->cs));
+  launch_draft_pass(p, c->pass_grid, c->d, c->cs);
+  c->launches++;
+  return check_launch(c, "draft_pass");
+}
+
+ss_status draft_loop_fused(ss_ctx* c, int D, int k, float T) {
+  ss_status s;
+  launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, false, c->cs);
+  c->launches++;
+  if ((s = check_launch(c, "tree_init")) != SS_OK) return s;
+  for (int dd = 0; dd < D; ++dd) {
+    const int M = dd == 0 ? 1 : k;
+    const int base = dd == 0 ? 0 : 1 + (dd - 1) * k;
+    if ((s = launch_fused_pass(c, M, base, 1 + dd * k, dd + 1, k, T, 0, nullptr)) != SS_OK) return s;
+  }
+  return SS_OK;
+}
+
 ss_status run_draft(ss_ctx* c, int D, int k, float T) {
   uint32_t tb;
   std::memcpy(&tb, &T, 4);
@@ -498,14 +640,14 @@ ss_status run_draft(ss_ctx* c, int D, int k, float T) {
     if (it == c->graphs.end()) {
       // first use: run eagerly (sets kernel attributes), then capture for later steps
       const int64_t l0 = c->launches;
-      ss_status s = draft_loop(c, D, k, T);
+      ss_status s = c->use_fused ? draft_loop_fused(c, D, k, T) : draft_loop(c, D, k, T);
       if (s != SS_OK) return s;
       const int64_t nl = c->launches - l0;
       cudaGraph_t g = nullptr;
       if (cudaStreamBeginCapture(c->cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
         c->capturing = true;
         const int64_t lsave = c->launches;
-        ss_status s2 = draft_loop(c, D, k, T);
+        ss_status s2 = c->use_fused ? draft_loop_fused(c, D, k, T) : draft_loop(c, D, k, T);
         c->launches = lsave;
         c->capturing = false;
         cudaError_t e = cudaStreamEndCapture(c->cs, &g);
@@ -530,7 +672,7 @@ ss_status run_draft(ss_ctx* c, int D, int k, float T) {
     c->launches += c->graph_launches[key];
     return SS_OK;
   }
-  return draft_loop(c, D, k, T);
+  return c->use_fused ? draft_loop_fused(c, D, k, T) : draft_loop(c, D, k, T);
 }
 
 ss_status do_verify(ss_ctx* c) {
@@ -684,6 +826,10 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->actxs = (float*)chk(A(size_t(c->mpad_max) * (c->F / 64) * 4));
   c->logits = (float*)chk(A(size_t(32) * c->V * 4));
   c->tracebuf = (unsigned long long*)chk(A(size_t(512) * 8 * 8));
+  c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
+  c->pass_bar = (unsigned*)chk(A(256));
+  c->attn_ctr = (int*)chk(A(size_t(32) * c->nkv * 4));
+  c->norm_ctr = (int*)chk(A(64));
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32
   size_t gvf = 0;
@@ -777,7 +923,9 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
         w.q4[g] = (uint8_t*)c->ar.alloc(q4_bytes(c->gN[g], c->gK[g]), 1024);
     }
   }
-  c->ring_bytes = (c->ar.cap - c->ar.used - 4096) / 4096 * 4096;
+  // the staging ring takes what is left after the fused-pass tables (reserved here, see below)
+  const size_t pass_reserve = size_t(64) << 20;
+  c->ring_bytes = (c->ar.cap - c->ar.used - pass_reserve - 4096) / 4096 * 4096;
   c->ring = (uint8_t*)c->ar.alloc(c->ring_bytes, 4096);
   if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
   // pinned host store for offloaded layers (device layout)
@@ -849,6 +997,107 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
     c->ev_t1.push_back(t1);
   }
   c->ev_pending.assign(c->ev_pool, false);
+  // ---- fused draft pass: phase table, Stream-K partial buffer, launch geometry ----
+  {
+    const char* ev = getenv("SS_FUSED_DRAFT");
+    c->use_fused = ev && ev[0] == '1';
+    const char* pv = getenv("SS_L2_PREFETCH");
+    c->l2_prefetch = pv && pv[0] == '1';
+    const char* fv = getenv("SS_FUSE_NORM");
+    c->fuse_norm = !(fv && fv[0] == '0');
+    const char* av = getenv("SS_ATTN_V2");
+    c->attn_v2 = !(av && av[0] == '0');
+    c->pass_stages = 5;
+    while (c->pass_stages > 2 && pass_smem_bytes(c->d, c->pass_stages) > 227 * 1024) --c->pass_stages;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int maxg = pass_max_grid(c->d, c->pass_stages);
+    c->pass_grid = std::min(sms, maxg);
+    if (c->pass_grid < 1) c->use_fused = false;
+    std::vector<PhaseDesc>& P = c->phases;
+    P.clear();
+    auto base = [&]() {
+      PhaseDesc d{};
+      d.epi = base_epi(c, 1);
+      return d;
+    };
+    PhaseDesc d = base();
+    d.kind = PH_EMBED;
+    P.push_back(d);
+    size_t part_need = 0;
+    auto gemv = [&](const uint8_t* W, int N, int K, bool q4, int xsrc, const uint16_t* gain, const uint16_t* X,
+                    const float* XS, EpiParams epi) {
+      PhaseDesc g = base();
+      g.kind = PH_GEMV;
+      g.W = W;
+      g.N = N;
+      g.K = K;
+      g.q4 = q4 ? 1 : 0;
+      g.xsrc = xsrc;
+      g.gain = gain;
+      g.X = X;
+      g.XSUM = XS;
+      g.epi = epi;
+      P.push_back(g);
+      part_need = std::max(part_need, size_t(N / 128) * pass_max_segments(N, K, c->pass_grid));
+    };
+    for (int l = 0; l < c->L; ++l) {
+      const LayerW& w = c->lw[l];
+      auto Wg = [&](int g) { return (const uint8_t*)(w.resident ? w.bf16[g] : w.q4[g]); };
+      EpiParams q = base_epi(c, 1);
+      q.kind = EPI_QKV;
+      q.bias = w.bias;
+      q.q_out = c->qbuf;
+      q.k_tree = c->kt + l * c->kt_layer;
+      q.v_tree = c->vt + l * c->kt_layer;
+      PhaseDesc nm = base();
+      nm.kind = PH_NORM;
+      nm.gain = w.attn_norm;
+      nm.X = c->hfrag;
+      nm.XSUM = c->hxs;
+      P.push_back(nm);
+      gemv(Wg(0), c->gN[0], c->gK[0], !w.resident, XS_FRAGX, nullptr, c->hfrag, c->hxs, q);
+      PhaseDesc a = base();
+      a.kind = PH_ATTN;
+      a.layer = l;
+      P.push_back(a);
+      a.kind = PH_COMBINE;
+      P.push_back(a);
+      EpiParams r = base_epi(c, 1);
+      r.kind = EPI_RESID_SS;
+      r.sumsq = c->sumsq;
+      gemv(Wg(1), c->gN[1], c->gK[1], !w.resident, XS_FRAGX, nullptr, c->attnfrag, c->attnxs, r);
+      EpiParams u = base_epi(c, 1);
+      u.kind = EPI_SILU;
+      u.act = c->actfrag;
+      u.act_xs = c->actxs;
+      nm.gain = w.mlp_norm;
+      P.push_back(nm);
+      gemv(Wg(2), c->gN[2], c->gK[2], !w.resident, XS_FRAGX, nullptr, c->hfrag, c->hxs, u);
+      gemv(Wg(3), c->gN[3], c->gK[3], !w.resident, XS_FRAGX, nullptr, c->actfrag, c->actxs, r);
+    }
+    EpiParams hd = base_epi(c, 1);
+    hd.kind = EPI_LOGITS;
+    hd.out = c->logits;
+    hd.ldo = c->V;
+    PhaseDesc fn = base();
+    fn.kind = PH_NORM;
+    fn.gain = c->final_norm;
+    fn.X = c->hfrag;
+    fn.XSUM = c->hxs;
+    P.push_back(fn);
+    gemv(c->head, c->V, c->H, false, XS_FRAGX, nullptr, c->hfrag, c->hxs, hd);
+    d = base();
+    d.kind = PH_TOPK1;
+    P.push_back(d);
+    d.kind = PH_TOPK2;
+    P.push_back(d);
+    c->d_phases = (PhaseDesc*)c->ar.alloc(P.size() * sizeof(PhaseDesc));
+    c->pass_part = (float*)c->ar.alloc(part_need * 128 * 32 * 4);
+    if (!c->d_phases || !c->pass_part) return fail(c, SS_ERR_BUDGET, "no room for the fused draft pass tables");
+    CK(cudaMemcpyAsync(c->d_phases, P.data(), P.size() * sizeof(PhaseDesc), cudaMemcpyHostToDevice, c->cs));
+    CK(cudaStreamSynchronize(c->cs));
+  }
   c->st.n_resident = nr;
   c->st.n_offloaded = c->L - nr;
   c->st.host_pinned_bytes = int64_t(c->host_bytes);
@@ -1302,10 +1551,15 @@ ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, 
   g_skip = skip;
   PassOut o;
   o.logits = true;
-  ss_status s = forward_pass(c, false, M, 1, o);   // warm-up
+  const bool fused = c->use_fused && skip == 0;
+  auto one = [&]() {
+    return fused ? launch_fused_pass(c, M, 1, 1 + M, 2, std::min(M, c->lim.max_top_k), 0.2f, 0, nullptr)
+                 : forward_pass(c, false, M, 1, o);
+  };
+  ss_status s = one();   // warm-up
   if (s == SS_OK) {
     CK(cudaEventRecord(c->e0, c->cs));
-    for (int i = 0; i < iters && s == SS_OK; ++i) s = forward_pass(c, false, M, 1, o);
+    for (int i = 0; i < iters && s == SS_OK; ++i) s = one();
     CK(cudaEventRecord(c->e1, c->cs));
   }
   g_skip = 0;
@@ -1336,8 +1590,15 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
   g_trace_cap = cap;
   PassOut o;
   o.logits = true;
-  s = forward_pass(c, false, M, 1, o);
-  const int n = g_trace_n;
+  int n;
+  if (c->use_fused) {
+    s = launch_fused_pass(c, M, 1, 1 + M, 2, std::min(M, c->lim.max_top_k), 0.2f, 0, buf);
+    n = std::min(cap * 4, int(c->phases.size()));   // [phase][start, end] pairs packed 4 per record of 8
+    n = (2 * n + 7) / 8;
+  } else {
+    s = forward_pass(c, false, M, 1, o);
+    n = g_trace_n;
+  }
   g_trace = nullptr;
   if (s != SS_OK) return s;
   CK(cudaMemcpyAsync(init.data(), buf, size_t(n) * 8 * 8, cudaMemcpyDeviceToHost, c->cs));
@@ -1385,7 +1646,8 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
       if (i1 - i0 > 32) return fail(c, SS_ERR_INVALID, "draft debug forward: <= 32 nodes per depth");
       PassOut o;
       o.logits = true;
-      if ((s = forward_pass(c, false, i1 - i0, i0, o)) != SS_OK) return s;
+      s = c->use_fused ? launch_fused_pass(c, i1 - i0, i0, 0, 0, 1, 1.0f, 1, nullptr) : forward_pass(c, false, i1 - i0, i0, o);
+      if (s != SS_OK) return s;
       CK(cudaMemcpyAsync(out_logits + int64_t(i0) * c->V, c->logits, size_t(i1 - i0) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
       CK(cudaStreamSynchronize(c->cs));
       i0 = i1;

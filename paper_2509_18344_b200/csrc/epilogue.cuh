@@ -8,7 +8,7 @@ namespace ss {
 
 // threads [0, nthreads) cooperate; caller syncs before and after.
 SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r, int m0, int ncols, int tid,
-                           int nthreads) {
+                           int nthreads, float* scratch = nullptr) {
   const int row0 = r * kTileRows;
   switch (e.kind) {
     case EPI_QKV: {
@@ -60,6 +60,78 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
         const int mg = m0 + m;
         if (mg >= e.M) continue;
         e.x[int64_t(mg) * e.ldx + row0 + n] += tile[n * ld + m];
+      }
+      break;
+    }
+    case EPI_RESID_NORM:
+    case EPI_RESID_SS: {
+      // x[m, row] += y; then sum over the tile's 128 rows of x_new^2 per token, in a fixed order:
+      // a warp covers 32 consecutive rows of one token -> 4 warp sums per token -> scratch -> ordered add
+      const int nitems = kTileRows * ncols;
+      for (int base = (tid & ~31); base < nitems; base += nthreads) {
+        const int it = base + (tid & 31);
+        const int m = it / kTileRows, n = it % kTileRows;
+        const int mg = m0 + m;
+        float v2 = 0.f;
+        if (it < nitems && mg < e.M) {
+          float* xp = e.x + int64_t(mg) * e.ldx + row0 + n;
+          const float xn = __ldcg(xp) + tile[n * ld + m];
+          *xp = xn;
+          v2 = xn * xn;
+        }
+        const float s = warp_sum(v2);
+        if ((tid & 31) == 0 && it < nitems) scratch[m * 4 + n / 32] = s;
+        __syncwarp();
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+      for (int m = tid; m < ncols; m += nthreads) {
+        const int mg = m0 + m;
+        if (mg < e.M) e.sumsq[int64_t(r) * ncols + mg] = ((scratch[m * 4] + scratch[m * 4 + 1]) + scratch[m * 4 + 2]) + scratch[m * 4 + 3];
+      }
+      if (e.kind != EPI_RESID_NORM) break;
+      // ---- fused RMSNorm: wait for every tile owner, then normalise this tile's 128 columns ----
+      __threadfence();
+      asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+      if (tid == 0) {
+        atomicAdd(&e.norm_ctr[0], 1);
+        unsigned v;
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(e.norm_ctr) : "memory");
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 4000000000ull) __trap();   // watchdog: never hang the GPU
+        } while (int(v) < e.n_tiles);
+        if (atomicAdd(&e.norm_ctr[1], 1) == e.n_tiles - 1) {   // last to leave resets both
+          e.norm_ctr[0] = 0;
+          e.norm_ctr[1] = 0;
+        }
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+      // r_m = 1/sqrt(mean(x_m^2) + eps): per-tile partials in tile order (fixed)
+      for (int m = tid; m < ncols; m += nthreads) {
+        float ssum = 0.f;
+        if (m0 + m < e.M)
+          for (int t = 0; t < e.n_tiles; ++t) ssum += __ldcg(e.sumsq + int64_t(t) * ncols + m0 + m);
+        scratch[m] = 1.0f / sqrtf(ssum / float(e.ldx) + e.eps);
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+      // (token m, group G) pairs: a warp takes 64 columns of one token: 2 per lane, warp sum
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int pr = warp; pr < ncols * 2; pr += nthreads / 32) {
+        const int m = pr >> 1, G = pr & 1;
+        const int mg = m0 + m;
+        float gs = 0.f;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = row0 + 64 * G + 32 * u + lane;
+          uint16_t hb = 0;
+          if (mg < e.M) hb = f2bf(__ldcg(e.x + int64_t(mg) * e.ldx + k) * scratch[m] * bf2f(e.norm_gain[k]));
+          e.norm_out[fragx_offset(mg, k, e.act_nt)] = hb;
+          gs += bf2f(hb);
+        }
+        gs = warp_sum(gs);
+        if (lane == 0) e.norm_xs[int64_t(row0 / 64 + G) * (e.act_nt * 8) + mg] = gs;
       }
       break;
     }

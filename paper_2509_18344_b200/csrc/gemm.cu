@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(const GemmParams 
       const uint8_t* xst = wst + kBF16TileBytes;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 r0 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 0) * 4 + q) * 32 + lane) * 16);
-        const uint4 r1 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 1) * 4 + q) * 32 + lane) * 16);
+        const uint4 r0 = *reinterpret_cast<const uint4*>(wst + bf16_piece_off(warp, 0, q, lane));
+        const uint4 r1 = *reinterpret_cast<const uint4*>(wst + bf16_piece_off(warp, 1, q, lane));
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int st = 2 * q + hh;

@@ -38,7 +38,7 @@ struct GemvCfg {
   static constexpr int kMaxStages = 16;
   static constexpr int kTileFloats = kTileRows * NT * 8;
   // runtime stage count S: ring S*stage + out tile + 2*kMaxStages barriers
-  static constexpr int smem_for(int S) { return S * kStageBytes + kTileFloats * 4 + 2 * kMaxStages * 8 + 64; }
+  static constexpr int smem_for(int S) { return S * kStageBytes + kTileFloats * 4 + 2 * kMaxStages * 8 + 64 + 512; }
 };
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + C::kTileFloats * 4);
   uint64_t* empty = full + C::kMaxStages;
   int* flag = reinterpret_cast<int*>(empty + C::kMaxStages);
+  float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SS_TRACE_MIN(0);
@@ -219,6 +220,17 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
         const int n = w.take(C::kCPS);
         issue_w(i, w, n);
         w.next(nC, n);
+      }
+      // L2 prefetch of the next matrix (independent of every activation): this CTA's slice, in
+      // 64 KB TMA prefetches, so HBM keeps streaming through the dependent steps that follow
+      if (p.pf && p.pf_bytes > 0) {
+        const int64_t per = ((p.pf_bytes / gridDim.x) + 15) & ~int64_t(15);
+        const int64_t b0 = per * blockIdx.x;
+        const int64_t b1 = b0 + per < p.pf_bytes ? b0 + per : p.pf_bytes;
+        for (int64_t o = b0; o < b1; o += 65536) {
+          const int64_t n = b1 - o < 65536 ? b1 - o : 65536;
+          prefetch_l2(p.pf + o, uint32_t(n));
+        }
       }
       griddep_wait();
       SS_TRACE_CTA0(1);
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
       }
       if (crank == 0) {
         named_bar(1, nthr);
-        apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr);
+        apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr, scratch);
         named_bar(1, nthr);
       }
       return;
@@ -361,9 +373,10 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
           const uint4 cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);
           const uint32_t m0 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g) * 4);
           const uint32_t m1 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4);
-          float cg[NT][4];
+          // two independent accumulator chains (even / odd k-steps) for MMA-latency ILP
+          float cg[NT][4], ch[NT][4];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) cg[j][0] = cg[j][1] = cg[j][2] = cg[j][3] = 0.f;
+          for (int j = 0; j < NT; ++j) cg[j][0] = cg[j][1] = cg[j][2] = cg[j][3] = ch[j][0] = ch[j][1] = ch[j][2] = ch[j][3] = 0.f;
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int st = 4 * G + k4;
@@ -376,9 +389,13 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
               const uint2 b = *reinterpret_cast<const uint2*>(xst + (j * 8 + st) * 256);
-              mma_bf16_16816(cg[j], a0, a1, a2, a3, b.x, b.y);
+              mma_bf16_16816((k4 & 1) ? ch[j] : cg[j], a0, a1, a2, a3, b.x, b.y);
             }
           }
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cg[j][q] += ch[j][q];
           // y += s * sum((128 + c) x) + (z - 128 s) * sum(x)      (exact affine dequant, fp32)
           const float s0 = __uint_as_float(m0 << 16), z0 = __uint_as_float(m0 & 0xFFFF0000u);
           const float s1 = __uint_as_float(m1 << 16), z1 = __uint_as_float(m1 & 0xFFFF0000u);
@@ -395,8 +412,8 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint4 r0 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 0) * 4 + q) * 32 + lane) * 16);
-          const uint4 r1 = *reinterpret_cast<const uint4*>(wst + (((warp * 2 + 1) * 4 + q) * 32 + lane) * 16);
+          const uint4 r0 = *reinterpret_cast<const uint4*>(wst + bf16_piece_off(warp, 0, q, lane));
+          const uint4 r1 = *reinterpret_cast<const uint4*>(wst + bf16_piece_off(warp, 1, q, lane));
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int st = 2 * q + hh;
@@ -428,15 +445,24 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
 }
 
 // split factor of the cluster mode: ~one CTA per SM, <= 8 (portable cluster), <= chunks
-int gemv_cluster_split(int N, int K, int sms) {
+int gemv_cluster_split(int N, int K, int sms) {   // ~2 CTAs per SM; <= 16 (non-portable); <= chunks
   const int tiles = N / 128, nC = K / 128;
-  int S = (sms + tiles / 2) / tiles;
+  static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
+  static const int cap = env_int("SS_GEMV_MAX_CLUSTER", 8);
+  int S = (per_sm * sms) / tiles;
   if (S < 1) S = 1;
-  if (S > 8) S = 8;
+  if (S > cap) S = cap;
   if (S > nC) S = nC;
   return S;
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
+// every row tile has its own resident cluster (required by EPI_RESID_NORM's in-kernel barrier)
+bool gemv_tiles_all_resident(int N, int K, int sms) {
+  if (!gemv_use_cluster(N, K, sms)) return false;
+  const int S = gemv_cluster_split(N, K, sms);
+  static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
+  return sms * per_sm / S >= N / 128;
+}
 
 template <bool Q4, int NT, bool kCluster>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
@@ -448,6 +474,7 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
     if (stages < 2) stages = 2;
     if (stages > C::kMaxStages) stages = C::kMaxStages;
     cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(stages));
+    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   GemvParams p = p0;
   p.stages = stages;

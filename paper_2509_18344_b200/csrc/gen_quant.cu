@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) quantize_q4_kernel(const uint8_t* __restr
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 v = *reinterpret_cast<const uint4*>(s_tile + (((warp * 2 + h) * 4 + q) * 32 + lane) * 16);
+        const uint4 v = *reinterpret_cast<const uint4*>(s_tile + bf16_piece_off(warp, h, q, lane));
         const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {

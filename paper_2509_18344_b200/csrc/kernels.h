@@ -5,7 +5,7 @@
 
 namespace ss {
 
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5, EPI_RESID_SS = 6, EPI_RESID_NORM = 7 };
 
 // Epilogue parameters shared by the GEMV (draft, M <= 32) and GEMM (verify) kernels.
 struct EpiParams {
@@ -31,6 +31,16 @@ struct EpiParams {
   // EPI_LOGITS / EPI_STORE
   float* out;                    // [M x ldo]
   int ldo;
+  // EPI_RESID_SS: residual add + per-tile sum of squares of the new x rows (for the fused RMSNorm)
+  float* sumsq;                  // [N/128][Mpad]
+  // EPI_RESID_NORM (cluster GEMV only): + in-kernel barrier of the tile owners, then the owner of
+  // tile r writes h = bf16(x * r_m * gain) for columns [128 r, 128 r + 128) in FragX + group sums
+  const uint16_t* norm_gain;
+  uint16_t* norm_out;
+  float* norm_xs;
+  int* norm_ctr;                 // [2] arrive / depart counters, zero between launches
+  int n_tiles;
+  float eps;
   // EPI_ARGMAX: per (token, row tile) partial (max, idx, second max)
   float* am_val;                 // [M x n_tiles]
   int* am_idx;
@@ -47,11 +57,14 @@ struct GemvParams {
   int* counters;                 // [n_tiles], zero on entry, restored to zero on exit
   int max_seg;
   int stages;                    // ring depth (set by the launcher)
+  const uint8_t* pf;             // weights of the NEXT matrix: prefetched into L2 while this one runs
+  int64_t pf_bytes;
   unsigned long long* trace;     // optional %globaltimer trace: [8] events of this launch (debug)
   EpiParams epi;
 };
 
 int gemv_max_segments(int N, int K, int grid);
+bool gemv_tiles_all_resident(int N, int K, int sms);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
 
 struct GemmParams {
@@ -148,6 +161,49 @@ struct AcceptParams {
   int chain;                     // 1: commit all nodes (prefill chunk), ignore argmax
 };
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st);
+
+// ---- persistent draft pass (pass.cu) -------------------------------------------------------
+enum PhaseKind { PH_EMBED = 0, PH_GEMV = 1, PH_ATTN = 2, PH_TOPK1 = 3, PH_TOPK2 = 4, PH_NORM = 5, PH_COMBINE = 6 };
+enum XSrc { XS_NORM = 0, XS_FRAGX = 1 };
+struct PhaseDesc {
+  int kind;
+  // PH_GEMV
+  const uint8_t* W;
+  int N, K, q4;
+  int xsrc;                      // XS_NORM: h = bf16(x * r(sumsq) * gain); XS_FRAGX: X/XSUM given
+  const uint16_t* gain;
+  const uint16_t* X;
+  const float* XSUM;
+  EpiParams epi;                 // M / node_base / act_nt are patched per pass
+  // PH_ATTN
+  int layer;
+};
+struct PassParams {
+  const PhaseDesc* ph;
+  int n_ph;
+  int M, NT, node_base;
+  int H;
+  float eps;
+  float* x;                      // [Mpad x H] fp32 residual stream
+  float* sumsq;                  // [H/128][Mpad] per-tile sums of squares of x
+  const int* tok;
+  const uint16_t* embed;
+  float* partials;               // Stream-K partial tiles
+  int* tile_ctr;                 // per-tile arrival counters (zero between phases)
+  int max_seg;                   // partial slots per tile (host: max over phases of pass_max_segments)
+  unsigned* bar;                 // grid barrier counter (zeroed before each launch)
+  int stages;
+  AttnParams attn;               // layer 0 pointers; + layer * stride
+  int64_t kc_layer, kt_layer;
+  int* attn_ctr;                 // [Mpad * n_kv] segment-arrival counters
+  TopkParams topk;
+  unsigned long long* trace;     // optional: per-phase %globaltimer (CTA 0), [n_ph][2]
+  int skip_topk;                 // debug: logits only, leave the tree untouched
+};
+int pass_smem_bytes(int head_dim, int stages);
+void launch_draft_pass(const PassParams& p, int grid, int head_dim, cudaStream_t st);
+int pass_max_grid(int head_dim, int stages);
+int pass_max_segments(int N, int K, int grid);
 
 // tree init for a new step: root node (slot 0) with token *root_tok, depth 0
 void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,
