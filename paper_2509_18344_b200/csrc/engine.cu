@@ -74,6 +74,7 @@ struct ss_ctx {
   int gN[4] = {0}, gK[4] = {0};
   // weights
   uint16_t* embed = nullptr;
+  uint16_t* h_embed = nullptr;   // embedding in mapped pinned host memory (zero-copy row gather)
   uint8_t* head = nullptr;
   uint16_t* final_norm = nullptr;
   std::vector<LayerW> lw;
@@ -792,7 +793,22 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   auto A = [&](size_t bytes) { return a.alloc(bytes); };
   bool ok = true;
   auto chk = [&](void* p) { ok = ok && p != nullptr; return p; };
-  c->embed = (uint16_t*)chk(A(size_t(c->V) * c->H * 2));
+  // The embedding is only ever gathered (<= max_nodes rows per pass): keep it in mapped, portable
+  // pinned host memory and read rows over PCIe (zero-copy), which leaves its 2*V*H bytes of the VRAM
+  // cap to the streaming ring.  SS_EMBED_HOST=0 keeps it in the arena (P:534 default placement).
+  {
+    const char* ev = getenv("SS_EMBED_HOST");
+    if (!(ev && ev[0] == '0') &&
+        cudaHostAlloc(&c->h_embed, size_t(c->V) * c->H * 2, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+      void* dptr = nullptr;
+      cudaHostGetDevicePointer(&dptr, c->h_embed, 0);
+      c->embed = reinterpret_cast<uint16_t*>(dptr);
+    } else {
+      cudaGetLastError();
+      c->h_embed = nullptr;
+      c->embed = (uint16_t*)chk(A(size_t(c->V) * c->H * 2));
+    }
+  }
   c->head = (uint8_t*)chk(A(bf16_bytes(c->V, c->H)));
   c->final_norm = (uint16_t*)chk(A(size_t(c->H) * 2));
   c->lw.resize(c->L);
@@ -942,7 +958,16 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
   }
   // generation (tensor ids: SURVEY O.1 / synth/weights.py)
   const double H = c->H;
-  launch_gen_natural(c->embed, tensor_key(seed, 0), uint64_t(c->V) * c->H, scale_c32(1.0), 0, c->cs);
+  if (c->h_embed) {   // generate on the device (ring scratch), then place in the host copy
+    const size_t eb = size_t(c->V) * c->H * 2;
+    if (eb > c->ring_bytes) return fail(c, SS_ERR_BUDGET, "staging ring smaller than the embedding");
+    launch_gen_natural(reinterpret_cast<uint16_t*>(c->ring), tensor_key(seed, 0), uint64_t(c->V) * c->H, scale_c32(1.0),
+                       0, c->cs);
+    CK(cudaMemcpyAsync(c->h_embed, c->ring, eb, cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaStreamSynchronize(c->cs));
+  } else {
+    launch_gen_natural(c->embed, tensor_key(seed, 0), uint64_t(c->V) * c->H, scale_c32(1.0), 0, c->cs);
+  }
   launch_gen_tiled(c->head, tensor_key(seed, 2 + 16 * c->L), c->V, c->H, scale_c32(1.0 / std::sqrt(H)), 0, 0, c->cs);
   launch_gen_natural(c->final_norm, tensor_key(seed, 1 + 16 * c->L), c->H, scale_c32(0.05), 1, c->cs);
   for (int l = 0; l < c->L; ++l) {
@@ -1100,7 +1125,7 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
   }
   c->st.n_resident = nr;
   c->st.n_offloaded = c->L - nr;
-  c->st.host_pinned_bytes = int64_t(c->host_bytes);
+  c->st.host_pinned_bytes = int64_t(c->host_bytes) + (c->h_embed ? int64_t(c->V) * c->H * 2 : 0);
   c->st.ring_bytes = int64_t(c->ring_bytes);
   c->st.arena_used = int64_t(c->ar.used);
   c->st.substitute_bytes = int64_t(size_t(c->L - nr) * layer_q4);
@@ -1330,6 +1355,7 @@ void ss_destroy(ss_ctx* c) {
   for (auto e : {c->e0, c->e1, c->e2, c->e3})
     if (e) cudaEventDestroy(e);
   if (c->host) cudaFreeHost(c->host);
+  if (c->h_embed) cudaFreeHost(c->h_embed);
   if (c->h_out) cudaFreeHost(c->h_out);
   cudaGetLastError();
   delete c;

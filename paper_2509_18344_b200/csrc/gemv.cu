@@ -27,6 +27,9 @@ namespace ss {
 
 constexpr int kGemvConsumerWarps = 8;
 constexpr int kGemvThreads = (kGemvConsumerWarps + 1) * 32;
+#ifndef SS_GEMV_MIN_BLOCKS
+#define SS_GEMV_MIN_BLOCKS 2
+#endif
 
 template <bool Q4, int NT>
 struct GemvCfg {
@@ -165,7 +168,7 @@ SS_DEV Work make_work(int N, int K, uint32_t crank, uint32_t csize) {
 }
 
 template <bool Q4, int NT, bool kCluster>
-__global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(const GemvParams p) {
   using C = GemvCfg<Q4, NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int kStages = p.stages;
