@@ -166,9 +166,10 @@ ss_status ss_debug_time_matmul(ss_ctx* ctx, int32_t which, int32_t layer, int32_
  * over `iters` eager launches.  skip: bit mask of kernel classes left out (1 attention, 2 RMSNorm,
  * 4 dequant-GEMVs, 8 head) — attribution only; results are not meaningful when skip != 0. */
 ss_status ss_debug_time_pass(ss_ctx* ctx, int32_t M, int32_t iters, int32_t skip, float* out_ms);
-/* One traced draft pass: each dequant-GEMV launch records 8 %globaltimer events (ns) into
- * out[8*i .. 8*i+7] (entry, producer/consumer dependency release, first data, loop end, flush,
- * kernel end, loop end max); *out_n = number of launches traced (<= cap). */
+/* One traced draft pass: each dequant-GEMV launch records 16 %globaltimer events (ns) into
+ * out[16*i .. 16*i+15] (0 entry, 1/2 producer/consumer dependency release, 3 first data, 4 loop end,
+ * 5 flush, 6 kernel end, 7 loop end max, 8 cluster reduction done, 9-12 residual / norm barrier /
+ * norm scale / epilogue done; unused events 0); *out_n = number of launches traced (<= cap, <= 512). */
 ss_status ss_debug_trace_pass(ss_ctx* ctx, int32_t M, int64_t* out, int32_t cap, int32_t* out_n);
 
 #ifdef __cplusplus

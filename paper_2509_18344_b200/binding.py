@@ -274,10 +274,10 @@ class SubSpec:
         return ms.value
 
     def debug_trace_pass(self, M, cap=256):
-        out = np.zeros(cap * 8, np.int64)
+        out = np.zeros(cap * 16, np.int64)
         n = c_int32()
         self._check(self.lib.ss_debug_trace_pass(self.ctx, M, _ptr(out), cap, ctypes.byref(n)))
-        return out[: n.value * 8].reshape(n.value, 8)
+        return out[: n.value * 16].reshape(n.value, 16)
 
     def debug_time_matmul(self, layer, group, M, iters=20):
         ms = c_float()

@@ -16,6 +16,7 @@ constexpr int kQ4MetaBytes = 1024;  // 128 rows x 2 groups x (s,z) bf16
 constexpr int kQ4TileBytes = kQ4CodeBytes + kQ4MetaBytes;   // 9216
 constexpr int kBF16TileBytes = kTileRows * kChunkK * 2;     // 32768
 constexpr int kXChunkBytesPerNT = 8 * kChunkK * 2;          // 2048: 8 tokens x 128 k bf16
+constexpr int kTraceEvents = 16;   // u64 %globaltimer events per traced launch (debug)
 
 // ---------------------------------------------------------------------------
 // Weight "tiled fragment" layout.

@@ -96,7 +96,7 @@ struct ss_ctx {
   uint16_t *hfrag = nullptr, *attnfrag = nullptr, *actfrag = nullptr, *qbuf = nullptr;
   float *hxs = nullptr, *attnxs = nullptr, *actxs = nullptr;   // group sums of the FragX inputs
   float* logits = nullptr;
-  unsigned long long* tracebuf = nullptr;   // debug: %globaltimer events [512][8]
+  unsigned long long* tracebuf = nullptr;   // debug: %globaltimer events [512][kTraceEvents]
   int mpad_max = 0;
   float2* rope = nullptr;
   // gemv scratch
@@ -138,7 +138,7 @@ struct ss_ctx {
   float *sumsq = nullptr, *pass_part = nullptr;
   unsigned* pass_bar = nullptr;
   int* attn_ctr = nullptr;
-  int* norm_ctr = nullptr;
+  unsigned long long* norm_ctr = nullptr;
   bool fuse_norm = true;
   int pass_grid = 0, pass_stages = 0;
   // graphs
@@ -281,7 +281,7 @@ struct PassOut {
 };
 // debug timing only (ss_debug_time_pass): skip kernel classes to attribute pass time
 int g_skip = 0;
-unsigned long long* g_trace = nullptr;   // device buffer [launch][8] for ss_debug_trace_pass
+unsigned long long* g_trace = nullptr;   // device buffer [launch][kTraceEvents] for ss_debug_trace_pass
 int g_trace_n = 0, g_trace_cap = 0;
 enum { SKIP_ATTN = 1, SKIP_NORM = 2, SKIP_GEMV = 4, SKIP_HEAD = 8 };
 
@@ -323,7 +323,7 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = epi;
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
-    if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + 8 * (g_trace_n++);
+    if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
     c->launches++;
     return check_launch(c, "gemv");
@@ -418,16 +418,21 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     c->launches += c->attn_v2 ? 1 : 2;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
     const bool fnorm = !target && c->fuse_norm && !(g_skip & SKIP_NORM) &&
-                       gemv_tiles_all_resident(c->gN[1], c->gK[1], c->gv_grid) &&
-                       gemv_tiles_all_resident(c->gN[3], c->gK[3], c->gv_grid);
-    auto resid_norm = [&](const uint16_t* gain) {
+                       gemv_tiles_all_resident(true, NT, c->gN[1], c->gK[1], c->gv_grid) &&
+                       gemv_tiles_all_resident(true, NT, c->gN[3], c->gK[3], c->gv_grid) &&
+                       (c->n_resident == 0 || (gemv_tiles_all_resident(false, NT, c->gN[1], c->gK[1], c->gv_grid) &&
+                                               gemv_tiles_all_resident(false, NT, c->gN[3], c->gK[3], c->gv_grid)));
+    // one monotonic barrier counter per (matrix, weight format, NT): every launch on a counter has
+    // the same number of arrivals (tiles x cluster size), so generations stay aligned
+    auto resid_norm = [&](const uint16_t* gain, int which) {
       EpiParams r = base_epi(c, M);
       r.kind = EPI_RESID_NORM;
       r.sumsq = c->sumsq;
+      r.sumsq_ld = NT * 8;
       r.norm_gain = gain;
       r.norm_out = c->hfrag;
       r.norm_xs = c->hxs;
-      r.norm_ctr = c->norm_ctr;
+      r.norm_ctr = c->norm_ctr + (which * 2 + (c->lw[l].resident ? 1 : 0)) * 3 + (NT == 1 ? 0 : NT == 2 ? 1 : 2);
       r.n_tiles = c->H / 128;
       r.eps = eps;
       r.act_nt = NT;
@@ -435,7 +440,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     };
     e = base_epi(c, M);
     e.kind = EPI_RESID;
-    if (fnorm) e = resid_norm(c->lw[l].mlp_norm);
+    if (fnorm) e = resid_norm(c->lw[l].mlp_norm, 0);
     if ((s = matmul(c, target, l, 1, c->attnfrag, M, e)) != SS_OK) return s;
     if (!fnorm && !(g_skip & SKIP_NORM))
       launch_rmsnorm(c->x, M, c->H, c->lw[l].mlp_norm, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
@@ -450,7 +455,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
     e = base_epi(c, M);
     e.kind = EPI_RESID;
-    if (fnorm) e = resid_norm(nextg);
+    if (fnorm) e = resid_norm(nextg, 1);
     if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
     if (fnorm) {
     } else if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
@@ -841,11 +846,11 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->attnxs = (float*)chk(A(size_t(c->mpad_max) * (c->qd / 64) * 4));
   c->actxs = (float*)chk(A(size_t(c->mpad_max) * (c->F / 64) * 4));
   c->logits = (float*)chk(A(size_t(32) * c->V * 4));
-  c->tracebuf = (unsigned long long*)chk(A(size_t(512) * 8 * 8));
+  c->tracebuf = (unsigned long long*)chk(A(size_t(512) * kTraceEvents * 8));
   c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
   c->pass_bar = (unsigned*)chk(A(256));
   c->attn_ctr = (int*)chk(A(size_t(32) * c->nkv * 4));
-  c->norm_ctr = (int*)chk(A(64));
+  c->norm_ctr = (unsigned long long*)chk(A(128));   // 12 monotonic counters, zeroed below
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32
   size_t gvf = 0;
@@ -1030,6 +1035,8 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
     c->l2_prefetch = pv && pv[0] == '1';
     const char* fv = getenv("SS_FUSE_NORM");
     c->fuse_norm = !(fv && fv[0] == '0');
+    const char* gv = getenv("SS_GRAPHS");
+    if (gv && gv[0] == '0') c->use_graphs = false;
     const char* av = getenv("SS_ATTN_V2");
     c->attn_v2 = !(av && av[0] == '0');
     c->pass_stages = 5;
@@ -1090,7 +1097,7 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
       P.push_back(a);
       EpiParams r = base_epi(c, 1);
       r.kind = EPI_RESID_SS;
-      r.sumsq = c->sumsq;
+      r.sumsq = c->sumsq;   // sumsq_ld = 0: the pass kernel's tile stride (Mpad)
       gemv(Wg(1), c->gN[1], c->gK[1], !w.resident, XS_FRAGX, nullptr, c->attnfrag, c->attnxs, r);
       EpiParams u = base_epi(c, 1);
       u.kind = EPI_SILU;
@@ -1604,10 +1611,11 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
   float ms = 0.f;
   ss_status s = ss_debug_time_pass(c, M, 1, 0, &ms);   // sets up the frontier + warm-up
   if (s != SS_OK) return s;
-  std::vector<unsigned long long> init(size_t(cap) * 8);
-  for (int i = 0; i < cap; ++i)
-    for (int j = 0; j < 8; ++j) init[size_t(i) * 8 + j] = (j == 0) ? ~0ull : 0ull;
   if (cap > 512) cap = 512;
+  constexpr int E = kTraceEvents;
+  std::vector<unsigned long long> init(size_t(cap) * E);
+  for (int i = 0; i < cap; ++i)
+    for (int j = 0; j < E; ++j) init[size_t(i) * E + j] = (j == 0) ? ~0ull : 0ull;
   unsigned long long* buf = c->tracebuf;
   CK(cudaMemcpyAsync(buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c->cs));
   CK(cudaStreamSynchronize(c->cs));
@@ -1619,17 +1627,17 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
   int n;
   if (c->use_fused) {
     s = launch_fused_pass(c, M, 1, 1 + M, 2, std::min(M, c->lim.max_top_k), 0.2f, 0, buf);
-    n = std::min(cap * 4, int(c->phases.size()));   // [phase][start, end] pairs packed 4 per record of 8
-    n = (2 * n + 7) / 8;
+    n = std::min(cap * E / 2, int(c->phases.size()));   // [phase][start, end] pairs packed E/2 per record
+    n = (2 * n + E - 1) / E;
   } else {
     s = forward_pass(c, false, M, 1, o);
     n = g_trace_n;
   }
   g_trace = nullptr;
   if (s != SS_OK) return s;
-  CK(cudaMemcpyAsync(init.data(), buf, size_t(n) * 8 * 8, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaMemcpyAsync(init.data(), buf, size_t(n) * E * 8, cudaMemcpyDeviceToHost, c->cs));
   CK(cudaStreamSynchronize(c->cs));
-  std::memcpy(out, init.data(), size_t(n) * 8 * 8);
+  std::memcpy(out, init.data(), size_t(n) * E * 8);
   *out_n = n;
   return SS_OK;
 }

@@ -6,9 +6,23 @@
 
 namespace ss {
 
-// threads [0, nthreads) cooperate; caller syncs before and after.
+// threads [0, nthreads) cooperate; caller syncs before and after.  Token columns [m0, m0 + ncols)
+// of the tile are processed (a cluster GEMV splits a tile's tokens over its ranks).  EPI_RESID_NORM:
+// every call arrives once at the norm barrier, which completes after n_tiles * arrive_per_tile
+// arrivals; the norm_wait caller of a tile then writes the normalised activations of tokens
+// [0, norm_ncols).
 SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r, int m0, int ncols, int tid,
-                           int nthreads, float* scratch = nullptr) {
+                           int nthreads, float* scratch = nullptr, unsigned long long* trace = nullptr,
+                           int arrive_per_tile = 1, bool norm_wait = true, int norm_ncols = 0) {
+  // debug trace (max over CTAs of %globaltimer): 9 residual stored, 10 norm barrier passed,
+  // 11 r computed, 12 epilogue done
+  auto tr = [&](int ev) {
+    if (trace && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(&trace[ev], t);
+    }
+  };
   const int row0 = r * kTileRows;
   switch (e.kind) {
     case EPI_QKV: {
@@ -67,6 +81,7 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
     case EPI_RESID_SS: {
       // x[m, row] += y; then sum over the tile's 128 rows of x_new^2 per token, in a fixed order:
       // a warp covers 32 consecutive rows of one token -> 4 warp sums per token -> scratch -> ordered add
+      const int64_t ssld = e.sumsq_ld > 0 ? e.sumsq_ld : ld;
       const int nitems = kTileRows * ncols;
       for (int base = (tid & ~31); base < nitems; base += nthreads) {
         const int it = base + (tid & 31);
@@ -86,53 +101,74 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
       asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
       for (int m = tid; m < ncols; m += nthreads) {
         const int mg = m0 + m;
-        if (mg < e.M) e.sumsq[int64_t(r) * ncols + mg] = ((scratch[m * 4] + scratch[m * 4 + 1]) + scratch[m * 4 + 2]) + scratch[m * 4 + 3];
+        if (mg < e.M) e.sumsq[int64_t(r) * ssld + mg] = ((scratch[m * 4] + scratch[m * 4 + 1]) + scratch[m * 4 + 2]) + scratch[m * 4 + 3];
       }
+      tr(9);
       if (e.kind != EPI_RESID_NORM) break;
-      // ---- fused RMSNorm: wait for every tile owner, then normalise this tile's 128 columns ----
-      __threadfence();
+      // ---- fused RMSNorm ----
+      // Every caller arrives at a barrier on a monotonic 64-bit counter (release add; never reset);
+      // only the norm_wait caller of each tile (one CTA per tile, so the waiters are few enough to be
+      // co-resident) spins until the counter reaches this launch's generation, then normalises the
+      // tile's 128 columns for all norm_ncols tokens.
       asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
       if (tid == 0) {
-        atomicAdd(&e.norm_ctr[0], 1);
-        unsigned v;
-        unsigned long long t0, t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(e.norm_ctr) : "memory");
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-          if (t1 - t0 > 4000000000ull) __trap();   // watchdog: never hang the GPU
-        } while (int(v) < e.n_tiles);
-        if (atomicAdd(&e.norm_ctr[1], 1) == e.n_tiles - 1) {   // last to leave resets both
-          e.norm_ctr[0] = 0;
-          e.norm_ctr[1] = 0;
+        const unsigned long long n_arr = (unsigned long long)e.n_tiles * (unsigned long long)arrive_per_tile;
+        unsigned long long old, v;
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(e.norm_ctr) : "memory");
+        if (norm_wait) {
+          const unsigned long long target = (old / n_arr + 1) * n_arr;
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e.norm_ctr) : "memory");
+            if (v >= target) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 4000000000ull) __trap();   // watchdog: never hang the GPU
+          }
         }
       }
+      if (!norm_wait) break;
       asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
-      // r_m = 1/sqrt(mean(x_m^2) + eps): per-tile partials in tile order (fixed)
-      for (int m = tid; m < ncols; m += nthreads) {
+      tr(10);
+      const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
+      const int nn = norm_ncols > 0 ? norm_ncols : m0 + ncols;   // tokens [0, nn)
+      const int npairs = nn * 2;   // (token, 64-group) pairs; a warp takes 64 columns of one token
+      float xv[8][2];                      // x_new prefetched for this warp's pairs (<= 8 per warp)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int pr = warp + i * nwarps, m = pr >> 1, G = pr & 1;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          xv[i][u] = (pr < npairs && m < e.M) ? __ldcg(e.x + int64_t(m) * e.ldx + row0 + 64 * G + 32 * u + lane) : 0.f;
+      }
+      // r_m = 1/sqrt(mean(x_m^2) + eps): warp m loads the per-tile partials (lane t, t + 32, ...) and
+      // reduces them with a fixed shuffle tree (independent of M)
+      for (int m = warp; m < nn; m += nwarps) {
         float ssum = 0.f;
-        if (m0 + m < e.M)
-          for (int t = 0; t < e.n_tiles; ++t) ssum += __ldcg(e.sumsq + int64_t(t) * ncols + m0 + m);
-        scratch[m] = 1.0f / sqrtf(ssum / float(e.ldx) + e.eps);
+        if (m < e.M)
+          for (int t = lane; t < e.n_tiles; t += 32) ssum += __ldcg(e.sumsq + int64_t(t) * ssld + m);
+        ssum = warp_sum(ssum);
+        if (lane == 0) scratch[m] = 1.0f / sqrtf(ssum / float(e.ldx) + e.eps);
       }
       asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
-      // (token m, group G) pairs: a warp takes 64 columns of one token: 2 per lane, warp sum
-      const int warp = tid >> 5, lane = tid & 31;
-      for (int pr = warp; pr < ncols * 2; pr += nthreads / 32) {
-        const int m = pr >> 1, G = pr & 1;
-        const int mg = m0 + m;
+      tr(11);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int pr = warp + i * nwarps, m = pr >> 1, G = pr & 1;
+        if (pr >= npairs) break;
         float gs = 0.f;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int k = row0 + 64 * G + 32 * u + lane;
           uint16_t hb = 0;
-          if (mg < e.M) hb = f2bf(__ldcg(e.x + int64_t(mg) * e.ldx + k) * scratch[m] * bf2f(e.norm_gain[k]));
-          e.norm_out[fragx_offset(mg, k, e.act_nt)] = hb;
+          if (m < e.M) hb = f2bf(xv[i][u] * scratch[m] * bf2f(e.norm_gain[k]));
+          e.norm_out[fragx_offset(m, k, e.act_nt)] = hb;
           gs += bf2f(hb);
         }
         gs = warp_sum(gs);
-        if (lane == 0) e.norm_xs[int64_t(row0 / 64 + G) * (e.act_nt * 8) + mg] = gs;
+        if (lane == 0) e.norm_xs[int64_t(row0 / 64 + G) * (e.act_nt * 8) + m] = gs;
       }
+      tr(12);
       break;
     }
     case EPI_SILU: {

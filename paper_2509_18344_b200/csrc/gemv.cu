@@ -23,10 +23,15 @@
 #include "epilogue.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+
 namespace ss {
 
 constexpr int kGemvConsumerWarps = 8;
 constexpr int kGemvThreads = (kGemvConsumerWarps + 1) * 32;
+constexpr int kGemvMaxCluster = 8;   // portable cluster size; the split factor never exceeds it
 #ifndef SS_GEMV_MIN_BLOCKS
 #define SS_GEMV_MIN_BLOCKS 2
 #endif
@@ -40,8 +45,13 @@ struct GemvCfg {
   static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
   static constexpr int kMaxStages = 16;
   static constexpr int kTileFloats = kTileRows * NT * 8;
-  // runtime stage count S: ring S*stage + out tile + 2*kMaxStages barriers
-  static constexpr int smem_for(int S) { return S * kStageBytes + kTileFloats * 4 + 2 * kMaxStages * 8 + 64 + 512; }
+  // cluster reduction staging: [S][ceil(Mpad/S)][128] fp32 partial columns pushed by the ranks,
+  // S <= kGemvMaxCluster -> at most (Mpad + kGemvMaxCluster - 1) x 128 floats
+  static constexpr int kStagingFloats = (NT * 8 + kGemvMaxCluster - 1) * kTileRows;
+  // runtime stage count S: ring S*stage + out tile + staging + 2*kMaxStages barriers
+  static constexpr int smem_for(int S) {
+    return S * kStageBytes + kTileFloats * 4 + kStagingFloats * 4 + 2 * kMaxStages * 8 + 64 + 512;
+  }
 };
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -73,7 +83,8 @@ SS_DEV unsigned long long gtime() {
 }
 // trace events: 0 first CTA entry (min), 1 producer dep-wait done (CTA 0), 2 consumer dep-wait done
 // (CTA 0), 3 first stage arrived (CTA 0), 4 main loop done (CTA 0), 5 last flush start (CTA 0),
-// 6 kernel end (max over CTAs), 7 main loop done (max over CTAs)
+// 6 kernel end (max over CTAs), 7 main loop done (max over CTAs), 8 cluster reduction done (max),
+// 9..12 epilogue steps (see apply_epilogue), 13..15 spare; a record is kTraceEvents u64
 #define SS_TRACE_MIN(ev) do { if (p.trace) atomicMin(&p.trace[ev], gtime()); } while (0)
 #define SS_TRACE_MAX(ev) do { if (p.trace) atomicMax(&p.trace[ev], gtime()); } while (0)
 #define SS_TRACE_CTA0(ev) do { if (p.trace && blockIdx.x == 0) p.trace[ev] = gtime(); } while (0)
@@ -101,6 +112,19 @@ SS_DEV uint32_t cluster_count_x() {
 }
 SS_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+SS_DEV float ld_dsmem_f32(const float* local, uint32_t rank) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra));
+  return v;
+}
+SS_DEV void st_dsmem_f32x4(float* local, uint32_t rank, float4 v) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ra), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 SS_DEV float4 ld_dsmem_f32x4(const float* local, uint32_t rank) {
   uint32_t a = smem_u32(local), ra;
@@ -174,7 +198,8 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   const int kStages = p.stages;
   uint8_t* ring = smem;
   float* otile = reinterpret_cast<float*>(smem + kStages * C::kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + C::kTileFloats * 4);
+  float* staging = otile + C::kTileFloats;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + (C::kTileFloats + C::kStagingFloats) * 4);
   uint64_t* empty = full + C::kMaxStages;
   int* flag = reinterpret_cast<int*>(empty + C::kMaxStages);
   float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
@@ -262,7 +287,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         const int64_t tiles = per ? w.left / per : 0;
         for (int64_t t = 0; t < tiles; ++t) {
           cluster_sync_all();
-          cluster_sync_all();
+          if (t + 1 < tiles) cluster_sync_all();
         }
       }
     }
@@ -288,31 +313,54 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
     }
   };
 
-  auto flush = [&](int r, int c_first, int c_last) {
+  auto flush = [&](int r, int c_first, int c_last, bool last) {
     if constexpr (kCluster) {
-      stash(otile);
-      if (csize > 1) {
-        cluster_sync_all();                       // partial tiles of all ranks visible cluster-wide
-        if (crank == 0) {
-          for (int e = threadIdx.x * 4; e < kTileRows * Mpad; e += nthr * 4) {
-            float4 v = *reinterpret_cast<float4*>(otile + e);
-            for (uint32_t q = 1; q < csize; ++q) {
-              const float4 o = ld_dsmem_f32x4(otile + e, q);
-              v.x += o.x;
-              v.y += o.y;
-              v.z += o.z;
-              v.w += o.w;
-            }
-            *reinterpret_cast<float4*>(otile + e) = v;
-          }
-        }
-        cluster_sync_all();                       // peers reuse/exit only after rank 0 read them
-      }
-      if (crank == 0) {
+      if (csize == 1) {
+        stash(otile);
         named_bar(1, nthr);
-        apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr, scratch);
+        if (threadIdx.x == 0) SS_TRACE_MAX(8);
+        apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr, scratch, p.trace, 1, true, Mpad);
         named_bar(1, nthr);
+        return;
       }
+      // Split-K reduction spread over the cluster: rank q owns token columns [mlo, mhi) of the tile.
+      // Every rank stashes its partial tile token-major, pushes each owner's columns into the owner's
+      // staging buffer with 16-byte distributed-shared-memory stores, and after ONE cluster barrier
+      // each owner sums its staging in rank order (deterministic) and runs the epilogue for its
+      // tokens (one arrival per rank at EPI_RESID_NORM's barrier; only rank 0 waits there and
+      // normalises, so ranks 1..S-1 exit and the barrier never needs whole clusters co-resident).
+      const int S = int(csize);
+      const int mlo = int(crank) * Mpad / S, mhi = int(crank + 1) * Mpad / S;
+      const int nc = mhi - mlo, ncmax = (Mpad + S - 1) / S;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
+        const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
+        otile[m * kTileRows + n0] = acc[j][0];
+        otile[(m + 1) * kTileRows + n0] = acc[j][1];
+        otile[m * kTileRows + n0 + 8] = acc[j][2];
+        otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+      }
+      named_bar(1, nthr);
+      for (int i = threadIdx.x; i < Mpad * (kTileRows / 4); i += nthr) {
+        const int m = i / (kTileRows / 4), n4 = (i % (kTileRows / 4)) * 4;
+        const int q = int(owner_of(m, Mpad, S));          // owner rank of token m
+        const int mm = m - q * Mpad / S;
+        st_dsmem_f32x4(staging + (crank * ncmax + mm) * kTileRows + n4, uint32_t(q),
+                       *reinterpret_cast<const float4*>(otile + m * kTileRows + n4));
+      }
+      cluster_sync_all();                         // every push landed (release / acquire)
+      for (int it = threadIdx.x; it < kTileRows * nc; it += nthr) {
+        const int n = it % kTileRows, mm = it / kTileRows;
+        float v = staging[mm * kTileRows + n];
+        for (int q = 1; q < S; ++q) v += staging[(q * ncmax + mm) * kTileRows + n];
+        otile[n * nc + mm] = v;                   // [128][nc] for the epilogue
+      }
+      if (!last) cluster_sync_all();              // staging is reused by the next tile's pushes
+      named_bar(1, nthr);
+      if (threadIdx.x == 0) SS_TRACE_MAX(8);
+      apply_epilogue(p.epi, otile, nc, r, mlo, nc, threadIdx.x, nthr, scratch, p.trace, S, crank == 0, Mpad);
+      named_bar(1, nthr);
       return;
     } else {
       const bool complete = (c_first == 0 && c_last == nC - 1);
@@ -355,7 +403,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
   while (w.left > 0) {
     if (w.r != cur_r) {
-      flush(cur_r, c_first, c_last);
+      flush(cur_r, c_first, c_last, false);
       cur_r = w.r;
       c_first = w.c;
     }
@@ -443,15 +491,15 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
     SS_TRACE_CTA0(4);
     SS_TRACE_MAX(7);
   }
-  if (n_items > 0) flush(cur_r, c_first, c_last);   // the last tile of this CTA
+  if (n_items > 0) flush(cur_r, c_first, c_last, true);   // the last tile of this CTA
   if (threadIdx.x == 0) SS_TRACE_MAX(6);
 }
 
-// split factor of the cluster mode: ~one CTA per SM, <= 8 (portable cluster), <= chunks
-int gemv_cluster_split(int N, int K, int sms) {   // ~2 CTAs per SM; <= 16 (non-portable); <= chunks
+// split factor of the cluster mode: ~2 CTAs per SM, <= SS_GEMV_MAX_CLUSTER, <= chunks
+int gemv_cluster_split(int N, int K, int sms) {
   const int tiles = N / 128, nC = K / 128;
   static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
-  static const int cap = env_int("SS_GEMV_MAX_CLUSTER", 8);
+  static const int cap = std::min(env_int("SS_GEMV_MAX_CLUSTER", 8), kGemvMaxCluster);
   int S = (per_sm * sms) / tiles;
   if (S < 1) S = 1;
   if (S > cap) S = cap;
@@ -459,26 +507,91 @@ int gemv_cluster_split(int N, int K, int sms) {   // ~2 CTAs per SM; <= 16 (non-
   return S;
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
-// every row tile has its own resident cluster (required by EPI_RESID_NORM's in-kernel barrier)
-bool gemv_tiles_all_resident(int N, int K, int sms) {
-  if (!gemv_use_cluster(N, K, sms)) return false;
-  const int S = gemv_cluster_split(N, K, sms);
+
+template <bool Q4, int NT, bool kCluster>
+static int ensure_attrs() {   // ring stages for this instantiation; sets the smem/cluster attributes once
+  using C = GemvCfg<Q4, NT>;
+  static int stages = 0;
+  if (!stages) {
+    const int budget = env_int("SS_GEMV_RING_KB", 88) * 1024;
+    int st = budget / C::kStageBytes;
+    if (st < 2) st = 2;
+    if (st > C::kMaxStages) st = C::kMaxStages;
+    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
+    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    stages = st;
+  }
+  return stages;
+}
+
+// Cluster plan {S, clusters}: the GPC structure caps how many clusters of S CTAs are resident at
+// once (e.g. 33 clusters of 8 at 2 CTAs/SM, below qkv's 36 row tiles), and a tile whose cluster is
+// not resident waits for a second wave.  Take the largest S <= gemv_cluster_split whose resident
+// cluster count covers every row tile (queried with cudaOccupancyMaxActiveClusters).
+struct ClusterPlan {
+  int S, ncl;
+  bool all_resident;
+};
+template <bool Q4, int NT>
+static ClusterPlan cluster_plan(int N, int K, int sms) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, ClusterPlan> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(N, K);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  using C = GemvCfg<Q4, NT>;
+  const int stages = ensure_attrs<Q4, NT, true>();
+  const int tiles = N / 128;
   static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
-  return sms * per_sm / S >= N / 128;
+  const int S0 = gemv_cluster_split(N, K, sms);
+  ClusterPlan plan{S0, 0, false};
+  for (int S = S0; S >= 1; --S) {
+    int ncl = sms * per_sm / S;
+    if (ncl > tiles) ncl = tiles;
+    if (ncl < 1) ncl = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncl * S);
+    cfg.blockDim = dim3(kGemvThreads);
+    cfg.dynamicSmemBytes = C::smem_for(stages);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = S;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      active = ncl;   // cannot query: keep the arithmetic plan
+    }
+    if (S == S0) plan = ClusterPlan{S0, active < ncl ? active : ncl, active >= tiles};
+    if (active >= tiles) {
+      plan = ClusterPlan{S, tiles, true};
+      break;
+    }
+  }
+  if (plan.ncl < 1) plan.ncl = 1;
+  cache[key] = plan;
+  return plan;
+}
+
+// every row tile has its own resident cluster (required by EPI_RESID_NORM's in-kernel barrier)
+bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms) {
+  if (!gemv_use_cluster(N, K, sms)) return false;
+  switch (NT) {
+    case 1: return q4 ? cluster_plan<true, 1>(N, K, sms).all_resident : cluster_plan<false, 1>(N, K, sms).all_resident;
+    case 2: return q4 ? cluster_plan<true, 2>(N, K, sms).all_resident : cluster_plan<false, 2>(N, K, sms).all_resident;
+    case 4: return q4 ? cluster_plan<true, 4>(N, K, sms).all_resident : cluster_plan<false, 4>(N, K, sms).all_resident;
+    default: return false;
+  }
 }
 
 template <bool Q4, int NT, bool kCluster>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
   using C = GemvCfg<Q4, NT>;
-  static int stages = 0;
-  if (!stages) {
-    const int budget = env_int("SS_GEMV_RING_KB", 88) * 1024;
-    stages = budget / C::kStageBytes;
-    if (stages < 2) stages = 2;
-    if (stages > C::kMaxStages) stages = C::kMaxStages;
-    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(stages));
-    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  }
+  const int stages = ensure_attrs<Q4, NT, kCluster>();
   GemvParams p = p0;
   p.stages = stages;
   cudaLaunchConfig_t cfg = {};
@@ -508,13 +621,8 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
 template <bool Q4, int NT>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
   if (gemv_use_cluster(p.N, p.K, sms)) {
-    const int S = gemv_cluster_split(p.N, p.K, sms);
-    const int tiles = p.N / 128;
-    static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
-    int ncl = sms * per_sm / S;
-    if (ncl > tiles) ncl = tiles;
-    if (ncl < 1) ncl = 1;
-    launch_t<Q4, NT, true>(p, ncl * S, S, pdl, st);
+    const ClusterPlan pl = cluster_plan<Q4, NT>(p.N, p.K, sms);
+    launch_t<Q4, NT, true>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {
     launch_t<Q4, NT, false>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);
   }

@@ -32,13 +32,14 @@ struct EpiParams {
   float* out;                    // [M x ldo]
   int ldo;
   // EPI_RESID_SS: residual add + per-tile sum of squares of the new x rows (for the fused RMSNorm)
-  float* sumsq;                  // [N/128][Mpad]
+  float* sumsq;                  // [N/128][sumsq_ld]
+  int sumsq_ld;                  // Mpad; 0 = the caller's tile stride
   // EPI_RESID_NORM (cluster GEMV only): + in-kernel barrier of the tile owners, then the owner of
   // tile r writes h = bf16(x * r_m * gain) for columns [128 r, 128 r + 128) in FragX + group sums
   const uint16_t* norm_gain;
   uint16_t* norm_out;
   float* norm_xs;
-  int* norm_ctr;                 // [2] arrive / depart counters, zero between launches
+  unsigned long long* norm_ctr;  // monotonic arrival counter of the norm barrier (zero at creation)
   int n_tiles;
   float eps;
   // EPI_ARGMAX: per (token, row tile) partial (max, idx, second max)
@@ -59,12 +60,12 @@ struct GemvParams {
   int stages;                    // ring depth (set by the launcher)
   const uint8_t* pf;             // weights of the NEXT matrix: prefetched into L2 while this one runs
   int64_t pf_bytes;
-  unsigned long long* trace;     // optional %globaltimer trace: [8] events of this launch (debug)
+  unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
   EpiParams epi;
 };
 
 int gemv_max_segments(int N, int K, int grid);
-bool gemv_tiles_all_resident(int N, int K, int sms);
+bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
 
 struct GemmParams {

@@ -19,3 +19,5 @@ for i, r in enumerate(tr[:12]):
     gap = "" if prev_end is None else f" gap_from_prev_end={rel[0] - prev_end:6.2f}"
     print(f"{names[i % 4]:8s} " + " ".join(f"{v:6.2f}" for v in rel[[0, 1, 2, 3, 4, 7, 6]]) + gap)
     prev_end = rel[6]
+    if r[8]:
+        print("         epilogue: reduce %.2f resid %.2f barrier %.2f r %.2f done %.2f" % tuple((r[8:13] - t0) / 1e3))
