@@ -139,6 +139,8 @@ struct ss_ctx {
   unsigned* pass_bar = nullptr;
   int* attn_ctr = nullptr;
   unsigned long long* norm_ctr = nullptr;
+  int* mlp_flags = nullptr;   // fused MLP: per gate_up tile flags + exit counter
+  bool fuse_mlp = false;
   bool fuse_norm = true;
   int pass_grid = 0, pass_stages = 0;
   // graphs
@@ -451,12 +453,50 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     e.act = c->actfrag;
     e.act_xs = c->actxs;
     e.act_nt = NT;
-    if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
     const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
-    e = base_epi(c, M);
-    e.kind = EPI_RESID;
-    if (fnorm) e = resid_norm(nextg, 1);
-    if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
+    const int mgrid = (!target && c->fuse_mlp && !(g_skip & SKIP_GEMV)) ? mlp_grid(!c->lw[l].resident, NT, c->gv_grid) : 0;
+    if (mgrid > 0) {
+      // gate_up + down in one persistent launch (mlp.cu)
+      MlpParams mp{};
+      const LayerW& w = c->lw[l];
+      mp.Wgu = w.resident ? w.bf16[2] : w.q4[2];
+      mp.Wd = w.resident ? w.bf16[3] : w.q4[3];
+      mp.Xh = c->hfrag;
+      mp.XSh = c->hxs;
+      mp.Xa = c->actfrag;
+      mp.XSa = c->actxs;
+      mp.H = c->H;
+      mp.F = c->F;
+      mp.NT = NT;
+      mp.partials = c->gv_part;
+      mp.counters = c->gv_cnt;
+      mp.max_seg = gemv_max_segments(c->H, c->F, mgrid);
+      mp.flags = c->mlp_flags;
+      mp.exit_ctr = c->mlp_flags + 32 * (2 * c->F / 128);
+      mp.epi_gu = e;
+      static const int mlp_dbg = getenv("SS_MLP_DBG") ? atoi(getenv("SS_MLP_DBG")) : 0;
+      mp.dbg = mlp_dbg;
+      EpiParams d = base_epi(c, M);
+      d.kind = EPI_RESID;
+      if (fnorm) d = resid_norm(nextg, 2);
+      mp.epi_d = d;
+      if (g_trace && g_trace_n < g_trace_cap) mp.trace = g_trace + kTraceEvents * (g_trace_n++);
+      launch_mlp(!w.resident, mp, mgrid, c->use_pdl, c->cs);
+      c->launches++;
+      if ((s = check_launch(c, "mlp")) != SS_OK) return s;
+      if (mlp_dbg & 2) {   // debug: phase A only, down through the GEMV kernel
+        EpiParams d2 = base_epi(c, M);
+        d2.kind = EPI_RESID;
+        if (fnorm) d2 = resid_norm(nextg, 1);
+        if ((s = matmul(c, target, l, 3, c->actfrag, M, d2)) != SS_OK) return s;
+      }
+    } else {
+      if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
+      e = base_epi(c, M);
+      e.kind = EPI_RESID;
+      if (fnorm) e = resid_norm(nextg, 1);
+      if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
+    }
     if (fnorm) {
     } else if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
       launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
@@ -850,7 +890,8 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
   c->pass_bar = (unsigned*)chk(A(256));
   c->attn_ctr = (int*)chk(A(size_t(32) * c->nkv * 4));
-  c->norm_ctr = (unsigned long long*)chk(A(128));   // 12 monotonic counters, zeroed below
+  c->norm_ctr = (unsigned long long*)chk(A(256));   // 18 monotonic counters, zeroed below
+  c->mlp_flags = (int*)chk(A(size_t(2 * c->F / 128 + 1) * 32 * 4));
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32
   size_t gvf = 0;
@@ -860,6 +901,8 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
     gvf = std::max(gvf, size_t(N / 128) * gemv_max_segments(N, K, c->gv_grid) * 128 * 32);
     max_tiles = std::max(max_tiles, N / 128);
   }
+  // the fused MLP's down phase runs Stream-K over up to 2 CTAs per SM
+  gvf = std::max(gvf, size_t(c->H / 128) * gemv_max_segments(c->H, c->F, 2 * c->gv_grid) * 128 * 32);
   c->gv_part_floats = gvf;
   c->gv_part = (float*)chk(A(gvf * 4));
   c->gv_cnt = (int*)chk(A(size_t(max_tiles) * 4));
@@ -1035,6 +1078,8 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
     c->l2_prefetch = pv && pv[0] == '1';
     const char* fv = getenv("SS_FUSE_NORM");
     c->fuse_norm = !(fv && fv[0] == '0');
+    const char* mv = getenv("SS_FUSE_MLP");   // opt-in: measured slower than the two GEMVs
+    c->fuse_mlp = mv && mv[0] == '1';
     const char* gv = getenv("SS_GRAPHS");
     if (gv && gv[0] == '0') c->use_graphs = false;
     const char* av = getenv("SS_ATTN_V2");

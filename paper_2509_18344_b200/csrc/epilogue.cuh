@@ -6,6 +6,79 @@
 
 namespace ss {
 
+// Fused RMSNorm, second half: wait until the norm barrier counter reaches `target` (all tiles'
+// residual rows and sums of squares are published), then write h = bf16(x * r_m * gain) for the
+// 128 columns of tile r and tokens [0, nn) in FragX, plus the 64-group sums.  Threads [0, nthreads)
+// cooperate; scratch needs 32 floats (scratch[126..127] must stay untouched).
+SS_DEV void norm_finish(const EpiParams& e, int r, unsigned long long target, int nn, int ssld_tile, int tid,
+                        int nthreads, float* scratch, unsigned long long* trace) {
+  const int row0 = r * kTileRows;
+  const int64_t ssld = e.sumsq_ld > 0 ? e.sumsq_ld : ssld_tile;
+  if (tid == 0) {
+    unsigned long long v, t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e.norm_ctr) : "memory");
+      if (v >= target) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 4000000000ull) __trap();   // watchdog: never hang the GPU
+    }
+  }
+  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+  if (trace && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&trace[10], t);
+  }
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
+  const int npairs = nn * 2;   // (token, 64-group) pairs; a warp takes 64 columns of one token
+  float xv[8][2];              // x_new prefetched for this warp's pairs (<= 8 per warp)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int pr = warp + i * nwarps, m = pr >> 1, G = pr & 1;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      xv[i][u] = (pr < npairs && m < e.M) ? __ldcg(e.x + int64_t(m) * e.ldx + row0 + 64 * G + 32 * u + lane) : 0.f;
+  }
+  // r_m = 1/sqrt(mean(x_m^2) + eps): warp m loads the per-tile partials (lane t, t + 32, ...) and
+  // reduces them with a fixed shuffle tree (independent of M)
+  for (int m = warp; m < nn; m += nwarps) {
+    float ssum = 0.f;
+    if (m < e.M)
+      for (int t = lane; t < e.n_tiles; t += 32) ssum += __ldcg(e.sumsq + int64_t(t) * ssld + m);
+    ssum = warp_sum(ssum);
+    if (lane == 0) scratch[m] = 1.0f / sqrtf(ssum / float(e.ldx) + e.eps);
+  }
+  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+  if (trace && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&trace[11], t);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int pr = warp + i * nwarps, m = pr >> 1, G = pr & 1;
+    if (pr >= npairs) break;
+    float gs = 0.f;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = row0 + 64 * G + 32 * u + lane;
+      uint16_t hb = 0;
+      if (m < e.M) hb = f2bf(xv[i][u] * scratch[m] * bf2f(e.norm_gain[k]));
+      e.norm_out[fragx_offset(m, k, e.act_nt)] = hb;
+      gs += bf2f(hb);
+    }
+    gs = warp_sum(gs);
+    if (lane == 0) e.norm_xs[int64_t(row0 / 64 + G) * (e.act_nt * 8) + m] = gs;
+  }
+  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");   // scratch is reused by the caller
+  if (trace && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&trace[12], t);
+  }
+}
+
 // threads [0, nthreads) cooperate; caller syncs before and after.  Token columns [m0, m0 + ncols)
 // of the tile are processed (a cluster GEMV splits a tile's tokens over its ranks).  EPI_RESID_NORM:
 // every call arrives once at the norm barrier, which completes after n_tiles * arrive_per_tile
@@ -13,7 +86,8 @@ namespace ss {
 // [0, norm_ncols).
 SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r, int m0, int ncols, int tid,
                            int nthreads, float* scratch = nullptr, unsigned long long* trace = nullptr,
-                           int arrive_per_tile = 1, bool norm_wait = true, int norm_ncols = 0) {
+                           int arrive_per_tile = 1, bool norm_wait = true, int norm_ncols = 0,
+                           unsigned long long* arrive_target = nullptr) {
   // debug trace (max over CTAs of %globaltimer): 9 residual stored, 10 norm barrier passed,
   // 11 r computed, 12 epilogue done
   auto tr = [&](int ev) {
@@ -106,69 +180,24 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
       tr(9);
       if (e.kind != EPI_RESID_NORM) break;
       // ---- fused RMSNorm ----
-      // Every caller arrives at a barrier on a monotonic 64-bit counter (release add; never reset);
-      // only the norm_wait caller of each tile (one CTA per tile, so the waiters are few enough to be
-      // co-resident) spins until the counter reaches this launch's generation, then normalises the
-      // tile's 128 columns for all norm_ncols tokens.
+      // Every caller arrives at a barrier on a monotonic 64-bit counter (release add; never reset).
+      // The norm_wait caller of each tile (one CTA per tile, so the waiters are few enough to be
+      // co-resident) then waits for this launch's generation and normalises the tile's 128 columns
+      // (norm_finish); a caller that still has other work passes norm_wait = false, keeps the
+      // generation target (*arrive_target) and calls norm_finish itself later.
       asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
       if (tid == 0) {
         const unsigned long long n_arr = (unsigned long long)e.n_tiles * (unsigned long long)arrive_per_tile;
-        unsigned long long old, v;
+        unsigned long long old;
         asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(e.norm_ctr) : "memory");
-        if (norm_wait) {
-          const unsigned long long target = (old / n_arr + 1) * n_arr;
-          unsigned long long t0, t1;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          for (;;) {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e.norm_ctr) : "memory");
-            if (v >= target) break;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 4000000000ull) __trap();   // watchdog: never hang the GPU
-          }
-        }
+        const unsigned long long target = (old / n_arr + 1) * n_arr;
+        if (arrive_target) *arrive_target = target;
+        reinterpret_cast<unsigned long long*>(scratch)[63] = target;   // scratch[126..127]
       }
       if (!norm_wait) break;
       asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
-      tr(10);
-      const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
-      const int nn = norm_ncols > 0 ? norm_ncols : m0 + ncols;   // tokens [0, nn)
-      const int npairs = nn * 2;   // (token, 64-group) pairs; a warp takes 64 columns of one token
-      float xv[8][2];                      // x_new prefetched for this warp's pairs (<= 8 per warp)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int pr = warp + i * nwarps, m = pr >> 1, G = pr & 1;
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          xv[i][u] = (pr < npairs && m < e.M) ? __ldcg(e.x + int64_t(m) * e.ldx + row0 + 64 * G + 32 * u + lane) : 0.f;
-      }
-      // r_m = 1/sqrt(mean(x_m^2) + eps): warp m loads the per-tile partials (lane t, t + 32, ...) and
-      // reduces them with a fixed shuffle tree (independent of M)
-      for (int m = warp; m < nn; m += nwarps) {
-        float ssum = 0.f;
-        if (m < e.M)
-          for (int t = lane; t < e.n_tiles; t += 32) ssum += __ldcg(e.sumsq + int64_t(t) * ssld + m);
-        ssum = warp_sum(ssum);
-        if (lane == 0) scratch[m] = 1.0f / sqrtf(ssum / float(e.ldx) + e.eps);
-      }
-      asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
-      tr(11);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int pr = warp + i * nwarps, m = pr >> 1, G = pr & 1;
-        if (pr >= npairs) break;
-        float gs = 0.f;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k = row0 + 64 * G + 32 * u + lane;
-          uint16_t hb = 0;
-          if (m < e.M) hb = f2bf(xv[i][u] * scratch[m] * bf2f(e.norm_gain[k]));
-          e.norm_out[fragx_offset(m, k, e.act_nt)] = hb;
-          gs += bf2f(hb);
-        }
-        gs = warp_sum(gs);
-        if (lane == 0) e.norm_xs[int64_t(row0 / 64 + G) * (e.act_nt * 8) + m] = gs;
-      }
-      tr(12);
+      norm_finish(e, r, reinterpret_cast<unsigned long long*>(scratch)[63], norm_ncols > 0 ? norm_ncols : m0 + ncols, ld, tid,
+                  nthreads, scratch, trace);
       break;
     }
     case EPI_SILU: {

@@ -68,6 +68,30 @@ int gemv_max_segments(int N, int K, int grid);
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
 
+// Fused draft MLP of one layer (mlp.cu): gate_up (EPI_SILU) then down (epi_d) in one persistent
+// launch; down's K-chunks wait on per-gate_up-tile flags instead of a kernel boundary.
+struct MlpParams {
+  const uint8_t* Wgu;            // tiled weights [2F x H] (gate/up interleaved per 64 rows)
+  const uint8_t* Wd;             // tiled weights [H x F]
+  const uint16_t* Xh;            // FragX of the normed hidden state [Mpad x H]
+  const float* XSh;              // its group sums [H/64][Mpad]
+  const uint16_t* Xa;            // FragX of the activations [Mpad x F] (written by phase A)
+  const float* XSa;              // their group sums [F/64][Mpad]
+  int H, F, NT;
+  float* partials;               // down Stream-K partial tiles [H/128][max_seg][128*Mpad]
+  int* counters;                 // [H/128], zero on entry, restored to zero on exit
+  int max_seg;
+  int* flags;                    // [2F/128][32] gate_up tile done flags (one per 128 B), zero on entry, reset on exit
+  int* exit_ctr;                 // [1], zero on entry, reset on exit
+  int stages;                    // ring depth (set by the launcher)
+  unsigned long long* trace;     // optional [kTraceEvents] (debug)
+  int dbg;                       // debug bits: 1 phase B waits for every gate_up tile; 2 phase A only;
+                                 // 4 phase B only; 8 L2-prefetch phase B weights during phase A
+  EpiParams epi_gu, epi_d;
+};
+int mlp_grid(bool q4, int NT, int sms);   // all-resident persistent grid (0: unsupported)
+void launch_mlp(bool q4, const MlpParams& p, int grid, bool pdl, cudaStream_t st);
+
 struct GemmParams {
   const uint8_t* W;              // tiled BF16 weights [N x K]
   const uint16_t* X;             // FragX [Mpad x K], Mpad % 128 == 0

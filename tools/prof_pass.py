@@ -11,13 +11,15 @@ for name, skip in (("full", 0), ("-attn", 1), ("-norm", 2), ("-gemv", 4), ("-hea
     print(f"{name:16s} {ss.debug_time_pass(6, 5, skip) * 1e3:9.1f} us/pass", flush=True)
 tr = ss.debug_trace_pass(6).astype("float64")
 t0 = tr[:, 0].min()
-names = ["qkv", "o", "gate_up", "down"]
+names = ["qkv", "o", "gate_up", "down"] if os.environ.get("SS_FUSE_MLP") == "0" else ["qkv", "o", "mlp"]
 print("launch  entry  pdep  cdep  first  loop0  loopmax  end   (us, rel. to first entry)")
 prev_end = None
-for i, r in enumerate(tr[:12]):
+for i, r in enumerate(tr[:3 * len(names)]):
     rel = (r - t0) / 1e3
     gap = "" if prev_end is None else f" gap_from_prev_end={rel[0] - prev_end:6.2f}"
-    print(f"{names[i % 4]:8s} " + " ".join(f"{v:6.2f}" for v in rel[[0, 1, 2, 3, 4, 7, 6]]) + gap)
+    print(f"{names[i % len(names)]:8s} " + " ".join(f"{v:6.2f}" for v in rel[[0, 1, 2, 3, 4, 7, 6]]) + gap)
     prev_end = rel[6]
+    if names[i % len(names)] == "mlp":
+        print("         mlp: A-done0 %.2f A-donemax %.2f B-first0 %.2f B-loopmax %.2f fin-epi %.2f end %.2f" % tuple((r[[4, 7, 3, 5, 8, 6]] - t0) / 1e3))
     if r[8]:
         print("         epilogue: reduce %.2f resid %.2f barrier %.2f r %.2f done %.2f" % tuple((r[8:13] - t0) / 1e3))
