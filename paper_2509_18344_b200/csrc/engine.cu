@@ -106,6 +106,7 @@ struct ss_ctx {
   size_t gv_part_floats = 0;
   // attention scratch
   float *at_o = nullptr, *at_ml = nullptr;
+  size_t at_o_floats = 0;
   int* at_cnt = nullptr;
   int at_seg_max = 0;
   int split_draft = 32, split_target = 128;
@@ -907,7 +908,17 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->gv_part = (float*)chk(A(gvf * 4));
   c->gv_cnt = (int*)chk(A(size_t(max_tiles) * 4));
   c->at_seg_max = (c->C + std::min(c->split_draft, c->split_target) - 1) / std::min(c->split_draft, c->split_target);
-  c->at_o = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d * 4));
+  {
+    // split-attention partials are only needed by the legacy two-kernel attention (SS_ATTN_V2=0)
+    // and the fused pass; otherwise the buffer is just the debug-matmul output scratch
+    const char* av = getenv("SS_ATTN_V2");
+    const char* fv = getenv("SS_FUSED_DRAFT");
+    const bool legacy = (av && av[0] == '0') || (fv && fv[0] == '1');
+    size_t need = std::max(size_t(c->mpad_max) * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
+    if (legacy) need = std::max(need, size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d);
+    c->at_o_floats = need;
+    c->at_o = (float*)chk(A(need * 4));
+  }
   c->at_ml = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * 2 * 4));
   c->at_cnt = (int*)chk(A(size_t(c->nkv) * ((c->max_nodes + 7) / 8) * 4));
   c->tk_max = (float*)chk(A(size_t(32) * 296 * 4));
@@ -1170,8 +1181,11 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
     d.kind = PH_TOPK2;
     P.push_back(d);
     c->d_phases = (PhaseDesc*)c->ar.alloc(P.size() * sizeof(PhaseDesc));
-    c->pass_part = (float*)c->ar.alloc(part_need * 128 * 32 * 4);
-    if (!c->d_phases || !c->pass_part) return fail(c, SS_ERR_BUDGET, "no room for the fused draft pass tables");
+    // the persistent pass's Stream-K partials (tens of MB) only when it is enabled: otherwise that
+    // VRAM belongs to the streaming ring
+    c->pass_part = c->use_fused ? (float*)c->ar.alloc(part_need * 128 * 32 * 4) : nullptr;
+    if (!c->d_phases || (c->use_fused && !c->pass_part))
+      return fail(c, SS_ERR_BUDGET, "no room for the fused draft pass tables");
     CK(cudaMemcpyAsync(c->d_phases, P.data(), P.size() * sizeof(PhaseDesc), cudaMemcpyHostToDevice, c->cs));
     CK(cudaStreamSynchronize(c->cs));
   }
@@ -1516,8 +1530,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
   CK(cudaMemcpyAsync(X, fx.data(), fx.size() * 2, cudaMemcpyHostToDevice, c->cs));
   if (which == 0) CK(cudaMemcpyAsync(XS, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice, c->cs));
   float* Y = c->at_o;   // debug output scratch: the attention partial buffer
-  if (size_t(M) * N > size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d)
-    return fail(c, SS_ERR_BUDGET, "debug_matmul: output too large");
+  if (size_t(M) * N > c->at_o_floats) return fail(c, SS_ERR_BUDGET, "debug_matmul: output too large");
   EpiParams e = base_epi(c, M);
   e.kind = EPI_STORE;
   e.out = Y;
