@@ -171,6 +171,10 @@ ss_status ss_debug_time_pass(ss_ctx* ctx, int32_t M, int32_t iters, int32_t skip
  * 5 flush, 6 kernel end, 7 loop end max, 8 cluster reduction done, 9-12 residual / norm barrier /
  * norm scale / epilogue done; unused events 0); *out_n = number of launches traced (<= cap, <= 512). */
 ss_status ss_debug_trace_pass(ss_ctx* ctx, int32_t M, int64_t* out, int32_t cap, int32_t* out_n);
+/* One draft pass (non-fused) with a per-CTA trace of its `launch`-th dequant-GEMV launch (0 = layer
+ * 0 qkv, 1 = layer 0 o, ...): out[5*i .. 5*i+4] = (SM id, entry, first data, main loop end, end) of
+ * CTA i, %globaltimer ns; *out_n = CTAs recorded (<= cap <= 1638). */
+ss_status ss_debug_cta_trace(ss_ctx* ctx, int32_t M, int32_t launch, int64_t* out, int32_t cap, int32_t* out_n);
 
 #ifdef __cplusplus
 }

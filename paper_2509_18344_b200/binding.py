@@ -70,6 +70,7 @@ _FUNCS = {
     "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_time_pass": [c_void_p, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_trace_pass": [c_void_p, c_int32, c_void_p, c_int32, P(c_int32)],
+    "ss_debug_cta_trace": [c_void_p, c_int32, c_int32, c_void_p, c_int32, P(c_int32)],
 }
 EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy"]
 
@@ -278,6 +279,12 @@ class SubSpec:
         n = c_int32()
         self._check(self.lib.ss_debug_trace_pass(self.ctx, M, _ptr(out), cap, ctypes.byref(n)))
         return out[: n.value * 16].reshape(n.value, 16)
+
+    def debug_cta_trace(self, M, launch, cap=1024):
+        out = np.zeros(cap * 5, np.int64)
+        n = c_int32()
+        self._check(self.lib.ss_debug_cta_trace(self.ctx, M, launch, _ptr(out), cap, ctypes.byref(n)))
+        return out[: n.value * 5].reshape(n.value, 5)
 
     def debug_time_matmul(self, layer, group, M, iters=20):
         ms = c_float()

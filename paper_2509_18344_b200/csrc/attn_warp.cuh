@@ -264,14 +264,16 @@ SS_DEV void attn_task(const AttnParams& p, int P, int kvh, int seg, int qi, uint
 }
 
 // ---------------------------------------------------------------------------------------------
-// K3 v2: CTA per (kv head, query node); warp w processes the node's logical 16-key tiles
-// t = w, w+8, w+16, ... (online softmax, tensor-core QK^T / PV), then the 8 per-warp partials are
-// merged in shared memory in warp order (fixed).  No split across CTAs, no combine kernel.  The
-// reduction order depends only on the node's logical key count, so a node's output is bitwise the
-// same in a tree (verify) and as an AR step (batch invariance).
-// smem: 8 warps x 2 buffers x (K, V) x 16 x (D+8) bf16 + merge area 8 x 16 x (D+2) fp32.
+// K3 v2: a cluster of S CTAs per (kv head, query node); warp w of rank q processes the node's logical
+// 16-key tiles t = w + 8q, w + 8q + 8S, ... (online softmax, tensor-core QK^T / PV).  Each CTA merges
+// its 8 per-warp partials in shared memory in warp order, then rank q finalises head rows q, q + S, ...
+// by merging the S rank partials read through distributed shared memory in rank order (fixed).  No
+// combine kernel.  The reduction order depends only on the node's logical key count (S is fixed), so
+// a node's output is bitwise the same in a tree (verify) and as an AR step (batch invariance).
+// smem: 8 warps x 2 buffers x (K, V) x 16 x (D+8) bf16 + merge area 8 x 16 x (D+2) fp32 + the
+// rank partial 16 x (D+4) fp32.
 template <int D>
-SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* sm) {
+SS_DEV void attn_node_cta(const AttnParams& p, int kvh, int qi, uint8_t* sm, int rank = 0, int S = 1) {
   constexpr int RS = D + 8;
   constexpr int TILE = 16 * RS;
   constexpr int PIECES = 16 * D * 2 / 16;
@@ -279,10 +281,29 @@ SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int node = p.node_base + qi;
-  const int nkeys = P + p.depth[node] + 1;
+  auto trace_max = [&](int ev) {
+    if (p.trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(&p.trace[ev], t);
+    }
+  };
+  // prologue: the group's query rows (16 rows x D, one coalesced 16-byte load per thread), P and the
+  // node's depth are independent loads issued together; the first K/V stage goes out before the
+  // query fragments are read back with ldmatrix
+  constexpr int QRS = D + 8;   // padded smem row (conflict-free ldmatrix)
+  uint4 qv = make_uint4(0u, 0u, 0u, 0u);
+  const int q_row = threadIdx.x / (D / 8), q_col = (threadIdx.x % (D / 8)) * 8;
+  if (q_row < grp && q_row < 16)
+    qv = __ldcg(reinterpret_cast<const uint4*>(p.q + (int64_t(qi) * p.n_heads + kvh * grp + q_row) * D + q_col));
+  const int P = __ldcg(p.committed_len);
+  const int dep = __ldcg(p.depth + node);
+  const int nkeys = P + dep + 1;
   const int ntiles = (nkeys + 15) / 16;
   uint16_t* ks = reinterpret_cast<uint16_t*>(sm) + warp * 4 * TILE;
   float* mrg = reinterpret_cast<float*>(sm + 8 * 4 * TILE * 2);   // [8 warps][16 rows][D + 2]
+  float* cm = mrg + 8 * 16 * (D + 2);   // this rank's partial [16][D + 4] (16-byte aligned rows)
+  uint16_t* qs = reinterpret_cast<uint16_t*>(mrg);                 // query rows [16][QRS] (before the merge)
   const int* an = p.anc + int64_t(node) * p.anc_stride;
   const uint16_t* kc = p.k_cache + int64_t(kvh) * p.max_ctx * D;
   const uint16_t* vc = p.v_cache + int64_t(kvh) * p.max_ctx * D;
@@ -305,30 +326,32 @@ SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* 
     }
     cp_async_commit();
   };
+  const int t_first0 = warp + 8 * rank;
+  if (t_first0 < ntiles) stage(t_first0, 0);
+  if (q_row < 16) *reinterpret_cast<uint4*>(qs + q_row * QRS + q_col) = qv;
+  __syncthreads();
   uint32_t qa[D / 16][4];
   {
-    const int h0 = kvh * grp + g, h1 = kvh * grp + g + 8;
-    const uint16_t* q0 = p.q + (int64_t(qi) * p.n_heads + h0) * D;
-    const uint16_t* q1 = p.q + (int64_t(qi) * p.n_heads + h1) * D;
+    const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lc = (lane >> 4) * 8;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
-      const int c = kk * 16 + 2 * t4;
-      qa[kk][0] = g < grp ? __ldcg(reinterpret_cast<const unsigned*>(q0 + c)) : 0u;
-      qa[kk][1] = g + 8 < grp ? __ldcg(reinterpret_cast<const unsigned*>(q1 + c)) : 0u;
-      qa[kk][2] = g < grp ? __ldcg(reinterpret_cast<const unsigned*>(q0 + c + 8)) : 0u;
-      qa[kk][3] = g + 8 < grp ? __ldcg(reinterpret_cast<const unsigned*>(q1 + c + 8)) : 0u;
+      const uint32_t addr = smem_u32(qs + lr * QRS + kk * 16 + lc);
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(qa[kk][0]), "=r"(qa[kk][1]), "=r"(qa[kk][2]), "=r"(qa[kk][3])
+                   : "r"(addr));
     }
   }
+  int buf = 0;
+  const int t_first = t_first0, t_step = 8 * S;
+  trace_max(2);
   const float sl2 = rsqrtf(float(D)) * 1.4426950408889634f;
   float o[D / 8][4];
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  int buf = 0;
-  if (warp < ntiles) stage(warp, 0);
-  for (int t = warp; t < ntiles; t += 8) {
-    if (t + 8 < ntiles) {
-      stage(t + 8, buf ^ 1);
+  for (int t = t_first; t < ntiles; t += t_step) {
+    if (t + t_step < ntiles) {
+      stage(t + t_step, buf ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -399,6 +422,8 @@ SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* 
     __syncwarp();
     buf ^= 1;
   }
+  trace_max(3);
+  __syncthreads();   // qs (aliasing the merge area) is no longer read
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
@@ -417,13 +442,14 @@ SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* 
     mw[(g + 8) * (D + 2) + D + 1] = l1;
   }
   __syncthreads();
-  // merge: warp w takes head rows w, w+8; lane holds D/32 dims; warps in order 0..7 (fixed)
   constexpr int DPL = D / 32;
-  const int nw = ntiles < 8 ? ntiles : 8;
-  for (int row = warp; row < grp; row += 8) {
-    float mm = -INFINITY;
+  constexpr int LPG = 64 / DPL;   // lanes per 64-group: 16 (D = 128) or 32 (D = 64)
+  const int nw = ntiles - 8 * rank < 8 ? (ntiles - 8 * rank > 0 ? ntiles - 8 * rank : 0) : 8;
+  // merge 1 (this CTA): warp w takes head rows w, w+8; lane holds D/32 dims; warps in order (fixed)
+  auto merge_warps = [&](int row, float& mm, float& l, float (&acc)[DPL]) {
+    mm = -INFINITY;
     for (int w = 0; w < nw; ++w) mm = fmaxf(mm, mrg[(w * 16 + row) * (D + 2) + D]);
-    float acc[DPL], l = 0.f;
+    l = 0.f;
 #pragma unroll
     for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
     for (int w = 0; w < nw; ++w) {
@@ -433,6 +459,8 @@ SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* 
 #pragma unroll
       for (int t = 0; t < DPL; ++t) acc[t] += wgt * r[lane * DPL + t];
     }
+  };
+  auto write_row = [&](int row, float l, const float (&acc)[DPL]) {
     const float inv = 1.0f / l;
     const int hq = kvh * grp + row;
     float gs = 0.f;
@@ -442,11 +470,74 @@ SS_DEV void attn_node_cta(const AttnParams& p, int P, int kvh, int qi, uint8_t* 
       p.out_fragx[fragx_offset(qi, int64_t(hq) * D + lane * DPL + t, p.out_nt)] = ob;
       gs += bf2f(ob);
     }
-    constexpr int LPG = 64 / DPL;
 #pragma unroll
     for (int o2 = LPG / 2; o2; o2 >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o2);
     if (p.out_xs && (lane % LPG) == 0) p.out_xs[(int64_t(hq) * D / 64 + lane / LPG) * (p.out_nt * 8) + qi] = gs;
+  };
+  if (S == 1) {   // single CTA: finalise directly
+    for (int row = warp; row < grp; row += 8) {
+      float mm, l, acc[DPL];
+      merge_warps(row, mm, l, acc);
+      write_row(row, l, acc);
+    }
+    trace_max(4);
+    return;
   }
+  for (int row = warp; row < grp; row += 8) {   // unnormalised rank partial -> cm
+    float mm, l, acc[DPL];
+    merge_warps(row, mm, l, acc);
+    float* c = cm + row * (D + 4);
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) c[lane * DPL + t] = acc[t];
+    if (lane == 0) {
+      c[D] = mm;
+      c[D + 1] = l;
+    }
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  trace_max(4);
+  // merge 2 (cluster): rank q finalises rows q + S*w (warp w); every rank's partial is loaded
+  // (vector DSMEM loads) before the rank-ordered merge
+  const int row = rank + S * warp;
+  if (row < grp) {
+    float mr[8], lr[8], ar[8][DPL];
+    const uint32_t base = smem_u32(cm + row * (D + 4));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < S) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(q));
+        asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(mr[q]), "=f"(lr[q]) : "r"(ra + D * 4));
+        if constexpr (DPL == 4) {
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(ar[q][0]), "=f"(ar[q][1]), "=f"(ar[q][2]), "=f"(ar[q][3])
+                       : "r"(ra + lane * DPL * 4));
+        } else {
+#pragma unroll
+          for (int t = 0; t < DPL; ++t)
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(ar[q][t]) : "r"(ra + (lane * DPL + t) * 4));
+        }
+      }
+    }
+    float mm = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < S) mm = fmaxf(mm, mr[q]);
+    float acc[DPL], l = 0.f;
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < S) {
+        const float wgt = exp2f(mr[q] - mm);
+        l += wgt * lr[q];
+#pragma unroll
+        for (int t = 0; t < DPL; ++t) acc[t] += wgt * ar[q][t];
+      }
+    write_row(row, l, acc);
+  }
+  // peers read this CTA's partial: stay resident until every rank is done
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace ss

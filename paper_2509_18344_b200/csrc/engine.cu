@@ -286,6 +286,8 @@ struct PassOut {
 int g_skip = 0;
 unsigned long long* g_trace = nullptr;   // device buffer [launch][kTraceEvents] for ss_debug_trace_pass
 int g_trace_n = 0, g_trace_cap = 0;
+unsigned long long* g_cta_trace = nullptr;   // per-CTA trace of GEMV launch number g_cta_launch
+int g_cta_launch = -1, g_gemv_n = 0, g_cta_grid = 0;
 enum { SKIP_ATTN = 1, SKIP_NORM = 2, SKIP_GEMV = 4, SKIP_HEAD = 8 };
 
 // the draft's weight stream in pass order: qkv, o, gate_up, down of each layer, then the head
@@ -326,7 +328,10 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = epi;
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
+    static const int pre_after = getenv("SS_GEMV_PRE_AFTER") ? atoi(getenv("SS_GEMV_PRE_AFTER")) : 0;
+    p.pre_after = (pre_after >> g) & 1;   // bit g: group g issues its first stages after the wait
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
+    if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
     c->launches++;
     return check_launch(c, "gemv");
@@ -417,6 +422,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     a.out_nt = NT;
     // logical keys of a node: P + depth + 1 <= max_context.  The draft loop is replayed from a CUDA
     // graph while P grows, so its grid is sized for max_context.
+    if (g_trace && g_trace_n < g_trace_cap && c->attn_v2) a.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (!(g_skip & SKIP_ATTN)) launch_attention(a, target ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
     c->launches += c->attn_v2 ? 1 : 2;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
@@ -1697,6 +1703,37 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
   CK(cudaStreamSynchronize(c->cs));
   std::memcpy(out, init.data(), size_t(n) * E * 8);
   *out_n = n;
+  return SS_OK;
+}
+
+ss_status ss_debug_cta_trace(ss_ctx* c, int32_t M, int32_t launch, int64_t* out, int32_t cap, int32_t* out_n) {
+  GUARD(c);
+  if (c->state != ST_SESSION || !out || cap < 1 || !out_n || launch < 0) return fail(c, SS_ERR_INVALID, "cta_trace args");
+  float ms = 0.f;
+  ss_status s = ss_debug_time_pass(c, M, 1, 0, &ms);   // frontier set-up + warm-up
+  if (s != SS_OK) return s;
+  const size_t n = size_t(cap) * 5;
+  if (n * 8 > size_t(512) * kTraceEvents * 8) return fail(c, SS_ERR_INVALID, "cta_trace: cap too large");
+  CK(cudaMemsetAsync(c->tracebuf, 0, n * 8, c->cs));
+  g_cta_trace = c->tracebuf;
+  g_cta_launch = launch;
+  g_gemv_n = 0;
+  PassOut o;
+  o.logits = true;
+  const bool fused = c->use_fused;
+  c->use_fused = false;
+  s = forward_pass(c, false, M, 1, o);
+  c->use_fused = fused;
+  g_cta_trace = nullptr;
+  if (s != SS_OK) return s;
+  std::vector<unsigned long long> h(n);
+  CK(cudaMemcpyAsync(h.data(), c->tracebuf, n * 8, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  int k = 0;
+  for (int i = 0; i < cap; ++i)
+    if (h[size_t(i) * 5 + 1]) k = i + 1;   // CTAs that ran
+  std::memcpy(out, h.data(), size_t(k) * 5 * 8);
+  *out_n = k;
   return SS_OK;
 }
 

@@ -67,6 +67,13 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SS_TRACE_MIN(0);
+  unsigned long long* ct = p.cta_trace ? p.cta_trace + 5 * blockIdx.x : nullptr;
+  if (ct && threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    ct[0] = sm;
+    ct[1] = gtime();
+  }
   const int nC = p.K >> 7;
   const int64_t T = int64_t(p.N >> 7) * nC;
   const int Mpad = NT * 8;
@@ -105,6 +112,8 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
           bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * NT * 8, uint32_t(n) * C::kSBytes, &full[st]);
       };
       // weights do not depend on the previous kernel: issue before the grid-dependency wait
+      // (p.pre_after: after it instead — debug A/B of the prefetch's interference)
+      if (p.pre_after) griddep_wait();
       for (int i = 0; i < pre; ++i) {
         const int n = w.take(C::kCPS);
         issue_w(i, w, n);
@@ -262,7 +271,10 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
     const int nch = w.take(C::kCPS);
     c_last = w.c + nch - 1;
     mbar_wait(&full[s], ph);
-    if (threadIdx.x == 0 && w.left == n_items) SS_TRACE_CTA0(3);
+    if (threadIdx.x == 0 && w.left == n_items) {
+      SS_TRACE_CTA0(3);
+      if (ct) ct[2] = gtime();
+    }
     consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -275,9 +287,13 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   if (threadIdx.x == 0) {
     SS_TRACE_CTA0(4);
     SS_TRACE_MAX(7);
+    if (ct) ct[3] = gtime();
   }
   if (n_items > 0) flush(cur_r, c_first, c_last, true);   // the last tile of this CTA
-  if (threadIdx.x == 0) SS_TRACE_MAX(6);
+  if (threadIdx.x == 0) {
+    SS_TRACE_MAX(6);
+    if (ct) ct[4] = gtime();
+  }
 }
 
 // split factor of the cluster mode: ~2 CTAs per SM, <= SS_GEMV_MAX_CLUSTER, <= chunks

@@ -61,6 +61,8 @@ struct GemvParams {
   const uint8_t* pf;             // weights of the NEXT matrix: prefetched into L2 while this one runs
   int64_t pf_bytes;
   unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
+  unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
+  int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
   EpiParams epi;
 };
 
@@ -134,6 +136,9 @@ struct AttnParams {
   float* part_ml;                // [n_q * n_heads][n_seg_max][2]
   int* counters;                 // unused (reserved)
   int single;                    // set by the launcher: all rows fit one segment
+  int cluster;                   // K3 v2: CTAs per (kv head, node) cluster (set by the launcher)
+  unsigned long long* trace;     // optional (debug): 0 entry min, 1 dep released max, 2 q loaded max,
+                                 // 3 key loop done max, 4 CTA merge done max, 5 end max
   uint16_t* out_fragx;           // [Mpad x n_heads*d] FragX
   float* out_xs;                 // group sums [n_heads*d/64][Mpad]
   int out_nt;

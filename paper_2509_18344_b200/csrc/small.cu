@@ -127,24 +127,62 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
 template <int D>
 __global__ void __launch_bounds__(256, 1) attn_node_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t sm[];
+  if (p.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&p.trace[0], t);
+  }
   griddep_launch();
   griddep_wait();
-  attn_node_cta<D>(p, *p.committed_len, blockIdx.x, blockIdx.y, sm);
+  if (p.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&p.trace[1], t);
+  }
+  const int S = p.cluster;   // grid.x = n_kv * S, clusters of S along x
+  attn_node_cta<D>(p, blockIdx.x / S, blockIdx.y, sm, blockIdx.x % S, S);
+  if (p.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&p.trace[5], t);
+  }
 }
 
 void launch_attention(const AttnParams& p, int max_prefix, bool pdl, cudaStream_t st) {
-  if (p.split <= 0) {   // K3 v2: CTA per (kv head, node), intra-CTA key split, no combine kernel
-    const size_t smem = size_t(8) * 4 * 16 * (p.head_dim + 8) * 2 + size_t(8) * 16 * (p.head_dim + 2) * 4;
+  if (p.split <= 0) {   // K3 v2: cluster of S CTAs per (kv head, node), DSMEM merge, no combine kernel
+    static const int S_env = [] {
+      const char* v = getenv("SS_ATTN_CLUSTER");
+      const int s = v ? atoi(v) : 1;
+      return s < 1 ? 1 : (s > 8 ? 8 : s);
+    }();
+    const int S = S_env;
+    const size_t smem = size_t(8) * 4 * 16 * (p.head_dim + 8) * 2 + size_t(8) * 16 * (p.head_dim + 2) * 4 +
+                        size_t(16) * (p.head_dim + 4) * 4;
     AttnParams pp = p;
-    void* args[] = {&pp};
-    const dim3 grid(p.n_kv, p.n_q);
-    if (p.head_dim == 128) {
-      cudaFuncSetAttribute(attn_node_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      launch_pdl((const void*)attn_node_kernel<128>, grid, dim3(256), smem, pdl, st, args);
-    } else {
-      cudaFuncSetAttribute(attn_node_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      launch_pdl((const void*)attn_node_kernel<64>, grid, dim3(256), smem, pdl, st, args);
+    pp.cluster = S;
+    const void* fn = p.head_dim == 128 ? (const void*)attn_node_kernel<128> : (const void*)attn_node_kernel<64>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.n_kv * S, p.n_q);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = S;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
     }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    if (p.head_dim == 128) cudaLaunchKernelEx(&cfg, attn_node_kernel<128>, pp);
+    else cudaLaunchKernelEx(&cfg, attn_node_kernel<64>, pp);
     return;
   }
   const int grp = p.n_heads / p.n_kv;

@@ -11,7 +11,7 @@ for name, skip in (("full", 0), ("-attn", 1), ("-norm", 2), ("-gemv", 4), ("-hea
     print(f"{name:16s} {ss.debug_time_pass(6, 5, skip) * 1e3:9.1f} us/pass", flush=True)
 tr = ss.debug_trace_pass(6).astype("float64")
 t0 = tr[:, 0].min()
-names = ["qkv", "o", "gate_up", "down"] if os.environ.get("SS_FUSE_MLP") == "0" else ["qkv", "o", "mlp"]
+names = ["qkv", "attn", "o", "gate_up", "down"] if os.environ.get("SS_FUSE_MLP") != "1" else ["qkv", "attn", "o", "mlp"]
 print("launch  entry  pdep  cdep  first  loop0  loopmax  end   (us, rel. to first entry)")
 prev_end = None
 for i, r in enumerate(tr[:3 * len(names)]):
@@ -19,6 +19,10 @@ for i, r in enumerate(tr[:3 * len(names)]):
     gap = "" if prev_end is None else f" gap_from_prev_end={rel[0] - prev_end:6.2f}"
     print(f"{names[i % len(names)]:8s} " + " ".join(f"{v:6.2f}" for v in rel[[0, 1, 2, 3, 4, 7, 6]]) + gap)
     prev_end = rel[6]
+    if names[i % len(names)] == "attn":
+        print("         attn: entry %.2f dep %.2f q %.2f loop %.2f merge1 %.2f end %.2f" % tuple((r[0:6] - t0) / 1e3))
+        prev_end = (r[5] - t0) / 1e3
+        continue
     if names[i % len(names)] == "mlp":
         print("         mlp: A-done0 %.2f A-donemax %.2f B-first0 %.2f B-loopmax %.2f fin-epi %.2f end %.2f" % tuple((r[[4, 7, 3, 5, 8, 6]] - t0) / 1e3))
     if r[8]:
