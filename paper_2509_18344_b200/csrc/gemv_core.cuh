@@ -175,10 +175,11 @@ SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], in
         const uint4 cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);
         const uint32_t m0 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g) * 4);
         const uint32_t m1 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4);
-        // two independent accumulator chains (even / odd k-steps) for MMA-latency ILP
-        float cg[NT][4], ch[NT][4];
+        // one accumulator chain per token tile (the 8 consumer warps x 2 CTAs hide the MMA latency;
+        // a second chain would cost 4 FADDs per group in an issue-bound loop)
+        float cg[NT][4];
 #pragma unroll
-        for (int j = 0; j < NT; ++j) cg[j][0] = cg[j][1] = cg[j][2] = cg[j][3] = ch[j][0] = ch[j][1] = ch[j][2] = ch[j][3] = 0.f;
+        for (int j = 0; j < NT; ++j) cg[j][0] = cg[j][1] = cg[j][2] = cg[j][3] = 0.f;
 #pragma unroll
         for (int k4 = 0; k4 < 4; ++k4) {
           const int st = 4 * G + k4;
@@ -191,13 +192,9 @@ SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], in
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint2 b = *reinterpret_cast<const uint2*>(xst + (j * 8 + st) * 256);
-            mma_bf16_16816((k4 & 1) ? ch[j] : cg[j], a0, a1, a2, a3, b.x, b.y);
+            mma_bf16_16816(cg[j], a0, a1, a2, a3, b.x, b.y);
           }
         }
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) cg[j][q] += ch[j][q];
         // y += s * sum((128 + c) x) + (z - 128 s) * sum(x)      (exact affine dequant, fp32)
         const float s0 = __uint_as_float(m0 << 16), z0 = __uint_as_float(m0 & 0xFFFF0000u);
         const float s1 = __uint_as_float(m1 << 16), z1 = __uint_as_float(m1 & 0xFFFF0000u);
