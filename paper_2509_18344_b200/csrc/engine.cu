@@ -141,6 +141,10 @@ struct ss_ctx {
   int* attn_ctr = nullptr;
   unsigned long long* norm_ctr = nullptr;
   int* mlp_flags = nullptr;   // fused MLP: per gate_up tile flags + exit counter
+  int* h_root = nullptr;      // pinned staging word for draft_tree's root token
+  bool xnorm = false;         // draft: next layer's qkv normalises its own K range (SS_XNORM=1)
+  bool xn_pending = false;    // the previous down left x + sums of squares, not a normed h
+  cudaEvent_t ev_root = nullptr;
   bool fuse_mlp = false;
   bool fuse_norm = true;
   int pass_grid = 0, pass_stages = 0;
@@ -327,6 +331,18 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.counters = c->gv_cnt;
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = epi;
+    if (g == 0 && c->xn_pending) {   // RMSNorm folded into this qkv GEMV (see GemvParams::xnorm)
+      p.xnorm = 1;
+      p.xn_x = c->x;
+      p.xn_ldx = c->H;
+      p.xn_ss = c->sumsq;
+      p.xn_ss_ld = p.NT * 8;
+      p.xn_ss_tiles = c->H / 128;
+      p.xn_gain = w.attn_norm;
+      p.xn_eps = c->cfg.rms_eps;
+      p.xn_M = M;
+      c->xn_pending = false;
+    }
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
     static const int pre_after = getenv("SS_GEMV_PRE_AFTER") ? atoi(getenv("SS_GEMV_PRE_AFTER")) : 0;
     p.pre_after = (pre_after >> g) & 1;   // bit g: group g issues its first stages after the wait
@@ -382,6 +398,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
   const int NT = target ? gemm_nt(M) : gemv_nt(M);
   const float eps = c->cfg.rms_eps;
   ss_status s;
+  c->xn_pending = false;
   launch_embed_rmsnorm(c->tok, node_base, M, c->embed, c->x, c->H, c->lw[0].attn_norm, eps, c->hfrag, c->hxs, NT,
                        c->use_pdl, c->cs);
   c->launches++;
@@ -502,9 +519,17 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
       e = base_epi(c, M);
       e.kind = EPI_RESID;
       if (fnorm) e = resid_norm(nextg, 1);
+      // the next layer's qkv normalises its own K range: down only adds the residual and publishes
+      // per-tile sums of squares (no barrier, no normalise pass)
+      const bool xn = fnorm && c->xnorm && NT == 1 && l + 1 < c->L;
+      if (xn) {
+        e.kind = EPI_RESID_SS;
+        c->xn_pending = true;
+      }
       if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
     }
     if (fnorm) {
+    } else if (c->xn_pending) {
     } else if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
       launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
       c->launches++;
@@ -964,7 +989,9 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   cudaEventCreate(&c->e1);
   cudaEventCreate(&c->e2);
   cudaEventCreate(&c->e3);
-  if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess || !c->h_out) {
+  cudaEventCreateWithFlags(&c->ev_root, cudaEventDisableTiming);
+  cudaHostAlloc(&c->h_root, 64, cudaHostAllocPortable);
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess || !c->h_out || !c->h_root) {
     delete c;
     return SS_ERR_CUDA;
   }
@@ -1097,6 +1124,8 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
     c->fuse_norm = !(fv && fv[0] == '0');
     const char* mv = getenv("SS_FUSE_MLP");   // opt-in: measured slower than the two GEMVs
     c->fuse_mlp = mv && mv[0] == '1';
+    const char* xv = getenv("SS_XNORM");   // opt-in: measured slower
+    c->xnorm = xv && xv[0] == '1';
     const char* gv = getenv("SS_GRAPHS");
     if (gv && gv[0] == '0') c->use_graphs = false;
     const char* av = getenv("SS_ATTN_V2");
@@ -1268,7 +1297,14 @@ static ss_status draft_impl(ss_ctx* c, int32_t root_token, const ss_draft_params
   if (root_token >= c->V) return fail(c, SS_ERR_INVALID, "root token out of range");
   const int k = p->top_k;
   const int deff = std::max(0, std::min(p->depth, (c->C - c->P - 1) / k));
-  if (root_token >= 0) CK(cudaMemcpyAsync(c->root_tok, &root_token, 4, cudaMemcpyHostToDevice, c->cs));
+  if (root_token >= 0) {
+    // pinned staging word: the copy is ordered on the compute stream and the host does not wait for
+    // the draft (a blocked host would stop feeding the streaming ring during the draft)
+    CK(cudaEventSynchronize(c->ev_root));   // the previous root copy has left the staging word
+    *c->h_root = root_token;
+    CK(cudaMemcpyAsync(c->root_tok, c->h_root, 4, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaEventRecord(c->ev_root, c->cs));
+  }
   CK(cudaEventRecord(c->e0, c->cs));
   ss_status s;
   if (deff == 0) {
@@ -1285,7 +1321,6 @@ static ss_status draft_impl(ss_ctx* c, int32_t root_token, const ss_draft_params
   c->n_nodes = 1 + k * deff;
   c->st.last_d_eff = deff;
   c->state = ST_DRAFTED;
-  if (root_token >= 0) CK(cudaStreamSynchronize(c->cs));   // host int on the stack was the source
   return SS_OK;
 }
 
@@ -1424,8 +1459,9 @@ void ss_destroy(ss_ctx* c) {
   for (auto e : c->ev_consumed) cudaEventDestroy(e);
   for (auto e : c->ev_t0) cudaEventDestroy(e);
   for (auto e : c->ev_t1) cudaEventDestroy(e);
-  for (auto e : {c->e0, c->e1, c->e2, c->e3})
+  for (auto e : {c->e0, c->e1, c->e2, c->e3, c->ev_root})
     if (e) cudaEventDestroy(e);
+  if (c->h_root) cudaFreeHost(c->h_root);
   if (c->host) cudaFreeHost(c->host);
   if (c->h_embed) cudaFreeHost(c->h_embed);
   if (c->h_out) cudaFreeHost(c->h_out);

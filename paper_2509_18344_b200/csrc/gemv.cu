@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   uint64_t* empty = full + C::kMaxStages;
   int* flag = reinterpret_cast<int*>(empty + C::kMaxStages);
   float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
+  uint8_t* xres = reinterpret_cast<uint8_t*>(scratch) + 512;    // xnorm: [xn_chunks][X chunk]
+  float* xsres = reinterpret_cast<float*>(xres + size_t(p.xn_chunks) * C::kXBytes);   // [xn_chunks][2][Mpad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SS_TRACE_MIN(0);
@@ -100,12 +102,14 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       const uint64_t pol = policy_evict_first();
       const int pre = int(n_stage < kStages ? n_stage : kStages);
       Work wx = w;   // replayed below for the activation copies of the prefetched stages
+      const uint32_t per_chunk = p.xnorm ? uint32_t(C::kWBytes) : uint32_t(C::kWBytes + C::kXBytes + C::kSBytes);
       auto issue_w = [&](int st, const Work& ww, int n) {
-        mbar_arrive_expect_tx(&full[st], uint32_t(n) * (C::kWBytes + C::kXBytes + C::kSBytes));
+        mbar_arrive_expect_tx(&full[st], uint32_t(n) * per_chunk);
         bulk_g2s_hint(ring + st * C::kStageBytes, p.W + (int64_t(ww.r) * nC + ww.c) * C::kWBytes,
                       uint32_t(n) * C::kWBytes, &full[st], pol);
       };
       auto issue_x = [&](int st, const Work& ww, int n) {
+        if (p.xnorm) return;
         uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
         bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
         if constexpr (Q4)
@@ -169,6 +173,78 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   if (threadIdx.x == 0) SS_TRACE_CTA0(2);
   const int g = lane >> 2, t4 = lane & 3;
   const int nthr = kGemvConsumerWarps * 32;
+  int xc0 = 0;   // first chunk of the resident X
+  if constexpr (kCluster) {
+    if (p.xnorm) {
+      // RMSNorm of this CTA's K range: r_m from the per-tile sums of squares (warp m, fixed shuffle
+      // tree), then (token, 64-group) pairs: a warp takes 64 columns of one token, 2 per lane
+      const Work w0 = make_work<kCluster>(p.N, p.K, crank, csize);
+      xc0 = w0.c_begin;
+      const int nchl = w0.c_end - w0.c_begin, k0 = w0.c_begin * 128;
+      // all global loads first (x, gain and the sums of squares are independent), then the math
+      const int npairs = Mpad * nchl * 2;
+      for (int base = warp; base < npairs; base += 8 * kGemvConsumerWarps) {
+        float xv[8][2], gv[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int pr = base + i * kGemvConsumerWarps, m = pr % Mpad, cg2 = pr / Mpad;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int k = k0 + 64 * cg2 + 32 * u + lane;
+            const bool ok = pr < npairs && m < p.xn_M;
+            xv[i][u] = ok ? __ldcg(p.xn_x + int64_t(m) * p.xn_ldx + k) : 0.f;
+            gv[i][u] = ok ? bf2f(p.xn_gain[k]) : 0.f;
+          }
+        }
+        if (base == warp) {   // first block: r_m while the loads fly
+          // warp 0 reads the [tiles][Mpad] sums of squares once (lane = tile, contiguous rows; every
+          // CTA re-reading them per token would hammer the same few L2 lines) and reduces each
+          // token's column with a fixed shuffle tree
+          if (warp == 0) {
+            float part[32];
+#pragma unroll
+            for (int m = 0; m < 32; ++m) part[m] = 0.f;
+            for (int t = lane; t < p.xn_ss_tiles; t += 32) {
+              const float4* row = reinterpret_cast<const float4*>(p.xn_ss + int64_t(t) * p.xn_ss_ld);
+#pragma unroll
+              for (int q = 0; q < NT * 2; ++q) {
+                const float4 v = __ldcg(row + q);
+                part[4 * q] += v.x;
+                part[4 * q + 1] += v.y;
+                part[4 * q + 2] += v.z;
+                part[4 * q + 3] += v.w;
+              }
+            }
+#pragma unroll
+            for (int m = 0; m < NT * 8; ++m) {
+              const float ssum = warp_sum(part[m]);
+              if (lane == 0) scratch[m] = m < p.xn_M ? 1.0f / sqrtf(ssum / float(p.xn_ldx) + p.xn_eps) : 0.f;
+            }
+          }
+          named_bar(1, nthr);
+          if (threadIdx.x == 0) SS_TRACE_CTA0(13);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int pr = base + i * kGemvConsumerWarps, m = pr % Mpad, cg2 = pr / Mpad;
+          if (pr >= npairs) break;
+          float gs = 0.f;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int kl = 64 * cg2 + 32 * u + lane;
+            uint16_t hb = 0;
+            if (m < p.xn_M) hb = f2bf(xv[i][u] * scratch[m] * gv[i][u]);
+            reinterpret_cast<uint16_t*>(xres)[fragx_offset(m, kl, NT)] = hb;
+            gs += bf2f(hb);
+          }
+          gs = warp_sum(gs);
+          if (lane == 0) xsres[cg2 * Mpad + m] = gs;   // chunk cg2/2, group cg2%2
+        }
+      }
+      named_bar(1, nthr);
+      if (threadIdx.x == 0) SS_TRACE_CTA0(14);
+    }
+  }
   float acc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
@@ -275,7 +351,11 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       SS_TRACE_CTA0(3);
       if (ct) ct[2] = gtime();
     }
-    consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane);
+    if (p.xnorm)
+      consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
+                            xsres + (w.c - xc0) * 2 * Mpad);
+    else
+      consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == kStages) {
@@ -318,7 +398,8 @@ static int ensure_attrs() {   // ring stages for this instantiation; sets the sm
     int st = budget / C::kStageBytes;
     if (st < 2) st = 2;
     if (st > C::kMaxStages) st = C::kMaxStages;
-    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
+    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::smem_for(st) + (kCluster ? 8 * (C::kXBytes + C::kSBytes) : 0));
     if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     stages = st;
   }
@@ -395,10 +476,17 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   const int stages = ensure_attrs<Q4, NT, kCluster>();
   GemvParams p = p0;
   p.stages = stages;
+  p.xn_chunks = 0;
+  if (p.xnorm) {
+    if (!kCluster) return;   // xnorm needs a fixed per-CTA K range (engine guarantees cluster mode)
+    const int nC = p.K / 128;
+    p.xn_chunks = (nC + S - 1) / S;
+  }
+  const size_t xbytes = size_t(p.xn_chunks) * (C::kXBytes + C::kSBytes);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemvThreads);
-  cfg.dynamicSmemBytes = C::smem_for(stages);
+  cfg.dynamicSmemBytes = C::smem_for(stages) + xbytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;

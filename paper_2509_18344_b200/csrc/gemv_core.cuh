@@ -159,7 +159,8 @@ SS_DEV Work make_work(int N, int K, uint32_t crank, uint32_t csize) {
 // One pipeline stage (nch tile-chunks of weights + the matching activation chunks + group sums)
 // accumulated into this warp's 16 rows x Mpad tokens.
 template <bool Q4, int NT>
-SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], int warp, int lane) {
+SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], int warp, int lane,
+                          const uint8_t* xres = nullptr, const float* xsres = nullptr) {
   using C = GemvCfg<Q4, NT>;
   const int g = lane >> 2, t4 = lane & 3;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
@@ -167,9 +168,11 @@ SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], in
   for (int ci = 0; ci < C::kCPS; ++ci) {
     if (ci >= nch) break;
     const uint8_t* wst = stage + ci * C::kWBytes;
-    const uint8_t* xst = stage + C::kCPS * C::kWBytes + ci * C::kXBytes + ((t4 * 8 + g) * 8);
+    // activations: from the stage (TMA) or from a CTA-resident normalised copy (xres, xsres)
+    const uint8_t* xst = (xres ? xres + ci * C::kXBytes : stage + C::kCPS * C::kWBytes + ci * C::kXBytes) + ((t4 * 8 + g) * 8);
     if constexpr (Q4) {
-      const float* xsum = reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
+      const float* xsum = xsres ? xsres + ci * 2 * NT * 8
+                                : reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
 #pragma unroll
       for (int G = 0; G < 2; ++G) {
         const uint4 cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);

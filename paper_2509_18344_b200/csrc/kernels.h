@@ -63,6 +63,18 @@ struct GemvParams {
   unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
   int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
+  // xnorm (cluster mode): instead of TMA-ing X/XS, the consumers build this CTA's K range of
+  // X = bf16(x * r_m * gain) (RMSNorm of the residual stream, r_m from per-tile sums of squares)
+  // and its group sums in shared memory once, before the main loop
+  int xnorm;
+  const float* xn_x;             // residual stream [M x xn_ldx] fp32
+  int xn_ldx;
+  const float* xn_ss;            // sums of squares [xn_ss_tiles][xn_ss_ld]
+  int xn_ss_ld, xn_ss_tiles;
+  const uint16_t* xn_gain;       // RMSNorm gain [K] bf16
+  float xn_eps;
+  int xn_M;                      // valid tokens
+  int xn_chunks;                 // set by the launcher: resident chunks per CTA (smem sizing)
   EpiParams epi;
 };
 

@@ -25,5 +25,7 @@ for i, r in enumerate(tr[:3 * len(names)]):
         continue
     if names[i % len(names)] == "mlp":
         print("         mlp: A-done0 %.2f A-donemax %.2f B-first0 %.2f B-loopmax %.2f fin-epi %.2f end %.2f" % tuple((r[[4, 7, 3, 5, 8, 6]] - t0) / 1e3))
+    if r[13]:
+        print("         xnorm: r-ready %.2f built %.2f" % tuple((r[13:15] - t0) / 1e3))
     if r[8]:
         print("         epilogue: reduce %.2f resid %.2f barrier %.2f r %.2f done %.2f" % tuple((r[8:13] - t0) / 1e3))
