@@ -111,45 +111,58 @@ def blas_threads():
 
 
 # ---------------------------------------------------------------------------------------------
-def oracle_step_seconds(cfg, depth, topk, nodes=6):
+class OracleSample:
     """Bounded sample of the oracle on the SAME shape: one decoder layer (target + 4-bit substitute)
     plus the head, `nodes` draft and `nodes` target node-forwards, extrapolated to one full step of
-    (1 + k(D-1)) draft + (1 + kD) target node-forwards through all layers.  Returns (seconds/step, info)."""
-    from oracle.model import TargetWeights, draft_layers, KVCache, forward_nodes
-    from oracle.tree import tempered_log_softmax, select_topk
-    cfg1 = cfg.with_(n_layers=1)
-    t0 = time.time()
-    tw = TargetWeights(cfg1, SEED)
-    dl = draft_layers(tw, 0)
-    setup = time.time() - t0
-    kv = KVCache(cfg1, nodes + 1)
-    toks = list(range(1, nodes + 1))
-    slots = list(range(nodes))
-    anc = [[s] for s in slots]
-    pos = [0] * nodes
-    t0 = time.perf_counter()
-    forward_nodes(cfg1, dl, tw, kv, toks, slots, pos, anc)
-    t_draft_node = (time.perf_counter() - t0) / nodes
-    t0 = time.perf_counter()
-    logits = forward_nodes(cfg1, tw.layers, tw, kv, toks, slots, pos, anc)
-    t_target_node = (time.perf_counter() - t0) / nodes
-    h = np.ones(cfg.hidden)
-    t0 = time.perf_counter()
-    for _ in range(nodes):
-        tw.head @ h
-    t_head = (time.perf_counter() - t0) / nodes
-    t0 = time.perf_counter()
-    lp = np.stack([tempered_log_softmax(logits[i], 0.2) for i in range(min(topk, nodes))])
-    select_topk(list(range(len(lp))), [0.0] * len(lp), lp, topk)
-    t_select = time.perf_counter() - t0
-    L = cfg.n_layers
-    n_draft = 1 + topk * (depth - 1)
-    n_verify = 1 + topk * depth
-    step = (n_draft * ((t_draft_node - t_head) * L + t_head) + n_verify * ((t_target_node - t_head) * L + t_head)
-            + depth * t_select)
-    info = {"t_draft_node_1layer_s": t_draft_node, "t_target_node_1layer_s": t_target_node, "t_head_s": t_head,
-            "t_select_s": t_select, "setup_s": setup, "node_forwards": n_draft + n_verify}
-    return step, info
+    (1 + k(D-1)) draft + (1 + kD) target node-forwards through all layers.  The seeded weights are
+    generated once (setup); every call of step_seconds() re-times the sample."""
+
+    def __init__(self, cfg, depth, topk, nodes=6):
+        from oracle.model import TargetWeights, draft_layers
+        self.cfg, self.depth, self.topk, self.nodes = cfg, depth, topk, nodes
+        self.cfg1 = cfg.with_(n_layers=1)
+        t0 = time.time()
+        self.tw = TargetWeights(self.cfg1, SEED)
+        self.dl = draft_layers(self.tw, 0)
+        self.setup = time.time() - t0
+
+    def step_seconds(self):
+        from oracle.model import KVCache, forward_nodes
+        from oracle.tree import tempered_log_softmax, select_topk
+        cfg, cfg1, tw, nodes, topk, depth = self.cfg, self.cfg1, self.tw, self.nodes, self.topk, self.depth
+        kv = KVCache(cfg1, nodes + 1)
+        toks = list(range(1, nodes + 1))
+        slots = list(range(nodes))
+        anc = [[s] for s in slots]
+        pos = [0] * nodes
+        t0 = time.perf_counter()
+        forward_nodes(cfg1, self.dl, tw, kv, toks, slots, pos, anc)
+        t_draft_node = (time.perf_counter() - t0) / nodes
+        t0 = time.perf_counter()
+        logits = forward_nodes(cfg1, tw.layers, tw, kv, toks, slots, pos, anc)
+        t_target_node = (time.perf_counter() - t0) / nodes
+        h = np.ones(cfg.hidden)
+        t0 = time.perf_counter()
+        for _ in range(nodes):
+            tw.head @ h
+        t_head = (time.perf_counter() - t0) / nodes
+        t0 = time.perf_counter()
+        lp = np.stack([tempered_log_softmax(logits[i], 0.2) for i in range(min(topk, nodes))])
+        select_topk(list(range(len(lp))), [0.0] * len(lp), lp, topk)
+        t_select = time.perf_counter() - t0
+        L = cfg.n_layers
+        n_draft = 1 + topk * (depth - 1)
+        n_verify = 1 + topk * depth
+        step = (n_draft * ((t_draft_node - t_head) * L + t_head) + n_verify * ((t_target_node - t_head) * L + t_head)
+                + depth * t_select)
+        info = {"t_draft_node_1layer_s": t_draft_node, "t_target_node_1layer_s": t_target_node, "t_head_s": t_head,
+                "t_select_s": t_select, "setup_s": self.setup, "node_forwards": n_draft + n_verify}
+        return step, info
+
+
+def oracle_step_seconds(cfg, depth, topk, nodes=6):
+    """One-shot OracleSample (setup + one timed sample) -> (seconds/step, info)."""
+    return OracleSample(cfg, depth, topk, nodes).step_seconds()
 
 
 def load_tau():
@@ -168,8 +181,9 @@ def run_reference(a):
     tau = tau_rec["tau"] if tau_rec and tau_rec.get("config") == a.config else 1.0
     times = []
     info = None
+    sample = OracleSample(cfg, a.depth, a.topk)   # weights generated once, each step re-timed
     for i in range(a.warmup + a.steps):
-        s, info = oracle_step_seconds(cfg, a.depth, a.topk)
+        s, info = sample.step_seconds()
         if i >= a.warmup:
             times.append(s)
     step_s = statistics.mean(times)

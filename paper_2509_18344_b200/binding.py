@@ -77,10 +77,11 @@ EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy"]
 _lib = None
 
 
-def load_library(path=LIB):
+def load_library(path=None):
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("SS_LIBSUBSPEC", LIB)   # SS_LIBSUBSPEC: an experimental build
     if not os.path.exists(path):
         raise RuntimeError(f"libsubspec.so not built ({path}); run __graft_entry__.build()")
     lib = ctypes.CDLL(path)

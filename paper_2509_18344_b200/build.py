@@ -14,6 +14,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # no --use_fast_math: the quantizer needs IEEE div.rn / rint
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
+# experiments only: extra nvcc flags and an alternative output (the default build ignores both)
+EXTRA = os.environ.get("SS_NVCC_FLAGS", "").split()
+if os.environ.get("SS_LIB_OUT"):
+    LIB = os.path.abspath(os.environ["SS_LIB_OUT"])
+    BUILD = LIB + ".objs"
 
 
 def sources():
@@ -39,7 +44,7 @@ def build(force=False, verbose=False):
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-dc" if False else "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
