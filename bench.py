@@ -234,20 +234,75 @@ def k2_bytes(N, K, M):
     return N * K // 2 + N * K // 64 * 4 + M * K * 2 + M * N * 2
 
 
+def load_weights_for_job(ss, dist, local, n_resident):
+    """the node holds ONE copy of the offloaded layers.  Under torchrun the node-local
+    rank 0 creates a POSIX shared-memory segment and fills it; the other ranks attach after a
+    barrier (each process page-locks its mapping).  Falls back to a per-rank store when /dev/shm is
+    too small or SS_SHARED_HOST=0.  Returns the SharedMemory handle (kept alive) or None."""
+    if dist is None or n_resident < 0 or os.environ.get("SS_SHARED_HOST", "1") == "0":
+        ss.load_weights(SEED, n_resident=n_resident)
+        return None
+    import torch
+    from multiprocessing import shared_memory
+    nbytes = ss.host_store_bytes(n_resident)
+    name = f"ss_store_{os.environ.get('MASTER_PORT', '0')}"
+    ok = 1
+    shm = None
+    if local == 0:
+        try:
+            st = os.statvfs("/dev/shm")
+            if st.f_bavail * st.f_frsize < nbytes + (1 << 30):
+                raise OSError("/dev/shm too small")
+            shm = shared_memory.SharedMemory(name=name, create=True, size=nbytes)
+        except Exception:
+            ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=dist_device(local))
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag) == 0:
+        if shm is not None:
+            shm.close()
+            shm.unlink()
+        ss.load_weights(SEED, n_resident=n_resident)
+        return None
+    import ctypes
+    if local == 0:
+        addr = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
+        ss.load_weights_shared(SEED, n_resident, addr, nbytes, fill=True)
+    dist.barrier()
+    if local != 0:
+        shm = shared_memory.SharedMemory(name=name)
+        try:   # attaching processes must not unlink the segment at exit (the creator does)
+            from multiprocessing import resource_tracker
+            resource_tracker.unregister(shm._name, "shared_memory")
+        except Exception:
+            pass
+        addr = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
+        ss.load_weights_shared(SEED, n_resident, addr, nbytes, fill=False)
+    return shm
+
+
+def dist_device(local):
+    return "cpu" if os.environ.get("SS_DIST_BACKEND", "nccl") == "gloo" else f"cuda:{local}"
+
+
 def run_ours(a):
     import torch
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    dev = int(os.environ.get("SS_BENCH_DEVICE", local))   # test override: several ranks on one GPU (gloo)
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if os.environ.get("SS_DIST_BACKEND", "nccl") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2509_18344_b200.binding import SubSpec
     cfg = PRESETS[a.config]
     D, k, T = a.depth, a.topk, a.temp
     t_setup = time.time()
-    ss = SubSpec(cfg, int(a.cap_gib * GIB), device=local, max_depth=D, max_top_k=max(k, 6), max_chunk=256)
-    ss.load_weights(SEED, n_resident=a.n_resident)
+    ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256)
+    shm = load_weights_for_job(ss, dist, local, a.n_resident)
     ss.build_substitutes(4, 64)
     prompt = request_for_rank(rank, cfg.vocab)
     ss.prefill(prompt)
@@ -257,7 +312,7 @@ def run_ours(a):
     ss.reset_stats()
     cs = ss.compute_stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -308,14 +363,14 @@ def run_ours(a):
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         st1 = ss.stats()
-        wall, e2e_tok = aggregate_ranks(dist, wall, e2e_tok, f"cuda:{local}")
+        wall, e2e_tok = aggregate_ranks(dist, wall, e2e_tok, dist_device(local))
         streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / n_e2e
         e2e = {"value": e2e_tok / wall, "unit": "tokens/s", "h2d_bytes_per_step": int(4 + streamed),
                "d2h_bytes_per_step": int(4 * (e2e_tok / max(1, n_e2e)) + 4),
                "h2d_breakdown": {"root_token": 4, "streamed_layer_weights": int(streamed)}, "steps": n_e2e}
     # host link measured in the same run: pinned H2D 1 GiB on the copy stream, best of 5
     hbuf = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
-    dbuf = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{local}")
+    dbuf = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{dev}")
     best = 1e9
     with torch.cuda.stream(ss.copy_stream):
         for _ in range(5):
@@ -328,7 +383,7 @@ def run_ours(a):
     link_gbs = (1 << 30) / (best * 1e-3) / 1e9
     del hbuf, dbuf
     # ---- aggregate over ranks ----
-    tmax, tot_tokens = aggregate_ranks(dist, ms, emitted, f"cuda:{local}")
+    tmax, tot_tokens = aggregate_ranks(dist, ms, emitted, dist_device(local))
     value = tot_tokens / (tmax / 1e3)
     tau = float(np.mean(taus))
     steps_per_s = a.steps / (ms / 1e3)
@@ -357,7 +412,8 @@ def run_ours(a):
         "streaming": {"bytes_per_step": st["stream_bytes"] / a.steps, "busy_gbs": stream_gbs,
                       "host_link_gbs_measured": link_gbs, "frac": (stream_gbs / link_gbs) if stream_gbs else None,
                       "duty_cycle": (st["stream_busy_ms"] / ms) if ms else None},
-        "memory": {"arena_used": st["arena_used"], "arena_cap": st["arena_cap"], "ring_bytes": st["ring_bytes"],
+        "memory": {"shared_host_store": shm is not None,
+                   "arena_used": st["arena_used"], "arena_cap": st["arena_cap"], "ring_bytes": st["ring_bytes"],
                    "substitute_bytes": st["substitute_bytes"], "host_pinned_bytes": st["host_pinned_bytes"],
                    "n_resident": st["n_resident"]},
         "gpu_launches": int(st["gpu_launches"]),
@@ -381,6 +437,12 @@ def run_ours(a):
                 "seconds_per_step": s}
         print(json.dumps(line), flush=True)
     ss.close()
+    if dist:
+        dist.barrier()   # every rank has released the shared store before it is unlinked
+    if shm is not None:
+        shm.close()
+        if local == 0:
+            shm.unlink()
     if dist:
         dist.destroy_process_group()
 

@@ -95,6 +95,21 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
  * (SPEC.md:205-213).  Embedding, final norm and head are always resident. */
 ss_status ss_load_weights(ss_ctx* ctx, uint64_t seed, int32_t n_resident);
 
+/* Bytes of the offloaded layers' host store for an explicit n_resident >= 0 (bf16, device layout).
+ * Errors: INVALID. */
+ss_status ss_host_store_bytes(ss_ctx* ctx, int32_t n_resident, size_t* out_bytes);
+
+/* As ss_load_weights, but the offloaded layers live in a CALLER-OWNED host store (e.g. one POSIX
+ * shared-memory segment mapped by every rank of a multi-GPU job, so the node holds one copy —
+ * SURVEY §8(e)).  host_store: >= ss_host_store_bytes(n_resident) bytes, page-aligned, owned by the
+ * caller and kept alive until ss_destroy; the library page-locks it with cudaHostRegister (portable,
+ * refcounted per process) and unregisters it at ss_destroy.  fill = 1: generate the offloaded
+ * layers into the store (one context of the job); fill = 0: the store already holds them (the caller
+ * orders the filling context's return before this call, e.g. with a barrier).  n_resident >= 0.
+ * Errors: INVALID, BUDGET (store too small), CUDA (registration failed), as ss_load_weights. */
+ss_status ss_load_weights_shared(ss_ctx* ctx, uint64_t seed, int32_t n_resident, void* host_store,
+                                 size_t host_bytes, int32_t fill);
+
 /* Build the 4-bit group-64 substitute of every offloaded layer: stream it host->device through
  * the staging ring and quantize on the device (K1).  Norms/biases are shared. */
 ss_status ss_build_substitutes(ss_ctx* ctx, const ss_quant_spec* q);

@@ -51,6 +51,8 @@ P = ctypes.POINTER
 _FUNCS = {
     "ss_create": [P(ModelConfigC), P(LimitsC), ctypes.c_int, c_void_p, c_size_t, c_void_p, c_void_p, P(c_void_p)],
     "ss_load_weights": [c_void_p, c_uint64, c_int32],
+    "ss_host_store_bytes": [c_void_p, c_int32, P(c_size_t)],
+    "ss_load_weights_shared": [c_void_p, c_uint64, c_int32, c_void_p, c_size_t, c_int32],
     "ss_build_substitutes": [c_void_p, P(QuantSpecC)],
     "ss_prefill": [c_void_p, c_void_p, c_int32, c_int32, P(c_int32)],
     "ss_draft_tree": [c_void_p, c_int32, P(DraftParamsC), c_void_p, c_void_p, c_void_p, c_void_p, P(c_int32)],
@@ -154,6 +156,18 @@ class SubSpec:
     # ---- the method ---------------------------------------------------------------------
     def load_weights(self, seed, n_resident=0):
         self._check(self.lib.ss_load_weights(self.ctx, c_uint64(seed), n_resident))
+
+    def host_store_bytes(self, n_resident=0):
+        out = c_size_t()
+        self._check(self.lib.ss_host_store_bytes(self.ctx, n_resident, ctypes.byref(out)))
+        return out.value
+
+    def load_weights_shared(self, seed, n_resident, store_addr, store_bytes, fill):
+        """Offloaded layers in a caller-owned host store (address of a page-aligned mapping that
+        outlives this context, e.g. multiprocessing.shared_memory); fill=True generates them."""
+        self._keep_store = store_addr
+        self._check(self.lib.ss_load_weights_shared(self.ctx, c_uint64(seed), n_resident, c_void_p(store_addr),
+                                                     store_bytes, 1 if fill else 0))
 
     def build_substitutes(self, bits=4, group=64):
         self._check(self.lib.ss_build_substitutes(self.ctx, ctypes.byref(QuantSpecC(bits, group))))

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -81,6 +82,7 @@ struct ss_ctx {
   int n_resident = 0;
   uint64_t seed = 0;
   uint8_t* host = nullptr;
+  bool host_external = false;   // caller-owned store (ss_load_weights_shared), registered here
   size_t host_bytes = 0;
   bool substitutes_built = false;
   // kv + tree
@@ -1000,8 +1002,66 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   return SS_OK;
 }
 
+// Caller-owned host stores are page-locked with cudaHostRegister once per process (refcounted:
+// several contexts of one process may share a store).
+static std::mutex g_reg_mu;
+static std::map<void*, int> g_reg_count;
+static bool host_register(void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  int& n = g_reg_count[p];
+  if (n == 0) {
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+      n = 1 << 20;   // registered by someone else: never unregister it here
+    } else if (e != cudaSuccess) {
+      cudaGetLastError();
+      g_reg_count.erase(p);
+      return false;
+    }
+  }
+  ++n;
+  return true;
+}
+static void host_unregister(void* p) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  auto it = g_reg_count.find(p);
+  if (it == g_reg_count.end()) return;
+  if (--it->second == 0) {
+    cudaHostUnregister(p);
+    cudaGetLastError();
+    g_reg_count.erase(it);
+  }
+}
+
+static size_t host_store_bytes(ss_ctx* c, int nr) {
+  size_t layer_bf16 = 0;
+  for (int g = 0; g < 4; ++g) layer_bf16 += bf16_bytes(c->gN[g], c->gK[g]);
+  return size_t(c->L - nr) * layer_bf16;
+}
+
+ss_status ss_host_store_bytes(ss_ctx* c, int32_t n_resident, size_t* out) {
+  GUARD(c);
+  if (!out || n_resident < 0 || n_resident > c->L) return fail(c, SS_ERR_INVALID, "host_store_bytes args");
+  *out = host_store_bytes(c, n_resident);
+  return SS_OK;
+}
+
+static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* ext_host, size_t ext_bytes, bool fill);
+
 ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
   GUARD(c);
+  return load_impl(c, seed, n_resident, nullptr, 0, true);
+}
+
+ss_status ss_load_weights_shared(ss_ctx* c, uint64_t seed, int32_t n_resident, void* host_store, size_t host_bytes,
+                                 int32_t fill) {
+  GUARD(c);
+  if (!host_store || n_resident < 0) return fail(c, SS_ERR_INVALID, "load_weights_shared: store and n_resident >= 0");
+  return load_impl(c, seed, n_resident, host_store, host_bytes, fill != 0);
+}
+
+static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* ext_host, size_t ext_bytes, bool fill) {
   if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "load_weights: already loaded");
   c->seed = seed;
   const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
@@ -1038,8 +1098,15 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
   if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
   // pinned host store for offloaded layers (device layout)
   c->host_bytes = size_t(c->L - nr) * layer_bf16;
+  if (ext_host) {
+    if (ext_bytes < c->host_bytes) return fail(c, SS_ERR_BUDGET, "shared host store smaller than ss_host_store_bytes");
+    if (c->host_bytes && !host_register(ext_host, c->host_bytes))
+      return fail(c, SS_ERR_CUDA, "cudaHostRegister of the shared host store failed");
+    c->host = reinterpret_cast<uint8_t*>(ext_host);
+    c->host_external = true;
+  }
   if (c->host_bytes) {
-    if (cudaHostAlloc(&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess)
+    if (!c->host_external && cudaHostAlloc(&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess)
       return fail(c, SS_ERR_CUDA, "cudaHostAlloc of the pinned host store failed");
     size_t off = 0;
     for (int l = nr; l < c->L; ++l)
@@ -1073,6 +1140,7 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
       launch_gen_natural(w.bias + c->qd + c->kvd, tensor_key(seed, b + 6), c->kvd, scale_c32(0.02), 0, c->cs);
     }
     for (int g = 0; g < 4; ++g) {
+      if (!w.resident && !fill) continue;   // shared store already holds this matrix
       uint8_t* dst = w.resident ? w.bf16[g] : c->ring;
       const int K = c->gK[g];
       const float cin = scale_c32(1.0 / std::sqrt(double(K)));
@@ -1088,7 +1156,7 @@ ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
       } else {
         launch_gen_tiled(dst, tensor_key(seed, b + 11), c->H, K, cin, 0, 0, c->cs);
       }
-      if (!w.resident) {
+      if (!w.resident && fill) {
         CK(cudaMemcpyAsync(c->host + w.host_off[g], c->ring, bf16_bytes(c->gN[g], K), cudaMemcpyDeviceToHost, c->cs));
         CK(cudaStreamSynchronize(c->cs));
       }
@@ -1462,7 +1530,8 @@ void ss_destroy(ss_ctx* c) {
   for (auto e : {c->e0, c->e1, c->e2, c->e3, c->ev_root})
     if (e) cudaEventDestroy(e);
   if (c->h_root) cudaFreeHost(c->h_root);
-  if (c->host) cudaFreeHost(c->host);
+  if (c->host && c->host_external) host_unregister(c->host);
+  else if (c->host) cudaFreeHost(c->host);
   if (c->h_embed) cudaFreeHost(c->h_embed);
   if (c->h_out) cudaFreeHost(c->h_out);
   cudaGetLastError();
