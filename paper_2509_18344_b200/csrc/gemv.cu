@@ -25,6 +25,8 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -455,6 +457,9 @@ static ClusterPlan cluster_plan(int N, int K, int sms) {
     }
   }
   if (plan.ncl < 1) plan.ncl = 1;
+  if (getenv("SS_VERBOSE"))
+    fprintf(stderr, "gemv cluster plan<%d,%d> N=%d K=%d: S=%d clusters=%d all_resident=%d\n", int(Q4), NT, N, K, plan.S,
+            plan.ncl, int(plan.all_resident));
   cache[key] = plan;
   return plan;
 }
