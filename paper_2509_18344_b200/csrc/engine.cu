@@ -146,6 +146,8 @@ struct ss_ctx {
   int* h_root = nullptr;      // pinned staging word for draft_tree's root token
   bool xnorm = false;         // draft: next layer's qkv normalises its own K range (SS_XNORM=1)
   bool xn_pending = false;    // the previous down left x + sums of squares, not a normed h
+  bool serial_stream = false; // ablation: no copy/compute overlap in the verify streaming
+  int last_consumed_ev = -1;
   cudaEvent_t ev_root = nullptr;
   bool fuse_mlp = false;
   bool fuse_norm = true;
@@ -198,6 +200,9 @@ ss_status pump(ss_ctx* c) {
     const int64_t seq = c->next_issue;
     // never run more than one cycle ahead of consumption
     if (seq >= c->next_consume + n_items) return SS_OK;
+    // ablation (SS_STREAM_SERIAL=1, the paper's "async transfer" off, P:172-176 / Table 2): copy a
+    // group only when it is the next one consumed and after the previous group's compute
+    if (c->serial_stream && seq > c->next_consume) return SS_OK;
     const auto [l, g] = c->cycle[seq % n_items];
     const size_t B = bf16_bytes(c->gN[g], c->gK[g]);
     size_t off = c->ring_head;
@@ -229,6 +234,7 @@ ss_status pump(ss_ctx* c) {
       c->ev_pending[ev] = false;
     }
     for (size_t i : dead) CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[c->inflight[i].ev], 0));
+    if (c->serial_stream && c->last_consumed_ev >= 0) CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[c->last_consumed_ev], 0));
     for (size_t k = dead.size(); k-- > 0;) c->inflight.erase(c->inflight.begin() + dead[k]);
     CK(cudaEventRecord(c->ev_t0[ev], c->xs));
     CK(cudaMemcpyAsync(c->ring + off, c->host + c->lw[l].host_off[g], B, cudaMemcpyHostToDevice, c->xs));
@@ -277,6 +283,7 @@ ss_status consume_begin(ss_ctx* c, int l, int g, const uint8_t** w, int* ev_out)
 }
 ss_status consume_end(ss_ctx* c, int ev) {
   CK(cudaEventRecord(c->ev_consumed[ev], c->cs));
+  c->last_consumed_ev = ev;
   for (auto& it : c->inflight)
     if (it.ev == ev) it.consumed = true;
   c->next_consume++;
@@ -1192,6 +1199,8 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
     c->fuse_norm = !(fv && fv[0] == '0');
     const char* mv = getenv("SS_FUSE_MLP");   // opt-in: measured slower than the two GEMVs
     c->fuse_mlp = mv && mv[0] == '1';
+    const char* sv = getenv("SS_STREAM_SERIAL");
+    c->serial_stream = sv && sv[0] == '1';
     const char* xv = getenv("SS_XNORM");   // opt-in: measured slower
     c->xnorm = xv && xv[0] == '1';
     const char* gv = getenv("SS_GRAPHS");
