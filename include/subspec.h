@@ -64,6 +64,9 @@ typedef struct {
   int32_t max_depth;    /* D_max (48) */
   int32_t max_top_k;    /* k_max (<= 32) */
   int32_t max_chunk;    /* prefill chunk (256) */
+  int32_t max_batch;    /* request slots of one weight stream (0 or 1 = one
+                           request, the paper's batch 1); max_batch * max_top_k <= 32.  Each
+                           slot owns max_context rows of committed KV inside the arena. */
 } ss_limits;
 
 /* Substitute quantization: bits = 4, group_size = 64 are supported. */
@@ -143,6 +146,37 @@ ss_status ss_step(ss_ctx* ctx, const ss_draft_params* p, int32_t* out_tokens, in
  * max_new; opt_tau_hist capacity D+2 (histogram of tokens per step). */
 ss_status ss_generate(ss_ctx* ctx, const int32_t* prompt, int32_t n, int32_t max_new, int32_t chunk,
                       const ss_draft_params* p, int32_t* out_tokens, int32_t* out_n, int32_t* opt_tau_hist);
+
+/* ---- batched requests: one weight stream serves several trees ----------
+ * The paper decodes one request at a time (batch 1) and avoids batching for latency;
+ * every tree is still verified losslessly, so each request's output is its own greedy AR
+ * output whatever the batch.  A context created with ss_limits.max_batch = Bmax has Bmax request
+ * slots, each with its own tree arrays, committed KV (max_context rows) and committed length.  A
+ * step drafts all B active trees together (B*k frontier rows per draft pass, one pass of the
+ * substitute weights), verifies all B*(1+kD) nodes in ONE streamed target pass, and accepts and
+ * commits each tree independently.  The trees share one shape per step: D_eff is clamped by the
+ * longest request (O.10).  Ownership and synchronisation as for the one-request calls. */
+
+/* Number of active slots n_req in [1, max_batch].  Changing it (or any n_req > 1) starts a new
+ * batch session: every active slot must be prefilled again.  Errors: INVALID (range; the opt-in
+ * persistent draft pass or legacy attention with n_req > 1), STRUCTURE (inside a step). */
+ss_status ss_set_batch(ss_ctx* ctx, int32_t n_req);
+
+/* ss_prefill for slot `slot` < n_req (ss_prefill == slot 0).  Drafting needs every active slot
+ * prefilled.  Errors as ss_prefill, plus INVALID for a slot outside the active batch. */
+ss_status ss_prefill_slot(ss_ctx* ctx, int32_t slot, const int32_t* prompt, int32_t n, int32_t chunk,
+                          int32_t* out_first_token);
+
+/* One batched step (draft + verify + accept/commit of every active slot).  out_tokens: host
+ * [n_req][stride] (stride >= D + 1), out_n: host [n_req].  Synchronizes.  Errors as ss_step. */
+ss_status ss_step_batch(ss_ctx* ctx, const ss_draft_params* p, int32_t stride, int32_t* out_tokens, int32_t* out_n);
+
+/* Batched ss_generate: set_batch(n_req), prefill slot b with prompts[off_b .. off_b + lens[b])
+ * (prompts concatenated on the host), then batched steps until every request has max_new tokens.
+ * out_tokens: host [n_req][max_new]; out_n: [n_req]; opt_tau_hist as ss_generate (all requests). */
+ss_status ss_generate_batch(ss_ctx* ctx, int32_t n_req, const int32_t* prompts, const int32_t* prompt_lens,
+                            int32_t max_new, int32_t chunk, const ss_draft_params* p, int32_t* out_tokens,
+                            int32_t* out_n, int32_t* opt_tau_hist);
 
 ss_status ss_get_stats(ss_ctx* ctx, ss_stats* out);
 ss_status ss_reset_stats(ss_ctx* ctx);

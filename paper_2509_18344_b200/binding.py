@@ -27,7 +27,7 @@ class ModelConfigC(ctypes.Structure):
 
 
 class LimitsC(ctypes.Structure):
-    _fields_ = [("max_depth", c_int32), ("max_top_k", c_int32), ("max_chunk", c_int32)]
+    _fields_ = [("max_depth", c_int32), ("max_top_k", c_int32), ("max_chunk", c_int32), ("max_batch", c_int32)]
 
 
 class QuantSpecC(ctypes.Structure):
@@ -60,6 +60,11 @@ _FUNCS = {
     "ss_accept_and_commit": [c_void_p, c_void_p, P(c_int32), c_void_p],
     "ss_step": [c_void_p, P(DraftParamsC), c_void_p, P(c_int32)],
     "ss_generate": [c_void_p, c_void_p, c_int32, c_int32, c_int32, P(DraftParamsC), c_void_p, P(c_int32), c_void_p],
+    "ss_set_batch": [c_void_p, c_int32],
+    "ss_prefill_slot": [c_void_p, c_int32, c_void_p, c_int32, c_int32, P(c_int32)],
+    "ss_step_batch": [c_void_p, P(DraftParamsC), c_int32, c_void_p, c_void_p],
+    "ss_generate_batch": [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32, P(DraftParamsC), c_void_p, c_void_p,
+                          c_void_p],
     "ss_get_stats": [c_void_p, P(StatsC)],
     "ss_reset_stats": [c_void_p],
     "ss_debug_gen_tensor": [c_void_p, c_uint64, c_int32, c_int64, c_int64, c_int32, c_double, c_void_p],
@@ -117,14 +122,14 @@ def model_config_c(cfg):
 class SubSpec:
     """One decode session on one GPU: the C-ABI context plus its torch-owned arena and streams."""
 
-    def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256):
+    def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256, max_batch=1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("SubSpec needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
         self.cfg = cfg
         self.device = device
-        self.limits = LimitsC(max_depth, max_top_k, max_chunk)
+        self.limits = LimitsC(max_depth, max_top_k, max_chunk, max_batch)
         self.arena = torch.empty(int(arena_bytes), dtype=torch.uint8, device=f"cuda:{device}")
         self.compute_stream = torch.cuda.Stream(device=device)
         self.copy_stream = torch.cuda.Stream(device=device)
@@ -222,6 +227,36 @@ class SubSpec:
                                          ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)), _ptr(out),
                                          ctypes.byref(n), _ptr(hist)))
         return out[:n.value].tolist(), hist
+
+    # ---- batched requests (NEXT-2) ---------------------------------------------------------
+    def set_batch(self, n_req):
+        self._check(self.lib.ss_set_batch(self.ctx, n_req))
+
+    def prefill_slot(self, slot, prompt, chunk=256):
+        p = np.ascontiguousarray(prompt, dtype=np.int32)
+        out = c_int32()
+        self._check(self.lib.ss_prefill_slot(self.ctx, slot, _ptr(p), len(p), chunk, ctypes.byref(out)))
+        return out.value
+
+    def step_batch(self, n_req, depth, top_k, sharpen_t):
+        stride = depth + 1
+        toks = np.zeros(n_req * stride, np.int32)
+        n = np.zeros(n_req, np.int32)
+        self._check(self.lib.ss_step_batch(self.ctx, ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)), stride,
+                                           _ptr(toks), _ptr(n)))
+        return [toks[b * stride: b * stride + n[b]].tolist() for b in range(n_req)]
+
+    def generate_batch(self, prompts, max_new, depth, top_k, sharpen_t, chunk=256):
+        lens = np.array([len(p) for p in prompts], np.int32)
+        cat = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts]), dtype=np.int32)
+        B = len(prompts)
+        out = np.zeros(B * max_new, np.int32)
+        n = np.zeros(B, np.int32)
+        hist = np.zeros(depth + 2, np.int32)
+        self._check(self.lib.ss_generate_batch(self.ctx, B, _ptr(cat), _ptr(lens), max_new, chunk,
+                                               ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)), _ptr(out),
+                                               _ptr(n), _ptr(hist)))
+        return [out[b * max_new: b * max_new + n[b]].tolist() for b in range(B)], hist
 
     def stats(self):
         s = StatsC()

@@ -280,7 +280,8 @@ SS_DEV void attn_node_cta(const AttnParams& p, int kvh, int qi, uint8_t* sm, int
   const int grp = p.n_heads / p.n_kv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  const int node = p.node_base + qi;
+  const int req = rq_req(p.rq, qi);   // batched requests: request req, local node, strided state
+  const int node = req * p.rq.node_stride + p.node_base + rq_loc(p.rq, qi);
   auto trace_max = [&](int ev) {
     if (p.trace && threadIdx.x == 0) {
       unsigned long long t;
@@ -296,7 +297,7 @@ SS_DEV void attn_node_cta(const AttnParams& p, int kvh, int qi, uint8_t* sm, int
   const int q_row = threadIdx.x / (D / 8), q_col = (threadIdx.x % (D / 8)) * 8;
   if (q_row < grp && q_row < 16)
     qv = __ldcg(reinterpret_cast<const uint4*>(p.q + (int64_t(qi) * p.n_heads + kvh * grp + q_row) * D + q_col));
-  const int P = __ldcg(p.committed_len);
+  const int P = __ldcg(p.committed_len + req);
   const int dep = __ldcg(p.depth + node);
   const int nkeys = P + dep + 1;
   const int ntiles = (nkeys + 15) / 16;
@@ -304,11 +305,11 @@ SS_DEV void attn_node_cta(const AttnParams& p, int kvh, int qi, uint8_t* sm, int
   float* mrg = reinterpret_cast<float*>(sm + 8 * 4 * TILE * 2);   // [8 warps][16 rows][D + 2]
   float* cm = mrg + 8 * 16 * (D + 2);   // this rank's partial [16][D + 4] (16-byte aligned rows)
   uint16_t* qs = reinterpret_cast<uint16_t*>(mrg);                 // query rows [16][QRS] (before the merge)
-  const int* an = p.anc + int64_t(node) * p.anc_stride;
-  const uint16_t* kc = p.k_cache + int64_t(kvh) * p.max_ctx * D;
-  const uint16_t* vc = p.v_cache + int64_t(kvh) * p.max_ctx * D;
-  const uint16_t* kt = p.k_tree + int64_t(kvh) * p.max_nodes * D;
-  const uint16_t* vt = p.v_tree + int64_t(kvh) * p.max_nodes * D;
+  const int* an = p.anc + int64_t(node) * p.anc_stride;   // ancestor slots are request-local
+  const uint16_t* kc = p.k_cache + (int64_t(kvh) * p.max_ctx + int64_t(req) * p.rq.ctx_stride) * D;
+  const uint16_t* vc = p.v_cache + (int64_t(kvh) * p.max_ctx + int64_t(req) * p.rq.ctx_stride) * D;
+  const uint16_t* kt = p.k_tree + (int64_t(kvh) * p.max_nodes + int64_t(req) * p.rq.node_stride) * D;
+  const uint16_t* vt = p.v_tree + (int64_t(kvh) * p.max_nodes + int64_t(req) * p.rq.node_stride) * D;
   auto stage = [&](int t, int buf) {
     uint16_t* kd = ks + buf * 2 * TILE;
     uint16_t* vd = kd + TILE;

@@ -93,6 +93,12 @@ struct ss_ctx {
   float* score = nullptr;
   int *committed_len = nullptr, *root_tok = nullptr, *tokbuf = nullptr;
   int P = 0, n_nodes = 0, cur_k = 0, cur_deff = 0;
+  // batched requests (NEXT-2): slots [0, B) of Bmax; per-slot tree arrays of max_nodes and committed
+  // KV of C rows, so the kv-head strides of the KV buffers are kv_nodes = Bmax*max_nodes, kv_ctx = Bmax*C
+  int Bmax = 1, B = 1, kv_nodes = 0, kv_ctx = 0;
+  std::vector<int> Pb;                 // committed length per slot (host mirror)
+  std::vector<char> slot_ready;        // slot prefilled in this batch session
+  ReqMap cur_rq{0, 0, 0, 0};           // request map of the pass being enqueued
   // activations
   float* x = nullptr;
   uint16_t *hfrag = nullptr, *attnfrag = nullptr, *actfrag = nullptr, *qbuf = nullptr;
@@ -355,6 +361,8 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
     static const int pre_after = getenv("SS_GEMV_PRE_AFTER") ? atoi(getenv("SS_GEMV_PRE_AFTER")) : 0;
     p.pre_after = (pre_after >> g) & 1;   // bit g: group g issues its first stages after the wait
+    static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
+    p.self_pf = (self_pf >> g) & 1;        // bit g: group g prefetches its own range into L2
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
@@ -394,7 +402,8 @@ EpiParams base_epi(ss_ctx* c, int M) {
   e.q_dim = c->qd;
   e.kv_dim = c->kvd;
   e.head_dim = c->d;
-  e.max_nodes = c->max_nodes;
+  e.max_nodes = c->kv_nodes;
+  e.rq = c->cur_rq;
   e.x = c->x;
   e.ldx = c->H;
   e.ffn = c->F;
@@ -409,7 +418,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
   ss_status s;
   c->xn_pending = false;
   launch_embed_rmsnorm(c->tok, node_base, M, c->embed, c->x, c->H, c->lw[0].attn_norm, eps, c->hfrag, c->hxs, NT,
-                       c->use_pdl, c->cs);
+                       c->use_pdl, c->cs, c->cur_rq);
   c->launches++;
   if ((s = check_launch(c, "embed_rmsnorm")) != SS_OK) return s;
   for (int l = 0; l < c->L; ++l) {
@@ -431,8 +440,9 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     a.anc = c->anc;
     a.depth = c->depth;
     a.anc_stride = c->anc_stride;
-    a.max_ctx = c->C;
-    a.max_nodes = c->max_nodes;
+    a.max_ctx = c->kv_ctx;
+    a.max_nodes = c->kv_nodes;
+    a.rq = c->cur_rq;
     a.n_q = M;
     a.node_base = node_base;
     a.n_heads = c->nh;
@@ -449,7 +459,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     // logical keys of a node: P + depth + 1 <= max_context.  The draft loop is replayed from a CUDA
     // graph while P grows, so its grid is sized for max_context.
     if (g_trace && g_trace_n < g_trace_cap && c->attn_v2) a.trace = g_trace + kTraceEvents * (g_trace_n++);
-    if (!(g_skip & SKIP_ATTN)) launch_attention(a, target ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
+    if (!(g_skip & SKIP_ATTN)) launch_attention(a, (target && c->B == 1) ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
     c->launches += c->attn_v2 ? 1 : 2;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
     const bool fnorm = !target && c->fuse_norm && !(g_skip & SKIP_NORM) &&
@@ -592,18 +602,30 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
   return SS_OK;
 }
 
+// request map of a pass over `rows` rows per request of all B slots (zero map for one request)
+static ReqMap batch_map(ss_ctx* c, int rows) {
+  return c->B > 1 ? ReqMap{rows, 0, c->max_nodes, c->C} : ReqMap{0, 0, 0, 0};
+}
+
 ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
   ss_status s;
-  launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, c->use_pdl, c->cs);
+  launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, c->use_pdl, c->cs, c->B, c->max_nodes,
+                   c->anc_stride);
   c->launches++;
   if ((s = check_launch(c, "tree_init")) != SS_OK) return s;
   for (int dd = 0; dd < D; ++dd) {
-    const int M = dd == 0 ? 1 : k;
+    const int Mr = dd == 0 ? 1 : k;   // frontier rows per request
+    const int M = c->B * Mr;
     const int base = dd == 0 ? 0 : 1 + (dd - 1) * k;
     PassOut o;
     o.logits = true;
-    if ((s = forward_pass(c, false, M, base, o)) != SS_OK) return s;
+    c->cur_rq = batch_map(c, Mr);
+    s = forward_pass(c, false, M, base, o);
+    c->cur_rq = ReqMap{0, 0, 0, 0};
+    if (s != SS_OK) return s;
     TopkParams t{};
+    t.req_rows = c->B > 1 ? Mr : 0;
+    t.node_stride = c->max_nodes;
     t.logits = c->logits;
     t.M = M;
     t.V = c->V;
@@ -663,8 +685,8 @@ ss_status launch_fused_pass(ss_ctx* c, int M, int base, int child_base, int chil
   a.anc = c->anc;
   a.depth = c->depth;
   a.anc_stride = c->anc_stride;
-  a.max_ctx = c->C;
-  a.max_nodes = c->max_nodes;
+  a.max_ctx = c->kv_ctx;
+  a.max_nodes = c->kv_nodes;
   a.n_heads = c->nh;
   a.n_kv = c->nkv;
   a.head_dim = c->d;
@@ -721,7 +743,7 @@ ss_status draft_loop_fused(ss_ctx* c, int D, int k, float T) {
 ss_status run_draft(ss_ctx* c, int D, int k, float T) {
   uint32_t tb;
   std::memcpy(&tb, &T, 4);
-  const auto key = std::make_tuple(D, k, tb);
+  const auto key = std::make_tuple(D + (c->B << 16), k, tb);   // one graph per (D, batch, k, T)
   if (c->use_graphs) {
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
@@ -765,11 +787,29 @@ ss_status run_draft(ss_ctx* c, int D, int k, float T) {
 ss_status do_verify(ss_ctx* c) {
   PassOut o;
   o.argmax = true;
-  return forward_pass(c, true, c->n_nodes, 0, o);
+  c->cur_rq = batch_map(c, c->n_nodes);   // rows request-major: request b's nodes at b * n_nodes
+  ss_status s = forward_pass(c, true, c->B * c->n_nodes, 0, o);
+  c->cur_rq = ReqMap{0, 0, 0, 0};
+  return s;
 }
 
-ss_status do_accept(ss_ctx* c, bool chain) {
+// prefill chunk of slot b: a chain of m nodes of that request (rows all belong to request b)
+ss_status do_verify_slot(ss_ctx* c, int b) {
+  PassOut o;
+  o.argmax = true;
+  c->cur_rq = c->Bmax > 1 ? ReqMap{0, b, c->max_nodes, c->C} : ReqMap{0, 0, 0, 0};
+  ss_status s = forward_pass(c, true, c->n_nodes, 0, o);
+  c->cur_rq = ReqMap{0, 0, 0, 0};
+  return s;
+}
+
+ss_status do_accept(ss_ctx* c, bool chain, int slot = 0) {
   AcceptParams a{};
+  a.n_req = chain ? 1 : c->B;   // a prefill chunk commits one slot
+  a.req0 = chain ? slot : 0;
+  a.node_stride = c->max_nodes;
+  a.ctx_stride = c->C;
+  a.out_stride = c->max_nodes + 1;
   a.argmax = c->argmax;
   a.tok = c->tok;
   a.parent = c->parent;
@@ -791,18 +831,19 @@ ss_status do_accept(ss_ctx* c, bool chain) {
   a.n_layers = c->L;
   a.n_kv = c->nkv;
   a.head_dim = c->d;
-  a.max_ctx = c->C;
-  a.max_nodes = c->max_nodes;
+  a.max_ctx = c->kv_ctx;
+  a.max_nodes = c->kv_nodes;
   a.chain = chain ? 1 : 0;
   launch_accept_commit(a, c->use_pdl, c->cs);
   c->launches += 2;
   return check_launch(c, "accept_commit");
 }
 
-ss_status read_outputs(ss_ctx* c, int cap, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path) {
-  CK(cudaMemcpyAsync(c->h_out, c->out_n, 4, cudaMemcpyDeviceToHost, c->cs));
-  CK(cudaMemcpyAsync(c->h_out + 1, c->out_tokens, size_t(cap) * 4, cudaMemcpyDeviceToHost, c->cs));
-  if (opt_path) CK(cudaMemcpyAsync(c->h_out + 1 + cap, c->out_path, size_t(cap) * 4, cudaMemcpyDeviceToHost, c->cs));
+ss_status read_outputs(ss_ctx* c, int cap, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path, int slot = 0) {
+  const int64_t so = int64_t(slot) * (c->max_nodes + 1);
+  CK(cudaMemcpyAsync(c->h_out, c->out_n + slot, 4, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaMemcpyAsync(c->h_out + 1, c->out_tokens + so, size_t(cap) * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (opt_path) CK(cudaMemcpyAsync(c->h_out + 1 + cap, c->out_path + so, size_t(cap) * 4, cudaMemcpyDeviceToHost, c->cs));
   CK(cudaStreamSynchronize(c->cs));
   const int n = c->h_out[0];
   if (out_n) *out_n = n;
@@ -822,6 +863,8 @@ bool valid_cfg(const ss_model_config* m, const ss_limits* l) {
   if (m->max_context < 2 || m->max_context > 8192) return false;
   if (m->n_heads / m->n_kv_heads > 16) return false;
   if (l->max_depth < 0 || l->max_top_k < 1 || l->max_top_k > 32 || l->max_chunk < 1 || l->max_chunk > 1024) return false;
+  // batched slots: a draft pass forwards max_batch * k <= 32 frontier rows (GEMV token tiles)
+  if (l->max_batch < 0 || l->max_batch > 32 || (l->max_batch > 1 && l->max_batch * l->max_top_k > 32)) return false;
   return true;
 }
 
@@ -874,7 +917,14 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   const int k = lim->max_top_k, D = lim->max_depth;
   c->max_nodes = std::max(1 + k * D, lim->max_chunk);
   c->anc_stride = std::max(D + 1, lim->max_chunk);
-  c->mpad_max = std::max(32, ((c->max_nodes + 127) / 128) * 128);
+  c->Bmax = std::max(1, int(lim->max_batch));
+  c->B = 1;
+  c->Pb.assign(size_t(c->Bmax), 0);
+  c->slot_ready.assign(size_t(c->Bmax), 0);
+  c->kv_nodes = c->Bmax * c->max_nodes;
+  c->kv_ctx = c->Bmax * c->C;
+  // rows of a pass: a prefill chunk, or a verify over every slot's tree
+  c->mpad_max = std::max(32, ((std::max(c->max_nodes, c->Bmax * (1 + k * D)) + 127) / 128) * 128);
   Arena& a = c->ar;
   auto A = [&](size_t bytes) { return a.alloc(bytes); };
   bool ok = true;
@@ -903,26 +953,26 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
     w.mlp_norm = (uint16_t*)chk(A(size_t(c->H) * 2));
     if (cfg->qkv_bias) w.bias = (uint16_t*)chk(A(size_t(c->qkv_rows) * 2));
   }
-  c->kc_layer = int64_t(c->nkv) * c->C * c->d;
-  c->kt_layer = int64_t(c->nkv) * c->max_nodes * c->d;
+  c->kc_layer = int64_t(c->nkv) * c->kv_ctx * c->d;
+  c->kt_layer = int64_t(c->nkv) * c->kv_nodes * c->d;
   c->kc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
   c->vc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
   c->kt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
   c->vt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
-  c->tok = (int*)chk(A(size_t(c->max_nodes) * 4));
-  c->parent = (int*)chk(A(size_t(c->max_nodes) * 4));
-  c->depth = (int*)chk(A(size_t(c->max_nodes) * 4));
-  c->score = (float*)chk(A(size_t(c->max_nodes) * 4));
-  c->anc = (int*)chk(A(size_t(c->max_nodes) * c->anc_stride * 4));
-  c->committed_len = (int*)chk(A(64));
-  c->root_tok = (int*)chk(A(64));
+  c->tok = (int*)chk(A(size_t(c->kv_nodes) * 4));
+  c->parent = (int*)chk(A(size_t(c->kv_nodes) * 4));
+  c->depth = (int*)chk(A(size_t(c->kv_nodes) * 4));
+  c->score = (float*)chk(A(size_t(c->kv_nodes) * 4));
+  c->anc = (int*)chk(A(size_t(c->kv_nodes) * c->anc_stride * 4));
+  c->committed_len = (int*)chk(A(std::max<size_t>(64, size_t(c->Bmax) * 4)));
+  c->root_tok = (int*)chk(A(std::max<size_t>(64, size_t(c->Bmax) * 4)));
   c->tokbuf = (int*)chk(A(size_t(lim->max_chunk) * 4));
   const int fx_cols = std::max({c->H, c->qd, c->F});
   c->x = (float*)chk(A(size_t(c->mpad_max) * c->H * 4));
   c->hfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * fx_cols * 2));
   c->attnfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * c->qd * 2));
   c->actfrag = (uint16_t*)chk(A(size_t(c->mpad_max) * c->F * 2));
-  c->qbuf = (uint16_t*)chk(A(size_t(c->max_nodes) * c->qd * 2));
+  c->qbuf = (uint16_t*)chk(A(size_t(c->mpad_max) * c->qd * 2));
   c->hxs = (float*)chk(A(size_t(c->mpad_max) * (fx_cols / 64) * 4));
   c->attnxs = (float*)chk(A(size_t(c->mpad_max) * (c->qd / 64) * 4));
   c->actxs = (float*)chk(A(size_t(c->mpad_max) * (c->F / 64) * 4));
@@ -954,7 +1004,8 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
     const char* av = getenv("SS_ATTN_V2");
     const char* fv = getenv("SS_FUSED_DRAFT");
     const bool legacy = (av && av[0] == '0') || (fv && fv[0] == '1');
-    size_t need = std::max(size_t(c->mpad_max) * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
+    const size_t mpad_one = size_t(std::max(32, ((c->max_nodes + 127) / 128) * 128));   // one request's rows
+    size_t need = std::max(mpad_one * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
     if (legacy) need = std::max(need, size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d);
     c->at_o_floats = need;
     c->at_o = (float*)chk(A(need * 4));
@@ -969,12 +1020,12 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->am_val = (float*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
   c->am_sec = (float*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
   c->am_idx = (int*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
-  c->argmax = (int*)chk(A(size_t(c->max_nodes) * 4));
-  c->gap = (float*)chk(A(size_t(c->max_nodes) * 4));
-  c->out_tokens = (int*)chk(A(size_t(c->max_nodes + 1) * 4));
-  c->out_n = (int*)chk(A(64));
-  c->out_path = (int*)chk(A(size_t(c->max_nodes + 1) * 4));
-  c->commit_meta = (int*)chk(A(64));
+  c->argmax = (int*)chk(A(size_t(c->mpad_max) * 4));
+  c->gap = (float*)chk(A(size_t(c->mpad_max) * 4));
+  c->out_tokens = (int*)chk(A(size_t(c->Bmax) * (c->max_nodes + 1) * 4));
+  c->out_n = (int*)chk(A(std::max<size_t>(64, size_t(c->Bmax) * 4)));
+  c->out_path = (int*)chk(A(size_t(c->Bmax) * (c->max_nodes + 1) * 4));
+  c->commit_meta = (int*)chk(A(std::max<size_t>(64, size_t(c->Bmax) * 8)));
   if (!ok) {
     delete c;
     return SS_ERR_BUDGET;
@@ -993,7 +1044,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
     }
   cudaMemcpyAsync(c->rope, rope.data(), rope.size() * 8, cudaMemcpyHostToDevice, c->cs);
   cudaStreamSynchronize(c->cs);
-  cudaHostAlloc(&c->h_out, size_t(2 * c->max_nodes + 8) * 4, cudaHostAllocPortable);
+  cudaHostAlloc(&c->h_out, (size_t(2 * c->Bmax) * (c->max_nodes + 1) + c->Bmax + 8) * 4, cudaHostAllocPortable);
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
   cudaEventCreate(&c->e2);
@@ -1330,38 +1381,70 @@ ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
   return pump(c);   // start streaming the first verify's layers right away
 }
 
-ss_status ss_prefill(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t chunk, int32_t* out_first) {
-  GUARD(c);
+static ss_status prefill_slot_impl(ss_ctx* c, int slot, const int32_t* prompt, int32_t n, int32_t chunk,
+                                   int32_t* out_first) {
   if (c->state < ST_READY) return fail(c, SS_ERR_STRUCTURE, "prefill before build_substitutes");
   if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "prefill inside a step");
+  if (slot < 0 || slot >= c->B) return fail(c, SS_ERR_INVALID, "prefill: slot outside the active batch");
   if (!prompt || n < 1 || chunk < 1 || chunk > c->lim.max_chunk) return fail(c, SS_ERR_INVALID, "prefill: bad prompt/chunk");
   if (n > c->C) return fail(c, SS_ERR_CAPACITY, "prompt longer than max_context");
   for (int i = 0; i < n; ++i)
     if (prompt[i] < 0 || prompt[i] >= c->V) return fail(c, SS_ERR_INVALID, "token id out of range");
-  CK(cudaMemsetAsync(c->committed_len, 0, 4, c->cs));
-  c->P = 0;
+  CK(cudaMemsetAsync(c->committed_len + slot, 0, 4, c->cs));
+  c->Pb[slot] = 0;
+  const int64_t no = int64_t(slot) * c->max_nodes;
   for (int c0 = 0; c0 < n; c0 += chunk) {
     const int m = std::min(chunk, n - c0);
     CK(cudaMemcpyAsync(c->tokbuf, prompt + c0, size_t(m) * 4, cudaMemcpyHostToDevice, c->cs));
-    launch_chain_init(c->tokbuf, m, c->tok, c->parent, c->depth, c->score, c->anc, c->anc_stride, c->cs);
+    launch_chain_init(c->tokbuf, m, c->tok + no, c->parent + no, c->depth + no, c->score + no,
+                      c->anc + no * c->anc_stride, c->anc_stride, c->cs);
     c->n_nodes = m;
     c->cur_k = 1;
     c->cur_deff = 0;
-    ss_status s = do_verify(c);
+    ss_status s = do_verify_slot(c, slot);
     if (s != SS_OK) return s;
-    if ((s = do_accept(c, true)) != SS_OK) return s;
-    c->P += m;
+    if ((s = do_accept(c, true, slot)) != SS_OK) return s;
+    c->Pb[slot] += m;
     // the pageable prompt buffer is reused next chunk: make the H2D copy complete
     CK(cudaStreamSynchronize(c->cs));
   }
   int32_t first = 0, nn = 0;
-  ss_status s = read_outputs(c, 1, &first, &nn, nullptr);
+  ss_status s = read_outputs(c, 1, &first, &nn, nullptr, slot);
   if (s != SS_OK) return s;
   if (out_first) *out_first = first;
   c->st.prefill_tokens += n;
+  c->P = c->Pb[0];
   c->st.committed_len = c->P;
-  c->state = ST_SESSION;
+  c->slot_ready[slot] = 1;
+  bool all = true;
+  for (int b = 0; b < c->B; ++b) all = all && c->slot_ready[b];
+  c->state = all ? ST_SESSION : ST_READY;
   harvest_timing(c);
+  return SS_OK;
+}
+
+ss_status ss_prefill(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t chunk, int32_t* out_first) {
+  GUARD(c);
+  return prefill_slot_impl(c, 0, prompt, n, chunk, out_first);
+}
+
+ss_status ss_prefill_slot(ss_ctx* c, int32_t slot, const int32_t* prompt, int32_t n, int32_t chunk, int32_t* out_first) {
+  GUARD(c);
+  return prefill_slot_impl(c, slot, prompt, n, chunk, out_first);
+}
+
+ss_status ss_set_batch(ss_ctx* c, int32_t n_req) {
+  GUARD(c);
+  if (n_req < 1 || n_req > c->Bmax) return fail(c, SS_ERR_INVALID, "set_batch: n_req outside [1, max_batch]");
+  if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "set_batch inside a step");
+  if (c->B > 1 || n_req > 1) {
+    // a batch session starts over: every active slot is prefilled again
+    std::fill(c->slot_ready.begin(), c->slot_ready.end(), 0);
+    if (c->state == ST_SESSION) c->state = ST_READY;
+  }
+  if (n_req > 1 && (c->use_fused || !c->attn_v2))
+    return fail(c, SS_ERR_INVALID, "batched requests need the default multi-kernel draft pass and K3 v2 attention");
+  c->B = n_req;
   return SS_OK;
 }
 
@@ -1370,10 +1453,14 @@ static ss_status draft_impl(ss_ctx* c, int32_t root_token, const ss_draft_params
       !(p->sharpen_t > 0.f) || !std::isfinite(p->sharpen_t))
     return fail(c, SS_ERR_INVALID, "draft params");
   if (c->state != ST_SESSION) return fail(c, SS_ERR_STRUCTURE, "draft_tree needs a prefilled session (and no pending step)");
-  if (c->P + 1 > c->C) return fail(c, SS_ERR_CAPACITY, "context full");
+  if (c->B > 1 && root_token >= 0) return fail(c, SS_ERR_INVALID, "batched draft: roots come from the previous step");
+  int Pmax = 0;
+  for (int b = 0; b < c->B; ++b) Pmax = std::max(Pmax, c->Pb[b]);
+  if (Pmax + 1 > c->C) return fail(c, SS_ERR_CAPACITY, "context full");
   if (root_token >= c->V) return fail(c, SS_ERR_INVALID, "root token out of range");
   const int k = p->top_k;
-  const int deff = std::max(0, std::min(p->depth, (c->C - c->P - 1) / k));
+  // O.10 capacity clamp; a batch shares one tree shape, clamped by its longest request
+  const int deff = std::max(0, std::min(p->depth, (c->C - Pmax - 1) / k));
   if (root_token >= 0) {
     // pinned staging word: the copy is ordered on the compute stream and the host does not wait for
     // the draft (a blocked host would stop feeding the streaming ring during the draft)
@@ -1385,7 +1472,8 @@ static ss_status draft_impl(ss_ctx* c, int32_t root_token, const ss_draft_params
   CK(cudaEventRecord(c->e0, c->cs));
   ss_status s;
   if (deff == 0) {
-    launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, c->use_pdl, c->cs);
+    launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, c->use_pdl, c->cs, c->B, c->max_nodes,
+                     c->anc_stride);
     c->launches++;
     s = check_launch(c, "tree_init");
   } else {
@@ -1435,23 +1523,47 @@ ss_status ss_verify_tree(ss_ctx* c, int32_t* opt_argmax, float* opt_gap) {
   return SS_OK;
 }
 
-static ss_status accept_impl(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path) {
+// out_tokens/opt_path: [B][stride] (stride >= D_eff + 1), out_n: [B]
+static ss_status accept_impl(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path, int stride) {
   if (c->state != ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "accept before verify");
   ss_status s = do_accept(c, false);
   if (s != SS_OK) return s;
   CK(cudaEventRecord(c->e3, c->cs));
-  int32_t n = 0;
   const int cap = c->cur_deff + 1;
-  if ((s = read_outputs(c, cap, out_tokens, &n, opt_path)) != SS_OK) return s;
-  if (out_n) *out_n = n;
-  c->P += n;
+  int total = 0;
+  if (c->B == 1) {
+    int32_t n = 0;
+    if ((s = read_outputs(c, cap, out_tokens, &n, opt_path)) != SS_OK) return s;
+    if (out_n) *out_n = n;
+    c->Pb[0] += n;
+    total = n;
+  } else {
+    // every slot's count and tokens in two copies (outputs are [B][max_nodes + 1] on the device)
+    const int os = c->max_nodes + 1, B = c->B;
+    int* hn = c->h_out;
+    int* ht = c->h_out + B;
+    CK(cudaMemcpyAsync(hn, c->out_n, size_t(B) * 4, cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaMemcpyAsync(ht, c->out_tokens, size_t(B) * os * 4, cudaMemcpyDeviceToHost, c->cs));
+    if (opt_path) CK(cudaMemcpyAsync(ht + size_t(B) * os, c->out_path, size_t(B) * os * 4, cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaStreamSynchronize(c->cs));
+    for (int b = 0; b < B; ++b) {
+      const int n = hn[b];
+      if (out_n) out_n[b] = n;
+      if (out_tokens) std::memcpy(out_tokens + size_t(b) * stride, ht + size_t(b) * os, size_t(std::min(n, cap)) * 4);
+      if (opt_path)
+        std::memcpy(opt_path + size_t(b) * stride, ht + size_t(B) * os + size_t(b) * os, size_t(std::min(n, cap)) * 4);
+      c->Pb[b] += n;
+      total += n;
+    }
+  }
+  c->P = c->Pb[0];
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, c->e0, c->e1) == cudaSuccess) c->st.draft_ms += ms;
   if (cudaEventElapsedTime(&ms, c->e1, c->e2) == cudaSuccess) c->st.verify_ms += ms;
   if (cudaEventElapsedTime(&ms, c->e2, c->e3) == cudaSuccess) c->st.accept_ms += ms;
   cudaGetLastError();
   c->st.steps++;
-  c->st.tokens_emitted += n;
+  c->st.tokens_emitted += total;
   c->st.committed_len = c->P;
   c->st.gpu_launches = c->launches;
   harvest_timing(c);
@@ -1461,15 +1573,25 @@ static ss_status accept_impl(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int
 
 ss_status ss_accept_and_commit(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path) {
   GUARD(c);
-  return accept_impl(c, out_tokens, out_n, opt_path);
+  return accept_impl(c, out_tokens, out_n, opt_path, c->cur_deff + 1);
 }
 
 ss_status ss_step(ss_ctx* c, const ss_draft_params* p, int32_t* out_tokens, int32_t* out_n) {
   GUARD(c);
+  if (c->B != 1) return fail(c, SS_ERR_STRUCTURE, "ss_step is the one-request step; use ss_step_batch");
   ss_status s = draft_impl(c, -1, p);
   if (s != SS_OK) return s;
   if ((s = verify_impl(c)) != SS_OK) return s;
-  return accept_impl(c, out_tokens, out_n, nullptr);
+  return accept_impl(c, out_tokens, out_n, nullptr, c->cur_deff + 1);
+}
+
+ss_status ss_step_batch(ss_ctx* c, const ss_draft_params* p, int32_t stride, int32_t* out_tokens, int32_t* out_n) {
+  GUARD(c);
+  if (!p || !out_tokens || !out_n || stride < p->depth + 1) return fail(c, SS_ERR_INVALID, "step_batch args");
+  ss_status s = draft_impl(c, -1, p);
+  if (s != SS_OK) return s;
+  if ((s = verify_impl(c)) != SS_OK) return s;
+  return accept_impl(c, out_tokens, out_n, nullptr, stride);
 }
 
 ss_status ss_generate(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t max_new, int32_t chunk,
@@ -1477,6 +1599,7 @@ ss_status ss_generate(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t max_n
   GUARD(c);
   if (!p || !out_tokens || max_new < 1) return fail(c, SS_ERR_INVALID, "generate args");
   if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "generate inside a step");
+  if (c->B != 1) return fail(c, SS_ERR_STRUCTURE, "ss_generate is the one-request loop; use ss_generate_batch");
   int32_t first = 0;
   ss_status s = ss_prefill(c, prompt, n, chunk, &first);
   if (s != SS_OK) return s;
@@ -1497,6 +1620,44 @@ ss_status ss_generate(ss_ctx* c, const int32_t* prompt, int32_t n, int32_t max_n
     for (int i = 0; i < m && produced < max_new; ++i) out_tokens[produced++] = buf[i];
   }
   if (out_n) *out_n = produced;
+  return SS_OK;
+}
+
+ss_status ss_generate_batch(ss_ctx* c, int32_t n_req, const int32_t* prompts, const int32_t* prompt_lens,
+                            int32_t max_new, int32_t chunk, const ss_draft_params* p, int32_t* out_tokens,
+                            int32_t* out_n, int32_t* tau_hist) {
+  GUARD(c);
+  if (!p || !prompts || !prompt_lens || !out_tokens || !out_n || max_new < 1)
+    return fail(c, SS_ERR_INVALID, "generate_batch args");
+  ss_status s = ss_set_batch(c, n_req);
+  if (s != SS_OK) return s;
+  std::vector<int> produced(size_t(n_req), 0);
+  int64_t off = 0;
+  for (int b = 0; b < n_req; ++b) {
+    int32_t first = 0;
+    if ((s = prefill_slot_impl(c, b, prompts + off, prompt_lens[b], chunk, &first)) != SS_OK) return s;
+    off += prompt_lens[b];
+    out_tokens[size_t(b) * max_new] = first;
+    produced[b] = 1;
+  }
+  ss_draft_params q = *p;
+  if (p->depth == 0) q.top_k = 1;
+  const int stride = q.depth + 1;
+  std::vector<int32_t> buf(size_t(n_req) * stride);
+  std::vector<int32_t> m(static_cast<size_t>(n_req));
+  // every slot steps until the slowest one has max_new tokens (the others' surplus is dropped)
+  while (*std::min_element(produced.begin(), produced.end()) < max_new) {
+    int Pmax = 0;
+    for (int b = 0; b < n_req; ++b) Pmax = std::max(Pmax, c->Pb[b]);
+    if (Pmax + 1 > c->C) break;
+    if ((s = ss_step_batch(c, &q, stride, buf.data(), m.data())) != SS_OK) return s;
+    for (int b = 0; b < n_req; ++b) {
+      if (produced[b] >= max_new) continue;
+      if (tau_hist && m[b] >= 0 && m[b] <= p->depth + 1) tau_hist[m[b]]++;
+      for (int i = 0; i < m[b] && produced[b] < max_new; ++i) out_tokens[size_t(b) * max_new + produced[b]++] = buf[size_t(b) * stride + i];
+    }
+  }
+  for (int b = 0; b < n_req; ++b) out_n[b] = produced[b];
   return SS_OK;
 }
 
@@ -1720,6 +1881,8 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = base_epi(c, M);
     p.epi.kind = EPI_STORE;
+    static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
+    p.self_pf = head ? 0 : (self_pf >> g) & 1;
     p.epi.out = c->at_o;
     p.epi.ldo = N;
     launch_gemv(!head && !w.resident, p, c->gv_grid, c->use_pdl, c->cs);
@@ -1965,7 +2128,7 @@ ss_status ss_debug_read_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, ui
     return fail(c, SS_ERR_INVALID, "read_kv args");
   CK(cudaStreamSynchronize(c->cs));
   for (int h = 0; h < c->nkv; ++h) {
-    const int64_t src = layer * c->kc_layer + (int64_t(h) * c->C + pos0) * c->d;
+    const int64_t src = layer * c->kc_layer + (int64_t(h) * c->kv_ctx + pos0) * c->d;
     CK(cudaMemcpyAsync(k + int64_t(h) * n * c->d, c->kc + src, size_t(n) * c->d * 2, cudaMemcpyDeviceToHost, c->cs));
     CK(cudaMemcpyAsync(v + int64_t(h) * n * c->d, c->vc + src, size_t(n) * c->d * 2, cudaMemcpyDeviceToHost, c->cs));
   }

@@ -103,7 +103,7 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
       // item = (RoPE pair u, token m): rows (lo, lo + d/2) of one head; bias + rotate-half RoPE at
       // pos = P + depth(node) on (acc + bias) in fp32, then one bf16 rounding (reading R3).
       const int d = e.head_dim, half = d >> 1;
-      const int P = *e.committed_len;
+      const int P0 = e.committed_len[e.rq.req0];
       const int nitems = (kTileRows / 2) * ncols;
       for (int it = tid; it < nitems; it += nthreads) {
         const int u = it / ncols, m = it % ncols;
@@ -116,7 +116,9 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
           vlo += bf2f(e.bias[rlo]);
           vhi += bf2f(e.bias[rhi]);
         }
-        const int node = e.node_base + mg;
+        const int rb = rq_req(e.rq, mg);   // batched requests: request rb's local node, strided slot
+        const int node = rb * e.rq.node_stride + e.node_base + rq_loc(e.rq, mg);
+        const int P = e.rq.rows > 0 ? e.committed_len[rb] : P0;
         const int i = u % half;
         if (rlo < e.q_dim + e.kv_dim) {   // q or k head: rotate
           const float2 cs = e.rope[(P + e.depth[node]) * half + i];

@@ -125,6 +125,32 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         issue_w(i, w, n);
         w.next(nC, n);
       }
+      // L2 prefetch of this CTA's own remaining weights (beyond the ring): raises the bytes in
+      // flight from the ring depth to the whole work range, so the DRAM queue stays full and the
+      // ring refills from L2
+      if (p.self_pf) {
+        Work wp = w;
+        int64_t run0 = -1, run1 = -1;
+        auto flush = [&]() {
+          for (int64_t o = run0; o < run1; o += 65536) {
+            const int64_t n = run1 - o < 65536 ? run1 - o : 65536;
+            prefetch_l2(p.W + o, uint32_t(n));
+          }
+        };
+        while (wp.left > 0) {
+          const int n = wp.take(C::kCPS);
+          const int64_t b = (int64_t(wp.r) * nC + wp.c) * C::kWBytes, e = b + int64_t(n) * C::kWBytes;
+          if (b == run1) {
+            run1 = e;
+          } else {
+            if (run0 >= 0) flush();
+            run0 = b;
+            run1 = e;
+          }
+          wp.next(nC, n);
+        }
+        if (run0 >= 0) flush();
+      }
       // L2 prefetch of the next matrix (independent of every activation): this CTA's slice, in
       // 64 KB TMA prefetches, so HBM keeps streaming through the dependent steps that follow
       if (p.pf && p.pf_bytes > 0) {

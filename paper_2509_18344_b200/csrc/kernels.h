@@ -5,6 +5,19 @@
 
 namespace ss {
 
+// Batched requests: row m of a pass belongs to request req0 + m / rows and is
+// that request's local node node_base + m % rows.  Per-request state is strided: tree arrays and
+// tree-KV rows by node_stride, committed-KV rows by ctx_stride, committed_len / root_tok by 1.
+// The zero map (rows = 0) is the single-request case: request req0 for every row, no offsets.
+struct ReqMap {
+  int rows;         // rows per request in this pass (0: all rows belong to request req0)
+  int req0;         // first request of the pass
+  int node_stride;  // per-request node capacity NS
+  int ctx_stride;   // per-request committed-KV rows C
+};
+__host__ __device__ inline int rq_req(const ReqMap& r, int m) { return r.rows > 0 ? r.req0 + m / r.rows : r.req0; }
+__host__ __device__ inline int rq_loc(const ReqMap& r, int m) { return r.rows > 0 ? m % r.rows : m; }
+
 enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5, EPI_RESID_SS = 6, EPI_RESID_NORM = 7 };
 
 // Epilogue parameters shared by the GEMV (draft, M <= 32) and GEMM (verify) kernels.
@@ -16,9 +29,10 @@ struct EpiParams {
   uint16_t* q_out;               // [M x q_dim] bf16 natural
   uint16_t* k_tree;              // this layer's tree scratch K [n_kv][max_nodes][d]
   uint16_t* v_tree;
-  int max_nodes, node_base;
-  const int* committed_len;      // device P
-  const int* depth;              // per-node depth (indexed node_base + m)
+  int max_nodes, node_base;      // max_nodes: tree-KV rows per kv head (all requests)
+  const int* committed_len;      // device P (per request)
+  const int* depth;              // per-node depth (request b, row m: b * rq.node_stride + node_base + local m)
+  ReqMap rq;                     // batched requests (zero: one request)
   const float2* rope;            // [max_ctx][d/2] (cos, sin)
   int q_dim, kv_dim, head_dim;
   // EPI_RESID
@@ -63,6 +77,7 @@ struct GemvParams {
   unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
   int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
+  int self_pf;                   // prefetch this CTA's own remaining weight range into L2 at entry
   // xnorm (cluster mode): instead of TMA-ing X/XS, the consumers build this CTA's K range of
   // X = bf16(x * r_m * gain) (RMSNorm of the residual stream, r_m from per-tile sums of squares)
   // and its group sums in shared memory once, before the main loop
@@ -126,7 +141,7 @@ void launch_tiled_to_natural(const uint8_t* t, uint16_t* out, int64_t N, int64_t
 // small kernels (K4, K5, K8, K9)
 void launch_embed_rmsnorm(const int* tokens_dev, int tok_offset, int M, const uint16_t* embed, float* x, int H,
                           const uint16_t* gain, float eps, uint16_t* h_fragx, float* h_xs, int nt, bool pdl,
-                          cudaStream_t st);
+                          cudaStream_t st, ReqMap rq = ReqMap{0, 0, 0, 0});
 void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float eps, uint16_t* h_fragx, float* h_xs,
                     int nt, bool pdl, cudaStream_t st);
 
@@ -139,8 +154,9 @@ struct AttnParams {
   const int* committed_len;
   const int* anc;                // [max_nodes][anc_stride] ancestor slots root..self
   const int* depth;              // [max_nodes]
-  int anc_stride, max_ctx, max_nodes;
+  int anc_stride, max_ctx, max_nodes;   // max_ctx / max_nodes: rows per kv head (all requests)
   int n_q, node_base;            // query rows are nodes node_base .. node_base + n_q - 1
+  ReqMap rq;                     // batched requests (zero: one request)
   int n_heads, n_kv, head_dim;
   int split;                     // prefix keys per segment
   int n_seg_max;                 // segments allocated in the partial buffers
@@ -176,6 +192,8 @@ struct TopkParams {
   int node_base;                 // frontier nodes node_base .. node_base + M - 1
   int child_base;                // new nodes child_base .. child_base + k - 1
   int child_depth;
+  int req_rows;                  // batched: frontier rows per request (0: all M rows, one request);
+  int node_stride;               // one select CTA per request, tree arrays strided by node_stride
 };
 void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st);
 
@@ -201,6 +219,9 @@ struct AcceptParams {
   int64_t cache_layer_stride, tree_layer_stride;   // elements
   int n_layers, n_kv, head_dim, max_ctx, max_nodes;
   int chain;                     // 1: commit all nodes (prefill chunk), ignore argmax
+  // batched requests: request b = req0 + blockIdx; argmax rows by n_nodes, tree arrays / tree-KV rows
+  // by node_stride, committed-KV rows by ctx_stride, outputs by out_stride, meta by 2
+  int n_req, req0, node_stride, ctx_stride, out_stride;
 };
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st);
 
@@ -249,7 +270,7 @@ int pass_max_segments(int N, int K, int grid);
 
 // tree init for a new step: root node (slot 0) with token *root_tok, depth 0
 void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,
-                      cudaStream_t st);
+                      cudaStream_t st, int n_req = 1, int node_stride = 0, int anc_stride = 0);
 // chain tree for prefill chunk: tokens copied from device buffer
 void launch_chain_init(const int* tokens, int n, int* tok, int* parent, int* depth, float* score, int* anc,
                        int anc_stride, cudaStream_t st);

@@ -42,14 +42,15 @@ SS_DEV float block_sum_256(float v, float* red) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const int* tokens, int tok_offset, const uint16_t* embed,
                                                       float* x, int H, const uint16_t* gain, float eps,
-                                                      uint16_t* out, float* xs, int nt) {
+                                                      uint16_t* out, float* xs, int nt, ReqMap rq) {
   __shared__ float red[9];
   const int m = blockIdx.x;
   griddep_launch();   // small grid: let the next kernel start its prologue (weight prefetch) now
   griddep_wait();
   float* xr = x + int64_t(m) * H;
   if (embed) {
-    const uint16_t* er = embed + int64_t(tokens[tok_offset + m]) * H;
+    const int node = rq_req(rq, m) * rq.node_stride + tok_offset + rq_loc(rq, m);   // batched requests
+    const uint16_t* er = embed + int64_t(tokens[node]) * H;
     for (int i = threadIdx.x; i < H; i += 256) xr[i] = bf2f(er[i]);
     __syncthreads();
   }
@@ -75,8 +76,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const int* tokens, int tok
 
 void launch_embed_rmsnorm(const int* tokens_dev, int tok_offset, int M, const uint16_t* embed, float* x, int H,
                           const uint16_t* gain, float eps, uint16_t* h_fragx, float* h_xs, int nt, bool pdl,
-                          cudaStream_t st) {
-  void* args[] = {&tokens_dev, &tok_offset, &embed, &x, &H, &gain, &eps, &h_fragx, &h_xs, &nt};
+                          cudaStream_t st, ReqMap rq) {
+  void* args[] = {&tokens_dev, &tok_offset, &embed, &x, &H, &gain, &eps, &h_fragx, &h_xs, &nt, &rq};
   launch_pdl((const void*)rmsnorm_kernel, dim3(M), dim3(256), 0, pdl, st, args);
 }
 void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float eps, uint16_t* h_fragx, float* h_xs,
@@ -85,7 +86,8 @@ void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float ep
   int off = 0;
   const uint16_t* embed = nullptr;
   float* xx = const_cast<float*>(x);
-  void* args[] = {&tokens, &off, &embed, &xx, &H, &gain, &eps, &h_fragx, &h_xs, &nt};
+  ReqMap rq{0, 0, 0, 0};
+  void* args[] = {&tokens, &off, &embed, &xx, &H, &gain, &eps, &h_fragx, &h_xs, &nt, &rq};
   launch_pdl((const void*)rmsnorm_kernel, dim3(M), dim3(256), 0, pdl, st, args);
 }
 
@@ -291,28 +293,35 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
   griddep_launch();   // small grid: let the next kernel start its prologue (weight prefetch) now
   griddep_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < p.M) {
-    const int m = threadIdx.x;
+  // batched requests: CTA q selects request q's children from its own frontier rows [r0, r0 + Mr)
+  const int q = blockIdx.x;
+  const int Mr = p.req_rows > 0 ? p.req_rows : p.M, r0 = q * Mr;
+  const int64_t nofs = int64_t(q) * p.node_stride;
+  if (threadIdx.x < Mr) {
+    const int m = threadIdx.x, mg = r0 + m;
     float mx = -INFINITY;
-    for (int b = 0; b < B; ++b) mx = fmaxf(mx, p.blk_max[m * B + b]);
+    for (int b = 0; b < B; ++b) mx = fmaxf(mx, p.blk_max[mg * B + b]);
     float s = 0.f;
-    for (int b = 0; b < B; ++b) s += p.blk_sum[m * B + b] * expf((p.blk_max[m * B + b] - mx) * p.inv_t);
+    for (int b = 0; b < B; ++b) s += p.blk_sum[mg * B + b] * expf((p.blk_max[mg * B + b] - mx) * p.inv_t);
     rmax[m] = mx;
     lse[m] = logf(s);
   }
   __syncthreads();
-  const int ncand = p.M * B * p.k;
+  const int ncand = Mr * B * p.k;
+  const int* blk_idx = p.blk_idx + int64_t(r0) * B * p.k;
+  const float* blk_val = p.blk_val + int64_t(r0) * B * p.k;
+  const float* score = p.score + nofs;
   for (int r = 0; r < p.k; ++r) {
     float bs = -INFINITY;
     int bt = INT32_MAX, bp = INT32_MAX, bc = -1;
     for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
       const int m = c / (B * p.k);
-      const int tok = p.blk_idx[c];
+      const int tok = blk_idx[c];
       bool tk = false;
       for (int q = 0; q < r; ++q) tk |= (sel_t[q] == tok && sel_p[q] == m);
       if (tk) continue;
-      const float lp = (p.blk_val[c] - rmax[m]) * p.inv_t - lse[m];
-      const float sc = p.score[p.node_base + m] + lp;
+      const float lp = (blk_val[c] - rmax[m]) * p.inv_t - lse[m];
+      const float sc = score[p.node_base + m] + lp;
       if (sc > bs || (sc == bs && (tok < bt || (tok == bt && m < bp)))) {
         bs = sc;
         bt = tok;
@@ -372,17 +381,18 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
     }
   }
   __syncthreads();
+  int* anc = p.anc + nofs * p.anc_stride;   // slots, parents and ancestors are request-local
   for (int j = warp; j < p.k; j += blockDim.x >> 5) {
     const int node = p.child_base + j, par = p.node_base + sel_p[j];
     if (lane == 0) {
-      p.tok[node] = sel_t[j];
-      p.parent[node] = par;
-      p.depth[node] = p.child_depth;
-      p.score[node] = sel_s[j];
+      p.tok[nofs + node] = sel_t[j];
+      p.parent[nofs + node] = par;
+      p.depth[nofs + node] = p.child_depth;
+      p.score[nofs + node] = sel_s[j];
     }
     for (int a = lane; a < p.child_depth; a += 32)
-      p.anc[int64_t(node) * p.anc_stride + a] = p.anc[int64_t(par) * p.anc_stride + a];
-    if (lane == 0) p.anc[int64_t(node) * p.anc_stride + p.child_depth] = node;
+      anc[int64_t(node) * p.anc_stride + a] = anc[int64_t(par) * p.anc_stride + a];
+    if (lane == 0) anc[int64_t(node) * p.anc_stride + p.child_depth] = node;
   }
 }
 
@@ -390,7 +400,8 @@ void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
   TopkParams pp = p;
   void* args[] = {&pp};
   launch_pdl((const void*)topk_block_kernel, dim3(p.M, p.blocks_per_row), dim3(256), 0, pdl, st, args);
-  launch_pdl((const void*)topk_select_kernel, dim3(1), dim3(1024), 32 * 4 * 5, pdl, st, args);
+  const int n_req = p.req_rows > 0 ? p.M / p.req_rows : 1;
+  launch_pdl((const void*)topk_select_kernel, dim3(n_req), dim3(1024), 32 * 4 * 5, pdl, st, args);
 }
 
 // ---------------------------------------------------------------------------
@@ -443,9 +454,21 @@ void launch_argmax_merge(const float* am_val, const int* am_idx, const float* am
 // K9: greedy acceptance (one warp, ballot over the <= 32 children of each depth) and the
 // KV commit/compaction of root + accepted path into committed positions P..P+a.
 // ---------------------------------------------------------------------------
-__global__ void accept_kernel(const AcceptParams p) {
+__global__ void accept_kernel(const AcceptParams p0) {
   griddep_launch();   // small grid: let the next kernel start its prologue (weight prefetch) now
   griddep_wait();
+  // batched requests: one warp per request, every per-request array offset by its stride
+  const int q = p0.req0 + blockIdx.x;
+  AcceptParams p = p0;
+  p.argmax += int64_t(blockIdx.x) * p0.n_nodes;
+  p.tok += int64_t(q) * p0.node_stride;
+  p.parent += int64_t(q) * p0.node_stride;
+  p.commit_meta += 2 * q;
+  p.committed_len += q;
+  p.root_tok += q;
+  p.out_tokens += int64_t(q) * p0.out_stride;
+  p.out_n += q;
+  p.out_path += int64_t(q) * p0.out_stride;
   const int lane = threadIdx.x;
   int n = 1, cur = 0;
   if (p.chain) {
@@ -488,14 +511,17 @@ __global__ void accept_kernel(const AcceptParams p) {
 __global__ void __launch_bounds__(256) commit_kernel(const AcceptParams p) {
   griddep_launch();   // small grid: let the next kernel start its prologue (weight prefetch) now
   griddep_wait();
-  const int l = blockIdx.x, h = blockIdx.y, which = blockIdx.z;
-  const int base = p.commit_meta[0], n = p.commit_meta[1];
-  uint16_t* cache = (which ? p.v_cache : p.k_cache) + l * p.cache_layer_stride + int64_t(h) * p.max_ctx * p.head_dim;
-  const uint16_t* tree = (which ? p.v_tree : p.k_tree) + l * p.tree_layer_stride + int64_t(h) * p.max_nodes * p.head_dim;
+  const int l = blockIdx.x, h = blockIdx.y, which = blockIdx.z & 1, q = p.req0 + (blockIdx.z >> 1);
+  const int base = p.commit_meta[2 * q], n = p.commit_meta[2 * q + 1];
+  uint16_t* cache = (which ? p.v_cache : p.k_cache) + l * p.cache_layer_stride +
+                    (int64_t(h) * p.max_ctx + int64_t(q) * p.ctx_stride) * p.head_dim;
+  const uint16_t* tree = (which ? p.v_tree : p.k_tree) + l * p.tree_layer_stride +
+                         (int64_t(h) * p.max_nodes + int64_t(q) * p.node_stride) * p.head_dim;
+  const int* path = p.out_path + int64_t(q) * p.out_stride;
   const int dw = p.head_dim / 2;
   for (int e = threadIdx.x; e < n * dw; e += 256) {
     const int j = e / dw, i = e % dw;
-    const int slot = p.out_path[j];
+    const int slot = path[j];
     reinterpret_cast<uint32_t*>(cache + int64_t(base + j) * p.head_dim)[i] =
         reinterpret_cast<const uint32_t*>(tree + int64_t(slot) * p.head_dim)[i];
   }
@@ -504,23 +530,27 @@ __global__ void __launch_bounds__(256) commit_kernel(const AcceptParams p) {
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st) {
   AcceptParams pp = p;
   void* args[] = {&pp};
-  launch_pdl((const void*)accept_kernel, dim3(1), dim3(32), 0, pdl, st, args);
-  launch_pdl((const void*)commit_kernel, dim3(p.n_layers, p.n_kv, 2), dim3(256), 0, pdl, st, args);
+  const int n_req = p.n_req > 0 ? p.n_req : 1;
+  launch_pdl((const void*)accept_kernel, dim3(n_req), dim3(32), 0, pdl, st, args);
+  launch_pdl((const void*)commit_kernel, dim3(p.n_layers, p.n_kv, 2 * n_req), dim3(256), 0, pdl, st, args);
 }
 
-__global__ void tree_init_kernel(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc) {
+__global__ void tree_init_kernel(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc,
+                                 int node_stride, int anc_stride) {
   griddep_launch();   // small grid: let the next kernel start its prologue (weight prefetch) now
   griddep_wait();
-  tok[0] = *root_tok;
-  parent[0] = -1;
-  depth[0] = 0;
-  score[0] = 0.f;
-  anc[0] = 0;
+  const int q = threadIdx.x;   // request q's root at its slot 0
+  const int64_t o = int64_t(q) * node_stride;
+  tok[o] = root_tok[q];
+  parent[o] = -1;
+  depth[o] = 0;
+  score[o] = 0.f;
+  anc[o * anc_stride] = 0;
 }
 void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,
-                      cudaStream_t st) {
-  void* args[] = {&root_tok, &tok, &parent, &depth, &score, &anc};
-  launch_pdl((const void*)tree_init_kernel, dim3(1), dim3(1), 0, pdl, st, args);
+                      cudaStream_t st, int n_req, int node_stride, int anc_stride) {
+  void* args[] = {&root_tok, &tok, &parent, &depth, &score, &anc, &node_stride, &anc_stride};
+  launch_pdl((const void*)tree_init_kernel, dim3(1), dim3(n_req < 1 ? 1 : n_req), 0, pdl, st, args);
 }
 
 __global__ void chain_init_kernel(const int* tokens, int n, int* tok, int* parent, int* depth, float* score, int* anc,
