@@ -45,6 +45,8 @@ def args_():
     ap.add_argument("--depth", type=int, default=48)
     ap.add_argument("--topk", type=int, default=6)
     ap.add_argument("--temp", type=float, default=0.2)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="request slots per GPU sharing one weight stream (SURVEY 8(f) NEXT-2); 1 = the paper's batch 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -204,10 +206,11 @@ def run_reference(a):
 
 
 def workload_config(a, cfg):
+    batch = "" if a.batch == 1 else f", {a.batch} requests per GPU sharing one weight stream (NEXT-2)"
     return {"workload": f"{cfg.name} SubSpec step, {a.cap_gib:g} GiB cap, n_resident={a.n_resident}, "
-                        f"4-bit g64 substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt",
+                        f"4-bit g64 substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt{batch}",
             "model_shape": cfg.name, "vram_cap_gib": a.cap_gib, "n_resident": a.n_resident, "depth": a.depth,
-            "top_k": a.topk, "sharpen_t": a.temp, "batch": 1, "max_context": cfg.max_context,
+            "top_k": a.topk, "sharpen_t": a.temp, "batch": a.batch, "max_context": cfg.max_context,
             "l2": "inputs larger than L2 (>= 4.76 GB of draft weights per draft pass; 13 GB streamed per verify)",
             "parallelism": f"requests partitioned, {a.gpus} GPU(s), no collective"}
 
@@ -301,14 +304,22 @@ def run_ours(a):
     cfg = PRESETS[a.config]
     D, k, T = a.depth, a.topk, a.temp
     t_setup = time.time()
-    ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256)
+    Bq = a.batch
+    ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256,
+                 max_batch=Bq)
     shm = load_weights_for_job(ss, dist, local, a.n_resident)
     ss.build_substitutes(4, 64)
-    prompt = request_for_rank(rank, cfg.vocab)
-    ss.prefill(prompt)
+    if Bq == 1:
+        ss.prefill(request_for_rank(rank, cfg.vocab))
+        step = lambda: [ss.step(D, k, T)]                     # noqa: E731
+    else:   # rank r decodes requests r*B .. r*B + B - 1, all B in one step
+        ss.set_batch(Bq)
+        for b in range(Bq):
+            ss.prefill_slot(b, request_for_rank(rank * Bq + b, cfg.vocab))
+        step = lambda: ss.step_batch(Bq, D, k, T)            # noqa: E731
     t_setup = time.time() - t_setup
     for _ in range(a.warmup):
-        ss.step(D, k, T)
+        step()
     ss.reset_stats()
     cs = ss.compute_stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -320,9 +331,9 @@ def run_ours(a):
     e0.record(cs)
     emitted, taus = 0, []
     for _ in range(a.steps):
-        t = ss.step(D, k, T)
-        emitted += len(t)
-        taus.append(len(t))
+        for t in step():
+            emitted += len(t)
+            taus.append(len(t))
     e1.record(cs)
     torch.cuda.synchronize()
     if dist:
@@ -331,7 +342,7 @@ def run_ours(a):
     ms = e0.elapsed_time(e1)
     st = ss.stats()
     # ---- dominant kernel: K2 dequant-GEMV, live sweep over every layer (weights from HBM) ----
-    M = k
+    M = k * Bq   # frontier rows of a draft pass (all requests)
     groups = [ss.group_shape(g) for g in range(4)]
     per_group = {}
     for g, name in enumerate(("qkv", "o", "gate_up", "down")):
@@ -345,7 +356,26 @@ def run_ours(a):
     head_gbs = (cfg.vocab * cfg.hidden * 2 + M * cfg.hidden * 2 + M * cfg.vocab * 4) / (t_head * 1e-3) / 1e9
     # ---- e2e through the C-ABI with host buffers: root token H2D, emitted tokens D2H ----
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and Bq > 1:
+        # batched: ss_step_batch's host outputs are the step's D2H; roots stay on the device
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st0 = ss.stats()
+        t0 = time.perf_counter()
+        e2e_tok = 0
+        n_e2e = max(2, a.steps // 2)
+        for _ in range(n_e2e):
+            e2e_tok += sum(len(t) for t in step())
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        st1 = ss.stats()
+        wall, e2e_tok = aggregate_ranks(dist, wall, e2e_tok, dist_device(local))
+        streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / n_e2e
+        e2e = {"value": e2e_tok / wall, "unit": "tokens/s", "h2d_bytes_per_step": int(streamed),
+               "d2h_bytes_per_step": int(4 * Bq * (D + 2)),
+               "h2d_breakdown": {"streamed_layer_weights": int(streamed)}, "steps": n_e2e}
+    elif not a.no_e2e:
         root = int(ss.step(D, k, T)[-1])
         if dist:
             dist.barrier()
@@ -402,10 +432,11 @@ def run_ours(a):
         "data": "synthetic (seeded random-init bf16 weights of the named shape; MT-Bench-shaped prompts)",
         "config": workload_config(a, cfg),
         "tau_mean": tau, "tau_hist": np.bincount(taus, minlength=D + 2).tolist(), "steps_per_s": steps_per_s,
-        "tokens_per_s_at_paper_tau_27.08": 27.08 * steps_per_s,
+        "tokens_per_s_at_paper_tau_27.08": 27.08 * steps_per_s * Bq,
+        "requests_per_gpu": Bq,
         "step_breakdown_ms": {"draft": st["draft_ms"] / a.steps, "verify": st["verify_ms"] / a.steps,
                               "accept": st["accept_ms"] / a.steps},
-        "roofline": {"kernel": "K2 dequant-GEMV (4-bit g64 substitutes, M=k tokens), all layers x 4 groups",
+        "roofline": {"kernel": f"K2 dequant-GEMV (4-bit g64 substitutes, M={M} tokens), all layers x 4 groups",
                      "bound": "hbm", "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      "per_group": per_group, "head_bf16_gemv_gbs": head_gbs},
@@ -421,7 +452,7 @@ def run_ours(a):
     }
     if rank == 0:
         os.makedirs(os.path.dirname(TAU_FILE), exist_ok=True)
-        if world == 1:
+        if world == 1 and Bq == 1:
             try:
                 json.dump({"config": a.config, "tau": tau, "steps": a.steps, "note": "deterministic seeded workload"},
                           open(TAU_FILE, "w"))
