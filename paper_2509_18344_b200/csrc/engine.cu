@@ -195,7 +195,10 @@ ss_status check_launch(ss_ctx* c, const char* what) {
 size_t q4_bytes(int N, int K) { return size_t(N / 128) * (K / 128) * kQ4TileBytes; }
 size_t bf16_bytes(int N, int K) { return size_t(N) * K * 2; }
 
-int gemv_nt(int M) { return M <= 8 ? 1 : (M <= 16 ? 2 : 4); }
+// token tiles of 8 for a draft GEMV over M <= 32 rows: M = 17..24 (e.g. 4 batched requests x k = 6)
+// uses 3 tiles, since the legacy MMA pipe time grows with the tile count
+int gemv_nt(int M) { return M <= 8 ? 1 : (M <= 16 ? 2 : (M <= 24 ? 3 : 4)); }
+int gemv_nt_pow2(int M) { return M <= 8 ? 1 : (M <= 16 ? 2 : 4); }   // the persistent pass (pass.cu)
 int gemm_nt(int M) { return ((M + 127) / 128) * 16; }
 
 // ---------------------------------- K7 streaming ------------------------------------------
@@ -477,7 +480,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
       r.norm_gain = gain;
       r.norm_out = c->hfrag;
       r.norm_xs = c->hxs;
-      r.norm_ctr = c->norm_ctr + (which * 2 + (c->lw[l].resident ? 1 : 0)) * 3 + (NT == 1 ? 0 : NT == 2 ? 1 : 2);
+      r.norm_ctr = c->norm_ctr + (which * 2 + (c->lw[l].resident ? 1 : 0)) * 4 + (NT - 1);   // NT in 1..4
       r.n_tiles = c->H / 128;
       r.eps = eps;
       r.act_nt = NT;
@@ -660,7 +663,7 @@ ss_status launch_fused_pass(ss_ctx* c, int M, int base, int child_base, int chil
   p.ph = c->d_phases;
   p.n_ph = int(c->phases.size());
   p.M = M;
-  p.NT = gemv_nt(M);
+  p.NT = gemv_nt_pow2(M);
   p.node_base = base;
   p.H = c->H;
   p.eps = c->cfg.rms_eps;
@@ -981,7 +984,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
   c->pass_bar = (unsigned*)chk(A(256));
   c->attn_ctr = (int*)chk(A(size_t(32) * c->nkv * 4));
-  c->norm_ctr = (unsigned long long*)chk(A(256));   // 18 monotonic counters, zeroed below
+  c->norm_ctr = (unsigned long long*)chk(A(256));   // 24 monotonic counters (3 x 2 formats x NT 1..4), zeroed below
   c->mlp_flags = (int*)chk(A(size_t(2 * c->F / 128 + 1) * 32 * 4));
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32

@@ -496,6 +496,7 @@ bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms) {
   switch (NT) {
     case 1: return q4 ? cluster_plan<true, 1>(N, K, sms).all_resident : cluster_plan<false, 1>(N, K, sms).all_resident;
     case 2: return q4 ? cluster_plan<true, 2>(N, K, sms).all_resident : cluster_plan<false, 2>(N, K, sms).all_resident;
+    case 3: return q4 ? cluster_plan<true, 3>(N, K, sms).all_resident : cluster_plan<false, 3>(N, K, sms).all_resident;
     case 4: return q4 ? cluster_plan<true, 4>(N, K, sms).all_resident : cluster_plan<false, 4>(N, K, sms).all_resident;
     default: return false;
   }
@@ -552,6 +553,7 @@ void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t 
   switch (p.NT) {
     case 1: q4 ? launch_mode<true, 1>(p, grid, pdl, st) : launch_mode<false, 1>(p, grid, pdl, st); break;
     case 2: q4 ? launch_mode<true, 2>(p, grid, pdl, st) : launch_mode<false, 2>(p, grid, pdl, st); break;
+    case 3: q4 ? launch_mode<true, 3>(p, grid, pdl, st) : launch_mode<false, 3>(p, grid, pdl, st); break;
     case 4: q4 ? launch_mode<true, 4>(p, grid, pdl, st) : launch_mode<false, 4>(p, grid, pdl, st); break;
     default: break;
   }
