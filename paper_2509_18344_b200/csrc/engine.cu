@@ -366,6 +366,11 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.pre_after = (pre_after >> g) & 1;   // bit g: group g issues its first stages after the wait
     static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
     p.self_pf = (self_pf >> g) & 1;        // bit g: group g prefetches its own range into L2
+    // qkv substitutes: plan one CTA per SM.  Its whole per-CTA weight range (9.3 MB / 144 CTAs =
+    // 64 KB at Qwen-7B) then sits in the ring before the grid-dependency wait, and the CTAs find
+    // free slots next to the previous layer's down GEMV (2 CTAs on ~84 SMs), so they are resident
+    // and prefetched early (measured: pass 2082 -> 2013 us; o and down are slower at 1 CTA/SM).
+    p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
@@ -1886,6 +1891,7 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.epi.kind = EPI_STORE;
     static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
     p.self_pf = head ? 0 : (self_pf >> g) & 1;
+    p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
     p.epi.out = c->at_o;
     p.epi.ldo = N;
     launch_gemv(!head && !w.resident, p, c->gv_grid, c->use_pdl, c->cs);

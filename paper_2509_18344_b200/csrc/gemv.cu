@@ -27,8 +27,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 
 namespace ss {
 
@@ -363,52 +365,78 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
 
   Work w = make_work<kCluster>(p.N, p.K, crank, csize);
   const int64_t n_items = w.left;
-  int cur_r = w.r, c_first = w.c, c_last = w.c;
   int s = 0;
   uint32_t ph = 0;
+  // Outer loop over this CTA's row tiles, inner loop over the tile's stages: the inner loop is a
+  // compact basic-block chain and the (large) reduction/epilogue code sits after it, so the hot
+  // path never jumps across the flush code (ncu: the single-loop form lost ~20% of the consumer's
+  // issue slots to instruction-fetch stalls on two far branches per stage).
   while (w.left > 0) {
-    if (w.r != cur_r) {
-      flush(cur_r, c_first, c_last, false);
-      cur_r = w.r;
-      c_first = w.c;
+    const int cur_r = w.r, c_first = w.c;
+    int c_last = w.c;
+    do {
+      const int nch = w.take(C::kCPS);
+      c_last = w.c + nch - 1;
+      mbar_wait(&full[s], ph);
+      if (threadIdx.x == 0 && w.left == n_items) {
+        SS_TRACE_CTA0(3);
+        if (ct) ct[2] = gtime();
+      }
+      if (p.xnorm)
+        consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
+                              xsres + (w.c - xc0) * 2 * Mpad);
+      else
+        consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == kStages) {
+        s = 0;
+        ph ^= 1;
+      }
+      w.next(nC, nch);
+    } while (w.left > 0 && w.r == cur_r);
+    const bool last = w.left == 0;
+    if (last && threadIdx.x == 0) {
+      SS_TRACE_CTA0(4);
+      SS_TRACE_MAX(7);
+      if (ct) ct[3] = gtime();
     }
-    const int nch = w.take(C::kCPS);
-    c_last = w.c + nch - 1;
-    mbar_wait(&full[s], ph);
-    if (threadIdx.x == 0 && w.left == n_items) {
-      SS_TRACE_CTA0(3);
-      if (ct) ct[2] = gtime();
-    }
-    if (p.xnorm)
-      consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
-                            xsres + (w.c - xc0) * 2 * Mpad);
-    else
-      consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (++s == kStages) {
-      s = 0;
-      ph ^= 1;
-    }
-    w.next(nC, nch);
+    flush(cur_r, c_first, c_last, last);
   }
-  if (threadIdx.x == 0) {
-    SS_TRACE_CTA0(4);
-    SS_TRACE_MAX(7);
-    if (ct) ct[3] = gtime();
-  }
-  if (n_items > 0) flush(cur_r, c_first, c_last, true);   // the last tile of this CTA
   if (threadIdx.x == 0) {
     SS_TRACE_MAX(6);
     if (ct) ct[4] = gtime();
   }
 }
 
+
+// CTAs per SM of the cluster plan: SS_GEMV_CTAS_PER_SM (default 2), overridable per shape with
+// SS_GEMV_PERSM_OVR="N:K:v,N:K:v" (debug A/B of the plan per matrix group)
+static int per_sm_for(int N, int K, int hint) {
+  static const int env_dflt = env_int("SS_GEMV_CTAS_PER_SM", 0);
+  const int dflt = env_dflt > 0 ? env_dflt : (hint > 0 ? hint : 2);
+  const char* o = getenv("SS_GEMV_PERSM_OVR");
+  while (o && *o) {
+    int n = 0, k = 0, v = 0;
+    if (sscanf(o, "%d:%d:%d", &n, &k, &v) == 3 && n == N && k == K && v > 0) return v;
+    o = strchr(o, ',');
+    if (o) ++o;
+  }
+  return dflt;
+}
+
 // split factor of the cluster mode: ~2 CTAs per SM, <= SS_GEMV_MAX_CLUSTER, <= chunks
-int gemv_cluster_split(int N, int K, int sms) {
+int gemv_cluster_split(int N, int K, int sms, int hint) {
   const int tiles = N / 128, nC = K / 128;
-  static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
-  static const int cap = std::min(env_int("SS_GEMV_MAX_CLUSTER", 8), kGemvMaxCluster);
+  const int per_sm = per_sm_for(N, K, hint);
+  int cap = std::min(env_int("SS_GEMV_MAX_CLUSTER", 8), kGemvMaxCluster);
+  const char* o = getenv("SS_GEMV_SPLIT_OVR");   // debug A/B: "N:K:cap,..." per shape
+  while (o && *o) {
+    int n = 0, k = 0, v = 0;
+    if (sscanf(o, "%d:%d:%d", &n, &k, &v) == 3 && n == N && k == K && v > 0) cap = std::min(v, kGemvMaxCluster);
+    o = strchr(o, ',');
+    if (o) ++o;
+  }
   int S = (per_sm * sms) / tiles;
   if (S < 1) S = 1;
   if (S > cap) S = cap;
@@ -443,18 +471,18 @@ struct ClusterPlan {
   bool all_resident;
 };
 template <bool Q4, int NT>
-static ClusterPlan cluster_plan(int N, int K, int sms) {
+static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   static std::mutex mu;
-  static std::map<std::pair<int, int>, ClusterPlan> cache;
+  static std::map<std::tuple<int, int, int>, ClusterPlan> cache;
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_pair(N, K);
+  const auto key = std::make_tuple(N, K, hint);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   using C = GemvCfg<Q4, NT>;
   const int stages = ensure_attrs<Q4, NT, true>();
   const int tiles = N / 128;
-  static const int per_sm = env_int("SS_GEMV_CTAS_PER_SM", 2);
-  const int S0 = gemv_cluster_split(N, K, sms);
+  const int per_sm = per_sm_for(N, K, hint);
+  const int S0 = gemv_cluster_split(N, K, sms, hint);
   ClusterPlan plan{S0, 0, false};
   for (int S = S0; S >= 1; --S) {
     int ncl = sms * per_sm / S;
@@ -484,8 +512,8 @@ static ClusterPlan cluster_plan(int N, int K, int sms) {
   }
   if (plan.ncl < 1) plan.ncl = 1;
   if (getenv("SS_VERBOSE"))
-    fprintf(stderr, "gemv cluster plan<%d,%d> N=%d K=%d: S=%d clusters=%d all_resident=%d\n", int(Q4), NT, N, K, plan.S,
-            plan.ncl, int(plan.all_resident));
+    fprintf(stderr, "gemv cluster plan<%d,%d> N=%d K=%d hint=%d: S=%d clusters=%d all_resident=%d\n", int(Q4), NT, N, K,
+            hint, plan.S, plan.ncl, int(plan.all_resident));
   cache[key] = plan;
   return plan;
 }
@@ -542,7 +570,7 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
 template <bool Q4, int NT>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
   if (gemv_use_cluster(p.N, p.K, sms)) {
-    const ClusterPlan pl = cluster_plan<Q4, NT>(p.N, p.K, sms);
+    const ClusterPlan pl = cluster_plan<Q4, NT>(p.N, p.K, sms, p.ctas_per_sm);
     launch_t<Q4, NT, true>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {
     launch_t<Q4, NT, false>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);

@@ -8,7 +8,7 @@ namespace ss {
 
 constexpr int kGemvConsumerWarps = 8;
 constexpr int kGemvThreads = (kGemvConsumerWarps + 1) * 32;
-constexpr int kGemvMaxCluster = 8;   // portable cluster size; the split factor never exceeds it
+constexpr int kGemvMaxCluster = 16;  // largest (non-portable) cluster the split factor may use
 #ifndef SS_GEMV_MIN_BLOCKS
 #define SS_GEMV_MIN_BLOCKS 2
 #endif

@@ -78,6 +78,7 @@ struct GemvParams {
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
   int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
   int self_pf;                   // prefetch this CTA's own remaining weight range into L2 at entry
+  int ctas_per_sm;               // cluster plan: resident CTAs per SM to plan for (0 = default 2)
   // xnorm (cluster mode): instead of TMA-ing X/XS, the consumers build this CTA's K range of
   // X = bf16(x * r_m * gain) (RMSNorm of the residual stream, r_m from per-tile sums of squares)
   // and its group sums in shared memory once, before the main loop
