@@ -371,6 +371,16 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     // free slots next to the previous layer's down GEMV (2 CTAs on ~84 SMs), so they are resident
     // and prefetched early (measured: pass 2082 -> 2013 us; o and down are slower at 1 CTA/SM).
     p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
+    static const int pf_down = getenv("SS_PF_DOWN") ? atoi(getenv("SS_PF_DOWN")) : 0;
+    if (pf_down && g == 0 && !w.resident && !c->lw[l].resident) {
+      // L2 prefetch of this layer's down substitute while qkv, attention and o (latency-bound, HBM
+      // mostly idle) run, issued after the dependency wait so it does not compete with the previous
+      // down's stream (SS_PF_DOWN=2: only the first half of the matrix, tiles 0..13)
+      p.pf = w.q4[3];
+      p.pf_bytes = int64_t(q4_bytes(c->gN[3], c->gK[3]));
+      if (pf_down == 2) p.pf_bytes /= 2;
+      p.pf_late = 1;
+    }
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);

@@ -87,7 +87,9 @@ SS_DEV void norm_finish(const EpiParams& e, int r, unsigned long long target, in
 SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r, int m0, int ncols, int tid,
                            int nthreads, float* scratch = nullptr, unsigned long long* trace = nullptr,
                            int arrive_per_tile = 1, bool norm_wait = true, int norm_ncols = 0,
-                           unsigned long long* arrive_target = nullptr) {
+                           unsigned long long* arrive_target = nullptr, const float* xpre = nullptr) {
+  // xpre (optional): the residual rows x[m0 + m][128 r .. 128 r + 127] already in shared memory,
+  // [ncols][128], for EPI_RESID / EPI_RESID_SS / EPI_RESID_NORM
   // debug trace (max over CTAs of %globaltimer): 9 residual stored, 10 norm barrier passed,
   // 11 r computed, 12 epilogue done
   auto tr = [&](int ev) {
@@ -149,7 +151,8 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
         const int m = idx / kTileRows, n = idx % kTileRows;   // coalesced along n
         const int mg = m0 + m;
         if (mg >= e.M) continue;
-        e.x[int64_t(mg) * e.ldx + row0 + n] += tile[n * ld + m];
+        float* xp = e.x + int64_t(mg) * e.ldx + row0 + n;
+        *xp = (xpre ? xpre[m * kTileRows + n] : *xp) + tile[n * ld + m];
       }
       break;
     }
@@ -166,7 +169,7 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
         float v2 = 0.f;
         if (it < nitems && mg < e.M) {
           float* xp = e.x + int64_t(mg) * e.ldx + row0 + n;
-          const float xn = __ldcg(xp) + tile[n * ld + m];
+          const float xn = (xpre ? xpre[m * kTileRows + n] : __ldcg(xp)) + tile[n * ld + m];
           *xp = xn;
           v2 = xn * xn;
         }
@@ -221,12 +224,21 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
         }
         const float s = warp_sum(a);   // u in [0,32) or [32,64) of token m
         if (e.act_xs && ok && (u == 0 || u == 32)) {
-          float* dst = e.act_xs + int64_t(r) * (e.act_nt * 8) + mg;
-          if (u == 0) *dst = s;        // first half; the second half adds after the barrier below
+          if (scratch && ncols <= 32) {
+            scratch[2 * m + (u >> 5)] = s;   // both halves in shared memory, combined below
+          } else {
+            float* dst = e.act_xs + int64_t(r) * (e.act_nt * 8) + mg;
+            if (u == 0) *dst = s;        // first half; the second half adds after the barrier below
+          }
         }
         __syncwarp();
       }
-      if (e.act_xs) {
+      if (e.act_xs && scratch && ncols <= 32) {
+        // group sum = first half + second half (the same fixed order as the two-pass form below)
+        asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+        for (int m = tid; m < ncols; m += nthreads)
+          if (m0 + m < e.M) e.act_xs[int64_t(r) * (e.act_nt * 8) + m0 + m] = scratch[2 * m] + scratch[2 * m + 1];
+      } else if (e.act_xs) {
         // second halves: add the u in [32, 64) sums after the first halves are stored
         asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
         for (int base = (tid & ~31); base < nitems; base += nthreads) {

@@ -68,7 +68,9 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   uint64_t* empty = full + C::kMaxStages;
   int* flag = reinterpret_cast<int*>(empty + C::kMaxStages);
   float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
-  uint8_t* xres = reinterpret_cast<uint8_t*>(scratch) + 512;    // xnorm: [xn_chunks][X chunk]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(flag) + 4;      // x prefetch barrier (in the flag block)
+  float* xpre = scratch + 128;                                  // [kXPreFloats] residual rows
+  uint8_t* xres = reinterpret_cast<uint8_t*>(xpre + C::kXPreFloats);   // xnorm: [xn_chunks][X chunk]
   float* xsres = reinterpret_cast<float*>(xres + size_t(p.xn_chunks) * C::kXBytes);   // [xn_chunks][2][Mpad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGemvConsumerWarps);
     }
+    mbar_init(xbar, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       }
       // L2 prefetch of the next matrix (independent of every activation): this CTA's slice, in
       // 64 KB TMA prefetches, so HBM keeps streaming through the dependent steps that follow
-      if (p.pf && p.pf_bytes > 0) {
+      auto prefetch_next = [&]() {
         const int64_t per = ((p.pf_bytes / gridDim.x) + 15) & ~int64_t(15);
         const int64_t b0 = per * blockIdx.x;
         const int64_t b1 = b0 + per < p.pf_bytes ? b0 + per : p.pf_bytes;
@@ -163,7 +166,8 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
           const int64_t n = b1 - o < 65536 ? b1 - o : 65536;
           prefetch_l2(p.pf + o, uint32_t(n));
         }
-      }
+      };
+      if (p.pf && p.pf_bytes > 0 && !p.pf_late) prefetch_next();
       griddep_wait();
       SS_TRACE_CTA0(1);
       for (int i = 0; i < pre; ++i) {
@@ -171,6 +175,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         issue_x(i, wx, n);
         wx.next(nC, n);
       }
+      if (p.pf && p.pf_bytes > 0 && p.pf_late) prefetch_next();
       int st = pre % kStages;
       uint32_t ph = pre / kStages;   // 0 or 1 (pre <= kStages)
       for (int64_t i = pre; i < n_stage; ++i) {
@@ -281,6 +286,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
 
   auto stash = [&](float* dst) { stash_acc<NT>(acc, dst, warp, lane); };
 
+  uint32_t xph = 0;   // phase of xbar
   auto flush = [&](int r, int c_first, int c_last, bool last) {
     if constexpr (kCluster) {
       if (csize == 1) {
@@ -300,6 +306,16 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       const int S = int(csize);
       const int mlo = int(crank) * Mpad / S, mhi = int(crank + 1) * Mpad / S;
       const int nc = mhi - mlo, ncmax = (Mpad + S - 1) / S;
+      // residual epilogues: TMA-load the owned tokens' residual rows of this tile now, so the
+      // epilogue's read-modify-write does not pay an L2 round trip after the reduction
+      const int nvalid = nc < p.epi.M - mlo ? nc : (p.epi.M - mlo > 0 ? p.epi.M - mlo : 0);
+      const bool xp = nvalid > 0 && nc <= C::kXPreTokens &&
+                      (p.epi.kind == EPI_RESID || p.epi.kind == EPI_RESID_SS || p.epi.kind == EPI_RESID_NORM);
+      if (xp && threadIdx.x == 0) {
+        mbar_arrive_expect_tx(xbar, uint32_t(nvalid) * kTileRows * 4);
+        for (int m = 0; m < nvalid; ++m)
+          bulk_g2s(xpre + m * kTileRows, p.epi.x + int64_t(mlo + m) * p.epi.ldx + int64_t(r) * kTileRows, kTileRows * 4, xbar);
+      }
 #pragma unroll
       for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
         const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
@@ -327,7 +343,12 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       if (!last) cluster_sync_all();              // staging is reused by the next tile's pushes
       named_bar(1, nthr);
       if (threadIdx.x == 0) SS_TRACE_MAX(8);
-      apply_epilogue(p.epi, otile, nc, r, mlo, nc, threadIdx.x, nthr, scratch, p.trace, S, crank == 0, Mpad);
+      if (xp) {
+        mbar_wait(xbar, xph);
+        xph ^= 1;
+      }
+      apply_epilogue(p.epi, otile, nc, r, mlo, nc, threadIdx.x, nthr, scratch, p.trace, S, crank == 0, Mpad, nullptr,
+                     xp ? xpre : nullptr);
       named_bar(1, nthr);
       return;
     } else {

@@ -22,12 +22,15 @@ struct GemvCfg {
   static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
   static constexpr int kMaxStages = 16;
   static constexpr int kTileFloats = kTileRows * NT * 8;
+  // residual rows of a tile's owned tokens (<= 8), TMA-prefetched before the split-K reduction
+  static constexpr int kXPreTokens = 8;
+  static constexpr int kXPreFloats = kXPreTokens * kTileRows;
   // cluster reduction staging: [S][ceil(Mpad/S)][128] fp32 partial columns pushed by the ranks,
   // S <= kGemvMaxCluster -> at most (Mpad + kGemvMaxCluster - 1) x 128 floats
   static constexpr int kStagingFloats = (NT * 8 + kGemvMaxCluster - 1) * kTileRows;
   // runtime stage count S: ring S*stage + out tile + staging + 2*kMaxStages barriers
   static constexpr int smem_for(int S) {
-    return S * kStageBytes + kTileFloats * 4 + kStagingFloats * 4 + 2 * kMaxStages * 8 + 64 + 512;
+    return S * kStageBytes + kTileFloats * 4 + kStagingFloats * 4 + 2 * kMaxStages * 8 + 64 + 512 + kXPreFloats * 4;
   }
 };
 SS_HD int64_t owner_of(int64_t t, int64_t T, int G) { return ((t + 1) * G - 1) / T; }

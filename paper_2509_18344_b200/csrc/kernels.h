@@ -74,6 +74,7 @@ struct GemvParams {
   int stages;                    // ring depth (set by the launcher)
   const uint8_t* pf;             // weights of the NEXT matrix: prefetched into L2 while this one runs
   int64_t pf_bytes;
+  int pf_late;                   // issue the L2 prefetch of pf after the grid-dependency wait
   unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
   int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
