@@ -47,6 +47,8 @@ def args_():
     ap.add_argument("--temp", type=float, default=0.2)
     ap.add_argument("--batch", type=int, default=1,
                     help="request slots per GPU sharing one weight stream (SURVEY 8(f) NEXT-2); 1 = the paper's batch 1")
+    ap.add_argument("--sub-bits", type=int, default=4, choices=[4, 2],
+                    help="substitute code bits (4 = the paper's setting, P:278; 2 = NEXT-3, P:343)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -208,7 +210,7 @@ def run_reference(a):
 def workload_config(a, cfg):
     batch = "" if a.batch == 1 else f", {a.batch} requests per GPU sharing one weight stream (NEXT-2)"
     return {"workload": f"{cfg.name} SubSpec step, {a.cap_gib:g} GiB cap, n_resident={a.n_resident}, "
-                        f"4-bit g64 substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt{batch}",
+                        f"{a.sub_bits}-bit g64 substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt{batch}",
             "model_shape": cfg.name, "vram_cap_gib": a.cap_gib, "n_resident": a.n_resident, "depth": a.depth,
             "top_k": a.topk, "sharpen_t": a.temp, "batch": a.batch, "max_context": cfg.max_context,
             "l2": "inputs larger than L2 (>= 4.76 GB of draft weights per draft pass; 13 GB streamed per verify)",
@@ -232,9 +234,9 @@ def request_for_rank(rank, vocab):
     return mtbench_prompt(SEED, rank, vocab)
 
 
-def k2_bytes(N, K, M):
-    # codes N*K/2 + meta N*K/64*4 + X M*K*2 + Y M*N*2
-    return N * K // 2 + N * K // 64 * 4 + M * K * 2 + M * N * 2
+def k2_bytes(N, K, M, bits=4):
+    # codes N*K*bits/8 + meta N*K/64*4 + X M*K*2 + Y M*N*2
+    return N * K * bits // 8 + N * K // 64 * 4 + M * K * 2 + M * N * 2
 
 
 def load_weights_for_job(ss, dist, local, n_resident):
@@ -307,8 +309,10 @@ def run_ours(a):
     Bq = a.batch
     ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256,
                  max_batch=Bq)
+    if a.sub_bits != 4:
+        ss.set_substitute_bits(a.sub_bits)
     shm = load_weights_for_job(ss, dist, local, a.n_resident)
-    ss.build_substitutes(4, 64)
+    ss.build_substitutes(a.sub_bits, 64)
     if Bq == 1:
         ss.prefill(request_for_rank(rank, cfg.vocab))
         step = lambda: [ss.step(D, k, T)]                     # noqa: E731
@@ -348,9 +352,9 @@ def run_ours(a):
     for g, name in enumerate(("qkv", "o", "gate_up", "down")):
         t = ss.debug_time_matmul(-1, g, M, iters=3)
         per_group[name] = {"N": groups[g][0], "K": groups[g][1], "us": t * 1e3,
-                           "gbs": k2_bytes(*groups[g], M) / (t * 1e-3) / 1e9}
+                           "gbs": k2_bytes(*groups[g], M, a.sub_bits) / (t * 1e-3) / 1e9}
     t_sweep = ss.debug_time_matmul(-1, -2, M, iters=3)       # avg per launch, 4 groups x L layers
-    bytes_layer = sum(k2_bytes(N, K, M) for N, K in groups)
+    bytes_layer = sum(k2_bytes(N, K, M, a.sub_bits) for N, K in groups)
     k2_gbs = bytes_layer / (4 * t_sweep * 1e-3) / 1e9
     t_head = ss.debug_time_matmul(0, -1, M, iters=5)
     head_gbs = (cfg.vocab * cfg.hidden * 2 + M * cfg.hidden * 2 + M * cfg.vocab * 4) / (t_head * 1e-3) / 1e9
@@ -436,7 +440,7 @@ def run_ours(a):
         "requests_per_gpu": Bq,
         "step_breakdown_ms": {"draft": st["draft_ms"] / a.steps, "verify": st["verify_ms"] / a.steps,
                               "accept": st["accept_ms"] / a.steps},
-        "roofline": {"kernel": f"K2 dequant-GEMV (4-bit g64 substitutes, M={M} tokens), all layers x 4 groups",
+        "roofline": {"kernel": f"K2 dequant-GEMV ({a.sub_bits}-bit g64 substitutes, M={M} tokens), all layers x 4 groups",
                      "bound": "hbm", "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      "per_group": per_group, "head_bf16_gemv_gbs": head_gbs},

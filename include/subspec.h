@@ -98,6 +98,14 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
  * (SPEC.md:205-213).  Embedding, final norm and head are always resident. */
 ss_status ss_load_weights(ss_ctx* ctx, uint64_t seed, int32_t n_resident);
 
+/* Code width of the substitutes this context will build: 4 (default; "4 bits with a
+ * group size 64") or 2 (the paper's "more aggressive ... 2-bit" direction,
+ * PAPER.md:343; same min/max RTN rule with 2^bits - 1 levels).  Fixes the substitutes' layout and
+ * footprint (2-bit: 0.3125 B/weight vs 0.5625), so it is only valid before ss_load_weights; the
+ * arena bytes it frees go to the streaming ring.  ss_build_substitutes must then pass the same bits.
+ * Errors: STRUCTURE (after load), INVALID (bits not 2 or 4). */
+ss_status ss_set_substitute_bits(ss_ctx* ctx, int32_t bits);
+
 /* Bytes of the offloaded layers' host store for an explicit n_resident >= 0 (bf16, device layout).
  * Errors: INVALID. */
 ss_status ss_host_store_bytes(ss_ctx* ctx, int32_t n_resident, size_t* out_bytes);
@@ -113,7 +121,7 @@ ss_status ss_host_store_bytes(ss_ctx* ctx, int32_t n_resident, size_t* out_bytes
 ss_status ss_load_weights_shared(ss_ctx* ctx, uint64_t seed, int32_t n_resident, void* host_store,
                                  size_t host_bytes, int32_t fill);
 
-/* Build the 4-bit group-64 substitute of every offloaded layer: stream it host->device through
+/* Build the 4-bit (or, after ss_set_substitute_bits(2), 2-bit) group-64 substitute of every offloaded layer: stream it host->device through
  * the staging ring and quantize on the device (K1).  Norms/biases are shared. */
 ss_status ss_build_substitutes(ss_ctx* ctx, const ss_quant_spec* q);
 

@@ -51,6 +51,7 @@ P = ctypes.POINTER
 _FUNCS = {
     "ss_create": [P(ModelConfigC), P(LimitsC), ctypes.c_int, c_void_p, c_size_t, c_void_p, c_void_p, P(c_void_p)],
     "ss_load_weights": [c_void_p, c_uint64, c_int32],
+    "ss_set_substitute_bits": [c_void_p, c_int32],
     "ss_host_store_bytes": [c_void_p, c_int32, P(c_size_t)],
     "ss_load_weights_shared": [c_void_p, c_uint64, c_int32, c_void_p, c_size_t, c_int32],
     "ss_build_substitutes": [c_void_p, P(QuantSpecC)],
@@ -159,6 +160,10 @@ class SubSpec:
             pass
 
     # ---- the method ---------------------------------------------------------------------
+    def set_substitute_bits(self, bits):
+        """Substitute code width (4 or 2); before load_weights (sizes the substitutes' layout)."""
+        self._check(self.lib.ss_set_substitute_bits(self.ctx, bits))
+
     def load_weights(self, seed, n_resident=0):
         self._check(self.lib.ss_load_weights(self.ctx, c_uint64(seed), n_resident))
 

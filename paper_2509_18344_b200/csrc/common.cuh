@@ -78,6 +78,33 @@ SS_HD uint64_t q4_meta_offset(int64_t n, int64_t k, int64_t K) {     // bytes; 4
   return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((w * 2 + kpos(k).G) * 16 + rr) * 4);
 }
 
+// Q2 (NEXT-3, 2-bit substitutes): per (warp w, group G, lane) 8 bytes = [row g word][row g+8 word];
+// the word holds i16 = 0..15 of the lane's 16 k of group G: code i16 lives in bits
+// (i16 % 2) * 16 + 2 * (i16 / 2), so (word >> 2p) & 0x00030003 yields the bf16x2 pair
+// (c_2p, c_2p+1) — k-step k4 uses pairs 2 k4 (a0/a1) and 2 k4 + 1 (a2/a3).
+// Meta as Q4, at kQ2CodeBytes + ((w*2 + G)*16 + row_in_warp) * 4.
+constexpr int kQ2CodeBytes = 4096;  // 128 x 128 x 2 bit
+constexpr int kQ2TileBytes = kQ2CodeBytes + kQ4MetaBytes;   // 5120
+SS_HD int qtile_bytes(int bits) { return bits == 2 ? kQ2TileBytes : kQ4TileBytes; }
+SS_HD int qcode_bytes(int bits) { return bits == 2 ? kQ2CodeBytes : kQ4CodeBytes; }
+SS_HD void q2_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
+  const int nn = int(n & 127);
+  const int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
+  const KPos p = kpos(k);
+  const int lane = g * 4 + p.t4;
+  const int bit = (p.i16 & 1) * 16 + 2 * (p.i16 >> 1);
+  const uint64_t wordoff = uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes +
+                           uint64_t(((w * 2 + p.G) * 32 + lane) * 8 + h * 4);
+  *byte_off = wordoff + (bit >> 3);
+  *shift = bit & 7;
+}
+SS_HD uint64_t q2_meta_offset(int64_t n, int64_t k, int64_t K) {
+  const int nn = int(n & 127);
+  const int w = nn >> 4, rr = nn & 15;
+  return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes + kQ2CodeBytes +
+         uint64_t(((w * 2 + kpos(k).G) * 16 + rr) * 4);
+}
+
 // ---------------------------------------------------------------------------
 // FragX activation layout: X [Mpad x K] bf16, Mpad % 8 == 0, NT = Mpad/8.
 // Chunk c (128 k) of all NT n-tiles is contiguous (NT * 2 KB); within it
@@ -124,6 +151,11 @@ SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 SS_DEV uint32_t lop3_and_or(uint32_t x, uint32_t magic) {
   uint32_t d;
   asm("lop3.b32 %0, %1, 0x000F000F, %2, 0xEA;" : "=r"(d) : "r"(x), "r"(magic));
+  return d;
+}
+SS_DEV uint32_t lop3_and_or2(uint32_t x, uint32_t magic) {   // 2-bit codes: (x & 0x00030003) | magic
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 0x00030003, %2, 0xEA;" : "=r"(d) : "r"(x), "r"(magic));
   return d;
 }
 // 1-D bulk async copy global -> shared, completion counted on an mbarrier (TMA engine; SASS UBLKCP)

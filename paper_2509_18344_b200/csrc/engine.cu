@@ -140,6 +140,7 @@ struct ss_ctx {
   int ev_pool = 0;
   // fused persistent draft pass (pass.cu)
   bool use_fused = false;
+  int sub_bits = 4;           // substitute code bits (ss_set_substitute_bits; 2 = NEXT-3)
   bool l2_prefetch = true;
   bool attn_v2 = true;
   std::vector<PhaseDesc> phases;
@@ -193,6 +194,7 @@ ss_status check_launch(ss_ctx* c, const char* what) {
 }
 
 size_t q4_bytes(int N, int K) { return size_t(N / 128) * (K / 128) * kQ4TileBytes; }
+size_t sub_bytes(int N, int K, int bits) { return size_t(N / 128) * (K / 128) * size_t(qtile_bytes(bits)); }
 size_t bf16_bytes(int N, int K) { return size_t(N) * K * 2; }
 
 // token tiles of 8 for a draft GEMV over M <= 32 rows: M = 17..24 (e.g. 4 batched requests x k = 6)
@@ -326,10 +328,10 @@ static void next_weights(ss_ctx* c, int l, int g, const uint8_t** ptr, int64_t* 
   }
   const LayerW& w = c->lw[nl];
   *ptr = w.resident ? w.bf16[ng] : w.q4[ng];
-  *bytes = int64_t(w.resident ? bf16_bytes(c->gN[ng], c->gK[ng]) : q4_bytes(c->gN[ng], c->gK[ng]));
+  *bytes = int64_t(w.resident ? bf16_bytes(c->gN[ng], c->gK[ng]) : sub_bytes(c->gN[ng], c->gK[ng], c->sub_bits));
   if (ng == 0) {   // qkv is small: let it cover o as well (two kernels ahead)
     const uint8_t* p2 = w.resident ? w.bf16[1] : w.q4[1];
-    if (p2 == *ptr + *bytes) *bytes += int64_t(w.resident ? bf16_bytes(c->gN[1], c->gK[1]) : q4_bytes(c->gN[1], c->gK[1]));
+    if (p2 == *ptr + *bytes) *bytes += int64_t(w.resident ? bf16_bytes(c->gN[1], c->gK[1]) : sub_bytes(c->gN[1], c->gK[1], c->sub_bits));
   }
 }
 
@@ -371,13 +373,14 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     // free slots next to the previous layer's down GEMV (2 CTAs on ~84 SMs), so they are resident
     // and prefetched early (measured: pass 2082 -> 2013 us; o and down are slower at 1 CTA/SM).
     p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
+    p.qbits = c->sub_bits;
     static const int pf_down = getenv("SS_PF_DOWN") ? atoi(getenv("SS_PF_DOWN")) : 0;
     if (pf_down && g == 0 && !w.resident && !c->lw[l].resident) {
       // L2 prefetch of this layer's down substitute while qkv, attention and o (latency-bound, HBM
       // mostly idle) run, issued after the dependency wait so it does not compete with the previous
       // down's stream (SS_PF_DOWN=2: only the first half of the matrix, tiles 0..13)
       p.pf = w.q4[3];
-      p.pf_bytes = int64_t(q4_bytes(c->gN[3], c->gK[3]));
+      p.pf_bytes = int64_t(sub_bytes(c->gN[3], c->gK[3], c->sub_bits));
       if (pf_down == 2) p.pf_bytes /= 2;
       p.pf_late = 1;
     }
@@ -481,8 +484,8 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     c->launches += c->attn_v2 ? 1 : 2;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
     const bool fnorm = !target && c->fuse_norm && !(g_skip & SKIP_NORM) &&
-                       gemv_tiles_all_resident(true, NT, c->gN[1], c->gK[1], c->gv_grid) &&
-                       gemv_tiles_all_resident(true, NT, c->gN[3], c->gK[3], c->gv_grid) &&
+                       gemv_tiles_all_resident(true, NT, c->gN[1], c->gK[1], c->gv_grid, c->sub_bits) &&
+                       gemv_tiles_all_resident(true, NT, c->gN[3], c->gK[3], c->gv_grid, c->sub_bits) &&
                        (c->n_resident == 0 || (gemv_tiles_all_resident(false, NT, c->gN[1], c->gK[1], c->gv_grid) &&
                                                gemv_tiles_all_resident(false, NT, c->gN[3], c->gK[3], c->gv_grid)));
     // one monotonic barrier counter per (matrix, weight format, NT): every launch on a counter has
@@ -1125,6 +1128,14 @@ ss_status ss_host_store_bytes(ss_ctx* c, int32_t n_resident, size_t* out) {
 
 static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* ext_host, size_t ext_bytes, bool fill);
 
+ss_status ss_set_substitute_bits(ss_ctx* c, int32_t bits) {
+  GUARD(c);
+  if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "set_substitute_bits: only before load_weights");
+  if (bits != 4 && bits != 2) return fail(c, SS_ERR_INVALID, "set_substitute_bits: 4 or 2");
+  c->sub_bits = bits;
+  return SS_OK;
+}
+
 ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
   GUARD(c);
   return load_impl(c, seed, n_resident, nullptr, 0, true);
@@ -1141,7 +1152,7 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
   if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "load_weights: already loaded");
   c->seed = seed;
   const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
-  const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += q4_bytes(c->gN[g], c->gK[g]); return s; }();
+  const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += sub_bytes(c->gN[g], c->gK[g], c->sub_bits); return s; }();
   size_t max_group = 0;
   for (int g = 0; g < 4; ++g) max_group = std::max(max_group, bf16_bytes(c->gN[g], c->gK[g]));
   const size_t avail = c->ar.cap - c->ar.used - 4096 * 8;
@@ -1164,7 +1175,7 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
       if (w.resident)
         w.bf16[g] = (uint8_t*)c->ar.alloc(bf16_bytes(c->gN[g], c->gK[g]), 1024);
       else
-        w.q4[g] = (uint8_t*)c->ar.alloc(q4_bytes(c->gN[g], c->gK[g]), 1024);
+        w.q4[g] = (uint8_t*)c->ar.alloc(sub_bytes(c->gN[g], c->gK[g], c->sub_bits), 1024);
     }
   }
   // the staging ring takes what is left after the fused-pass tables (reserved here, see below)
@@ -1276,6 +1287,7 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
     if (gv && gv[0] == '0') c->use_graphs = false;
     const char* av = getenv("SS_ATTN_V2");
     c->attn_v2 = !(av && av[0] == '0');
+    if (c->sub_bits != 4) c->use_fused = c->fuse_mlp = c->xnorm = false;   // Q4-only opt-in variants
     c->pass_stages = 5;
     while (c->pass_stages > 2 && pass_smem_bytes(c->d, c->pass_stages) > 227 * 1024) --c->pass_stages;
     int sms = 148;
@@ -1382,13 +1394,16 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
 
 ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
   GUARD(c);
-  if (!q || q->bits != 4 || q->group_size != 64) return fail(c, SS_ERR_INVALID, "only 4-bit group-64 substitutes");
+  if (!q || (q->bits != 4 && q->bits != 2) || q->group_size != 64)
+    return fail(c, SS_ERR_INVALID, "substitutes are 4- or 2-bit with group 64");
+  if (q->bits != c->sub_bits)
+    return fail(c, SS_ERR_INVALID, "quant bits differ from the layout sized at load (ss_set_substitute_bits)");
   if (c->state != ST_LOADED) return fail(c, SS_ERR_STRUCTURE, "build_substitutes before load_weights");
   for (int l = c->n_resident; l < c->L; ++l)
     for (int g = 0; g < 4; ++g) {
       const LayerW& w = c->lw[l];
       CK(cudaMemcpyAsync(c->ring, c->host + w.host_off[g], bf16_bytes(c->gN[g], c->gK[g]), cudaMemcpyHostToDevice, c->cs));
-      launch_quantize_q4(c->ring, w.q4[g], c->gN[g], c->gK[g], c->cs);
+      launch_quantize(c->ring, w.q4[g], c->gN[g], c->gK[g], c->sub_bits, c->cs);
       CK(cudaStreamSynchronize(c->cs));
     }
   ss_status s = check_launch(c, "quantize");
@@ -1783,18 +1798,20 @@ ss_status ss_debug_get_substitute(ss_ctx* c, int32_t layer, int32_t group, uint8
   if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || c->lw[layer].resident)
     return fail(c, SS_ERR_INVALID, "get_substitute: not an offloaded layer (or substitutes not built)");
   const int N = c->gN[group], K = c->gK[group];
-  std::vector<uint8_t> q(q4_bytes(N, K));
+  const bool q2 = c->sub_bits == 2;
+  std::vector<uint8_t> q(sub_bytes(N, K, c->sub_bits));
   CK(cudaMemcpyAsync(q.data(), c->lw[layer].q4[group], q.size(), cudaMemcpyDeviceToHost, c->cs));
   CK(cudaStreamSynchronize(c->cs));
   for (int64_t n = 0; n < N; ++n)
     for (int64_t k = 0; k < K; ++k) {
       uint64_t off;
       int sh;
-      q4_code_pos(n, k, K, &off, &sh);
-      if (codes) codes[n * K + k] = (q[off] >> sh) & 15;
+      if (q2) q2_code_pos(n, k, K, &off, &sh);
+      else q4_code_pos(n, k, K, &off, &sh);
+      if (codes) codes[n * K + k] = (q[off] >> sh) & (q2 ? 3 : 15);
       if ((k & 63) == 0) {
         uint32_t m;
-        std::memcpy(&m, q.data() + q4_meta_offset(n, k, K), 4);
+        std::memcpy(&m, q.data() + (q2 ? q2_meta_offset(n, k, K) : q4_meta_offset(n, k, K)), 4);
         if (s) s[n * (K / 64) + k / 64] = uint16_t(m & 0xFFFF);
         if (z) z[n * (K / 64) + k / 64] = uint16_t(m >> 16);
       }
@@ -1847,6 +1864,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
     p.counters = c->gv_cnt;
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = e;
+    p.qbits = c->sub_bits;
     launch_gemv(!w.resident, p, c->gv_grid, false, c->cs);
   } else {
     GemmParams p{};
@@ -1902,6 +1920,7 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
     p.self_pf = head ? 0 : (self_pf >> g) & 1;
     p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
+    p.qbits = c->sub_bits;
     p.epi.out = c->at_o;
     p.epi.ldo = N;
     launch_gemv(!head && !w.resident, p, c->gv_grid, c->use_pdl, c->cs);

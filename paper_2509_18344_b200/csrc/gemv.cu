@@ -56,9 +56,9 @@ int gemv_max_segments(int N, int K, int grid) {
   return mx;
 }
 
-template <bool Q4, int NT, bool kCluster>
+template <bool Q4, int NT, bool kCluster, int QB = 4>
 __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(const GemvParams p) {
-  using C = GemvCfg<Q4, NT>;
+  using C = GemvCfg<Q4, NT, QB>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int kStages = p.stages;
   uint8_t* ring = smem;
@@ -404,10 +404,10 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         if (ct) ct[2] = gtime();
       }
       if (p.xnorm)
-        consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
+        consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
                               xsres + (w.c - xc0) * 2 * Mpad);
       else
-        consume_stage<Q4, NT>(ring + s * C::kStageBytes, nch, acc, warp, lane);
+        consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) {
@@ -466,18 +466,20 @@ int gemv_cluster_split(int N, int K, int sms, int hint) {
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
 
-template <bool Q4, int NT, bool kCluster>
+template <bool Q4, int NT, bool kCluster, int QB = 4>
 static int ensure_attrs() {   // ring stages for this instantiation; sets the smem/cluster attributes once
-  using C = GemvCfg<Q4, NT>;
+  using C = GemvCfg<Q4, NT, QB>;
   static int stages = 0;
   if (!stages) {
-    const int budget = env_int("SS_GEMV_RING_KB", 88) * 1024;
+    // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
+    // down to ~68 KB of whole stages)
+    const int budget = (QB == 2 ? env_int("SS_GEMV_RING_KB_Q2", 72) : env_int("SS_GEMV_RING_KB", 88)) * 1024;
     int st = budget / C::kStageBytes;
     if (st < 2) st = 2;
     if (st > C::kMaxStages) st = C::kMaxStages;
-    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::smem_for(st) + (kCluster ? 8 * (C::kXBytes + C::kSBytes) : 0));
-    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     stages = st;
   }
   return stages;
@@ -491,7 +493,7 @@ struct ClusterPlan {
   int S, ncl;
   bool all_resident;
 };
-template <bool Q4, int NT>
+template <bool Q4, int NT, int QB = 4>
 static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   static std::mutex mu;
   static std::map<std::tuple<int, int, int>, ClusterPlan> cache;
@@ -499,8 +501,8 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   const auto key = std::make_tuple(N, K, hint);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  using C = GemvCfg<Q4, NT>;
-  const int stages = ensure_attrs<Q4, NT, true>();
+  using C = GemvCfg<Q4, NT, QB>;
+  const int stages = ensure_attrs<Q4, NT, true, QB>();
   const int tiles = N / 128;
   const int per_sm = per_sm_for(N, K, hint);
   const int S0 = gemv_cluster_split(N, K, sms, hint);
@@ -521,7 +523,7 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true, QB>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       active = ncl;   // cannot query: keep the arithmetic plan
     }
@@ -540,8 +542,17 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
 }
 
 // every row tile has its own resident cluster (required by EPI_RESID_NORM's in-kernel barrier)
-bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms) {
+bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits) {
   if (!gemv_use_cluster(N, K, sms)) return false;
+  if (q4 && bits == 2) {
+    switch (NT) {
+      case 1: return cluster_plan<true, 1, 2>(N, K, sms).all_resident;
+      case 2: return cluster_plan<true, 2, 2>(N, K, sms).all_resident;
+      case 3: return cluster_plan<true, 3, 2>(N, K, sms).all_resident;
+      case 4: return cluster_plan<true, 4, 2>(N, K, sms).all_resident;
+      default: return false;
+    }
+  }
   switch (NT) {
     case 1: return q4 ? cluster_plan<true, 1>(N, K, sms).all_resident : cluster_plan<false, 1>(N, K, sms).all_resident;
     case 2: return q4 ? cluster_plan<true, 2>(N, K, sms).all_resident : cluster_plan<false, 2>(N, K, sms).all_resident;
@@ -551,10 +562,10 @@ bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms) {
   }
 }
 
-template <bool Q4, int NT, bool kCluster>
+template <bool Q4, int NT, bool kCluster, int QB = 4>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
-  using C = GemvCfg<Q4, NT>;
-  const int stages = ensure_attrs<Q4, NT, kCluster>();
+  using C = GemvCfg<Q4, NT, QB>;
+  const int stages = ensure_attrs<Q4, NT, kCluster, QB>();
   GemvParams p = p0;
   p.stages = stages;
   p.xn_chunks = 0;
@@ -585,20 +596,30 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster>, p);
+  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster, QB>, p);
 }
 
-template <bool Q4, int NT>
+template <bool Q4, int NT, int QB = 4>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
   if (gemv_use_cluster(p.N, p.K, sms)) {
-    const ClusterPlan pl = cluster_plan<Q4, NT>(p.N, p.K, sms, p.ctas_per_sm);
-    launch_t<Q4, NT, true>(p, pl.ncl * pl.S, pl.S, pdl, st);
+    const ClusterPlan pl = cluster_plan<Q4, NT, QB>(p.N, p.K, sms, p.ctas_per_sm);
+    launch_t<Q4, NT, true, QB>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {
-    launch_t<Q4, NT, false>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);
+    launch_t<Q4, NT, false, QB>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);
   }
 }
 
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st) {
+  if (q4 && p.qbits == 2) {   // 2-bit substitutes (NEXT-3)
+    switch (p.NT) {
+      case 1: launch_mode<true, 1, 2>(p, grid, pdl, st); break;
+      case 2: launch_mode<true, 2, 2>(p, grid, pdl, st); break;
+      case 3: launch_mode<true, 3, 2>(p, grid, pdl, st); break;
+      case 4: launch_mode<true, 4, 2>(p, grid, pdl, st); break;
+      default: break;
+    }
+    return;
+  }
   switch (p.NT) {
     case 1: q4 ? launch_mode<true, 1>(p, grid, pdl, st) : launch_mode<false, 1>(p, grid, pdl, st); break;
     case 2: q4 ? launch_mode<true, 2>(p, grid, pdl, st) : launch_mode<false, 2>(p, grid, pdl, st); break;

@@ -13,10 +13,11 @@ constexpr int kGemvMaxCluster = 16;  // largest (non-portable) cluster the split
 #define SS_GEMV_MIN_BLOCKS 2
 #endif
 
-template <bool Q4, int NT>
+template <bool Q4, int NT, int QB = 4>   // QB: code bits of a quantised (Q4 = true) matrix, 4 or 2
 struct GemvCfg {
   static constexpr int kCPS = Q4 ? 2 : 1;                       // tile-chunks per pipeline stage
-  static constexpr int kWBytes = Q4 ? kQ4TileBytes : kBF16TileBytes;
+  static constexpr int kWBytes = Q4 ? (QB == 2 ? kQ2TileBytes : kQ4TileBytes) : kBF16TileBytes;
+  static constexpr int kCodeBytes = QB == 2 ? kQ2CodeBytes : kQ4CodeBytes;
   static constexpr int kXBytes = NT * kXChunkBytesPerNT;
   static constexpr int kSBytes = Q4 ? 2 * NT * 8 * 4 : 0;       // group sums of x: [2 groups][Mpad] fp32
   static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
@@ -161,10 +162,10 @@ SS_DEV Work make_work(int N, int K, uint32_t crank, uint32_t csize) {
 
 // One pipeline stage (nch tile-chunks of weights + the matching activation chunks + group sums)
 // accumulated into this warp's 16 rows x Mpad tokens.
-template <bool Q4, int NT>
+template <bool Q4, int NT, int QB = 4>
 SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], int warp, int lane,
                           const uint8_t* xres = nullptr, const float* xsres = nullptr) {
-  using C = GemvCfg<Q4, NT>;
+  using C = GemvCfg<Q4, NT, QB>;
   const int g = lane >> 2, t4 = lane & 3;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
 #pragma unroll
@@ -178,9 +179,15 @@ SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], in
                                 : reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
 #pragma unroll
       for (int G = 0; G < 2; ++G) {
-        const uint4 cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);
-        const uint32_t m0 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g) * 4);
-        const uint32_t m1 = *reinterpret_cast<const uint32_t*>(wst + kQ4CodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4);
+        uint4 cw;
+        if constexpr (QB == 2) {   // [row g word][row g+8 word], 16 codes each
+          const uint2 c2 = *reinterpret_cast<const uint2*>(wst + ((warp * 2 + G) * 32 + lane) * 8);
+          cw = make_uint4(c2.x, 0u, c2.y, 0u);
+        } else {
+          cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);
+        }
+        const uint32_t m0 = *reinterpret_cast<const uint32_t*>(wst + C::kCodeBytes + ((warp * 2 + G) * 16 + g) * 4);
+        const uint32_t m1 = *reinterpret_cast<const uint32_t*>(wst + C::kCodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4);
         // one accumulator chain per token tile (the 8 consumer warps x 2 CTAs hide the MMA latency;
         // a second chain would cost 4 FADDs per group in an issue-bound loop)
         float cg[NT][4];
@@ -189,12 +196,20 @@ SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], in
 #pragma unroll
         for (int k4 = 0; k4 < 4; ++k4) {
           const int st = 4 * G + k4;
-          const uint32_t wg = (k4 < 2) ? cw.x : cw.y, wg8 = (k4 < 2) ? cw.z : cw.w;
-          const int pp = 2 * (k4 & 1);
-          const uint32_t a0 = lop3_and_or(wg >> (4 * pp), kMagic);
-          const uint32_t a1 = lop3_and_or(wg8 >> (4 * pp), kMagic);
-          const uint32_t a2 = lop3_and_or(wg >> (4 * pp + 4), kMagic);
-          const uint32_t a3 = lop3_and_or(wg8 >> (4 * pp + 4), kMagic);
+          uint32_t a0, a1, a2, a3;
+          if constexpr (QB == 2) {   // pairs 2 k4 (a0/a1) and 2 k4 + 1 (a2/a3) at bit 2p
+            a0 = lop3_and_or2(cw.x >> (4 * k4), kMagic);
+            a1 = lop3_and_or2(cw.z >> (4 * k4), kMagic);
+            a2 = lop3_and_or2(cw.x >> (4 * k4 + 2), kMagic);
+            a3 = lop3_and_or2(cw.z >> (4 * k4 + 2), kMagic);
+          } else {
+            const uint32_t wg = (k4 < 2) ? cw.x : cw.y, wg8 = (k4 < 2) ? cw.z : cw.w;
+            const int pp = 2 * (k4 & 1);
+            a0 = lop3_and_or(wg >> (4 * pp), kMagic);
+            a1 = lop3_and_or(wg8 >> (4 * pp), kMagic);
+            a2 = lop3_and_or(wg >> (4 * pp + 4), kMagic);
+            a3 = lop3_and_or(wg8 >> (4 * pp + 4), kMagic);
+          }
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint2 b = *reinterpret_cast<const uint2*>(xst + (j * 8 + st) * 256);

@@ -69,13 +69,17 @@ void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float
 //   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / 15) ; z = m
 //   code = clamp(rint_even(fp32(x - z) / s), 0, 15)       (IEEE div.rn; built without fast-math)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) quantize_q4_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                                                          int64_t n_tc) {
+// BITS = 2 (NEXT-3): the same rule with 2^BITS - 1 = 3 levels, packed in the Q2 layout (common.cuh).
+template <int BITS>
+__global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                         int64_t n_tc) {
+  constexpr float kLevels = float((1 << BITS) - 1);
+  constexpr int kTile = BITS == 2 ? kQ2TileBytes : kQ4TileBytes, kCode = BITS == 2 ? kQ2CodeBytes : kQ4CodeBytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t4 = lane & 3, g = lane >> 2;
   for (int64_t tc = blockIdx.x; tc < n_tc; tc += gridDim.x) {
     const uint8_t* s_tile = src + tc * kBF16TileBytes;
-    uint8_t* d_tile = dst + tc * kQ4TileBytes;
+    uint8_t* d_tile = dst + tc * kTile;
     float x[2][32];   // [h][q*8 + e] with q = 2G + i16/8, e = i16 % 8
 #pragma unroll
     for (int h = 0; h < 2; ++h)
@@ -106,31 +110,41 @@ __global__ void __launch_bounds__(256) quantize_q4_kernel(const uint8_t* __restr
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), 15.0f))) << 16);
+        const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), kLevels))) << 16);
         const float z = mn;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float t = __fdiv_rn(__fsub_rn(xv[i], z), sc);
-          const float r = fminf(fmaxf(rintf(t), 0.0f), 15.0f);
-          const int c8 = i & 7, slot = (c8 & 1) * 4 + (c8 >> 1);
-          words[h][i >> 3] |= uint32_t(r) << (4 * slot);
+          const float r = fminf(fmaxf(rintf(t), 0.0f), kLevels);
+          if constexpr (BITS == 2) {
+            words[h][0] |= uint32_t(r) << ((i & 1) * 16 + 2 * (i >> 1));
+          } else {
+            const int c8 = i & 7, slot = (c8 & 1) * 4 + (c8 >> 1);
+            words[h][i >> 3] |= uint32_t(r) << (4 * slot);
+          }
         }
         meta[h] = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
       }
-      *reinterpret_cast<uint4*>(d_tile + ((warp * 2 + G) * 32 + lane) * 16) =
-          make_uint4(words[0][0], words[0][1], words[1][0], words[1][1]);
+      if constexpr (BITS == 2)
+        *reinterpret_cast<uint2*>(d_tile + ((warp * 2 + G) * 32 + lane) * 8) = make_uint2(words[0][0], words[1][0]);
+      else
+        *reinterpret_cast<uint4*>(d_tile + ((warp * 2 + G) * 32 + lane) * 16) =
+            make_uint4(words[0][0], words[0][1], words[1][0], words[1][1]);
       if (t4 == 0) {
-        *reinterpret_cast<uint32_t*>(d_tile + kQ4CodeBytes + ((warp * 2 + G) * 16 + g) * 4) = meta[0];
-        *reinterpret_cast<uint32_t*>(d_tile + kQ4CodeBytes + ((warp * 2 + G) * 16 + g + 8) * 4) = meta[1];
+        *reinterpret_cast<uint32_t*>(d_tile + kCode + ((warp * 2 + G) * 16 + g) * 4) = meta[0];
+        *reinterpret_cast<uint32_t*>(d_tile + kCode + ((warp * 2 + G) * 16 + g + 8) * 4) = meta[1];
       }
     }
   }
 }
 
-void launch_quantize_q4(const uint8_t* src_bf16_tiled, uint8_t* dst_q4, int64_t N, int64_t K, cudaStream_t st) {
+void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, cudaStream_t st) {
   int64_t n_tc = (N / 128) * (K / 128);
   int blocks = int(n_tc < 148 * 8 ? n_tc : 148 * 8);
-  quantize_q4_kernel<<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q4, n_tc);
+  if (bits == 2)
+    quantize_q_kernel<2><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc);
+  else
+    quantize_q_kernel<4><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc);
 }
 
 // ---- debug readbacks --------------------------------------------------------

@@ -80,6 +80,7 @@ struct GemvParams {
   int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
   int self_pf;                   // prefetch this CTA's own remaining weight range into L2 at entry
   int ctas_per_sm;               // cluster plan: resident CTAs per SM to plan for (0 = default 2)
+  int qbits;                     // code bits of a quantised matrix: 4 (0 = 4) or 2 (NEXT-3)
   // xnorm (cluster mode): instead of TMA-ing X/XS, the consumers build this CTA's K range of
   // X = bf16(x * r_m * gain) (RMSNorm of the residual stream, r_m from per-tile sums of squares)
   // and its group sums in shared memory once, before the main loop
@@ -96,7 +97,7 @@ struct GemvParams {
 };
 
 int gemv_max_segments(int N, int K, int grid);
-bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms);
+bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits = 4);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
 
 // Fused draft MLP of one layer (mlp.cu): gate_up (EPI_SILU) then down (epi_d) in one persistent
@@ -135,7 +136,7 @@ void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st);
 void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st);
 void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float c32, int map, int64_t row_off,
                       cudaStream_t st);
-void launch_quantize_q4(const uint8_t* src_bf16_tiled, uint8_t* dst_q4, int64_t N, int64_t K, cudaStream_t st);
+void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, cudaStream_t st);
 void launch_q4_to_canonical(const uint8_t* q4, uint8_t* codes, uint16_t* s, uint16_t* z, int64_t N, int64_t K,
                             cudaStream_t st);
 void launch_tiled_to_natural(const uint8_t* t, uint16_t* out, int64_t N, int64_t K, cudaStream_t st);

@@ -87,3 +87,37 @@ def test_nonfinite_rejected():
     x = np.zeros((1, 64)); x[0, 3] = np.nan
     with pytest.raises(ValueError):
         quantize(x)
+
+
+# ---- 2-bit substitutes: the same rule with 3 levels ----------
+def test_ramp_2bit_closed_form():
+    # ramp 0..63: s = (63 - 0)/3 = 21 (exact in bf16), z = 0; no x/21 lands on a .5 tie, so the code
+    # is plain integer rounding (2x + 21) // 42, and every error is |21 c - x| <= 10 < s/2
+    x = np.arange(64, dtype=np.float64)[None, :]
+    codes, s, z = quantize(x, 2, 64)
+    assert s[0, 0] == 21.0 and z[0, 0] == 0.0
+    want = (2 * np.arange(64) + 21) // 42
+    assert codes[0].tolist() == want.tolist()
+    assert codes[0, 10] == 0 and codes[0, 11] == 1 and codes[0, 31] == 1 and codes[0, 32] == 2 and codes[0, 63] == 3
+    xh = dequantize(codes, s, z)
+    assert np.array_equal(xh[0], 21.0 * want)
+    assert np.abs(xh - x).max() == 10.0
+
+
+def test_error_bound_2bit():
+    x = _bf16_random((64, 512), 0.05, 13)
+    codes, s, z = quantize(x, 2)
+    xh = dequantize(codes, s, z)
+    S = np.repeat(s, 64, axis=1)
+    top = np.repeat(z + 3 * s, 64, axis=1)
+    assert np.all((np.abs(xh - x) <= S / 2 * (1 + 2**-20)) | ((codes == 3) & (x >= top)))
+    assert codes.max() == 3 and codes.min() == 0
+
+
+def test_fewer_bits_more_error():
+    # SPEC.md "monotone fidelity": mean abs error non-increasing in bits (2 -> 4 roughly / 5 here:
+    # the step shrinks from range/3 to range/15)
+    x = _bf16_random((32, 256), 0.05, 15)
+    e2 = np.abs(substitute_matrix(x, 2) - x).mean()
+    e4 = np.abs(substitute_matrix(x, 4) - x).mean()
+    assert e2 > 3 * e4
