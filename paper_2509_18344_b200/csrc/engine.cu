@@ -1205,12 +1205,14 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
   // generation (tensor ids: SURVEY O.1 / synth/weights.py)
   const double H = c->H;
   if (c->h_embed) {   // generate on the device (ring scratch), then place in the host copy
-    const size_t eb = size_t(c->V) * c->H * 2;
-    if (eb > c->ring_bytes) return fail(c, SS_ERR_BUDGET, "staging ring smaller than the embedding");
-    launch_gen_natural(reinterpret_cast<uint16_t*>(c->ring), tensor_key(seed, 0), uint64_t(c->V) * c->H, scale_c32(1.0),
-                       0, c->cs);
-    CK(cudaMemcpyAsync(c->h_embed, c->ring, eb, cudaMemcpyDeviceToHost, c->cs));
-    CK(cudaStreamSynchronize(c->cs));
+    // in ring-sized pieces (a planner-max placement leaves a ring of only two matrix groups)
+    const uint64_t total = uint64_t(c->V) * c->H, piece = uint64_t(c->ring_bytes / 2);
+    for (uint64_t first = 0; first < total; first += piece) {
+      const uint64_t n = std::min(piece, total - first);
+      launch_gen_natural(reinterpret_cast<uint16_t*>(c->ring), tensor_key(seed, 0), n, scale_c32(1.0), 0, c->cs, first);
+      CK(cudaMemcpyAsync(reinterpret_cast<uint16_t*>(c->h_embed) + first, c->ring, n * 2, cudaMemcpyDeviceToHost, c->cs));
+      CK(cudaStreamSynchronize(c->cs));
+    }
   } else {
     launch_gen_natural(c->embed, tensor_key(seed, 0), uint64_t(c->V) * c->H, scale_c32(1.0), 0, c->cs);
   }

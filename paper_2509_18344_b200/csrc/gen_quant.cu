@@ -25,9 +25,10 @@ SS_DEV uint16_t gen_value(uint64_t key, uint64_t idx, float c32, int gain) {
 }
 
 // natural row-major destination (embedding, norm gains, biases)
-__global__ void gen_natural_kernel(uint16_t* __restrict__ dst, uint64_t key, uint64_t count, float c32, int gain) {
+__global__ void gen_natural_kernel(uint16_t* __restrict__ dst, uint64_t key, uint64_t first, uint64_t count, float c32,
+                                   int gain) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count; i += uint64_t(gridDim.x) * blockDim.x)
-    dst[i] = gen_value(key, i, c32, gain);
+    dst[i] = gen_value(key, first + i, c32, gain);
 }
 
 // tiled destination: src [rows x K] row-major index space, dst row = map(src row)
@@ -49,10 +50,11 @@ __global__ void gen_tiled_kernel(uint8_t* __restrict__ dst, uint64_t key, int64_
   }
 }
 
-void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st) {
+void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st,
+                        uint64_t first) {
   int blocks = int((count + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  gen_natural_kernel<<<blocks, 256, 0, st>>>(dst, key, count, c32, gain);
+  gen_natural_kernel<<<blocks, 256, 0, st>>>(dst, key, first, count, c32, gain);
 }
 void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float c32, int map, int64_t row_off,
                       cudaStream_t st) {

@@ -133,7 +133,8 @@ struct GemmParams {
 void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st);
 
 // generator / quantizer / readback
-void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st);
+void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st,
+                        uint64_t first = 0);   // elements [first, first + count) of the tensor
 void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float c32, int map, int64_t row_off,
                       cudaStream_t st);
 void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, cudaStream_t st);
