@@ -134,3 +134,18 @@ def test_q2_qwen7b_footprint_and_lossless(cuda_required):
     ar, _ = ss.generate(prompt, 12, 0, 1, 0.2)
     assert sd == ar
     ss.close()
+
+
+def test_q2_abi_errors(cuda_required):
+    from paper_2509_18344_b200.binding import SubSpec, SubSpecError
+    ss = SubSpec(TINY, 256 << 20, max_depth=4, max_top_k=6)
+    with pytest.raises(SubSpecError, match="INVALID"):
+        ss.set_substitute_bits(3)                     # 4 or 2 only
+    ss.set_substitute_bits(2)
+    ss.load_weights(SEED, n_resident=1)
+    with pytest.raises(SubSpecError, match="STRUCTURE"):
+        ss.set_substitute_bits(4)                     # the layout is fixed at placement
+    with pytest.raises(SubSpecError, match="INVALID"):
+        ss.build_substitutes(4, 64)                   # must match the placed layout
+    ss.build_substitutes(2, 64)
+    ss.close()
