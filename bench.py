@@ -404,6 +404,16 @@ def run_ours(a):
                "d2h_bytes_per_step": int(4 * (e2e_tok / max(1, n_e2e)) + 4),
                "h2d_breakdown": {"root_token": 4, "streamed_layer_weights": int(streamed)}, "steps": n_e2e,
                "ms_per_step": wall / n_e2e * 1e3}
+    # context: one whole draft pass (all layers + head + attention/norm/top-k kernels), bytes of the
+    # weights it must read (substitutes of offloaded layers, bf16 of resident ones, the bf16 head)
+    draft_pass = None
+    if Bq == 1:
+        n_off = st["n_offloaded"]
+        n_res = cfg.n_layers - n_off
+        pass_bytes = n_off * sum(k2_bytes(N, K, M, a.sub_bits) for N, K in groups) + \
+            n_res * sum(2 * N * K for N, K in groups) + cfg.vocab * cfg.hidden * 2
+        t_pass = ss.debug_time_pass(M, 5, 0)
+        draft_pass = {"us": t_pass * 1e3, "weight_bytes": pass_bytes, "gbs": pass_bytes / (t_pass * 1e-3) / 1e9}
     # host link measured in the same run: pinned H2D 1 GiB on the copy stream, best of 5
     hbuf = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
     dbuf = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -445,7 +455,7 @@ def run_ours(a):
         "roofline": {"kernel": f"K2 dequant-GEMV ({a.sub_bits}-bit g64 substitutes, M={M} tokens), all layers x 4 groups",
                      "bound": "hbm", "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                     "per_group": per_group, "head_bf16_gemv_gbs": head_gbs},
+                     "per_group": per_group, "head_bf16_gemv_gbs": head_gbs, "draft_pass": draft_pass},
         "streaming": {"bytes_per_step": st["stream_bytes"] / a.steps, "busy_gbs": stream_gbs,
                       "host_link_gbs_measured": link_gbs, "frac": (stream_gbs / link_gbs) if stream_gbs else None,
                       "duty_cycle": (st["stream_busy_ms"] / ms) if ms else None},

@@ -40,7 +40,8 @@ want = ["Kernel Name", "Grid Size", "Block Size", "launch__cluster_dim_x", "gpu_
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second"]
 traffic = {}
-for name, rep in (("gate_up (N=37888, K=3584, M=6)", f"k2_gate_up_{tag}.ncu-rep"), ("qkv (N=4608, K=3584, M=6)", f"k2_qkv_{tag}.ncu-rep")):
+for name, rep in (("gate_up (N=37888, K=3584, M=6)", f"k2_gate_up_{tag}.ncu-rep"), ("qkv (N=4608, K=3584, M=6)", f"k2_qkv_{tag}.ncu-rep"),
+                  ("2-bit gate_up (N=37888, K=3584, M=6; NEXT-3)", f"k2q2_gate_up_{tag}.ncu-rep")):
     path = os.path.join(src, rep)
     if not os.path.exists(path):
         continue
@@ -68,7 +69,8 @@ if traffic:
     json.dump({"traffic_bytes_per_launch": traffic.get("gate_up (N=37888, K=3584, M=6)"),
                "per_kernel_traffic_bytes": traffic,
                "algorithmic_bytes": {"gate_up": 37888 * 3584 // 2 + 37888 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 37888 * 2,
-                                     "qkv": 4608 * 3584 // 2 + 4608 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 4608 * 2},
+                                     "qkv": 4608 * 3584 // 2 + 4608 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 4608 * 2,
+                                     "2-bit gate_up": 37888 * 3584 // 4 + 37888 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 37888 * 2},
                "source": f"gpurun_out/k2_*_{tag}.ncu-rep (ncu --set full)"},
               open(os.path.join(dst, "k2_traffic.json"), "w"), indent=1)
 print("\n".join(out))
