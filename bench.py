@@ -338,6 +338,12 @@ def run_ours(a):
         for t in step():
             emitted += len(t)
             taus.append(len(t))
+    # steady state: the region starts with the streaming ring already prefetched for the next verify
+    # (by the warm-up steps), so it also ends only when the ring is prefetched again — the copy
+    # stream's outstanding prefetch is inside the timed region
+    ring_full = torch.cuda.Event()
+    ring_full.record(ss.copy_stream)
+    cs.wait_event(ring_full)
     e1.record(cs)
     torch.cuda.synchronize()
     if dist:
@@ -382,6 +388,10 @@ def run_ours(a):
                "ms_per_step": wall / n_e2e * 1e3}
     elif not a.no_e2e:
         root = int(ss.step(D, k, T)[-1])
+        # one untimed step through the same calls (the host-root draft path has its own graph instance)
+        ss.draft_tree(D, k, T, root_token=root, want_tree=False)
+        ss.verify_tree(want=False)
+        root = ss.accept_and_commit(D + 1)[0][-1]
         if dist:
             dist.barrier()
         torch.cuda.synchronize()

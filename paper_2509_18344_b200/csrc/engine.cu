@@ -1867,6 +1867,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = e;
     p.qbits = c->sub_bits;
+    p.ctas_per_sm = (group == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
     launch_gemv(!w.resident, p, c->gv_grid, false, c->cs);
   } else {
     GemmParams p{};

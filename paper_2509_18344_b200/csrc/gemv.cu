@@ -56,8 +56,10 @@ int gemv_max_segments(int N, int K, int grid) {
   return mx;
 }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4>
-__global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(const GemvParams p) {
+// CW: consumer warps (8; 16 for the one-CTA-per-SM qkv plan: warps w and w + 8 take the two
+// tile-chunks of every stage for the same 16 rows and their partial sums are added at the flush)
+template <bool Q4, int NT, bool kCluster, int QB = 4, int CW = 8>
+__global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 1) gemv_kernel(const GemvParams p) {
   using C = GemvCfg<Q4, NT, QB>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int kStages = p.stages;
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kGemvConsumerWarps);
+      mbar_init(&empty[s], CW);
     }
     mbar_init(xbar, 1);
     fence_barrier_init();
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   __syncthreads();
   griddep_launch();   // grid <= one CTA per SM: let the next kernel prefetch now
 
-  if (warp == kGemvConsumerWarps) {
+  if (warp == CW) {
     // ------------------------------ producer -------------------------------
     Work w = make_work<kCluster>(p.N, p.K, crank, csize);
     const int64_t n_stage = w.stages(nC, C::kCPS);
@@ -207,10 +209,11 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   griddep_wait();
   if (threadIdx.x == 0) SS_TRACE_CTA0(2);
   const int g = lane >> 2, t4 = lane & 3;
-  const int nthr = kGemvConsumerWarps * 32;
+  const int nthr = CW * 32;
+  const int rw = warp & 7, hh = CW == 16 ? (warp >> 3) : -1;   // row warp, chunk half
   int xc0 = 0;   // first chunk of the resident X
   if constexpr (kCluster) {
-    if (p.xnorm) {
+    if (CW == 8 && p.xnorm) {
       // RMSNorm of this CTA's K range: r_m from the per-tile sums of squares (warp m, fixed shuffle
       // tree), then (token, 64-group) pairs: a warp takes 64 columns of one token, 2 per lane
       const Work w0 = make_work<kCluster>(p.N, p.K, crank, csize);
@@ -284,7 +287,25 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
 #pragma unroll
   for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
-  auto stash = [&](float* dst) { stash_acc<NT>(acc, dst, warp, lane); };
+  auto stash = [&](float* dst) {   // [128][Mpad] partial tile (CW = 16: half 0 stores, half 1 adds)
+    if constexpr (CW == 16) {
+      if (hh == 0) stash_acc<NT>(acc, dst, rw, lane);
+      named_bar(1, nthr);
+      if (hh == 1) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int n0 = rw * 16 + g, m = j * 8 + 2 * t4, Mp = NT * 8;
+          dst[n0 * Mp + m] += acc[j][0];
+          dst[n0 * Mp + m + 1] += acc[j][1];
+          dst[(n0 + 8) * Mp + m] += acc[j][2];
+          dst[(n0 + 8) * Mp + m + 1] += acc[j][3];
+          acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        }
+      }
+    } else {
+      stash_acc<NT>(acc, dst, warp, lane);
+    }
+  };
 
   uint32_t xph = 0;   // phase of xbar
   auto flush = [&](int r, int c_first, int c_last, bool last) {
@@ -316,14 +337,30 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         for (int m = 0; m < nvalid; ++m)
           bulk_g2s(xpre + m * kTileRows, p.epi.x + int64_t(mlo + m) * p.epi.ldx + int64_t(r) * kTileRows, kTileRows * 4, xbar);
       }
+      if (CW == 8 || hh == 0) {
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
-        const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
-        otile[m * kTileRows + n0] = acc[j][0];
-        otile[(m + 1) * kTileRows + n0] = acc[j][1];
-        otile[m * kTileRows + n0 + 8] = acc[j][2];
-        otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
-        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
+          const int n0 = rw * 16 + g, m = j * 8 + 2 * t4;
+          otile[m * kTileRows + n0] = acc[j][0];
+          otile[(m + 1) * kTileRows + n0] = acc[j][1];
+          otile[m * kTileRows + n0 + 8] = acc[j][2];
+          otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
+          acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        }
+      }
+      if constexpr (CW == 16) {   // the other chunk half adds its partial sums (fixed order)
+        named_bar(1, nthr);
+        if (hh == 1) {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int n0 = rw * 16 + g, m = j * 8 + 2 * t4;
+            otile[m * kTileRows + n0] += acc[j][0];
+            otile[(m + 1) * kTileRows + n0] += acc[j][1];
+            otile[m * kTileRows + n0 + 8] += acc[j][2];
+            otile[(m + 1) * kTileRows + n0 + 8] += acc[j][3];
+            acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+          }
+        }
       }
       named_bar(1, nthr);
       for (int i = threadIdx.x; i < Mpad * (kTileRows / 4); i += nthr) {
@@ -403,11 +440,11 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         SS_TRACE_CTA0(3);
         if (ct) ct[2] = gtime();
       }
-      if (p.xnorm)
+      if (CW == 8 && p.xnorm)
         consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
                               xsres + (w.c - xc0) * 2 * Mpad);
       else
-        consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane);
+        consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, rw, lane, nullptr, nullptr, hh);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) {
@@ -466,7 +503,7 @@ int gemv_cluster_split(int N, int K, int sms, int hint) {
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4>
+template <bool Q4, int NT, bool kCluster, int QB = 4, int CW = 8>
 static int ensure_attrs() {   // ring stages for this instantiation; sets the smem/cluster attributes once
   using C = GemvCfg<Q4, NT, QB>;
   static int stages = 0;
@@ -477,9 +514,9 @@ static int ensure_attrs() {   // ring stages for this instantiation; sets the sm
     int st = budget / C::kStageBytes;
     if (st < 2) st = 2;
     if (st > C::kMaxStages) st = C::kMaxStages;
-    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::smem_for(st) + (kCluster ? 8 * (C::kXBytes + C::kSBytes) : 0));
-    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB, CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     stages = st;
   }
   return stages;
@@ -493,7 +530,7 @@ struct ClusterPlan {
   int S, ncl;
   bool all_resident;
 };
-template <bool Q4, int NT, int QB = 4>
+template <bool Q4, int NT, int QB = 4, int CW = 8>
 static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   static std::mutex mu;
   static std::map<std::tuple<int, int, int>, ClusterPlan> cache;
@@ -502,7 +539,7 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   using C = GemvCfg<Q4, NT, QB>;
-  const int stages = ensure_attrs<Q4, NT, true, QB>();
+  const int stages = ensure_attrs<Q4, NT, true, QB, CW>();
   const int tiles = N / 128;
   const int per_sm = per_sm_for(N, K, hint);
   const int S0 = gemv_cluster_split(N, K, sms, hint);
@@ -513,7 +550,7 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     if (ncl < 1) ncl = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncl * S);
-    cfg.blockDim = dim3(kGemvThreads);
+    cfg.blockDim = dim3((CW + 1) * 32);
     cfg.dynamicSmemBytes = C::smem_for(stages);
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -523,7 +560,7 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true, QB>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true, QB, CW>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       active = ncl;   // cannot query: keep the arithmetic plan
     }
@@ -562,10 +599,10 @@ bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits) {
   }
 }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4>
+template <bool Q4, int NT, bool kCluster, int QB = 4, int CW = 8>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
   using C = GemvCfg<Q4, NT, QB>;
-  const int stages = ensure_attrs<Q4, NT, kCluster, QB>();
+  const int stages = ensure_attrs<Q4, NT, kCluster, QB, CW>();
   GemvParams p = p0;
   p.stages = stages;
   p.xn_chunks = 0;
@@ -577,7 +614,7 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   const size_t xbytes = size_t(p.xn_chunks) * (C::kXBytes + C::kSBytes);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemvThreads);
+  cfg.blockDim = dim3((CW + 1) * 32);
   cfg.dynamicSmemBytes = C::smem_for(stages) + xbytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -596,12 +633,17 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster, QB>, p);
+  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster, QB, CW>, p);
 }
 
 template <bool Q4, int NT, int QB = 4>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
-  if (gemv_use_cluster(p.N, p.K, sms)) {
+  static const bool cw16 = env_int("SS_GEMV_CW16", 0) != 0;   // opt-in: measured slower in the pass
+  if (gemv_use_cluster(p.N, p.K, sms) && Q4 && cw16 && p.ctas_per_sm == 1 && !p.xnorm) {
+    // one CTA per SM: 16 consumer warps (two per 16-row block, one per tile-chunk of a stage)
+    const ClusterPlan pl = cluster_plan<Q4, NT, QB, 16>(p.N, p.K, sms, p.ctas_per_sm);
+    launch_t<Q4, NT, true, QB, 16>(p, pl.ncl * pl.S, pl.S, pdl, st);
+  } else if (gemv_use_cluster(p.N, p.K, sms)) {
     const ClusterPlan pl = cluster_plan<Q4, NT, QB>(p.N, p.K, sms, p.ctas_per_sm);
     launch_t<Q4, NT, true, QB>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {

@@ -164,13 +164,16 @@ SS_DEV Work make_work(int N, int K, uint32_t crank, uint32_t csize) {
 // accumulated into this warp's 16 rows x Mpad tokens.
 template <bool Q4, int NT, int QB = 4>
 SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], int warp, int lane,
-                          const uint8_t* xres = nullptr, const float* xsres = nullptr) {
+                          const uint8_t* xres = nullptr, const float* xsres = nullptr, int ci_only = -1) {
+  // warp: row warp (rows 16 warp .. +15 of the tile); ci_only >= 0: only that tile-chunk of the
+  // stage (16-consumer-warp CTAs split a stage's two chunks over two warp halves)
   using C = GemvCfg<Q4, NT, QB>;
   const int g = lane >> 2, t4 = lane & 3;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
 #pragma unroll
   for (int ci = 0; ci < C::kCPS; ++ci) {
     if (ci >= nch) break;
+    if (ci_only >= 0 && ci != ci_only) continue;
     const uint8_t* wst = stage + ci * C::kWBytes;
     // activations: from the stage (TMA) or from a CTA-resident normalised copy (xres, xsres)
     const uint8_t* xst = (xres ? xres + ci * C::kXBytes : stage + C::kCPS * C::kWBytes + ci * C::kXBytes) + ((t4 * 8 + g) * 8);
