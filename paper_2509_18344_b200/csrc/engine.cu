@@ -1179,7 +1179,10 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
     }
   }
   // the staging ring takes what is left after the fused-pass tables (reserved here, see below)
-  const size_t pass_reserve = size_t(64) << 20;
+  // the phase table of the persistent pass (~100 KB) always; its Stream-K partials only when the
+  // opt-in fused pass is requested — otherwise that VRAM belongs to the streaming ring
+  const char* fdv = getenv("SS_FUSED_DRAFT");
+  const size_t pass_reserve = (fdv && fdv[0] == '1') ? (size_t(64) << 20) : (size_t(1) << 20);
   c->ring_bytes = (c->ar.cap - c->ar.used - pass_reserve - 4096) / 4096 * 4096;
   c->ring = (uint8_t*)c->ar.alloc(c->ring_bytes, 4096);
   if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
