@@ -121,13 +121,13 @@ class OracleSample:
     (1 + k(D-1)) draft + (1 + kD) target node-forwards through all layers.  The seeded weights are
     generated once (setup); every call of step_seconds() re-times the sample."""
 
-    def __init__(self, cfg, depth, topk, nodes=6):
+    def __init__(self, cfg, depth, topk, nodes=6, bits=4):
         from oracle.model import TargetWeights, draft_layers
         self.cfg, self.depth, self.topk, self.nodes = cfg, depth, topk, nodes
         self.cfg1 = cfg.with_(n_layers=1)
         t0 = time.time()
         self.tw = TargetWeights(self.cfg1, SEED)
-        self.dl = draft_layers(self.tw, 0)
+        self.dl = draft_layers(self.tw, 0, bits)
         self.setup = time.time() - t0
 
     def step_seconds(self):
@@ -164,9 +164,9 @@ class OracleSample:
         return step, info
 
 
-def oracle_step_seconds(cfg, depth, topk, nodes=6):
+def oracle_step_seconds(cfg, depth, topk, nodes=6, bits=4):
     """One-shot OracleSample (setup + one timed sample) -> (seconds/step, info)."""
-    return OracleSample(cfg, depth, topk, nodes).step_seconds()
+    return OracleSample(cfg, depth, topk, nodes, bits).step_seconds()
 
 
 def load_tau():
@@ -185,7 +185,7 @@ def run_reference(a):
     tau = tau_rec["tau"] if tau_rec and tau_rec.get("config") == a.config else 1.0
     times = []
     info = None
-    sample = OracleSample(cfg, a.depth, a.topk)   # weights generated once, each step re-timed
+    sample = OracleSample(cfg, a.depth, a.topk, bits=a.sub_bits)   # weights generated once, each step re-timed
     for i in range(a.warmup + a.steps):
         s, info = sample.step_seconds()
         if i >= a.warmup:
@@ -193,7 +193,7 @@ def run_reference(a):
     step_s = statistics.mean(times)
     value = tau / step_s
     cores = blas_threads()
-    sample = (f"1 {cfg.name}-shape decoder layer (bf16 target + 4-bit substitute, fp64 NumPy oracle) + head, 6 draft "
+    sample = (f"1 {cfg.name}-shape decoder layer (bf16 target + {a.sub_bits}-bit substitute, fp64 NumPy oracle) + head, 6 draft "
               f"and 6 target node-forwards per step, extrapolated to a D={a.depth},k={a.topk} step "
               f"({info['node_forwards']} node-forwards x {cfg.n_layers} layers); tau={tau:.3f} "
               f"({'from the deterministic GPU run, ' + TAU_FILE if tau_rec else 'assumed 1'})")
@@ -485,7 +485,7 @@ def run_ours(a):
             except Exception:
                 pass
         if world == 1 and not a.no_cpu_baseline:
-            s, info = oracle_step_seconds(cfg, D, k)
+            s, info = oracle_step_seconds(cfg, D, k, bits=a.sub_bits)
             line["cpu_baseline"] = {
                 "value": tau / s, "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
                 "sample": (f"1 {cfg.name}-shape decoder layer + head, 6 draft + 6 target node-forwards (fp64 NumPy "

@@ -18,3 +18,13 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
     assert "workload" in line["config"]
+
+
+def test_reference_arm_2bit_workload():
+    # --sub-bits 2 (NEXT-3): the oracle sample quantizes its substitute with 2 bits and says so
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "tiny",
+                        "--steps", "1", "--warmup", "0", "--depth", "4", "--sub-bits", "2"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert "2-bit" in line["config"]["workload"] and "2-bit substitute" in line["cpu_baseline"]["sample"]
