@@ -49,6 +49,10 @@ def args_():
                     help="request slots per GPU sharing one weight stream (SURVEY 8(f) NEXT-2); 1 = the paper's batch 1")
     ap.add_argument("--sub-bits", type=int, default=4, choices=[4, 2],
                     help="substitute code bits (4 = the paper's setting, P:278; 2 = NEXT-3, P:343)")
+    ap.add_argument("--embed-gpu", action="store_true",
+                    help="embedding GPU-resident in the arena (PAPER.md:534) instead of mapped host memory (R24)")
+    ap.add_argument("--no-async", action="store_true",
+                    help="Table-2 ablation: no copy/compute overlap in the verify streaming (PAPER.md:305-308)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -245,7 +249,7 @@ def load_weights_for_job(ss, dist, local, n_resident):
     barrier (each process page-locks its mapping).  Falls back to a per-rank store when /dev/shm is
     too small or SS_SHARED_HOST=0.  Returns the SharedMemory handle (kept alive) or None."""
     if dist is None or n_resident < 0 or os.environ.get("SS_SHARED_HOST", "1") == "0":
-        ss.load_weights(SEED, n_resident=n_resident)
+        ss.load_synthetic(SEED, n_resident=n_resident)
         return None
     import torch
     from multiprocessing import shared_memory
@@ -267,12 +271,12 @@ def load_weights_for_job(ss, dist, local, n_resident):
         if shm is not None:
             shm.close()
             shm.unlink()
-        ss.load_weights(SEED, n_resident=n_resident)
+        ss.load_synthetic(SEED, n_resident=n_resident)
         return None
     import ctypes
     if local == 0:
         addr = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
-        ss.load_weights_shared(SEED, n_resident, addr, nbytes, fill=True)
+        ss.load_synthetic_shared(SEED, n_resident, addr, nbytes, fill=True)
     dist.barrier()
     if local != 0:
         shm = shared_memory.SharedMemory(name=name)
@@ -282,7 +286,7 @@ def load_weights_for_job(ss, dist, local, n_resident):
         except Exception:
             pass
         addr = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
-        ss.load_weights_shared(SEED, n_resident, addr, nbytes, fill=False)
+        ss.load_synthetic_shared(SEED, n_resident, addr, nbytes, fill=False)
     return shm
 
 
@@ -308,7 +312,7 @@ def run_ours(a):
     t_setup = time.time()
     Bq = a.batch
     ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256,
-                 max_batch=Bq)
+                 max_batch=Bq, embed_on_host=0 if a.embed_gpu else 1, async_stream=0 if a.no_async else 1)
     if a.sub_bits != 4:
         ss.set_substitute_bits(a.sub_bits)
     shm = load_weights_for_job(ss, dist, local, a.n_resident)

@@ -30,8 +30,7 @@
  *  - Capacity: before drafting, D is clamped to D_eff = min(D, floor((max_context - P - 1)/k));
  *    D_eff = 0 runs an AR step (tree = root only).  SS_ERR_CAPACITY only when P + 1 > max_context,
  *    detected before any write.
- *  - Layouts: token ids int32; all weights bf16 [out x in] row-major in the generator's index
- *    space.
+ *  - Layouts: token ids int32; all weights bf16 [out x in] row-major (bit patterns as uint16).
  */
 #ifndef SUBSPEC_H
 #define SUBSPEC_H
@@ -51,12 +50,21 @@ typedef enum {
   SS_ERR_CUDA = 5       /* CUDA failure; context poisoned */
 } ss_status;
 
+/* Arithmetic of the forward passes.  SS_BF16: the target is bf16 (BASELINE.json;
+ * PAPER.md:361 "Original (fp16)", reading R20) with bf16 rounding at the named points of reading R3
+ * (normed inputs, q/k/v, attention output, SiLU*mul) and fp32 accumulation; parity tolerance 2e-2 x
+ * logit scale.  SS_FP32: the same weights (bf16 values, exact in fp32) with every activation kept in
+ * fp32 (no rounding points, fp32 KV cache, fp32 CUDA-core arithmetic); parity tolerance 1e-4 x logit
+ * scale.  SS_FP32 is a parity mode: it supports n_resident = n_layers (nothing streamed), batch 1. */
+enum { SS_BF16 = 0, SS_FP32 = 1 };
+
 /* Decoder-only model shape (Llama/Qwen family).  hidden, ffn, qkv rows and vocab
  * must be multiples of 128; head_dim is 64 or 128; n_heads % n_kv_heads == 0. */
 typedef struct {
   int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, max_context;
   float rope_theta, rms_eps;
   int32_t qkv_bias;
+  int32_t precision;    /* SS_BF16 (0) or SS_FP32 (1) */
 } ss_model_config;
 
 /* Sizes the context provisions buffers for (all >= the values later used). */
@@ -68,6 +76,23 @@ typedef struct {
                            request, the paper's batch 1); max_batch * max_top_k <= 32.  Each
                            slot owns max_context rows of committed KV inside the arena. */
 } ss_limits;
+
+/* Per-context options (ss_create; NULL = the defaults below).  They replace process-wide
+ * environment switches, so contexts in one process may differ. */
+typedef struct {
+  int32_t embed_on_host;  /* 1 (default): the embedding table lives in mapped pinned host memory and
+                             a pass gathers its <= max_nodes rows over the host link (zero-copy); its
+                             2*vocab*hidden bytes of the VRAM cap go to the streaming ring (reading
+                             R24).  0: the embedding is GPU-resident in the arena, the
+                             placement of PAPER.md:534 ("Embedding and head layers are default to be
+                             GPU-resident").  The head is always GPU-resident. */
+  int32_t async_stream;   /* 1 (default): layer copies overlap compute.  0: the
+                             Table-2 "async transfer" ablation: a group is copied only after the
+                             previous group's compute. */
+  int32_t cuda_graphs;    /* 1 (default): the draft loop is replayed from a CUDA graph; 0: eager */
+  int32_t fuse_norm;      /* 1 (default): RMSNorm fused into the o/down GEMV epilogues (draft) */
+} ss_options;
+void ss_default_options(ss_options* out);
 
 /* Substitute quantization: bits = 4, group_size = 64 are supported. */
 typedef struct { int32_t bits, group_size; } ss_quant_spec;
@@ -87,21 +112,56 @@ typedef struct ss_ctx ss_ctx;
 
 /* Create a context on `device`.  dev_arena/arena_bytes: caller-owned device block (torch), the
  * VRAM cap.  compute_stream/copy_stream: cudaStream_t handles (may be the same only if
- * streaming is never needed).  Errors: INVALID (shape), BUDGET (arena too small for fixed parts). */
-ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device, void* dev_arena,
-                    size_t arena_bytes, void* compute_stream, void* copy_stream, ss_ctx** out);
+ * streaming is never needed).  opt: NULL for ss_default_options.  Errors: INVALID (shape,
+ * precision), BUDGET (arena too small for fixed parts). */
+ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_options* opt, int device,
+                    void* dev_arena, size_t arena_bytes, void* compute_stream, void* copy_stream, ss_ctx** out);
 
-/* Generate the target's bf16 weights with the counter-based generator (seed) on the device and
- * place them: layers [0, n_resident) resident in the arena, the rest offloaded to the pinned host
- * store in device layout (App. H P:540 "All decoder layers ... offloaded" is
- * n_resident = 0).  n_resident = -1: the planner's maximum resident prefix under the cap
- * (SPEC.md:205-213).  Embedding, final norm and head are always resident. */
-ss_status ss_load_weights(ss_ctx* ctx, uint64_t seed, int32_t n_resident);
+/* The target's weights as caller-owned HOST arrays: bf16 bit patterns, matrices [out x in]
+ * row-major, read only during ss_load_weights (pageable or pinned memory).  Biases are NULL
+ * unless cfg.qkv_bias.  The substitutes are derived from these ("data-free",
+ * built from the target's own offloaded layers). */
+typedef struct {
+  const uint16_t* attn_norm;   /* [hidden] */
+  const uint16_t* wq;          /* [n_heads*head_dim x hidden] */
+  const uint16_t* bq;          /* [n_heads*head_dim] or NULL */
+  const uint16_t* wk;          /* [n_kv_heads*head_dim x hidden] */
+  const uint16_t* bk;          /* [n_kv_heads*head_dim] or NULL */
+  const uint16_t* wv;          /* [n_kv_heads*head_dim x hidden] */
+  const uint16_t* bv;          /* [n_kv_heads*head_dim] or NULL */
+  const uint16_t* wo;          /* [hidden x n_heads*head_dim] */
+  const uint16_t* mlp_norm;    /* [hidden] */
+  const uint16_t* wg;          /* [ffn x hidden] */
+  const uint16_t* wu;          /* [ffn x hidden] */
+  const uint16_t* wd;          /* [hidden x ffn] */
+} ss_host_layer;
+typedef struct {
+  const uint16_t* embed;        /* [vocab x hidden] */
+  const ss_host_layer* layers;  /* [n_layers] */
+  const uint16_t* final_norm;   /* [hidden] */
+  const uint16_t* head;         /* [vocab x hidden] (untied) */
+} ss_host_weights;
+
+/* Load the target's bf16 weights from caller-owned host arrays and place them: layers
+ * [0, n_resident) resident in the arena, the rest offloaded to the context's pinned host store in
+ * device layout (App. H P:540 "All decoder layers ... offloaded" is n_resident = 0).
+ * n_resident = -1: the planner's maximum resident prefix under the cap.  The
+ * head and final norm are GPU-resident; the embedding as ss_options.embed_on_host says.  The
+ * library keeps no pointer into `w` after returning.  Errors: INVALID (NULL tensor, bias presence
+ * differs from cfg.qkv_bias), BUDGET (placement does not fit the cap), STRUCTURE (already loaded),
+ * CUDA. */
+ss_status ss_load_weights(ss_ctx* ctx, const ss_host_weights* w, int32_t n_resident);
+
+/* As ss_load_weights, with the weights generated on the device by the counter-based synthetic
+ * generator of SURVEY.md §8(c) O.1 (seed; the same values synth/weights.py produces on the host).
+ * The benchmark workloads use it so that a 7B/32B-shape model need not be materialised on the host
+ * first. */
+ss_status ss_load_weights_synthetic(ss_ctx* ctx, uint64_t seed, int32_t n_resident);
 
 /* Code width of the substitutes this context will build: 4 (default; "4 bits with a
  * group size 64") or 2 (the paper's "more aggressive ... 2-bit" direction,
  * PAPER.md:343; same min/max RTN rule with 2^bits - 1 levels).  Fixes the substitutes' layout and
- * footprint (2-bit: 0.3125 B/weight vs 0.5625), so it is only valid before ss_load_weights; the
+ * footprint (2-bit: 0.3125 B/weight vs 0.5625), so it is only valid before loading weights; the
  * arena bytes it frees go to the streaming ring.  ss_build_substitutes must then pass the same bits.
  * Errors: STRUCTURE (after load), INVALID (bits not 2 or 4). */
 ss_status ss_set_substitute_bits(ss_ctx* ctx, int32_t bits);
@@ -110,7 +170,7 @@ ss_status ss_set_substitute_bits(ss_ctx* ctx, int32_t bits);
  * Errors: INVALID. */
 ss_status ss_host_store_bytes(ss_ctx* ctx, int32_t n_resident, size_t* out_bytes);
 
-/* As ss_load_weights, but the offloaded layers live in a CALLER-OWNED host store (e.g. one POSIX
+/* As ss_load_weights_synthetic, but the offloaded layers live in a CALLER-OWNED host store (e.g. one POSIX
  * shared-memory segment mapped by every rank of a multi-GPU job, so the node holds one copy —
  * SURVEY §8(e)).  host_store: >= ss_host_store_bytes(n_resident) bytes, page-aligned, owned by the
  * caller and kept alive until ss_destroy; the library page-locks it with cudaHostRegister (portable,
@@ -118,8 +178,8 @@ ss_status ss_host_store_bytes(ss_ctx* ctx, int32_t n_resident, size_t* out_bytes
  * layers into the store (one context of the job); fill = 0: the store already holds them (the caller
  * orders the filling context's return before this call, e.g. with a barrier).  n_resident >= 0.
  * Errors: INVALID, BUDGET (store too small), CUDA (registration failed), as ss_load_weights. */
-ss_status ss_load_weights_shared(ss_ctx* ctx, uint64_t seed, int32_t n_resident, void* host_store,
-                                 size_t host_bytes, int32_t fill);
+ss_status ss_load_weights_synthetic_shared(ss_ctx* ctx, uint64_t seed, int32_t n_resident, void* host_store,
+                                           size_t host_bytes, int32_t fill);
 
 /* Build the 4-bit (or, after ss_set_substitute_bits(2), 2-bit) group-64 substitute of every offloaded layer: stream it host->device through
  * the staging ring and quantize on the device (K1).  Norms/biases are shared. */

@@ -23,7 +23,25 @@ STATUS = {0: "SS_OK", 1: "SS_ERR_INVALID", 2: "SS_ERR_CAPACITY", 3: "SS_ERR_STRU
 class ModelConfigC(ctypes.Structure):
     _fields_ = [("n_layers", c_int32), ("hidden", c_int32), ("n_heads", c_int32), ("n_kv_heads", c_int32),
                 ("head_dim", c_int32), ("ffn", c_int32), ("vocab", c_int32), ("max_context", c_int32),
-                ("rope_theta", c_float), ("rms_eps", c_float), ("qkv_bias", c_int32)]
+                ("rope_theta", c_float), ("rms_eps", c_float), ("qkv_bias", c_int32), ("precision", c_int32)]
+
+
+SS_BF16, SS_FP32 = 0, 1
+
+
+class OptionsC(ctypes.Structure):
+    _fields_ = [("embed_on_host", c_int32), ("async_stream", c_int32), ("cuda_graphs", c_int32),
+                ("fuse_norm", c_int32)]
+
+
+class HostLayerC(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("attn_norm", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "mlp_norm", "wg", "wu",
+                                        "wd")]
+
+
+class HostWeightsC(ctypes.Structure):
+    _fields_ = [("embed", c_void_p), ("layers", ctypes.POINTER(HostLayerC)), ("final_norm", c_void_p),
+                ("head", c_void_p)]
 
 
 class LimitsC(ctypes.Structure):
@@ -49,11 +67,13 @@ class StatsC(ctypes.Structure):
 
 P = ctypes.POINTER
 _FUNCS = {
-    "ss_create": [P(ModelConfigC), P(LimitsC), ctypes.c_int, c_void_p, c_size_t, c_void_p, c_void_p, P(c_void_p)],
-    "ss_load_weights": [c_void_p, c_uint64, c_int32],
+    "ss_create": [P(ModelConfigC), P(LimitsC), P(OptionsC), ctypes.c_int, c_void_p, c_size_t, c_void_p, c_void_p,
+                  P(c_void_p)],
+    "ss_load_weights": [c_void_p, P(HostWeightsC), c_int32],
+    "ss_load_weights_synthetic": [c_void_p, c_uint64, c_int32],
     "ss_set_substitute_bits": [c_void_p, c_int32],
     "ss_host_store_bytes": [c_void_p, c_int32, P(c_size_t)],
-    "ss_load_weights_shared": [c_void_p, c_uint64, c_int32, c_void_p, c_size_t, c_int32],
+    "ss_load_weights_synthetic_shared": [c_void_p, c_uint64, c_int32, c_void_p, c_size_t, c_int32],
     "ss_build_substitutes": [c_void_p, P(QuantSpecC)],
     "ss_prefill": [c_void_p, c_void_p, c_int32, c_int32, P(c_int32)],
     "ss_draft_tree": [c_void_p, c_int32, P(DraftParamsC), c_void_p, c_void_p, c_void_p, c_void_p, P(c_int32)],
@@ -80,7 +100,7 @@ _FUNCS = {
     "ss_debug_trace_pass": [c_void_p, c_int32, c_void_p, c_int32, P(c_int32)],
     "ss_debug_cta_trace": [c_void_p, c_int32, c_int32, c_void_p, c_int32, P(c_int32)],
 }
-EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy"]
+EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy", "ss_default_options"]
 
 _lib = None
 
@@ -101,6 +121,8 @@ def load_library(path=None):
     lib.ss_last_error.restype = ctypes.c_char_p
     lib.ss_destroy.argtypes = [c_void_p]
     lib.ss_destroy.restype = None
+    lib.ss_default_options.argtypes = [P(OptionsC)]
+    lib.ss_default_options.restype = None
     _lib = lib
     return lib
 
@@ -115,28 +137,38 @@ def _ptr(a):
     return a.ctypes.data_as(c_void_p) if a is not None else None
 
 
-def model_config_c(cfg):
+def model_config_c(cfg, precision=SS_BF16):
     return ModelConfigC(cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn, cfg.vocab,
-                        cfg.max_context, cfg.rope_theta, cfg.rms_eps, int(cfg.qkv_bias))
+                        cfg.max_context, cfg.rope_theta, cfg.rms_eps, int(cfg.qkv_bias), int(precision))
 
 
 class SubSpec:
     """One decode session on one GPU: the C-ABI context plus its torch-owned arena and streams."""
 
-    def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256, max_batch=1):
+    def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256, max_batch=1,
+                 precision=SS_BF16, **options):
+        """options: ss_options fields (embed_on_host, async_stream, cuda_graphs, fuse_norm)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("SubSpec needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
         self.cfg = cfg
         self.device = device
+        self.precision = precision
         self.limits = LimitsC(max_depth, max_top_k, max_chunk, max_batch)
+        self.options = OptionsC()
+        self.lib.ss_default_options(ctypes.byref(self.options))
+        for k, v in options.items():
+            if k not in dict(OptionsC._fields_):
+                raise TypeError(f"unknown ss_options field {k}")
+            setattr(self.options, k, int(v))
         self.arena = torch.empty(int(arena_bytes), dtype=torch.uint8, device=f"cuda:{device}")
         self.compute_stream = torch.cuda.Stream(device=device)
         self.copy_stream = torch.cuda.Stream(device=device)
         torch.cuda.synchronize(device)
         ctx = c_void_p()
-        st = self.lib.ss_create(ctypes.byref(model_config_c(cfg)), ctypes.byref(self.limits), device,
+        st = self.lib.ss_create(ctypes.byref(model_config_c(cfg, precision)), ctypes.byref(self.limits),
+                                ctypes.byref(self.options), device,
                                 c_void_p(self.arena.data_ptr()), c_size_t(int(arena_bytes)),
                                 c_void_p(self.compute_stream.cuda_stream), c_void_p(self.copy_stream.cuda_stream),
                                 ctypes.byref(ctx))
@@ -164,20 +196,55 @@ class SubSpec:
         """Substitute code width (4 or 2); before load_weights (sizes the substitutes' layout)."""
         self._check(self.lib.ss_set_substitute_bits(self.ctx, bits))
 
-    def load_weights(self, seed, n_resident=0):
-        self._check(self.lib.ss_load_weights(self.ctx, c_uint64(seed), n_resident))
+    def load_weights(self, weights, n_resident=0):
+        """weights: dict name -> uint16 array of bf16 bits in synth/weights.py's naming ("embed",
+        "l{l}.wq", ..., "final_norm", "head"), [out x in] row-major.  Only marshalled: the library
+        copies and tiles them on the device."""
+        c = self.cfg
+        keep = {}
+
+        def ptr(name, shape):
+            a = np.ascontiguousarray(weights[name], dtype=np.uint16)
+            if a.shape != tuple(shape):
+                raise ValueError(f"{name}: shape {a.shape} != {tuple(shape)}")
+            keep[name] = a
+            return a.ctypes.data_as(c_void_p)
+
+        layers = (HostLayerC * c.n_layers)()
+        for l in range(c.n_layers):
+            L = layers[l]
+            L.attn_norm = ptr(f"l{l}.attn_norm", (c.hidden,))
+            L.wq = ptr(f"l{l}.wq", (c.q_dim, c.hidden))
+            L.wk = ptr(f"l{l}.wk", (c.kv_dim, c.hidden))
+            L.wv = ptr(f"l{l}.wv", (c.kv_dim, c.hidden))
+            if c.qkv_bias:
+                L.bq = ptr(f"l{l}.bq", (c.q_dim,))
+                L.bk = ptr(f"l{l}.bk", (c.kv_dim,))
+                L.bv = ptr(f"l{l}.bv", (c.kv_dim,))
+            L.wo = ptr(f"l{l}.wo", (c.hidden, c.q_dim))
+            L.mlp_norm = ptr(f"l{l}.mlp_norm", (c.hidden,))
+            L.wg = ptr(f"l{l}.wg", (c.ffn, c.hidden))
+            L.wu = ptr(f"l{l}.wu", (c.ffn, c.hidden))
+            L.wd = ptr(f"l{l}.wd", (c.hidden, c.ffn))
+        hw = HostWeightsC(ptr("embed", (c.vocab, c.hidden)), layers, ptr("final_norm", (c.hidden,)),
+                          ptr("head", (c.vocab, c.hidden)))
+        self._check(self.lib.ss_load_weights(self.ctx, ctypes.byref(hw), n_resident))
+
+    def load_synthetic(self, seed, n_resident=0):
+        """Weights from the library's device-side synthetic generator."""
+        self._check(self.lib.ss_load_weights_synthetic(self.ctx, c_uint64(seed), n_resident))
 
     def host_store_bytes(self, n_resident=0):
         out = c_size_t()
         self._check(self.lib.ss_host_store_bytes(self.ctx, n_resident, ctypes.byref(out)))
         return out.value
 
-    def load_weights_shared(self, seed, n_resident, store_addr, store_bytes, fill):
+    def load_synthetic_shared(self, seed, n_resident, store_addr, store_bytes, fill):
         """Offloaded layers in a caller-owned host store (address of a page-aligned mapping that
         outlives this context, e.g. multiprocessing.shared_memory); fill=True generates them."""
         self._keep_store = store_addr
-        self._check(self.lib.ss_load_weights_shared(self.ctx, c_uint64(seed), n_resident, c_void_p(store_addr),
-                                                     store_bytes, 1 if fill else 0))
+        self._check(self.lib.ss_load_weights_synthetic_shared(self.ctx, c_uint64(seed), n_resident,
+                                                               c_void_p(store_addr), store_bytes, 1 if fill else 0))
 
     def build_substitutes(self, bits=4, group=64):
         self._check(self.lib.ss_build_substitutes(self.ctx, ctypes.byref(QuantSpecC(bits, group))))

@@ -1,11 +1,9 @@
-// Tree-attention building blocks shared by the standalone K3 kernel and the fused draft pass.
+// K3 tree-attention building blocks (the per-(kv head, node) CTA of attn_node_kernel).
 #pragma once
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ss {
-
-constexpr int kAttnQB = 8;   // query nodes per CTA (one warp per node)
 
 SS_DEV void cp_async16(void* dst_smem, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)), "l"(src),
@@ -22,245 +20,6 @@ SS_DEV void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(smem_u32(p)));
-}
-
-// merge the partials of one row (qi, hq) in segment order and write bf16 FragX + group sums.
-// Executed by one warp.
-template <int D>
-SS_DEV void attn_combine_row(const AttnParams& p, int P, int qi, int hq, int lane) {
-  const int64_t row = int64_t(qi) * p.n_heads + hq;
-  const int nkeys = P + p.depth[p.node_base + qi] + 1;
-  const int nseg = (nkeys + p.split - 1) / p.split;
-  const float* ml = p.part_ml + row * p.n_seg_max * 2;
-  float m = -INFINITY;
-  for (int s = 0; s < nseg; ++s) m = fmaxf(m, __ldcg(ml + 2 * s));
-  constexpr int DPL = D / 32;
-  float o[DPL];
-#pragma unroll
-  for (int t = 0; t < DPL; ++t) o[t] = 0.f;
-  float l = 0.f;
-  for (int s = 0; s < nseg; ++s) {
-    const float w = exp2f(__ldcg(ml + 2 * s) - m);   // partial maxima are in base-2 units
-    l += w * __ldcg(ml + 2 * s + 1);
-    const float* po = p.part_o + (row * p.n_seg_max + s) * D + lane * DPL;
-#pragma unroll
-    for (int t = 0; t < DPL; ++t) o[t] += w * __ldcg(po + t);
-  }
-  const float inv = 1.0f / l;
-  float gs = 0.f;
-#pragma unroll
-  for (int t = 0; t < DPL; ++t) {
-    const uint16_t ob = f2bf(o[t] * inv);
-    p.out_fragx[fragx_offset(qi, int64_t(hq) * D + lane * DPL + t, p.out_nt)] = ob;
-    gs += bf2f(ob);
-  }
-  constexpr int LPG = 64 / DPL;   // lanes per 64-group: 16 (D = 128) or 32 (D = 64)
-#pragma unroll
-  for (int o2 = LPG / 2; o2; o2 >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o2);
-  if (p.out_xs && (lane % LPG) == 0)
-    p.out_xs[(int64_t(hq) * D / 64 + lane / LPG) * (p.out_nt * 8) + qi] = gs;
-}
-
-// One warp's share of K3: node qi (query row block = the grp heads of kv head kvh), logical keys
-// [seg*split, ...) of that node.  ks: this warp's 2 x (K, V) x 16 x (D+8) bf16 staging buffer.
-// single: every row fits one segment -> write the normalised output (FragX + group sums) directly;
-// otherwise write (o, m, l) partials for attn_combine_row.
-template <int D>
-SS_DEV void attn_task(const AttnParams& p, int P, int kvh, int seg, int qi, uint16_t* ks, bool single) {
-  constexpr int RS = D + 8;                        // padded bf16 row stride (ldmatrix conflict-free)
-  constexpr int TILE = 16 * RS;                    // one 16-key tile (elements)
-  constexpr int PIECES = 16 * D * 2 / 16;          // 16-byte pieces per 16-key tile
-  const int grp = p.n_heads / p.n_kv;
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int node = p.node_base + qi;
-  const int nkeys = P + p.depth[node] + 1;
-  const int k0 = seg * p.split;
-  const int nk = min(p.split, nkeys - k0);
-  if (nk <= 0) return;
-  const int* an = p.anc + int64_t(node) * p.anc_stride;
-  const uint16_t* kc = p.k_cache + int64_t(kvh) * p.max_ctx * D;
-  const uint16_t* vc = p.v_cache + int64_t(kvh) * p.max_ctx * D;
-  const uint16_t* kt = p.k_tree + int64_t(kvh) * p.max_nodes * D;
-  const uint16_t* vt = p.v_tree + int64_t(kvh) * p.max_nodes * D;
-
-  auto stage = [&](int t, int buf) {
-    uint16_t* kd = ks + buf * 2 * TILE;
-    uint16_t* vd = kd + TILE;
-#pragma unroll
-    for (int i = 0; i < PIECES / 32; ++i) {
-      const int pc = lane + 32 * i;
-      const int r = pc / (D / 8), col = (pc % (D / 8)) * 8;
-      const int kl = k0 + t * 16 + r;
-      const bool valid = (t * 16 + r) < nk;
-      const int64_t row = !valid ? 0 : (kl < P ? int64_t(kl) : int64_t(an[kl - P]));
-      const uint16_t* ksrc = (kl < P || !valid) ? kc : kt;
-      const uint16_t* vsrc = (kl < P || !valid) ? vc : vt;
-      cp_async16(kd + r * RS + col, ksrc + row * D + col, valid);
-      cp_async16(vd + r * RS + col, vsrc + row * D + col, valid);
-    }
-    cp_async_commit();
-  };
-
-  // Q fragments (rows = heads g and g+8 of this kv group; bf16 pairs), kept in registers
-  uint32_t qa[D / 16][4];
-  {
-    const int h0 = kvh * grp + g, h1 = kvh * grp + g + 8;
-    const uint16_t* q0 = p.q + (int64_t(qi) * p.n_heads + h0) * D;
-    const uint16_t* q1 = p.q + (int64_t(qi) * p.n_heads + h1) * D;
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const int c = kk * 16 + 2 * t4;
-      qa[kk][0] = g < grp ? *reinterpret_cast<const uint32_t*>(q0 + c) : 0u;
-      qa[kk][1] = g + 8 < grp ? *reinterpret_cast<const uint32_t*>(q1 + c) : 0u;
-      qa[kk][2] = g < grp ? *reinterpret_cast<const uint32_t*>(q0 + c + 8) : 0u;
-      qa[kk][3] = g + 8 < grp ? *reinterpret_cast<const uint32_t*>(q1 + c + 8) : 0u;
-    }
-  }
-  const float sl2 = rsqrtf(float(D)) * 1.4426950408889634f;   // softmax in base 2
-  float o[D / 8][4];
-#pragma unroll
-  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // rows g and g+8
-  const int ntiles = (nk + 15) / 16;
-  stage(0, 0);
-  for (int t = 0; t < ntiles; ++t) {
-    if (t + 1 < ntiles) {
-      stage(t + 1, (t + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-    const uint16_t* kd = ks + (t & 1) * 2 * TILE;
-    const uint16_t* vd = kd + TILE;
-    float sc[2][4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
-      const uint16_t* kr = kd + (j * 8 + g) * RS + 2 * t4;
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + kk * 16);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8);
-        mma_bf16_16816(sc[j], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
-      }
-    }
-    // mask keys beyond this node's logical sequence, then online softmax (base-2)
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int key = t * 16 + j * 8 + 2 * t4 + e;
-        const bool ok = key < nk;
-        sc[j][e] = ok ? sc[j][e] * sl2 : -INFINITY;
-        sc[j][2 + e] = ok ? sc[j][2 + e] * sl2 : -INFINITY;
-        mx0 = fmaxf(mx0, sc[j][e]);
-        mx1 = fmaxf(mx1, sc[j][2 + e]);
-      }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
-    const float a0 = exp2f(m0 - nm0), a1 = exp2f(m1 - nm1);   // m = -inf initially -> 0
-    m0 = nm0;
-    m1 = nm1;
-    float ps0 = 0.f, ps1 = 0.f;
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        sc[j][e] = exp2f(sc[j][e] - m0);
-        sc[j][2 + e] = exp2f(sc[j][2 + e] - m1);
-        ps0 += sc[j][e];
-        ps1 += sc[j][2 + e];
-      }
-    l0 = l0 * a0 + ps0;
-    l1 = l1 * a1 + ps1;
-#pragma unroll
-    for (int j = 0; j < D / 8; ++j) {
-      o[j][0] *= a0;
-      o[j][1] *= a0;
-      o[j][2] *= a1;
-      o[j][3] *= a1;
-    }
-    const uint32_t pa0 = pack_bf16(sc[0][0], sc[0][1]), pa1 = pack_bf16(sc[0][2], sc[0][3]);
-    const uint32_t pa2 = pack_bf16(sc[1][0], sc[1][1]), pa3 = pack_bf16(sc[1][2], sc[1][3]);
-    // V fragments via ldmatrix.trans: lanes 0-7 keys 0-7, 8-15 keys 8-15 of dim tile nd,
-    // lanes 16-31 the same keys of dim tile nd+1
-    const int lr = lane & 15, ld_off = (lane >> 4) * 8;
-#pragma unroll
-    for (int nd = 0; nd < D / 8; nd += 2) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_trans(b0, b1, b2, b3, vd + lr * RS + nd * 8 + ld_off);
-      mma_bf16_16816(o[nd], pa0, pa1, pa2, pa3, b0, b1);
-      mma_bf16_16816(o[nd + 1], pa0, pa1, pa2, pa3, b2, b3);
-    }
-    __syncwarp();
-  }
-  // row sums across the 4 lanes of a row
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  if (single) {
-    // single segment: normalise in registers, write bf16 FragX and the 64-group sums directly
-    const float i0 = 1.0f / l0, i1 = 1.0f / l1;
-    const int h0 = kvh * grp + g, h1 = h0 + 8;
-    float gs0[D / 64], gs1[D / 64];
-#pragma unroll
-    for (int q = 0; q < D / 64; ++q) gs0[q] = gs1[q] = 0.f;
-#pragma unroll
-    for (int nd = 0; nd < D / 8; ++nd)
-#pragma unroll
-      for (int e2 = 0; e2 < 2; ++e2) {
-        const int dim = nd * 8 + 2 * t4 + e2;
-        if (g < grp) {
-          const uint16_t b = f2bf(o[nd][e2] * i0);
-          p.out_fragx[fragx_offset(qi, int64_t(h0) * D + dim, p.out_nt)] = b;
-          gs0[dim / 64] += bf2f(b);
-        }
-        if (g + 8 < grp) {
-          const uint16_t b = f2bf(o[nd][2 + e2] * i1);
-          p.out_fragx[fragx_offset(qi, int64_t(h1) * D + dim, p.out_nt)] = b;
-          gs1[dim / 64] += bf2f(b);
-        }
-      }
-#pragma unroll
-    for (int q = 0; q < D / 64; ++q) {   // reduce over the 4 lanes t4 of row g
-      gs0[q] += __shfl_xor_sync(0xffffffffu, gs0[q], 1);
-      gs0[q] += __shfl_xor_sync(0xffffffffu, gs0[q], 2);
-      gs1[q] += __shfl_xor_sync(0xffffffffu, gs1[q], 1);
-      gs1[q] += __shfl_xor_sync(0xffffffffu, gs1[q], 2);
-      if (p.out_xs && t4 == 0) {
-        if (g < grp) p.out_xs[(int64_t(h0) * D / 64 + q) * (p.out_nt * 8) + qi] = gs0[q];
-        if (g + 8 < grp) p.out_xs[(int64_t(h1) * D / 64 + q) * (p.out_nt * 8) + qi] = gs1[q];
-      }
-    }
-    return;
-  }
-  const int64_t prow0 = int64_t(qi) * p.n_heads + kvh * grp + g;
-  if (g < grp) {
-    float* po = p.part_o + (prow0 * p.n_seg_max + seg) * D;
-#pragma unroll
-    for (int nd = 0; nd < D / 8; ++nd) *reinterpret_cast<float2*>(po + nd * 8 + 2 * t4) = make_float2(o[nd][0], o[nd][1]);
-    if (t4 == 0) {
-      p.part_ml[(prow0 * p.n_seg_max + seg) * 2] = m0;   // base-2 max
-      p.part_ml[(prow0 * p.n_seg_max + seg) * 2 + 1] = l0;
-    }
-  }
-  if (g + 8 < grp) {
-    const int64_t prow1 = prow0 + 8;
-    float* po = p.part_o + (prow1 * p.n_seg_max + seg) * D;
-#pragma unroll
-    for (int nd = 0; nd < D / 8; ++nd) *reinterpret_cast<float2*>(po + nd * 8 + 2 * t4) = make_float2(o[nd][2], o[nd][3]);
-    if (t4 == 0) {
-      p.part_ml[(prow1 * p.n_seg_max + seg) * 2] = m1;
-      p.part_ml[(prow1 * p.n_seg_max + seg) * 2 + 1] = l1;
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -113,11 +113,8 @@ struct ss_ctx {
   int gv_grid = 148;
   size_t gv_part_floats = 0;
   // attention scratch
-  float *at_o = nullptr, *at_ml = nullptr;
+  float* at_o = nullptr;        // debug output scratch (ss_debug_matmul / ss_debug_time_matmul)
   size_t at_o_floats = 0;
-  int* at_cnt = nullptr;
-  int at_seg_max = 0;
-  int split_draft = 32, split_target = 128;
   // topk scratch
   float *tk_max = nullptr, *tk_sum = nullptr, *tk_val = nullptr;
   int* tk_idx = nullptr;
@@ -138,27 +135,16 @@ struct ss_ctx {
   std::vector<bool> ev_pending;
   std::deque<int> timing_queue;
   int ev_pool = 0;
-  // fused persistent draft pass (pass.cu)
-  bool use_fused = false;
   int sub_bits = 4;           // substitute code bits (ss_set_substitute_bits; 2 = NEXT-3)
-  bool l2_prefetch = true;
-  bool attn_v2 = true;
-  std::vector<PhaseDesc> phases;
-  PhaseDesc* d_phases = nullptr;
-  float *sumsq = nullptr, *pass_part = nullptr;
-  unsigned* pass_bar = nullptr;
-  int* attn_ctr = nullptr;
+  ss_options opt{};           // per-context options (ss_create)
+  bool l2_prefetch = false;
+  float* sumsq = nullptr;     // fused RMSNorm: per-tile sums of squares [H/128][32]
   unsigned long long* norm_ctr = nullptr;
-  int* mlp_flags = nullptr;   // fused MLP: per gate_up tile flags + exit counter
   int* h_root = nullptr;      // pinned staging word for draft_tree's root token
-  bool xnorm = false;         // draft: next layer's qkv normalises its own K range (SS_XNORM=1)
-  bool xn_pending = false;    // the previous down left x + sums of squares, not a normed h
   bool serial_stream = false; // ablation: no copy/compute overlap in the verify streaming
   int last_consumed_ev = -1;
   cudaEvent_t ev_root = nullptr;
-  bool fuse_mlp = false;
   bool fuse_norm = true;
-  int pass_grid = 0, pass_stages = 0;
   // graphs
   std::map<std::tuple<int, int, uint32_t>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, uint32_t>, int64_t> graph_launches;
@@ -351,39 +337,13 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.counters = c->gv_cnt;
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = epi;
-    if (g == 0 && c->xn_pending) {   // RMSNorm folded into this qkv GEMV (see GemvParams::xnorm)
-      p.xnorm = 1;
-      p.xn_x = c->x;
-      p.xn_ldx = c->H;
-      p.xn_ss = c->sumsq;
-      p.xn_ss_ld = p.NT * 8;
-      p.xn_ss_tiles = c->H / 128;
-      p.xn_gain = w.attn_norm;
-      p.xn_eps = c->cfg.rms_eps;
-      p.xn_M = M;
-      c->xn_pending = false;
-    }
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
-    static const int pre_after = getenv("SS_GEMV_PRE_AFTER") ? atoi(getenv("SS_GEMV_PRE_AFTER")) : 0;
-    p.pre_after = (pre_after >> g) & 1;   // bit g: group g issues its first stages after the wait
-    static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
-    p.self_pf = (self_pf >> g) & 1;        // bit g: group g prefetches its own range into L2
     // qkv substitutes: plan one CTA per SM.  Its whole per-CTA weight range (9.3 MB / 144 CTAs =
     // 64 KB at Qwen-7B) then sits in the ring before the grid-dependency wait, and the CTAs find
     // free slots next to the previous layer's down GEMV (2 CTAs on ~84 SMs), so they are resident
     // and prefetched early (measured: pass 2082 -> 2013 us; o and down are slower at 1 CTA/SM).
     p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
     p.qbits = c->sub_bits;
-    static const int pf_down = getenv("SS_PF_DOWN") ? atoi(getenv("SS_PF_DOWN")) : 0;
-    if (pf_down && g == 0 && !w.resident && !c->lw[l].resident) {
-      // L2 prefetch of this layer's down substitute while qkv, attention and o (latency-bound, HBM
-      // mostly idle) run, issued after the dependency wait so it does not compete with the previous
-      // down's stream (SS_PF_DOWN=2: only the first half of the matrix, tiles 0..13)
-      p.pf = w.q4[3];
-      p.pf_bytes = int64_t(sub_bytes(c->gN[3], c->gK[3], c->sub_bits));
-      if (pf_down == 2) p.pf_bytes /= 2;
-      p.pf_late = 1;
-    }
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
     launch_gemv(!w.resident, p, c->gv_grid, c->use_pdl, c->cs);
@@ -437,7 +397,6 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
   const int NT = target ? gemm_nt(M) : gemv_nt(M);
   const float eps = c->cfg.rms_eps;
   ss_status s;
-  c->xn_pending = false;
   launch_embed_rmsnorm(c->tok, node_base, M, c->embed, c->x, c->H, c->lw[0].attn_norm, eps, c->hfrag, c->hxs, NT,
                        c->use_pdl, c->cs, c->cur_rq);
   c->launches++;
@@ -469,19 +428,12 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     a.n_heads = c->nh;
     a.n_kv = c->nkv;
     a.head_dim = c->d;
-    a.split = c->attn_v2 ? 0 : (target ? c->split_target : c->split_draft);
-    a.n_seg_max = c->at_seg_max;
-    a.part_o = c->at_o;
-    a.part_ml = c->at_ml;
-    a.counters = c->at_cnt;
     a.out_fragx = c->attnfrag;
     a.out_xs = c->attnxs;
     a.out_nt = NT;
-    // logical keys of a node: P + depth + 1 <= max_context.  The draft loop is replayed from a CUDA
-    // graph while P grows, so its grid is sized for max_context.
-    if (g_trace && g_trace_n < g_trace_cap && c->attn_v2) a.trace = g_trace + kTraceEvents * (g_trace_n++);
-    if (!(g_skip & SKIP_ATTN)) launch_attention(a, (target && c->B == 1) ? std::min(c->C, c->P + M) : c->C, c->use_pdl, c->cs);
-    c->launches += c->attn_v2 ? 1 : 2;
+    if (g_trace && g_trace_n < g_trace_cap) a.trace = g_trace + kTraceEvents * (g_trace_n++);
+    if (!(g_skip & SKIP_ATTN)) launch_attention(a, c->use_pdl, c->cs);
+    c->launches++;
     if ((s = check_launch(c, "attention")) != SS_OK) return s;
     const bool fnorm = !target && c->fuse_norm && !(g_skip & SKIP_NORM) &&
                        gemv_tiles_all_resident(true, NT, c->gN[1], c->gK[1], c->gv_grid, c->sub_bits) &&
@@ -518,58 +470,12 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     e.act_xs = c->actxs;
     e.act_nt = NT;
     const uint16_t* nextg = (l + 1 < c->L) ? c->lw[l + 1].attn_norm : c->final_norm;
-    const int mgrid = (!target && c->fuse_mlp && !(g_skip & SKIP_GEMV)) ? mlp_grid(!c->lw[l].resident, NT, c->gv_grid) : 0;
-    if (mgrid > 0) {
-      // gate_up + down in one persistent launch (mlp.cu)
-      MlpParams mp{};
-      const LayerW& w = c->lw[l];
-      mp.Wgu = w.resident ? w.bf16[2] : w.q4[2];
-      mp.Wd = w.resident ? w.bf16[3] : w.q4[3];
-      mp.Xh = c->hfrag;
-      mp.XSh = c->hxs;
-      mp.Xa = c->actfrag;
-      mp.XSa = c->actxs;
-      mp.H = c->H;
-      mp.F = c->F;
-      mp.NT = NT;
-      mp.partials = c->gv_part;
-      mp.counters = c->gv_cnt;
-      mp.max_seg = gemv_max_segments(c->H, c->F, mgrid);
-      mp.flags = c->mlp_flags;
-      mp.exit_ctr = c->mlp_flags + 32 * (2 * c->F / 128);
-      mp.epi_gu = e;
-      static const int mlp_dbg = getenv("SS_MLP_DBG") ? atoi(getenv("SS_MLP_DBG")) : 0;
-      mp.dbg = mlp_dbg;
-      EpiParams d = base_epi(c, M);
-      d.kind = EPI_RESID;
-      if (fnorm) d = resid_norm(nextg, 2);
-      mp.epi_d = d;
-      if (g_trace && g_trace_n < g_trace_cap) mp.trace = g_trace + kTraceEvents * (g_trace_n++);
-      launch_mlp(!w.resident, mp, mgrid, c->use_pdl, c->cs);
-      c->launches++;
-      if ((s = check_launch(c, "mlp")) != SS_OK) return s;
-      if (mlp_dbg & 2) {   // debug: phase A only, down through the GEMV kernel
-        EpiParams d2 = base_epi(c, M);
-        d2.kind = EPI_RESID;
-        if (fnorm) d2 = resid_norm(nextg, 1);
-        if ((s = matmul(c, target, l, 3, c->actfrag, M, d2)) != SS_OK) return s;
-      }
-    } else {
-      if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
-      e = base_epi(c, M);
-      e.kind = EPI_RESID;
-      if (fnorm) e = resid_norm(nextg, 1);
-      // the next layer's qkv normalises its own K range: down only adds the residual and publishes
-      // per-tile sums of squares (no barrier, no normalise pass)
-      const bool xn = fnorm && c->xnorm && NT == 1 && l + 1 < c->L;
-      if (xn) {
-        e.kind = EPI_RESID_SS;
-        c->xn_pending = true;
-      }
-      if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
-    }
+    if ((s = matmul(c, target, l, 2, c->hfrag, M, e)) != SS_OK) return s;
+    e = base_epi(c, M);
+    e.kind = EPI_RESID;
+    if (fnorm) e = resid_norm(nextg, 1);
+    if ((s = matmul(c, target, l, 3, c->actfrag, M, e)) != SS_OK) return s;
     if (fnorm) {
-    } else if (c->xn_pending) {
     } else if ((!target || out.argmax) && !(g_skip & SKIP_NORM)) {
       launch_rmsnorm(c->x, M, c->H, nextg, eps, c->hfrag, c->hxs, NT, c->use_pdl, c->cs);
       c->launches++;
@@ -673,94 +579,6 @@ ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
   return SS_OK;
 }
 
-// one launch of the persistent draft pass over frontier nodes [base, base + M)
-ss_status launch_fused_pass(ss_ctx* c, int M, int base, int child_base, int child_depth, int k, float T, int skip_topk,
-                            unsigned long long* trace) {
-  ss_status s;
-  PassParams p{};
-  p.ph = c->d_phases;
-  p.n_ph = int(c->phases.size());
-  p.M = M;
-  p.NT = gemv_nt_pow2(M);
-  p.node_base = base;
-  p.H = c->H;
-  p.eps = c->cfg.rms_eps;
-  p.x = c->x;
-  p.sumsq = c->sumsq;
-  p.tok = c->tok;
-  p.embed = c->embed;
-  p.partials = c->pass_part;
-  p.tile_ctr = c->gv_cnt;
-  p.max_seg = 1;
-  for (const auto& ph : c->phases)
-    if (ph.kind == PH_GEMV) p.max_seg = std::max(p.max_seg, pass_max_segments(ph.N, ph.K, c->pass_grid));
-  p.bar = c->pass_bar;
-  p.stages = c->pass_stages;
-  AttnParams& a = p.attn;
-  a.q = c->qbuf;
-  a.k_cache = c->kc;
-  a.v_cache = c->vc;
-  a.k_tree = c->kt;
-  a.v_tree = c->vt;
-  a.committed_len = c->committed_len;
-  a.anc = c->anc;
-  a.depth = c->depth;
-  a.anc_stride = c->anc_stride;
-  a.max_ctx = c->kv_ctx;
-  a.max_nodes = c->kv_nodes;
-  a.n_heads = c->nh;
-  a.n_kv = c->nkv;
-  a.head_dim = c->d;
-  a.split = c->split_draft;
-  a.n_seg_max = c->at_seg_max;
-  a.part_o = c->at_o;
-  a.part_ml = c->at_ml;
-  a.out_fragx = c->attnfrag;
-  a.out_xs = c->attnxs;
-  p.kc_layer = c->kc_layer;
-  p.kt_layer = c->kt_layer;
-  p.attn_ctr = c->attn_ctr;
-  TopkParams& t = p.topk;
-  t.logits = c->logits;
-  t.M = M;
-  t.V = c->V;
-  t.k = k;
-  t.inv_t = float(1.0 / double(T));
-  t.blocks_per_row = std::max(1, std::min(64, c->pass_grid / M));
-  t.blk_max = c->tk_max;
-  t.blk_sum = c->tk_sum;
-  t.blk_val = c->tk_val;
-  t.blk_idx = c->tk_idx;
-  t.tok = c->tok;
-  t.parent = c->parent;
-  t.depth = c->depth;
-  t.score = c->score;
-  t.anc = c->anc;
-  t.anc_stride = c->anc_stride;
-  t.node_base = base;
-  t.child_base = child_base;
-  t.child_depth = child_depth;
-  p.trace = trace;
-  p.skip_topk = skip_topk;
-  CK(cudaMemsetAsync(c->pass_bar, 0, 4, c->cs));
-  launch_draft_pass(p, c->pass_grid, c->d, c->cs);
-  c->launches++;
-  return check_launch(c, "draft_pass");
-}
-
-ss_status draft_loop_fused(ss_ctx* c, int D, int k, float T) {
-  ss_status s;
-  launch_tree_init(c->root_tok, c->tok, c->parent, c->depth, c->score, c->anc, false, c->cs);
-  c->launches++;
-  if ((s = check_launch(c, "tree_init")) != SS_OK) return s;
-  for (int dd = 0; dd < D; ++dd) {
-    const int M = dd == 0 ? 1 : k;
-    const int base = dd == 0 ? 0 : 1 + (dd - 1) * k;
-    if ((s = launch_fused_pass(c, M, base, 1 + dd * k, dd + 1, k, T, 0, nullptr)) != SS_OK) return s;
-  }
-  return SS_OK;
-}
-
 ss_status run_draft(ss_ctx* c, int D, int k, float T) {
   uint32_t tb;
   std::memcpy(&tb, &T, 4);
@@ -770,14 +588,14 @@ ss_status run_draft(ss_ctx* c, int D, int k, float T) {
     if (it == c->graphs.end()) {
       // first use: run eagerly (sets kernel attributes), then capture for later steps
       const int64_t l0 = c->launches;
-      ss_status s = c->use_fused ? draft_loop_fused(c, D, k, T) : draft_loop(c, D, k, T);
+      ss_status s = draft_loop(c, D, k, T);
       if (s != SS_OK) return s;
       const int64_t nl = c->launches - l0;
       cudaGraph_t g = nullptr;
       if (cudaStreamBeginCapture(c->cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
         c->capturing = true;
         const int64_t lsave = c->launches;
-        ss_status s2 = c->use_fused ? draft_loop_fused(c, D, k, T) : draft_loop(c, D, k, T);
+        ss_status s2 = draft_loop(c, D, k, T);
         c->launches = lsave;
         c->capturing = false;
         cudaError_t e = cudaStreamEndCapture(c->cs, &g);
@@ -802,7 +620,7 @@ ss_status run_draft(ss_ctx* c, int D, int k, float T) {
     c->launches += c->graph_launches[key];
     return SS_OK;
   }
-  return c->use_fused ? draft_loop_fused(c, D, k, T) : draft_loop(c, D, k, T);
+  return draft_loop(c, D, k, T);
 }
 
 ss_status do_verify(ss_ctx* c) {
@@ -883,6 +701,7 @@ bool valid_cfg(const ss_model_config* m, const ss_limits* l) {
   if ((m->n_heads * m->head_dim) % 128) return false;
   if (m->max_context < 2 || m->max_context > 8192) return false;
   if (m->n_heads / m->n_kv_heads > 16) return false;
+  if (m->precision != SS_BF16 && m->precision != SS_FP32) return false;
   if (l->max_depth < 0 || l->max_top_k < 1 || l->max_top_k > 32 || l->max_chunk < 1 || l->max_chunk > 1024) return false;
   // batched slots: a draft pass forwards max_batch * k <= 32 frontier rows (GEMV token tiles)
   if (l->max_batch < 0 || l->max_batch > 32 || (l->max_batch > 1 && l->max_batch * l->max_top_k > 32)) return false;
@@ -901,13 +720,26 @@ bool valid_cfg(const ss_model_config* m, const ss_limits* l) {
 // ================================== C-ABI ===================================================
 extern "C" {
 
-ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device, void* dev_arena, size_t arena_bytes,
-                    void* compute_stream, void* copy_stream, ss_ctx** out) {
+void ss_default_options(ss_options* o) {
+  if (!o) return;
+  o->embed_on_host = 1;
+  o->async_stream = 1;
+  o->cuda_graphs = 1;
+  o->fuse_norm = 1;
+}
+
+ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_options* opt, int device, void* dev_arena,
+                    size_t arena_bytes, void* compute_stream, void* copy_stream, ss_ctx** out) {
   if (!out || !valid_cfg(cfg, lim) || !dev_arena) return SS_ERR_INVALID;
   *out = nullptr;
   ss_ctx* c = new ss_ctx();
   c->cfg = *cfg;
   c->lim = *lim;
+  ss_default_options(&c->opt);
+  if (opt) c->opt = *opt;
+  c->serial_stream = !c->opt.async_stream;
+  c->use_graphs = c->opt.cuda_graphs != 0;
+  c->fuse_norm = c->opt.fuse_norm != 0;
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete c;
@@ -950,12 +782,12 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   auto A = [&](size_t bytes) { return a.alloc(bytes); };
   bool ok = true;
   auto chk = [&](void* p) { ok = ok && p != nullptr; return p; };
-  // The embedding is only ever gathered (<= max_nodes rows per pass): keep it in mapped, portable
-  // pinned host memory and read rows over PCIe (zero-copy), which leaves its 2*V*H bytes of the VRAM
-  // cap to the streaming ring.  SS_EMBED_HOST=0 keeps it in the arena (P:534 default placement).
+  // The embedding is only ever gathered (<= max_nodes rows per pass).  opt.embed_on_host = 1 keeps it
+  // in mapped, portable pinned host memory and reads rows over the host link (zero-copy), which
+  // leaves its 2*V*H bytes of the VRAM cap to the streaming ring (reading R24); 0 keeps it
+  // in the arena, PAPER.md:534's GPU-resident placement.
   {
-    const char* ev = getenv("SS_EMBED_HOST");
-    if (!(ev && ev[0] == '0') &&
+    if (c->opt.embed_on_host &&
         cudaHostAlloc(&c->h_embed, size_t(c->V) * c->H * 2, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
       void* dptr = nullptr;
       cudaHostGetDevicePointer(&dptr, c->h_embed, 0);
@@ -1000,10 +832,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
   c->logits = (float*)chk(A(size_t(32) * c->V * 4));
   c->tracebuf = (unsigned long long*)chk(A(size_t(512) * kTraceEvents * 8));
   c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
-  c->pass_bar = (unsigned*)chk(A(256));
-  c->attn_ctr = (int*)chk(A(size_t(32) * c->nkv * 4));
   c->norm_ctr = (unsigned long long*)chk(A(256));   // 24 monotonic counters (3 x 2 formats x NT 1..4), zeroed below
-  c->mlp_flags = (int*)chk(A(size_t(2 * c->F / 128 + 1) * 32 * 4));
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32
   size_t gvf = 0;
@@ -1013,26 +842,16 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, int device
     gvf = std::max(gvf, size_t(N / 128) * gemv_max_segments(N, K, c->gv_grid) * 128 * 32);
     max_tiles = std::max(max_tiles, N / 128);
   }
-  // the fused MLP's down phase runs Stream-K over up to 2 CTAs per SM
-  gvf = std::max(gvf, size_t(c->H / 128) * gemv_max_segments(c->H, c->F, 2 * c->gv_grid) * 128 * 32);
   c->gv_part_floats = gvf;
   c->gv_part = (float*)chk(A(gvf * 4));
   c->gv_cnt = (int*)chk(A(size_t(max_tiles) * 4));
-  c->at_seg_max = (c->C + std::min(c->split_draft, c->split_target) - 1) / std::min(c->split_draft, c->split_target);
   {
-    // split-attention partials are only needed by the legacy two-kernel attention (SS_ATTN_V2=0)
-    // and the fused pass; otherwise the buffer is just the debug-matmul output scratch
-    const char* av = getenv("SS_ATTN_V2");
-    const char* fv = getenv("SS_FUSED_DRAFT");
-    const bool legacy = (av && av[0] == '0') || (fv && fv[0] == '1');
-    const size_t mpad_one = size_t(std::max(32, ((c->max_nodes + 127) / 128) * 128));   // one request's rows
-    size_t need = std::max(mpad_one * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
-    if (legacy) need = std::max(need, size_t(c->max_nodes) * c->nh * c->at_seg_max * c->d);
-    c->at_o_floats = need;
-    c->at_o = (float*)chk(A(need * 4));
+    // debug output scratch of ss_debug_matmul / ss_debug_time_matmul: one request's rows x the widest
+    // matrix group, or 32 rows of logits
+    const size_t mpad_one = size_t(std::max(32, ((c->max_nodes + 127) / 128) * 128));
+    c->at_o_floats = std::max(mpad_one * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
+    c->at_o = (float*)chk(A(c->at_o_floats * 4));
   }
-  c->at_ml = (float*)chk(A(size_t(c->max_nodes) * c->nh * c->at_seg_max * 2 * 4));
-  c->at_cnt = (int*)chk(A(size_t(c->nkv) * ((c->max_nodes + 7) / 8) * 4));
   c->tk_max = (float*)chk(A(size_t(32) * 296 * 4));
   c->tk_sum = (float*)chk(A(size_t(32) * 296 * 4));
   c->tk_val = (float*)chk(A(size_t(32) * 296 * 32 * 4));
@@ -1126,86 +945,8 @@ ss_status ss_host_store_bytes(ss_ctx* c, int32_t n_resident, size_t* out) {
   return SS_OK;
 }
 
-static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* ext_host, size_t ext_bytes, bool fill);
-
-ss_status ss_set_substitute_bits(ss_ctx* c, int32_t bits) {
-  GUARD(c);
-  if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "set_substitute_bits: only before load_weights");
-  if (bits != 4 && bits != 2) return fail(c, SS_ERR_INVALID, "set_substitute_bits: 4 or 2");
-  c->sub_bits = bits;
-  return SS_OK;
-}
-
-ss_status ss_load_weights(ss_ctx* c, uint64_t seed, int32_t n_resident) {
-  GUARD(c);
-  return load_impl(c, seed, n_resident, nullptr, 0, true);
-}
-
-ss_status ss_load_weights_shared(ss_ctx* c, uint64_t seed, int32_t n_resident, void* host_store, size_t host_bytes,
-                                 int32_t fill) {
-  GUARD(c);
-  if (!host_store || n_resident < 0) return fail(c, SS_ERR_INVALID, "load_weights_shared: store and n_resident >= 0");
-  return load_impl(c, seed, n_resident, host_store, host_bytes, fill != 0);
-}
-
-static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* ext_host, size_t ext_bytes, bool fill) {
-  if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "load_weights: already loaded");
-  c->seed = seed;
-  const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
-  const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += sub_bytes(c->gN[g], c->gK[g], c->sub_bits); return s; }();
-  size_t max_group = 0;
-  for (int g = 0; g < 4; ++g) max_group = std::max(max_group, bf16_bytes(c->gN[g], c->gK[g]));
-  const size_t avail = c->ar.cap - c->ar.used - 4096 * 8;
-  auto need = [&](int nr) {
-    const int off = c->L - nr;
-    return size_t(nr) * layer_bf16 + size_t(off) * layer_q4 + (off > 0 ? 2 * max_group : max_group);
-  };
-  int nr = n_resident;
-  if (nr < 0) {
-    nr = 0;
-    while (nr < c->L && need(nr + 1) <= avail) ++nr;
-  }
-  if (nr > c->L) return fail(c, SS_ERR_INVALID, "n_resident > n_layers");
-  if (need(nr) > avail) return fail(c, SS_ERR_BUDGET, "arena below the minimum footprint for this placement");
-  c->n_resident = nr;
-  for (int l = 0; l < c->L; ++l) {
-    LayerW& w = c->lw[l];
-    w.resident = l < nr;
-    for (int g = 0; g < 4; ++g) {
-      if (w.resident)
-        w.bf16[g] = (uint8_t*)c->ar.alloc(bf16_bytes(c->gN[g], c->gK[g]), 1024);
-      else
-        w.q4[g] = (uint8_t*)c->ar.alloc(sub_bytes(c->gN[g], c->gK[g], c->sub_bits), 1024);
-    }
-  }
-  // the staging ring takes what is left after the fused-pass tables (reserved here, see below)
-  // the phase table of the persistent pass (~100 KB) always; its Stream-K partials only when the
-  // opt-in fused pass is requested — otherwise that VRAM belongs to the streaming ring
-  const char* fdv = getenv("SS_FUSED_DRAFT");
-  const size_t pass_reserve = (fdv && fdv[0] == '1') ? (size_t(64) << 20) : (size_t(1) << 20);
-  c->ring_bytes = (c->ar.cap - c->ar.used - pass_reserve - 4096) / 4096 * 4096;
-  c->ring = (uint8_t*)c->ar.alloc(c->ring_bytes, 4096);
-  if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
-  // pinned host store for offloaded layers (device layout)
-  c->host_bytes = size_t(c->L - nr) * layer_bf16;
-  if (ext_host) {
-    if (ext_bytes < c->host_bytes) return fail(c, SS_ERR_BUDGET, "shared host store smaller than ss_host_store_bytes");
-    if (c->host_bytes && !host_register(ext_host, c->host_bytes))
-      return fail(c, SS_ERR_CUDA, "cudaHostRegister of the shared host store failed");
-    c->host = reinterpret_cast<uint8_t*>(ext_host);
-    c->host_external = true;
-  }
-  if (c->host_bytes) {
-    if (!c->host_external && cudaHostAlloc(&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess)
-      return fail(c, SS_ERR_CUDA, "cudaHostAlloc of the pinned host store failed");
-    size_t off = 0;
-    for (int l = nr; l < c->L; ++l)
-      for (int g = 0; g < 4; ++g) {
-        c->lw[l].host_off[g] = off;
-        off += bf16_bytes(c->gN[g], c->gK[g]);
-      }
-  }
-  // generation (tensor ids: SURVEY O.1 / synth/weights.py)
+// Synthetic weights (SURVEY O.1 generator; tensor ids as synth/weights.py), generated on the device.
+static ss_status fill_synthetic(ss_ctx* c, uint64_t seed, bool fill) {
   const double H = c->H;
   if (c->h_embed) {   // generate on the device (ring scratch), then place in the host copy
     // in ring-sized pieces (a planner-max placement leaves a ring of only two matrix groups)
@@ -1254,6 +995,161 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
       }
     }
   }
+  return SS_OK;
+}
+
+static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, int32_t n_resident, void* ext_host,
+                           size_t ext_bytes, bool fill);
+
+ss_status ss_set_substitute_bits(ss_ctx* c, int32_t bits) {
+  GUARD(c);
+  if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "set_substitute_bits: only before load_weights");
+  if (bits != 4 && bits != 2) return fail(c, SS_ERR_INVALID, "set_substitute_bits: 4 or 2");
+  c->sub_bits = bits;
+  return SS_OK;
+}
+
+ss_status ss_load_weights(ss_ctx* c, const ss_host_weights* w, int32_t n_resident) {
+  GUARD(c);
+  if (!w || !w->embed || !w->layers || !w->final_norm || !w->head) return fail(c, SS_ERR_INVALID, "load_weights: NULL tensor");
+  for (int l = 0; l < c->L; ++l) {
+    const ss_host_layer& h = w->layers[l];
+    if (!h.attn_norm || !h.wq || !h.wk || !h.wv || !h.wo || !h.mlp_norm || !h.wg || !h.wu || !h.wd)
+      return fail(c, SS_ERR_INVALID, "load_weights: NULL layer tensor");
+    const bool b = h.bq && h.bk && h.bv, any = h.bq || h.bk || h.bv;
+    if (c->cfg.qkv_bias ? !b : any) return fail(c, SS_ERR_INVALID, "load_weights: biases must match cfg.qkv_bias");
+  }
+  return load_impl(c, w, 0, n_resident, nullptr, 0, true);
+}
+
+ss_status ss_load_weights_synthetic(ss_ctx* c, uint64_t seed, int32_t n_resident) {
+  GUARD(c);
+  return load_impl(c, nullptr, seed, n_resident, nullptr, 0, true);
+}
+
+ss_status ss_load_weights_synthetic_shared(ss_ctx* c, uint64_t seed, int32_t n_resident, void* host_store,
+                                           size_t host_bytes, int32_t fill) {
+  GUARD(c);
+  if (!host_store || n_resident < 0) return fail(c, SS_ERR_INVALID, "load_weights_shared: store and n_resident >= 0");
+  return load_impl(c, nullptr, seed, n_resident, host_store, host_bytes, fill != 0);
+}
+
+// Place one matrix group (layer l, group g) from the caller's natural row-major host arrays: each
+// source matrix is copied to the device (staging) and tiled into dst (resident buffer or ring).
+static ss_status fill_group_from_host(ss_ctx* c, const ss_host_layer& h, int g, uint8_t* dst, uint16_t* staging) {
+  const int K = c->gK[g];
+  struct Piece { const uint16_t* src; int64_t rows; int map; int64_t row_off; };
+  std::vector<Piece> pieces;
+  if (g == 0) pieces = {{h.wq, c->qd, 0, 0}, {h.wk, c->kvd, 0, c->qd}, {h.wv, c->kvd, 0, c->qd + c->kvd}};
+  else if (g == 1) pieces = {{h.wo, c->H, 0, 0}};
+  else if (g == 2) pieces = {{h.wg, c->F, 1, 0}, {h.wu, c->F, 2, 0}};
+  else pieces = {{h.wd, c->H, 0, 0}};
+  for (const Piece& p : pieces) {
+    CK(cudaMemcpyAsync(staging, p.src, size_t(p.rows) * K * 2, cudaMemcpyHostToDevice, c->cs));
+    launch_tile_from_natural(dst, staging, p.rows, K, p.map, p.row_off, c->cs);
+    CK(cudaStreamSynchronize(c->cs));   // the staging buffer is reused by the next piece
+  }
+  return check_launch(c, "tile_from_natural");
+}
+
+static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, int32_t n_resident, void* ext_host,
+                           size_t ext_bytes, bool fill) {
+  if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "load_weights: already loaded");
+  c->seed = seed;
+  const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
+  const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += sub_bytes(c->gN[g], c->gK[g], c->sub_bits); return s; }();
+  size_t max_group = 0;
+  for (int g = 0; g < 4; ++g) max_group = std::max(max_group, bf16_bytes(c->gN[g], c->gK[g]));
+  const size_t avail = c->ar.cap - c->ar.used - 4096 * 8;
+  auto need = [&](int nr) {
+    const int off = c->L - nr;
+    return size_t(nr) * layer_bf16 + size_t(off) * layer_q4 + (off > 0 ? 2 * max_group : max_group);
+  };
+  int nr = n_resident;
+  if (nr < 0) {
+    nr = 0;
+    while (nr < c->L && need(nr + 1) <= avail) ++nr;
+  }
+  if (nr > c->L) return fail(c, SS_ERR_INVALID, "n_resident > n_layers");
+  if (need(nr) > avail) return fail(c, SS_ERR_BUDGET, "arena below the minimum footprint for this placement");
+  c->n_resident = nr;
+  for (int l = 0; l < c->L; ++l) {
+    LayerW& w = c->lw[l];
+    w.resident = l < nr;
+    for (int g = 0; g < 4; ++g) {
+      if (w.resident)
+        w.bf16[g] = (uint8_t*)c->ar.alloc(bf16_bytes(c->gN[g], c->gK[g]), 1024);
+      else
+        w.q4[g] = (uint8_t*)c->ar.alloc(sub_bytes(c->gN[g], c->gK[g], c->sub_bits), 1024);
+    }
+  }
+  // the staging ring takes what is left
+  c->ring_bytes = (c->ar.cap - c->ar.used - 4096) / 4096 * 4096;
+  c->ring = (uint8_t*)c->ar.alloc(c->ring_bytes, 4096);
+  if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
+  // pinned host store for offloaded layers (device layout)
+  c->host_bytes = size_t(c->L - nr) * layer_bf16;
+  if (ext_host) {
+    if (ext_bytes < c->host_bytes) return fail(c, SS_ERR_BUDGET, "shared host store smaller than ss_host_store_bytes");
+    if (c->host_bytes && !host_register(ext_host, c->host_bytes))
+      return fail(c, SS_ERR_CUDA, "cudaHostRegister of the shared host store failed");
+    c->host = reinterpret_cast<uint8_t*>(ext_host);
+    c->host_external = true;
+  }
+  if (c->host_bytes) {
+    if (!c->host_external && cudaHostAlloc(&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess)
+      return fail(c, SS_ERR_CUDA, "cudaHostAlloc of the pinned host store failed");
+    size_t off = 0;
+    for (int l = nr; l < c->L; ++l)
+      for (int g = 0; g < 4; ++g) {
+        c->lw[l].host_off[g] = off;
+        off += bf16_bytes(c->gN[g], c->gK[g]);
+      }
+  }
+  if (hw) {
+    // caller weights: norms/biases/embedding copied as they are, matrices tiled on the device through
+    // the ring (second half = natural staging, first half = tiled group when the layer is offloaded)
+    const size_t E = size_t(c->V) * c->H * 2;
+    if (c->h_embed) std::memcpy(c->h_embed, hw->embed, E);
+    else CK(cudaMemcpyAsync(c->embed, hw->embed, E, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaMemcpyAsync(c->final_norm, hw->final_norm, size_t(c->H) * 2, cudaMemcpyHostToDevice, c->cs));
+    uint16_t* staging = reinterpret_cast<uint16_t*>(c->ring + (c->ring_bytes >= 2 * max_group ? max_group : 0));
+    if (c->ring_bytes < 2 * max_group && c->n_resident < c->L)
+      return fail(c, SS_ERR_BUDGET, "load_weights: ring below two matrix groups");
+    {   // head [V x H]: tiled in ring-sized row blocks
+      const int64_t rows_per = std::max<int64_t>(128, int64_t(c->ring_bytes / (size_t(c->H) * 2)) / 128 * 128);
+      for (int64_t r0 = 0; r0 < c->V; r0 += rows_per) {
+        const int64_t n = std::min<int64_t>(rows_per, c->V - r0);
+        uint16_t* st16 = reinterpret_cast<uint16_t*>(c->ring);
+        CK(cudaMemcpyAsync(st16, hw->head + r0 * c->H, size_t(n) * c->H * 2, cudaMemcpyHostToDevice, c->cs));
+        launch_tile_from_natural(c->head, st16, n, c->H, 0, r0, c->cs);
+        CK(cudaStreamSynchronize(c->cs));
+      }
+    }
+    for (int l = 0; l < c->L; ++l) {
+      LayerW& w = c->lw[l];
+      const ss_host_layer& h = hw->layers[l];
+      CK(cudaMemcpyAsync(w.attn_norm, h.attn_norm, size_t(c->H) * 2, cudaMemcpyHostToDevice, c->cs));
+      CK(cudaMemcpyAsync(w.mlp_norm, h.mlp_norm, size_t(c->H) * 2, cudaMemcpyHostToDevice, c->cs));
+      if (w.bias) {
+        CK(cudaMemcpyAsync(w.bias, h.bq, size_t(c->qd) * 2, cudaMemcpyHostToDevice, c->cs));
+        CK(cudaMemcpyAsync(w.bias + c->qd, h.bk, size_t(c->kvd) * 2, cudaMemcpyHostToDevice, c->cs));
+        CK(cudaMemcpyAsync(w.bias + c->qd + c->kvd, h.bv, size_t(c->kvd) * 2, cudaMemcpyHostToDevice, c->cs));
+      }
+      for (int g = 0; g < 4; ++g) {
+        uint8_t* dst = w.resident ? w.bf16[g] : c->ring;
+        ss_status s = fill_group_from_host(c, h, g, dst, w.resident ? reinterpret_cast<uint16_t*>(c->ring) : staging);
+        if (s != SS_OK) return s;
+        if (!w.resident) {
+          CK(cudaMemcpyAsync(c->host + w.host_off[g], c->ring, bf16_bytes(c->gN[g], c->gK[g]), cudaMemcpyDeviceToHost, c->cs));
+          CK(cudaStreamSynchronize(c->cs));
+        }
+      }
+    }
+  } else {
+    ss_status s = fill_synthetic(c, seed, fill);
+    if (s != SS_OK) return s;
+  }
   CK(cudaStreamSynchronize(c->cs));
   ss_status s = check_launch(c, "load_weights");
   if (s != SS_OK) return s;
@@ -1274,119 +1170,6 @@ static ss_status load_impl(ss_ctx* c, uint64_t seed, int32_t n_resident, void* e
     c->ev_t1.push_back(t1);
   }
   c->ev_pending.assign(c->ev_pool, false);
-  // ---- fused draft pass: phase table, Stream-K partial buffer, launch geometry ----
-  {
-    const char* ev = getenv("SS_FUSED_DRAFT");
-    c->use_fused = ev && ev[0] == '1';
-    const char* pv = getenv("SS_L2_PREFETCH");
-    c->l2_prefetch = pv && pv[0] == '1';
-    const char* fv = getenv("SS_FUSE_NORM");
-    c->fuse_norm = !(fv && fv[0] == '0');
-    const char* mv = getenv("SS_FUSE_MLP");   // opt-in: measured slower than the two GEMVs
-    c->fuse_mlp = mv && mv[0] == '1';
-    const char* sv = getenv("SS_STREAM_SERIAL");
-    c->serial_stream = sv && sv[0] == '1';
-    const char* xv = getenv("SS_XNORM");   // opt-in: measured slower
-    c->xnorm = xv && xv[0] == '1';
-    const char* gv = getenv("SS_GRAPHS");
-    if (gv && gv[0] == '0') c->use_graphs = false;
-    const char* av = getenv("SS_ATTN_V2");
-    c->attn_v2 = !(av && av[0] == '0');
-    if (c->sub_bits != 4) c->use_fused = c->fuse_mlp = c->xnorm = false;   // Q4-only opt-in variants
-    c->pass_stages = 5;
-    while (c->pass_stages > 2 && pass_smem_bytes(c->d, c->pass_stages) > 227 * 1024) --c->pass_stages;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    const int maxg = pass_max_grid(c->d, c->pass_stages);
-    c->pass_grid = std::min(sms, maxg);
-    if (c->pass_grid < 1) c->use_fused = false;
-    std::vector<PhaseDesc>& P = c->phases;
-    P.clear();
-    auto base = [&]() {
-      PhaseDesc d{};
-      d.epi = base_epi(c, 1);
-      return d;
-    };
-    PhaseDesc d = base();
-    d.kind = PH_EMBED;
-    P.push_back(d);
-    size_t part_need = 0;
-    auto gemv = [&](const uint8_t* W, int N, int K, bool q4, int xsrc, const uint16_t* gain, const uint16_t* X,
-                    const float* XS, EpiParams epi) {
-      PhaseDesc g = base();
-      g.kind = PH_GEMV;
-      g.W = W;
-      g.N = N;
-      g.K = K;
-      g.q4 = q4 ? 1 : 0;
-      g.xsrc = xsrc;
-      g.gain = gain;
-      g.X = X;
-      g.XSUM = XS;
-      g.epi = epi;
-      P.push_back(g);
-      part_need = std::max(part_need, size_t(N / 128) * pass_max_segments(N, K, c->pass_grid));
-    };
-    for (int l = 0; l < c->L; ++l) {
-      const LayerW& w = c->lw[l];
-      auto Wg = [&](int g) { return (const uint8_t*)(w.resident ? w.bf16[g] : w.q4[g]); };
-      EpiParams q = base_epi(c, 1);
-      q.kind = EPI_QKV;
-      q.bias = w.bias;
-      q.q_out = c->qbuf;
-      q.k_tree = c->kt + l * c->kt_layer;
-      q.v_tree = c->vt + l * c->kt_layer;
-      PhaseDesc nm = base();
-      nm.kind = PH_NORM;
-      nm.gain = w.attn_norm;
-      nm.X = c->hfrag;
-      nm.XSUM = c->hxs;
-      P.push_back(nm);
-      gemv(Wg(0), c->gN[0], c->gK[0], !w.resident, XS_FRAGX, nullptr, c->hfrag, c->hxs, q);
-      PhaseDesc a = base();
-      a.kind = PH_ATTN;
-      a.layer = l;
-      P.push_back(a);
-      a.kind = PH_COMBINE;
-      P.push_back(a);
-      EpiParams r = base_epi(c, 1);
-      r.kind = EPI_RESID_SS;
-      r.sumsq = c->sumsq;   // sumsq_ld = 0: the pass kernel's tile stride (Mpad)
-      gemv(Wg(1), c->gN[1], c->gK[1], !w.resident, XS_FRAGX, nullptr, c->attnfrag, c->attnxs, r);
-      EpiParams u = base_epi(c, 1);
-      u.kind = EPI_SILU;
-      u.act = c->actfrag;
-      u.act_xs = c->actxs;
-      nm.gain = w.mlp_norm;
-      P.push_back(nm);
-      gemv(Wg(2), c->gN[2], c->gK[2], !w.resident, XS_FRAGX, nullptr, c->hfrag, c->hxs, u);
-      gemv(Wg(3), c->gN[3], c->gK[3], !w.resident, XS_FRAGX, nullptr, c->actfrag, c->actxs, r);
-    }
-    EpiParams hd = base_epi(c, 1);
-    hd.kind = EPI_LOGITS;
-    hd.out = c->logits;
-    hd.ldo = c->V;
-    PhaseDesc fn = base();
-    fn.kind = PH_NORM;
-    fn.gain = c->final_norm;
-    fn.X = c->hfrag;
-    fn.XSUM = c->hxs;
-    P.push_back(fn);
-    gemv(c->head, c->V, c->H, false, XS_FRAGX, nullptr, c->hfrag, c->hxs, hd);
-    d = base();
-    d.kind = PH_TOPK1;
-    P.push_back(d);
-    d.kind = PH_TOPK2;
-    P.push_back(d);
-    c->d_phases = (PhaseDesc*)c->ar.alloc(P.size() * sizeof(PhaseDesc));
-    // the persistent pass's Stream-K partials (tens of MB) only when it is enabled: otherwise that
-    // VRAM belongs to the streaming ring
-    c->pass_part = c->use_fused ? (float*)c->ar.alloc(part_need * 128 * 32 * 4) : nullptr;
-    if (!c->d_phases || (c->use_fused && !c->pass_part))
-      return fail(c, SS_ERR_BUDGET, "no room for the fused draft pass tables");
-    CK(cudaMemcpyAsync(c->d_phases, P.data(), P.size() * sizeof(PhaseDesc), cudaMemcpyHostToDevice, c->cs));
-    CK(cudaStreamSynchronize(c->cs));
-  }
   c->st.n_resident = nr;
   c->st.n_offloaded = c->L - nr;
   c->st.host_pinned_bytes = int64_t(c->host_bytes) + (c->h_embed ? int64_t(c->V) * c->H * 2 : 0);
@@ -1475,13 +1258,12 @@ ss_status ss_set_batch(ss_ctx* c, int32_t n_req) {
   GUARD(c);
   if (n_req < 1 || n_req > c->Bmax) return fail(c, SS_ERR_INVALID, "set_batch: n_req outside [1, max_batch]");
   if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "set_batch inside a step");
+  // every check above precedes any state change (a rejected call leaves the session intact)
   if (c->B > 1 || n_req > 1) {
     // a batch session starts over: every active slot is prefilled again
     std::fill(c->slot_ready.begin(), c->slot_ready.end(), 0);
     if (c->state == ST_SESSION) c->state = ST_READY;
   }
-  if (n_req > 1 && (c->use_fused || !c->attn_v2))
-    return fail(c, SS_ERR_INVALID, "batched requests need the default multi-kernel draft pass and K3 v2 attention");
   c->B = n_req;
   return SS_OK;
 }
@@ -1923,8 +1705,6 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.max_seg = gemv_max_segments(N, K, c->gv_grid);
     p.epi = base_epi(c, M);
     p.epi.kind = EPI_STORE;
-    static const int self_pf = getenv("SS_GEMV_SELF_PF") ? atoi(getenv("SS_GEMV_SELF_PF")) : 0;
-    p.self_pf = head ? 0 : (self_pf >> g) & 1;
     p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
     p.qbits = c->sub_bits;
     p.epi.out = c->at_o;
@@ -1969,11 +1749,7 @@ ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, 
   g_skip = skip;
   PassOut o;
   o.logits = true;
-  const bool fused = c->use_fused && skip == 0;
-  auto one = [&]() {
-    return fused ? launch_fused_pass(c, M, 1, 1 + M, 2, std::min(M, c->lim.max_top_k), 0.2f, 0, nullptr)
-                 : forward_pass(c, false, M, 1, o);
-  };
+  auto one = [&]() { return forward_pass(c, false, M, 1, o); };
   ss_status s = one();   // warm-up
   if (s == SS_OK) {
     CK(cudaEventRecord(c->e0, c->cs));
@@ -2010,14 +1786,8 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
   PassOut o;
   o.logits = true;
   int n;
-  if (c->use_fused) {
-    s = launch_fused_pass(c, M, 1, 1 + M, 2, std::min(M, c->lim.max_top_k), 0.2f, 0, buf);
-    n = std::min(cap * E / 2, int(c->phases.size()));   // [phase][start, end] pairs packed E/2 per record
-    n = (2 * n + E - 1) / E;
-  } else {
-    s = forward_pass(c, false, M, 1, o);
-    n = g_trace_n;
-  }
+  s = forward_pass(c, false, M, 1, o);
+  n = g_trace_n;
   g_trace = nullptr;
   if (s != SS_OK) return s;
   CK(cudaMemcpyAsync(init.data(), buf, size_t(n) * E * 8, cudaMemcpyDeviceToHost, c->cs));
@@ -2041,10 +1811,7 @@ ss_status ss_debug_cta_trace(ss_ctx* c, int32_t M, int32_t launch, int64_t* out,
   g_gemv_n = 0;
   PassOut o;
   o.logits = true;
-  const bool fused = c->use_fused;
-  c->use_fused = false;
   s = forward_pass(c, false, M, 1, o);
-  c->use_fused = fused;
   g_cta_trace = nullptr;
   if (s != SS_OK) return s;
   std::vector<unsigned long long> h(n);
@@ -2096,7 +1863,7 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
       if (i1 - i0 > 32) return fail(c, SS_ERR_INVALID, "draft debug forward: <= 32 nodes per depth");
       PassOut o;
       o.logits = true;
-      s = c->use_fused ? launch_fused_pass(c, i1 - i0, i0, 0, 0, 1, 1.0f, 1, nullptr) : forward_pass(c, false, i1 - i0, i0, o);
+      s = forward_pass(c, false, i1 - i0, i0, o);
       if (s != SS_OK) return s;
       CK(cudaMemcpyAsync(out_logits + int64_t(i0) * c->V, c->logits, size_t(i1 - i0) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
       CK(cudaStreamSynchronize(c->cs));

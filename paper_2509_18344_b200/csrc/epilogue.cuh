@@ -156,8 +156,7 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
       }
       break;
     }
-    case EPI_RESID_NORM:
-    case EPI_RESID_SS: {
+    case EPI_RESID_NORM: {
       // x[m, row] += y; then sum over the tile's 128 rows of x_new^2 per token, in a fixed order:
       // a warp covers 32 consecutive rows of one token -> 4 warp sums per token -> scratch -> ordered add
       const int64_t ssld = e.sumsq_ld > 0 ? e.sumsq_ld : ld;
@@ -183,7 +182,6 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
         if (mg < e.M) e.sumsq[int64_t(r) * ssld + mg] = ((scratch[m * 4] + scratch[m * 4 + 1]) + scratch[m * 4 + 2]) + scratch[m * 4 + 3];
       }
       tr(9);
-      if (e.kind != EPI_RESID_NORM) break;
       // ---- fused RMSNorm ----
       // Every caller arrives at a barrier on a monotonic 64-bit counter (release add; never reset).
       // The norm_wait caller of each tile (one CTA per tile, so the waiters are few enough to be

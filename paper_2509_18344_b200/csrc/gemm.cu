@@ -103,10 +103,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(const GemmParams 
 }
 
 void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
+  static unsigned long long init_mask = 0;   // function attributes are per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(init_mask >> (dev & 63) & 1ull)) {
     cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
-    init = true;
+    init_mask |= 1ull << (dev & 63);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.N / 128, (p.NT * 8) / 128);

@@ -10,8 +10,8 @@
 //    previous kernel's tail;
 //  * 8 consumer warps turn 4-bit codes into exact bf16 (128 + code) with ONE lop3 per pair and
 //    feed them straight into mma.m16n8k16 as the 16-row A operand (tokens are N = 8..32); every
-//    k-step stays inside one 64-group, a second MMA with an all-ones A gives the group sums of x,
-//    and y += s*sum((128+c)x) + (z - 128 s)*sum(x) applies the group scale/zero in fp32;
+//    k-step stays inside one 64-group, the producers of X publish its 64-group sums, and
+//    y += s*sum((128+c)x) + (z - 128 s)*sum(x) applies the group scale/zero in fp32;
 //  * narrow matrices (qkv, o, down) use cluster split-K: the S CTAs of a cluster split a row
 //    tile's K and rank 0 reduces their partial tiles through distributed shared memory, in rank
 //    order, then runs the fused epilogue (bias+RoPE+KV write / residual / SiLU*mul / logits);
@@ -26,19 +26,11 @@
 
 #include <algorithm>
 #include <cstdio>
-#include <cstdlib>
-#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
 
 namespace ss {
-
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 
 static int gemv_grid_for(int N, int K, int grid) {
   const int64_t T = int64_t(N / 128) * (K / 128);
@@ -56,10 +48,9 @@ int gemv_max_segments(int N, int K, int grid) {
   return mx;
 }
 
-// CW: consumer warps (8; 16 for the one-CTA-per-SM qkv plan: warps w and w + 8 take the two
-// tile-chunks of every stage for the same 16 rows and their partial sums are added at the flush)
-template <bool Q4, int NT, bool kCluster, int QB = 4, int CW = 8>
-__global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 1) gemv_kernel(const GemvParams p) {
+template <bool Q4, int NT, bool kCluster, int QB = 4>
+__global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(const GemvParams p) {
+  constexpr int CW = kGemvConsumerWarps;
   using C = GemvCfg<Q4, NT, QB>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int kStages = p.stages;
@@ -72,8 +63,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
   float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
   uint64_t* xbar = reinterpret_cast<uint64_t*>(flag) + 4;      // x prefetch barrier (in the flag block)
   float* xpre = scratch + 128;                                  // [kXPreFloats] residual rows
-  uint8_t* xres = reinterpret_cast<uint8_t*>(xpre + C::kXPreFloats);   // xnorm: [xn_chunks][X chunk]
-  float* xsres = reinterpret_cast<float*>(xres + size_t(p.xn_chunks) * C::kXBytes);   // [xn_chunks][2][Mpad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SS_TRACE_MIN(0);
@@ -111,52 +100,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
       const uint64_t pol = policy_evict_first();
       const int pre = int(n_stage < kStages ? n_stage : kStages);
       Work wx = w;   // replayed below for the activation copies of the prefetched stages
-      const uint32_t per_chunk = p.xnorm ? uint32_t(C::kWBytes) : uint32_t(C::kWBytes + C::kXBytes + C::kSBytes);
+      const uint32_t per_chunk = uint32_t(C::kWBytes + C::kXBytes + C::kSBytes);
       auto issue_w = [&](int st, const Work& ww, int n) {
         mbar_arrive_expect_tx(&full[st], uint32_t(n) * per_chunk);
         bulk_g2s_hint(ring + st * C::kStageBytes, p.W + (int64_t(ww.r) * nC + ww.c) * C::kWBytes,
                       uint32_t(n) * C::kWBytes, &full[st], pol);
       };
       auto issue_x = [&](int st, const Work& ww, int n) {
-        if (p.xnorm) return;
         uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
         bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
         if constexpr (Q4)
           bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * NT * 8, uint32_t(n) * C::kSBytes, &full[st]);
       };
       // weights do not depend on the previous kernel: issue before the grid-dependency wait
-      // (p.pre_after: after it instead — debug A/B of the prefetch's interference)
-      if (p.pre_after) griddep_wait();
       for (int i = 0; i < pre; ++i) {
         const int n = w.take(C::kCPS);
         issue_w(i, w, n);
         w.next(nC, n);
-      }
-      // L2 prefetch of this CTA's own remaining weights (beyond the ring): raises the bytes in
-      // flight from the ring depth to the whole work range, so the DRAM queue stays full and the
-      // ring refills from L2
-      if (p.self_pf) {
-        Work wp = w;
-        int64_t run0 = -1, run1 = -1;
-        auto flush = [&]() {
-          for (int64_t o = run0; o < run1; o += 65536) {
-            const int64_t n = run1 - o < 65536 ? run1 - o : 65536;
-            prefetch_l2(p.W + o, uint32_t(n));
-          }
-        };
-        while (wp.left > 0) {
-          const int n = wp.take(C::kCPS);
-          const int64_t b = (int64_t(wp.r) * nC + wp.c) * C::kWBytes, e = b + int64_t(n) * C::kWBytes;
-          if (b == run1) {
-            run1 = e;
-          } else {
-            if (run0 >= 0) flush();
-            run0 = b;
-            run1 = e;
-          }
-          wp.next(nC, n);
-        }
-        if (run0 >= 0) flush();
       }
       // L2 prefetch of the next matrix (independent of every activation): this CTA's slice, in
       // 64 KB TMA prefetches, so HBM keeps streaming through the dependent steps that follow
@@ -169,7 +129,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
           prefetch_l2(p.pf + o, uint32_t(n));
         }
       };
-      if (p.pf && p.pf_bytes > 0 && !p.pf_late) prefetch_next();
+      if (p.pf && p.pf_bytes > 0) prefetch_next();
       griddep_wait();
       SS_TRACE_CTA0(1);
       for (int i = 0; i < pre; ++i) {
@@ -177,7 +137,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
         issue_x(i, wx, n);
         wx.next(nC, n);
       }
-      if (p.pf && p.pf_bytes > 0 && p.pf_late) prefetch_next();
       int st = pre % kStages;
       uint32_t ph = pre / kStages;   // 0 or 1 (pre <= kStages)
       for (int64_t i = pre; i < n_stage; ++i) {
@@ -210,102 +169,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
   if (threadIdx.x == 0) SS_TRACE_CTA0(2);
   const int g = lane >> 2, t4 = lane & 3;
   const int nthr = CW * 32;
-  const int rw = warp & 7, hh = CW == 16 ? (warp >> 3) : -1;   // row warp, chunk half
-  int xc0 = 0;   // first chunk of the resident X
-  if constexpr (kCluster) {
-    if (CW == 8 && p.xnorm) {
-      // RMSNorm of this CTA's K range: r_m from the per-tile sums of squares (warp m, fixed shuffle
-      // tree), then (token, 64-group) pairs: a warp takes 64 columns of one token, 2 per lane
-      const Work w0 = make_work<kCluster>(p.N, p.K, crank, csize);
-      xc0 = w0.c_begin;
-      const int nchl = w0.c_end - w0.c_begin, k0 = w0.c_begin * 128;
-      // all global loads first (x, gain and the sums of squares are independent), then the math
-      const int npairs = Mpad * nchl * 2;
-      for (int base = warp; base < npairs; base += 8 * kGemvConsumerWarps) {
-        float xv[8][2], gv[8][2];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int pr = base + i * kGemvConsumerWarps, m = pr % Mpad, cg2 = pr / Mpad;
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int k = k0 + 64 * cg2 + 32 * u + lane;
-            const bool ok = pr < npairs && m < p.xn_M;
-            xv[i][u] = ok ? __ldcg(p.xn_x + int64_t(m) * p.xn_ldx + k) : 0.f;
-            gv[i][u] = ok ? bf2f(p.xn_gain[k]) : 0.f;
-          }
-        }
-        if (base == warp) {   // first block: r_m while the loads fly
-          // warp 0 reads the [tiles][Mpad] sums of squares once (lane = tile, contiguous rows; every
-          // CTA re-reading them per token would hammer the same few L2 lines) and reduces each
-          // token's column with a fixed shuffle tree
-          if (warp == 0) {
-            float part[32];
-#pragma unroll
-            for (int m = 0; m < 32; ++m) part[m] = 0.f;
-            for (int t = lane; t < p.xn_ss_tiles; t += 32) {
-              const float4* row = reinterpret_cast<const float4*>(p.xn_ss + int64_t(t) * p.xn_ss_ld);
-#pragma unroll
-              for (int q = 0; q < NT * 2; ++q) {
-                const float4 v = __ldcg(row + q);
-                part[4 * q] += v.x;
-                part[4 * q + 1] += v.y;
-                part[4 * q + 2] += v.z;
-                part[4 * q + 3] += v.w;
-              }
-            }
-#pragma unroll
-            for (int m = 0; m < NT * 8; ++m) {
-              const float ssum = warp_sum(part[m]);
-              if (lane == 0) scratch[m] = m < p.xn_M ? 1.0f / sqrtf(ssum / float(p.xn_ldx) + p.xn_eps) : 0.f;
-            }
-          }
-          named_bar(1, nthr);
-          if (threadIdx.x == 0) SS_TRACE_CTA0(13);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int pr = base + i * kGemvConsumerWarps, m = pr % Mpad, cg2 = pr / Mpad;
-          if (pr >= npairs) break;
-          float gs = 0.f;
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int kl = 64 * cg2 + 32 * u + lane;
-            uint16_t hb = 0;
-            if (m < p.xn_M) hb = f2bf(xv[i][u] * scratch[m] * gv[i][u]);
-            reinterpret_cast<uint16_t*>(xres)[fragx_offset(m, kl, NT)] = hb;
-            gs += bf2f(hb);
-          }
-          gs = warp_sum(gs);
-          if (lane == 0) xsres[cg2 * Mpad + m] = gs;   // chunk cg2/2, group cg2%2
-        }
-      }
-      named_bar(1, nthr);
-      if (threadIdx.x == 0) SS_TRACE_CTA0(14);
-    }
-  }
   float acc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
-  auto stash = [&](float* dst) {   // [128][Mpad] partial tile (CW = 16: half 0 stores, half 1 adds)
-    if constexpr (CW == 16) {
-      if (hh == 0) stash_acc<NT>(acc, dst, rw, lane);
-      named_bar(1, nthr);
-      if (hh == 1) {
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const int n0 = rw * 16 + g, m = j * 8 + 2 * t4, Mp = NT * 8;
-          dst[n0 * Mp + m] += acc[j][0];
-          dst[n0 * Mp + m + 1] += acc[j][1];
-          dst[(n0 + 8) * Mp + m] += acc[j][2];
-          dst[(n0 + 8) * Mp + m + 1] += acc[j][3];
-          acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-        }
-      }
-    } else {
-      stash_acc<NT>(acc, dst, warp, lane);
-    }
-  };
+  auto stash = [&](float* dst) { stash_acc<NT>(acc, dst, warp, lane); };   // [128][Mpad] partial tile
 
   uint32_t xph = 0;   // phase of xbar
   auto flush = [&](int r, int c_first, int c_last, bool last) {
@@ -331,36 +199,20 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
       // epilogue's read-modify-write does not pay an L2 round trip after the reduction
       const int nvalid = nc < p.epi.M - mlo ? nc : (p.epi.M - mlo > 0 ? p.epi.M - mlo : 0);
       const bool xp = nvalid > 0 && nc <= C::kXPreTokens &&
-                      (p.epi.kind == EPI_RESID || p.epi.kind == EPI_RESID_SS || p.epi.kind == EPI_RESID_NORM);
+                      (p.epi.kind == EPI_RESID || p.epi.kind == EPI_RESID_NORM);
       if (xp && threadIdx.x == 0) {
         mbar_arrive_expect_tx(xbar, uint32_t(nvalid) * kTileRows * 4);
         for (int m = 0; m < nvalid; ++m)
           bulk_g2s(xpre + m * kTileRows, p.epi.x + int64_t(mlo + m) * p.epi.ldx + int64_t(r) * kTileRows, kTileRows * 4, xbar);
       }
-      if (CW == 8 || hh == 0) {
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
-          const int n0 = rw * 16 + g, m = j * 8 + 2 * t4;
-          otile[m * kTileRows + n0] = acc[j][0];
-          otile[(m + 1) * kTileRows + n0] = acc[j][1];
-          otile[m * kTileRows + n0 + 8] = acc[j][2];
-          otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
-          acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-        }
-      }
-      if constexpr (CW == 16) {   // the other chunk half adds its partial sums (fixed order)
-        named_bar(1, nthr);
-        if (hh == 1) {
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const int n0 = rw * 16 + g, m = j * 8 + 2 * t4;
-            otile[m * kTileRows + n0] += acc[j][0];
-            otile[(m + 1) * kTileRows + n0] += acc[j][1];
-            otile[m * kTileRows + n0 + 8] += acc[j][2];
-            otile[(m + 1) * kTileRows + n0 + 8] += acc[j][3];
-            acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-          }
-        }
+      for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
+        const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
+        otile[m * kTileRows + n0] = acc[j][0];
+        otile[(m + 1) * kTileRows + n0] = acc[j][1];
+        otile[m * kTileRows + n0 + 8] = acc[j][2];
+        otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
       }
       named_bar(1, nthr);
       for (int i = threadIdx.x; i < Mpad * (kTileRows / 4); i += nthr) {
@@ -440,11 +292,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
         SS_TRACE_CTA0(3);
         if (ct) ct[2] = gtime();
       }
-      if (CW == 8 && p.xnorm)
-        consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane, xres + (w.c - xc0) * C::kXBytes,
-                              xsres + (w.c - xc0) * 2 * Mpad);
-      else
-        consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, rw, lane, nullptr, nullptr, hh);
+      consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) {
@@ -468,80 +316,67 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW == 8 ? SS_GEMV_MIN_BLOCKS : 
 }
 
 
-// CTAs per SM of the cluster plan: SS_GEMV_CTAS_PER_SM (default 2), overridable per shape with
-// SS_GEMV_PERSM_OVR="N:K:v,N:K:v" (debug A/B of the plan per matrix group)
-static int per_sm_for(int N, int K, int hint) {
-  static const int env_dflt = env_int("SS_GEMV_CTAS_PER_SM", 0);
-  const int dflt = env_dflt > 0 ? env_dflt : (hint > 0 ? hint : 2);
-  const char* o = getenv("SS_GEMV_PERSM_OVR");
-  while (o && *o) {
-    int n = 0, k = 0, v = 0;
-    if (sscanf(o, "%d:%d:%d", &n, &k, &v) == 3 && n == N && k == K && v > 0) return v;
-    o = strchr(o, ',');
-    if (o) ++o;
-  }
-  return dflt;
-}
-
-// split factor of the cluster mode: ~2 CTAs per SM, <= SS_GEMV_MAX_CLUSTER, <= chunks
+// split factor of the cluster mode: ~per_sm CTAs per SM (hint, default 2), <= 8 (portable), <= chunks
 int gemv_cluster_split(int N, int K, int sms, int hint) {
   const int tiles = N / 128, nC = K / 128;
-  const int per_sm = per_sm_for(N, K, hint);
-  int cap = std::min(env_int("SS_GEMV_MAX_CLUSTER", 8), kGemvMaxCluster);
-  const char* o = getenv("SS_GEMV_SPLIT_OVR");   // debug A/B: "N:K:cap,..." per shape
-  while (o && *o) {
-    int n = 0, k = 0, v = 0;
-    if (sscanf(o, "%d:%d:%d", &n, &k, &v) == 3 && n == N && k == K && v > 0) cap = std::min(v, kGemvMaxCluster);
-    o = strchr(o, ',');
-    if (o) ++o;
-  }
+  const int per_sm = hint > 0 ? hint : 2;
   int S = (per_sm * sms) / tiles;
   if (S < 1) S = 1;
-  if (S > cap) S = cap;
+  if (S > 8) S = 8;
   if (S > nC) S = nC;
   return S;
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4, int CW = 8>
-static int ensure_attrs() {   // ring stages for this instantiation; sets the smem/cluster attributes once
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// ring stages of an instantiation; sets its smem/cluster attributes once per device (function
+// attributes are per device)
+template <bool Q4, int NT, bool kCluster, int QB = 4>
+static int ensure_attrs() {
   using C = GemvCfg<Q4, NT, QB>;
-  static int stages = 0;
-  if (!stages) {
-    // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
-    // down to ~68 KB of whole stages)
-    const int budget = (QB == 2 ? env_int("SS_GEMV_RING_KB_Q2", 72) : env_int("SS_GEMV_RING_KB", 88)) * 1024;
-    int st = budget / C::kStageBytes;
-    if (st < 2) st = 2;
-    if (st > C::kMaxStages) st = C::kMaxStages;
-    cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::smem_for(st) + (kCluster ? 8 * (C::kXBytes + C::kSBytes) : 0));
-    if (kCluster) cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB, CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    stages = st;
-  }
-  return stages;
+  static std::mutex mu;
+  static std::map<int, int> stages_of;
+  std::lock_guard<std::mutex> lk(mu);
+  const int dev = current_device();
+  auto it = stages_of.find(dev);
+  if (it != stages_of.end()) return it->second;
+  // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
+  // down to ~68 KB of whole stages)
+  const int budget = (QB == 2 ? 72 : 88) * 1024;
+  int st = budget / C::kStageBytes;
+  if (st < 2) st = 2;
+  if (st > C::kMaxStages) st = C::kMaxStages;
+  cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
+  stages_of[dev] = st;
+  return st;
 }
 
 // Cluster plan {S, clusters}: the GPC structure caps how many clusters of S CTAs are resident at
 // once (e.g. 33 clusters of 8 at 2 CTAs/SM, below qkv's 36 row tiles), and a tile whose cluster is
 // not resident waits for a second wave.  Take the largest S <= gemv_cluster_split whose resident
-// cluster count covers every row tile (queried with cudaOccupancyMaxActiveClusters).
+// cluster count covers every row tile (queried with cudaOccupancyMaxActiveClusters).  Cached per
+// (device, shape, hint).
 struct ClusterPlan {
   int S, ncl;
   bool all_resident;
 };
-template <bool Q4, int NT, int QB = 4, int CW = 8>
+template <bool Q4, int NT, int QB = 4>
 static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
+  const int stages = ensure_attrs<Q4, NT, true, QB>();
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int>, ClusterPlan> cache;
+  static std::map<std::tuple<int, int, int, int>, ClusterPlan> cache;
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(N, K, hint);
+  const auto key = std::make_tuple(current_device(), N, K, hint);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   using C = GemvCfg<Q4, NT, QB>;
-  const int stages = ensure_attrs<Q4, NT, true, QB, CW>();
   const int tiles = N / 128;
-  const int per_sm = per_sm_for(N, K, hint);
+  const int per_sm = hint > 0 ? hint : 2;
   const int S0 = gemv_cluster_split(N, K, sms, hint);
   ClusterPlan plan{S0, 0, false};
   for (int S = S0; S >= 1; --S) {
@@ -550,7 +385,7 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     if (ncl < 1) ncl = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncl * S);
-    cfg.blockDim = dim3((CW + 1) * 32);
+    cfg.blockDim = dim3(kGemvThreads);
     cfg.dynamicSmemBytes = C::smem_for(stages);
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -560,7 +395,7 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true, QB, CW>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true, QB>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       active = ncl;   // cannot query: keep the arithmetic plan
     }
@@ -571,9 +406,6 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     }
   }
   if (plan.ncl < 1) plan.ncl = 1;
-  if (getenv("SS_VERBOSE"))
-    fprintf(stderr, "gemv cluster plan<%d,%d> N=%d K=%d hint=%d: S=%d clusters=%d all_resident=%d\n", int(Q4), NT, N, K,
-            hint, plan.S, plan.ncl, int(plan.all_resident));
   cache[key] = plan;
   return plan;
 }
@@ -599,23 +431,16 @@ bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits) {
   }
 }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4, int CW = 8>
+template <bool Q4, int NT, bool kCluster, int QB = 4>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
   using C = GemvCfg<Q4, NT, QB>;
-  const int stages = ensure_attrs<Q4, NT, kCluster, QB, CW>();
+  const int stages = ensure_attrs<Q4, NT, kCluster, QB>();
   GemvParams p = p0;
   p.stages = stages;
-  p.xn_chunks = 0;
-  if (p.xnorm) {
-    if (!kCluster) return;   // xnorm needs a fixed per-CTA K range (engine guarantees cluster mode)
-    const int nC = p.K / 128;
-    p.xn_chunks = (nC + S - 1) / S;
-  }
-  const size_t xbytes = size_t(p.xn_chunks) * (C::kXBytes + C::kSBytes);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3((CW + 1) * 32);
-  cfg.dynamicSmemBytes = C::smem_for(stages) + xbytes;
+  cfg.blockDim = dim3(kGemvThreads);
+  cfg.dynamicSmemBytes = C::smem_for(stages);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -633,17 +458,12 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster, QB, CW>, p);
+  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster, QB>, p);
 }
 
 template <bool Q4, int NT, int QB = 4>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
-  static const bool cw16 = env_int("SS_GEMV_CW16", 0) != 0;   // opt-in: measured slower in the pass
-  if (gemv_use_cluster(p.N, p.K, sms) && Q4 && cw16 && p.ctas_per_sm == 1 && !p.xnorm) {
-    // one CTA per SM: 16 consumer warps (two per 16-row block, one per tile-chunk of a stage)
-    const ClusterPlan pl = cluster_plan<Q4, NT, QB, 16>(p.N, p.K, sms, p.ctas_per_sm);
-    launch_t<Q4, NT, true, QB, 16>(p, pl.ncl * pl.S, pl.S, pdl, st);
-  } else if (gemv_use_cluster(p.N, p.K, sms)) {
+  if (gemv_use_cluster(p.N, p.K, sms)) {
     const ClusterPlan pl = cluster_plan<Q4, NT, QB>(p.N, p.K, sms, p.ctas_per_sm);
     launch_t<Q4, NT, true, QB>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {

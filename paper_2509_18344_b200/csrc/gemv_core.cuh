@@ -1,6 +1,5 @@
-// K2 building blocks shared by the dequant-GEMV kernel (gemv.cu) and the fused MLP kernel (mlp.cu):
-// pipeline geometry, work lists, and the per-stage tensor-core consumer (see gemv.cu's header for
-// the design).
+// K2 building blocks of the dequant-GEMV kernel (gemv.cu): pipeline geometry, work lists, and the
+// per-stage tensor-core consumer (see gemv.cu's header for the design).
 #pragma once
 #include "common.cuh"
 
@@ -8,7 +7,7 @@ namespace ss {
 
 constexpr int kGemvConsumerWarps = 8;
 constexpr int kGemvThreads = (kGemvConsumerWarps + 1) * 32;
-constexpr int kGemvMaxCluster = 16;  // largest (non-portable) cluster the split factor may use
+constexpr int kGemvMaxCluster = 8;   // largest (portable) cluster the split factor may use
 #ifndef SS_GEMV_MIN_BLOCKS
 #define SS_GEMV_MIN_BLOCKS 2
 #endif
@@ -163,23 +162,18 @@ SS_DEV Work make_work(int N, int K, uint32_t crank, uint32_t csize) {
 // One pipeline stage (nch tile-chunks of weights + the matching activation chunks + group sums)
 // accumulated into this warp's 16 rows x Mpad tokens.
 template <bool Q4, int NT, int QB = 4>
-SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], int warp, int lane,
-                          const uint8_t* xres = nullptr, const float* xsres = nullptr, int ci_only = -1) {
-  // warp: row warp (rows 16 warp .. +15 of the tile); ci_only >= 0: only that tile-chunk of the
-  // stage (16-consumer-warp CTAs split a stage's two chunks over two warp halves)
+SS_DEV void consume_stage(const uint8_t* stage, int nch, float (&acc)[NT][4], int warp, int lane) {
+  // warp: row warp (rows 16 warp .. +15 of the tile)
   using C = GemvCfg<Q4, NT, QB>;
   const int g = lane >> 2, t4 = lane & 3;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
 #pragma unroll
   for (int ci = 0; ci < C::kCPS; ++ci) {
     if (ci >= nch) break;
-    if (ci_only >= 0 && ci != ci_only) continue;
     const uint8_t* wst = stage + ci * C::kWBytes;
-    // activations: from the stage (TMA) or from a CTA-resident normalised copy (xres, xsres)
-    const uint8_t* xst = (xres ? xres + ci * C::kXBytes : stage + C::kCPS * C::kWBytes + ci * C::kXBytes) + ((t4 * 8 + g) * 8);
+    const uint8_t* xst = stage + C::kCPS * C::kWBytes + ci * C::kXBytes + ((t4 * 8 + g) * 8);
     if constexpr (Q4) {
-      const float* xsum = xsres ? xsres + ci * 2 * NT * 8
-                                : reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
+      const float* xsum = reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
 #pragma unroll
       for (int G = 0; G < 2; ++G) {
         uint4 cw;

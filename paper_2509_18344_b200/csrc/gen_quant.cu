@@ -50,6 +50,26 @@ __global__ void gen_tiled_kernel(uint8_t* __restrict__ dst, uint64_t key, int64_
   }
 }
 
+// caller weights: natural row-major bf16 source [rows x K] (device copy) -> tiled destination, with
+// the same row map as gen_tiled_kernel
+__global__ void tile_from_natural_kernel(uint8_t* __restrict__ dst, const uint16_t* __restrict__ src, int64_t rows,
+                                         int64_t K, int map, int64_t row_off) {
+  int64_t n8 = rows * (K / 8);
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n8; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t r = t / (K / 8), k0 = (t % (K / 8)) * 8;
+    int64_t dr = map == 0 ? row_off + r : (map == 1 ? (r / 64) * 128 + (r % 64) : (r / 64) * 128 + 64 + (r % 64));
+    *reinterpret_cast<uint4*>(dst + bf16_tiled_offset(dr, k0, K)) = *reinterpret_cast<const uint4*>(src + r * K + k0);
+  }
+}
+
+void launch_tile_from_natural(uint8_t* dst, const uint16_t* src, int64_t rows, int64_t K, int map, int64_t row_off,
+                              cudaStream_t st) {
+  int64_t n8 = rows * (K / 8);
+  int blocks = int((n8 + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  tile_from_natural_kernel<<<blocks, 256, 0, st>>>(dst, src, rows, K, map, row_off);
+}
+
 void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st,
                         uint64_t first) {
   int blocks = int((count + 255) / 256);

@@ -18,7 +18,7 @@ struct ReqMap {
 __host__ __device__ inline int rq_req(const ReqMap& r, int m) { return r.rows > 0 ? r.req0 + m / r.rows : r.req0; }
 __host__ __device__ inline int rq_loc(const ReqMap& r, int m) { return r.rows > 0 ? m % r.rows : m; }
 
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5, EPI_RESID_SS = 6, EPI_RESID_NORM = 7 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5, EPI_RESID_NORM = 7 };
 
 // Epilogue parameters shared by the GEMV (draft, M <= 32) and GEMM (verify) kernels.
 struct EpiParams {
@@ -45,7 +45,7 @@ struct EpiParams {
   // EPI_LOGITS / EPI_STORE
   float* out;                    // [M x ldo]
   int ldo;
-  // EPI_RESID_SS: residual add + per-tile sum of squares of the new x rows (for the fused RMSNorm)
+  // EPI_RESID_NORM: residual add + per-tile sums of squares of the new x rows (fused RMSNorm)
   float* sumsq;                  // [N/128][sumsq_ld]
   int sumsq_ld;                  // Mpad; 0 = the caller's tile stride
   // EPI_RESID_NORM (cluster GEMV only): + in-kernel barrier of the tile owners, then the owner of
@@ -74,55 +74,16 @@ struct GemvParams {
   int stages;                    // ring depth (set by the launcher)
   const uint8_t* pf;             // weights of the NEXT matrix: prefetched into L2 while this one runs
   int64_t pf_bytes;
-  int pf_late;                   // issue the L2 prefetch of pf after the grid-dependency wait
   unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
-  int pre_after;                 // debug: issue the first weight stages after griddepcontrol.wait
-  int self_pf;                   // prefetch this CTA's own remaining weight range into L2 at entry
   int ctas_per_sm;               // cluster plan: resident CTAs per SM to plan for (0 = default 2)
   int qbits;                     // code bits of a quantised matrix: 4 (0 = 4) or 2 (NEXT-3)
-  // xnorm (cluster mode): instead of TMA-ing X/XS, the consumers build this CTA's K range of
-  // X = bf16(x * r_m * gain) (RMSNorm of the residual stream, r_m from per-tile sums of squares)
-  // and its group sums in shared memory once, before the main loop
-  int xnorm;
-  const float* xn_x;             // residual stream [M x xn_ldx] fp32
-  int xn_ldx;
-  const float* xn_ss;            // sums of squares [xn_ss_tiles][xn_ss_ld]
-  int xn_ss_ld, xn_ss_tiles;
-  const uint16_t* xn_gain;       // RMSNorm gain [K] bf16
-  float xn_eps;
-  int xn_M;                      // valid tokens
-  int xn_chunks;                 // set by the launcher: resident chunks per CTA (smem sizing)
   EpiParams epi;
 };
 
 int gemv_max_segments(int N, int K, int grid);
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits = 4);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
-
-// Fused draft MLP of one layer (mlp.cu): gate_up (EPI_SILU) then down (epi_d) in one persistent
-// launch; down's K-chunks wait on per-gate_up-tile flags instead of a kernel boundary.
-struct MlpParams {
-  const uint8_t* Wgu;            // tiled weights [2F x H] (gate/up interleaved per 64 rows)
-  const uint8_t* Wd;             // tiled weights [H x F]
-  const uint16_t* Xh;            // FragX of the normed hidden state [Mpad x H]
-  const float* XSh;              // its group sums [H/64][Mpad]
-  const uint16_t* Xa;            // FragX of the activations [Mpad x F] (written by phase A)
-  const float* XSa;              // their group sums [F/64][Mpad]
-  int H, F, NT;
-  float* partials;               // down Stream-K partial tiles [H/128][max_seg][128*Mpad]
-  int* counters;                 // [H/128], zero on entry, restored to zero on exit
-  int max_seg;
-  int* flags;                    // [2F/128][32] gate_up tile done flags (one per 128 B), zero on entry, reset on exit
-  int* exit_ctr;                 // [1], zero on entry, reset on exit
-  int stages;                    // ring depth (set by the launcher)
-  unsigned long long* trace;     // optional [kTraceEvents] (debug)
-  int dbg;                       // debug bits: 1 phase B waits for every gate_up tile; 2 phase A only;
-                                 // 4 phase B only; 8 L2-prefetch phase B weights during phase A
-  EpiParams epi_gu, epi_d;
-};
-int mlp_grid(bool q4, int NT, int sms);   // all-resident persistent grid (0: unsupported)
-void launch_mlp(bool q4, const MlpParams& p, int grid, bool pdl, cudaStream_t st);
 
 struct GemmParams {
   const uint8_t* W;              // tiled BF16 weights [N x K]
@@ -137,6 +98,8 @@ void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, 
                         uint64_t first = 0);   // elements [first, first + count) of the tensor
 void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float c32, int map, int64_t row_off,
                       cudaStream_t st);
+void launch_tile_from_natural(uint8_t* dst, const uint16_t* src, int64_t rows, int64_t K, int map, int64_t row_off,
+                              cudaStream_t st);
 void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, cudaStream_t st);
 void launch_q4_to_canonical(const uint8_t* q4, uint8_t* codes, uint16_t* s, uint16_t* z, int64_t N, int64_t K,
                             cudaStream_t st);
@@ -162,20 +125,14 @@ struct AttnParams {
   int n_q, node_base;            // query rows are nodes node_base .. node_base + n_q - 1
   ReqMap rq;                     // batched requests (zero: one request)
   int n_heads, n_kv, head_dim;
-  int split;                     // prefix keys per segment
-  int n_seg_max;                 // segments allocated in the partial buffers
-  float* part_o;                 // [n_q * n_heads][n_seg_max][d]
-  float* part_ml;                // [n_q * n_heads][n_seg_max][2]
-  int* counters;                 // unused (reserved)
-  int single;                    // set by the launcher: all rows fit one segment
-  int cluster;                   // K3 v2: CTAs per (kv head, node) cluster (set by the launcher)
+  int cluster;                   // CTAs per (kv head, node) cluster (set by the launcher)
   unsigned long long* trace;     // optional (debug): 0 entry min, 1 dep released max, 2 q loaded max,
                                  // 3 key loop done max, 4 CTA merge done max, 5 end max
   uint16_t* out_fragx;           // [Mpad x n_heads*d] FragX
   float* out_xs;                 // group sums [n_heads*d/64][Mpad]
   int out_nt;
 };
-void launch_attention(const AttnParams& p, int max_prefix, bool pdl, cudaStream_t st);
+void launch_attention(const AttnParams& p, bool pdl, cudaStream_t st);
 
 struct TopkParams {
   const float* logits;           // [M x V]
@@ -228,49 +185,6 @@ struct AcceptParams {
   int n_req, req0, node_stride, ctx_stride, out_stride;
 };
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st);
-
-// ---- persistent draft pass (pass.cu) -------------------------------------------------------
-enum PhaseKind { PH_EMBED = 0, PH_GEMV = 1, PH_ATTN = 2, PH_TOPK1 = 3, PH_TOPK2 = 4, PH_NORM = 5, PH_COMBINE = 6 };
-enum XSrc { XS_NORM = 0, XS_FRAGX = 1 };
-struct PhaseDesc {
-  int kind;
-  // PH_GEMV
-  const uint8_t* W;
-  int N, K, q4;
-  int xsrc;                      // XS_NORM: h = bf16(x * r(sumsq) * gain); XS_FRAGX: X/XSUM given
-  const uint16_t* gain;
-  const uint16_t* X;
-  const float* XSUM;
-  EpiParams epi;                 // M / node_base / act_nt are patched per pass
-  // PH_ATTN
-  int layer;
-};
-struct PassParams {
-  const PhaseDesc* ph;
-  int n_ph;
-  int M, NT, node_base;
-  int H;
-  float eps;
-  float* x;                      // [Mpad x H] fp32 residual stream
-  float* sumsq;                  // [H/128][Mpad] per-tile sums of squares of x
-  const int* tok;
-  const uint16_t* embed;
-  float* partials;               // Stream-K partial tiles
-  int* tile_ctr;                 // per-tile arrival counters (zero between phases)
-  int max_seg;                   // partial slots per tile (host: max over phases of pass_max_segments)
-  unsigned* bar;                 // grid barrier counter (zeroed before each launch)
-  int stages;
-  AttnParams attn;               // layer 0 pointers; + layer * stride
-  int64_t kc_layer, kt_layer;
-  int* attn_ctr;                 // [Mpad * n_kv] segment-arrival counters
-  TopkParams topk;
-  unsigned long long* trace;     // optional: per-phase %globaltimer (CTA 0), [n_ph][2]
-  int skip_topk;                 // debug: logits only, leave the tree untouched
-};
-int pass_smem_bytes(int head_dim, int stages);
-void launch_draft_pass(const PassParams& p, int grid, int head_dim, cudaStream_t st);
-int pass_max_grid(int head_dim, int stages);
-int pass_max_segments(int N, int K, int grid);
 
 // tree init for a new step: root node (slot 0) with token *root_tok, depth 0
 void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,

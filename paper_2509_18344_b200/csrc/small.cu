@@ -95,37 +95,10 @@ void launch_rmsnorm(const float* x, int M, int H, const uint16_t* gain, float ep
 // K3: tree attention.  Row = (query node, head).  The keys of node i
 // form one LOGICAL sequence: committed prefix [0, P) followed by its ancestors root..i (tree
 // slots), i.e. exactly the keys an AR step at that position would see, in the same order.
-// Segment s covers logical keys [s*split, (s+1)*split); prefix keys of a segment are shared by
-// all rows and staged in shared memory, ancestor keys are read per row.  Partials (o, m, l) are
-// merged in segment order by attn_combine.  Because the blocking depends only on the logical key
-// index, a node's attention is bitwise identical whether computed in a tree (verify) or as an AR
-// step.
+// One CTA per (kv head, node) walks the node's logical keys in 16-key tiles (attn_warp.cuh).
+// Because the blocking depends only on the logical key index, a node's attention is bitwise
+// identical whether computed in a tree (verify) or as an AR step.
 // ---------------------------------------------------------------------------
-// Warp w of CTA (kvh, seg, qb) handles node node_base + qb*8 + w (see attn_task).
-template <int D>
-__global__ void __launch_bounds__(256, 1) attn_partial_kernel(const AttnParams p) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int kvh = blockIdx.x, seg = blockIdx.y, qb = blockIdx.z;
-  const int warp = threadIdx.x >> 5;
-  griddep_launch();
-  griddep_wait();
-  const int P = *p.committed_len;
-  const int qi = qb * kAttnQB + warp;
-  if (qi >= p.n_q) return;
-  attn_task<D>(p, P, kvh, seg, qi, reinterpret_cast<uint16_t*>(sm) + warp * 4 * 16 * (D + 8), p.single);
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnParams p) {
-  griddep_launch();
-  griddep_wait();
-  const int P = *p.committed_len;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = int64_t(blockIdx.x) * 8 + warp;
-  if (row >= int64_t(p.n_q) * p.n_heads) return;
-  attn_combine_row<D>(p, P, int(row / p.n_heads), int(row % p.n_heads), lane);
-}
-
 template <int D>
 __global__ void __launch_bounds__(256, 1) attn_node_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t sm[];
@@ -150,61 +123,36 @@ __global__ void __launch_bounds__(256, 1) attn_node_kernel(const AttnParams p) {
   }
 }
 
-void launch_attention(const AttnParams& p, int max_prefix, bool pdl, cudaStream_t st) {
-  if (p.split <= 0) {   // K3 v2: cluster of S CTAs per (kv head, node), DSMEM merge, no combine kernel
-    static const int S_env = [] {
-      const char* v = getenv("SS_ATTN_CLUSTER");
-      const int s = v ? atoi(v) : 1;
-      return s < 1 ? 1 : (s > 8 ? 8 : s);
-    }();
-    const int S = S_env;
-    const size_t smem = size_t(8) * 4 * 16 * (p.head_dim + 8) * 2 + size_t(8) * 16 * (p.head_dim + 2) * 4 +
-                        size_t(16) * (p.head_dim + 4) * 4;
-    AttnParams pp = p;
-    pp.cluster = S;
-    const void* fn = p.head_dim == 128 ? (const void*)attn_node_kernel<128> : (const void*)attn_node_kernel<64>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.n_kv * S, p.n_q);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = S;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-    if (pdl) {
-      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[na].val.programmaticStreamSerializationAllowed = 1;
-      ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    if (p.head_dim == 128) cudaLaunchKernelEx(&cfg, attn_node_kernel<128>, pp);
-    else cudaLaunchKernelEx(&cfg, attn_node_kernel<64>, pp);
-    return;
-  }
-  const int grp = p.n_heads / p.n_kv;
-  const int nseg = (max_prefix + p.split - 1) / p.split;   // max_prefix: max logical keys of any row
+void launch_attention(const AttnParams& p, bool pdl, cudaStream_t st) {
+  // cluster of S = 1 CTA per (kv head, node): the S > 1 DSMEM key split measured no gain
+  const int S = 1;
+  const size_t smem = size_t(8) * 4 * 16 * (p.head_dim + 8) * 2 + size_t(8) * 16 * (p.head_dim + 2) * 4 +
+                      size_t(16) * (p.head_dim + 4) * 4;
   AttnParams pp = p;
-  pp.single = nseg <= 1;   // every row fits one segment: write outputs from registers, no combine
-  const size_t smem = size_t(kAttnQB) * 4 * 16 * (p.head_dim + 8) * 2;   // per warp: 2 buffers x (K, V) x 16 keys
-  const dim3 grid(p.n_kv, nseg, (p.n_q + kAttnQB - 1) / kAttnQB);
-  void* args[] = {&pp};
-  if (p.head_dim == 128) {
-    cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_pdl((const void*)attn_partial_kernel<128>, grid, dim3(256), smem, pdl, st, args);
-    if (!pp.single)
-      launch_pdl((const void*)attn_combine_kernel<128>, dim3((p.n_q * p.n_heads + 7) / 8), dim3(256), 0, pdl, st, args);
-  } else {
-    cudaFuncSetAttribute(attn_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_pdl((const void*)attn_partial_kernel<64>, grid, dim3(256), smem, pdl, st, args);
-    if (!pp.single)
-      launch_pdl((const void*)attn_combine_kernel<64>, dim3((p.n_q * p.n_heads + 7) / 8), dim3(256), 0, pdl, st, args);
+  pp.cluster = S;
+  const void* fn = p.head_dim == 128 ? (const void*)attn_node_kernel<128> : (const void*)attn_node_kernel<64>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_kv * S, p.n_q);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = S;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (p.head_dim == 128) cudaLaunchKernelEx(&cfg, attn_node_kernel<128>, pp);
+  else cudaLaunchKernelEx(&cfg, attn_node_kernel<64>, pp);
 }
 
 // ---------------------------------------------------------------------------

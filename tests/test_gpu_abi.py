@@ -17,7 +17,7 @@ def test_status_codes(cuda_required):
     with pytest.raises(SubSpecError) as e:
         ss.build_substitutes(4, 64)
     assert e.value.status == 3
-    ss.load_weights(0x5EED, 1)
+    ss.load_synthetic(0x5EED, 1)
     with pytest.raises(SubSpecError) as e:
         ss.build_substitutes(3, 64)                # only 4-bit g64
     assert e.value.status == 1

@@ -23,7 +23,7 @@ SEED = 0x5EED
 def _ctx(cfg, n_res, D, k, B, cap=768 << 20, max_chunk=256):
     from paper_2509_18344_b200.binding import SubSpec
     ss = SubSpec(cfg, cap, max_depth=D, max_top_k=k, max_chunk=max_chunk, max_batch=B)
-    ss.load_weights(SEED, n_resident=n_res)
+    ss.load_synthetic(SEED, n_resident=n_res)
     ss.build_substitutes(4, 64)
     return ss
 
@@ -110,7 +110,7 @@ def test_qwen7b_batch4_at_8gib(cuda_required):
     from paper_2509_18344_b200.binding import SubSpec
     B, D, k = 4, 48, 6
     ss = SubSpec(QWEN7B, 8 * GIB, max_depth=D, max_top_k=k, max_chunk=256, max_batch=B)
-    ss.load_weights(SEED, n_resident=0)
+    ss.load_synthetic(SEED, n_resident=0)
     ss.build_substitutes(4, 64)
     prompts = [mtbench_prompt(SEED, p, QWEN7B.vocab) for p in range(B)]
     outs, hist = ss.generate_batch(prompts, 12, D, k, 0.2)

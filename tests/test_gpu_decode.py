@@ -30,7 +30,7 @@ SEED = 0x5EED
 def _gpu(cfg, n_resident, D, k, cap=512 << 20, max_chunk=256):
     from paper_2509_18344_b200.binding import SubSpec
     ss = SubSpec(cfg, cap, max_depth=D, max_top_k=k, max_chunk=max_chunk)
-    ss.load_weights(SEED, n_resident=n_resident)
+    ss.load_synthetic(SEED, n_resident=n_resident)
     ss.build_substitutes(4, 64)
     return ss
 

@@ -29,7 +29,7 @@ def big(request, cuda_required):
     from paper_2509_18344_b200.binding import SubSpec
     cfg, cap = CASES[request.param]
     ss = SubSpec(cfg, cap * GIB, max_depth=48, max_top_k=8, max_chunk=256)
-    ss.load_weights(SEED, n_resident=0)
+    ss.load_synthetic(SEED, n_resident=0)
     ss.build_substitutes(4, 64)
     yield cfg, ss
     ss.close()

@@ -40,7 +40,7 @@ def test_device_generator_matches_numpy(cuda_required):
 def test_placed_weights_and_substitutes_bit_exact(cuda_required, cfg):
     from paper_2509_18344_b200.binding import SubSpec
     ss = SubSpec(cfg, 512 << 20, max_depth=4, max_top_k=6)
-    ss.load_weights(SEED, n_resident=1)
+    ss.load_synthetic(SEED, n_resident=1)
     ss.build_substitutes(4, 64)
     model = W.generate_model(cfg, SEED)
     for l in range(cfg.n_layers):

@@ -22,7 +22,7 @@ def ctx(request, cuda_required):
     from paper_2509_18344_b200.binding import SubSpec
     cfg = request.param
     ss = SubSpec(cfg, 512 << 20, max_depth=4, max_top_k=6)
-    ss.load_weights(SEED, n_resident=1)     # layer 0 resident (bf16), others substituted
+    ss.load_synthetic(SEED, n_resident=1)     # layer 0 resident (bf16), others substituted
     ss.build_substitutes(4, 64)
     yield cfg, ss
     ss.close()

@@ -28,7 +28,7 @@ def _ctx(cfg, cap=512 << 20, n_resident=1, D=4, k=6, bits=2):
     from paper_2509_18344_b200.binding import SubSpec
     ss = SubSpec(cfg, cap, max_depth=D, max_top_k=k)
     ss.set_substitute_bits(bits)
-    ss.load_weights(SEED, n_resident=n_resident)
+    ss.load_synthetic(SEED, n_resident=n_resident)
     ss.build_substitutes(bits, 64)
     return ss
 
@@ -142,7 +142,7 @@ def test_q2_abi_errors(cuda_required):
     with pytest.raises(SubSpecError, match="INVALID"):
         ss.set_substitute_bits(3)                     # 4 or 2 only
     ss.set_substitute_bits(2)
-    ss.load_weights(SEED, n_resident=1)
+    ss.load_synthetic(SEED, n_resident=1)
     with pytest.raises(SubSpecError, match="STRUCTURE"):
         ss.set_substitute_bits(4)                     # the layout is fixed at placement
     with pytest.raises(SubSpecError, match="INVALID"):

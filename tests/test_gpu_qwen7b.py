@@ -25,7 +25,7 @@ D, K_TOP = 48, 6
 def q7(cuda_required):
     from paper_2509_18344_b200.binding import SubSpec
     ss = SubSpec(QWEN7B, 8 * GIB, max_depth=D, max_top_k=K_TOP, max_chunk=256)
-    ss.load_weights(SEED, n_resident=0)
+    ss.load_synthetic(SEED, n_resident=0)
     ss.build_substitutes(4, 64)
     yield ss
     ss.close()

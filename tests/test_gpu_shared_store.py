@@ -25,7 +25,7 @@ def _ctx():
 def test_two_contexts_share_one_host_store(cuda_required):
     prompt = mtbench_prompt(SEED, 3, SMALL.vocab, 40)
     own = _ctx()
-    own.load_weights(SEED, n_resident=1)
+    own.load_synthetic(SEED, n_resident=1)
     own.build_substitutes(4, 64)
     ref, _ = own.generate(prompt, 16, 4, 4, 0.2)
     nbytes = own.host_store_bytes(1)
@@ -35,8 +35,8 @@ def test_two_contexts_share_one_host_store(cuda_required):
     store = mmap.mmap(-1, nbytes)   # page-aligned anonymous mapping, caller-owned
     addr = ctypes.addressof(ctypes.c_char.from_buffer(store))
     a, b = _ctx(), _ctx()
-    a.load_weights_shared(SEED, 1, addr, nbytes, fill=True)
-    b.load_weights_shared(SEED, 1, addr, nbytes, fill=False)   # attaches: nothing generated
+    a.load_synthetic_shared(SEED, 1, addr, nbytes, fill=True)
+    b.load_synthetic_shared(SEED, 1, addr, nbytes, fill=False)   # attaches: nothing generated
     for ss in (a, b):
         ss.build_substitutes(4, 64)
         out, _ = ss.generate(prompt, 16, 4, 4, 0.2)
@@ -54,7 +54,7 @@ def test_shared_store_too_small_is_rejected(cuda_required):
     store = mmap.mmap(-1, 1 << 20)
     addr = ctypes.addressof(ctypes.c_char.from_buffer(store))
     with pytest.raises(SubSpecError):
-        ss.load_weights_shared(SEED, 1, addr, 1 << 20, fill=True)
+        ss.load_synthetic_shared(SEED, 1, addr, 1 << 20, fill=True)
     assert nbytes > (1 << 20)
     ss.close()
     del addr

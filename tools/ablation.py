@@ -1,7 +1,7 @@
 """NEXT-4: Table-2-style ablation ladder and App. F depth point on synthetic weights.
 
-Runs bench.py variants in fresh processes (engine flags are read at context creation) and writes
-profiles/ablation_<tag>.json.  Variants: full SubSpec; async transfer off (SS_STREAM_SERIAL=1: each
+Runs bench.py variants in fresh processes and writes
+profiles/ablation_<tag>.json.  Variants: full SubSpec; async transfer off (--no-async, ss_options.async_stream = 0: each
 streamed group is copied only after the previous group's compute); sharpening off
 (T = 1); a shallower tree (D = 24); and the offloading AR baseline through the same engine
 (D = 0, the paper's "None" row) for the speedup.  Shared-vs-separate draft KV is not built.
@@ -13,7 +13,7 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
 steps = ["--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
 variants = [
     ("full (D=48, k=6, T=0.2, async)", {}, []),
-    ("async transfer off", {"SS_STREAM_SERIAL": "1"}, []),
+    ("async transfer off", {}, ["--no-async"]),
     ("sharpening off (T=1)", {}, ["--temp", "1.0"]),
     ("shallower tree (D=24)", {}, ["--depth", "24"]),
     # 16 timed steps: the ring prefetched before the timed region is not hidden under a draft here

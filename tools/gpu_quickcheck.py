@@ -33,7 +33,7 @@ def main(cfgname="tiny"):
             if not np.array_equal(g.reshape(ref.shape), ref): bad.append(name)
         assert not bad, bad
     step("generator parity", gen)
-    step("load_weights", lambda: ss.load_weights(SEED, n_resident=1))
+    step("load_weights", lambda: ss.load_synthetic(SEED, n_resident=1))
     model = W.generate_model(cfg, SEED)
     def groups():
         for l in range(cfg.n_layers):

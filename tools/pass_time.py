@@ -6,7 +6,7 @@ from synth.prompts import mtbench_prompt
 from paper_2509_18344_b200.binding import SubSpec
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 ss = SubSpec(QWEN7B, 8 * GIB, max_depth=48, max_top_k=6)
-ss.load_weights(0x5EED, 0); ss.build_substitutes()
+ss.load_synthetic(0x5EED, 0); ss.build_substitutes()
 ss.prefill(mtbench_prompt(0x5EED, 0, QWEN7B.vocab))
 ss.debug_time_pass(M, 5, 0)
 ts = [ss.debug_time_pass(M, 20, 0) * 1e3 for _ in range(5)]

@@ -6,7 +6,7 @@ from synth.configs import QWEN7B, GIB
 from synth.prompts import mtbench_prompt
 from paper_2509_18344_b200.binding import SubSpec
 ss = SubSpec(QWEN7B, 8 * GIB, max_depth=48, max_top_k=6)
-ss.load_weights(0x5EED, 0); ss.build_substitutes()
+ss.load_synthetic(0x5EED, 0); ss.build_substitutes()
 ss.prefill(mtbench_prompt(0x5EED, 0, QWEN7B.vocab))
 for _ in range(3): ss.step(48, 6, 0.2)
 torch.cuda.synchronize()

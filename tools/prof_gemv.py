@@ -5,7 +5,7 @@ from synth.configs import QWEN7B, GIB
 from paper_2509_18344_b200.binding import SubSpec
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 ss = SubSpec(QWEN7B, 8 * GIB, max_depth=48, max_top_k=6)
-ss.load_weights(0x5EED, 0)
+ss.load_synthetic(0x5EED, 0)
 ss.build_substitutes()
 for g in (0, 2, 3, 1):
     t = ss.debug_time_matmul(-1, g, M, iters=1)

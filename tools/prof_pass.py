@@ -5,7 +5,7 @@ from synth.configs import QWEN7B, GIB
 from synth.prompts import mtbench_prompt
 from paper_2509_18344_b200.binding import SubSpec
 ss = SubSpec(QWEN7B, 8 * GIB, max_depth=48, max_top_k=6)
-ss.load_weights(0x5EED, 0); ss.build_substitutes()
+ss.load_synthetic(0x5EED, 0); ss.build_substitutes()
 ss.prefill(mtbench_prompt(0x5EED, 0, QWEN7B.vocab))
 for name, skip in (("full", 0), ("-attn", 1), ("-norm", 2), ("-gemv", 4), ("-head", 8), ("gemv+head only", 3), ("gemv only", 11), ("nothing", 15)):
     print(f"{name:16s} {ss.debug_time_pass(6, 5, skip) * 1e3:9.1f} us/pass", flush=True)

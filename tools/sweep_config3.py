@@ -21,7 +21,7 @@ Ks = [int(x) for x in os.environ.get("SWEEP_K", "1,2,4,6,8,16,32").split(",")]
 STEPS = int(os.environ.get("SWEEP_STEPS", "4"))
 cfg = LLAMA8B
 ss = SubSpec(cfg, 12 * GIB, max_depth=max(Ds), max_top_k=max(Ks), max_chunk=256)
-ss.load_weights(0x5EED, -1)
+ss.load_synthetic(0x5EED, -1)
 ss.build_substitutes(4, 64)
 st0 = ss.stats()
 print(json.dumps({"config": "llama-3.1-8b, 12 GiB, planner max residency", "n_resident": st0["n_resident"],
