@@ -12,110 +12,77 @@ namespace ss {
 constexpr int kTileRows = 128;      // weight rows per tile (one head at d_h = 128)
 constexpr int kChunkK = 128;        // K elements per tile-chunk
 constexpr int kQ4CodeBytes = 8192;  // 128 x 128 x 4 bit
-constexpr int kQ4MetaBytes = 1024;  // 128 rows x 2 groups x (s,z) bf16
+constexpr int kQ4MetaBytes = 1024;  // 2 groups x 128 rows x (s,z) bf16
 constexpr int kQ4TileBytes = kQ4CodeBytes + kQ4MetaBytes;   // 9216
 constexpr int kBF16TileBytes = kTileRows * kChunkK * 2;     // 32768
 constexpr int kXChunkBytesPerNT = 8 * kChunkK * 2;          // 2048: 8 tokens x 128 k bf16
 constexpr int kTraceEvents = 16;   // u64 %globaltimer events per traced launch (debug)
 
 // ---------------------------------------------------------------------------
-// Weight "tiled fragment" layout.
-// Matrix W [N x K] (N % 128 == 0, K % 128 == 0) is stored as tile-chunks
-// (r = n/128, c = k/128), index tc = r * (K/128) + c, each contiguous.
-// Inside a tile-chunk warp w (0..7) owns rows 16w..16w+15; lane = g*4 + t4 owns rows
-// 16w+g (h=0) and 16w+g+8 (h=1).  Within the chunk, k = 64*G + 16*t4 + i16 (G = 64-group,
-// i16 = 0..15), so every mma.m16n8k16 k-step st = 4*G + i16/4 stays inside one quant group.
+// Core-matrix layouts.  A core matrix is 8 rows x 8 consecutive k
+// (bf16, 16 B per row, 128 B contiguous): the unit of both `ldmatrix` (one 8-lane phase) and the
+// tcgen05 K-major SWIZZLE_NONE shared-memory descriptor (LBO = K-direction core stride, SBO =
+// row-group stride).  A 128-k chunk of 8*R rows holds core (rg, kg) at ((rg * 16 + kg) * 128) bytes,
+// so LBO = 128 B and SBO = 2048 B for every operand below, and advancing K by 16 is +256 B.
 // ---------------------------------------------------------------------------
-struct KPos {
-  int G, t4, i16, st, j;
-};
-SS_HD KPos kpos(int64_t k) {
-  const int kk = int(k & 127);
-  KPos p;
-  p.G = kk >> 6;
-  p.t4 = (kk & 63) >> 4;
-  p.i16 = kk & 15;
-  p.st = 4 * p.G + (p.i16 >> 2);
-  p.j = p.i16 & 3;
-  return p;
-}
-// byte offset, inside a bf16 tile-chunk, of the 16-byte piece q (= 2*G + half) of (warp w, row half h,
-// lane): group-major, so each 64-k half of a tile-chunk (16 KB) is contiguous.
-SS_HD int bf16_piece_off(int w, int h, int q, int lane) {
-  return (((((q >> 1) * 8 + w) * 2 + h) * 2 + (q & 1)) * 32 + lane) * 16;
-}
+SS_HD uint32_t core_off(int rg, int kg, int r, int e) { return uint32_t(((rg * 16 + kg) * 64 + r * 8 + e) * 2); }
+
+// bf16 weights W [N x K] (N % 128 == 0, K % 128 == 0): tile-chunks (row tile n/128, chunk k/128),
+// index tc = (n/128) * (K/128) + k/128, 32 KB each, core matrices inside as above.
 SS_HD uint64_t bf16_tiled_offset(int64_t n, int64_t k, int64_t K) {   // in bytes
   const int64_t tc = (n >> 7) * (K >> 7) + (k >> 7);
-  const int nn = int(n & 127);
-  const int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
-  const KPos p = kpos(k);
-  const int q = 2 * p.G + (p.i16 >> 3), e = p.i16 & 7;
-  const int lane = g * 4 + p.t4;
-  return uint64_t(tc) * kBF16TileBytes + uint64_t(bf16_piece_off(w, h, q, lane) + e * 2);
+  const int nn = int(n & 127), kk = int(k & 127);
+  return uint64_t(tc) * kBF16TileBytes + core_off(nn >> 3, kk >> 3, nn & 7, kk & 7);
 }
 
-// Q4: per (warp w, group G, lane) 16 bytes = [row g: word0, word1][row g+8: word0, word1];
-// word holds i16 = 8*word .. +7; code c8 = i16 % 8 lives in nibble slot (c8%2)*4 + c8/2, so
-// (word >> 4p) & 0x000F000F yields the bf16x2 pair (c_2p, c_2p+1).
-// Meta (4 B: s bf16 lo, z bf16 hi) at 8192 + ((w*2 + G)*16 + row_in_warp) * 4.
+// Q4 substitutes (tcgen05 K2): per tile-chunk, for 64-group G (k = 64G .. 64G + 63 of the chunk),
+// codes at G * 4096 + half * 2048 + row * 16 (16 B = the 32 codes k = 64G + 32 half + 0..31 of one
+// row; word j holds k = 8j .. 8j + 7 of the half: the code of k = 8j + 2p sits at bits 4p..4p+3 and
+// that of k = 8j + 2p + 1 at bits 16 + 4p.., so (word >> 4p) & 0x000F000F is the pair's bf16x2
+// mantissa bits), then meta (s bf16 lo16, z bf16 hi16) at 8192 + G * 512 + row * 4.
 SS_HD uint64_t q4_tile_base(int64_t n, int64_t k, int64_t K) {
   return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ4TileBytes;
 }
 SS_HD void q4_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
-  const int nn = int(n & 127);
-  const int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
-  const KPos p = kpos(k);
-  const int lane = g * 4 + p.t4;
-  const int word = p.i16 >> 3, c8 = p.i16 & 7;
-  const int slot = (c8 & 1) * 4 + (c8 >> 1);
-  const uint64_t wordoff = q4_tile_base(n, k, K) + uint64_t(((w * 2 + p.G) * 32 + lane) * 16 + h * 8 + word * 4);
-  *byte_off = wordoff + (slot >> 1);
-  *shift = (slot & 1) * 4;
+  const int row = int(n & 127), kk = int(k & 127);
+  const int G = kk >> 6, half = (kk >> 5) & 1, j = (kk >> 3) & 3, q = kk & 7, p = q >> 1;
+  const int bit = (q & 1) * 16 + 4 * p;
+  *byte_off = q4_tile_base(n, k, K) + uint64_t(G * 4096 + half * 2048 + row * 16 + j * 4 + (bit >> 3));
+  *shift = bit & 7;
 }
 SS_HD uint64_t q4_meta_offset(int64_t n, int64_t k, int64_t K) {     // bytes; 4 B (s lo16, z hi16)
-  const int nn = int(n & 127);
-  const int w = nn >> 4, rr = nn & 15;
-  return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((w * 2 + kpos(k).G) * 16 + rr) * 4);
+  return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((k & 127) >> 6) * 512 + (n & 127) * 4);
 }
 
-// Q2 (NEXT-3, 2-bit substitutes): per (warp w, group G, lane) 8 bytes = [row g word][row g+8 word];
-// the word holds i16 = 0..15 of the lane's 16 k of group G: code i16 lives in bits
-// (i16 % 2) * 16 + 2 * (i16 / 2), so (word >> 2p) & 0x00030003 yields the bf16x2 pair
-// (c_2p, c_2p+1) — k-step k4 uses pairs 2 k4 (a0/a1) and 2 k4 + 1 (a2/a3).
-// Meta as Q4, at kQ2CodeBytes + ((w*2 + G)*16 + row_in_warp) * 4.
+// Q2 (NEXT-3, 2-bit substitutes): per 64-group G, codes at G * 2048 + row * 16 (16 B = the row's 64
+// codes; word j holds k = 16j .. 16j + 15: k = 16j + 2p at bits 2p, k = 16j + 2p + 1 at bits 16 + 2p,
+// so (word >> 2p) & 0x00030003 is a pair), meta as Q4 at kQ2CodeBytes + G * 512 + row * 4.
 constexpr int kQ2CodeBytes = 4096;  // 128 x 128 x 2 bit
 constexpr int kQ2TileBytes = kQ2CodeBytes + kQ4MetaBytes;   // 5120
 SS_HD int qtile_bytes(int bits) { return bits == 2 ? kQ2TileBytes : kQ4TileBytes; }
 SS_HD int qcode_bytes(int bits) { return bits == 2 ? kQ2CodeBytes : kQ4CodeBytes; }
 SS_HD void q2_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
-  const int nn = int(n & 127);
-  const int w = nn >> 4, rr = nn & 15, h = rr >> 3, g = rr & 7;
-  const KPos p = kpos(k);
-  const int lane = g * 4 + p.t4;
-  const int bit = (p.i16 & 1) * 16 + 2 * (p.i16 >> 1);
-  const uint64_t wordoff = uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes +
-                           uint64_t(((w * 2 + p.G) * 32 + lane) * 8 + h * 4);
-  *byte_off = wordoff + (bit >> 3);
+  const int row = int(n & 127), kk = int(k & 127);
+  const int G = kk >> 6, j = (kk >> 4) & 3, q = kk & 15, p = q >> 1;
+  const int bit = (q & 1) * 16 + 2 * p;
+  *byte_off = uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes + uint64_t(G * 2048 + row * 16 + j * 4 + (bit >> 3));
   *shift = bit & 7;
 }
 SS_HD uint64_t q2_meta_offset(int64_t n, int64_t k, int64_t K) {
-  const int nn = int(n & 127);
-  const int w = nn >> 4, rr = nn & 15;
   return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes + kQ2CodeBytes +
-         uint64_t(((w * 2 + kpos(k).G) * 16 + rr) * 4);
+         uint64_t(((k & 127) >> 6) * 512 + (n & 127) * 4);
 }
 
 // ---------------------------------------------------------------------------
-// FragX activation layout: X [Mpad x K] bf16, Mpad % 8 == 0, NT = Mpad/8.
-// Chunk c (128 k) of all NT n-tiles is contiguous (NT * 2 KB); within it
-// offset(m,k) = ((((c*NT + nt)*8 + st)*4 + t4)*8 + g)*4 + j  with (st, t4, j) = kpos(k),
-// nt = m/8, g = m%8: the 8 bytes lane (g, t4) needs for k-step st are contiguous.
+// Activation layout ("FragX", now core-matrix): X [Mpad x K] bf16, Mpad % 8 == 0, NT = Mpad / 8 token
+// groups.  Chunk c (128 k) of all NT token groups is contiguous (NT * 2 KB); inside it token group tg
+// holds core (tg, kg) at ((tg * 16 + kg) * 64) elements, so the B operand of a tcgen05 MMA (N = 8 NT
+// tokens, K-major) and the mma.sync B fragments (ldmatrix) read it directly.  offset in elements.
 // ---------------------------------------------------------------------------
 SS_HD int64_t fragx_offset(int64_t m, int64_t k, int NT) {
   const int64_t c = k >> 7;
-  const KPos p = kpos(k);
-  const int nt = int(m >> 3), g = int(m & 7);
-  return ((((c * NT + nt) * 8 + p.st) * 4 + p.t4) * 8 + g) * 4 + p.j;
+  const int kk = int(k & 127);
+  return ((c * NT + (m >> 3)) * 16 + (kk >> 3)) * 64 + (m & 7) * 8 + (kk & 7);
 }
 
 // ---------------------------------------------------------------------------
@@ -137,15 +104,27 @@ SS_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 SS_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
+SS_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return done != 0;
+}
+// wait for the phase with this parity; a watchdog traps after ~4 s instead of hanging the GPU
+SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try_wait(addr, parity)) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 4000000000ull) __trap();
+  }
 }
 // (x & 0x000F000F) | magic in ONE lop3 (C++ "(x & a) | b" becomes two LOP3s with immediates)
 SS_DEV uint32_t lop3_and_or(uint32_t x, uint32_t magic) {
@@ -190,6 +169,81 @@ SS_DEV void mma_bf16_16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// ldmatrix: four 8x8 b16 core matrices; lane L supplies the row address of matrix L / 8
+SS_DEV void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(saddr));
+}
+
+// ---- tcgen05 (5th-generation tensor core, TMEM) --------------------------------------------
+// shared-memory matrix descriptor, K-major, SWIZZLE_NONE (canonical core-matrix layout above)
+SS_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);   // version 1 (sm_100), layout 0
+}
+// instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major, M = 128, N
+SS_HD constexpr uint32_t umma_idesc_bf16(int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] * B[smem]   (A: 128 lanes = rows, K = 16 bf16 in 8 columns)
+SS_DEV void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// D[tmem] (+)= A[smem] * B[smem]
+SS_DEV void umma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// arrive on an mbarrier when every tcgen05.mma issued so far by this thread has completed
+SS_DEV void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+SS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SS_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {   // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+SS_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {   // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// this warp's 32 TMEM lanes, 32 consecutive 32-bit columns from taddr
+SS_DEV void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+SS_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+SS_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+SS_DEV void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+SS_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
 }
 
 SS_DEV float bf2f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }

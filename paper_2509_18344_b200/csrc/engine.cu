@@ -183,10 +183,8 @@ size_t q4_bytes(int N, int K) { return size_t(N / 128) * (K / 128) * kQ4TileByte
 size_t sub_bytes(int N, int K, int bits) { return size_t(N / 128) * (K / 128) * size_t(qtile_bytes(bits)); }
 size_t bf16_bytes(int N, int K) { return size_t(N) * K * 2; }
 
-// token tiles of 8 for a draft GEMV over M <= 32 rows: M = 17..24 (e.g. 4 batched requests x k = 6)
-// uses 3 tiles, since the legacy MMA pipe time grows with the tile count
-int gemv_nt(int M) { return M <= 8 ? 1 : (M <= 16 ? 2 : (M <= 24 ? 3 : 4)); }
-int gemv_nt_pow2(int M) { return M <= 8 ? 1 : (M <= 16 ? 2 : 4); }   // the persistent pass (pass.cu)
+// token groups of 8 for a draft GEMV over M <= 32 rows: the tcgen05 MMA's N is 16 or 32 (M = 128)
+int gemv_nt(int M) { return M <= 16 ? 2 : 4; }
 int gemm_nt(int M) { return ((M + 127) / 128) * 16; }
 
 // ---------------------------------- K7 streaming ------------------------------------------
@@ -335,7 +333,7 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.NT = gemv_nt(M);
     p.partials = c->gv_part;
     p.counters = c->gv_cnt;
-    p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+    p.max_seg = gemv_max_segments(N, K, gemv_streamk_grid(!w.resident, N, K, c->gv_grid));
     p.epi = epi;
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
     // qkv substitutes: plan one CTA per SM.  Its whole per-CTA weight range (9.3 MB / 144 CTAs =
@@ -516,7 +514,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
       p.NT = gemv_nt(m);
       p.partials = c->gv_part;
       p.counters = c->gv_cnt;
-      p.max_seg = gemv_max_segments(c->V, c->H, c->gv_grid);
+      p.max_seg = gemv_max_segments(c->V, c->H, gemv_streamk_grid(false, c->V, c->H, c->gv_grid));
       p.epi = base_epi(c, m);
       p.epi.kind = EPI_LOGITS;
       p.epi.out = c->logits;
@@ -839,7 +837,8 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   int max_tiles = 0;
   for (int g = 0; g < 5; ++g) {
     const int N = g < 4 ? c->gN[g] : c->V, K = g < 4 ? c->gK[g] : c->H;
-    gvf = std::max(gvf, size_t(N / 128) * gemv_max_segments(N, K, c->gv_grid) * 128 * 32);
+    for (int q4 = 0; q4 < 2; ++q4)
+      gvf = std::max(gvf, size_t(N / 128) * gemv_max_segments(N, K, gemv_streamk_grid(q4, N, K, c->gv_grid)) * 128 * 32);
     max_tiles = std::max(max_tiles, N / 128);
   }
   c->gv_part_floats = gvf;
@@ -1649,7 +1648,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
     p.NT = NT;
     p.partials = c->gv_part;
     p.counters = c->gv_cnt;
-    p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+    p.max_seg = gemv_max_segments(N, K, gemv_streamk_grid(!w.resident, N, K, c->gv_grid));
     p.epi = e;
     p.qbits = c->sub_bits;
     p.ctas_per_sm = (group == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
@@ -1702,7 +1701,7 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.NT = gemv_nt(M);
     p.partials = c->gv_part;
     p.counters = c->gv_cnt;
-    p.max_seg = gemv_max_segments(N, K, c->gv_grid);
+    p.max_seg = gemv_max_segments(N, K, gemv_streamk_grid(!head && !w.resident, N, K, c->gv_grid));
     p.epi = base_epi(c, M);
     p.epi.kind = EPI_STORE;
     p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
@@ -1884,7 +1883,7 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
       p.NT = gemv_nt(m);
       p.partials = c->gv_part;
       p.counters = c->gv_cnt;
-      p.max_seg = gemv_max_segments(c->V, c->H, c->gv_grid);
+      p.max_seg = gemv_max_segments(c->V, c->H, gemv_streamk_grid(false, c->V, c->H, c->gv_grid));
       p.epi = base_epi(c, m);
       p.epi.kind = EPI_LOGITS;
       p.epi.out = c->logits;

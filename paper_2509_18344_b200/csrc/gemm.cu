@@ -63,22 +63,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(const GemmParams 
     for (int i = 0; i < nC; ++i) {
       const int s = i % kGemmStages;
       mbar_wait(&full[s], uint32_t(i / kGemmStages) & 1);
-      const uint8_t* wst = ring + s * kGemmStageBytes;
-      const uint8_t* xst = wst + kBF16TileBytes;
+      const uint32_t wst = smem_u32(ring + s * kGemmStageBytes);
+      const uint32_t xst = wst + kBF16TileBytes;
+      // lane L addresses row L % 8 of core matrix L / 8 (ldmatrix.x4)
+      const int lq = lane >> 3, lr = lane & 7;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 r0 = *reinterpret_cast<const uint4*>(wst + bf16_piece_off(warp, 0, q, lane));
-        const uint4 r1 = *reinterpret_cast<const uint4*>(wst + bf16_piece_off(warp, 1, q, lane));
+      for (int s2 = 0; s2 < 8; s2 += 2) {   // two k-steps of 16 per iteration
+        uint32_t a[2][4];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int st = 2 * q + hh;
-          const uint32_t a0 = hh ? r0.z : r0.x, a2 = hh ? r0.w : r0.y;
-          const uint32_t a1 = hh ? r1.z : r1.x, a3 = hh ? r1.w : r1.y;
+        for (int h = 0; h < 2; ++h)        // A: rows 16 warp .. +15 (row groups 2w, 2w+1), k-step s2 + h
+          ldsm_x4(a[h][0], a[h][1], a[h][2], a[h][3], wst + core_off(2 * warp + (lq & 1), 2 * (s2 + h) + (lq >> 1), lr, 0));
 #pragma unroll
-          for (int j = 0; j < kGemmTokNT; ++j) {
-            const uint2 b = *reinterpret_cast<const uint2*>(xst + ((((j * 8 + st) * 4 + t4) * 8 + g) * 8));
-            mma_bf16_16816(acc[j], a0, a1, a2, a3, b.x, b.y);
-          }
+        for (int j = 0; j < kGemmTokNT; ++j) {
+          uint32_t b0, b1, b2, b3;           // B: token group j, k-steps s2 (b0, b1) and s2 + 1 (b2, b3)
+          ldsm_x4(b0, b1, b2, b3, xst + core_off(j, 2 * s2 + lq, lr, 0));
+          mma_bf16_16816(acc[j], a[0][0], a[0][1], a[0][2], a[0][3], b0, b1);
+          mma_bf16_16816(acc[j], a[1][0], a[1][1], a[1][2], a[1][3], b2, b3);
         }
       }
       __syncwarp();

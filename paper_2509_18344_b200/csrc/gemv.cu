@@ -48,21 +48,26 @@ int gemv_max_segments(int N, int K, int grid) {
   return mx;
 }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4>
-__global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(const GemvParams p) {
-  constexpr int CW = kGemvConsumerWarps;
-  using C = GemvCfg<Q4, NT, QB>;
+template <int WF, int NT, bool kCluster>
+__global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(const GemvParams p) {
+  using C = GemvCfg<WF, NT>;
+  constexpr int kN = C::kN;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int kStages = p.stages;
   uint8_t* ring = smem;
   float* otile = reinterpret_cast<float*>(smem + kStages * C::kStageBytes);
   float* staging = otile + C::kTileFloats;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes + (C::kTileFloats + C::kStagingFloats) * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStagingFloats);
   uint64_t* empty = full + C::kMaxStages;
-  int* flag = reinterpret_cast<int*>(empty + C::kMaxStages);
+  uint64_t* a_full = empty + C::kMaxStages;
+  uint64_t* a_empty = a_full + C::kASlots;
+  uint64_t* d_full = a_empty + C::kASlots;
+  uint64_t* d_empty = d_full + C::kDSlots;
+  uint64_t* xbar = d_empty + C::kDSlots;                         // residual-row prefetch
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 1);
+  int* flag = reinterpret_cast<int*>(xbar + 2);
   float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(flag) + 4;      // x prefetch barrier (in the flag block)
-  float* xpre = scratch + 128;                                  // [kXPreFloats] residual rows
+  float* xpre = scratch + 128;                                    // [kXPreFloats] residual rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SS_TRACE_MIN(0);
@@ -75,7 +80,6 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   }
   const int nC = p.K >> 7;
   const int64_t T = int64_t(p.N >> 7) * nC;
-  const int Mpad = NT * 8;
   uint32_t crank = 0, csize = 1;
   if constexpr (kCluster) {
     crank = cluster_rank();
@@ -84,16 +88,31 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CW);
+      mbar_init(&empty[s], C::kQ ? 9 : 1);   // Q: MMA commit + 4 convert + 4 accumulate warps
+    }
+    for (int j = 0; j < C::kASlots; ++j) {
+      mbar_init(&a_full[j], 4);
+      mbar_init(&a_empty[j], 1);
+    }
+    for (int j = 0; j < C::kDSlots; ++j) {
+      mbar_init(&d_full[j], 1);
+      mbar_init(&d_empty[j], 4);
     }
     mbar_init(xbar, 1);
     fence_barrier_init();
   }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
   __syncthreads();
-  griddep_launch();   // grid <= one CTA per SM: let the next kernel prefetch now
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  griddep_launch();   // grid <= the resident CTAs: let the next kernel prefetch now
+  // a CTA with two or more tiles in a cluster of > 1 would need one cluster barrier per tile from
+  // every warp; the launcher only plans clusters of one tile each (csize > 1) or csize == 1
+  const bool cl_sync = kCluster && csize > 1;
 
-  if (warp == CW) {
-    // ------------------------------ producer -------------------------------
+  if (warp == 0) {
+    // ------------------------------ producer (TMA) -------------------------------
     Work w = make_work<kCluster>(p.N, p.K, crank, csize);
     const int64_t n_stage = w.stages(nC, C::kCPS);
     if (lane == 0) {
@@ -109,8 +128,8 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
       auto issue_x = [&](int st, const Work& ww, int n) {
         uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
         bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
-        if constexpr (Q4)
-          bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * NT * 8, uint32_t(n) * C::kSBytes, &full[st]);
+        if constexpr (C::kQ)
+          bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * kN, uint32_t(n) * C::kSBytes, &full[st]);
       };
       // weights do not depend on the previous kernel: issue before the grid-dependency wait
       for (int i = 0; i < pre; ++i) {
@@ -118,18 +137,13 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         issue_w(i, w, n);
         w.next(nC, n);
       }
-      // L2 prefetch of the next matrix (independent of every activation): this CTA's slice, in
-      // 64 KB TMA prefetches, so HBM keeps streaming through the dependent steps that follow
-      auto prefetch_next = [&]() {
+      // L2 prefetch of the next matrix (independent of every activation): this CTA's slice
+      if (p.pf && p.pf_bytes > 0) {
         const int64_t per = ((p.pf_bytes / gridDim.x) + 15) & ~int64_t(15);
         const int64_t b0 = per * blockIdx.x;
         const int64_t b1 = b0 + per < p.pf_bytes ? b0 + per : p.pf_bytes;
-        for (int64_t o = b0; o < b1; o += 65536) {
-          const int64_t n = b1 - o < 65536 ? b1 - o : 65536;
-          prefetch_l2(p.pf + o, uint32_t(n));
-        }
-      };
-      if (p.pf && p.pf_bytes > 0) prefetch_next();
+        for (int64_t o = b0; o < b1; o += 65536) prefetch_l2(p.pf + o, uint32_t(b1 - o < 65536 ? b1 - o : 65536));
+      }
       griddep_wait();
       SS_TRACE_CTA0(1);
       for (int i = 0; i < pre; ++i) {
@@ -151,125 +165,186 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
         }
       }
     }
-    if constexpr (kCluster) {
-      if (csize > 1) {   // take part in the cluster barriers of every tile's reduction
-        const int64_t per = int64_t(w.c_end - w.c_begin);
-        const int64_t tiles = per ? w.left / per : 0;
-        for (int64_t t = 0; t < tiles; ++t) {
-          cluster_sync_all();
-          if (t + 1 < tiles) cluster_sync_all();
-        }
-      }
-    }
+    __syncwarp();
+    if (cl_sync) cluster_sync_all();
     return;
   }
 
-  // ------------------------------ consumers --------------------------------
-  griddep_wait();
-  if (threadIdx.x == 0) SS_TRACE_CTA0(2);
-  const int g = lane >> 2, t4 = lane & 3;
-  const int nthr = CW * 32;
-  float acc[NT][4];
+  if (warp == 1) {
+    // ------------------------------ MMA issuer -------------------------------
+    Work w = make_work<kCluster>(p.N, p.K, crank, csize);
+    if (lane == 0) {
+      griddep_wait();   // acquire side of the activations' dependency for the async proxy reads
+      constexpr uint32_t idesc = umma_idesc_bf16(kN);
+      int s = 0;
+      uint32_t ph = 0;
+      int ja = 0, jd = 0;
+      uint32_t ua[C::kASlots] = {}, ud[C::kDSlots] = {};
+      while (w.left > 0) {
+        const int cur_r = w.r;
+        bool first = true;
+        do {
+          const int nch = w.take(C::kCPS);
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sb = smem_u32(ring + s * C::kStageBytes);
+          const uint32_t xb = sb + C::kCPS * C::kWBytes;
+          w.next(nC, nch);
+          const bool last = w.left == 0 || w.r != cur_r;
+          if constexpr (C::kQ) {
+            for (int ci = 0; ci < nch; ++ci)
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+              for (int G = 0; G < 2; ++G) {
+                mbar_wait(&a_full[ja], ua[ja] & 1);
+                mbar_wait(&d_empty[jd], (ud[jd] & 1) ^ 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_ts(tbase + jd * kN, tbase + C::kACol0 + ja * 32 + kk * 8,
+                          umma_desc(xb + ci * C::kXBytes + G * 1024 + kk * 256, 128, 2048), idesc, kk > 0);
+                umma_commit(&a_empty[ja]);
+                umma_commit(&d_full[jd]);
+                ++ua[ja];
+                ++ud[jd];
+                ja = (ja + 1) % C::kASlots;
+                jd = (jd + 1) % C::kDSlots;
+              }
+          } else {
+            if (first) {
+              mbar_wait(&d_empty[jd], (ud[jd] & 1) ^ 1);
+              tc_fence_after();
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_ss(tbase + jd * kN, umma_desc(sb + kk * 256, 128, 2048), umma_desc(xb + kk * 256, 128, 2048), idesc,
+                      (first && kk == 0) ? 0u : 1u);
+            if (last) {
+              umma_commit(&d_full[jd]);
+              ++ud[jd];
+              jd = (jd + 1) % C::kDSlots;
+            }
+          }
+          umma_commit(&empty[s]);
+          first = false;
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        } while (w.left > 0 && w.r == cur_r);
+      }
+    }
+    __syncwarp();
+    named_bar(3, 160);   // the accumulate warps have read the last accumulator
+    tc_fence_after();
+    tmem_dealloc(tbase, C::kTmemCols);
+    if (cl_sync) cluster_sync_all();
+    return;
+  }
 
-  auto stash = [&](float* dst) { stash_acc<NT>(acc, dst, warp, lane); };   // [128][Mpad] partial tile
+  // ---------------------------- worker warps 2..9 ----------------------------
+  griddep_wait();
+  const int tid = threadIdx.x - 64;             // 0..255 over the worker warps
+  const int q = warp & 3;                       // TMEM lane quadrant of this warp
+  const int row = 32 * q + lane;                // weight row of the tile owned in TMEM
+  const uint32_t tl = tbase + (uint32_t(32 * q) << 16);
+  const bool is_convert = warp < 6;
+  const int Mv = p.epi.M < kN ? p.epi.M : kN;   // valid tokens
 
   uint32_t xph = 0;   // phase of xbar
+  // --- split-K reduction + epilogue of tile r from otile (worker threads only) ---
   auto flush = [&](int r, int c_first, int c_last, bool last) {
+    const int nthr = kGemvWorkers;
     if constexpr (kCluster) {
       if (csize == 1) {
-        stash(otile);
         named_bar(1, nthr);
-        if (threadIdx.x == 0) SS_TRACE_MAX(8);
-        apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr, scratch, p.trace, 1, true, Mpad);
+        if (tid == 0) SS_TRACE_MAX(8);
+        apply_epilogue(p.epi, otile, kN, r, 0, kN, tid, nthr, scratch, p.trace, 1, true, kN);
         named_bar(1, nthr);
         return;
       }
       // Split-K reduction spread over the cluster: rank q owns token columns [mlo, mhi) of the tile.
-      // Every rank stashes its partial tile token-major, pushes each owner's columns into the owner's
-      // staging buffer with 16-byte distributed-shared-memory stores, and after ONE cluster barrier
-      // each owner sums its staging in rank order (deterministic) and runs the epilogue for its
-      // tokens (one arrival per rank at EPI_RESID_NORM's barrier; only rank 0 waits there and
-      // normalises, so ranks 1..S-1 exit and the barrier never needs whole clusters co-resident).
+      // Every rank has its partial tile token-major in otile, pushes each owner's columns into the
+      // owner's staging buffer with 16-byte distributed-shared-memory stores, and after ONE cluster
+      // barrier each owner sums its staging in rank order (deterministic) and runs the epilogue for
+      // its tokens (one arrival per rank at EPI_RESID_NORM's barrier; only rank 0 waits there).
       const int S = int(csize);
-      const int mlo = int(crank) * Mpad / S, mhi = int(crank + 1) * Mpad / S;
-      const int nc = mhi - mlo, ncmax = (Mpad + S - 1) / S;
-      // residual epilogues: TMA-load the owned tokens' residual rows of this tile now, so the
-      // epilogue's read-modify-write does not pay an L2 round trip after the reduction
+      const int mlo = int(crank) * kN / S, mhi = int(crank + 1) * kN / S;
+      const int nc = mhi - mlo, ncmax = (kN + S - 1) / S;
       const int nvalid = nc < p.epi.M - mlo ? nc : (p.epi.M - mlo > 0 ? p.epi.M - mlo : 0);
-      const bool xp = nvalid > 0 && nc <= C::kXPreTokens &&
-                      (p.epi.kind == EPI_RESID || p.epi.kind == EPI_RESID_NORM);
-      if (xp && threadIdx.x == 0) {
+      const bool xp = nvalid > 0 && nc <= C::kXPreTokens && (p.epi.kind == EPI_RESID || p.epi.kind == EPI_RESID_NORM);
+      if (xp && tid == 0) {
         mbar_arrive_expect_tx(xbar, uint32_t(nvalid) * kTileRows * 4);
         for (int m = 0; m < nvalid; ++m)
           bulk_g2s(xpre + m * kTileRows, p.epi.x + int64_t(mlo + m) * p.epi.ldx + int64_t(r) * kTileRows, kTileRows * 4, xbar);
       }
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {   // token-major [Mpad][128] partial tile
-        const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
-        otile[m * kTileRows + n0] = acc[j][0];
-        otile[(m + 1) * kTileRows + n0] = acc[j][1];
-        otile[m * kTileRows + n0 + 8] = acc[j][2];
-        otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
-        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-      }
       named_bar(1, nthr);
-      for (int i = threadIdx.x; i < Mpad * (kTileRows / 4); i += nthr) {
+      for (int i = tid; i < kN * (kTileRows / 4); i += nthr) {
         const int m = i / (kTileRows / 4), n4 = (i % (kTileRows / 4)) * 4;
-        const int q = int(owner_of(m, Mpad, S));          // owner rank of token m
-        const int mm = m - q * Mpad / S;
-        st_dsmem_f32x4(staging + (crank * ncmax + mm) * kTileRows + n4, uint32_t(q),
+        const int qo = int(owner_of(m, kN, S));          // owner rank of token m
+        const int mm = m - qo * kN / S;
+        st_dsmem_f32x4(staging + (crank * ncmax + mm) * kTileRows + n4, uint32_t(qo),
                        *reinterpret_cast<const float4*>(otile + m * kTileRows + n4));
       }
       cluster_sync_all();                         // every push landed (release / acquire)
-      for (int it = threadIdx.x; it < kTileRows * nc; it += nthr) {
+      for (int it = tid; it < kTileRows * nc; it += nthr) {
         const int n = it % kTileRows, mm = it / kTileRows;
         float v = staging[mm * kTileRows + n];
-        for (int q = 1; q < S; ++q) v += staging[(q * ncmax + mm) * kTileRows + n];
+        for (int qq = 1; qq < S; ++qq) v += staging[(qq * ncmax + mm) * kTileRows + n];
         otile[n * nc + mm] = v;                   // [128][nc] for the epilogue
       }
-      if (!last) cluster_sync_all();              // staging is reused by the next tile's pushes
       named_bar(1, nthr);
-      if (threadIdx.x == 0) SS_TRACE_MAX(8);
+      if (tid == 0) SS_TRACE_MAX(8);
       if (xp) {
         mbar_wait(xbar, xph);
         xph ^= 1;
       }
-      apply_epilogue(p.epi, otile, nc, r, mlo, nc, threadIdx.x, nthr, scratch, p.trace, S, crank == 0, Mpad, nullptr,
+      apply_epilogue(p.epi, otile, nc, r, mlo, nc, tid, nthr, scratch, p.trace, S, crank == 0, kN, nullptr,
                      xp ? xpre : nullptr);
       named_bar(1, nthr);
       return;
     } else {
       const bool complete = (c_first == 0 && c_last == nC - 1);
-      if (complete) {
-        stash(otile);
-      } else {
+      named_bar(1, nthr);
+      if (!complete) {
         const int G = gridDim.x;
         const int64_t first = owner_of(int64_t(r) * nC, T, G);
         const int64_t nseg = owner_of(int64_t(r + 1) * nC - 1, T, G) - first + 1;
         const int64_t slot = blockIdx.x - first;
-        stash(p.partials + (int64_t(r) * p.max_seg + slot) * int64_t(kTileRows * Mpad));
+        float* dst = p.partials + (int64_t(r) * p.max_seg + slot) * int64_t(kTileRows * kN);
+        for (int e = tid; e < kTileRows * kN; e += nthr) dst[e] = otile[e];
         __threadfence();
         named_bar(1, nthr);
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
           const int old = atomicAdd(&p.counters[r], 1);
           *flag = (old == nseg - 1);
         }
         named_bar(1, nthr);
         if (!*flag) return;
         __threadfence();
-        const float* base = p.partials + int64_t(r) * p.max_seg * int64_t(kTileRows * Mpad);
-        for (int e = threadIdx.x; e < kTileRows * Mpad; e += nthr) {
-          float s = 0.f;
-          for (int q = 0; q < nseg; ++q) s += __ldcg(base + q * int64_t(kTileRows * Mpad) + e);
-          otile[e] = s;
+        const float* base = p.partials + int64_t(r) * p.max_seg * int64_t(kTileRows * kN);
+        for (int e = tid; e < kTileRows * kN; e += nthr) {
+          float sum = 0.f;
+          for (int qq = 0; qq < nseg; ++qq) sum += __ldcg(base + qq * int64_t(kTileRows * kN) + e);
+          otile[e] = sum;
         }
-        if (threadIdx.x == 0) p.counters[r] = 0;
+        if (tid == 0) p.counters[r] = 0;
+        named_bar(1, nthr);
       }
+      apply_epilogue(p.epi, otile, kN, r, 0, kN, tid, nthr);
       named_bar(1, nthr);
-      apply_epilogue(p.epi, otile, Mpad, r, 0, Mpad, threadIdx.x, nthr);
-      named_bar(1, nthr);
+    }
+  };
+  // the accumulated rows of the tile -> otile: token-major [N][128] in cluster mode (the push layout),
+  // row-major [128][N] otherwise (the epilogue / Stream-K partial layout)
+  auto to_otile = [&](const float (&y)[kN]) {
+#pragma unroll
+    for (int t = 0; t < kN; ++t) {
+      if constexpr (kCluster) {
+        if (csize > 1) otile[t * kTileRows + row] = y[t];
+        else otile[row * kN + t] = y[t];
+      } else {
+        otile[row * kN + t] = y[t];
+      }
     }
   };
 
@@ -277,39 +352,145 @@ __global__ void __launch_bounds__(kGemvThreads, SS_GEMV_MIN_BLOCKS) gemv_kernel(
   const int64_t n_items = w.left;
   int s = 0;
   uint32_t ph = 0;
-  // Outer loop over this CTA's row tiles, inner loop over the tile's stages: the inner loop is a
-  // compact basic-block chain and the (large) reduction/epilogue code sits after it, so the hot
-  // path never jumps across the flush code (ncu: the single-loop form lost ~20% of the consumer's
-  // issue slots to instruction-fetch stalls on two far branches per stage).
+  int ja = 0, jd = 0;
+  uint32_t ua[C::kASlots] = {}, ud[C::kDSlots] = {};
+  const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128): 128 + code is exact in bf16
   while (w.left > 0) {
     const int cur_r = w.r, c_first = w.c;
     int c_last = w.c;
+    float y[kN];
+#pragma unroll
+    for (int t = 0; t < kN; ++t) y[t] = 0.f;
     do {
       const int nch = w.take(C::kCPS);
       c_last = w.c + nch - 1;
-      mbar_wait(&full[s], ph);
-      if (threadIdx.x == 0 && w.left == n_items) {
+      const uint8_t* stage = ring + s * C::kStageBytes;
+      if (C::kQ) mbar_wait(&full[s], ph);   // bf16: the MMAs read the stage, the workers only the accumulator
+      if (threadIdx.x == 64 && w.left == n_items) {
         SS_TRACE_CTA0(3);
         if (ct) ct[2] = gtime();
       }
-      consume_stage<Q4, NT, QB>(ring + s * C::kStageBytes, nch, acc, warp, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      w.next(nC, nch);
+      const bool last_of_tile = w.left == 0 || w.r != cur_r;
+      if constexpr (C::kQ) {
+        if (is_convert) {
+          // ---- codes of row `row` -> exact bf16 (128 + code) pairs -> TMEM A slot (32 columns) ----
+          for (int ci = 0; ci < nch; ++ci)
+#pragma unroll
+            for (int G = 0; G < 2; ++G) {
+              const uint8_t* wst = stage + ci * C::kWBytes;
+              uint32_t v[32];
+              if constexpr (WF == 4) {
+                const uint4 c0 = *reinterpret_cast<const uint4*>(wst + G * 4096 + row * 16);
+                const uint4 c1 = *reinterpret_cast<const uint4*>(wst + G * 4096 + 2048 + row * 16);
+                const uint32_t wd[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                  for (int pp = 0; pp < 4; ++pp) v[4 * j + pp] = lop3_and_or(wd[j] >> (4 * pp), kMagic);
+              } else {
+                const uint4 c0 = *reinterpret_cast<const uint4*>(wst + G * 2048 + row * 16);
+                const uint32_t wd[4] = {c0.x, c0.y, c0.z, c0.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                  for (int pp = 0; pp < 8; ++pp) v[8 * j + pp] = lop3_and_or2(wd[j] >> (2 * pp), kMagic);
+              }
+              mbar_wait(&a_empty[ja], (ua[ja] & 1) ^ 1);
+              tc_fence_after();
+              tmem_st32(tl + C::kACol0 + ja * 32, v);
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&a_full[ja]);
+              ++ua[ja];
+              ja = (ja + 1) % C::kASlots;
+            }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        } else {
+          // ---- per-group accumulators -> y += s * acc + (z - 128 s) * sum(x)  (exact affine, fp32) ----
+          for (int ci = 0; ci < nch; ++ci)
+#pragma unroll
+            for (int G = 0; G < 2; ++G) {
+              const uint32_t meta = *reinterpret_cast<const uint32_t*>(stage + ci * C::kWBytes + C::kCodeBytes + G * 512 + row * 4);
+              const float* xs = reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes) + G * kN;
+              const float sc = __uint_as_float(meta << 16), z = __uint_as_float(meta & 0xFFFF0000u);
+              const float zz = fmaf(-128.0f, sc, z);   // exact
+              mbar_wait(&d_full[jd], ud[jd] & 1);
+              tc_fence_after();
+              uint32_t d[kN];
+              if constexpr (kN == 16) {
+                tmem_ld16(tl + jd * kN, d);
+              } else {
+                uint32_t d0[16], d1[16];
+                tmem_ld16(tl + jd * kN, d0);
+                tmem_ld16(tl + jd * kN + 16, d1);
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                  d[t] = d0[t];
+                  d[16 + t] = d1[t];
+                }
+              }
+              tmem_wait_ld();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&d_empty[jd]);
+              ++ud[jd];
+              jd = (jd + 1) % C::kDSlots;
+#pragma unroll
+              for (int t = 0; t < kN; ++t)
+                if (t < Mv) y[t] = fmaf(sc, __uint_as_float(d[t]), fmaf(zz, xs[t], y[t]));
+            }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+      } else {
+        if (!is_convert && last_of_tile) {   // bf16: the tile's accumulator, K reduced by the MMAs
+          mbar_wait(&d_full[jd], ud[jd] & 1);
+          tc_fence_after();
+          uint32_t d[kN];
+          if constexpr (kN == 16) {
+            tmem_ld16(tl + jd * kN, d);
+          } else {
+            uint32_t d0[16], d1[16];
+            tmem_ld16(tl + jd * kN, d0);
+            tmem_ld16(tl + jd * kN + 16, d1);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              d[t] = d0[t];
+              d[16 + t] = d1[t];
+            }
+          }
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[jd]);
+          ++ud[jd];
+          jd = (jd + 1) % C::kDSlots;
+#pragma unroll
+          for (int t = 0; t < kN; ++t) y[t] = __uint_as_float(d[t]);
+        }
+      }
       if (++s == kStages) {
         s = 0;
         ph ^= 1;
       }
-      w.next(nC, nch);
     } while (w.left > 0 && w.r == cur_r);
     const bool last = w.left == 0;
-    if (last && threadIdx.x == 0) {
+    if (!is_convert) {
+      to_otile(y);
+      if (last) named_bar(3, 160);   // let warp 1 free TMEM: every accumulator has been read
+    }
+    if (last && tid == 0) {
       SS_TRACE_CTA0(4);
       SS_TRACE_MAX(7);
       if (ct) ct[3] = gtime();
     }
     flush(cur_r, c_first, c_last, last);
   }
-  if (threadIdx.x == 0) {
+  if (w.left == 0 && n_items == 0 && !is_convert) named_bar(3, 160);   // no work: still release warp 1
+  if (tid == 0) {
     SS_TRACE_MAX(6);
     if (ct) ct[4] = gtime();
   }
@@ -327,6 +508,8 @@ int gemv_cluster_split(int N, int K, int sms, int hint) {
   return S;
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
+// Stream-K grid of a tall matrix: one CTA per SM for bf16, two for substitutes
+int gemv_streamk_grid(bool q4, int N, int K, int sms) { return gemv_grid_for(N, K, sms * (q4 ? 2 : 1)); }
 
 static int current_device() {
   int d = 0;
@@ -334,55 +517,50 @@ static int current_device() {
   return d;
 }
 
-// ring stages of an instantiation; sets its smem/cluster attributes once per device (function
-// attributes are per device)
-template <bool Q4, int NT, bool kCluster, int QB = 4>
+// ring stages of an instantiation; sets its smem attribute once per device (function attributes are
+// per device).  Substitutes: ~88 KB of ring keeps two CTAs per SM; bf16 (head / resident layers):
+// one CTA per SM with a ~190 KB ring.
+template <int WF, int NT, bool kCluster>
 static int ensure_attrs() {
-  using C = GemvCfg<Q4, NT, QB>;
+  using C = GemvCfg<WF, NT>;
   static std::mutex mu;
   static std::map<int, int> stages_of;
   std::lock_guard<std::mutex> lk(mu);
   const int dev = current_device();
   auto it = stages_of.find(dev);
   if (it != stages_of.end()) return it->second;
-  // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
-  // down to ~68 KB of whole stages)
-  const int budget = (QB == 2 ? 72 : 88) * 1024;
+  const int budget = (WF == 16 ? 190 : 88) * 1024;
   int st = budget / C::kStageBytes;
   if (st < 2) st = 2;
   if (st > C::kMaxStages) st = C::kMaxStages;
-  cudaFuncSetAttribute(gemv_kernel<Q4, NT, kCluster, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
+  cudaFuncSetAttribute(gemv_kernel<WF, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
   stages_of[dev] = st;
   return st;
 }
 
 // Cluster plan {S, clusters}: the GPC structure caps how many clusters of S CTAs are resident at
-// once (e.g. 33 clusters of 8 at 2 CTAs/SM, below qkv's 36 row tiles), and a tile whose cluster is
-// not resident waits for a second wave.  Take the largest S <= gemv_cluster_split whose resident
-// cluster count covers every row tile (queried with cudaOccupancyMaxActiveClusters).  Cached per
-// (device, shape, hint).
+// once (e.g. 33 clusters of 8 at 2 CTAs/SM, below qkv's 36 row tiles).  Take the largest
+// S <= gemv_cluster_split whose resident cluster count covers every row tile (one tile per cluster,
+// queried with cudaOccupancyMaxActiveClusters); if none does, S = 1 (each CTA loops over row tiles
+// with no cluster barrier).  Cached per (device, shape, hint).
 struct ClusterPlan {
   int S, ncl;
   bool all_resident;
 };
-template <bool Q4, int NT, int QB = 4>
+template <int WF, int NT>
 static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
-  const int stages = ensure_attrs<Q4, NT, true, QB>();
+  const int stages = ensure_attrs<WF, NT, true>();
   static std::mutex mu;
   static std::map<std::tuple<int, int, int, int>, ClusterPlan> cache;
   std::lock_guard<std::mutex> lk(mu);
   const auto key = std::make_tuple(current_device(), N, K, hint);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  using C = GemvCfg<Q4, NT, QB>;
+  using C = GemvCfg<WF, NT>;
   const int tiles = N / 128;
-  const int per_sm = hint > 0 ? hint : 2;
-  const int S0 = gemv_cluster_split(N, K, sms, hint);
-  ClusterPlan plan{S0, 0, false};
-  for (int S = S0; S >= 1; --S) {
-    int ncl = sms * per_sm / S;
-    if (ncl > tiles) ncl = tiles;
-    if (ncl < 1) ncl = 1;
+  const int per_sm = WF == 16 ? 1 : (hint > 0 ? hint : 2);
+  const int S0 = gemv_cluster_split(N, K, sms, per_sm);
+  auto active_of = [&](int S, int ncl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncl * S);
     cfg.blockDim = dim3(kGemvThreads);
@@ -395,46 +573,41 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<Q4, NT, true, QB>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<WF, NT, true>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       active = ncl;   // cannot query: keep the arithmetic plan
     }
-    if (S == S0) plan = ClusterPlan{S0, active < ncl ? active : ncl, active >= tiles};
-    if (active >= tiles) {
+    return active;
+  };
+  ClusterPlan plan{1, std::max(1, std::min(tiles, sms * per_sm)), false};
+  for (int S = S0; S >= 2; --S) {
+    if (active_of(S, tiles) >= tiles) {
       plan = ClusterPlan{S, tiles, true};
       break;
     }
   }
-  if (plan.ncl < 1) plan.ncl = 1;
+  if (plan.S == 1) {
+    const int act = active_of(1, plan.ncl);
+    plan.ncl = std::max(1, std::min(plan.ncl, act));
+    plan.all_resident = plan.ncl >= tiles;
+  }
   cache[key] = plan;
   return plan;
 }
 
-// every row tile has its own resident cluster (required by EPI_RESID_NORM's in-kernel barrier)
+// every row tile has its own resident CTA or cluster (required by EPI_RESID_NORM's in-kernel barrier)
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits) {
   if (!gemv_use_cluster(N, K, sms)) return false;
-  if (q4 && bits == 2) {
-    switch (NT) {
-      case 1: return cluster_plan<true, 1, 2>(N, K, sms).all_resident;
-      case 2: return cluster_plan<true, 2, 2>(N, K, sms).all_resident;
-      case 3: return cluster_plan<true, 3, 2>(N, K, sms).all_resident;
-      case 4: return cluster_plan<true, 4, 2>(N, K, sms).all_resident;
-      default: return false;
-    }
-  }
-  switch (NT) {
-    case 1: return q4 ? cluster_plan<true, 1>(N, K, sms).all_resident : cluster_plan<false, 1>(N, K, sms).all_resident;
-    case 2: return q4 ? cluster_plan<true, 2>(N, K, sms).all_resident : cluster_plan<false, 2>(N, K, sms).all_resident;
-    case 3: return q4 ? cluster_plan<true, 3>(N, K, sms).all_resident : cluster_plan<false, 3>(N, K, sms).all_resident;
-    case 4: return q4 ? cluster_plan<true, 4>(N, K, sms).all_resident : cluster_plan<false, 4>(N, K, sms).all_resident;
-    default: return false;
-  }
+  const int nt = NT <= 2 ? 2 : 4;
+  if (!q4) return nt == 2 ? cluster_plan<16, 2>(N, K, sms).all_resident : cluster_plan<16, 4>(N, K, sms).all_resident;
+  if (bits == 2) return nt == 2 ? cluster_plan<2, 2>(N, K, sms).all_resident : cluster_plan<2, 4>(N, K, sms).all_resident;
+  return nt == 2 ? cluster_plan<4, 2>(N, K, sms).all_resident : cluster_plan<4, 4>(N, K, sms).all_resident;
 }
 
-template <bool Q4, int NT, bool kCluster, int QB = 4>
+template <int WF, int NT, bool kCluster>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
-  using C = GemvCfg<Q4, NT, QB>;
-  const int stages = ensure_attrs<Q4, NT, kCluster, QB>();
+  using C = GemvCfg<WF, NT>;
+  const int stages = ensure_attrs<WF, NT, kCluster>();
   GemvParams p = p0;
   p.stages = stages;
   cudaLaunchConfig_t cfg = {};
@@ -458,36 +631,29 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, gemv_kernel<Q4, NT, kCluster, QB>, p);
+  cudaLaunchKernelEx(&cfg, gemv_kernel<WF, NT, kCluster>, p);
 }
 
-template <bool Q4, int NT, int QB = 4>
+template <int WF, int NT>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
   if (gemv_use_cluster(p.N, p.K, sms)) {
-    const ClusterPlan pl = cluster_plan<Q4, NT, QB>(p.N, p.K, sms, p.ctas_per_sm);
-    launch_t<Q4, NT, true, QB>(p, pl.ncl * pl.S, pl.S, pdl, st);
+    const ClusterPlan pl = cluster_plan<WF, NT>(p.N, p.K, sms, p.ctas_per_sm);
+    launch_t<WF, NT, true>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {
-    launch_t<Q4, NT, false, QB>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);
+    const int per_sm = WF == 16 ? 1 : 2;
+    launch_t<WF, NT, false>(p, gemv_grid_for(p.N, p.K, sms * per_sm), 1, pdl, st);
   }
 }
 
+// the K2 dequant-GEMV / bf16 GEMV: NT = 2 (M <= 16) or 4 (M <= 32)
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st) {
-  if (q4 && p.qbits == 2) {   // 2-bit substitutes (NEXT-3)
-    switch (p.NT) {
-      case 1: launch_mode<true, 1, 2>(p, grid, pdl, st); break;
-      case 2: launch_mode<true, 2, 2>(p, grid, pdl, st); break;
-      case 3: launch_mode<true, 3, 2>(p, grid, pdl, st); break;
-      case 4: launch_mode<true, 4, 2>(p, grid, pdl, st); break;
-      default: break;
-    }
-    return;
-  }
-  switch (p.NT) {
-    case 1: q4 ? launch_mode<true, 1>(p, grid, pdl, st) : launch_mode<false, 1>(p, grid, pdl, st); break;
-    case 2: q4 ? launch_mode<true, 2>(p, grid, pdl, st) : launch_mode<false, 2>(p, grid, pdl, st); break;
-    case 3: q4 ? launch_mode<true, 3>(p, grid, pdl, st) : launch_mode<false, 3>(p, grid, pdl, st); break;
-    case 4: q4 ? launch_mode<true, 4>(p, grid, pdl, st) : launch_mode<false, 4>(p, grid, pdl, st); break;
-    default: break;
+  const bool nt2 = p.NT <= 2;
+  if (!q4) {
+    nt2 ? launch_mode<16, 2>(p, grid, pdl, st) : launch_mode<16, 4>(p, grid, pdl, st);
+  } else if (p.qbits == 2) {
+    nt2 ? launch_mode<2, 2>(p, grid, pdl, st) : launch_mode<2, 4>(p, grid, pdl, st);
+  } else {
+    nt2 ? launch_mode<4, 2>(p, grid, pdl, st) : launch_mode<4, 4>(p, grid, pdl, st);
   }
 }
 

@@ -85,78 +85,61 @@ void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float
 }
 
 // ---------------------------------------------------------------------------
-// K1: RTN min/max 4-bit group-64 quantizer, bf16 tiled -> Q4 tiled.
-// One warp per (tile-chunk, 16-row block).  Lane (g, t4) holds rows 16w+g, 16w+g+8 and, for each
-// 64-group G of the chunk, k = 64G + 16 t4 .. +15; a group spans the 4 lanes t4 = 0..3 of a g.
-//   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / 15) ; z = m
-//   code = clamp(rint_even(fp32(x - z) / s), 0, 15)       (IEEE div.rn; built without fast-math)
+// K1: RTN min/max group-64 quantizer, bf16 tiled -> Q4 (or Q2) tiled (layouts in
+// common.cuh).  One thread per (row, 64-group) of a tile-chunk (256 threads per chunk):
+//   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / (2^BITS - 1)) ; z = m
+//   code = clamp(rint_even(fp32(x - z) / s), 0, 2^BITS - 1)       (IEEE div.rn; built without fast-math)
 // ---------------------------------------------------------------------------
-// BITS = 2 (NEXT-3): the same rule with 2^BITS - 1 = 3 levels, packed in the Q2 layout (common.cuh).
 template <int BITS>
 __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                                          int64_t n_tc) {
   constexpr float kLevels = float((1 << BITS) - 1);
   constexpr int kTile = BITS == 2 ? kQ2TileBytes : kQ4TileBytes, kCode = BITS == 2 ? kQ2CodeBytes : kQ4CodeBytes;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t4 = lane & 3, g = lane >> 2;
+  const int row = threadIdx.x & 127, G = threadIdx.x >> 7;
   for (int64_t tc = blockIdx.x; tc < n_tc; tc += gridDim.x) {
     const uint8_t* s_tile = src + tc * kBF16TileBytes;
     uint8_t* d_tile = dst + tc * kTile;
-    float x[2][32];   // [h][q*8 + e] with q = 2G + i16/8, e = i16 % 8
+    float x[64];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int q = 0; q < 8; ++q) {   // core matrices kg = 8G + q: k = 64G + 8q .. +7 of this row
+      const uint4 v = *reinterpret_cast<const uint4*>(s_tile + core_off(row >> 3, 8 * G + q, row & 7, 0));
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 v = *reinterpret_cast<const uint4*>(s_tile + bf16_piece_off(warp, h, q, lane));
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          x[h][q * 8 + 2 * e] = __uint_as_float(w4[e] << 16);
-          x[h][q * 8 + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
-        }
-      }
-#pragma unroll
-    for (int G = 0; G < 2; ++G) {
-      uint32_t words[2][2] = {{0, 0}, {0, 0}};
-      uint32_t meta[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float* xv = &x[h][16 * G];   // i16 = 0..15
-        float mn = xv[0], mx = xv[0];
-#pragma unroll
-        for (int i = 1; i < 16; ++i) {
-          mn = fminf(mn, xv[i]);
-          mx = fmaxf(mx, xv[i]);
-        }
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), kLevels))) << 16);
-        const float z = mn;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float t = __fdiv_rn(__fsub_rn(xv[i], z), sc);
-          const float r = fminf(fmaxf(rintf(t), 0.0f), kLevels);
-          if constexpr (BITS == 2) {
-            words[h][0] |= uint32_t(r) << ((i & 1) * 16 + 2 * (i >> 1));
-          } else {
-            const int c8 = i & 7, slot = (c8 & 1) * 4 + (c8 >> 1);
-            words[h][i >> 3] |= uint32_t(r) << (4 * slot);
-          }
-        }
-        meta[h] = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
-      }
-      if constexpr (BITS == 2)
-        *reinterpret_cast<uint2*>(d_tile + ((warp * 2 + G) * 32 + lane) * 8) = make_uint2(words[0][0], words[1][0]);
-      else
-        *reinterpret_cast<uint4*>(d_tile + ((warp * 2 + G) * 32 + lane) * 16) =
-            make_uint4(words[0][0], words[0][1], words[1][0], words[1][1]);
-      if (t4 == 0) {
-        *reinterpret_cast<uint32_t*>(d_tile + kCode + ((warp * 2 + G) * 16 + g) * 4) = meta[0];
-        *reinterpret_cast<uint32_t*>(d_tile + kCode + ((warp * 2 + G) * 16 + g + 8) * 4) = meta[1];
+      for (int e = 0; e < 4; ++e) {
+        x[8 * q + 2 * e] = __uint_as_float(w4[e] << 16);
+        x[8 * q + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
       }
     }
+    float mn = x[0], mx = x[0];
+#pragma unroll
+    for (int i = 1; i < 64; ++i) {
+      mn = fminf(mn, x[i]);
+      mx = fmaxf(mx, x[i]);
+    }
+    const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), kLevels))) << 16);
+    const float z = mn;
+    uint32_t words[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) words[j] = 0u;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const float t = __fdiv_rn(__fsub_rn(x[i], z), sc);
+      const uint32_t r = uint32_t(fminf(fmaxf(rintf(t), 0.0f), kLevels));
+      if constexpr (BITS == 2) {   // word j = i / 16; pair p = (i % 16) / 2 at bit 2p (+16 for odd i)
+        const int q = i & 15;
+        words[i >> 4] |= r << ((q & 1) * 16 + 2 * (q >> 1));
+      } else {                     // half h = i / 32, word j = (i % 32) / 8; pair p = (i % 8) / 2 at bit 4p (+16 odd)
+        const int q = i & 7;
+        words[i >> 3] |= r << ((q & 1) * 16 + 4 * (q >> 1));
+      }
+    }
+    if constexpr (BITS == 2) {
+      *reinterpret_cast<uint4*>(d_tile + G * 2048 + row * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+    } else {
+      *reinterpret_cast<uint4*>(d_tile + G * 4096 + row * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+      *reinterpret_cast<uint4*>(d_tile + G * 4096 + 2048 + row * 16) = make_uint4(words[4], words[5], words[6], words[7]);
+    }
+    *reinterpret_cast<uint32_t*>(d_tile + kCode + G * 512 + row * 4) = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
   }
 }
 

@@ -81,7 +81,8 @@ struct GemvParams {
   EpiParams epi;
 };
 
-int gemv_max_segments(int N, int K, int grid);
+int gemv_max_segments(int N, int K, int grid);   // grid: the Stream-K grid (gemv_streamk_grid)
+int gemv_streamk_grid(bool q4, int N, int K, int sms);
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits = 4);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
 
