@@ -145,6 +145,8 @@ struct ss_ctx {
   int last_consumed_ev = -1;
   cudaEvent_t ev_root = nullptr;
   bool fuse_norm = true;
+  int k2_dbg = 0;             // K2 debug A/B bits (ss_debug_set_knob 1)
+  int k2_self_pf = 0;         // K2: L2-prefetch each CTA's own weight range (ss_debug_set_knob 0; measured slower)
   // graphs
   std::map<std::tuple<int, int, uint32_t>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, uint32_t>, int64_t> graph_launches;
@@ -341,6 +343,8 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     // free slots next to the previous layer's down GEMV (2 CTAs on ~84 SMs), so they are resident
     // and prefetched early (measured: pass 2082 -> 2013 us; o and down are slower at 1 CTA/SM).
     p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
+    p.self_pf = c->k2_self_pf;
+    p.dbg = c->k2_dbg;
     p.qbits = c->sub_bits;
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
@@ -1705,6 +1709,9 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.epi = base_epi(c, M);
     p.epi.kind = EPI_STORE;
     p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
+    p.self_pf = c->k2_self_pf;
+    p.dbg = c->k2_dbg;
+    p.dbg = c->k2_dbg;
     p.qbits = c->sub_bits;
     p.epi.out = c->at_o;
     p.epi.ldo = N;
@@ -1722,6 +1729,61 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
   CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
   *out_ms = ms / float(iters * seq.size());
   return check_launch(c, "time_matmul");
+}
+
+ss_status ss_debug_set_knob(ss_ctx* c, int32_t knob, int32_t value) {
+  GUARD(c);
+  switch (knob) {
+    case 0: c->k2_self_pf = value; break;
+    case 1: c->k2_dbg = value; break;
+    default: return fail(c, SS_ERR_INVALID, "unknown knob");
+  }
+  CK(cudaStreamSynchronize(c->cs));
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  c->graphs.clear();   // captured graphs hold the old launch parameters
+  c->graph_launches.clear();
+  return SS_OK;
+}
+
+ss_status ss_debug_gemv_plan(ss_ctx* c, int32_t group, int32_t M, int32_t* out4) {
+  GUARD(c);
+  if (group < 0 || group > 3 || !out4) return fail(c, SS_ERR_INVALID, "gemv_plan args");
+  gemv_debug_plan(true, c->sub_bits, gemv_nt(M), c->gN[group], c->gK[group], c->gv_grid, group == 0 ? 1 : 0, out4);
+  return check_launch(c, "gemv_plan");
+}
+
+ss_status ss_debug_group_trace(ss_ctx* c, int32_t layer, int32_t group, int32_t M, int64_t* out) {
+  GUARD(c);
+  if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || M < 1 || M > 32 || !out ||
+      c->lw[layer].resident)
+    return fail(c, SS_ERR_INVALID, "group_trace args (an offloaded layer)");
+  ss_status s = drain_stream(c);
+  if (s != SS_OK) return s;
+  const int N = c->gN[group], K = c->gK[group];
+  const LayerW& w = c->lw[layer];
+  GemvParams p{};
+  p.W = w.q4[group];
+  p.X = K == c->F ? c->actfrag : c->hfrag;
+  p.XS = K == c->F ? c->actxs : c->hxs;
+  p.N = N;
+  p.K = K;
+  p.NT = gemv_nt(M);
+  p.partials = c->gv_part;
+  p.counters = c->gv_cnt;
+  p.max_seg = gemv_max_segments(N, K, gemv_streamk_grid(true, N, K, c->gv_grid));
+  p.epi = base_epi(c, M);
+  p.epi.kind = EPI_STORE;
+  p.epi.out = c->at_o;
+  p.epi.ldo = N;
+  p.ctas_per_sm = group == 0 ? 1 : 0;
+  p.qbits = c->sub_bits;
+  launch_gemv(true, p, c->gv_grid, false, c->cs);   // warm-up
+  CK(cudaMemsetAsync(c->tracebuf, 0, 64 * 16 * 8, c->cs));
+  p.gtrace = c->tracebuf;
+  launch_gemv(true, p, c->gv_grid, false, c->cs);
+  CK(cudaMemcpyAsync(out, c->tracebuf, 64 * 16 * 8, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  return check_launch(c, "group_trace");
 }
 
 ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, float* out_ms) {

@@ -48,22 +48,27 @@ int gemv_max_segments(int N, int K, int grid) {
   return mx;
 }
 
-template <int WF, int NT, bool kCluster>
-__global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(const GemvParams p) {
+// MV: token columns that carry tokens (8 when M <= 8, else N): the accumulator registers per row.
+// One CTA per SM (the whole TMEM); 14 warps spread 4,4,3,3 over the sub-partitions: <= 128 registers.
+template <int WF, int NT, bool kCluster, int MV>
+__global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const GemvParams p) {
   using C = GemvCfg<WF, NT>;
+  using Sh = GemvShape<WF, MV>;
   constexpr int kN = C::kN;
+  static_assert(MV == 8 || MV == kN, "MV");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int kStages = p.stages;
   uint8_t* ring = smem;
   float* otile = reinterpret_cast<float*>(smem + kStages * C::kStageBytes);
   float* staging = otile + C::kTileFloats;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStagingFloats);
+  uint8_t* metabuf = reinterpret_cast<uint8_t*>(staging + C::kStagingFloats);
+  uint64_t* full = reinterpret_cast<uint64_t*>(metabuf + C::kMetaBytes);
   uint64_t* empty = full + C::kMaxStages;
-  uint64_t* a_full = empty + C::kMaxStages;
-  uint64_t* a_empty = a_full + C::kASlots;
-  uint64_t* d_full = a_empty + C::kASlots;
-  uint64_t* d_empty = d_full + C::kDSlots;
-  uint64_t* xbar = d_empty + C::kDSlots;                         // residual-row prefetch
+  uint64_t* go = empty + C::kMaxStages;        // Q: chunk slot ready (A written, D slot free)
+  uint64_t* a_empty = go + 4;                  // Q: A slot free (MMAs done)
+  uint64_t* d_full = a_empty + 4;              // accumulator ready
+  uint64_t* d_empty = d_full + 4;              // bf16: tile accumulator consumed
+  uint64_t* xbar = d_empty + 2;                // residual-row prefetch
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 1);
   int* flag = reinterpret_cast<int*>(xbar + 2);
   float* scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(flag) + 64);   // [128]
@@ -88,55 +93,66 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::kQ ? 9 : 1);   // Q: MMA commit + 4 convert + 4 accumulate warps
+      mbar_init(&empty[s], C::kQ ? 8 + Sh::kMmaWarps : 1);   // Q: every MMA warp's commit + 8 convert warps
     }
-    for (int j = 0; j < C::kASlots; ++j) {
-      mbar_init(&a_full[j], 4);
-      mbar_init(&a_empty[j], 1);
+    for (int j = 0; j < 4; ++j) {
+      mbar_init(&go[j], 12);        // 8 convert warps (A halves) + 4 accumulate warps (D slot released)
+      mbar_init(&a_empty[j], C::kQ ? 2 : 1);   // Q: one commit per MMA warp (one per 64-group)
+      mbar_init(&d_full[j], C::kQ ? 2 : 1);
     }
-    for (int j = 0; j < C::kDSlots; ++j) {
-      mbar_init(&d_full[j], 1);
-      mbar_init(&d_empty[j], 4);
-    }
+    for (int j = 0; j < 2; ++j) mbar_init(&d_empty[j], 4);
     mbar_init(xbar, 1);
     fence_barrier_init();
   }
+  // producer: the weight part of the first stages does not depend on the previous kernel or on TMEM;
+  // issue it before the TMEM allocation
+  Work wp = make_work<kCluster>(p.N, p.K, crank, csize);
+  const int64_t n_stage_p = wp.stages(nC, C::kCPS);
+  const int pre = int(n_stage_p < kStages ? n_stage_p : kStages);
+  const uint64_t pol = policy_evict_first();
+  const uint32_t per_chunk = uint32_t(C::kWBytes + C::kXBytes + C::kSBytes);
+  auto issue_w = [&](int st, const Work& ww, int n) {
+    mbar_arrive_expect_tx(&full[st], uint32_t(n) * per_chunk);
+    bulk_g2s_hint(ring + st * C::kStageBytes, p.W + (int64_t(ww.r) * nC + ww.c) * C::kWBytes, uint32_t(n) * C::kWBytes,
+                  &full[st], pol);
+  };
+  const Work wx0 = wp;   // replayed for the activation copies of the prefetched stages
+  if (threadIdx.x == 0)
+    for (int i = 0; i < pre; ++i) {
+      const int n = wp.take(C::kCPS);
+      issue_w(i, wp, n);
+      wp.next(nC, n);
+    }
   if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-  griddep_launch();   // grid <= the resident CTAs: let the next kernel prefetch now
+  // a CTA alone on its SM that allocates all 512 columns always receives column 0, lane 0: the MMA
+  // warp uses the constant address (immediates instead of per-MMA register-to-uniform moves)
+  const uint32_t tbase = 0;
+  if (threadIdx.x == 32 && *tmem_slot != 0) __trap();
+  griddep_launch();
   // a CTA with two or more tiles in a cluster of > 1 would need one cluster barrier per tile from
   // every warp; the launcher only plans clusters of one tile each (csize > 1) or csize == 1
   const bool cl_sync = kCluster && csize > 1;
+  // debug (built with -DSS_GTRACE): per-chunk clock64 events of CTA 0 (gtrace[c * 8 + e], first 64)
+  auto gtr = [&](int g, int e) {
+#ifdef SS_GTRACE
+    if (p.gtrace && blockIdx.x == 0 && g < 64) p.gtrace[g * 16 + e] = clock64();
+#endif
+  };
 
   if (warp == 0) {
     // ------------------------------ producer (TMA) -------------------------------
-    Work w = make_work<kCluster>(p.N, p.K, crank, csize);
-    const int64_t n_stage = w.stages(nC, C::kCPS);
+    Work w = wp;   // continues after the prefetched stages
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      const int pre = int(n_stage < kStages ? n_stage : kStages);
-      Work wx = w;   // replayed below for the activation copies of the prefetched stages
-      const uint32_t per_chunk = uint32_t(C::kWBytes + C::kXBytes + C::kSBytes);
-      auto issue_w = [&](int st, const Work& ww, int n) {
-        mbar_arrive_expect_tx(&full[st], uint32_t(n) * per_chunk);
-        bulk_g2s_hint(ring + st * C::kStageBytes, p.W + (int64_t(ww.r) * nC + ww.c) * C::kWBytes,
-                      uint32_t(n) * C::kWBytes, &full[st], pol);
-      };
+      Work wx = wx0;
       auto issue_x = [&](int st, const Work& ww, int n) {
         uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
         bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
         if constexpr (C::kQ)
           bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * kN, uint32_t(n) * C::kSBytes, &full[st]);
       };
-      // weights do not depend on the previous kernel: issue before the grid-dependency wait
-      for (int i = 0; i < pre; ++i) {
-        const int n = w.take(C::kCPS);
-        issue_w(i, w, n);
-        w.next(nC, n);
-      }
       // L2 prefetch of the next matrix (independent of every activation): this CTA's slice
       if (p.pf && p.pf_bytes > 0) {
         const int64_t per = ((p.pf_bytes / gridDim.x) + 15) & ~int64_t(15);
@@ -153,8 +169,10 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
       }
       int st = pre % kStages;
       uint32_t ph = pre / kStages;   // 0 or 1 (pre <= kStages)
-      for (int64_t i = pre; i < n_stage; ++i) {
+      for (int64_t i = pre; i < n_stage_p; ++i) {
+        gtr(int(2 * i), 8);
         mbar_wait(&empty[st], (ph - 1) & 1);
+        gtr(int(2 * i), 9);
         const int n = w.take(C::kCPS);
         issue_w(st, w, n);
         issue_x(st, w, n);
@@ -170,93 +188,102 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
     return;
   }
 
-  if (warp == 1) {
-    // ------------------------------ MMA issuer -------------------------------
+  if (warp == 1 || warp >= 14) {
+    // ------------------------------ MMA issuers (whole warps, one elected lane issues) --------------
+    // substitutes: MMA warp m = (warp 1 -> 0, warp 14 + i -> 1 + i) issues the MMAs of 64-group m % 2 of
+    // the tile-chunks with cc % (kMmaWarps / 2) == m / 2 (independent accumulators; each warp commits
+    // its own MMAs, two commits per chunk); bf16: warp 1 alone
+    const int mw = warp == 1 ? 0 : warp - 13;
+    const int Gm = mw & 1, par = mw >> 1;
+    constexpr int kPar = Sh::kMmaWarps / 2;
     Work w = make_work<kCluster>(p.N, p.K, crank, csize);
-    if (lane == 0) {
-      griddep_wait();   // acquire side of the activations' dependency for the async proxy reads
-      constexpr uint32_t idesc = umma_idesc_bf16(kN);
-      int s = 0;
-      uint32_t ph = 0;
-      int ja = 0, jd = 0;
-      uint32_t ua[C::kASlots] = {}, ud[C::kDSlots] = {};
-      while (w.left > 0) {
-        const int cur_r = w.r;
-        bool first = true;
-        do {
-          const int nch = w.take(C::kCPS);
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t sb = smem_u32(ring + s * C::kStageBytes);
-          const uint32_t xb = sb + C::kCPS * C::kWBytes;
-          w.next(nC, nch);
-          const bool last = w.left == 0 || w.r != cur_r;
-          if constexpr (C::kQ) {
-            for (int ci = 0; ci < nch; ++ci)
-#pragma unroll
-              for (int G = 0; G < 2; ++G) {
-                mbar_wait(&a_full[ja], ua[ja] & 1);
-                mbar_wait(&d_empty[jd], (ud[jd] & 1) ^ 1);
-                tc_fence_after();
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  umma_ts(tbase + jd * kN, tbase + C::kACol0 + ja * 32 + kk * 8,
-                          umma_desc(xb + ci * C::kXBytes + G * 1024 + kk * 256, 128, 2048), idesc, kk > 0);
-                umma_commit(&a_empty[ja]);
-                umma_commit(&d_full[jd]);
-                ++ua[ja];
-                ++ud[jd];
-                ja = (ja + 1) % C::kASlots;
-                jd = (jd + 1) % C::kDSlots;
-              }
-          } else {
-            if (first) {
-              mbar_wait(&d_empty[jd], (ud[jd] & 1) ^ 1);
-              tc_fence_after();
+    constexpr uint32_t idesc = umma_idesc_bf16(kN);
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t cc = 0, tc = 0;   // chunk counter (Q: slot cc % 4, parity cc / 4 % 2); tile counter (bf16)
+    const uint32_t ring0 = smem_u32(ring);
+    while (w.left > 0) {
+      const int cur_r = w.r;
+      bool first = true;
+      do {
+        const int nch = w.take(C::kCPS);
+        mbar_wait(&full[s], ph);
+        if (Gm == 0) gtr(int(cc), 11);
+        tc_fence_after();
+        const uint32_t sb = ring0 + s * C::kStageBytes;
+        const uint64_t xdesc = umma_desc(sb + C::kCPS * C::kWBytes, 128, 2048);   // B: token groups at 2048 B
+        w.next(nC, nch);
+        const bool last = w.left == 0 || w.r != cur_r;
+        if constexpr (C::kQ) {
+          for (int ci = 0; ci < nch; ++ci) {
+            const uint32_t j = cc & 3;
+            if (kPar > 1 && int(cc % kPar) != par) {
+              ++cc;
+              continue;
             }
+            mbar_wait(&go[j], (cc >> 2) & 1);   // A of this chunk written and accumulator slot j free
+            if (Gm == 0) gtr(int(cc), 3); else gtr(int(cc), 4);
+            tc_fence_after();
+            const uint32_t acol = tbase + C::kACol0 + j * 64, dcol = tbase + j * C::kDCols;
+            const uint64_t xd = xdesc + uint64_t(ci * (C::kXBytes >> 4));
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_ss(tbase + jd * kN, umma_desc(sb + kk * 256, 128, 2048), umma_desc(xb + kk * 256, 128, 2048), idesc,
+            for (int kk = 0; kk < 4; ++kk)   // K = 16 per MMA: 8 A columns, +256 B of B (16 in desc units)
+              umma_ts_w(dcol + Gm * kN, acol + Gm * 32 + kk * 8, xd + uint64_t(Gm * 64 + kk * 16), idesc, kk > 0);
+            umma_commit_w(&a_empty[j]);
+            umma_commit_w(&d_full[j]);
+            if (Gm == 0) gtr(int(cc), 5); else gtr(int(cc), 13);
+            ++cc;
+          }
+        } else {
+          const uint32_t j = tc & 1;
+          if (first) {
+            mbar_wait(&d_empty[j], ((tc >> 1) & 1) ^ 1);
+            tc_fence_after();
+          }
+          const uint64_t wdesc = umma_desc(sb, 128, 2048);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_ss_w(tbase + j * C::kDCols, wdesc + uint64_t(kk * 16), xdesc + uint64_t(kk * 16), idesc,
                       (first && kk == 0) ? 0u : 1u);
-            if (last) {
-              umma_commit(&d_full[jd]);
-              ++ud[jd];
-              jd = (jd + 1) % C::kDSlots;
-            }
+          if (last) {
+            umma_commit_w(&d_full[j]);
+            ++tc;
           }
-          umma_commit(&empty[s]);
-          first = false;
-          if (++s == kStages) {
-            s = 0;
-            ph ^= 1;
-          }
-        } while (w.left > 0 && w.r == cur_r);
-      }
+        }
+        umma_commit_w(&empty[s]);
+        first = false;
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      } while (w.left > 0 && w.r == cur_r);
     }
-    __syncwarp();
-    named_bar(3, 160);   // the accumulate warps have read the last accumulator
-    tc_fence_after();
-    tmem_dealloc(tbase, C::kTmemCols);
+    named_bar(3, 128 + 32 * Sh::kMmaWarps);   // every MMA issued and the accumulate warps have read the last one
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc(tbase, C::kTmemCols);
+    }
     if (cl_sync) cluster_sync_all();
     return;
   }
 
-  // ---------------------------- worker warps 2..9 ----------------------------
+  // ---------------------------- worker warps 2..13 ----------------------------
   griddep_wait();
-  const int tid = threadIdx.x - 64;             // 0..255 over the worker warps
+  if (warp >= 2 + kGemvWorkers / 32) return;    // (no further roles)
+  const int tid = threadIdx.x - 64;             // 0..383 over the worker warps
   const int q = warp & 3;                       // TMEM lane quadrant of this warp
   const int row = 32 * q + lane;                // weight row of the tile owned in TMEM
   const uint32_t tl = tbase + (uint32_t(32 * q) << 16);
-  const bool is_convert = warp < 6;
-  const int Mv = p.epi.M < kN ? p.epi.M : kN;   // valid tokens
+  const bool is_acc = warp >= 10;               // accumulate warps 10..13; convert warps 2..9
+  const int Gc = (warp - 2) >> 2;               // convert warps: 64-group of every chunk
 
   uint32_t xph = 0;   // phase of xbar
   // --- split-K reduction + epilogue of tile r from otile (worker threads only) ---
   auto flush = [&](int r, int c_first, int c_last, bool last) {
     const int nthr = kGemvWorkers;
+    named_bar(1, nthr);   // otile written by the accumulate warps
     if constexpr (kCluster) {
       if (csize == 1) {
-        named_bar(1, nthr);
         if (tid == 0) SS_TRACE_MAX(8);
         apply_epilogue(p.epi, otile, kN, r, 0, kN, tid, nthr, scratch, p.trace, 1, true, kN);
         named_bar(1, nthr);
@@ -277,7 +304,6 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
         for (int m = 0; m < nvalid; ++m)
           bulk_g2s(xpre + m * kTileRows, p.epi.x + int64_t(mlo + m) * p.epi.ldx + int64_t(r) * kTileRows, kTileRows * 4, xbar);
       }
-      named_bar(1, nthr);
       for (int i = tid; i < kN * (kTileRows / 4); i += nthr) {
         const int m = i / (kTileRows / 4), n4 = (i % (kTileRows / 4)) * 4;
         const int qo = int(owner_of(m, kN, S));          // owner rank of token m
@@ -304,7 +330,6 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
       return;
     } else {
       const bool complete = (c_first == 0 && c_last == nC - 1);
-      named_bar(1, nthr);
       if (!complete) {
         const int G = gridDim.x;
         const int64_t first = owner_of(int64_t(r) * nC, T, G);
@@ -334,143 +359,200 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
       named_bar(1, nthr);
     }
   };
-  // the accumulated rows of the tile -> otile: token-major [N][128] in cluster mode (the push layout),
-  // row-major [128][N] otherwise (the epilogue / Stream-K partial layout)
-  auto to_otile = [&](const float (&y)[kN]) {
+  // the tile's rows -> otile: token-major [N][128] in cluster mode with csize > 1 (the push layout),
+  // row-major [128][N] otherwise (the epilogue / Stream-K partial layout); columns >= MV carry no token
+  auto to_otile = [&](const float (&y)[MV]) {
+    const bool tok_major = kCluster && csize > 1;
 #pragma unroll
-    for (int t = 0; t < kN; ++t) {
-      if constexpr (kCluster) {
-        if (csize > 1) otile[t * kTileRows + row] = y[t];
-        else otile[row * kN + t] = y[t];
-      } else {
-        otile[row * kN + t] = y[t];
-      }
-    }
+    for (int t = 0; t < MV; ++t) otile[tok_major ? t * kTileRows + row : row * kN + t] = y[t];
   };
 
   Work w = make_work<kCluster>(p.N, p.K, crank, csize);
   const int64_t n_items = w.left;
   int s = 0;
   uint32_t ph = 0;
-  int ja = 0, jd = 0;
-  uint32_t ua[C::kASlots] = {}, ud[C::kDSlots] = {};
+  uint32_t cc = 0, tc = 0;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128): 128 + code is exact in bf16
+  uint32_t* meta_s = reinterpret_cast<uint32_t*>(metabuf);                            // [8][2][128]
+  float* xs_s = reinterpret_cast<float*>(metabuf + C::kMetaSlots * 2 * kTileRows * 4);   // [8][2][N]
+  if (C::kQ && is_acc && lane == 0)
+    for (int j = 0; j < 4; ++j) mbar_arrive(&go[j]);   // every accumulator slot starts free
+  bool cpend = false;   // convert warps: a TMEM store whose "go" arrival is pending
+  uint32_t cj = 0;
   while (w.left > 0) {
     const int cur_r = w.r, c_first = w.c;
     int c_last = w.c;
-    float y[kN];
+    float y[MV];
 #pragma unroll
-    for (int t = 0; t < kN; ++t) y[t] = 0.f;
+    for (int t = 0; t < MV; ++t) y[t] = 0.f;
     do {
       const int nch = w.take(C::kCPS);
       c_last = w.c + nch - 1;
       const uint8_t* stage = ring + s * C::kStageBytes;
-      if (C::kQ) mbar_wait(&full[s], ph);   // bf16: the MMAs read the stage, the workers only the accumulator
-      if (threadIdx.x == 64 && w.left == n_items) {
+      if (tid == 0 && w.left == n_items) {
         SS_TRACE_CTA0(3);
         if (ct) ct[2] = gtime();
       }
       w.next(nC, nch);
       const bool last_of_tile = w.left == 0 || w.r != cur_r;
       if constexpr (C::kQ) {
-        if (is_convert) {
-          // ---- codes of row `row` -> exact bf16 (128 + code) pairs -> TMEM A slot (32 columns) ----
-          for (int ci = 0; ci < nch; ++ci)
+        if (!is_acc) {
+          // ---- convert: this row's 64 codes of group Gc -> exact bf16 (128 + code) pairs -> TMEM ----
+          // Software-pipelined: the TMEM store of chunk c completes while chunk c + 1 is converted, and
+          // only then does this warp report chunk c's A half (the "go" barrier).
+          if (warp == 2 && lane == 0) gtr(int(cc), 12);
+          mbar_wait(&full[s], ph);
+          if (warp == 2 && lane == 0) gtr(int(cc), 10);
+          for (int ci = 0; ci < nch; ++ci) {
+            const uint8_t* wst = stage + ci * C::kWBytes;
+            uint32_t v[32];
+            if constexpr (WF == 4) {
+              const uint4 c0 = *reinterpret_cast<const uint4*>(wst + Gc * 4096 + row * 16);
+              const uint4 c1 = *reinterpret_cast<const uint4*>(wst + Gc * 4096 + 2048 + row * 16);
+              const uint32_t wd[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+              if (p.dbg & 1) {   // debug A/B: no conversion work (results wrong)
 #pragma unroll
-            for (int G = 0; G < 2; ++G) {
-              const uint8_t* wst = stage + ci * C::kWBytes;
-              uint32_t v[32];
-              if constexpr (WF == 4) {
-                const uint4 c0 = *reinterpret_cast<const uint4*>(wst + G * 4096 + row * 16);
-                const uint4 c1 = *reinterpret_cast<const uint4*>(wst + G * 4096 + 2048 + row * 16);
-                const uint32_t wd[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                  for (int pp = 0; pp < 4; ++pp) v[4 * j + pp] = lop3_and_or(wd[j] >> (4 * pp), kMagic);
+                for (int jj = 0; jj < 32; ++jj) v[jj] = wd[jj & 7];
               } else {
-                const uint4 c0 = *reinterpret_cast<const uint4*>(wst + G * 2048 + row * 16);
-                const uint32_t wd[4] = {c0.x, c0.y, c0.z, c0.w};
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+              for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
-                  for (int pp = 0; pp < 8; ++pp) v[8 * j + pp] = lop3_and_or2(wd[j] >> (2 * pp), kMagic);
+                for (int pp = 0; pp < 4; ++pp) v[4 * jj + pp] = lop3_and_or(wd[jj] >> (4 * pp), kMagic);
               }
-              mbar_wait(&a_empty[ja], (ua[ja] & 1) ^ 1);
-              tc_fence_after();
-              tmem_st32(tl + C::kACol0 + ja * 32, v);
+            } else {
+              const uint4 c0 = *reinterpret_cast<const uint4*>(wst + Gc * 2048 + row * 16);
+              const uint32_t wd[4] = {c0.x, c0.y, c0.z, c0.w};
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int pp = 0; pp < 8; ++pp) v[8 * jj + pp] = lop3_and_or2(wd[jj] >> (2 * pp), kMagic);
+            }
+            const uint32_t meta = *reinterpret_cast<const uint32_t*>(wst + C::kCodeBytes + Gc * 512 + row * 4);
+            float4 xsv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q == 0 && lane < kN / 4)
+              xsv = reinterpret_cast<const float4*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes + Gc * kN * 4)[lane];
+            if (cpend) {   // the previous chunk's TMEM store has had this conversion's time to land
               tmem_wait_st();
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&a_full[ja]);
-              ++ua[ja];
-              ja = (ja + 1) % C::kASlots;
+              if (lane == 0) mbar_arrive(&go[cj]);
+              if (warp == 2 && lane == 0) gtr(int(cc) - 1, 2);
+              cpend = false;
             }
+            const uint32_t j = cc & 3;
+            if (warp == 2 && lane == 0) gtr(int(cc), 0);
+            mbar_wait(&a_empty[j], ((cc >> 2) & 1) ^ 1);
+            if (warp == 2 && lane == 0) gtr(int(cc), 1);
+            tc_fence_after();
+            tmem_st32(tl + C::kACol0 + j * 64 + Gc * 32, v);
+            // scale/zero and this group's activation sums -> side buffer slot cc % 8 (the stage can then be
+            // refilled as soon as the codes are converted).  Slot cc % 8 was last read by the accumulate
+            // step of chunk cc - 8, which precedes its release of accumulator slot j, which the MMAs of
+            // chunk cc - 4 waited for, which the a_empty wait above waited for.
+            const uint32_t k8 = cc & 7;
+            meta_s[(k8 * 2 + Gc) * kTileRows + row] = meta;
+            if (q == 0 && lane < kN / 4) reinterpret_cast<float4*>(xs_s + (k8 * 2 + Gc) * kN)[lane] = xsv;
+            cj = j;
+            cpend = true;
+            ++cc;
+            if (p.dbg & 2) {   // debug A/B: no software pipelining
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&go[cj]);
+              cpend = false;
+            }
+          }
+          if (last_of_tile && cpend) {   // the accumulate warps need the tile's last chunk before the flush
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&go[cj]);
+            cpend = false;
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
         } else {
-          // ---- per-group accumulators -> y += s * acc + (z - 128 s) * sum(x)  (exact affine, fp32) ----
-          for (int ci = 0; ci < nch; ++ci)
+          // ---- accumulate: y += s * acc + (z - 128 s) * sum(x) per 64-group (exact affine, fp32; R3) ----
+          for (int ci = 0; ci < nch; ++ci) {
+            const uint32_t j = cc & 3, k8 = cc & 7;
+            mbar_wait(&d_full[j], (cc >> 2) & 1);   // implies the side-buffer slot is written (via go)
+            if (warp == 10 && lane == 0) gtr(int(cc), 6);
+            tc_fence_after();
+            uint32_t m[2];
+            float4 xv[2][MV / 4];
 #pragma unroll
             for (int G = 0; G < 2; ++G) {
-              const uint32_t meta = *reinterpret_cast<const uint32_t*>(stage + ci * C::kWBytes + C::kCodeBytes + G * 512 + row * 4);
-              const float* xs = reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes) + G * kN;
-              const float sc = __uint_as_float(meta << 16), z = __uint_as_float(meta & 0xFFFF0000u);
-              const float zz = fmaf(-128.0f, sc, z);   // exact
-              mbar_wait(&d_full[jd], ud[jd] & 1);
-              tc_fence_after();
-              uint32_t d[kN];
-              if constexpr (kN == 16) {
-                tmem_ld16(tl + jd * kN, d);
-              } else {
-                uint32_t d0[16], d1[16];
-                tmem_ld16(tl + jd * kN, d0);
-                tmem_ld16(tl + jd * kN + 16, d1);
+              m[G] = meta_s[(k8 * 2 + G) * kTileRows + row];
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                  d[t] = d0[t];
-                  d[16 + t] = d1[t];
+              for (int t4 = 0; t4 < MV / 4; ++t4) xv[G][t4] = reinterpret_cast<const float4*>(xs_s + (k8 * 2 + G) * kN)[t4];
+            }
+            uint32_t d[2][MV];
+#pragma unroll
+            for (int G = 0; G < 2; ++G) {
+              if constexpr (MV == 8) {
+                uint32_t d8[8];
+                tmem_ld8(tl + j * C::kDCols + G * kN, d8);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) d[G][t] = d8[t];
+              } else {
+#pragma unroll
+                for (int h = 0; h < MV / 16; ++h) {
+                  uint32_t d16[16];
+                  tmem_ld16(tl + j * C::kDCols + G * kN + h * 16, d16);
+#pragma unroll
+                  for (int t = 0; t < 16; ++t) d[G][16 * h + t] = d16[t];
                 }
               }
-              tmem_wait_ld();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&d_empty[jd]);
-              ++ud[jd];
-              jd = (jd + 1) % C::kDSlots;
-#pragma unroll
-              for (int t = 0; t < kN; ++t)
-                if (t < Mv) y[t] = fmaf(sc, __uint_as_float(d[t]), fmaf(zz, xs[t], y[t]));
             }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&go[j]);   // accumulator slot j free for the chunk four ahead
+            if (warp == 10 && lane == 0) gtr(int(cc), 7);
+#pragma unroll
+            for (int G = 0; G < 2; ++G) {
+              const float sc = __uint_as_float(m[G] << 16);
+              const float zz = fmaf(-128.0f, sc, __uint_as_float(m[G] & 0xFFFF0000u));   // z - 128 s, exact
+#pragma unroll
+              for (int t4 = 0; t4 < MV / 4; ++t4) {
+                y[4 * t4 + 0] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 0]), fmaf(zz, xv[G][t4].x, y[4 * t4 + 0]));
+                y[4 * t4 + 1] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 1]), fmaf(zz, xv[G][t4].y, y[4 * t4 + 1]));
+                y[4 * t4 + 2] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 2]), fmaf(zz, xv[G][t4].z, y[4 * t4 + 2]));
+                y[4 * t4 + 3] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 3]), fmaf(zz, xv[G][t4].w, y[4 * t4 + 3]));
+              }
+            }
+            ++cc;
+          }
         }
       } else {
-        if (!is_convert && last_of_tile) {   // bf16: the tile's accumulator, K reduced by the MMAs
-          mbar_wait(&d_full[jd], ud[jd] & 1);
+        if (is_acc && last_of_tile) {   // bf16: the tile's accumulator, K reduced by the MMAs
+          const uint32_t j = tc & 1;
+          mbar_wait(&d_full[j], (tc >> 1) & 1);
           tc_fence_after();
-          uint32_t d[kN];
-          if constexpr (kN == 16) {
-            tmem_ld16(tl + jd * kN, d);
-          } else {
-            uint32_t d0[16], d1[16];
-            tmem_ld16(tl + jd * kN, d0);
-            tmem_ld16(tl + jd * kN + 16, d1);
+          uint32_t d[MV];
+          if constexpr (MV == 8) {
+            uint32_t d8[8];
+            tmem_ld8(tl + j * C::kDCols, d8);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              d[t] = d0[t];
-              d[16 + t] = d1[t];
+            for (int t = 0; t < 8; ++t) d[t] = d8[t];
+          } else {
+#pragma unroll
+            for (int h = 0; h < MV / 16; ++h) {
+              uint32_t d16[16];
+              tmem_ld16(tl + j * C::kDCols + h * 16, d16);
+#pragma unroll
+              for (int t = 0; t < 16; ++t) d[16 * h + t] = d16[t];
             }
           }
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[jd]);
-          ++ud[jd];
-          jd = (jd + 1) % C::kDSlots;
+          if (lane == 0) mbar_arrive(&d_empty[j]);
 #pragma unroll
-          for (int t = 0; t < kN; ++t) y[t] = __uint_as_float(d[t]);
+          for (int t = 0; t < MV; ++t) y[t] = __uint_as_float(d[t]);
         }
+        if (last_of_tile) ++tc;
       }
       if (++s == kStages) {
         s = 0;
@@ -478,9 +560,9 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
       }
     } while (w.left > 0 && w.r == cur_r);
     const bool last = w.left == 0;
-    if (!is_convert) {
+    if (is_acc) {
       to_otile(y);
-      if (last) named_bar(3, 160);   // let warp 1 free TMEM: every accumulator has been read
+      if (last) named_bar(3, 128 + 32 * Sh::kMmaWarps);   // let warp 1 free TMEM: every accumulator read
     }
     if (last && tid == 0) {
       SS_TRACE_CTA0(4);
@@ -489,7 +571,7 @@ __global__ void __launch_bounds__(kGemvThreads, WF == 16 ? 1 : 2) gemv_kernel(co
     }
     flush(cur_r, c_first, c_last, last);
   }
-  if (w.left == 0 && n_items == 0 && !is_convert) named_bar(3, 160);   // no work: still release warp 1
+  if (n_items == 0 && is_acc) named_bar(3, 128 + 32 * Sh::kMmaWarps);   // no work: still release warp 1
   if (tid == 0) {
     SS_TRACE_MAX(6);
     if (ct) ct[4] = gtime();
@@ -508,8 +590,11 @@ int gemv_cluster_split(int N, int K, int sms, int hint) {
   return S;
 }
 bool gemv_use_cluster(int N, int K, int sms) { return N / 128 <= 2 * sms; }
-// Stream-K grid of a tall matrix: one CTA per SM for bf16, two for substitutes
-int gemv_streamk_grid(bool q4, int N, int K, int sms) { return gemv_grid_for(N, K, sms * (q4 ? 2 : 1)); }
+// Stream-K grid of a tall matrix
+int gemv_streamk_grid(bool q4, int N, int K, int sms) {
+  (void)q4;
+  return gemv_grid_for(N, K, sms);   // one CTA per SM
+}
 
 static int current_device() {
   int d = 0;
@@ -517,10 +602,9 @@ static int current_device() {
   return d;
 }
 
-// ring stages of an instantiation; sets its smem attribute once per device (function attributes are
-// per device).  Substitutes: ~88 KB of ring keeps two CTAs per SM; bf16 (head / resident layers):
-// one CTA per SM with a ~190 KB ring.
-template <int WF, int NT, bool kCluster>
+// ring stages of an instantiation (one CTA per SM: the ring takes what the 227 KB leave); sets its
+// smem attribute once per device (function attributes are per device).
+template <int WF, int NT, bool kCluster, int MV>
 static int ensure_attrs() {
   using C = GemvCfg<WF, NT>;
   static std::mutex mu;
@@ -529,14 +613,18 @@ static int ensure_attrs() {
   const int dev = current_device();
   auto it = stages_of.find(dev);
   if (it != stages_of.end()) return it->second;
-  const int budget = (WF == 16 ? 190 : 88) * 1024;
-  int st = budget / C::kStageBytes;
-  if (st < 2) st = 2;
-  if (st > C::kMaxStages) st = C::kMaxStages;
-  cudaFuncSetAttribute(gemv_kernel<WF, NT, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
+  const int st = C::stages();
+  cudaFuncSetAttribute(gemv_kernel<WF, NT, kCluster, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(st));
+  // the whole unified L1/shared array as shared memory
+  cudaFuncSetAttribute(gemv_kernel<WF, NT, kCluster, MV>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   stages_of[dev] = st;
   return st;
 }
+
+// The occupancy calculator reports 1 resident CTA per SM for any kernel that allocates TMEM (measured,
+// tools/probes/occ_probe.cu, although the hardware co-schedules two: tools/probes/coresid_probe.cu).
+// Cluster residency is queried on a proxy kernel with the same block size and dynamic shared memory.
+__global__ void __launch_bounds__(kGemvMaxThreads) gemv_occ_proxy(int) {}
 
 // Cluster plan {S, clusters}: the GPC structure caps how many clusters of S CTAs are resident at
 // once (e.g. 33 clusters of 8 at 2 CTAs/SM, below qkv's 36 row tiles).  Take the largest
@@ -549,7 +637,7 @@ struct ClusterPlan {
 };
 template <int WF, int NT>
 static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
-  const int stages = ensure_attrs<WF, NT, true>();
+  const int stages = ensure_attrs<WF, NT, true, GemvCfg<WF, NT>::kN>();
   static std::mutex mu;
   static std::map<std::tuple<int, int, int, int>, ClusterPlan> cache;
   std::lock_guard<std::mutex> lk(mu);
@@ -558,12 +646,13 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   if (it != cache.end()) return it->second;
   using C = GemvCfg<WF, NT>;
   const int tiles = N / 128;
-  const int per_sm = WF == 16 ? 1 : (hint > 0 ? hint : 2);
+  const int per_sm = 1;   // one CTA per SM (the whole TMEM)
+  (void)hint;
   const int S0 = gemv_cluster_split(N, K, sms, per_sm);
   auto active_of = [&](int S, int ncl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncl * S);
-    cfg.blockDim = dim3(kGemvThreads);
+    cfg.blockDim = dim3(kGemvMaxThreads);
     cfg.dynamicSmemBytes = C::smem_for(stages);
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -573,7 +662,9 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, gemv_kernel<WF, NT, true>, &cfg) != cudaSuccess) {
+    cudaFuncSetAttribute(gemv_occ_proxy, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem_for(stages));
+    cudaFuncSetAttribute(gemv_occ_proxy, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaOccupancyMaxActiveClusters(&active, gemv_occ_proxy, &cfg) != cudaSuccess) {
       cudaGetLastError();
       active = ncl;   // cannot query: keep the arithmetic plan
     }
@@ -581,13 +672,13 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   };
   ClusterPlan plan{1, std::max(1, std::min(tiles, sms * per_sm)), false};
   for (int S = S0; S >= 2; --S) {
-    if (active_of(S, tiles) >= tiles) {
+    if (std::min(active_of(S, tiles), sms * per_sm / S) >= tiles) {
       plan = ClusterPlan{S, tiles, true};
       break;
     }
   }
   if (plan.S == 1) {
-    const int act = active_of(1, plan.ncl);
+    const int act = std::min(active_of(1, plan.ncl), sms * per_sm);
     plan.ncl = std::max(1, std::min(plan.ncl, act));
     plan.all_resident = plan.ncl >= tiles;
   }
@@ -604,15 +695,15 @@ bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits) {
   return nt == 2 ? cluster_plan<4, 2>(N, K, sms).all_resident : cluster_plan<4, 4>(N, K, sms).all_resident;
 }
 
-template <int WF, int NT, bool kCluster>
+template <int WF, int NT, bool kCluster, int MV>
 static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream_t st) {
   using C = GemvCfg<WF, NT>;
-  const int stages = ensure_attrs<WF, NT, kCluster>();
+  const int stages = ensure_attrs<WF, NT, kCluster, MV>();
   GemvParams p = p0;
   p.stages = stages;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemvThreads);
+  cfg.blockDim = dim3(GemvShape<WF, MV>::kThreads);
   cfg.dynamicSmemBytes = C::smem_for(stages);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -631,29 +722,71 @@ static void launch_t(const GemvParams& p0, int grid, int S, bool pdl, cudaStream
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, gemv_kernel<WF, NT, kCluster>, p);
+  cudaLaunchKernelEx(&cfg, gemv_kernel<WF, NT, kCluster, MV>, p);
 }
 
-template <int WF, int NT>
+template <int WF, int NT, int MV>
 static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
   if (gemv_use_cluster(p.N, p.K, sms)) {
     const ClusterPlan pl = cluster_plan<WF, NT>(p.N, p.K, sms, p.ctas_per_sm);
-    launch_t<WF, NT, true>(p, pl.ncl * pl.S, pl.S, pdl, st);
+    launch_t<WF, NT, true, MV>(p, pl.ncl * pl.S, pl.S, pdl, st);
   } else {
-    const int per_sm = WF == 16 ? 1 : 2;
-    launch_t<WF, NT, false>(p, gemv_grid_for(p.N, p.K, sms * per_sm), 1, pdl, st);
+    launch_t<WF, NT, false, MV>(p, gemv_grid_for(p.N, p.K, sms), 1, pdl, st);
+  }
+}
+
+// debug: launch plan of a GEMV (cluster size, CTAs, ring stages, resident CTAs per SM)
+void gemv_debug_plan(bool q4, int bits, int NT, int N, int K, int sms, int hint, int* out4) {
+  auto fill = [&](auto kern, int smem, int stages, ClusterPlan pl) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemv_occ_proxy, kGemvMaxThreads, smem);
+    out4[0] = pl.S;
+    out4[1] = pl.ncl * pl.S;
+    out4[2] = stages;
+    out4[3] = per;
+    const int probe[4] = {0, 50000, 100000, 110000};
+    for (int i = 0; i < 4; ++i) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kGemvMaxThreads, probe[i]);
+      out4[4 + i] = per;
+    }
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    out4[8] = fa.numRegs;
+    out4[9] = int(fa.sharedSizeBytes);
+    out4[10] = fa.maxDynamicSharedSizeBytes;
+    out4[11] = fa.preferredShmemCarveout;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
+    out4[12] = v;
+    cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, 0);
+    out4[13] = v;
+    out4[14] = fa.maxThreadsPerBlock;
+    out4[15] = smem;
+  };
+  if (q4 && bits == 4 && NT <= 2) {
+    using C = GemvCfg<4, 2>;
+    const ClusterPlan pl = cluster_plan<4, 2>(N, K, sms, hint);
+    const int st = ensure_attrs<4, 2, true, 8>();
+    fill(gemv_kernel<4, 2, true, 8>, C::smem_for(st), st, pl);
   }
 }
 
 // the K2 dequant-GEMV / bf16 GEMV: NT = 2 (M <= 16) or 4 (M <= 32)
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st) {
-  const bool nt2 = p.NT <= 2;
+  // M <= 8: only 8 accumulator columns per row are kept (MV = 8)
+  const int mode = p.NT > 2 ? 2 : (p.epi.M <= 8 ? 0 : 1);
   if (!q4) {
-    nt2 ? launch_mode<16, 2>(p, grid, pdl, st) : launch_mode<16, 4>(p, grid, pdl, st);
+    if (mode == 0) launch_mode<16, 2, 8>(p, grid, pdl, st);
+    else if (mode == 1) launch_mode<16, 2, 16>(p, grid, pdl, st);
+    else launch_mode<16, 4, 32>(p, grid, pdl, st);
   } else if (p.qbits == 2) {
-    nt2 ? launch_mode<2, 2>(p, grid, pdl, st) : launch_mode<2, 4>(p, grid, pdl, st);
+    if (mode == 0) launch_mode<2, 2, 8>(p, grid, pdl, st);
+    else if (mode == 1) launch_mode<2, 2, 16>(p, grid, pdl, st);
+    else launch_mode<2, 4, 32>(p, grid, pdl, st);
   } else {
-    nt2 ? launch_mode<4, 2>(p, grid, pdl, st) : launch_mode<4, 4>(p, grid, pdl, st);
+    if (mode == 0) launch_mode<4, 2, 8>(p, grid, pdl, st);
+    else if (mode == 1) launch_mode<4, 2, 16>(p, grid, pdl, st);
+    else launch_mode<4, 4, 32>(p, grid, pdl, st);
   }
 }
 

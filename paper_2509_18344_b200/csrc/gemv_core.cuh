@@ -5,13 +5,24 @@
 
 namespace ss {
 
-// Warp roles of the tcgen05 K2 kernel (gemv.cu): 0 producer (TMA), 1 MMA issuer + TMEM owner,
-// 2..5 convert (4-/2-bit codes -> bf16 A operand in TMEM), 6..9 accumulate (per-group TMEM
-// accumulators -> fp32 rows).  Warps 2..9 (256 threads) run the split-K reduction and epilogue.
-constexpr int kGemvWarps = 10;
-constexpr int kGemvThreads = kGemvWarps * 32;
-constexpr int kGemvWorkers = 256;        // warps 2..9
+// Warp roles of the tcgen05 K2 kernel (gemv.cu), one CTA per SM: 0 producer (TMA), 1 MMA issuer +
+// TMEM owner, 2..9 convert (quadrant w % 4, 64-group (w - 2) / 4 of every tile-chunk: 4-/2-bit codes ->
+// bf16 A operand in TMEM), 10..13 accumulate (quadrant w % 4: per-group TMEM accumulators -> fp32
+// rows), 14.. further MMA issuers.  Substitutes use 2 (MV = 32) or 4 MMA warps: warp (G, parity)
+// issues the MMAs of 64-group G of the tile-chunks of that parity (MMA issue from one thread is ~13
+// instructions per tcgen05.mma and shares its sub-partition with three busy warps).  Warps 2..13
+// (384 threads) run the split-K reduction and epilogue.
+template <int WF, int MV>
+struct GemvShape {
+  static constexpr int kMmaWarps = WF == 16 ? 1 : (MV <= 16 ? 4 : 2);
+  static constexpr int kWarps = 14 + (kMmaWarps > 1 ? kMmaWarps - 1 : 0);
+  static constexpr int kThreads = kWarps * 32;
+  static constexpr int kMaxReg = kWarps > 16 ? 96 : 128;   // <= 5 warps x 96 x 32 per sub-partition
+};
+constexpr int kGemvMaxThreads = 17 * 32;
+constexpr int kGemvWorkers = 384;        // warps 2..13
 constexpr int kGemvMaxCluster = 8;       // largest (portable) cluster the split factor may use
+constexpr int kGemvSmemBudget = 227 * 1024;
 
 // WF: weight format, 16 = bf16 (A from shared memory), 4 / 2 = group-64 substitutes (A dequantised
 // into TMEM).  NT: token groups of 8 (MMA N = 8 NT: 16 or 32).
@@ -26,19 +37,27 @@ struct GemvCfg {
   static constexpr int kSBytes = kQ ? 2 * kN * 4 : 0;           // group sums of x: [2 groups][N] fp32
   static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
   static constexpr int kMaxStages = 16;
-  static constexpr int kASlots = 2, kDSlots = 2;                // TMEM A operand / accumulator slots
-  static constexpr int kACol0 = kDSlots * kN;                   // A slots follow the D slots
-  static constexpr int kTmemCols = kQ ? 128 : (kDSlots * kN <= 32 ? 32 : 64);
+  // TMEM (all 512 columns): Q: 4 chunk slots of accumulators (2 groups x N columns) then 4 A slots of
+  // 64 columns (128 k as bf16 pairs); bf16: 2 tile slots of N columns
+  static constexpr int kSlots = kQ ? 4 : 2;
+  static constexpr int kDCols = kQ ? 2 * kN : kN;
+  static constexpr int kACol0 = kSlots * kDCols;
+  static constexpr int kTmemCols = 512;
+  static constexpr int kMetaSlots = 8;                          // scale/zero + group-sum side buffer
+  static constexpr int kMetaBytes = kQ ? kMetaSlots * (2 * kTileRows * 4 + 2 * kN * 4) : 0;
   static constexpr int kTileFloats = kTileRows * kN;
   static constexpr int kXPreTokens = 8;
   static constexpr int kXPreFloats = kXPreTokens * kTileRows;
   // cluster reduction staging: [S][ceil(N/S)][128] fp32 partial columns pushed by the ranks
   static constexpr int kStagingFloats = (kN + kGemvMaxCluster - 1) * kTileRows;
-  static constexpr int kBars = 2 * kMaxStages + 2 * kASlots + 2 * kDSlots + 2;
-  static constexpr int smem_for(int S) {
-    return S * kStageBytes + kTileFloats * 4 + kStagingFloats * 4 + kBars * 8 + 64 + 512 + kXPreFloats * 4;
+  static constexpr int kBars = 2 * kMaxStages + 3 * 4 + 2 + 2;   // full, empty, go, a_empty, d_full, d_empty, xbar
+  static constexpr int kFixed = kTileFloats * 4 + kStagingFloats * 4 + kMetaBytes + kBars * 8 + 64 + 512 + kXPreFloats * 4;
+  static constexpr int smem_for(int S) { return S * kStageBytes + kFixed; }
+  static constexpr int stages() {
+    const int s = (kGemvSmemBudget - kFixed - 1024) / kStageBytes;
+    return s > kMaxStages ? kMaxStages : (s < 2 ? 2 : s);
   }
-  static_assert(kQ ? (2 * kASlots * 16 + kDSlots * kN <= kTmemCols) : true, "TMEM columns");
+  static_assert(kACol0 + (kQ ? kSlots * 64 : 0) <= kTmemCols, "TMEM columns");
 };
 SS_HD int64_t owner_of(int64_t t, int64_t T, int G) { return ((t + 1) * G - 1) / T; }
 

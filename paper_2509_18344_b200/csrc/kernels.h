@@ -76,7 +76,10 @@ struct GemvParams {
   int64_t pf_bytes;
   unsigned long long* trace;     // optional %globaltimer trace: [kTraceEvents] events of this launch (debug)
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
+  unsigned long long* gtrace;    // optional per-group clock64 events of CTA 0 [64][8] (debug)
   int ctas_per_sm;               // cluster plan: resident CTAs per SM to plan for (0 = default 2)
+  int self_pf;                   // substitutes: L2-prefetch this CTA's whole weight range at entry
+  int dbg;                       // debug A/B bits (ss_debug_set_knob 1)
   int qbits;                     // code bits of a quantised matrix: 4 (0 = 4) or 2 (NEXT-3)
   EpiParams epi;
 };
@@ -85,6 +88,7 @@ int gemv_max_segments(int N, int K, int grid);   // grid: the Stream-K grid (gem
 int gemv_streamk_grid(bool q4, int N, int K, int sms);
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits = 4);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
+void gemv_debug_plan(bool q4, int bits, int NT, int N, int K, int sms, int hint, int* out4);
 
 struct GemmParams {
   const uint8_t* W;              // tiled BF16 weights [N x K]
