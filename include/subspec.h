@@ -282,14 +282,6 @@ ss_status ss_debug_time_matmul(ss_ctx* ctx, int32_t which, int32_t layer, int32_
 /* Debug A/B switches of the kernels (tests and tools only): knob 0 = K2 L2 self-prefetch of each
  * CTA's weight range (1 default, 0 off).  Captured draft graphs are dropped. */
 ss_status ss_debug_set_knob(ss_ctx* ctx, int32_t knob, int32_t value);
-/* Launch plan of the 4-bit draft GEMV of matrix group `group` at M tokens: out4 = {cluster size S,
- * CTAs, ring stages, resident CTAs per SM by the occupancy calculator}. */
-ss_status ss_debug_gemv_plan(ss_ctx* ctx, int32_t group, int32_t M, int32_t* out16);
-/* One draft GEMV launch of (layer, group) with M tokens, traced: out[g*8 + e] = clock64 of event e
- * of quantisation group g (first 64 groups of CTA 0): 0 converted, 1 A slot free, 2 A slot filled,
- * 3 MMA sees A, 4 MMA sees D slot, 5 MMAs committed, 6 accumulator ready, 7 accumulator consumed. */ 
-ss_status ss_debug_group_trace(ss_ctx* ctx, int32_t layer, int32_t group, int32_t M, int64_t* out);
-
 /* Time the draft forward of M frontier nodes (one draft pass incl. head, no top-k): average device ms
  * over `iters` eager launches.  skip: bit mask of kernel classes left out (1 attention, 2 RMSNorm,
  * 4 dequant-GEMVs, 8 head) — attribution only; results are not meaningful when skip != 0. */

@@ -97,8 +97,6 @@ _FUNCS = {
     "ss_debug_read_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
     "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_time_pass": [c_void_p, c_int32, c_int32, c_int32, P(c_float)],
-    "ss_debug_group_trace": [c_void_p, c_int32, c_int32, c_int32, c_void_p],
-    "ss_debug_gemv_plan": [c_void_p, c_int32, c_int32, c_void_p],
     "ss_debug_set_knob": [c_void_p, c_int32, c_int32],
     "ss_debug_trace_pass": [c_void_p, c_int32, c_void_p, c_int32, P(c_int32)],
     "ss_debug_cta_trace": [c_void_p, c_int32, c_int32, c_void_p, c_int32, P(c_int32)],
@@ -413,17 +411,6 @@ class SubSpec:
 
     def debug_set_knob(self, knob, value):
         self._check(self.lib.ss_debug_set_knob(self.ctx, knob, value))
-
-    def debug_gemv_plan(self, group, M):
-        out = np.zeros(16, np.int32)
-        self._check(self.lib.ss_debug_gemv_plan(self.ctx, group, M, _ptr(out)))
-        return dict(zip(("S", "ctas", "stages", "ctas_per_sm", "occ0", "occ50k", "occ100k", "occ110k", "regs", "static_smem",
-                         "max_dyn", "carveout", "sm_smem", "reserved", "max_thr", "smem"), out.tolist()))
-
-    def debug_group_trace(self, layer, group, M):
-        out = np.zeros(64 * 16, np.int64)
-        self._check(self.lib.ss_debug_group_trace(self.ctx, layer, group, M, _ptr(out)))
-        return out.reshape(64, 16)
 
     def debug_time_matmul(self, layer, group, M, iters=20):
         ms = c_float()

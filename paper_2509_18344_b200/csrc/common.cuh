@@ -35,37 +35,44 @@ SS_HD uint64_t bf16_tiled_offset(int64_t n, int64_t k, int64_t K) {   // in byte
   return uint64_t(tc) * kBF16TileBytes + core_off(nn >> 3, kk >> 3, nn & 7, kk & 7);
 }
 
-// Q4 substitutes (tcgen05 K2): per tile-chunk, for 64-group G (k = 64G .. 64G + 63 of the chunk),
-// codes at G * 4096 + half * 2048 + row * 16 (16 B = the 32 codes k = 64G + 32 half + 0..31 of one
-// row; word j holds k = 8j .. 8j + 7 of the half: the code of k = 8j + 2p sits at bits 4p..4p+3 and
-// that of k = 8j + 2p + 1 at bits 16 + 4p.., so (word >> 4p) & 0x000F000F is the pair's bf16x2
-// mantissa bits), then meta (s bf16 lo16, z bf16 hi16) at 8192 + G * 512 + row * 4.
+// Q4 substitutes: codes in mma.m16n8k16 A-fragment order with natural k.  Per tile-chunk, for warp
+// w (rows 16w .. 16w+15), 64-group G and lane (g = lane / 4, t4 = lane % 4): 16 bytes at
+// ((w * 2 + G) * 32 + lane) * 16 = [row 16w+g: word0, word1][row 16w+g+8: word0, word1].  Word h
+// holds the k-steps k4 = 2h, 2h+1 of the group; pair p = 2 (k4 % 2) + e (e = 0: k = 16 k4 + 2 t4,
+// +1; e = 1: k + 8, +9) has its first code at bits 4p .. 4p+3 and its second at bits 16 + 4p, so
+// (word >> 4p) & 0x000F000F is the pair's bf16x2 mantissa bits (the A registers a0..a3 of the
+// k-step).  Then meta (s bf16 lo16, z bf16 hi16) at 8192 + G * 512 + row * 4.
 SS_HD uint64_t q4_tile_base(int64_t n, int64_t k, int64_t K) {
   return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ4TileBytes;
 }
 SS_HD void q4_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
   const int row = int(n & 127), kk = int(k & 127);
-  const int G = kk >> 6, half = (kk >> 5) & 1, j = (kk >> 3) & 3, q = kk & 7, p = q >> 1;
-  const int bit = (q & 1) * 16 + 4 * p;
-  *byte_off = q4_tile_base(n, k, K) + uint64_t(G * 4096 + half * 2048 + row * 16 + j * 4 + (bit >> 3));
+  const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
+  const int G = kk >> 6, kl = kk & 63, k4 = kl >> 4, r16 = kl & 15;
+  const int t4 = (r16 & 7) >> 1, e = r16 >> 3, d = r16 & 1;
+  const int lane = g * 4 + t4, p = 2 * (k4 & 1) + e, bit = d * 16 + 4 * p;
+  *byte_off = q4_tile_base(n, k, K) + uint64_t(((w * 2 + G) * 32 + lane) * 16 + h * 8 + (k4 >> 1) * 4 + (bit >> 3));
   *shift = bit & 7;
 }
 SS_HD uint64_t q4_meta_offset(int64_t n, int64_t k, int64_t K) {     // bytes; 4 B (s lo16, z hi16)
   return q4_tile_base(n, k, K) + kQ4CodeBytes + uint64_t(((k & 127) >> 6) * 512 + (n & 127) * 4);
 }
 
-// Q2 (NEXT-3, 2-bit substitutes): per 64-group G, codes at G * 2048 + row * 16 (16 B = the row's 64
-// codes; word j holds k = 16j .. 16j + 15: k = 16j + 2p at bits 2p, k = 16j + 2p + 1 at bits 16 + 2p,
-// so (word >> 2p) & 0x00030003 is a pair), meta as Q4 at kQ2CodeBytes + G * 512 + row * 4.
+// Q2 (NEXT-3, 2-bit substitutes): per (w, G, lane) 8 bytes = [row g word][row g+8 word]; pair
+// p = 2 k4 + e (k as for Q4) at bits 2p (first) and 16 + 2p (second), so (word >> 2p) & 0x00030003
+// is a pair; meta as Q4 at kQ2CodeBytes + G * 512 + row * 4.
 constexpr int kQ2CodeBytes = 4096;  // 128 x 128 x 2 bit
 constexpr int kQ2TileBytes = kQ2CodeBytes + kQ4MetaBytes;   // 5120
 SS_HD int qtile_bytes(int bits) { return bits == 2 ? kQ2TileBytes : kQ4TileBytes; }
 SS_HD int qcode_bytes(int bits) { return bits == 2 ? kQ2CodeBytes : kQ4CodeBytes; }
 SS_HD void q2_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
   const int row = int(n & 127), kk = int(k & 127);
-  const int G = kk >> 6, j = (kk >> 4) & 3, q = kk & 15, p = q >> 1;
-  const int bit = (q & 1) * 16 + 2 * p;
-  *byte_off = uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes + uint64_t(G * 2048 + row * 16 + j * 4 + (bit >> 3));
+  const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
+  const int G = kk >> 6, kl = kk & 63, k4 = kl >> 4, r16 = kl & 15;
+  const int t4 = (r16 & 7) >> 1, e = r16 >> 3, d = r16 & 1;
+  const int lane = g * 4 + t4, p = 2 * k4 + e, bit = d * 16 + 2 * p;
+  *byte_off = uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes +
+              uint64_t(((w * 2 + G) * 32 + lane) * 8 + h * 4 + (bit >> 3));
   *shift = bit & 7;
 }
 SS_HD uint64_t q2_meta_offset(int64_t n, int64_t k, int64_t K) {

@@ -1745,47 +1745,6 @@ ss_status ss_debug_set_knob(ss_ctx* c, int32_t knob, int32_t value) {
   return SS_OK;
 }
 
-ss_status ss_debug_gemv_plan(ss_ctx* c, int32_t group, int32_t M, int32_t* out4) {
-  GUARD(c);
-  if (group < 0 || group > 3 || !out4) return fail(c, SS_ERR_INVALID, "gemv_plan args");
-  gemv_debug_plan(true, c->sub_bits, gemv_nt(M), c->gN[group], c->gK[group], c->gv_grid, group == 0 ? 1 : 0, out4);
-  return check_launch(c, "gemv_plan");
-}
-
-ss_status ss_debug_group_trace(ss_ctx* c, int32_t layer, int32_t group, int32_t M, int64_t* out) {
-  GUARD(c);
-  if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || M < 1 || M > 32 || !out ||
-      c->lw[layer].resident)
-    return fail(c, SS_ERR_INVALID, "group_trace args (an offloaded layer)");
-  ss_status s = drain_stream(c);
-  if (s != SS_OK) return s;
-  const int N = c->gN[group], K = c->gK[group];
-  const LayerW& w = c->lw[layer];
-  GemvParams p{};
-  p.W = w.q4[group];
-  p.X = K == c->F ? c->actfrag : c->hfrag;
-  p.XS = K == c->F ? c->actxs : c->hxs;
-  p.N = N;
-  p.K = K;
-  p.NT = gemv_nt(M);
-  p.partials = c->gv_part;
-  p.counters = c->gv_cnt;
-  p.max_seg = gemv_max_segments(N, K, gemv_streamk_grid(true, N, K, c->gv_grid));
-  p.epi = base_epi(c, M);
-  p.epi.kind = EPI_STORE;
-  p.epi.out = c->at_o;
-  p.epi.ldo = N;
-  p.ctas_per_sm = group == 0 ? 1 : 0;
-  p.qbits = c->sub_bits;
-  launch_gemv(true, p, c->gv_grid, false, c->cs);   // warm-up
-  CK(cudaMemsetAsync(c->tracebuf, 0, 64 * 16 * 8, c->cs));
-  p.gtrace = c->tracebuf;
-  launch_gemv(true, p, c->gv_grid, false, c->cs);
-  CK(cudaMemcpyAsync(out, c->tracebuf, 64 * 16 * 8, cudaMemcpyDeviceToHost, c->cs));
-  CK(cudaStreamSynchronize(c->cs));
-  return check_launch(c, "group_trace");
-}
-
 ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, float* out_ms) {
   GUARD(c);
   if (c->state != ST_SESSION || M < 1 || M > std::min(32, c->max_nodes - 1) || iters < 1 || !out_ms)

@@ -686,13 +686,11 @@ static ClusterPlan cluster_plan(int N, int K, int sms, int hint = 0) {
   return plan;
 }
 
-// every row tile has its own resident CTA or cluster (required by EPI_RESID_NORM's in-kernel barrier)
+// every row tile has its own resident cluster (required by EPI_RESID_NORM's in-kernel barrier)
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits) {
+  if (q4) return gemv_q_tiles_all_resident(NT, N, K, sms, bits);
   if (!gemv_use_cluster(N, K, sms)) return false;
-  const int nt = NT <= 2 ? 2 : 4;
-  if (!q4) return nt == 2 ? cluster_plan<16, 2>(N, K, sms).all_resident : cluster_plan<16, 4>(N, K, sms).all_resident;
-  if (bits == 2) return nt == 2 ? cluster_plan<2, 2>(N, K, sms).all_resident : cluster_plan<2, 4>(N, K, sms).all_resident;
-  return nt == 2 ? cluster_plan<4, 2>(N, K, sms).all_resident : cluster_plan<4, 4>(N, K, sms).all_resident;
+  return NT <= 2 ? cluster_plan<16, 2>(N, K, sms).all_resident : cluster_plan<16, 4>(N, K, sms).all_resident;
 }
 
 template <int WF, int NT, bool kCluster, int MV>
@@ -735,59 +733,17 @@ static void launch_mode(const GemvParams& p, int sms, bool pdl, cudaStream_t st)
   }
 }
 
-// debug: launch plan of a GEMV (cluster size, CTAs, ring stages, resident CTAs per SM)
-void gemv_debug_plan(bool q4, int bits, int NT, int N, int K, int sms, int hint, int* out4) {
-  auto fill = [&](auto kern, int smem, int stages, ClusterPlan pl) {
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemv_occ_proxy, kGemvMaxThreads, smem);
-    out4[0] = pl.S;
-    out4[1] = pl.ncl * pl.S;
-    out4[2] = stages;
-    out4[3] = per;
-    const int probe[4] = {0, 50000, 100000, 110000};
-    for (int i = 0; i < 4; ++i) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kGemvMaxThreads, probe[i]);
-      out4[4 + i] = per;
-    }
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, kern);
-    out4[8] = fa.numRegs;
-    out4[9] = int(fa.sharedSizeBytes);
-    out4[10] = fa.maxDynamicSharedSizeBytes;
-    out4[11] = fa.preferredShmemCarveout;
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
-    out4[12] = v;
-    cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, 0);
-    out4[13] = v;
-    out4[14] = fa.maxThreadsPerBlock;
-    out4[15] = smem;
-  };
-  if (q4 && bits == 4 && NT <= 2) {
-    using C = GemvCfg<4, 2>;
-    const ClusterPlan pl = cluster_plan<4, 2>(N, K, sms, hint);
-    const int st = ensure_attrs<4, 2, true, 8>();
-    fill(gemv_kernel<4, 2, true, 8>, C::smem_for(st), st, pl);
-  }
-}
-
-// the K2 dequant-GEMV / bf16 GEMV: NT = 2 (M <= 16) or 4 (M <= 32)
+// the draft GEMVs: substitutes on the mma.sync kernel (gemv_q.cu), bf16 on tcgen05 (this file);
+// NT = 2 (M <= 16) or 4 (M <= 32)
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st) {
-  // M <= 8: only 8 accumulator columns per row are kept (MV = 8)
-  const int mode = p.NT > 2 ? 2 : (p.epi.M <= 8 ? 0 : 1);
-  if (!q4) {
-    if (mode == 0) launch_mode<16, 2, 8>(p, grid, pdl, st);
-    else if (mode == 1) launch_mode<16, 2, 16>(p, grid, pdl, st);
-    else launch_mode<16, 4, 32>(p, grid, pdl, st);
-  } else if (p.qbits == 2) {
-    if (mode == 0) launch_mode<2, 2, 8>(p, grid, pdl, st);
-    else if (mode == 1) launch_mode<2, 2, 16>(p, grid, pdl, st);
-    else launch_mode<2, 4, 32>(p, grid, pdl, st);
-  } else {
-    if (mode == 0) launch_mode<4, 2, 8>(p, grid, pdl, st);
-    else if (mode == 1) launch_mode<4, 2, 16>(p, grid, pdl, st);
-    else launch_mode<4, 4, 32>(p, grid, pdl, st);
+  if (q4) {
+    launch_gemv_q(p, grid, pdl, st);
+    return;
   }
+  const int mode = p.NT > 2 ? 2 : (p.epi.M <= 8 ? 0 : 1);   // M <= 8: 8 accumulator columns per row
+  if (mode == 0) launch_mode<16, 2, 8>(p, grid, pdl, st);
+  else if (mode == 1) launch_mode<16, 2, 16>(p, grid, pdl, st);
+  else launch_mode<16, 4, 32>(p, grid, pdl, st);
 }
 
 }  // namespace ss

@@ -118,26 +118,30 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restri
     }
     const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), kLevels))) << 16);
     const float z = mn;
-    uint32_t words[8];
+    // codes in A-fragment order (common.cuh): lane t4 of this row's 8-row group takes the k with
+    // (k % 16) / 2 % 4 == t4; word h of lane t4 holds k-steps 2h, 2h+1
+    const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
+    uint32_t words[4][2];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) words[j] = 0u;
+    for (int t = 0; t < 4; ++t) words[t][0] = words[t][1] = 0u;
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       const float t = __fdiv_rn(__fsub_rn(x[i], z), sc);
       const uint32_t r = uint32_t(fminf(fmaxf(rintf(t), 0.0f), kLevels));
-      if constexpr (BITS == 2) {   // word j = i / 16; pair p = (i % 16) / 2 at bit 2p (+16 for odd i)
-        const int q = i & 15;
-        words[i >> 4] |= r << ((q & 1) * 16 + 2 * (q >> 1));
-      } else {                     // half h = i / 32, word j = (i % 32) / 8; pair p = (i % 8) / 2 at bit 4p (+16 odd)
-        const int q = i & 7;
-        words[i >> 3] |= r << ((q & 1) * 16 + 4 * (q >> 1));
+      const int k4 = i >> 4, r16 = i & 15, t4 = (r16 & 7) >> 1, e = r16 >> 3, d = r16 & 1;
+      if constexpr (BITS == 2) {
+        words[t4][0] |= r << (d * 16 + 2 * (2 * k4 + e));
+      } else {
+        words[t4][k4 >> 1] |= r << (d * 16 + 4 * (2 * (k4 & 1) + e));
       }
     }
-    if constexpr (BITS == 2) {
-      *reinterpret_cast<uint4*>(d_tile + G * 2048 + row * 16) = make_uint4(words[0], words[1], words[2], words[3]);
-    } else {
-      *reinterpret_cast<uint4*>(d_tile + G * 4096 + row * 16) = make_uint4(words[0], words[1], words[2], words[3]);
-      *reinterpret_cast<uint4*>(d_tile + G * 4096 + 2048 + row * 16) = make_uint4(words[4], words[5], words[6], words[7]);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int lane = g * 4 + t;
+      if constexpr (BITS == 2)
+        *reinterpret_cast<uint32_t*>(d_tile + ((w * 2 + G) * 32 + lane) * 8 + h * 4) = words[t][0];
+      else
+        *reinterpret_cast<uint2*>(d_tile + ((w * 2 + G) * 32 + lane) * 16 + h * 8) = make_uint2(words[t][0], words[t][1]);
     }
     *reinterpret_cast<uint32_t*>(d_tile + kCode + G * 512 + row * 4) = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
   }

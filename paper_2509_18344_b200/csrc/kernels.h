@@ -88,7 +88,8 @@ int gemv_max_segments(int N, int K, int grid);   // grid: the Stream-K grid (gem
 int gemv_streamk_grid(bool q4, int N, int K, int sms);
 bool gemv_tiles_all_resident(bool q4, int NT, int N, int K, int sms, int bits = 4);
 void launch_gemv(bool q4, const GemvParams& p, int grid, bool pdl, cudaStream_t st);
-void gemv_debug_plan(bool q4, int bits, int NT, int N, int K, int sms, int hint, int* out4);
+void launch_gemv_q(const GemvParams& p, int sms, bool pdl, cudaStream_t st);   // substitutes (gemv_q.cu)
+bool gemv_q_tiles_all_resident(int NT, int N, int K, int sms, int bits);
 
 struct GemmParams {
   const uint8_t* W;              // tiled BF16 weights [N x K]
