@@ -191,14 +191,15 @@ ss_status ss_build_substitutes(ss_ctx* ctx, const ss_quant_spec* q);
 ss_status ss_prefill(ss_ctx* ctx, const int32_t* prompt, int32_t n, int32_t chunk, int32_t* out_first_token);
 
 /* Draft pass loop (K2-K5): grow the tree from the current root (the last emitted token; or
- * root_token >= 0 to override).  Optional host outputs, each [1 + k*D_eff]: tokens, parents,
- * depths, cumulative log-scores (NULL to skip). *opt_n_nodes receives 1 + k*D_eff. */
+ * root_token >= 0 to override).  Optional host outputs, each [1 + k*D_eff] (batched: [B][1 + k*D_eff]
+ * over the active slots): tokens, parents, depths, cumulative log-scores (NULL to skip).
+ * *opt_n_nodes receives 1 + k*D_eff. */
 ss_status ss_draft_tree(ss_ctx* ctx, int32_t root_token, const ss_draft_params* p, int32_t* opt_tokens,
                         int32_t* opt_parents, int32_t* opt_depths, float* opt_scores, int32_t* opt_n_nodes);
 
 /* Verification (K6-K8): one target pass over every node; offloaded layers streamed from the
- * pinned host store (K7).  Optional host outputs [n_nodes]: target argmax per node and the
- * top-1/top-2 logit gap (near-tie flags). */
+ * pinned host store (K7).  Optional host outputs [n_nodes] (batched: [B][n_nodes]): target argmax
+ * per node and the top-1/top-2 logit gap (near-tie flags). */
 ss_status ss_verify_tree(ss_ctx* ctx, int32_t* opt_argmax, float* opt_gap);
 
 /* Greedy acceptance + KV commit/compaction (K9).  out_tokens (capacity D+1) receives the
@@ -266,13 +267,17 @@ ss_status ss_debug_get_substitute(ss_ctx* ctx, int32_t layer, int32_t group, uin
 ss_status ss_debug_matmul(ss_ctx* ctx, int32_t which /*0 draft K2, 1 target K6*/, int32_t layer, int32_t group,
                           const uint16_t* x, int32_t M, float* y);
 /* Teacher-forced forward of a depth-major tree (tokens/parents, n nodes) at the current committed
- * length: which = 0 draft (depth by depth, as the draft loop), 1 target (one pass).  Writes the
- * tree KV (draft or target values) but commits nothing.  out_logits [n x V] fp32 (host). */
+ * length: which = 0 draft (depth by depth, as the draft loop, the same kernels and batching), 1
+ * target (one pass).  Writes the tree KV (draft or target values) but commits nothing.  With
+ * B > 1 active slots the arrays are [B][n] (one tree per slot, all of one shape) and the passes
+ * batch the slots as ss_step_batch does.  out_logits [B][n][V] fp32; opt_hidden (NULL to skip)
+ * [B][n][hidden] fp32: the final RMSNorm output the head reads (bf16 values in SS_BF16). */
 ss_status ss_debug_forward(ss_ctx* ctx, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
-                           float* out_logits);
+                           float* out_logits, float* opt_hidden);
 /* Replace the device tree by a given depth-major tree (root first) for verify/accept tests. */
 ss_status ss_debug_set_tree(ss_ctx* ctx, const int32_t* tokens, const int32_t* parents, int32_t n, int32_t top_k);
-/* Committed K/V rows [pos0, pos0+n) of a layer -> host [n_kv x n x head_dim] bf16 bits each. */
+/* Committed K/V rows [pos0, pos0+n) of a layer -> host [n_kv x n x head_dim] bf16 bits each (batched
+ * slots: slot b's position p is row b * max_context + p). */
 ss_status ss_debug_read_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
 /* Time one launch of the draft dequant-GEMV of (layer, group) with M tokens: average device ms of
  * `iters` back-to-back launches (CUDA events on the compute stream). */

@@ -17,7 +17,7 @@ accept -> commit.
 import numpy as np
 
 from synth.configs import ModelConfig
-from .model import TargetWeights, KVCache, draft_layers, forward_nodes
+from .model import TargetWeights, KVCache, draft_layers, forward_nodes, forward_nodes_batched
 from .tree import build_tree, Tree
 from .verify import argmax_and_gap, accept, commit
 
@@ -27,11 +27,15 @@ class Session:
 
     def __init__(self, cfg: ModelConfig, seed: int, n_resident: int = 0, bits: int = 4,
                  group: int = 64, mode: str = "exact", max_nodes: int | None = None,
-                 target: TargetWeights | None = None):
+                 target: TargetWeights | None = None, dlayers=None):
+        """mode: "exact" (fp64), "bf16" (fp64 + the GPU's bf16 rounding points) or "bf16-fp32" (the
+        rounding points with fp32 weights and node-batched fp32 matrix products: full-width shapes)."""
         self.cfg, self.mode = cfg, mode
-        self.target = target if target is not None else TargetWeights(cfg, seed)
+        wdt = np.float32 if mode == "bf16-fp32" else np.float64
+        self.target = target if target is not None else TargetWeights(cfg, seed, dtype=wdt)
         self.tlayers = self.target.layers
-        self.dlayers = draft_layers(self.target, n_resident, bits, group)
+        # dlayers: a draft view built once and shared by several sessions (batched requests)
+        self.dlayers = dlayers if dlayers is not None else draft_layers(self.target, n_resident, bits, group)
         self.kv = KVCache(cfg, max_nodes or 512)
         self.n_forward_nodes = 0
 
@@ -39,16 +43,16 @@ class Session:
     def _forward(self, which, tokens, slots, positions, ancestors, **kw):
         layers = self.tlayers if which == "target" else self.dlayers
         self.n_forward_nodes += len(tokens)
-        return forward_nodes(self.cfg, layers, self.target, self.kv, tokens, slots,
-                             positions, ancestors, self.mode, **kw)
+        fwd = forward_nodes_batched if self.mode == "bf16-fp32" else forward_nodes
+        return fwd(self.cfg, layers, self.target, self.kv, tokens, slots, positions, ancestors, self.mode, **kw)
 
-    def forward_tree(self, which, tree: Tree, slots=None):
-        """Teacher-forced forward of tree nodes (all nodes if slots is None)."""
+    def forward_tree(self, which, tree: Tree, slots=None, **kw):
+        """Teacher-forced forward of tree nodes (all nodes if slots is None); kw: return_hidden."""
         slots = list(range(len(tree))) if slots is None else list(slots)
         P = self.kv.P
         return self._forward(which, [tree.tokens[s] for s in slots], slots,
                              [P + tree.depths[s] for s in slots],
-                             [tree.ancestors(s) for s in slots])
+                             [tree.ancestors(s) for s in slots], **kw)
 
     # -- O.9 -------------------------------------------------------------
     def prefill(self, prompt, chunk=256):

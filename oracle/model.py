@@ -29,7 +29,16 @@ SiLU-mul activation.  Logits, scores, softmax and the residual stream are
 never rounded.  Every node's arithmetic is a per-row op sequence identical to
 what an autoregressive forward would do at that position, so chain ==
 sequential and path replay hold bitwise.
+
+mode "bf16-fp32" (SURVEY §8(c) "fp32-BLAS mode", for the full-width shapes): the
+same steps and rounding points, with the weights held in float32 (bf16 values and
+the substitutes' code*s + z are exact in fp32) and each linear map one float32
+matrix product over all forwarded nodes (forward_nodes_batched).  Only the
+summation order and fp32 accumulation of the products differ from "bf16".
 """
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from synth.configs import ModelConfig
@@ -41,36 +50,62 @@ LAYER_MATS = ("wq", "wk", "wv", "wo", "wg", "wu", "wd")
 
 
 class TargetWeights:
-    """The target's bf16 weights as float64 arrays (all values exactly bf16)."""
+    """The target's bf16 weights as float64 (or, for mode "bf16-fp32", float32) arrays; every value
+    is exactly a bf16.  Matrices are generated in row blocks of `block_rows` (memory)."""
 
-    def __init__(self, cfg: ModelConfig, seed: int, layers=None):
+    def __init__(self, cfg: ModelConfig, seed: int, layers=None, dtype=np.float64, block_rows=4096):
         self.cfg = cfg
+        self.dtype = np.dtype(dtype)
         self.layers = [dict() for _ in range(cfg.n_layers)]
         want = set(range(cfg.n_layers)) if layers is None else set(layers)
+
+        def gen(tid, shape, kind, sigma):
+            if len(shape) == 1:
+                return bf16_bits_to_f64(gen_tensor_bits(seed, tid, shape, kind, sigma)).astype(self.dtype)
+            out = np.empty(shape, dtype=self.dtype)
+
+            def block(r0):   # row blocks are independent (counter-based generator): threads
+                r1 = min(shape[0], r0 + block_rows)
+                out[r0:r1] = bf16_bits_to_f64(gen_tensor_bits(seed, tid, shape, kind, sigma, rows=slice(r0, r1)))
+            with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+                list(ex.map(block, range(0, shape[0], block_rows)))
+            return out
+
         for tid, name, shape, kind, sigma in tensor_specs(cfg):
             if name.startswith("l"):
                 l = int(name[1:name.index(".")])
                 if l not in want:
                     continue
-                self.layers[l][name.split(".", 1)[1]] = bf16_bits_to_f64(
-                    gen_tensor_bits(seed, tid, shape, kind, sigma))
+                self.layers[l][name.split(".", 1)[1]] = gen(tid, shape, kind, sigma)
             else:
-                setattr(self, name, bf16_bits_to_f64(gen_tensor_bits(seed, tid, shape, kind, sigma)))
+                setattr(self, name, gen(tid, shape, kind, sigma))
 
 
-def draft_layers(target: TargetWeights, n_resident: int, bits=4, group=64):
+def draft_layers(target: TargetWeights, n_resident: int, bits=4, group=64, block_rows=2048):
     """Draft model view (SPEC.md:214-222 build_draft_view):
     layers [0, n_resident) are Shared (the target's own dict); the rest are
     Substitute: every linear matrix replaced by its dequantized low-bit copy,
-    norms and biases kept (reading R6)."""
+    norms and biases kept (reading R6).  Groups are rows' 64
+    consecutive inputs, so the substitute is computed row block by row block."""
     out = []
+    dt = getattr(target, "dtype", np.dtype(np.float64))
     for l, lw in enumerate(target.layers):
         if l < n_resident:
             out.append(lw)
         else:
             sub = dict(lw)
             for m in LAYER_MATS:
-                sub[m] = substitute_matrix(lw[m], bits, group)
+                w = lw[m]
+                q = np.empty(w.shape, dtype=dt)
+
+                def block(r0, w=w, q=q):   # groups lie inside rows: row blocks are independent
+                    blk = substitute_matrix(np.asarray(w[r0:r0 + block_rows], dtype=np.float64), bits, group)
+                    q[r0:r0 + block_rows] = blk
+                    if dt != np.float64:   # code*s + z must be exact in the storage type
+                        assert np.array_equal(q[r0:r0 + block_rows].astype(np.float64), blk), "substitute not exact in fp32"
+                with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+                    list(ex.map(block, range(0, w.shape[0], block_rows)))
+                sub[m] = q
             out.append(sub)
     return out
 
@@ -139,4 +174,69 @@ def forward_nodes(cfg: ModelConfig, layers, target: TargetWeights, kv: KVCache,
     logits = np.stack([target.head @ hf[i] for i in range(n)])
     if return_hidden:
         return logits, np.stack(hf)
+    return logits
+
+
+def _rmsnorm_rows(X, g, eps):
+    """rmsnorm of every row of X (the per-row definition of numerics.rmsnorm)."""
+    return X / np.sqrt(np.mean(X * X, axis=1, keepdims=True) + eps) * g
+
+
+def _rope_rows(Q, positions, theta, d):
+    """Rotate-half RoPE of every head vector: Q [n, heads, d], positions [n] (numerics.rope_rotate_half)."""
+    half = d // 2
+    j = np.arange(half, dtype=np.float64)
+    ang = np.asarray(positions, dtype=np.float64)[:, None] * theta ** (-2.0 * j / d)   # [n, half]
+    c, s = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    a, b = Q[..., :half], Q[..., half:]
+    return np.concatenate([a * c - b * s, b * c + a * s], axis=-1)
+
+
+def forward_nodes_batched(cfg: ModelConfig, layers, target: TargetWeights, kv: KVCache,
+                          tokens, slots, positions, ancestors, mode="bf16-fp32", return_hidden=False):
+    """forward_nodes with each linear map applied to all nodes as one matrix product in the weights'
+    storage type (float32 for mode "bf16-fp32").  Same steps, order and rounding points as
+    forward_nodes; every node still attends only to its own key list (prefix ++ ancestors)."""
+    R = round_bf16 if mode in ("bf16", "bf16-fp32") else (lambda a: a)
+    n = len(tokens)
+    H, nh, nkv, d = cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+    grp = nh // nkv
+    P = kv.P
+    wdt = getattr(target, "dtype", np.dtype(np.float64))
+
+    def mm(A, W):   # A [n, K] (float64 values), W [N, K] -> [n, N] float64
+        return (A.astype(wdt) @ W.T).astype(np.float64)
+
+    X = np.stack([target.embed[int(t)].astype(np.float64) for t in tokens])
+    inv_sqrt_d = 1.0 / np.sqrt(d)
+    slots = list(slots)
+    for l, lw in enumerate(layers):
+        Hn = R(_rmsnorm_rows(X, lw["attn_norm"].astype(np.float64), cfg.rms_eps))
+        Q, Kx, Vx = mm(Hn, lw["wq"]), mm(Hn, lw["wk"]), mm(Hn, lw["wv"])
+        if cfg.qkv_bias:
+            Q = Q + lw["bq"].astype(np.float64)
+            Kx = Kx + lw["bk"].astype(np.float64)
+            Vx = Vx + lw["bv"].astype(np.float64)
+        Q = R(_rope_rows(Q.reshape(n, nh, d), positions, cfg.rope_theta, d))
+        Kx = R(_rope_rows(Kx.reshape(n, nkv, d), positions, cfg.rope_theta, d))
+        kv.tK[l, slots] = Kx
+        kv.tV[l, slots] = R(Vx.reshape(n, nkv, d))
+        O = np.empty((n, nh, d))
+        for i in range(n):
+            anc = list(ancestors[i])
+            for g in range(nkv):
+                Kall = np.concatenate([kv.K[l, :P, g], kv.tK[l, anc, g]])
+                Vall = np.concatenate([kv.V[l, :P, g], kv.tV[l, anc, g]])
+                S = (Q[i, g * grp:(g + 1) * grp] @ Kall.T) * inv_sqrt_d      # [grp, keys]
+                E = np.exp(S - S.max(axis=1, keepdims=True))
+                O[i, g * grp:(g + 1) * grp] = (E / E.sum(axis=1, keepdims=True)) @ Vall
+        O = R(O.reshape(n, nh * d))
+        X = X + mm(O, lw["wo"])
+        H2 = R(_rmsnorm_rows(X, lw["mlp_norm"].astype(np.float64), cfg.rms_eps))
+        A = R(silu(mm(H2, lw["wg"])) * mm(H2, lw["wu"]))
+        X = X + mm(A, lw["wd"])
+    HF = R(_rmsnorm_rows(X, target.final_norm.astype(np.float64), cfg.rms_eps))
+    logits = mm(HF, target.head)
+    if return_hidden:
+        return logits, HF
     return logits

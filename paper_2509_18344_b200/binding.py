@@ -78,7 +78,7 @@ _FUNCS = {
     "ss_prefill": [c_void_p, c_void_p, c_int32, c_int32, P(c_int32)],
     "ss_draft_tree": [c_void_p, c_int32, P(DraftParamsC), c_void_p, c_void_p, c_void_p, c_void_p, P(c_int32)],
     "ss_verify_tree": [c_void_p, c_void_p, c_void_p],
-    "ss_accept_and_commit": [c_void_p, c_void_p, P(c_int32), c_void_p],
+    "ss_accept_and_commit": [c_void_p, c_void_p, c_void_p, c_void_p],
     "ss_step": [c_void_p, P(DraftParamsC), c_void_p, P(c_int32)],
     "ss_generate": [c_void_p, c_void_p, c_int32, c_int32, c_int32, P(DraftParamsC), c_void_p, P(c_int32), c_void_p],
     "ss_set_batch": [c_void_p, c_int32],
@@ -92,7 +92,7 @@ _FUNCS = {
     "ss_debug_read_group": [c_void_p, c_int32, c_int32, c_void_p],
     "ss_debug_get_substitute": [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p],
     "ss_debug_matmul": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p],
-    "ss_debug_forward": [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p],
+    "ss_debug_forward": [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p, c_void_p],
     "ss_debug_set_tree": [c_void_p, c_void_p, c_void_p, c_int32, c_int32],
     "ss_debug_read_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
     "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
@@ -256,33 +256,46 @@ class SubSpec:
         self._check(self.lib.ss_prefill(self.ctx, _ptr(p), len(p), chunk, ctypes.byref(out)))
         return out.value
 
-    def draft_tree(self, depth, top_k, sharpen_t, root_token=-1, want_tree=True):
+    def draft_tree(self, depth, top_k, sharpen_t, root_token=-1, want_tree=True, n_req=1):
+        """n_req > 1 (batched slots): every array is [n_req, n_nodes]."""
         n_max = 1 + top_k * depth
-        arrs = [np.zeros(n_max, np.int32), np.zeros(n_max, np.int32), np.zeros(n_max, np.int32),
-                np.zeros(n_max, np.float32)] if want_tree else [None] * 4
+        arrs = [np.zeros(n_req * n_max, np.int32), np.zeros(n_req * n_max, np.int32), np.zeros(n_req * n_max, np.int32),
+                np.zeros(n_req * n_max, np.float32)] if want_tree else [None] * 4
         n = c_int32()
         self._check(self.lib.ss_draft_tree(self.ctx, root_token, ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)),
                                            *[_ptr(a) for a in arrs], ctypes.byref(n)))
         if not want_tree:
             return n.value
-        return {"tokens": arrs[0][:n.value], "parents": arrs[1][:n.value], "depths": arrs[2][:n.value],
-                "scores": arrs[3][:n.value]}
+        nn = n.value
+        cut = (lambda a: a[:nn]) if n_req == 1 else (lambda a: a[:n_req * nn].reshape(n_req, nn))
+        return {"tokens": cut(arrs[0]), "parents": cut(arrs[1]), "depths": cut(arrs[2]), "scores": cut(arrs[3])}
 
-    def verify_tree(self, n_nodes=None, want=True):
+    def verify_tree(self, n_nodes=None, want=True, n_req=1):
         if not want:
             self._check(self.lib.ss_verify_tree(self.ctx, None, None))
             return None
-        am = np.zeros(n_nodes, np.int32)
-        gap = np.zeros(n_nodes, np.float32)
+        am = np.zeros(n_req * n_nodes, np.int32)
+        gap = np.zeros(n_req * n_nodes, np.float32)
         self._check(self.lib.ss_verify_tree(self.ctx, _ptr(am), _ptr(gap)))
+        if n_req > 1:
+            return am.reshape(n_req, n_nodes), gap.reshape(n_req, n_nodes)
         return am, gap
+
+    def accept_and_commit_batch(self, n_req, stride):
+        """Batched accept/commit: per-slot emitted tokens and committed tree slots (root first)."""
+        toks = np.zeros(n_req * stride, np.int32)
+        path = np.zeros(n_req * stride, np.int32)
+        n = np.zeros(n_req, np.int32)
+        self._check(self.lib.ss_accept_and_commit(self.ctx, _ptr(toks), _ptr(n), _ptr(path)))
+        return ([toks[b * stride: b * stride + n[b]].tolist() for b in range(n_req)],
+                [path[b * stride: b * stride + n[b]].tolist() for b in range(n_req)])
 
     def accept_and_commit(self, cap):
         toks = np.zeros(cap, np.int32)
         path = np.zeros(cap, np.int32)
-        n = c_int32()
-        self._check(self.lib.ss_accept_and_commit(self.ctx, _ptr(toks), ctypes.byref(n), _ptr(path)))
-        return toks[:n.value].tolist(), path[:n.value].tolist()
+        n = np.zeros(1, np.int32)
+        self._check(self.lib.ss_accept_and_commit(self.ctx, _ptr(toks), _ptr(n), _ptr(path)))
+        return toks[:n[0]].tolist(), path[:n[0]].tolist()
 
     def step(self, depth, top_k, sharpen_t):
         toks = np.zeros(depth + 1, np.int32)
@@ -373,12 +386,19 @@ class SubSpec:
         self._check(self.lib.ss_debug_matmul(self.ctx, which, layer, group, _ptr(x), M, _ptr(y)))
         return y.reshape(M, N)
 
-    def debug_forward(self, which, tokens, parents):
+    def debug_forward(self, which, tokens, parents, hidden=False):
+        """tokens/parents [n] (or [B][n] with B active slots) -> logits [n, V] (or [B, n, V]);
+        hidden=True also returns the final normed hidden rows [.., n, hidden]."""
         t = np.ascontiguousarray(tokens, dtype=np.int32)
         p = np.ascontiguousarray(parents, dtype=np.int32)
-        out = np.zeros(len(t) * self.cfg.vocab, np.float32)
-        self._check(self.lib.ss_debug_forward(self.ctx, which, _ptr(t), _ptr(p), len(t), _ptr(out)))
-        return out.reshape(len(t), self.cfg.vocab)
+        n = t.shape[-1]
+        rows = t.size
+        out = np.zeros(rows * self.cfg.vocab, np.float32)
+        hid = np.zeros(rows * self.cfg.hidden, np.float32) if hidden else None
+        self._check(self.lib.ss_debug_forward(self.ctx, which, _ptr(t), _ptr(p), n, _ptr(out), _ptr(hid)))
+        shape = t.shape
+        lg = out.reshape(*shape, self.cfg.vocab)
+        return (lg, hid.reshape(*shape, self.cfg.hidden)) if hidden else lg
 
     def debug_set_tree(self, tokens, parents, top_k):
         t = np.ascontiguousarray(tokens, dtype=np.int32)

@@ -1319,10 +1319,13 @@ ss_status ss_draft_tree(ss_ctx* c, int32_t root_token, const ss_draft_params* p,
   if (s != SS_OK) return s;
   const int n = c->n_nodes;
   if (on) *on = n;
-  if (ot) CK(cudaMemcpyAsync(ot, c->tok, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
-  if (op) CK(cudaMemcpyAsync(op, c->parent, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
-  if (od) CK(cudaMemcpyAsync(od, c->depth, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
-  if (os) CK(cudaMemcpyAsync(os, c->score, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+  for (int b = 0; b < c->B; ++b) {   // batched: [B][n] over the active slots
+    const int64_t so = int64_t(b) * c->max_nodes, ho = int64_t(b) * n;
+    if (ot) CK(cudaMemcpyAsync(ot + ho, c->tok + so, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+    if (op) CK(cudaMemcpyAsync(op + ho, c->parent + so, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+    if (od) CK(cudaMemcpyAsync(od + ho, c->depth + so, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+    if (os) CK(cudaMemcpyAsync(os + ho, c->score + so, size_t(n) * 4, cudaMemcpyDeviceToHost, c->cs));
+  }
   if (ot || op || od || os) CK(cudaStreamSynchronize(c->cs));
   return SS_OK;
 }
@@ -1340,8 +1343,9 @@ ss_status ss_verify_tree(ss_ctx* c, int32_t* opt_argmax, float* opt_gap) {
   GUARD(c);
   ss_status s = verify_impl(c);
   if (s != SS_OK) return s;
-  if (opt_argmax) CK(cudaMemcpyAsync(opt_argmax, c->argmax, size_t(c->n_nodes) * 4, cudaMemcpyDeviceToHost, c->cs));
-  if (opt_gap) CK(cudaMemcpyAsync(opt_gap, c->gap, size_t(c->n_nodes) * 4, cudaMemcpyDeviceToHost, c->cs));
+  const size_t nn = size_t(c->B) * c->n_nodes;   // batched: [B][n_nodes], request-major rows
+  if (opt_argmax) CK(cudaMemcpyAsync(opt_argmax, c->argmax, nn * 4, cudaMemcpyDeviceToHost, c->cs));
+  if (opt_gap) CK(cudaMemcpyAsync(opt_gap, c->gap, nn * 4, cudaMemcpyDeviceToHost, c->cs));
   if (opt_argmax || opt_gap) CK(cudaStreamSynchronize(c->cs));
   return SS_OK;
 }
@@ -1845,56 +1849,94 @@ ss_status ss_debug_cta_trace(ss_ctx* c, int32_t M, int32_t launch, int64_t* out,
   return SS_OK;
 }
 
+// FragX rows [0, rows) of an activation buffer (layout NT) -> host fp32 [rows x cols] (debug)
+static ss_status read_fragx(ss_ctx* c, const uint16_t* buf, int rows, int cols, int NT, float* out) {
+  std::vector<uint16_t> h(size_t(NT) * 8 * cols);
+  CK(cudaMemcpyAsync(h.data(), buf, h.size() * 2, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  for (int m = 0; m < rows; ++m)
+    for (int k = 0; k < cols; ++k) {
+      const uint32_t b = uint32_t(h[fragx_offset(m, k, NT)]) << 16;
+      std::memcpy(out + int64_t(m) * cols + k, &b, 4);
+    }
+  return SS_OK;
+}
+
 ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
-                           float* out_logits) {
+                           float* out_logits, float* opt_hidden) {
   GUARD(c);
   if (c->state != ST_SESSION && c->state != ST_DRAFTED)
     return fail(c, SS_ERR_STRUCTURE, "debug_forward needs a session (or a drafted tree)");
   if (!tokens || !parents || n < 1 || n > c->max_nodes || !out_logits) return fail(c, SS_ERR_INVALID, "debug_forward args");
   if (which == 1 && c->state == ST_DRAFTED) return fail(c, SS_ERR_STRUCTURE, "target debug_forward inside a step");
-  // depth-major tree check + host-side depths/ancestors
-  std::vector<int> dep(n), anc(size_t(n) * c->anc_stride, 0), par(parents, parents + n), tk(tokens, tokens + n);
-  for (int i = 0; i < n; ++i) {
-    if (i == 0 ? parents[0] != -1 : (parents[i] < 0 || parents[i] >= i)) return fail(c, SS_ERR_STRUCTURE, "tree not depth-major");
-    dep[i] = i == 0 ? 0 : dep[parents[i]] + 1;
-    if (i > 0 && dep[i] < dep[i - 1]) return fail(c, SS_ERR_STRUCTURE, "tree not depth-major");
-    if (dep[i] >= c->anc_stride) return fail(c, SS_ERR_CAPACITY, "tree too deep");
-    if (tokens[i] < 0 || tokens[i] >= c->V) return fail(c, SS_ERR_INVALID, "token id");
-    int a = i, dd = dep[i];
-    while (a >= 0) {
-      anc[size_t(i) * c->anc_stride + dd--] = a;
-      a = parents[a];
+  // batched requests: tokens/parents/outputs are [B][n] over the active slots, trees of one shape
+  const int B = c->B;
+  std::vector<int> dep0(n);
+  for (int b = 0; b < B; ++b) {
+    const int32_t* tb = tokens + int64_t(b) * n;
+    const int32_t* pb = parents + int64_t(b) * n;
+    std::vector<int> dep(n), anc(size_t(n) * c->anc_stride, 0), par(pb, pb + n), tk(tb, tb + n);
+    for (int i = 0; i < n; ++i) {
+      if (i == 0 ? pb[0] != -1 : (pb[i] < 0 || pb[i] >= i)) return fail(c, SS_ERR_STRUCTURE, "tree not depth-major");
+      dep[i] = i == 0 ? 0 : dep[pb[i]] + 1;
+      if (i > 0 && dep[i] < dep[i - 1]) return fail(c, SS_ERR_STRUCTURE, "tree not depth-major");
+      if (dep[i] >= c->anc_stride) return fail(c, SS_ERR_CAPACITY, "tree too deep");
+      if (tb[i] < 0 || tb[i] >= c->V) return fail(c, SS_ERR_INVALID, "token id");
+      if (b > 0 && dep[i] != dep0[i]) return fail(c, SS_ERR_STRUCTURE, "batched debug_forward: trees of one shape");
+      int a = i, dd = dep[i];
+      while (a >= 0) {
+        anc[size_t(i) * c->anc_stride + dd--] = a;
+        a = pb[a];
+      }
     }
+    if (b == 0) dep0 = dep;
+    if (c->Pb[b] + dep[n - 1] + 1 > c->C) return fail(c, SS_ERR_CAPACITY, "tree beyond max_context");
+    std::vector<float> sc(n, 0.f);
+    const int64_t no = int64_t(b) * c->max_nodes;
+    CK(cudaMemcpyAsync(c->tok + no, tk.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaMemcpyAsync(c->parent + no, par.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaMemcpyAsync(c->depth + no, dep.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaMemcpyAsync(c->score + no, sc.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaMemcpyAsync(c->anc + no * c->anc_stride, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, c->cs));
+    CK(cudaStreamSynchronize(c->cs));   // the host vectors die with this iteration
   }
-  if (c->P + dep[n - 1] + 1 > c->C) return fail(c, SS_ERR_CAPACITY, "tree beyond max_context");
-  std::vector<float> sc(n, 0.f);
-  CK(cudaMemcpyAsync(c->tok, tk.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
-  CK(cudaMemcpyAsync(c->parent, par.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
-  CK(cudaMemcpyAsync(c->depth, dep.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
-  CK(cudaMemcpyAsync(c->score, sc.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->cs));
-  CK(cudaMemcpyAsync(c->anc, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, c->cs));
-  CK(cudaStreamSynchronize(c->cs));
   ss_status s;
+  std::vector<float> hid;
   if (which == 0) {
     int i0 = 0;
     while (i0 < n) {
       int i1 = i0;
-      while (i1 < n && dep[i1] == dep[i0]) ++i1;
-      if (i1 - i0 > 32) return fail(c, SS_ERR_INVALID, "draft debug forward: <= 32 nodes per depth");
+      while (i1 < n && dep0[i1] == dep0[i0]) ++i1;
+      const int rows = i1 - i0, M = B * rows;
+      if (M > 32) return fail(c, SS_ERR_INVALID, "draft debug forward: <= 32 rows per depth (all slots)");
       PassOut o;
       o.logits = true;
-      s = forward_pass(c, false, i1 - i0, i0, o);
+      c->cur_rq = batch_map(c, rows);
+      s = forward_pass(c, false, M, i0, o);
+      c->cur_rq = ReqMap{0, 0, 0, 0};
       if (s != SS_OK) return s;
-      CK(cudaMemcpyAsync(out_logits + int64_t(i0) * c->V, c->logits, size_t(i1 - i0) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
+      for (int b = 0; b < B; ++b)
+        CK(cudaMemcpyAsync(out_logits + (int64_t(b) * n + i0) * c->V, c->logits + int64_t(b) * rows * c->V,
+                           size_t(rows) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
+      if (opt_hidden) {   // the final normed rows the head just read (FragX, NT of the pass)
+        hid.resize(size_t(M) * c->H);
+        if ((s = read_fragx(c, c->hfrag, M, c->H, gemv_nt(M), hid.data())) != SS_OK) return s;
+        for (int b = 0; b < B; ++b)
+          std::memcpy(opt_hidden + (int64_t(b) * n + i0) * c->H, hid.data() + size_t(b) * rows * c->H,
+                      size_t(rows) * c->H * 4);
+      }
       CK(cudaStreamSynchronize(c->cs));
       i0 = i1;
     }
   } else {
     PassOut o;   // no head: we read logits via the GEMV head in 32-row groups below
     c->n_nodes = n;
-    if ((s = forward_pass(c, true, n, 0, o)) != SS_OK) return s;
-    for (int r0 = 0; r0 < n; r0 += 32) {
-      const int m = std::min(32, n - r0);
+    c->cur_rq = batch_map(c, n);   // rows request-major: request b's nodes at b * n
+    s = forward_pass(c, true, B * n, 0, o);
+    c->cur_rq = ReqMap{0, 0, 0, 0};
+    if (s != SS_OK) return s;
+    for (int r0 = 0; r0 < B * n; r0 += 32) {
+      const int m = std::min(32, B * n - r0);
       launch_rmsnorm(c->x + int64_t(r0) * c->H, m, c->H, c->final_norm, c->cfg.rms_eps, c->hfrag, c->hxs, gemv_nt(m), false, c->cs);
       GemvParams p{};
       p.W = c->head;
@@ -1911,6 +1953,8 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
       p.epi.ldo = c->V;
       launch_gemv(false, p, c->gv_grid, false, c->cs);
       CK(cudaMemcpyAsync(out_logits + int64_t(r0) * c->V, c->logits, size_t(m) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
+      if (opt_hidden && (s = read_fragx(c, c->hfrag, m, c->H, gemv_nt(m), opt_hidden + int64_t(r0) * c->H)) != SS_OK)
+        return s;
       CK(cudaStreamSynchronize(c->cs));
     }
   }
@@ -1955,7 +1999,8 @@ ss_status ss_debug_set_tree(ss_ctx* c, const int32_t* tokens, const int32_t* par
 
 ss_status ss_debug_read_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v) {
   GUARD(c);
-  if (layer < 0 || layer >= c->L || pos0 < 0 || n < 1 || pos0 + n > c->C || !k || !v)
+  // pos0 indexes the kv-head row space of all slots: slot b's committed rows start at b * max_context
+  if (layer < 0 || layer >= c->L || pos0 < 0 || n < 1 || pos0 + n > c->kv_ctx || !k || !v)
     return fail(c, SS_ERR_INVALID, "read_kv args");
   CK(cudaStreamSynchronize(c->cs));
   for (int h = 0; h < c->nkv; ++h) {
