@@ -30,7 +30,6 @@ from synth.configs import PRESETS, GIB  # noqa: E402
 from synth.prompts import mtbench_prompt  # noqa: E402
 
 SEED = 0x5EED
-TAU_FILE = os.path.join(ROOT, "profiles", "bench_tau.json")
 
 
 def args_():
@@ -53,6 +52,8 @@ def args_():
                     help="embedding GPU-resident in the arena (PAPER.md:534) instead of mapped host memory (R24)")
     ap.add_argument("--no-async", action="store_true",
                     help="Table-2 ablation: no copy/compute overlap in the verify streaming (PAPER.md:305-308)")
+    ap.add_argument("--prompts", type=int, default=4, help="prompt sweep: MT-Bench-shaped prompts (0 = skip)")
+    ap.add_argument("--repeats", type=int, default=1, help="prompt sweep: repeats of each prompt")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -120,64 +121,42 @@ def blas_threads():
 
 # ---------------------------------------------------------------------------------------------
 class OracleSample:
-    """Bounded sample of the oracle on the SAME shape: one decoder layer (target + 4-bit substitute)
-    plus the head, `nodes` draft and `nodes` target node-forwards, extrapolated to one full step of
-    (1 + k(D-1)) draft + (1 + kD) target node-forwards through all layers.  The seeded weights are
-    generated once (setup); every call of step_seconds() re-times the sample."""
+    """Bounded sample of the oracle (oracle/, fp32-BLAS mode) on the SAME workload: real SubSpec steps
+    (D draft passes of the frontier, sharpened top-k, one verify of all 1 + kD nodes, greedy accept,
+    KV commit) on a 1/L slice of the full-size model — ONE of its L decoder layers (full width) and the
+    first V/L rows of its head (so the head GEMMs and the top-k over the vocabulary are 1/L of a step's
+    too).  Every per-layer and per-vocabulary cost of a step is L x the slice's, so the step time is
+    L x the measured sample step; tau is the slice model's own acceptance (measured, not borrowed)."""
 
-    def __init__(self, cfg, depth, topk, nodes=6, bits=4):
-        from oracle.model import TargetWeights, draft_layers
-        self.cfg, self.depth, self.topk, self.nodes = cfg, depth, topk, nodes
-        self.cfg1 = cfg.with_(n_layers=1)
+    def __init__(self, cfg, depth, topk, temp, bits=4):
+        from oracle.decode import Session
+        self.L = cfg.n_layers
+        self.vs = max(128, (cfg.vocab // self.L) // 128 * 128)
+        self.cfg1 = cfg.with_(name=cfg.name + "-slice", n_layers=1, vocab=self.vs)
+        self.depth, self.topk, self.temp, self.bits = depth, topk, temp, bits
         t0 = time.time()
-        self.tw = TargetWeights(self.cfg1, SEED)
-        self.dl = draft_layers(self.tw, 0, bits)
+        self.sess = Session(self.cfg1, SEED, n_resident=0, bits=bits, mode="bf16-fp32", max_nodes=max(1 + topk * depth, 256))
+        self.prompt = [int(t) % self.vs for t in mtbench_prompt(SEED, 0, cfg.vocab)]
+        self.root = self.sess.prefill(self.prompt)
         self.setup = time.time() - t0
 
     def step_seconds(self):
-        from oracle.model import KVCache, forward_nodes
-        from oracle.tree import tempered_log_softmax, select_topk
-        cfg, cfg1, tw, nodes, topk, depth = self.cfg, self.cfg1, self.tw, self.nodes, self.topk, self.depth
-        kv = KVCache(cfg1, nodes + 1)
-        toks = list(range(1, nodes + 1))
-        slots = list(range(nodes))
-        anc = [[s] for s in slots]
-        pos = [0] * nodes
+        """One real SubSpec step of the slice model -> (seconds for the full-size step, emitted tokens)."""
+        if self.sess.kv.P + 1 + self.topk * self.depth >= self.cfg1.max_context:   # start over when full
+            self.sess.kv.P = 0
+            self.root = self.sess.prefill(self.prompt)
         t0 = time.perf_counter()
-        forward_nodes(cfg1, self.dl, tw, kv, toks, slots, pos, anc)
-        t_draft_node = (time.perf_counter() - t0) / nodes
-        t0 = time.perf_counter()
-        logits = forward_nodes(cfg1, tw.layers, tw, kv, toks, slots, pos, anc)
-        t_target_node = (time.perf_counter() - t0) / nodes
-        h = np.ones(cfg.hidden)
-        t0 = time.perf_counter()
-        for _ in range(nodes):
-            tw.head @ h
-        t_head = (time.perf_counter() - t0) / nodes
-        t0 = time.perf_counter()
-        lp = np.stack([tempered_log_softmax(logits[i], 0.2) for i in range(min(topk, nodes))])
-        select_topk(list(range(len(lp))), [0.0] * len(lp), lp, topk)
-        t_select = time.perf_counter() - t0
-        L = cfg.n_layers
-        n_draft = 1 + topk * (depth - 1)
-        n_verify = 1 + topk * depth
-        step = (n_draft * ((t_draft_node - t_head) * L + t_head) + n_verify * ((t_target_node - t_head) * L + t_head)
-                + depth * t_select)
-        info = {"t_draft_node_1layer_s": t_draft_node, "t_target_node_1layer_s": t_target_node, "t_head_s": t_head,
-                "t_select_s": t_select, "setup_s": self.setup, "node_forwards": n_draft + n_verify}
-        return step, info
+        tree, path, emitted = self.sess.step(self.root, self.depth, self.topk, self.temp)
+        dt = time.perf_counter() - t0
+        self.root = emitted[-1]
+        return dt * self.L, len(emitted)
 
-
-def oracle_step_seconds(cfg, depth, topk, nodes=6, bits=4):
-    """One-shot OracleSample (setup + one timed sample) -> (seconds/step, info)."""
-    return OracleSample(cfg, depth, topk, nodes, bits).step_seconds()
-
-
-def load_tau():
-    try:
-        return json.load(open(TAU_FILE))
-    except Exception:
-        return None
+    def describe(self):
+        return (f"real SubSpec steps (D={self.depth}, k={self.topk}, T={self.temp}) of a 1/{self.L} slice of the "
+                f"{self.cfg1.name[:-6]} model: 1 of {self.L} decoder layers at full width ({self.bits}-bit substitute) "
+                f"+ the first {self.vs} head rows, fp32-BLAS NumPy oracle; step time = {self.L} x the slice's step "
+                f"time; tau = the slice model's own acceptance (a 1-layer draft agrees with its target more often "
+                f"than the {self.L}-layer one: compare steps_per_s)")
 
 
 def run_reference(a):
@@ -185,30 +164,38 @@ def run_reference(a):
     if rank != 0:
         return
     cfg = PRESETS[a.config]
-    tau_rec = load_tau()
-    tau = tau_rec["tau"] if tau_rec and tau_rec.get("config") == a.config else 1.0
-    times = []
-    info = None
-    sample = OracleSample(cfg, a.depth, a.topk, bits=a.sub_bits)   # weights generated once, each step re-timed
+    sample = OracleSample(cfg, a.depth, a.topk, a.temp, bits=a.sub_bits)
+    times, toks = [], []
     for i in range(a.warmup + a.steps):
-        s, info = sample.step_seconds()
+        s, n = sample.step_seconds()
         if i >= a.warmup:
             times.append(s)
+            toks.append(n)
     step_s = statistics.mean(times)
-    value = tau / step_s
+    tau = float(np.mean(toks))
+    value = sum(toks) / sum(times)
     cores = blas_threads()
-    sample = (f"1 {cfg.name}-shape decoder layer (bf16 target + {a.sub_bits}-bit substitute, fp64 NumPy oracle) + head, 6 draft "
-              f"and 6 target node-forwards per step, extrapolated to a D={a.depth},k={a.topk} step "
-              f"({info['node_forwards']} node-forwards x {cfg.n_layers} layers); tau={tau:.3f} "
-              f"({'from the deterministic GPU run, ' + TAU_FILE if tau_rec else 'assumed 1'})")
     line = {"metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init weights, MT-Bench-shaped prompt)",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded random-init weights, MT-Bench-shaped prompt)",
             "config": workload_config(a, cfg), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": sample.describe()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "oracle_timing": info}
+            "tau_mean": tau, "steps_per_s": 1.0 / step_s,
+            "oracle_timing": {"setup_s": sample.setup, "sample_seconds_per_step": step_s / sample.L,
+                              "scale": sample.L, "wall_seconds_in_run": sum(times) / sample.L}}
     print(json.dumps(line), flush=True)
+
+
+def ngram_repetition(tokens, n=4):
+    """Fraction of the sequence's n-grams that occurred earlier in it (a greedy-loop detector)."""
+    seen, rep = set(), 0
+    grams = [tuple(tokens[i:i + n]) for i in range(len(tokens) - n + 1)]
+    for g in grams:
+        rep += g in seen
+        seen.add(g)
+    return rep / max(1, len(grams))
 
 
 def workload_config(a, cfg):
@@ -326,35 +313,38 @@ def run_ours(a):
             ss.prefill_slot(b, request_for_rank(rank * Bq + b, cfg.vocab))
         step = lambda: ss.step_batch(Bq, D, k, T)            # noqa: E731
     t_setup = time.time() - t_setup
+    prompt0 = request_for_rank(rank, cfg.vocab)
+
+    def timed_window(step_fn, n_steps):
+        """Device time of n_steps steps (CUDA events on the compute stream, barrier + sync on both sides;
+        the region ends when the copy stream has prefetched the ring again: steady state)."""
+        cs = ss.compute_stream
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(cs)
+        out = [step_fn() for _ in range(n_steps)]
+        ring_full = torch.cuda.Event()
+        ring_full.record(ss.copy_stream)
+        cs.wait_event(ring_full)
+        e1.record(cs)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        return e0.elapsed_time(e1), out
+
     for _ in range(a.warmup):
         step()
     ss.reset_stats()
-    cs = ss.compute_stream
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(dev)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
-    e0.record(cs)
-    emitted, taus = 0, []
-    for _ in range(a.steps):
-        for t in step():
-            emitted += len(t)
-            taus.append(len(t))
-    # steady state: the region starts with the streaming ring already prefetched for the next verify
-    # (by the warm-up steps), so it also ends only when the ring is prefetched again — the copy
-    # stream's outstanding prefetch is inside the timed region
-    ring_full = torch.cuda.Event()
-    ring_full.record(ss.copy_stream)
-    cs.wait_event(ring_full)
-    e1.record(cs)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    ms, outs = timed_window(step, a.steps)
     ck = clocks.stop()
-    ms = e0.elapsed_time(e1)
     st = ss.stats()
+    emitted_seq = [t for o in outs for r in o for t in r]
+    taus = [len(r) for o in outs for r in o]
+    emitted = sum(taus)
     # ---- dominant kernel: K2 dequant-GEMV, live sweep over every layer (weights from HBM) ----
     M = k * Bq   # frontier rows of a draft pass (all requests)
     groups = [ss.group_shape(g) for g in range(4)]
@@ -368,64 +358,101 @@ def run_ours(a):
     k2_gbs = bytes_layer / (4 * t_sweep * 1e-3) / 1e9
     t_head = ss.debug_time_matmul(0, -1, M, iters=5)
     head_gbs = (cfg.vocab * cfg.hidden * 2 + M * cfg.hidden * 2 + M * cfg.vocab * 4) / (t_head * 1e-3) / 1e9
-    # ---- e2e through the C-ABI with host buffers: root token H2D, emitted tokens D2H ----
+    # K2 inside a real draft pass: per-launch (first CTA entry .. last CTA end) from %globaltimer traces
+    k2_in_pass = None
+    if Bq == 1 and st["n_offloaded"] == cfg.n_layers:
+        tr = ss.debug_trace_pass(M, cap=512)
+        gemv = [r for r in tr if r[6] > r[0] > 0]
+        if len(gemv) >= 4 * cfg.n_layers:
+            dur = [(int(r[6]) - int(r[0])) * 1e-9 for r in gemv[:4 * cfg.n_layers]]
+            k2_in_pass = {"gbs": cfg.n_layers * bytes_layer / sum(dur) / 1e9,
+                          "us_per_layer": sum(dur) / cfg.n_layers * 1e6,
+                          "note": "per-launch first-CTA-entry .. last-CTA-end of the 4 K2 launches per layer "
+                                  "inside one draft pass (PDL overlap of neighbours is counted in both)"}
+    # ---- e2e through the C-ABI with host buffers, replaying the SAME steps: re-prefill the same prompt,
+    # the same warm-up, then the same K steps (deterministic: identical tokens); each step copies the root
+    # token H2D and reads the emitted tokens D2H; the 13 GB of streamed layer weights per step are
+    # host->device copies inside the region too ----
     e2e = None
-    if not a.no_e2e and Bq > 1:
-        # batched: ss_step_batch's host outputs are the step's D2H; roots stay on the device
+    if not a.no_e2e and Bq == 1:
+        root = ss.prefill(prompt0)
+        for _ in range(a.warmup):
+            ss.draft_tree(D, k, T, root_token=root, want_tree=False)
+            ss.verify_tree(want=False)
+            root = ss.accept_and_commit(D + 1)[0][-1]
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         st0 = ss.stats()
         t0 = time.perf_counter()
-        e2e_tok = 0
-        n_e2e = max(2, a.steps)   # as many steps as the device-timed region (tau varies per step)
-        for _ in range(n_e2e):
-            e2e_tok += sum(len(t) for t in step())
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        st1 = ss.stats()
-        wall, e2e_tok = aggregate_ranks(dist, wall, e2e_tok, dist_device(local))
-        streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / n_e2e
-        e2e = {"value": e2e_tok / wall, "unit": "tokens/s", "h2d_bytes_per_step": int(streamed),
-               "d2h_bytes_per_step": int(4 * Bq * (D + 2)),
-               "h2d_breakdown": {"streamed_layer_weights": int(streamed)}, "steps": n_e2e,
-               "ms_per_step": wall / n_e2e * 1e3}
-    elif not a.no_e2e:
-        root = int(ss.step(D, k, T)[-1])
-        # one untimed step through the same calls (the host-root draft path has its own graph instance)
-        ss.draft_tree(D, k, T, root_token=root, want_tree=False)
-        ss.verify_tree(want=False)
-        root = ss.accept_and_commit(D + 1)[0][-1]
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        st0 = ss.stats()
-        t0 = time.perf_counter()
-        e2e_tok = 0
-        n_e2e = max(2, a.steps)   # as many steps as the device-timed region (tau varies per step)
-        for _ in range(n_e2e):
+        e2e_seq = []
+        for _ in range(a.steps):
             ss.draft_tree(D, k, T, root_token=root, want_tree=False)
             ss.verify_tree(want=False)
             toks, _ = ss.accept_and_commit(D + 1)
             root = toks[-1]
-            e2e_tok += len(toks)
+            e2e_seq.extend(toks)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         st1 = ss.stats()
-        wall, e2e_tok = aggregate_ranks(dist, wall, e2e_tok, dist_device(local))
-        streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / n_e2e
-        e2e = {"value": e2e_tok / wall, "unit": "tokens/s", "h2d_bytes_per_step": int(4 + streamed),
-               "d2h_bytes_per_step": int(4 * (e2e_tok / max(1, n_e2e)) + 4),
-               "h2d_breakdown": {"root_token": 4, "streamed_layer_weights": int(streamed)}, "steps": n_e2e,
-               "ms_per_step": wall / n_e2e * 1e3}
+        wall_max, e2e_tok = aggregate_ranks(dist, wall, len(e2e_seq), dist_device(local))
+        streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / a.steps
+        e2e = {"value": e2e_tok / wall_max, "unit": "tokens/s", "h2d_bytes_per_step": int(4 + streamed),
+               "d2h_bytes_per_step": int(4 * (len(e2e_seq) / a.steps) + 4),
+               "h2d_breakdown": {"root_token": 4, "streamed_layer_weights": int(streamed)}, "steps": a.steps,
+               "ms_per_step": wall / a.steps * 1e3, "same_steps_as_device_window": e2e_seq == emitted_seq}
+    elif not a.no_e2e:
+        # batched: re-prefill every slot and replay; ss_step_batch's host outputs are the step's D2H
+        for b in range(Bq):
+            ss.prefill_slot(b, request_for_rank(rank * Bq + b, cfg.vocab))
+        for _ in range(a.warmup):
+            step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st0 = ss.stats()
+        t0 = time.perf_counter()
+        e2e_seq = [t for _ in range(a.steps) for r in step() for t in r]
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        st1 = ss.stats()
+        wall_max, e2e_tok = aggregate_ranks(dist, wall, len(e2e_seq), dist_device(local))
+        streamed = (st1["stream_bytes"] - st0["stream_bytes"]) / a.steps
+        e2e = {"value": e2e_tok / wall_max, "unit": "tokens/s", "h2d_bytes_per_step": int(streamed),
+               "d2h_bytes_per_step": int(4 * Bq * (D + 2)), "h2d_breakdown": {"streamed_layer_weights": int(streamed)},
+               "steps": a.steps, "ms_per_step": wall / a.steps * 1e3,
+               "same_steps_as_device_window": e2e_seq == emitted_seq}
+    # ---- prompt sweep: P MT-Bench-shaped prompts x R repeats (P:275 uses 20 samples; P:293 reports a std) ----
+    sweep = None
+    if a.prompts > 0 and Bq == 1:
+        runs = []
+        for rep in range(a.repeats):
+            for p in range(a.prompts):
+                pr = mtbench_prompt(SEED, 1000 + world * p + rank, cfg.vocab)
+                ss.prefill(pr)
+                for _ in range(a.warmup):
+                    step()
+                pms, pouts = timed_window(step, a.steps)
+                ptaus = [len(r) for o in pouts for r in o]
+                seq = [t for o in pouts for r in o for t in r]
+                runs.append({"prompt": p, "repeat": rep, "len": len(pr), "ms_per_step": pms / a.steps,
+                             "tokens_per_s": sum(ptaus) / (pms / 1e3), "steps_per_s": a.steps / (pms / 1e3),
+                             "tau": float(np.mean(ptaus)), "full_accept_frac": float(np.mean([t == D + 1 for t in ptaus])),
+                             "ngram4_repetition": ngram_repetition(seq)})
+        tps = [r["tokens_per_s"] for r in runs]
+        sps = [r["steps_per_s"] for r in runs]
+        sweep = {"prompts": a.prompts, "repeats": a.repeats, "steps_each": a.steps,
+                 "tokens_per_s_mean": statistics.mean(tps), "tokens_per_s_std": statistics.pstdev(tps),
+                 "steps_per_s_mean": statistics.mean(sps), "steps_per_s_std": statistics.pstdev(sps),
+                 "tau_mean": statistics.mean(r["tau"] for r in runs), "runs": runs}
     # context: one whole draft pass (all layers + head + attention/norm/top-k kernels), bytes of the
     # weights it must read (substitutes of offloaded layers, bf16 of resident ones, the bf16 head)
     draft_pass = None
+    n_off = st["n_offloaded"]
+    n_res = cfg.n_layers - n_off
+    pass_bytes = n_off * sum(k2_bytes(N, K, M, a.sub_bits) for N, K in groups) + \
+        n_res * sum(2 * N * K for N, K in groups) + cfg.vocab * cfg.hidden * 2
     if Bq == 1:
-        n_off = st["n_offloaded"]
-        n_res = cfg.n_layers - n_off
-        pass_bytes = n_off * sum(k2_bytes(N, K, M, a.sub_bits) for N, K in groups) + \
-            n_res * sum(2 * N * K for N, K in groups) + cfg.vocab * cfg.hidden * 2
         t_pass = ss.debug_time_pass(M, 5, 0)
         draft_pass = {"us": t_pass * 1e3, "weight_bytes": pass_bytes, "gbs": pass_bytes / (t_pass * 1e-3) / 1e9}
     # host link measured in the same run: pinned H2D 1 GiB on the copy stream, best of 5
@@ -455,6 +482,10 @@ def run_ours(a):
     except Exception:
         pass
     stream_gbs = st["stream_bytes"] / (st["stream_busy_ms"] * 1e-3) / 1e9 if st["stream_busy_ms"] else None
+    # step roofline: streamed bytes over the host link, plus the draft's HBM time not
+    # covered by the ring's prefetch of the next verify's layers
+    s_host = st["stream_bytes"] / a.steps
+    t_roof = s_host / (link_gbs * 1e9) + max(0.0, D * pass_bytes / (hbm_peak * 1e9) - st["ring_bytes"] / (link_gbs * 1e9))
     line = {
         "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
@@ -462,40 +493,41 @@ def run_ours(a):
         "data": "synthetic (seeded random-init bf16 weights of the named shape; MT-Bench-shaped prompts)",
         "config": workload_config(a, cfg),
         "tau_mean": tau, "tau_hist": np.bincount(taus, minlength=D + 2).tolist(), "steps_per_s": steps_per_s,
+        "full_accept_frac": float(np.mean([t == D + 1 for t in taus])),
+        "ngram4_repetition": ngram_repetition(emitted_seq),
         "tokens_per_s_at_paper_tau_27.08": 27.08 * steps_per_s * Bq,
         "requests_per_gpu": Bq,
         "step_breakdown_ms": {"draft": st["draft_ms"] / a.steps, "verify": st["verify_ms"] / a.steps,
                               "accept": st["accept_ms"] / a.steps},
+        "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / (ms / a.steps),
+                          "formula": "streamed bytes / host link + max(0, D x draft-pass bytes / HBM peak - ring / host link)"},
         "roofline": {"kernel": f"K2 dequant-GEMV ({a.sub_bits}-bit g64 substitutes, M={M} tokens), all layers x 4 groups",
                      "bound": "hbm", "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
-                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                     "per_group": per_group, "head_bf16_gemv_gbs": head_gbs, "draft_pass": draft_pass},
-        "streaming": {"bytes_per_step": st["stream_bytes"] / a.steps, "busy_gbs": stream_gbs,
+                     "traffic": traffic, "traffic_launch": "gate_up (ncu --set full, profiles/k2_traffic.json)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                     "per_group": per_group, "in_pass": k2_in_pass, "head_bf16_gemv_gbs": head_gbs,
+                     "draft_pass": draft_pass},
+        "streaming": {"bytes_per_step": s_host, "busy_gbs": stream_gbs,
                       "host_link_gbs_measured": link_gbs, "frac": (stream_gbs / link_gbs) if stream_gbs else None,
                       "duty_cycle": (st["stream_busy_ms"] / ms) if ms else None},
-        "memory": {"shared_host_store": shm is not None,
+        "memory": {"shared_host_store": shm is not None, "embedding": "GPU (P:534)" if a.embed_gpu else "mapped host (R24)",
                    "arena_used": st["arena_used"], "arena_cap": st["arena_cap"], "ring_bytes": st["ring_bytes"],
                    "substitute_bytes": st["substitute_bytes"], "host_pinned_bytes": st["host_pinned_bytes"],
                    "n_resident": st["n_resident"]},
         "gpu_launches": int(st["gpu_launches"]),
-        "clocks": ck, "e2e": e2e, "setup_s": t_setup,
+        "clocks": ck, "e2e": e2e, "prompt_sweep": sweep, "setup_s": t_setup,
     }
     if rank == 0:
-        os.makedirs(os.path.dirname(TAU_FILE), exist_ok=True)
-        if world == 1 and Bq == 1:
-            try:
-                json.dump({"config": a.config, "tau": tau, "steps": a.steps, "note": "deterministic seeded workload"},
-                          open(TAU_FILE, "w"))
-            except Exception:
-                pass
         if world == 1 and not a.no_cpu_baseline:
-            s, info = oracle_step_seconds(cfg, D, k, bits=a.sub_bits)
-            line["cpu_baseline"] = {
-                "value": tau / s, "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
-                "sample": (f"1 {cfg.name}-shape decoder layer + head, 6 draft + 6 target node-forwards (fp64 NumPy "
-                           f"oracle), extrapolated to one D={D},k={k} step ({info['node_forwards']} node-forwards x "
-                           f"{cfg.n_layers} layers) at this run's tau={tau:.3f}"),
-                "seconds_per_step": s}
+            sample = OracleSample(cfg, D, k, T, bits=a.sub_bits)
+            ts, ns = [], []
+            for _ in range(2):
+                s_, n_ = sample.step_seconds()
+                ts.append(s_)
+                ns.append(n_)
+            line["cpu_baseline"] = {"value": sum(ns) / sum(ts), "unit": "tokens/s", "cores": blas_threads(),
+                                    "kind": "oracle", "sample": sample.describe() + " (2 steps)",
+                                    "seconds_per_step": statistics.mean(ts), "tau": float(np.mean(ns))}
         print(json.dumps(line), flush=True)
     ss.close()
     if dist:

@@ -406,8 +406,9 @@ class SubSpec:
         self._check(self.lib.ss_debug_set_tree(self.ctx, _ptr(t), _ptr(p), len(t), top_k))
 
     def debug_read_kv(self, layer, pos0, n):
+        """Committed K/V rows: bf16 bit patterns (uint16), or float32 values in SS_FP32 mode."""
         c = self.cfg
-        k = np.zeros(c.n_kv_heads * n * c.head_dim, np.uint16)
+        k = np.zeros(c.n_kv_heads * n * c.head_dim, np.float32 if self.precision == SS_FP32 else np.uint16)
         v = np.zeros_like(k)
         self._check(self.lib.ss_debug_read_kv(self.ctx, layer, pos0, n, _ptr(k), _ptr(v)))
         return k.reshape(c.n_kv_heads, n, c.head_dim), v.reshape(c.n_kv_heads, n, c.head_dim)

@@ -151,9 +151,18 @@ struct ss_ctx {
   std::map<std::tuple<int, int, uint32_t>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, uint32_t>, int64_t> graph_launches;
   bool use_graphs = true, use_pdl = true;
+  // SS_FP32 precision mode (f32.cu): fp32 activations, q, attention output, KV cache, logits
+  bool f32 = false;
+  int kv_es = 2;                         // bytes per K/V element (2 bf16, 4 fp32)
+  float *h32 = nullptr, *q32 = nullptr, *o32 = nullptr, *y32 = nullptr, *a32 = nullptr, *logits32 = nullptr;
+  uint8_t* host_dev = nullptr;           // fp32 mode: device-mapped view of the pinned host store
   // stats
   ss_stats st{};
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  // copy-busy accounting: every copy interval is clipped to start no earlier than the last
+  // ss_reset_stats (ev_region), all times measured from ev_ref (recorded once at creation)
+  cudaEvent_t ev_ref = nullptr, ev_region = nullptr;
+  bool region_set = false;
   int64_t launches = 0;
   bool capturing = false;
 };
@@ -188,6 +197,19 @@ size_t bf16_bytes(int N, int K) { return size_t(N) * K * 2; }
 // token groups of 8 for a draft GEMV over M <= 32 rows: the tcgen05 MMA's N is 16 or 32 (M = 128)
 int gemv_nt(int M) { return M <= 16 ? 2 : 4; }
 int gemm_nt(int M) { return ((M + 127) / 128) * 16; }
+
+// busy ms of copy slot ev, clipped to the current stats region
+static float copy_busy_ms(ss_ctx* c, int ev) {
+  float a = 0.f, b = 0.f, r = 0.f;
+  if (cudaEventElapsedTime(&a, c->ev_ref, c->ev_t0[ev]) != cudaSuccess ||
+      cudaEventElapsedTime(&b, c->ev_ref, c->ev_t1[ev]) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  if (c->region_set && cudaEventElapsedTime(&r, c->ev_ref, c->ev_region) == cudaSuccess) a = std::max(a, r);
+  cudaGetLastError();
+  return std::max(0.f, b - a);
+}
 
 // ---------------------------------- K7 streaming ------------------------------------------
 ss_status pump(ss_ctx* c) {
@@ -225,9 +247,7 @@ ss_status pump(ss_ctx* c) {
     }
     if (c->ev_pending[ev]) {   // timing of a previous copy with this slot not yet harvested
       CK(cudaEventSynchronize(c->ev_t1[ev]));
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, c->ev_t0[ev], c->ev_t1[ev]));
-      c->st.stream_busy_ms += ms;
+      c->st.stream_busy_ms += copy_busy_ms(c, ev);
       c->ev_pending[ev] = false;
     }
     for (size_t i : dead) CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[c->inflight[i].ev], 0));
@@ -254,8 +274,7 @@ void harvest_timing(ss_ctx* c) {
       continue;
     }
     if (cudaEventQuery(c->ev_t1[ev]) != cudaSuccess) break;
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, c->ev_t0[ev], c->ev_t1[ev]) == cudaSuccess) c->st.stream_busy_ms += ms;
+    c->st.stream_busy_ms += copy_busy_ms(c, ev);
     c->ev_pending[ev] = false;
     c->timing_queue.pop_front();
   }
@@ -393,9 +412,69 @@ EpiParams base_epi(ss_ctx* c, int M) {
   return e;
 }
 
+// SS_FP32: the forward of M nodes in fp32 on the f32.cu kernels.  Weights: resident bf16; offloaded
+// layers: the draft's substitutes (4/2-bit tiles) and the target's bf16 tiles read in place from the
+// device-mapped pinned host store (parity mode: no staging ring).  Output: draft logits -> c->logits,
+// target logits -> c->logits32 (+ argmax/gap when out.argmax).
+static const uint8_t* weights_f32(ss_ctx* c, bool target, int l, int g, int* fmt) {
+  const LayerW& w = c->lw[l];
+  if (w.resident) {
+    *fmt = 0;
+    return w.bf16[g];
+  }
+  if (!target) {
+    *fmt = c->sub_bits;
+    return w.q4[g];
+  }
+  *fmt = 0;
+  return c->host_dev + w.host_off[g];
+}
+
+ss_status forward_pass_f32(ss_ctx* c, bool target, int M, int node_base, const PassOut& out) {
+  const float eps = c->cfg.rms_eps;
+  const int H = c->H, F = c->F;
+  launch_rmsnorm_f32(c->tok, node_base, c->embed, c->x, M, H, c->lw[0].attn_norm, eps, c->h32, c->cs);
+  float* kc = reinterpret_cast<float*>(c->kc);
+  float* vc = reinterpret_cast<float*>(c->vc);
+  float* kt = reinterpret_cast<float*>(c->kt);
+  float* vt = reinterpret_cast<float*>(c->vt);
+  for (int l = 0; l < c->L; ++l) {
+    const LayerW& w = c->lw[l];
+    int fmt = 0;
+    const uint8_t* W = weights_f32(c, target, l, 0, &fmt);
+    launch_linear_f32(c->h32, M, H, W, fmt, c->qkv_rows, c->y32, c->cs);
+    launch_qkv_post_f32(c->y32, M, w.bias, c->qd, c->kvd, c->d, c->rope, c->committed_len, c->depth, node_base, c->q32,
+                        kt + l * c->kt_layer, vt + l * c->kt_layer, c->kv_nodes, c->cs);
+    launch_attention_f32(c->q32, kc + l * c->kc_layer, vc + l * c->kc_layer, kt + l * c->kt_layer, vt + l * c->kt_layer,
+                         c->committed_len, c->anc, c->depth, c->anc_stride, c->kv_ctx, c->kv_nodes, node_base, M, c->nh,
+                         c->nkv, c->d, c->o32, c->cs);
+    W = weights_f32(c, target, l, 1, &fmt);
+    launch_linear_f32(c->o32, M, c->qd, W, fmt, H, c->y32, c->cs);
+    launch_add_f32(c->x, c->y32, int64_t(M) * H, c->cs);
+    launch_rmsnorm_f32(nullptr, 0, nullptr, c->x, M, H, w.mlp_norm, eps, c->h32, c->cs);
+    W = weights_f32(c, target, l, 2, &fmt);
+    launch_linear_f32(c->h32, M, H, W, fmt, 2 * F, c->y32, c->cs);
+    launch_silu_mul_f32(c->y32, M, F, c->a32, c->cs);
+    W = weights_f32(c, target, l, 3, &fmt);
+    launch_linear_f32(c->a32, M, F, W, fmt, H, c->y32, c->cs);
+    launch_add_f32(c->x, c->y32, int64_t(M) * H, c->cs);
+    c->launches += 10;
+  }
+  launch_rmsnorm_f32(nullptr, 0, nullptr, c->x, M, H, c->final_norm, eps, c->h32, c->cs);
+  float* lg = target ? c->logits32 : c->logits;
+  launch_linear_f32(c->h32, M, H, c->head, 0, c->V, lg, c->cs);
+  c->launches += 3;
+  if (out.argmax) {
+    launch_argmax_f32(c->logits32, M, c->V, c->argmax, c->gap, c->cs);
+    c->launches++;
+  }
+  return check_launch(c, "forward_f32");
+}
+
 // Forward M nodes [node_base, node_base + M) through the draft (GEMV path) or the target (GEMM
 // path, streamed).  Tree slots of these nodes receive their K/V.
 ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassOut& out) {
+  if (c->f32) return forward_pass_f32(c, target, M, node_base, out);
   const int NT = target ? gemm_nt(M) : gemv_nt(M);
   const float eps = c->cfg.rms_eps;
   ss_status s;
@@ -667,11 +746,13 @@ ss_status do_accept(ss_ctx* c, bool chain, int slot = 0) {
   a.v_cache = c->vc;
   a.k_tree = c->kt;
   a.v_tree = c->vt;
-  a.cache_layer_stride = c->kc_layer;
-  a.tree_layer_stride = c->kt_layer;
+  // the commit copies 16-bit units: fp32 K/V rows are 2 head_dim units (strides in units too)
+  const int u = c->kv_es / 2;
+  a.cache_layer_stride = c->kc_layer * u;
+  a.tree_layer_stride = c->kt_layer * u;
   a.n_layers = c->L;
   a.n_kv = c->nkv;
-  a.head_dim = c->d;
+  a.head_dim = c->d * u;
   a.max_ctx = c->kv_ctx;
   a.max_nodes = c->kv_nodes;
   a.chain = chain ? 1 : 0;
@@ -741,6 +822,15 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   if (opt) c->opt = *opt;
   c->serial_stream = !c->opt.async_stream;
   c->use_graphs = c->opt.cuda_graphs != 0;
+  c->f32 = cfg->precision == SS_FP32;
+  if (c->f32) {
+    if (lim->max_batch > 1) {   // the fp32 parity mode serves one request
+      delete c;
+      return SS_ERR_INVALID;
+    }
+    c->kv_es = 4;
+    c->use_graphs = false;
+  }
   c->fuse_norm = c->opt.fuse_norm != 0;
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -810,10 +900,19 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   }
   c->kc_layer = int64_t(c->nkv) * c->kv_ctx * c->d;
   c->kt_layer = int64_t(c->nkv) * c->kv_nodes * c->d;
-  c->kc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
-  c->vc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
-  c->kt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
-  c->vt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
+  c->kc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * c->kv_es));
+  c->vc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * c->kv_es));
+  c->kt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * c->kv_es));
+  c->vt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * c->kv_es));
+  if (c->f32) {
+    const size_t rows = size_t(c->mpad_max);
+    c->h32 = (float*)chk(A(rows * std::max(c->H, c->qd) * 4));
+    c->q32 = (float*)chk(A(rows * c->qd * 4));
+    c->o32 = (float*)chk(A(rows * c->qd * 4));
+    c->y32 = (float*)chk(A(rows * std::max({c->qkv_rows, 2 * c->F, c->H}) * 4));
+    c->a32 = (float*)chk(A(rows * c->F * 4));
+    c->logits32 = (float*)chk(A(rows * c->V * 4));
+  }
   c->tok = (int*)chk(A(size_t(c->kv_nodes) * 4));
   c->parent = (int*)chk(A(size_t(c->kv_nodes) * 4));
   c->depth = (int*)chk(A(size_t(c->kv_nodes) * 4));
@@ -893,6 +992,9 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   cudaEventCreate(&c->e2);
   cudaEventCreate(&c->e3);
   cudaEventCreateWithFlags(&c->ev_root, cudaEventDisableTiming);
+  cudaEventCreate(&c->ev_ref);
+  cudaEventCreate(&c->ev_region);
+  cudaEventRecord(c->ev_ref, c->cs);
   cudaHostAlloc(&c->h_root, 64, cudaHostAllocPortable);
   if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess || !c->h_out || !c->h_root) {
     delete c;
@@ -1058,6 +1160,7 @@ static ss_status fill_group_from_host(ss_ctx* c, const ss_host_layer& h, int g, 
 static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, int32_t n_resident, void* ext_host,
                            size_t ext_bytes, bool fill) {
   if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "load_weights: already loaded");
+  if (c->f32 && ext_host) return fail(c, SS_ERR_INVALID, "the fp32 parity mode keeps its own host store");
   c->seed = seed;
   const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
   const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += sub_bytes(c->gN[g], c->gK[g], c->sub_bits); return s; }();
@@ -1100,8 +1203,15 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
     c->host_external = true;
   }
   if (c->host_bytes) {
-    if (!c->host_external && cudaHostAlloc(&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess)
+    // fp32 parity mode: the target reads offloaded layers in place through a device-mapped view
+    const unsigned flags = cudaHostAllocPortable | (c->f32 ? cudaHostAllocMapped : 0u);
+    if (!c->host_external && cudaHostAlloc(&c->host, c->host_bytes, flags) != cudaSuccess)
       return fail(c, SS_ERR_CUDA, "cudaHostAlloc of the pinned host store failed");
+    if (c->f32) {
+      void* dp = nullptr;
+      CK(cudaHostGetDevicePointer(&dp, c->host, 0));
+      c->host_dev = reinterpret_cast<uint8_t*>(dp);
+    }
     size_t off = 0;
     for (int l = nr; l < c->L; ++l)
       for (int g = 0; g < 4; ++g) {
@@ -1156,9 +1266,9 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
   CK(cudaStreamSynchronize(c->cs));
   ss_status s = check_launch(c, "load_weights");
   if (s != SS_OK) return s;
-  // streaming cycle: offloaded layers in order, groups qkv, o, gate_up, down
+  // streaming cycle: offloaded layers in order, groups qkv, o, gate_up, down (none in fp32 mode)
   c->cycle.clear();
-  for (int l = nr; l < c->L; ++l)
+  for (int l = nr; l < c->L && !c->f32; ++l)
     for (int g = 0; g < 4; ++g) c->cycle.emplace_back(l, g);
   c->ev_pool = 4 * int(c->cycle.size()) + 64;
   for (int i = 0; i < c->ev_pool; ++i) {
@@ -1499,6 +1609,9 @@ ss_status ss_get_stats(ss_ctx* c, ss_stats* out) {
 ss_status ss_reset_stats(ss_ctx* c) {
   if (!c) return SS_ERR_INVALID;
   harvest_timing(c);
+  // copies still in flight count only from here on (the stats region starts on the compute stream now)
+  cudaEventRecord(c->ev_region, c->cs);
+  c->region_set = true;
   const ss_stats keep = c->st;
   c->st = ss_stats{};
   c->st.arena_used = keep.arena_used;
@@ -1524,7 +1637,7 @@ void ss_destroy(ss_ctx* c) {
   for (auto e : c->ev_consumed) cudaEventDestroy(e);
   for (auto e : c->ev_t0) cudaEventDestroy(e);
   for (auto e : c->ev_t1) cudaEventDestroy(e);
-  for (auto e : {c->e0, c->e1, c->e2, c->e3, c->ev_root})
+  for (auto e : {c->e0, c->e1, c->e2, c->e3, c->ev_root, c->ev_ref, c->ev_region})
     if (e) cudaEventDestroy(e);
   if (c->h_root) cudaFreeHost(c->h_root);
   if (c->host && c->host_external) host_unregister(c->host);
@@ -1918,9 +2031,11 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
       for (int b = 0; b < B; ++b)
         CK(cudaMemcpyAsync(out_logits + (int64_t(b) * n + i0) * c->V, c->logits + int64_t(b) * rows * c->V,
                            size_t(rows) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
-      if (opt_hidden) {   // the final normed rows the head just read (FragX, NT of the pass)
+      if (opt_hidden) {   // the final normed rows the head just read (FragX, NT of the pass; fp32: h32)
         hid.resize(size_t(M) * c->H);
-        if ((s = read_fragx(c, c->hfrag, M, c->H, gemv_nt(M), hid.data())) != SS_OK) return s;
+        if (c->f32) CK(cudaMemcpyAsync(hid.data(), c->h32, hid.size() * 4, cudaMemcpyDeviceToHost, c->cs));
+        else if ((s = read_fragx(c, c->hfrag, M, c->H, gemv_nt(M), hid.data())) != SS_OK) return s;
+        CK(cudaStreamSynchronize(c->cs));
         for (int b = 0; b < B; ++b)
           std::memcpy(opt_hidden + (int64_t(b) * n + i0) * c->H, hid.data() + size_t(b) * rows * c->H,
                       size_t(rows) * c->H * 4);
@@ -1935,6 +2050,12 @@ ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, cons
     s = forward_pass(c, true, B * n, 0, o);
     c->cur_rq = ReqMap{0, 0, 0, 0};
     if (s != SS_OK) return s;
+    if (c->f32) {   // logits and the final normed rows of the fp32 pass
+      CK(cudaMemcpyAsync(out_logits, c->logits32, size_t(n) * c->V * 4, cudaMemcpyDeviceToHost, c->cs));
+      if (opt_hidden) CK(cudaMemcpyAsync(opt_hidden, c->h32, size_t(n) * c->H * 4, cudaMemcpyDeviceToHost, c->cs));
+      CK(cudaStreamSynchronize(c->cs));
+      return check_launch(c, "debug_forward");
+    }
     for (int r0 = 0; r0 < B * n; r0 += 32) {
       const int m = std::min(32, B * n - r0);
       launch_rmsnorm(c->x + int64_t(r0) * c->H, m, c->H, c->final_norm, c->cfg.rms_eps, c->hfrag, c->hxs, gemv_nt(m), false, c->cs);
@@ -2003,10 +2124,13 @@ ss_status ss_debug_read_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, ui
   if (layer < 0 || layer >= c->L || pos0 < 0 || n < 1 || pos0 + n > c->kv_ctx || !k || !v)
     return fail(c, SS_ERR_INVALID, "read_kv args");
   CK(cudaStreamSynchronize(c->cs));
+  const int es = c->kv_es;   // SS_FP32: 4-byte elements (k, v hold fp32 values)
   for (int h = 0; h < c->nkv; ++h) {
-    const int64_t src = layer * c->kc_layer + (int64_t(h) * c->kv_ctx + pos0) * c->d;
-    CK(cudaMemcpyAsync(k + int64_t(h) * n * c->d, c->kc + src, size_t(n) * c->d * 2, cudaMemcpyDeviceToHost, c->cs));
-    CK(cudaMemcpyAsync(v + int64_t(h) * n * c->d, c->vc + src, size_t(n) * c->d * 2, cudaMemcpyDeviceToHost, c->cs));
+    const int64_t src = (layer * c->kc_layer + (int64_t(h) * c->kv_ctx + pos0) * c->d) * es;
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(k) + int64_t(h) * n * c->d * es, reinterpret_cast<uint8_t*>(c->kc) + src,
+                       size_t(n) * c->d * es, cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(v) + int64_t(h) * n * c->d * es, reinterpret_cast<uint8_t*>(c->vc) + src,
+                       size_t(n) * c->d * es, cudaMemcpyDeviceToHost, c->cs));
   }
   CK(cudaStreamSynchronize(c->cs));
   return SS_OK;

@@ -192,6 +192,21 @@ struct AcceptParams {
 };
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st);
 
+// SS_FP32 precision mode (f32.cu)
+void launch_rmsnorm_f32(const int* tokens, int tok_offset, const uint16_t* embed, float* x, int M, int H,
+                        const uint16_t* gain, float eps, float* h, cudaStream_t st);
+void launch_linear_f32(const float* X, int M, int K, const uint8_t* W, int fmt, int N, float* Y, cudaStream_t st);
+void launch_qkv_post_f32(const float* Y, int M, const uint16_t* bias, int qd, int kvd, int d, const float2* rope,
+                         const int* committed_len, const int* depth, int node_base, float* q_out, float* k_tree,
+                         float* v_tree, int max_nodes, cudaStream_t st);
+void launch_attention_f32(const float* q, const float* k_cache, const float* v_cache, const float* k_tree,
+                          const float* v_tree, const int* committed_len, const int* anc, const int* depth, int anc_stride,
+                          int max_ctx, int max_nodes, int node_base, int M, int n_heads, int n_kv, int d, float* out,
+                          cudaStream_t st);
+void launch_add_f32(float* x, const float* y, int64_t n, cudaStream_t st);
+void launch_silu_mul_f32(const float* Y, int M, int F, float* act, cudaStream_t st);
+void launch_argmax_f32(const float* logits, int M, int V, int* argmax, float* gap, cudaStream_t st);
+
 // tree init for a new step: root node (slot 0) with token *root_tok, depth 0
 void launch_tree_init(const int* root_tok, int* tok, int* parent, int* depth, float* score, int* anc, bool pdl,
                       cudaStream_t st, int n_req = 1, int node_stride = 0, int anc_stride = 0);
