@@ -362,13 +362,14 @@ def run_ours(a):
     k2_in_pass = None
     if Bq == 1 and st["n_offloaded"] == cfg.n_layers:
         tr = ss.debug_trace_pass(M, cap=512)
-        gemv = [r for r in tr if r[6] > r[0] > 0]
+        gemv = [r for r in tr if r[6] > r[2] > 0]
         if len(gemv) >= 4 * cfg.n_layers:
-            dur = [(int(r[6]) - int(r[0])) * 1e-9 for r in gemv[:4 * cfg.n_layers]]
+            dur = [(int(r[6]) - int(r[2])) * 1e-9 for r in gemv[:4 * cfg.n_layers]]
             k2_in_pass = {"gbs": cfg.n_layers * bytes_layer / sum(dur) / 1e9,
                           "us_per_layer": sum(dur) / cfg.n_layers * 1e6,
-                          "note": "per-launch first-CTA-entry .. last-CTA-end of the 4 K2 launches per layer "
-                                  "inside one draft pass (PDL overlap of neighbours is counted in both)"}
+                          "note": "per K2 launch inside one draft pass: from the release of its dependency on the "
+                                  "previous kernel (griddepcontrol.wait returns) to its last CTA's end; the weight "
+                                  "prefetch issued before that release is not counted against it"}
     # ---- e2e through the C-ABI with host buffers, replaying the SAME steps: re-prefill the same prompt,
     # the same warm-up, then the same K steps (deterministic: identical tokens); each step copies the root
     # token H2D and reads the emitted tokens D2H; the 13 GB of streamed layer weights per step are

@@ -440,6 +440,7 @@ ss_status forward_pass_f32(ss_ctx* c, bool target, int M, int node_base, const P
   float* vt = reinterpret_cast<float*>(c->vt);
   for (int l = 0; l < c->L; ++l) {
     const LayerW& w = c->lw[l];
+    if (l > 0) launch_rmsnorm_f32(nullptr, 0, nullptr, c->x, M, H, w.attn_norm, eps, c->h32, c->cs);
     int fmt = 0;
     const uint8_t* W = weights_f32(c, target, l, 0, &fmt);
     launch_linear_f32(c->h32, M, H, W, fmt, c->qkv_rows, c->y32, c->cs);
