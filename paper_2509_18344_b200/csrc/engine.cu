@@ -310,6 +310,9 @@ ss_status consume_end(ss_ctx* c, int ev) {
 struct PassOut {
   bool logits = false;        // draft: logits to c->logits [M x V]
   bool argmax = false;        // target: per-node argmax + gap
+  bool topk = false;          // draft: per vocab-tile top-k statistics (EPI_TOPK), no logits in HBM
+  int tk_k = 0;
+  float tk_inv_t = 1.f;
 };
 // debug timing only (ss_debug_time_pass): skip kernel classes to attribute pass time
 int g_skip = 0;
@@ -586,8 +589,9 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     c->launches += 2;
     return check_launch(c, "verify head");
   }
-  if (out.logits) {
-    // head over the final normed rows (GEMV, <= 32 rows at a time)
+  if (out.logits || out.topk) {
+    // head over the final normed rows (GEMV, <= 32 rows at a time); topk: the K5 statistics are
+    // produced in the GEMV's epilogue and the logits never leave the SMs
     for (int r0 = 0; r0 < M && !target && !(g_skip & SKIP_HEAD); r0 += 32) {
       const int m = std::min(32, M - r0);
       GemvParams p{};
@@ -603,6 +607,16 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
       p.epi.kind = EPI_LOGITS;
       p.epi.out = c->logits;
       p.epi.ldo = c->V;
+      if (out.topk) {
+        p.epi.kind = EPI_TOPK;
+        p.epi.tk_max = c->tk_max;
+        p.epi.tk_sum = c->tk_sum;
+        p.epi.tk_val = c->tk_val;
+        p.epi.tk_idx = c->tk_idx;
+        p.epi.tk_k = out.tk_k;
+        p.epi.tk_tiles = c->V / 128;
+        p.epi.tk_inv_t = out.tk_inv_t;
+      }
       launch_gemv(false, p, c->gv_grid, c->use_pdl, c->cs);
       c->launches++;
       if ((s = check_launch(c, "head gemv")) != SS_OK) return s;
@@ -627,7 +641,12 @@ ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
     const int M = c->B * Mr;
     const int base = dd == 0 ? 0 : 1 + (dd - 1) * k;
     PassOut o;
-    o.logits = true;
+    // bf16: the head GEMV's epilogue produces the per-tile top-k statistics (K5 folded);
+    // fp32 parity mode: logits, then the two-stage top-k kernels
+    o.topk = !c->f32;
+    o.logits = c->f32;
+    o.tk_k = k;
+    o.tk_inv_t = float(1.0 / double(T));
     c->cur_rq = batch_map(c, Mr);
     s = forward_pass(c, false, M, base, o);
     c->cur_rq = ReqMap{0, 0, 0, 0};
@@ -654,8 +673,14 @@ ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
     t.node_base = base;
     t.child_base = 1 + dd * k;
     t.child_depth = dd + 1;
-    launch_topk(t, c->use_pdl, c->cs);
-    c->launches += 2;
+    if (o.topk) {
+      t.blocks_per_row = c->V / 128;
+      launch_topk_select(t, c->use_pdl, c->cs);
+      c->launches += 1;
+    } else {
+      launch_topk(t, c->use_pdl, c->cs);
+      c->launches += 2;
+    }
     if ((s = check_launch(c, "topk")) != SS_OK) return s;
   }
   return SS_OK;
@@ -955,10 +980,13 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
     c->at_o_floats = std::max(mpad_one * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
     c->at_o = (float*)chk(A(c->at_o_floats * 4));
   }
-  c->tk_max = (float*)chk(A(size_t(32) * 296 * 4));
-  c->tk_sum = (float*)chk(A(size_t(32) * 296 * 4));
-  c->tk_val = (float*)chk(A(size_t(32) * 296 * 32 * 4));
-  c->tk_idx = (int*)chk(A(size_t(32) * 296 * 32 * 4));
+  {   // top-k statistics: [32 rows][blocks] of the two-stage kernels (296) or of the head's vocab tiles
+    const size_t nb = std::max<size_t>(296, size_t(c->V / 128));
+    c->tk_max = (float*)chk(A(size_t(32) * nb * 4));
+    c->tk_sum = (float*)chk(A(size_t(32) * nb * 4));
+    c->tk_val = (float*)chk(A(size_t(32) * nb * lim->max_top_k * 4));
+    c->tk_idx = (int*)chk(A(size_t(32) * nb * lim->max_top_k * 4));
+  }
   c->vtiles = c->V / 128;
   c->am_val = (float*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));
   c->am_sec = (float*)chk(A(size_t(c->mpad_max) * c->vtiles * 4));

@@ -266,6 +266,55 @@ SS_DEV void apply_epilogue(const EpiParams& e, const float* tile, int ld, int r,
       }
       break;
     }
+    case EPI_TOPK: {
+      // sharpened top-k statistics of one 128-logit vocab tile per token (reading R13:
+      // fp32 logits from the accumulator): warp w takes tokens w, w + nwarps, ...; lane holds rows
+      // lane + 32 i; max, sum exp((l - max) / T) in a fixed shuffle order, then tk_k rounds of warp argmax
+      // (value desc, index asc) with the picked row excluded
+      const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
+      for (int m = warp; m < ncols; m += nwarps) {
+        const int mg = m0 + m;
+        if (mg >= e.M) continue;
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = tile[(lane + 32 * i) * ld + m];
+        float mx = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+        mx = warp_max(mx);
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s += expf((v[i] - mx) * e.tk_inv_t);
+        s = warp_sum(s);
+        const int64_t base = int64_t(mg) * e.tk_tiles + r;
+        if (lane == 0) {
+          e.tk_max[base] = mx;
+          e.tk_sum[base] = s;
+        }
+        for (int q = 0; q < e.tk_k; ++q) {
+          float bv = -INFINITY;
+          int bi = 0x7fffffff;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (v[i] > bv) {   // i ascending: the first of equal values has the smaller row
+              bv = v[i];
+              bi = lane + 32 * i;
+            }
+          for (int o = 16; o; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          if (lane == 0) {
+            e.tk_val[base * e.tk_k + q] = bv;
+            e.tk_idx[base * e.tk_k + q] = row0 + bi;
+          }
+          if ((bi & 31) == lane) v[bi >> 5] = -INFINITY;   // excluded from the next rounds
+        }
+      }
+      break;
+    }
     case EPI_ARGMAX: {   // one thread per token column: max, first argmax, second max over the 128 rows
       for (int m = tid; m < ncols; m += nthreads) {
         const int mg = m0 + m;

@@ -18,7 +18,8 @@ struct ReqMap {
 __host__ __device__ inline int rq_req(const ReqMap& r, int m) { return r.rows > 0 ? r.req0 + m / r.rows : r.req0; }
 __host__ __device__ inline int rq_loc(const ReqMap& r, int m) { return r.rows > 0 ? m % r.rows : m; }
 
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5, EPI_RESID_NORM = 7 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_LOGITS = 3, EPI_ARGMAX = 4, EPI_STORE = 5, EPI_RESID_NORM = 7,
+               EPI_TOPK = 8 };
 
 // Epilogue parameters shared by the GEMV (draft, M <= 32) and GEMM (verify) kernels.
 struct EpiParams {
@@ -56,6 +57,14 @@ struct EpiParams {
   unsigned long long* norm_ctr;  // monotonic arrival counter of the norm barrier (zero at creation)
   int n_tiles;
   float eps;
+  // EPI_TOPK (draft head, K5 folded into the GEMV): per (token, 128-row vocab tile) the tile's max logit,
+  // sum exp((l - max) / T) and its top tk_k logits (value desc, index asc) -> [token][tile] arrays
+  float* tk_max;                 // [M][tk_tiles]
+  float* tk_sum;
+  float* tk_val;                 // [M][tk_tiles][tk_k]
+  int* tk_idx;
+  int tk_k, tk_tiles;
+  float tk_inv_t;
   // EPI_ARGMAX: per (token, row tile) partial (max, idx, second max)
   float* am_val;                 // [M x n_tiles]
   int* am_idx;
@@ -163,6 +172,9 @@ struct TopkParams {
   int node_stride;               // one select CTA per request, tree arrays strided by node_stride
 };
 void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st);
+// the global selection only, over per-tile statistics the head GEMV's EPI_TOPK epilogue wrote
+// (blocks_per_row = vocab tiles)
+void launch_topk_select(const TopkParams& p, bool pdl, cudaStream_t st);
 
 void launch_argmax_merge(const float* am_val, const int* am_idx, const float* am_second, int M, int tiles,
                          int* argmax, float* gap, bool pdl, cudaStream_t st);

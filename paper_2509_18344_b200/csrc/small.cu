@@ -344,6 +344,12 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
   }
 }
 
+void launch_topk_select(const TopkParams& p, bool pdl, cudaStream_t st) {
+  void* args[] = {const_cast<TopkParams*>(&p)};
+  const int nreq = p.req_rows > 0 ? p.M / p.req_rows : 1;
+  launch_pdl((const void*)topk_select_kernel, dim3(nreq), dim3(1024), 64 * 4 + 4 * 32 * 4, pdl, st, args);
+}
+
 void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
   TopkParams pp = p;
   void* args[] = {&pp};
