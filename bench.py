@@ -54,6 +54,9 @@ def args_():
                     help="Table-2 ablation: no copy/compute overlap in the verify streaming (PAPER.md:305-308)")
     ap.add_argument("--prompts", type=int, default=4, help="prompt sweep: MT-Bench-shaped prompts (0 = skip)")
     ap.add_argument("--repeats", type=int, default=1, help="prompt sweep: repeats of each prompt")
+    ap.add_argument("--coop", action="store_true",
+                    help="NEXT-1 cooperative weight streaming under torchrun: rank r pulls 1/N of every streamed "
+                         "group over its host link and pushes it to the peers over NVLink (ss_coop_*)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -205,7 +208,9 @@ def workload_config(a, cfg):
             "model_shape": cfg.name, "vram_cap_gib": a.cap_gib, "n_resident": a.n_resident, "depth": a.depth,
             "top_k": a.topk, "sharpen_t": a.temp, "batch": a.batch, "max_context": cfg.max_context,
             "l2": "inputs larger than L2 (>= 4.76 GB of draft weights per draft pass; 13 GB streamed per verify)",
-            "parallelism": f"requests partitioned, {a.gpus} GPU(s), no collective"}
+            "parallelism": (f"requests partitioned, {a.gpus} GPU(s); layer stream shared (NEXT-1: 1/{a.gpus} per host "
+                            f"link + NVLink peer copies)" if a.coop and a.gpus > 1 else
+                            f"requests partitioned, {a.gpus} GPU(s), no collective")}
 
 
 def aggregate_ranks(dist, ms, tokens, device="cpu"):
@@ -277,6 +282,17 @@ def load_weights_for_job(ss, dist, local, n_resident):
     return shm
 
 
+def coop_handshake(ss, dist, rank, world):
+    """NEXT-1 (include/subspec.h ss_coop_*): every rank exports its 256-byte handle, the handles are
+    all-gathered in rank order, every rank enables cooperative streaming with them, then a barrier (no
+    rank may stream into a peer's ring before that peer has drained and reset its own)."""
+    handles = [None] * world
+    dist.all_gather_object(handles, ss.coop_export())
+    ss.coop_enable(rank, handles)
+    dist.barrier()
+    return handles
+
+
 def dist_device(local):
     return "cpu" if os.environ.get("SS_DIST_BACKEND", "nccl") == "gloo" else f"cuda:{local}"
 
@@ -312,6 +328,9 @@ def run_ours(a):
         for b in range(Bq):
             ss.prefill_slot(b, request_for_rank(rank * Bq + b, cfg.vocab))
         step = lambda: ss.step_batch(Bq, D, k, T)            # noqa: E731
+    coop = bool(a.coop and dist is not None)
+    if coop:   # every rank has prefilled (one target pass each); from here on the ranks verify in lockstep
+        coop_handshake(ss, dist, rank, world)
     t_setup = time.time() - t_setup
     prompt0 = request_for_rank(rank, cfg.vocab)
 
@@ -339,7 +358,12 @@ def run_ours(a):
     ss.reset_stats()
     clocks = ClockSampler(dev)
     clocks.start()
+    prof = os.environ.get("SS_PROFILE_TIMED") == "1"   # ncu --profile-from-start off: the timed steps only
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     ms, outs = timed_window(step, a.steps)
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     ck = clocks.stop()
     st = ss.stats()
     emitted_seq = [t for o in outs for r in o for t in r]
@@ -508,7 +532,9 @@ def run_ours(a):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      "per_group": per_group, "in_pass": k2_in_pass, "head_bf16_gemv_gbs": head_gbs,
                      "draft_pass": draft_pass},
-        "streaming": {"bytes_per_step": s_host, "busy_gbs": stream_gbs,
+        "streaming": {"mode": f"cooperative over {world} ranks (NEXT-1)" if coop else "per rank",
+                      "peer_bytes_per_step": st["peer_bytes"] / a.steps,
+                      "bytes_per_step": s_host, "busy_gbs": stream_gbs,
                       "host_link_gbs_measured": link_gbs, "frac": (stream_gbs / link_gbs) if stream_gbs else None,
                       "duty_cycle": (st["stream_busy_ms"] / ms) if ms else None},
         "memory": {"shared_host_store": shm is not None, "embedding": "GPU (P:534)" if a.embed_gpu else "mapped host (R24)",
@@ -530,6 +556,9 @@ def run_ours(a):
                                     "kind": "oracle", "sample": sample.describe() + " (2 steps)",
                                     "seconds_per_step": statistics.mean(ts), "tau": float(np.mean(ns))}
         print(json.dumps(line), flush=True)
+    if coop:
+        ss.coop_finish()
+        dist.barrier()   # no rank's ring is still written by a peer
     ss.close()
     if dist:
         dist.barrier()   # every rank has released the shared store before it is unlinked

@@ -106,6 +106,7 @@ typedef struct {
   double stream_bytes, stream_busy_ms;        /* host->device layer streaming (copy stream) */
   int64_t arena_used, arena_cap, ring_bytes, host_pinned_bytes, substitute_bytes;
   int32_t n_resident, n_offloaded, committed_len, last_d_eff;
+  double peer_bytes;                          /* NEXT-1: bytes this rank pushed to peers' rings */
 } ss_stats;
 
 typedef struct ss_ctx ss_ctx;
@@ -248,6 +249,31 @@ ss_status ss_generate_batch(ss_ctx* ctx, int32_t n_req, const int32_t* prompts, 
                             int32_t* out_n, int32_t* opt_tau_hist);
 
 ss_status ss_get_stats(ss_ctx* ctx, ss_stats* out);
+
+/* cooperative weight streaming across the G GPUs of a node (PAPER.md:172-176
+ * asynchronous transfer; P:382 faster interconnects).  Each rank's verify needs every offloaded layer;
+ * instead of every rank pulling all of them over its own host link, rank r copies only slice r (1/G of
+ * the bytes, 4 KiB aligned) of each streamed group from its host store into its ring and pushes that
+ * slice over NVLink (copy engine, CUDA IPC mapping of the peers' arenas) into every peer's ring at the
+ * same offset.  Completion and ring reuse are ordered by monotonic per-rank counters in device memory
+ * (stream memory operations): "rank h's slice of item s has landed here" and "rank h has consumed items
+ * < n".  Weights are bit-identical, so the output is unchanged.
+ * Protocol: every rank calls ss_coop_export (outside a step, after ss_build_substitutes and prefill);
+ * the caller exchanges the handles (e.g. all_gather); every rank calls ss_coop_enable(rank, world,
+ * handles[world]), which drains this rank's stream and restarts its ring at offset 0; then the caller
+ * BARRIERS before any rank continues.  From then on every rank must run the same sequence of target
+ * passes (the same number of steps / prefill chunks: the GPUs verify in lockstep), and
+ * no rank destroys its context before ss_coop_finish + a barrier.  export / enable / finish may be
+ * repeated (one cooperative epoch each).  Errors: INVALID (handles, ranks differ in model/placement/ring), STRUCTURE (order, inside
+ * a step, no streamed layers, fp32 mode, serial-stream ablation), CUDA (IPC or stream memory ops). */
+typedef struct { uint8_t bytes[256]; } ss_coop_handle;
+ss_status ss_coop_export(ss_ctx* ctx, ss_coop_handle* out);
+ss_status ss_coop_enable(ss_ctx* ctx, int32_t rank, int32_t world, const ss_coop_handle* all);
+/* End cooperative streaming on every rank (a common point after the last lockstep pass): releases
+ * the peers' pending writes into this rank's ring, waits for this rank's pending pushes, and restarts
+ * the stream alone.  The caller BARRIERS afterwards, before any rank destroys its context or decodes
+ * alone.  Errors: STRUCTURE (not enabled, inside a step), CUDA. */
+ss_status ss_coop_finish(ss_ctx* ctx);
 ss_status ss_reset_stats(ss_ctx* ctx);
 const char* ss_last_error(ss_ctx* ctx);
 void ss_destroy(ss_ctx* ctx);
@@ -279,13 +305,18 @@ ss_status ss_debug_set_tree(ss_ctx* ctx, const int32_t* tokens, const int32_t* p
 /* Committed K/V rows [pos0, pos0+n) of a layer -> host [n_kv x n x head_dim] bf16 bits each (batched
  * slots: slot b's position p is row b * max_context + p). */
 ss_status ss_debug_read_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
-/* Time one launch of the draft dequant-GEMV of (layer, group) with M tokens: average device ms of
- * `iters` back-to-back launches (CUDA events on the compute stream). */
+/* Time launches of a matrix kernel with M tokens: average device ms per launch over `iters` rounds
+ * (CUDA events on the compute stream).  which 0: the draft GEMV (K2 on substitutes, bf16 GEMV on
+ * resident layers / the head), M <= 32; which 1: the target GEMM (K6) on resident layers or the head
+ * (group -1, with the verify's per-tile argmax epilogue), M <= the verify rows.  layer -1: every
+ * layer in turn; group -2: the four groups of each layer.  Errors: INVALID, STRUCTURE (which 1 on
+ * an offloaded layer). */
 ss_status ss_debug_time_matmul(ss_ctx* ctx, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
                                float* out_ms);
 
 /* Debug A/B switches of the kernels (tests and tools only): knob 0 = K2 L2 self-prefetch of each
- * CTA's weight range (1 default, 0 off).  Captured draft graphs are dropped. */
+ * CTA's weight range (0 default, 1 on); knob 1 = K2 debug bits; knob 2 = the K6 kernel variant
+ * (0 default: tcgen05 with whole-chunk stages; 1: legacy mma.sync; 2: tcgen05 with half-chunk stages).  Captured draft graphs are dropped.  Errors: INVALID (unknown knob). */
 ss_status ss_debug_set_knob(ss_ctx* ctx, int32_t knob, int32_t value);
 /* Time the draft forward of M frontier nodes (one draft pass incl. head, no top-k): average device ms
  * over `iters` eager launches.  skip: bit mask of kernel classes left out (1 attention, 2 RMSNorm,

@@ -62,7 +62,8 @@ class StatsC(ctypes.Structure):
                 ("accept_ms", c_double), ("stream_bytes", c_double), ("stream_busy_ms", c_double),
                 ("arena_used", c_int64), ("arena_cap", c_int64), ("ring_bytes", c_int64),
                 ("host_pinned_bytes", c_int64), ("substitute_bytes", c_int64), ("n_resident", c_int32),
-                ("n_offloaded", c_int32), ("committed_len", c_int32), ("last_d_eff", c_int32)]
+                ("n_offloaded", c_int32), ("committed_len", c_int32), ("last_d_eff", c_int32),
+                ("peer_bytes", c_double)]
 
 
 P = ctypes.POINTER
@@ -87,6 +88,9 @@ _FUNCS = {
     "ss_generate_batch": [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32, P(DraftParamsC), c_void_p, c_void_p,
                           c_void_p],
     "ss_get_stats": [c_void_p, P(StatsC)],
+    "ss_coop_export": [c_void_p, c_void_p],
+    "ss_coop_enable": [c_void_p, c_int32, c_int32, c_void_p],
+    "ss_coop_finish": [c_void_p],
     "ss_reset_stats": [c_void_p],
     "ss_debug_gen_tensor": [c_void_p, c_uint64, c_int32, c_int64, c_int64, c_int32, c_double, c_void_p],
     "ss_debug_read_group": [c_void_p, c_int32, c_int32, c_void_p],
@@ -352,6 +356,27 @@ class SubSpec:
     def reset_stats(self):
         self._check(self.lib.ss_reset_stats(self.ctx))
 
+    # ---- NEXT-1: cooperative weight streaming (see ss_coop_export / ss_coop_enable) ---------
+    def coop_export(self):
+        """This rank's 256-byte handle (bytes) for the other ranks."""
+        buf = (ctypes.c_uint8 * 256)()
+        self._check(self.lib.ss_coop_export(self.ctx, buf))
+        return bytes(buf)
+
+    def coop_enable(self, rank, handles):
+        """handles: every rank's coop_export() bytes, in rank order.  The caller barriers afterwards."""
+        world = len(handles)
+        arr = (ctypes.c_uint8 * (256 * world))()
+        for h, b in enumerate(handles):
+            if len(b) != 256:
+                raise ValueError("coop handle must be 256 bytes")
+            ctypes.memmove(ctypes.byref(arr, 256 * h), b, 256)
+        self._check(self.lib.ss_coop_enable(self.ctx, rank, world, arr))
+
+    def coop_finish(self):
+        """Every rank, at a common point; the caller barriers afterwards."""
+        self._check(self.lib.ss_coop_finish(self.ctx))
+
     # ---- debug / parity -----------------------------------------------------------------
     def debug_gen_tensor(self, seed, tid, shape, kind, sigma):
         rows, cols = (shape[0], shape[1]) if len(shape) == 2 else (1, shape[0])
@@ -433,7 +458,7 @@ class SubSpec:
     def debug_set_knob(self, knob, value):
         self._check(self.lib.ss_debug_set_knob(self.ctx, knob, value))
 
-    def debug_time_matmul(self, layer, group, M, iters=20):
+    def debug_time_matmul(self, layer, group, M, iters=20, which=0):
         ms = c_float()
-        self._check(self.lib.ss_debug_time_matmul(self.ctx, 0, layer, group, M, iters, ctypes.byref(ms)))
+        self._check(self.lib.ss_debug_time_matmul(self.ctx, which, layer, group, M, iters, ctypes.byref(ms)))
         return ms.value

@@ -10,6 +10,8 @@
 #include <string>
 #include <tuple>
 #include <vector>
+#include <unistd.h>
+#include <cuda.h>
 
 #include "subspec.h"
 #include "common.cuh"
@@ -147,6 +149,18 @@ struct ss_ctx {
   bool fuse_norm = true;
   int k2_dbg = 0;             // K2 debug A/B bits (ss_debug_set_knob 1)
   int k2_self_pf = 0;         // K2: L2-prefetch each CTA's own weight range (ss_debug_set_knob 0; measured slower)
+  int k6_variant = 0;         // K6 kernel variant (ss_debug_set_knob 2; launch_gemm; A/B only)
+  // NEXT-1 cooperative streaming (ss_coop_*): rank r of `coop_world` copies slice r of every streamed
+  // group from its host store and pushes it into every peer's ring at the same offset; flags[h] =
+  // "rank h's slice of item seq landed here" (= seq + 1), flags[kCoopMax + h] = "rank h consumed
+  // items < value" (both monotonic, written by the peers' streams)
+  int coop_world = 1, coop_rank = 0;
+  bool coop_exported = false;
+  uint32_t* flags = nullptr;
+  std::vector<uint8_t*> peer_ring;
+  std::vector<uint32_t*> peer_flags;
+  std::vector<void*> ipc_opened;
+  std::deque<std::tuple<size_t, size_t, int64_t>> placed;   // ring occupancy (off, bytes, seq)
   // graphs
   std::map<std::tuple<int, int, uint32_t>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, uint32_t>, int64_t> graph_launches;
@@ -212,6 +226,38 @@ static float copy_busy_ms(ss_ctx* c, int ev) {
 }
 
 // ---------------------------------- K7 streaming ------------------------------------------
+// Stream memory operations (driver API, fetched at run time: no libcuda link dependency)
+namespace {
+constexpr int kCoopMax = 64;
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_wait32 g_wait32 = nullptr;
+PFN_write32 g_write32 = nullptr;
+PFN_range g_range = nullptr;
+bool load_driver_fns() {
+  static std::once_flag once;
+  static bool ok = false;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    ok = cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", (void**)&g_wait32, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+         q == cudaDriverEntryPointSuccess &&
+         cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", (void**)&g_write32, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+         q == cudaDriverEntryPointSuccess &&
+         cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", (void**)&g_range, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+         q == cudaDriverEntryPointSuccess;
+    cudaGetLastError();
+  });
+  return ok;
+}
+}  // namespace
+#define CKD(x)                                                                         \
+  do {                                                                                 \
+    CUresult r_ = (x);                                                                 \
+    if (r_ != CUDA_SUCCESS) return fail(c, SS_ERR_CUDA, std::string("driver: ") + #x); \
+  } while (0)
+static size_t coop_slice_lo(size_t B, int h, int G) { return h >= G ? B : (B * size_t(h) / size_t(G)) & ~size_t(4095); }
+
 ss_status pump(ss_ctx* c) {
   if (c->cycle.empty()) return SS_OK;
   const int n_items = int(c->cycle.size());
@@ -219,7 +265,7 @@ ss_status pump(ss_ctx* c) {
     const int64_t seq = c->next_issue;
     // never run more than one cycle ahead of consumption
     if (seq >= c->next_consume + n_items) return SS_OK;
-    // ablation (SS_STREAM_SERIAL=1, the paper's "async transfer" off, P:172-176 / Table 2): copy a
+    // ablation (ss_options.async_stream = 0, the paper's "async transfer" off, P:172-176 / Table 2): copy a
     // group only when it is the next one consumed and after the previous group's compute
     if (c->serial_stream && seq > c->next_consume) return SS_OK;
     const auto [l, g] = c->cycle[seq % n_items];
@@ -254,12 +300,39 @@ ss_status pump(ss_ctx* c) {
     if (c->serial_stream && c->last_consumed_ev >= 0) CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[c->last_consumed_ev], 0));
     for (size_t k = dead.size(); k-- > 0;) c->inflight.erase(c->inflight.begin() + dead[k]);
     CK(cudaEventRecord(c->ev_t0[ev], c->xs));
-    CK(cudaMemcpyAsync(c->ring + off, c->host + c->lw[l].host_off[g], B, cudaMemcpyHostToDevice, c->xs));
+    if (c->coop_world > 1) {
+      // NEXT-1: the items that occupied [off, off + B) before must have been consumed by every peer
+      int64_t need = 0;
+      for (auto it = c->placed.begin(); it != c->placed.end();) {
+        if (std::get<0>(*it) < off + B && off < std::get<0>(*it) + std::get<1>(*it)) {
+          need = std::max(need, std::get<2>(*it) + 1);
+          it = c->placed.erase(it);
+        } else {
+          ++it;
+        }
+      }
+      c->placed.emplace_back(off, B, seq);
+      const int G = c->coop_world, me = c->coop_rank;
+      const size_t lo = coop_slice_lo(B, me, G), hi = coop_slice_lo(B, me + 1, G);
+      if (hi > lo)
+        CK(cudaMemcpyAsync(c->ring + off + lo, c->host + c->lw[l].host_off[g] + lo, hi - lo, cudaMemcpyHostToDevice, c->xs));
+      for (int h = 0; h < G; ++h) {
+        if (h == me) continue;
+        if (need > 0) CKD(g_wait32((CUstream)c->xs, (CUdeviceptr)(c->flags + kCoopMax + h), cuuint32_t(need), CU_STREAM_WAIT_VALUE_GEQ));
+        if (hi > lo) CK(cudaMemcpyAsync(c->peer_ring[h] + off + lo, c->ring + off + lo, hi - lo, cudaMemcpyDeviceToDevice, c->xs));
+      }
+      for (int h = 0; h < G; ++h)   // my slice of item seq is in every ring
+        CKD(g_write32((CUstream)c->xs, (CUdeviceptr)(c->peer_flags[h] + me), cuuint32_t(seq + 1), 0));
+      c->st.stream_bytes += double(hi - lo);
+      c->st.peer_bytes += double(hi - lo) * (G - 1);
+    } else {
+      CK(cudaMemcpyAsync(c->ring + off, c->host + c->lw[l].host_off[g], B, cudaMemcpyHostToDevice, c->xs));
+      c->st.stream_bytes += double(B);
+    }
     CK(cudaEventRecord(c->ev_t1[ev], c->xs));
     CK(cudaEventRecord(c->ev_copied[ev], c->xs));
     c->ev_pending[ev] = true;
     c->timing_queue.push_back(ev);
-    c->st.stream_bytes += double(B);
     c->inflight.push_back({seq, l, g, off, B, ev, false});
     c->ring_head = off + B;
     c->next_issue = seq + 1;
@@ -291,6 +364,9 @@ ss_status consume_begin(ss_ctx* c, int l, int g, const uint8_t** w, int* ev_out)
   for (auto& it : c->inflight)
     if (it.seq == seq) {
       CK(cudaStreamWaitEvent(c->cs, c->ev_copied[it.ev], 0));
+      for (int h = 0; h < c->coop_world && c->coop_world > 1; ++h)   // every rank's slice landed
+        if (h != c->coop_rank)
+          CKD(g_wait32((CUstream)c->cs, (CUdeviceptr)(c->flags + h), cuuint32_t(seq + 1), CU_STREAM_WAIT_VALUE_GEQ));
       *w = c->ring + it.off;
       *ev_out = it.ev;
       return SS_OK;
@@ -299,6 +375,10 @@ ss_status consume_begin(ss_ctx* c, int l, int g, const uint8_t** w, int* ev_out)
 }
 ss_status consume_end(ss_ctx* c, int ev) {
   CK(cudaEventRecord(c->ev_consumed[ev], c->cs));
+  for (int h = 0; h < c->coop_world && c->coop_world > 1; ++h)   // tell every peer: item consumed here
+    if (h != c->coop_rank)
+      CKD(g_write32((CUstream)c->cs, (CUdeviceptr)(c->peer_flags[h] + kCoopMax + c->coop_rank),
+                    cuuint32_t(c->next_consume + 1), 0));
   c->last_consumed_ev = ev;
   for (auto& it : c->inflight)
     if (it.ev == ev) it.consumed = true;
@@ -382,7 +462,7 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
   p.epi = epi;
   if (w.resident) {
     p.W = w.bf16[g];
-    launch_gemm(p, c->use_pdl, c->cs);
+    launch_gemm(p, c->use_pdl, c->cs, c->k6_variant);
     c->launches++;
     return check_launch(c, "gemm");
   }
@@ -391,7 +471,7 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
   ss_status s = consume_begin(c, l, g, &wp, &ev);
   if (s != SS_OK) return s;
   p.W = wp;
-  launch_gemm(p, false, c->cs);   // follows a cross-stream event wait: plain serialisation
+  launch_gemm(p, false, c->cs, c->k6_variant);   // follows a cross-stream event wait: plain serialisation
   c->launches++;
   s = check_launch(c, "gemm");
   if (s != SS_OK) return s;
@@ -584,7 +664,7 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     p.epi.am_idx = c->am_idx;
     p.epi.am_second = c->am_sec;
     p.epi.am_tiles = c->vtiles;
-    launch_gemm(p, c->use_pdl, c->cs);
+    launch_gemm(p, c->use_pdl, c->cs, c->k6_variant);
     launch_argmax_merge(c->am_val, c->am_idx, c->am_sec, M, c->vtiles, c->argmax, c->gap, c->use_pdl, c->cs);
     c->launches += 2;
     return check_launch(c, "verify head");
@@ -960,6 +1040,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   c->tracebuf = (unsigned long long*)chk(A(size_t(512) * kTraceEvents * 8));
   c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
   c->norm_ctr = (unsigned long long*)chk(A(256));   // 24 monotonic counters (3 x 2 formats x NT 1..4), zeroed below
+  c->flags = (uint32_t*)chk(A(2 * kCoopMax * 4));   // NEXT-1 stream flags, zeroed by ss_coop_export
   c->rope = (float2*)chk(A(size_t(c->C) * (c->d / 2) * 8));
   // gemv partials: worst case over groups and the head at Mpad = 32
   size_t gvf = 0;
@@ -1668,6 +1749,7 @@ void ss_destroy(ss_ctx* c) {
   for (auto e : c->ev_t1) cudaEventDestroy(e);
   for (auto e : {c->e0, c->e1, c->e2, c->e3, c->ev_root, c->ev_ref, c->ev_region})
     if (e) cudaEventDestroy(e);
+  for (void* b : c->ipc_opened) cudaIpcCloseMemHandle(b);
   if (c->h_root) cudaFreeHost(c->h_root);
   if (c->host && c->host_external) host_unregister(c->host);
   else if (c->host) cudaFreeHost(c->host);
@@ -1675,6 +1757,127 @@ void ss_destroy(ss_ctx* c) {
   if (c->h_out) cudaFreeHost(c->h_out);
   cudaGetLastError();
   delete c;
+}
+
+// ------------------------- NEXT-1: cooperative weight streaming -----------------------------
+namespace {
+struct CoopBlob {
+  uint32_t magic, version;
+  int32_t pid, device;
+  uint64_t ring_off, flags_off, ring_bytes, n_items, host_bytes;
+  uint64_t ring_ptr, flags_ptr;
+  cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kCoopMagic = 0x53534350u;   // "SSCP"
+static_assert(sizeof(CoopBlob) <= sizeof(ss_coop_handle), "coop handle size");
+}  // namespace
+
+ss_status ss_coop_export(ss_ctx* c, ss_coop_handle* out) {
+  GUARD(c);
+  if (!out) return fail(c, SS_ERR_INVALID, "coop_export: null handle");
+  if (c->state < ST_READY || c->state == ST_DRAFTED || c->state == ST_VERIFIED)
+    return fail(c, SS_ERR_STRUCTURE, "coop_export: after build_substitutes, outside a step");
+  if (c->cycle.empty() || c->f32 || c->serial_stream || c->coop_world > 1)
+    return fail(c, SS_ERR_STRUCTURE, "coop_export: needs streamed layers, bf16, async streaming, not yet enabled");
+  if (!load_driver_fns()) return fail(c, SS_ERR_CUDA, "coop_export: stream memory operations unavailable");
+  CK(cudaMemsetAsync(c->flags, 0, 2 * kCoopMax * 4, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CKD(g_range(&base, &size, (CUdeviceptr)c->ar.base));
+  CoopBlob b{};
+  b.magic = kCoopMagic;
+  b.version = 1;
+  b.pid = int32_t(getpid());
+  b.device = c->device;
+  b.ring_off = uint64_t(reinterpret_cast<uintptr_t>(c->ring) - base);
+  b.flags_off = uint64_t(reinterpret_cast<uintptr_t>(c->flags) - base);
+  b.ring_bytes = c->ring_bytes;
+  b.n_items = c->cycle.size();
+  b.host_bytes = c->host_bytes;
+  b.ring_ptr = uint64_t(reinterpret_cast<uintptr_t>(c->ring));
+  b.flags_ptr = uint64_t(reinterpret_cast<uintptr_t>(c->flags));
+  CK(cudaIpcGetMemHandle(&b.ipc, c->ar.base));
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out, &b, sizeof(b));
+  c->coop_exported = true;
+  return SS_OK;
+}
+
+ss_status ss_coop_enable(ss_ctx* c, int32_t rank, int32_t world, const ss_coop_handle* all) {
+  GUARD(c);
+  if (!all || world < 2 || world > kCoopMax || rank < 0 || rank >= world)
+    return fail(c, SS_ERR_INVALID, "coop_enable: rank/world/handles");
+  if (!c->coop_exported || c->coop_world > 1) return fail(c, SS_ERR_STRUCTURE, "coop_enable: export first, once");
+  if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "coop_enable inside a step");
+  if (c->next_consume % int64_t(c->cycle.size()) != 0) return fail(c, SS_ERR_STRUCTURE, "coop_enable: mid-pass");
+  std::vector<CoopBlob> bl(world);
+  for (int h = 0; h < world; ++h) {
+    std::memcpy(&bl[h], &all[h], sizeof(CoopBlob));
+    if (bl[h].magic != kCoopMagic || bl[h].version != 1) return fail(c, SS_ERR_INVALID, "coop_enable: bad handle");
+    if (bl[h].ring_bytes != c->ring_bytes || bl[h].n_items != c->cycle.size() || bl[h].host_bytes != c->host_bytes)
+      return fail(c, SS_ERR_INVALID, "coop_enable: ranks differ in model, placement or ring size");
+  }
+  if (bl[rank].ring_ptr != uint64_t(reinterpret_cast<uintptr_t>(c->ring)))
+    return fail(c, SS_ERR_INVALID, "coop_enable: handle `rank` is not this context's");
+  // drain the non-cooperative stream: every prefetched item is dropped, the ring restarts at 0
+  CK(cudaStreamSynchronize(c->cs));
+  CK(cudaStreamSynchronize(c->xs));
+  harvest_timing(c);
+  c->inflight.clear();
+  c->placed.clear();
+  c->ring_head = 0;
+  c->next_issue = c->next_consume = 0;
+  c->peer_ring.assign(world, nullptr);
+  c->peer_flags.assign(world, nullptr);
+  for (int h = 0; h < world; ++h) {
+    if (h == rank) {
+      c->peer_ring[h] = c->ring;
+      c->peer_flags[h] = c->flags;
+      continue;
+    }
+    uint8_t* base = nullptr;
+    if (bl[h].pid == int32_t(getpid())) {   // another context of this process: its pointers as they are
+      c->peer_ring[h] = reinterpret_cast<uint8_t*>(uintptr_t(bl[h].ring_ptr));
+      c->peer_flags[h] = reinterpret_cast<uint32_t*>(uintptr_t(bl[h].flags_ptr));
+      continue;
+    }
+    void* vb = nullptr;
+    CK(cudaIpcOpenMemHandle(&vb, bl[h].ipc, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(vb);
+    base = reinterpret_cast<uint8_t*>(vb);
+    c->peer_ring[h] = base + bl[h].ring_off;
+    c->peer_flags[h] = reinterpret_cast<uint32_t*>(base + bl[h].flags_off);
+  }
+  c->coop_world = world;
+  c->coop_rank = rank;
+  return SS_OK;   // streaming resumes at the next target pass (after the caller's barrier)
+}
+
+ss_status ss_coop_finish(ss_ctx* c) {
+  GUARD(c);
+  if (c->coop_world < 2) return fail(c, SS_ERR_STRUCTURE, "coop_finish: cooperative streaming not enabled");
+  if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "coop_finish inside a step");
+  // release every peer's pending ring writes into this rank (they wait for our consumption), then
+  // wait for our own pending pushes, which the peers release the same way
+  for (int h = 0; h < c->coop_world; ++h)
+    if (h != c->coop_rank)
+      CKD(g_write32((CUstream)c->cs, (CUdeviceptr)(c->peer_flags[h] + kCoopMax + c->coop_rank), 0x7fffffffu, 0));
+  CK(cudaStreamSynchronize(c->cs));
+  CK(cudaStreamSynchronize(c->xs));
+  harvest_timing(c);
+  c->inflight.clear();
+  c->placed.clear();
+  c->ring_head = 0;
+  c->next_issue = c->next_consume = 0;
+  for (void* b : c->ipc_opened) CK(cudaIpcCloseMemHandle(b));
+  c->ipc_opened.clear();
+  c->peer_ring.clear();
+  c->peer_flags.clear();
+  c->coop_world = 1;
+  c->coop_rank = 0;
+  c->coop_exported = false;   // a new cooperative epoch starts with ss_coop_export again
+  return SS_OK;   // streaming resumes alone at the next target pass (after the caller's barrier)
 }
 
 // ---------------------------------- debug ---------------------------------------------------
@@ -1815,7 +2018,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
     } else {
       return fail(c, SS_ERR_STRUCTURE, "debug target matmul on an offloaded layer: use a resident layer");
     }
-    launch_gemm(p, false, c->cs);
+    launch_gemm(p, false, c->cs, c->k6_variant);
   }
   CK(cudaMemcpyAsync(y, Y, size_t(M) * N * 4, cudaMemcpyDeviceToHost, c->cs));
   CK(cudaStreamSynchronize(c->cs));
@@ -1827,8 +2030,10 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
   GUARD(c);
   // layer >= 0: that layer only; layer == -1: every layer in turn (weights stream from HBM, not L2).
   // group 0..3: that matrix group; -1: the bf16 head; -2: the four groups of each layer in pass order.
-  if (c->state < ST_READY || which != 0 || layer < -1 || layer >= c->L || group < -2 || group > 3 || M < 1 || M > 32 ||
-      iters < 1 || !out_ms)
+  // which 0: the draft GEMV (K2 / bf16 head), M <= 32; which 1: the target GEMM (K6) on resident
+  // layers (EPI_STORE) or the head (group -1, EPI_ARGMAX as in the verify), M <= the verify rows
+  if (c->state < ST_READY || which < 0 || which > 1 || layer < -1 || layer >= c->L || group < -2 || group > 3 || M < 1 ||
+      M > (which == 0 ? 32 : c->mpad_max) || iters < 1 || !out_ms)
     return fail(c, SS_ERR_INVALID, "time_matmul args");
   std::vector<std::pair<int, int>> seq;
   for (int l = (layer < 0 ? 0 : layer); l < (layer < 0 ? c->L : layer + 1); ++l) {
@@ -1838,10 +2043,36 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
       seq.emplace_back(l, group);
   }
   if (group == -1) seq.assign(1, {0, -1});
+  if (which == 1)
+    for (auto& lg : seq)
+      if (lg.second >= 0 && (!c->lw[lg.first].resident || size_t(M) * c->gN[lg.second] > c->at_o_floats))
+        return fail(c, SS_ERR_STRUCTURE, "time_matmul: the target GEMM is timed on resident layers");
   auto launch = [&](int l, int g) {
     const bool head = g == -1;
     const int N = head ? c->V : c->gN[g], K = head ? c->H : c->gK[g];
     const LayerW& w = c->lw[l];
+    if (which == 1) {
+      GemmParams q{};
+      q.W = head ? c->head : w.bf16[g];
+      q.X = K == c->F ? c->actfrag : c->hfrag;
+      q.N = N;
+      q.K = K;
+      q.NT = gemm_nt(M);
+      q.epi = base_epi(c, M);
+      if (head) {
+        q.epi.kind = EPI_ARGMAX;
+        q.epi.am_val = c->am_val;
+        q.epi.am_idx = c->am_idx;
+        q.epi.am_second = c->am_sec;
+        q.epi.am_tiles = c->vtiles;
+      } else {
+        q.epi.kind = EPI_STORE;
+        q.epi.out = c->at_o;
+        q.epi.ldo = N;
+      }
+      launch_gemm(q, c->use_pdl, c->cs, c->k6_variant);
+      return;
+    }
     GemvParams p{};
     p.W = head ? c->head : (w.resident ? w.bf16[g] : w.q4[g]);
     p.X = K == c->F ? c->actfrag : c->hfrag;
@@ -1856,7 +2087,6 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.epi.kind = EPI_STORE;
     p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
     p.self_pf = c->k2_self_pf;
-    p.dbg = c->k2_dbg;
     p.dbg = c->k2_dbg;
     p.qbits = c->sub_bits;
     p.epi.out = c->at_o;
@@ -1882,6 +2112,7 @@ ss_status ss_debug_set_knob(ss_ctx* c, int32_t knob, int32_t value) {
   switch (knob) {
     case 0: c->k2_self_pf = value; break;
     case 1: c->k2_dbg = value; break;
+    case 2: c->k6_variant = value; break;
     default: return fail(c, SS_ERR_INVALID, "unknown knob");
   }
   CK(cudaStreamSynchronize(c->cs));

@@ -106,7 +106,9 @@ struct GemmParams {
   int N, K, NT;                  // NT = Mpad/8
   EpiParams epi;
 };
-void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st);
+// variant: 0 tcgen05 whole-chunk stages (default), 1 legacy mma.sync, 2 tcgen05 half-chunk stages
+void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st, int variant = 0);
+int gemm_tc_split(int N, int K, int sms);
 
 // generator / quantizer / readback
 void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st,

@@ -228,16 +228,19 @@ __global__ void __launch_bounds__(256) topk_block_kernel(const TopkParams p) {
   }
 }
 
+constexpr int kSelRegK = 8;   // topk_select: per-lane register top-k up to this k (the paper's k = 6)
+// the selection order of R12: score desc, then token asc, then parent (frontier row) asc
+SS_DEV bool sel_before(float s, int t, int m, float s2, int t2, int m2) {
+  return s > s2 || (s == s2 && (t < t2 || (t == t2 && m < m2)));
+}
 __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int B = p.blocks_per_row;
-  float* lse = reinterpret_cast<float*>(sm);        // [M]
-  float* rmax = lse + 32;                           // [M]
-  float* sel_s = rmax + 32;                         // [k]
+  float* sel_s = reinterpret_cast<float*>(sm);      // [k]
   int* sel_t = reinterpret_cast<int*>(sel_s + 32);  // [k] token
   int* sel_p = sel_t + 32;                          // [k] parent row m
-  __shared__ float wv[32];
-  __shared__ int wt[32], wp[32], wc[32];
+  __shared__ float cs[32][32];                      // per frontier row: its k best (score, token)
+  __shared__ int ct[32][32];
   griddep_launch();   // small grid: let the next kernel start its prologue (weight prefetch) now
   griddep_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -245,87 +248,209 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
   const int q = blockIdx.x;
   const int Mr = p.req_rows > 0 ? p.req_rows : p.M, r0 = q * Mr;
   const int64_t nofs = int64_t(q) * p.node_stride;
-  if (threadIdx.x < Mr) {
-    const int m = threadIdx.x, mg = r0 + m;
+  const float* score = p.score + nofs;
+  if (warp < Mr) {
+    // warp m: row m's max and sum exp((l - max) / T) merged over its B vocab tiles (fixed lane
+    // order + fixed shuffle tree: deterministic), then its k best children in selection order
+    const int m = warp, mg = r0 + m;
     float mx = -INFINITY;
-    for (int b = 0; b < B; ++b) mx = fmaxf(mx, p.blk_max[mg * B + b]);
-    float s = 0.f;
-    for (int b = 0; b < B; ++b) s += p.blk_sum[mg * B + b] * expf((p.blk_max[mg * B + b] - mx) * p.inv_t);
-    rmax[m] = mx;
-    lse[m] = logf(s);
+    for (int b = lane; b < B; b += 32) mx = fmaxf(mx, p.blk_max[int64_t(mg) * B + b]);
+    mx = warp_max(mx);
+    float sacc = 0.f;
+    for (int b = lane; b < B; b += 32)
+      sacc += p.blk_sum[int64_t(mg) * B + b] * expf((p.blk_max[int64_t(mg) * B + b] - mx) * p.inv_t);
+    const float lse = logf(warp_sum(sacc));
+    const int nc = B * p.k;
+    const int* bi = p.blk_idx + int64_t(mg) * nc;
+    const float* bv = p.blk_val + int64_t(mg) * nc;
+    const float base = score[p.node_base + m];
+    const bool fast = p.k <= kSelRegK && B >= p.k;
+    if (fast) {
+      // Every vocab tile's list is sorted in selection order (value desc, token asc; the candidate
+      // score is monotone in the value), so the row's k best lie in the k tiles with the best heads:
+      // (1) each lane keeps the k best tile heads it scans, in registers; (2) k rounds of a warp
+      // merge pick the k best heads; (3) the k x k candidates of those tiles -> the row's k best.
+      float ls[kSelRegK];
+      int lt[kSelRegK], lb[kSelRegK];
+#pragma unroll
+      for (int i = 0; i < kSelRegK; ++i) {
+        ls[i] = -INFINITY;
+        lt[i] = INT32_MAX;
+        lb[i] = 0;
+      }
+#pragma unroll 4
+      for (int t = lane; t < B; t += 32) {
+        const int tok = bi[int64_t(t) * p.k];
+        const float sc = base + ((bv[int64_t(t) * p.k] - mx) * p.inv_t - lse);
+        if (sel_before(sc, tok, 0, ls[kSelRegK - 1], lt[kSelRegK - 1], 0)) {
+          float cs_ = sc;
+          int ct_ = tok, cb_ = t;
+#pragma unroll
+          for (int i = 0; i < kSelRegK; ++i)
+            if (sel_before(cs_, ct_, 0, ls[i], lt[i], 0)) {
+              const float ts = ls[i];
+              const int tt = lt[i], tb = lb[i];
+              ls[i] = cs_;
+              lt[i] = ct_;
+              lb[i] = cb_;
+              cs_ = ts;
+              ct_ = tt;
+              cb_ = tb;
+            }
+        }
+      }
+      int mytile = -1;   // lane r < k: the r-th best tile
+      for (int r = 0; r < p.k; ++r) {
+        float bs = ls[0];
+        int bt = lt[0], bb = lb[0];
+        for (int o = 16; o; o >>= 1) {
+          const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+          const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+          const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+          if (sel_before(os, ot, 0, bs, bt, 0)) {
+            bs = os;
+            bt = ot;
+            bb = ob;
+          }
+        }
+        if (lane == r) mytile = bb;
+        if (lt[0] == bt && ls[0] == bs) {   // the winner's lane pops its head (tokens are distinct)
+#pragma unroll
+          for (int i = 0; i + 1 < kSelRegK; ++i) {
+            ls[i] = ls[i + 1];
+            lt[i] = lt[i + 1];
+            lb[i] = lb[i + 1];
+          }
+          ls[kSelRegK - 1] = -INFINITY;
+          lt[kSelRegK - 1] = INT32_MAX;
+        }
+      }
+      // candidates of the k chosen tiles: c = r * k + j -> tile of lane r, entry j (k * k <= 64)
+      const int ncand = p.k * p.k;
+      float c_s[2];
+      int c_t[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        const int tile = __shfl_sync(0xffffffffu, mytile, (c / p.k) & 31);
+        c_s[h] = -INFINITY;
+        c_t[h] = INT32_MAX;
+        if (c < ncand) {
+          const int64_t e = int64_t(tile) * p.k + c % p.k;
+          c_t[h] = bi[e];
+          c_s[h] = base + ((bv[e] - mx) * p.inv_t - lse);
+        }
+      }
+      float ps = INFINITY;
+      int pt = -1;
+      for (int r = 0; r < p.k; ++r) {
+        float bs = -INFINITY;
+        int bt = INT32_MAX;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (sel_before(ps, pt, 0, c_s[h], c_t[h], 0) && sel_before(c_s[h], c_t[h], 0, bs, bt, 0)) {
+            bs = c_s[h];
+            bt = c_t[h];
+          }
+        for (int o = 16; o; o >>= 1) {
+          const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+          const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+          if (sel_before(os, ot, 0, bs, bt, 0)) {
+            bs = os;
+            bt = ot;
+          }
+        }
+        if (lane == 0) {
+          cs[m][r] = bs;
+          ct[m][r] = bt;
+        }
+        ps = bs;
+        pt = bt;
+      }
+    }
+    float ps = INFINITY;   // the previous pick (candidates are distinct tokens within a row)
+    int pt = -1;
+    for (int r = 0; r < p.k && !fast; ++r) {   // otherwise: k scans of all the candidates
+      float bs = -INFINITY;
+      int bt = INT32_MAX;
+      for (int c = lane; c < nc; c += 32) {
+        const int tok = bi[c];
+        const float sc = base + ((bv[c] - mx) * p.inv_t - lse);
+        if (sel_before(ps, pt, 0, sc, tok, 0) && sel_before(sc, tok, 0, bs, bt, 0)) {
+          bs = sc;
+          bt = tok;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+        if (sel_before(os, ot, 0, bs, bt, 0)) {
+          bs = os;
+          bt = ot;
+        }
+      }
+      if (lane == 0) {
+        cs[m][r] = bs;
+        ct[m][r] = bt;
+      }
+      ps = bs;
+      pt = bt;
+    }
   }
   __syncthreads();
-  const int ncand = Mr * B * p.k;
-  const int* blk_idx = p.blk_idx + int64_t(r0) * B * p.k;
-  const float* blk_val = p.blk_val + int64_t(r0) * B * p.k;
-  const float* score = p.score + nofs;
-  for (int r = 0; r < p.k; ++r) {
-    float bs = -INFINITY;
-    int bt = INT32_MAX, bp = INT32_MAX, bc = -1;
-    for (int c = threadIdx.x; c < ncand; c += blockDim.x) {
-      const int m = c / (B * p.k);
-      const int tok = blk_idx[c];
-      bool tk = false;
-      for (int q = 0; q < r; ++q) tk |= (sel_t[q] == tok && sel_p[q] == m);
-      if (tk) continue;
-      const float lp = (blk_val[c] - rmax[m]) * p.inv_t - lse[m];
-      const float sc = score[p.node_base + m] + lp;
-      if (sc > bs || (sc == bs && (tok < bt || (tok == bt && m < bp)))) {
-        bs = sc;
-        bt = tok;
-        bp = m;
-        bc = c;
-      }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-      const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      if (os > bs || (os == bs && (ot < bt || (ot == bt && op < bp)))) {
-        bs = os;
-        bt = ot;
-        bp = op;
-        bc = oc;
-      }
-    }
-    if (lane == 0) {
-      wv[warp] = bs;
-      wt[warp] = bt;
-      wp[warp] = bp;
-      wc[warp] = bc;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float s = wv[0];
-      int t = wt[0], pp = wp[0];
-      for (int w = 1; w < int(blockDim.x >> 5); ++w)
-        if (wv[w] > s || (wv[w] == s && (wt[w] < t || (wt[w] == t && wp[w] < pp)))) {
-          s = wv[w];
-          t = wt[w];
-          pp = wp[w];
+  if (warp == 0) {
+    // the k best of the Mr x k row candidates, in selection order (key (score, token, row) is unique)
+    float ps = INFINITY;
+    int pt = -1, pm = -1;
+    for (int r = 0; r < p.k; ++r) {
+      float bs = -INFINITY;
+      int bt = INT32_MAX, bm = INT32_MAX;
+      for (int c = lane; c < Mr * p.k; c += 32) {
+        const int m = c / p.k, j = c % p.k;
+        const float sc = cs[m][j];
+        const int tok = ct[m][j];
+        if (sel_before(ps, pt, pm, sc, tok, m) && sel_before(sc, tok, m, bs, bt, bm)) {
+          bs = sc;
+          bt = tok;
+          bm = m;
         }
-      sel_s[r] = s;
-      sel_t[r] = t;
-      sel_p[r] = pp;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    // canonical order: parent asc, token asc (insertion sort, k <= 32)
-    for (int i = 1; i < p.k; ++i) {
-      const float s = sel_s[i];
-      const int t = sel_t[i], pp = sel_p[i];
-      int j = i - 1;
-      while (j >= 0 && (sel_p[j] > pp || (sel_p[j] == pp && sel_t[j] > t))) {
-        sel_s[j + 1] = sel_s[j];
-        sel_t[j + 1] = sel_t[j];
-        sel_p[j + 1] = sel_p[j];
-        --j;
       }
-      sel_s[j + 1] = s;
-      sel_t[j + 1] = t;
-      sel_p[j + 1] = pp;
+      for (int o = 16; o; o >>= 1) {
+        const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+        const int om = __shfl_xor_sync(0xffffffffu, bm, o);
+        if (sel_before(os, ot, om, bs, bt, bm)) {
+          bs = os;
+          bt = ot;
+          bm = om;
+        }
+      }
+      if (lane == 0) {
+        sel_s[r] = bs;
+        sel_t[r] = bt;
+        sel_p[r] = bm;
+      }
+      ps = bs;
+      pt = bt;
+      pm = bm;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      // canonical order: parent asc, token asc (insertion sort, k <= 32)
+      for (int i = 1; i < p.k; ++i) {
+        const float s = sel_s[i];
+        const int t = sel_t[i], pp = sel_p[i];
+        int j = i - 1;
+        while (j >= 0 && (sel_p[j] > pp || (sel_p[j] == pp && sel_t[j] > t))) {
+          sel_s[j + 1] = sel_s[j];
+          sel_t[j + 1] = sel_t[j];
+          sel_p[j + 1] = sel_p[j];
+          --j;
+        }
+        sel_s[j + 1] = s;
+        sel_t[j + 1] = t;
+        sel_p[j + 1] = pp;
+      }
     }
   }
   __syncthreads();
@@ -347,7 +472,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
 void launch_topk_select(const TopkParams& p, bool pdl, cudaStream_t st) {
   void* args[] = {const_cast<TopkParams*>(&p)};
   const int nreq = p.req_rows > 0 ? p.M / p.req_rows : 1;
-  launch_pdl((const void*)topk_select_kernel, dim3(nreq), dim3(1024), 64 * 4 + 4 * 32 * 4, pdl, st, args);
+  launch_pdl((const void*)topk_select_kernel, dim3(nreq), dim3(1024), 3 * 32 * 4, pdl, st, args);
 }
 
 void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
@@ -355,7 +480,7 @@ void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
   void* args[] = {&pp};
   launch_pdl((const void*)topk_block_kernel, dim3(p.M, p.blocks_per_row), dim3(256), 0, pdl, st, args);
   const int n_req = p.req_rows > 0 ? p.M / p.req_rows : 1;
-  launch_pdl((const void*)topk_select_kernel, dim3(n_req), dim3(1024), 32 * 4 * 5, pdl, st, args);
+  launch_pdl((const void*)topk_select_kernel, dim3(n_req), dim3(1024), 3 * 32 * 4, pdl, st, args);
 }
 
 // ---------------------------------------------------------------------------

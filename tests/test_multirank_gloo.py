@@ -24,7 +24,15 @@ def _worker(rank, world, port, q):
     from synth.configs import QWEN7B
     ms, tok = bench.aggregate_ranks(dist, 100.0 * (rank + 1), 7 * (rank + 1))
     prompt = bench.request_for_rank(rank, QWEN7B.vocab)
-    q.put((rank, ms, tok, prompt.tolist()))
+    class FakeCtx:   # records the cooperative-streaming handshake (NEXT-1) without a GPU
+        def coop_export(self):
+            return bytes([rank]) * 256
+
+        def coop_enable(self, r, handles):
+            self.enabled = (r, handles)
+    fc = FakeCtx()
+    bench.coop_handshake(fc, dist, rank, world)
+    q.put((rank, ms, tok, prompt.tolist(), fc.enabled[0], [h[0] for h in fc.enabled[1]]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -42,3 +50,5 @@ def test_partition_and_aggregate():
         assert p.exitcode == 0
     assert all(r[1] == 200.0 and r[2] == 21.0 for r in res)      # max time, summed tokens
     assert res[0][3] != res[1][3]                                # distinct requests per rank
+    for r in res:                                                # coop: own rank, every handle in rank order
+        assert r[4] == r[0] and r[5] == list(range(world))

@@ -11,7 +11,7 @@ for name, skip in (("full", 0), ("-attn", 1), ("-norm", 2), ("-gemv", 4), ("-hea
     print(f"{name:16s} {ss.debug_time_pass(6, 5, skip) * 1e3:9.1f} us/pass", flush=True)
 tr = ss.debug_trace_pass(6).astype("float64")
 t0 = tr[:, 0].min()
-names = ["qkv", "attn", "o", "gate_up", "down"] if os.environ.get("SS_FUSE_MLP") != "1" else ["qkv", "attn", "o", "mlp"]
+names = ["qkv", "attn", "o", "gate_up", "down"]
 print("launch  entry  pdep  cdep  first  loop0  loopmax  end   (us, rel. to first entry)")
 prev_end = None
 for i, r in enumerate(tr[:3 * len(names)]):

@@ -1,16 +1,24 @@
 #!/bin/bash
-# Round evidence: bench line, ncu launch list of the bench command, ncu --set full of K2 launches.
+# Round evidence (tag $1, default r2): GPU tests + smoke, the bench line, the ncu launch list of the
+# bench's timed region, ncu --set full of the K2 substitute GEMV (gemv_q_kernel) launches and of the
+# tcgen05 bf16 head GEMV (gemv_kernel) at Qwen2.5-7B shapes.
 set -x
+T=${1:-r2}
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench_r1.jsonl 2> gpurun_out/bench_r1.err
-tail -1 gpurun_out/bench_r1.jsonl
-# launch list: skip the load/prefill/first (eager + capture) step; capture ~1 draft/verify worth
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -s 2200 -c 2500 --csv \
-  --log-file gpurun_out/launches_r1.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
-  > gpurun_out/ncu_launch_r1.log 2>&1
-# full capture of dequant-GEMV launches at Qwen-7B shapes (M = 6): a gate_up and a qkv launch
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 60 -c 1 \
-  -o gpurun_out/k2_gate_up_r1 python tools/prof_gemv.py 6 > gpurun_out/ncu_k2_r1.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 4 -c 1 \
-  -o gpurun_out/k2_qkv_r1 python tools/prof_gemv.py 6 >> gpurun_out/ncu_k2_r1.log 2>&1
-ls -la gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/tests_$T.log 2>&1; echo "tests rc=$?" >> gpurun_out/tests_$T.log
+timeout 300 python -c 'import __graft_entry__ as g; g.smoke(); print("smoke ok")' > gpurun_out/smoke_$T.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_$T.jsonl 2> gpurun_out/bench_$T.err
+tail -1 gpurun_out/bench_$T.jsonl | cut -c1-400
+# launch list of exactly the timed steps (bench brackets them with cudaProfilerStart/Stop)
+SS_PROFILE_TIMED=1 timeout 1800 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_$T.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --prompts 0 \
+  > gpurun_out/ncu_launch_$T.log 2>&1
+# full captures at M = 6 (see tools/prof_gemv.py for the launch order)
+for spec in "gate_up 60" "qkv 4" "down 116"; do
+  set -- $spec
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_q_kernel -s $2 -c 1 \
+    -o gpurun_out/k2_$1_$T python tools/prof_gemv.py 6 >> gpurun_out/ncu_k2_$T.log 2>&1
+done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 \
+  -o gpurun_out/head_$T python tools/prof_gemv.py 6 >> gpurun_out/ncu_k2_$T.log 2>&1
+ls -la gpurun_out | tail -30

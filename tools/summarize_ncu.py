@@ -21,7 +21,7 @@ for r in data:
     agg[name][0] += 1
     agg[name][1] += us
 tot = sum(v[1] for v in agg.values())
-out.append(f"# ncu launch list, bench.py --steps 1 --warmup 1 ({len(data)} launches captured, tag {tag})\n")
+out.append(f"# ncu launch list of bench.py's timed region (SS_PROFILE_TIMED=1, --profile-from-start off; {len(data)} launches captured, tag {tag})\n")
 out.append("Per-launch `gpu__time_duration.sum` under ncu (serialised, cold caches): compare SHARES, not absolutes.\n")
 out.append("| kernel | launches | total us | avg us | share |\n|---|---:|---:|---:|---:|")
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -41,12 +41,14 @@ want = ["Kernel Name", "Grid Size", "Block Size", "launch__cluster_dim_x", "gpu_
         "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second"]
 traffic = {}
 for name, rep in (("gate_up (N=37888, K=3584, M=6)", f"k2_gate_up_{tag}.ncu-rep"), ("qkv (N=4608, K=3584, M=6)", f"k2_qkv_{tag}.ncu-rep"),
-                  ("2-bit gate_up (N=37888, K=3584, M=6; NEXT-3)", f"k2q2_gate_up_{tag}.ncu-rep")):
+                  ("down (N=3584, K=18944, M=6)", f"k2_down_{tag}.ncu-rep"),
+                  ("2-bit gate_up (N=37888, K=3584, M=6; NEXT-3)", f"k2q2_gate_up_{tag}.ncu-rep"),
+                  ("tcgen05 bf16 head (N=152064, K=3584, M=6)", f"head_{tag}.ncu-rep")):
     path = os.path.join(src, rep)
     if not os.path.exists(path):
         continue
     hdr, units, r = raw(path)
-    out.append(f"## ncu --set full: K2 dequant-GEMV {name}\n")
+    out.append(f"## ncu --set full: {name}\n")
     out.append("| metric | value | unit |\n|---|---|---|")
     for w in want:
         if w in hdr:
@@ -70,7 +72,9 @@ if traffic:
                "per_kernel_traffic_bytes": traffic,
                "algorithmic_bytes": {"gate_up": 37888 * 3584 // 2 + 37888 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 37888 * 2,
                                      "qkv": 4608 * 3584 // 2 + 4608 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 4608 * 2,
-                                     "2-bit gate_up": 37888 * 3584 // 4 + 37888 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 37888 * 2},
-               "source": f"gpurun_out/k2_*_{tag}.ncu-rep (ncu --set full)"},
+                                     "down": 3584 * 18944 // 2 + 3584 * 18944 // 64 * 4 + 6 * 18944 * 2 + 6 * 3584 * 2,
+                                     "2-bit gate_up": 37888 * 3584 // 4 + 37888 * 3584 // 64 * 4 + 6 * 3584 * 2 + 6 * 37888 * 2,
+                                     "head": 152064 * 3584 * 2 + 6 * 3584 * 2},
+               "source": f"gpurun_out/{{k2_*,head}}_{tag}.ncu-rep (ncu --set full)"},
               open(os.path.join(dst, "k2_traffic.json"), "w"), indent=1)
 print("\n".join(out))
