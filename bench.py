@@ -54,6 +54,8 @@ def args_():
                     help="Table-2 ablation: no copy/compute overlap in the verify streaming (PAPER.md:305-308)")
     ap.add_argument("--prompts", type=int, default=4, help="prompt sweep: MT-Bench-shaped prompts (0 = skip)")
     ap.add_argument("--repeats", type=int, default=1, help="prompt sweep: repeats of each prompt")
+    ap.add_argument("--separate-draft-kv", action="store_true",
+                    help="NEXT-4 ablation: the draft keeps its own KV-cache (Table 2 without '+ shared KV')")
     ap.add_argument("--coop", action="store_true",
                     help="NEXT-1 cooperative weight streaming under torchrun: rank r pulls 1/N of every streamed "
                          "group over its host link and pushes it to the peers over NVLink (ss_coop_*)")
@@ -315,7 +317,8 @@ def run_ours(a):
     t_setup = time.time()
     Bq = a.batch
     ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256,
-                 max_batch=Bq, embed_on_host=0 if a.embed_gpu else 1, async_stream=0 if a.no_async else 1)
+                 max_batch=Bq, embed_on_host=0 if a.embed_gpu else 1, async_stream=0 if a.no_async else 1,
+                 separate_draft_kv=1 if a.separate_draft_kv else 0)
     if a.sub_bits != 4:
         ss.set_substitute_bits(a.sub_bits)
     shm = load_weights_for_job(ss, dist, local, a.n_resident)

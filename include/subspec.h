@@ -91,6 +91,14 @@ typedef struct {
                              previous group's compute. */
   int32_t cuda_graphs;    /* 1 (default): the draft loop is replayed from a CUDA graph; 0: eager */
   int32_t fuse_norm;      /* 1 (default): RMSNorm fused into the o/down GEMV epilogues (draft) */
+  int32_t separate_draft_kv; /* 0 (default): the draft attends over the target's committed KV (shared
+                             KV-cache).  1: SURVEY §8(f) NEXT-4, Table 2's row
+                             without "+ shared KV": the draft keeps its own
+                             committed cache, filled with the draft's own K/V — by draft forwards of
+                             every prefill chunk and, each step, by committing the draft's tree K/V of
+                             the accepted path (one extra KV-only draft pass covers depth D).  Costs
+                             2 x L x max_context x n_kv x head_dim x 2 bytes of the cap plus tree
+                             scratch.  One request per context (max_batch <= 1), bf16 only. */
 } ss_options;
 void ss_default_options(ss_options* out);
 
@@ -303,8 +311,10 @@ ss_status ss_debug_forward(ss_ctx* ctx, int32_t which, const int32_t* tokens, co
 /* Replace the device tree by a given depth-major tree (root first) for verify/accept tests. */
 ss_status ss_debug_set_tree(ss_ctx* ctx, const int32_t* tokens, const int32_t* parents, int32_t n, int32_t top_k);
 /* Committed K/V rows [pos0, pos0+n) of a layer -> host [n_kv x n x head_dim] bf16 bits each (batched
- * slots: slot b's position p is row b * max_context + p). */
+ * slots: slot b's position p is row b * max_context + p).  ss_debug_read_draft_kv: the same rows of
+ * the draft's own cache (ss_options.separate_draft_kv = 1; STRUCTURE otherwise). */
 ss_status ss_debug_read_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
+ss_status ss_debug_read_draft_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
 /* Time launches of a matrix kernel with M tokens: average device ms per launch over `iters` rounds
  * (CUDA events on the compute stream).  which 0: the draft GEMV (K2 on substitutes, bf16 GEMV on
  * resident layers / the head), M <= 32; which 1: the target GEMM (K6) on resident layers or the head

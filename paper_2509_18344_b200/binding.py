@@ -31,7 +31,7 @@ SS_BF16, SS_FP32 = 0, 1
 
 class OptionsC(ctypes.Structure):
     _fields_ = [("embed_on_host", c_int32), ("async_stream", c_int32), ("cuda_graphs", c_int32),
-                ("fuse_norm", c_int32)]
+                ("fuse_norm", c_int32), ("separate_draft_kv", c_int32)]
 
 
 class HostLayerC(ctypes.Structure):
@@ -99,6 +99,7 @@ _FUNCS = {
     "ss_debug_forward": [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p, c_void_p],
     "ss_debug_set_tree": [c_void_p, c_void_p, c_void_p, c_int32, c_int32],
     "ss_debug_read_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
+    "ss_debug_read_draft_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
     "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_time_pass": [c_void_p, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_set_knob": [c_void_p, c_int32, c_int32],
@@ -152,7 +153,7 @@ class SubSpec:
 
     def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256, max_batch=1,
                  precision=SS_BF16, **options):
-        """options: ss_options fields (embed_on_host, async_stream, cuda_graphs, fuse_norm)."""
+        """options: ss_options fields (embed_on_host, async_stream, cuda_graphs, fuse_norm, separate_draft_kv)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("SubSpec needs a CUDA device (no CPU fallback)")
@@ -436,6 +437,14 @@ class SubSpec:
         k = np.zeros(c.n_kv_heads * n * c.head_dim, np.float32 if self.precision == SS_FP32 else np.uint16)
         v = np.zeros_like(k)
         self._check(self.lib.ss_debug_read_kv(self.ctx, layer, pos0, n, _ptr(k), _ptr(v)))
+        return k.reshape(c.n_kv_heads, n, c.head_dim), v.reshape(c.n_kv_heads, n, c.head_dim)
+
+    def debug_read_draft_kv(self, layer, pos0, n):
+        """The draft's own committed K/V rows (separate_draft_kv contexts), bf16 bit patterns."""
+        c = self.cfg
+        k = np.zeros(c.n_kv_heads * n * c.head_dim, np.uint16)
+        v = np.zeros_like(k)
+        self._check(self.lib.ss_debug_read_draft_kv(self.ctx, layer, pos0, n, _ptr(k), _ptr(v)))
         return k.reshape(c.n_kv_heads, n, c.head_dim), v.reshape(c.n_kv_heads, n, c.head_dim)
 
     def debug_time_pass(self, M, iters=5, skip=0):

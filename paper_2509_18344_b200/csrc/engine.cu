@@ -90,6 +90,7 @@ struct ss_ctx {
   // kv + tree
   uint16_t *kc = nullptr, *vc = nullptr, *kt = nullptr, *vt = nullptr;
   int64_t kc_layer = 0, kt_layer = 0;
+  uint16_t *kcd = nullptr, *vcd = nullptr, *ktd = nullptr, *vtd = nullptr;   // NEXT-4 separate draft KV (else null)
   int max_nodes = 0, anc_stride = 0;
   int *tok = nullptr, *parent = nullptr, *depth = nullptr, *anc = nullptr;
   float* score = nullptr;
@@ -571,16 +572,17 @@ ss_status forward_pass(ss_ctx* c, bool target, int M, int node_base, const PassO
     e.kind = EPI_QKV;
     e.bias = c->lw[l].bias;
     e.q_out = c->qbuf;
-    e.k_tree = c->kt + l * c->kt_layer;
-    e.v_tree = c->vt + l * c->kt_layer;
+    const bool own = !target && c->ktd;   // NEXT-4: the draft's own K/V (tree scratch and cache)
+    e.k_tree = (own ? c->ktd : c->kt) + l * c->kt_layer;
+    e.v_tree = (own ? c->vtd : c->vt) + l * c->kt_layer;
     e.node_base = node_base;
     if ((s = matmul(c, target, l, 0, c->hfrag, M, e)) != SS_OK) return s;
     AttnParams a{};
     a.q = c->qbuf;
-    a.k_cache = c->kc + l * c->kc_layer;
-    a.v_cache = c->vc + l * c->kc_layer;
-    a.k_tree = c->kt + l * c->kt_layer;
-    a.v_tree = c->vt + l * c->kt_layer;
+    a.k_cache = (own ? c->kcd : c->kc) + l * c->kc_layer;
+    a.v_cache = (own ? c->vcd : c->vc) + l * c->kc_layer;
+    a.k_tree = e.k_tree;
+    a.v_tree = e.v_tree;
     a.committed_len = c->committed_len;
     a.anc = c->anc;
     a.depth = c->depth;
@@ -763,6 +765,13 @@ ss_status draft_loop(ss_ctx* c, int D, int k, float T) {
     }
     if ((s = check_launch(c, "topk")) != SS_OK) return s;
   }
+  if (c->ktd) {
+    // NEXT-4 separate draft KV: the depth-D nodes (the root when D = 0) are never a draft frontier; one
+    // KV-only pass (no head) gives every tree node its draft K/V, so whatever path is accepted can be
+    // committed to the draft's cache
+    s = forward_pass(c, false, D > 0 ? k : 1, D > 0 ? 1 + (D - 1) * k : 0, PassOut{});
+    if (s != SS_OK) return s;
+  }
   return SS_OK;
 }
 
@@ -864,6 +873,15 @@ ss_status do_accept(ss_ctx* c, bool chain, int slot = 0) {
   a.chain = chain ? 1 : 0;
   launch_accept_commit(a, c->use_pdl, c->cs);
   c->launches += 2;
+  if (c->kcd) {   // NEXT-4: the same path's draft K/V into the draft's own cache (same commit meta)
+    AcceptParams d = a;
+    d.k_cache = c->kcd;
+    d.v_cache = c->vcd;
+    d.k_tree = c->ktd;
+    d.v_tree = c->vtd;
+    launch_commit(d, c->use_pdl, c->cs);
+    c->launches++;
+  }
   return check_launch(c, "accept_commit");
 }
 
@@ -915,6 +933,7 @@ void ss_default_options(ss_options* o) {
   o->async_stream = 1;
   o->cuda_graphs = 1;
   o->fuse_norm = 1;
+  o->separate_draft_kv = 0;
 }
 
 ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_options* opt, int device, void* dev_arena,
@@ -938,6 +957,10 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
     c->use_graphs = false;
   }
   c->fuse_norm = c->opt.fuse_norm != 0;
+  if (c->opt.separate_draft_kv && (c->f32 || lim->max_batch > 1)) {   // NEXT-4 variant: one bf16 request
+    delete c;
+    return SS_ERR_INVALID;
+  }
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete c;
@@ -1010,6 +1033,12 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   c->vc = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * c->kv_es));
   c->kt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * c->kv_es));
   c->vt = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * c->kv_es));
+  if (c->opt.separate_draft_kv) {
+    c->kcd = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
+    c->vcd = (uint16_t*)chk(A(size_t(c->L) * c->kc_layer * 2));
+    c->ktd = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
+    c->vtd = (uint16_t*)chk(A(size_t(c->L) * c->kt_layer * 2));
+  }
   if (c->f32) {
     const size_t rows = size_t(c->mpad_max);
     c->h32 = (float*)chk(A(rows * std::max(c->H, c->qd) * 4));
@@ -1445,6 +1474,10 @@ static ss_status prefill_slot_impl(ss_ctx* c, int slot, const int32_t* prompt, i
     c->n_nodes = m;
     c->cur_k = 1;
     c->cur_deff = 0;
+    for (int r0 = 0; c->kcd && r0 < m; r0 += 32) {   // NEXT-4: the draft's own K/V of the chunk (GEMV: <= 32 rows)
+      ss_status s = forward_pass(c, false, std::min(32, m - r0), r0, PassOut{});
+      if (s != SS_OK) return s;
+    }
     ss_status s = do_verify_slot(c, slot);
     if (s != SS_OK) return s;
     if ((s = do_accept(c, true, slot)) != SS_OK) return s;
@@ -2378,22 +2411,34 @@ ss_status ss_debug_set_tree(ss_ctx* c, const int32_t* tokens, const int32_t* par
   return SS_OK;
 }
 
-ss_status ss_debug_read_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v) {
-  GUARD(c);
+static ss_status read_kv_impl(ss_ctx* c, bool draft, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v) {
   // pos0 indexes the kv-head row space of all slots: slot b's committed rows start at b * max_context
   if (layer < 0 || layer >= c->L || pos0 < 0 || n < 1 || pos0 + n > c->kv_ctx || !k || !v)
     return fail(c, SS_ERR_INVALID, "read_kv args");
+  if (draft && !c->kcd) return fail(c, SS_ERR_STRUCTURE, "read_draft_kv: the draft shares the target's cache");
+  const uint16_t* kc = draft ? c->kcd : c->kc;
+  const uint16_t* vc = draft ? c->vcd : c->vc;
   CK(cudaStreamSynchronize(c->cs));
   const int es = c->kv_es;   // SS_FP32: 4-byte elements (k, v hold fp32 values)
   for (int h = 0; h < c->nkv; ++h) {
     const int64_t src = (layer * c->kc_layer + (int64_t(h) * c->kv_ctx + pos0) * c->d) * es;
-    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(k) + int64_t(h) * n * c->d * es, reinterpret_cast<uint8_t*>(c->kc) + src,
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(k) + int64_t(h) * n * c->d * es, reinterpret_cast<const uint8_t*>(kc) + src,
                        size_t(n) * c->d * es, cudaMemcpyDeviceToHost, c->cs));
-    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(v) + int64_t(h) * n * c->d * es, reinterpret_cast<uint8_t*>(c->vc) + src,
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(v) + int64_t(h) * n * c->d * es, reinterpret_cast<const uint8_t*>(vc) + src,
                        size_t(n) * c->d * es, cudaMemcpyDeviceToHost, c->cs));
   }
   CK(cudaStreamSynchronize(c->cs));
   return SS_OK;
+}
+
+ss_status ss_debug_read_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v) {
+  GUARD(c);
+  return read_kv_impl(c, false, layer, pos0, n, k, v);
+}
+
+ss_status ss_debug_read_draft_kv(ss_ctx* c, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v) {
+  GUARD(c);
+  return read_kv_impl(c, true, layer, pos0, n, k, v);
 }
 
 }  // extern "C"

@@ -204,6 +204,7 @@ struct AcceptParams {
   // by node_stride, committed-KV rows by ctx_stride, outputs by out_stride, meta by 2
   int n_req, req0, node_stride, ctx_stride, out_stride;
 };
+void launch_commit(const AcceptParams& p, bool pdl, cudaStream_t st);   // commit only (commit_meta from accept)
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st);
 
 // SS_FP32 precision mode (f32.cu)

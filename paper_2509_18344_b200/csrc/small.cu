@@ -233,7 +233,7 @@ constexpr int kSelRegK = 8;   // topk_select: per-lane register top-k up to this
 SS_DEV bool sel_before(float s, int t, int m, float s2, int t2, int m2) {
   return s > s2 || (s == s2 && (t < t2 || (t == t2 && m < m2)));
 }
-__global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
+__global__ void __launch_bounds__(512) topk_select_kernel(const TopkParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int B = p.blocks_per_row;
   float* sel_s = reinterpret_cast<float*>(sm);      // [k]
@@ -249,17 +249,33 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
   const int Mr = p.req_rows > 0 ? p.req_rows : p.M, r0 = q * Mr;
   const int64_t nofs = int64_t(q) * p.node_stride;
   const float* score = p.score + nofs;
-  if (warp < Mr) {
-    // warp m: row m's max and sum exp((l - max) / T) merged over its B vocab tiles (fixed lane
-    // order + fixed shuffle tree: deterministic), then its k best children in selection order
-    const int m = warp, mg = r0 + m;
-    float mx = -INFINITY;
-    for (int b = lane; b < B; b += 32) mx = fmaxf(mx, p.blk_max[int64_t(mg) * B + b]);
-    mx = warp_max(mx);
-    float sacc = 0.f;
-    for (int b = lane; b < B; b += 32)
-      sacc += p.blk_sum[int64_t(mg) * B + b] * expf((p.blk_max[int64_t(mg) * B + b] - mx) * p.inv_t);
-    const float lse = logf(warp_sum(sacc));
+  for (int m = warp; m < Mr; m += int(blockDim.x >> 5)) {
+    // warp per row m: the row's max and sum exp((l - max) / T) merged over its B vocab tiles (fixed
+    // lane order + fixed shuffle tree: deterministic), then its k best children in selection order
+    const int mg = r0 + m;
+    // one pass, 8 independent loads in flight per lane: a running (max, sum) per lane in its fixed
+    // tile order, then the lanes merged by a fixed shuffle tree
+    float lm = -INFINITY, lsum = 0.f;
+    const float* bmx = p.blk_max + int64_t(mg) * B;
+    const float* bsm = p.blk_sum + int64_t(mg) * B;
+    for (int b0 = lane; b0 < B; b0 += 32 * 8) {
+      float vm[8], vs[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int b = b0 + 32 * j;
+        vm[j] = b < B ? bmx[b] : -INFINITY;
+        vs[j] = b < B ? bsm[b] : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (vm[j] > -INFINITY) {
+          const float nm = fmaxf(lm, vm[j]);
+          lsum = lsum * expf((lm - nm) * p.inv_t) + vs[j] * expf((vm[j] - nm) * p.inv_t);
+          lm = nm;
+        }
+    }
+    const float mx = warp_max(lm);
+    const float lse = logf(warp_sum(lm > -INFINITY ? lsum * expf((lm - mx) * p.inv_t) : 0.f));
     const int nc = B * p.k;
     const int* bi = p.blk_idx + int64_t(mg) * nc;
     const float* bv = p.blk_val + int64_t(mg) * nc;
@@ -278,10 +294,20 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
         lt[i] = INT32_MAX;
         lb[i] = 0;
       }
-#pragma unroll 4
-      for (int t = lane; t < B; t += 32) {
-        const int tok = bi[int64_t(t) * p.k];
-        const float sc = base + ((bv[int64_t(t) * p.k] - mx) * p.inv_t - lse);
+      for (int t0 = lane; t0 < B; t0 += 32 * 8) {
+        int ht[8];
+        float hv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {   // 8 independent head loads in flight
+          const int t = t0 + 32 * j;
+          ht[j] = t < B ? bi[int64_t(t) * p.k] : INT32_MAX;
+          hv[j] = t < B ? bv[int64_t(t) * p.k] : -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+        const int t = t0 + 32 * j, tok = ht[j];
+        if (t >= B) continue;
+        const float sc = base + ((hv[j] - mx) * p.inv_t - lse);
         if (sel_before(sc, tok, 0, ls[kSelRegK - 1], lt[kSelRegK - 1], 0)) {
           float cs_ = sc;
           int ct_ = tok, cb_ = t;
@@ -297,6 +323,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
               ct_ = tt;
               cb_ = tb;
             }
+        }
         }
       }
       int mytile = -1;   // lane r < k: the r-th best tile
@@ -472,7 +499,7 @@ __global__ void __launch_bounds__(1024) topk_select_kernel(const TopkParams p) {
 void launch_topk_select(const TopkParams& p, bool pdl, cudaStream_t st) {
   void* args[] = {const_cast<TopkParams*>(&p)};
   const int nreq = p.req_rows > 0 ? p.M / p.req_rows : 1;
-  launch_pdl((const void*)topk_select_kernel, dim3(nreq), dim3(1024), 3 * 32 * 4, pdl, st, args);
+  launch_pdl((const void*)topk_select_kernel, dim3(nreq), dim3(512), 3 * 32 * 4, pdl, st, args);
 }
 
 void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
@@ -480,7 +507,7 @@ void launch_topk(const TopkParams& p, bool pdl, cudaStream_t st) {
   void* args[] = {&pp};
   launch_pdl((const void*)topk_block_kernel, dim3(p.M, p.blocks_per_row), dim3(256), 0, pdl, st, args);
   const int n_req = p.req_rows > 0 ? p.M / p.req_rows : 1;
-  launch_pdl((const void*)topk_select_kernel, dim3(n_req), dim3(1024), 3 * 32 * 4, pdl, st, args);
+  launch_pdl((const void*)topk_select_kernel, dim3(n_req), dim3(512), 3 * 32 * 4, pdl, st, args);
 }
 
 // ---------------------------------------------------------------------------
@@ -604,6 +631,13 @@ __global__ void __launch_bounds__(256) commit_kernel(const AcceptParams p) {
     reinterpret_cast<uint32_t*>(cache + int64_t(base + j) * p.head_dim)[i] =
         reinterpret_cast<const uint32_t*>(tree + int64_t(slot) * p.head_dim)[i];
   }
+}
+
+void launch_commit(const AcceptParams& p, bool pdl, cudaStream_t st) {
+  AcceptParams pp = p;
+  void* args[] = {&pp};
+  const int n_req = p.n_req > 0 ? p.n_req : 1;
+  launch_pdl((const void*)commit_kernel, dim3(p.n_layers, p.n_kv, 2 * n_req), dim3(256), 0, pdl, st, args);
 }
 
 void launch_accept_commit(const AcceptParams& p, bool pdl, cudaStream_t st) {

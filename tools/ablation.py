@@ -4,18 +4,23 @@ Runs bench.py variants in fresh processes and writes
 profiles/ablation_<tag>.json.  Variants: full SubSpec; async transfer off (--no-async, ss_options.async_stream = 0: each
 streamed group is copied only after the previous group's compute); sharpening off
 (T = 1); a shallower tree (D = 24); and the offloading AR baseline through the same engine
-(D = 0, the paper's "None" row) for the speedup.  Shared-vs-separate draft KV is not built.
+(D = 0, the paper's "None" row) for the speedup; the draft without the shared KV-cache
+(--separate-draft-kv, Table 2's row before "+ shared KV"); and the draft temperature
+sweep of Table 5 (T = 0.2 .. 1.2).  On random weights tau is not the paper's: the
+ladder measures what each switch costs or saves in step time on B200.
 """
 import json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-steps = ["--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+steps = ["--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--prompts", "0"]
 variants = [
     ("full (D=48, k=6, T=0.2, async)", {}, []),
     ("async transfer off", {}, ["--no-async"]),
     ("sharpening off (T=1)", {}, ["--temp", "1.0"]),
     ("shallower tree (D=24)", {}, ["--depth", "24"]),
+    ("separate draft KV (no '+ shared KV')", {}, ["--separate-draft-kv"]),
+    *[(f"draft temperature T={t}", {}, ["--temp", str(t)]) for t in (0.4, 0.6, 0.8, 1.2)],
     # 16 timed steps: the ring prefetched before the timed region is not hidden under a draft here
     ("offloading AR baseline (D=0)", {}, ["--depth", "0", "--topk", "1", "--steps", "16"]),
 ]

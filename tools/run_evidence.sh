@@ -21,4 +21,12 @@ for spec in "gate_up 60" "qkv 4" "down 116"; do
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 \
   -o gpurun_out/head_$T python tools/prof_gemv.py 6 >> gpurun_out/ncu_k2_$T.log 2>&1
+# K6 (tcgen05 verify GEMM) at M = 289 on a resident Qwen2.5-7B-width layer: gate_up and the head
+# (launch order in tools/prof_k6.py with K6_ITERS=1: qkv 0-1, o 2-3, gate_up 4-5, down 6-7, head 8-9)
+for spec in "gate_up 4" "head 8"; do
+  set -- $spec
+  K6_VARIANTS=0 K6_ITERS=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s $2 -c 1 \
+    -o gpurun_out/k6_$1_$T python tools/prof_k6.py 289 >> gpurun_out/ncu_k6_$T.log 2>&1
+done
+K6_VARIANTS=0,2,1 timeout 600 python tools/prof_k6.py 289 1025 > gpurun_out/k6_timing_$T.jsonl 2>> gpurun_out/ncu_k6_$T.log
 ls -la gpurun_out | tail -30

@@ -38,12 +38,15 @@ want = ["Kernel Name", "Grid Size", "Block Size", "launch__cluster_dim_x", "gpu_
         "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second"]
+        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second",
+        "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"]
 traffic = {}
 for name, rep in (("gate_up (N=37888, K=3584, M=6)", f"k2_gate_up_{tag}.ncu-rep"), ("qkv (N=4608, K=3584, M=6)", f"k2_qkv_{tag}.ncu-rep"),
                   ("down (N=3584, K=18944, M=6)", f"k2_down_{tag}.ncu-rep"),
                   ("2-bit gate_up (N=37888, K=3584, M=6; NEXT-3)", f"k2q2_gate_up_{tag}.ncu-rep"),
-                  ("tcgen05 bf16 head (N=152064, K=3584, M=6)", f"head_{tag}.ncu-rep")):
+                  ("tcgen05 bf16 head (N=152064, K=3584, M=6)", f"head_{tag}.ncu-rep"),
+                  ("K6 tcgen05 verify GEMM gate_up (N=37888, K=3584, M=289)", f"k6_gate_up_{tag}.ncu-rep"),
+                  ("K6 tcgen05 verify head + argmax (N=152064, K=3584, M=289)", f"k6_head_{tag}.ncu-rep")):
     path = os.path.join(src, rep)
     if not os.path.exists(path):
         continue
