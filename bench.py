@@ -54,6 +54,8 @@ def args_():
                     help="Table-2 ablation: no copy/compute overlap in the verify streaming (PAPER.md:305-308)")
     ap.add_argument("--prompts", type=int, default=4, help="prompt sweep: MT-Bench-shaped prompts (0 = skip)")
     ap.add_argument("--repeats", type=int, default=1, help="prompt sweep: repeats of each prompt")
+    ap.add_argument("--no-compress", action="store_true",
+                    help="stream plain bf16 layers (ss_options.compress_stream = 0) instead of the lossless codec")
     ap.add_argument("--separate-draft-kv", action="store_true",
                     help="NEXT-4 ablation: the draft keeps its own KV-cache (Table 2 without '+ shared KV')")
     ap.add_argument("--coop", action="store_true",
@@ -318,7 +320,7 @@ def run_ours(a):
     Bq = a.batch
     ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256,
                  max_batch=Bq, embed_on_host=0 if a.embed_gpu else 1, async_stream=0 if a.no_async else 1,
-                 separate_draft_kv=1 if a.separate_draft_kv else 0)
+                 separate_draft_kv=1 if a.separate_draft_kv else 0, compress_stream=0 if a.no_compress else 1)
     if a.sub_bits != 4:
         ss.set_substitute_bits(a.sub_bits)
     shm = load_weights_for_job(ss, dist, local, a.n_resident)
@@ -537,6 +539,10 @@ def run_ours(a):
                      "draft_pass": draft_pass},
         "streaming": {"mode": f"cooperative over {world} ranks (NEXT-1)" if coop else "per rank",
                       "peer_bytes_per_step": st["peer_bytes"] / a.steps,
+                      "codec": "off (plain bf16)" if a.no_compress else "lossless exponent-coded bf16 (K7 codec)",
+                      "bf16_bytes_per_step": st["stream_raw_bytes"] / a.steps,
+                      "codec_ratio": (st["stream_bytes"] / st["stream_raw_bytes"]) if st["stream_raw_bytes"] else None,
+                      "effective_bf16_gbs": st["stream_raw_bytes"] / (st["stream_busy_ms"] * 1e-3) / 1e9 if st["stream_busy_ms"] else None,
                       "bytes_per_step": s_host, "busy_gbs": stream_gbs,
                       "host_link_gbs_measured": link_gbs, "frac": (stream_gbs / link_gbs) if stream_gbs else None,
                       "duty_cycle": (st["stream_busy_ms"] / ms) if ms else None},

@@ -99,6 +99,13 @@ typedef struct {
                              the accepted path (one extra KV-only draft pass covers depth D).  Costs
                              2 x L x max_context x n_kv x head_dim x 2 bytes of the cap plus tree
                              scratch.  One request per context (max_batch <= 1), bf16 only. */
+  int32_t compress_stream;  /* 1 (default, bf16): the host store holds each offloaded matrix as a
+                             lossless exponent-coded blob (sign+mantissa bytes, 3-bit exponent codes,
+                             exceptions; ~0.69 of the bf16 bytes for Gaussian-like weights), streamed
+                             as is and decoded on the GPU before the verify GEMM: the same bf16
+                             weights, fewer bytes over the host link (A4).  Costs
+                             one decode buffer of the largest matrix group in the cap.  0: plain bf16.
+                             Ignored in SS_FP32 mode. */
 } ss_options;
 void ss_default_options(ss_options* out);
 
@@ -115,6 +122,8 @@ typedef struct {
   int64_t arena_used, arena_cap, ring_bytes, host_pinned_bytes, substitute_bytes;
   int32_t n_resident, n_offloaded, committed_len, last_d_eff;
   double peer_bytes;                          /* NEXT-1: bytes this rank pushed to peers' rings */
+  double stream_raw_bytes;                    /* bf16 bytes of the streamed groups delivered to the
+                                                 verify (stream_bytes: what crossed the host link) */
 } ss_stats;
 
 typedef struct ss_ctx ss_ctx;
@@ -315,6 +324,13 @@ ss_status ss_debug_set_tree(ss_ctx* ctx, const int32_t* tokens, const int32_t* p
  * the draft's own cache (ss_options.separate_draft_kv = 1; STRUCTURE otherwise). */
 ss_status ss_debug_read_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
 ss_status ss_debug_read_draft_kv(ss_ctx* ctx, int32_t layer, int32_t pos0, int32_t n, uint16_t* k, uint16_t* v);
+/* An offloaded group as the verify receives it: the host store's bytes copied to the device and
+ * decoded by the stream codec's GPU kernel (ss_options.compress_stream), natural [N x K] bf16 bits ->
+ * out.  out_mode: -1 plain bf16, 0 raw blob, 1 exponent-coded; out_stream_bytes: bytes streamed per
+ * step for this group (either may be NULL).  Needs an idle ring (before the first prefill).
+ * Errors: INVALID (resident group), STRUCTURE. */
+ss_status ss_debug_decode_group(ss_ctx* ctx, int32_t layer, int32_t group, uint16_t* out, int32_t* out_mode,
+                                uint64_t* out_stream_bytes);
 /* Time launches of a matrix kernel with M tokens: average device ms per launch over `iters` rounds
  * (CUDA events on the compute stream).  which 0: the draft GEMV (K2 on substitutes, bf16 GEMV on
  * resident layers / the head), M <= 32; which 1: the target GEMM (K6) on resident layers or the head

@@ -31,7 +31,7 @@ SS_BF16, SS_FP32 = 0, 1
 
 class OptionsC(ctypes.Structure):
     _fields_ = [("embed_on_host", c_int32), ("async_stream", c_int32), ("cuda_graphs", c_int32),
-                ("fuse_norm", c_int32), ("separate_draft_kv", c_int32)]
+                ("fuse_norm", c_int32), ("separate_draft_kv", c_int32), ("compress_stream", c_int32)]
 
 
 class HostLayerC(ctypes.Structure):
@@ -63,7 +63,7 @@ class StatsC(ctypes.Structure):
                 ("arena_used", c_int64), ("arena_cap", c_int64), ("ring_bytes", c_int64),
                 ("host_pinned_bytes", c_int64), ("substitute_bytes", c_int64), ("n_resident", c_int32),
                 ("n_offloaded", c_int32), ("committed_len", c_int32), ("last_d_eff", c_int32),
-                ("peer_bytes", c_double)]
+                ("peer_bytes", c_double), ("stream_raw_bytes", c_double)]
 
 
 P = ctypes.POINTER
@@ -100,6 +100,7 @@ _FUNCS = {
     "ss_debug_set_tree": [c_void_p, c_void_p, c_void_p, c_int32, c_int32],
     "ss_debug_read_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
     "ss_debug_read_draft_kv": [c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p],
+    "ss_debug_decode_group": [c_void_p, c_int32, c_int32, c_void_p, P(c_int32), P(c_uint64)],
     "ss_debug_time_matmul": [c_void_p, c_int32, c_int32, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_time_pass": [c_void_p, c_int32, c_int32, c_int32, P(c_float)],
     "ss_debug_set_knob": [c_void_p, c_int32, c_int32],
@@ -153,7 +154,8 @@ class SubSpec:
 
     def __init__(self, cfg, arena_bytes, device=0, max_depth=48, max_top_k=6, max_chunk=256, max_batch=1,
                  precision=SS_BF16, **options):
-        """options: ss_options fields (embed_on_host, async_stream, cuda_graphs, fuse_norm, separate_draft_kv)."""
+        """options: ss_options fields (embed_on_host, async_stream, cuda_graphs, fuse_norm, separate_draft_kv,
+        compress_stream)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("SubSpec needs a CUDA device (no CPU fallback)")
@@ -438,6 +440,14 @@ class SubSpec:
         v = np.zeros_like(k)
         self._check(self.lib.ss_debug_read_kv(self.ctx, layer, pos0, n, _ptr(k), _ptr(v)))
         return k.reshape(c.n_kv_heads, n, c.head_dim), v.reshape(c.n_kv_heads, n, c.head_dim)
+
+    def debug_decode_group(self, layer, group):
+        """(natural [N x K] bf16 bits as the verify's GPU decoder produces them, codec mode, streamed bytes)."""
+        N, K = self.group_shape(group)
+        out = np.zeros(N * K, np.uint16)
+        mode, nb = c_int32(), c_uint64()
+        self._check(self.lib.ss_debug_decode_group(self.ctx, layer, group, _ptr(out), ctypes.byref(mode), ctypes.byref(nb)))
+        return out.reshape(N, K), mode.value, nb.value
 
     def debug_read_draft_kv(self, layer, pos0, n):
         """The draft's own committed K/V rows (separate_draft_kv contexts), bf16 bit patterns."""

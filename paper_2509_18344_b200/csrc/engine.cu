@@ -50,6 +50,11 @@ struct LayerW {
   uint8_t* bf16[4] = {nullptr, nullptr, nullptr, nullptr};
   uint8_t* q4[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t host_off[4] = {0, 0, 0, 0};
+  // K7 stream codec (zstream.cu): -1 plain bf16 (no header), 0 raw blob, 1 exponent-coded blob; the
+  // bytes streamed per step and the offset of the raw bf16 data inside a blob
+  int zmode[4] = {-1, -1, -1, -1};
+  size_t host_used[4] = {0, 0, 0, 0};
+  size_t host_a0[4] = {0, 0, 0, 0};
 };
 
 struct StreamItem {
@@ -151,6 +156,8 @@ struct ss_ctx {
   int k2_dbg = 0;             // K2 debug A/B bits (ss_debug_set_knob 1)
   int k2_self_pf = 0;         // K2: L2-prefetch each CTA's own weight range (ss_debug_set_knob 0; measured slower)
   int k6_variant = 0;         // K6 kernel variant (ss_debug_set_knob 2; launch_gemm; A/B only)
+  bool zcomp = false;         // ss_options.compress_stream (bf16 mode): the host store holds coded blobs
+  uint16_t* dbuf = nullptr;   // decoded bf16 of the group being verified (one group; K6 reads it)
   // NEXT-1 cooperative streaming (ss_coop_*): rank r of `coop_world` copies slice r of every streamed
   // group from its host store and pushes it into every peer's ring at the same offset; flags[h] =
   // "rank h's slice of item seq landed here" (= seq + 1), flags[kCoopMax + h] = "rank h consumed
@@ -270,7 +277,7 @@ ss_status pump(ss_ctx* c) {
     // group only when it is the next one consumed and after the previous group's compute
     if (c->serial_stream && seq > c->next_consume) return SS_OK;
     const auto [l, g] = c->cycle[seq % n_items];
-    const size_t B = bf16_bytes(c->gN[g], c->gK[g]);
+    const size_t B = c->lw[l].host_used[g];   // the group's host-store bytes (a codec blob or plain bf16)
     size_t off = c->ring_head;
     if (off + B > c->ring_bytes) off = 0;
     const int ev = int(seq % c->ev_pool);
@@ -325,10 +332,12 @@ ss_status pump(ss_ctx* c) {
       for (int h = 0; h < G; ++h)   // my slice of item seq is in every ring
         CKD(g_write32((CUstream)c->xs, (CUdeviceptr)(c->peer_flags[h] + me), cuuint32_t(seq + 1), 0));
       c->st.stream_bytes += double(hi - lo);
+      c->st.stream_raw_bytes += double(bf16_bytes(c->gN[g], c->gK[g]));
       c->st.peer_bytes += double(hi - lo) * (G - 1);
     } else {
       CK(cudaMemcpyAsync(c->ring + off, c->host + c->lw[l].host_off[g], B, cudaMemcpyHostToDevice, c->xs));
       c->st.stream_bytes += double(B);
+      c->st.stream_raw_bytes += double(bf16_bytes(c->gN[g], c->gK[g]));
     }
     CK(cudaEventRecord(c->ev_t1[ev], c->xs));
     CK(cudaEventRecord(c->ev_copied[ev], c->xs));
@@ -471,7 +480,18 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
   int ev = -1;
   ss_status s = consume_begin(c, l, g, &wp, &ev);
   if (s != SS_OK) return s;
-  p.W = wp;
+  if (w.zmode[g] == 1) {
+    // K7 codec: decode the streamed blob into the group's bf16 tiles, release the ring region, then K6
+    launch_zdecode(wp, c->dbuf, int64_t(N) * K, c->cs);
+    c->launches++;
+    if ((s = check_launch(c, "zdecode")) != SS_OK) return s;
+    if ((s = consume_end(c, ev)) != SS_OK) return s;
+    p.W = reinterpret_cast<const uint8_t*>(c->dbuf);
+    launch_gemm(p, false, c->cs, c->k6_variant);
+    c->launches++;
+    return check_launch(c, "gemm");
+  }
+  p.W = wp + w.host_a0[g];
   launch_gemm(p, false, c->cs, c->k6_variant);   // follows a cross-stream event wait: plain serialisation
   c->launches++;
   s = check_launch(c, "gemm");
@@ -934,6 +954,7 @@ void ss_default_options(ss_options* o) {
   o->cuda_graphs = 1;
   o->fuse_norm = 1;
   o->separate_draft_kv = 0;
+  o->compress_stream = 1;
 }
 
 ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_options* opt, int device, void* dev_arena,
@@ -957,6 +978,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
     c->use_graphs = false;
   }
   c->fuse_norm = c->opt.fuse_norm != 0;
+  c->zcomp = c->opt.compress_stream != 0 && !c->f32;   // the fp32 parity mode reads the store in place
   if (c->opt.separate_draft_kv && (c->f32 || lim->max_batch > 1)) {   // NEXT-4 variant: one bf16 request
     delete c;
     return SS_ERR_INVALID;
@@ -1176,10 +1198,62 @@ static void host_unregister(void* p) {
   }
 }
 
+// host-store bytes of one offloaded group: plain bf16, or a codec blob's capacity (raw fallback fits)
+static size_t group_store_bytes(ss_ctx* c, int g) {
+  const int64_t n = int64_t(c->gN[g]) * c->gK[g];
+  return c->zcomp ? (zblob_cap(n) + 4095) / 4096 * 4096 : size_t(n) * 2;
+}
 static size_t host_store_bytes(ss_ctx* c, int nr) {
-  size_t layer_bf16 = 0;
-  for (int g = 0; g < 4; ++g) layer_bf16 += bf16_bytes(c->gN[g], c->gK[g]);
-  return size_t(c->L - nr) * layer_bf16;
+  size_t layer = 0;
+  for (int g = 0; g < 4; ++g) layer += group_store_bytes(c, g);
+  return size_t(c->L - nr) * layer;
+}
+
+// the offloaded group (l, g) whose tiled bf16 is at ring[0, 2n) -> the host store (blob or plain)
+static ss_status store_group(ss_ctx* c, int l, int g) {
+  LayerW& w = c->lw[l];
+  const int64_t n = int64_t(c->gN[g]) * c->gK[g];
+  if (!c->zcomp) {
+    CK(cudaMemcpyAsync(c->host + w.host_off[g], c->ring, size_t(n) * 2, cudaMemcpyDeviceToHost, c->cs));
+    CK(cudaStreamSynchronize(c->cs));
+    w.zmode[g] = -1;
+    w.host_used[g] = size_t(n) * 2;
+    w.host_a0[g] = 0;
+    return SS_OK;
+  }
+  const size_t a2n = (size_t(n) * 2 + 4095) / 4096 * 4096;
+  uint8_t* blob = c->ring + a2n;
+  uint8_t* scratch = blob + (zblob_cap(n) + 4095) / 4096 * 4096;
+  if (size_t(scratch - c->ring) + 4 * (256 + size_t(n / kZChunk)) > c->ring_bytes)
+    return fail(c, SS_ERR_BUDGET, "ring too small to encode a matrix group");
+  ZHeader hd{};
+  CK(zencode(reinterpret_cast<const uint16_t*>(c->ring), n, blob, scratch, c->cs, &hd));
+  CK(cudaMemcpyAsync(c->host + w.host_off[g], blob, hd.used, cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  w.zmode[g] = int(hd.mode);
+  w.host_used[g] = hd.used;
+  w.host_a0[g] = hd.a0;
+  return SS_OK;
+}
+
+// a group already in a shared host store (attach): its blob header says how it is stored
+static ss_status attach_group(ss_ctx* c, int l, int g) {
+  LayerW& w = c->lw[l];
+  const int64_t n = int64_t(c->gN[g]) * c->gK[g];
+  if (!c->zcomp) {
+    w.zmode[g] = -1;
+    w.host_used[g] = size_t(n) * 2;
+    w.host_a0[g] = 0;
+    return SS_OK;
+  }
+  ZHeader hd;
+  std::memcpy(&hd, c->host + w.host_off[g], sizeof(hd));
+  if (hd.magic != kZMagic || hd.n != uint64_t(n) || hd.used > group_store_bytes(c, g))
+    return fail(c, SS_ERR_INVALID, "shared host store: not filled by a context with the same model and codec");
+  w.zmode[g] = int(hd.mode);
+  w.host_used[g] = hd.used;
+  w.host_a0[g] = hd.a0;
+  return SS_OK;
 }
 
 ss_status ss_host_store_bytes(ss_ctx* c, int32_t n_resident, size_t* out) {
@@ -1217,7 +1291,11 @@ static ss_status fill_synthetic(ss_ctx* c, uint64_t seed, bool fill) {
       launch_gen_natural(w.bias + c->qd + c->kvd, tensor_key(seed, b + 6), c->kvd, scale_c32(0.02), 0, c->cs);
     }
     for (int g = 0; g < 4; ++g) {
-      if (!w.resident && !fill) continue;   // shared store already holds this matrix
+      if (!w.resident && !fill) {   // shared store already holds this matrix
+        ss_status s = attach_group(c, l, g);
+        if (s != SS_OK) return s;
+        continue;
+      }
       uint8_t* dst = w.resident ? w.bf16[g] : c->ring;
       const int K = c->gK[g];
       const float cin = scale_c32(1.0 / std::sqrt(double(K)));
@@ -1234,8 +1312,8 @@ static ss_status fill_synthetic(ss_ctx* c, uint64_t seed, bool fill) {
         launch_gen_tiled(dst, tensor_key(seed, b + 11), c->H, K, cin, 0, 0, c->cs);
       }
       if (!w.resident && fill) {
-        CK(cudaMemcpyAsync(c->host + w.host_off[g], c->ring, bf16_bytes(c->gN[g], K), cudaMemcpyDeviceToHost, c->cs));
-        CK(cudaStreamSynchronize(c->cs));
+        ss_status s = store_group(c, l, g);
+        if (s != SS_OK) return s;
       }
     }
   }
@@ -1308,7 +1386,9 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
   const size_t avail = c->ar.cap - c->ar.used - 4096 * 8;
   auto need = [&](int nr) {
     const int off = c->L - nr;
-    return size_t(nr) * layer_bf16 + size_t(off) * layer_q4 + (off > 0 ? 2 * max_group : max_group);
+    // offloaded layers: a ring of >= two groups (+ codec scratch) and, with the codec, the decode buffer
+    return size_t(nr) * layer_bf16 + size_t(off) * layer_q4 +
+           (off > 0 ? 2 * max_group + (c->zcomp ? max_group + (8u << 20) : 0) : max_group);
   };
   int nr = n_resident;
   if (nr < 0) {
@@ -1328,12 +1408,16 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
         w.q4[g] = (uint8_t*)c->ar.alloc(sub_bytes(c->gN[g], c->gK[g], c->sub_bits), 1024);
     }
   }
+  if (c->zcomp && nr < c->L) {
+    c->dbuf = (uint16_t*)c->ar.alloc(max_group, 4096);
+    if (!c->dbuf) return fail(c, SS_ERR_BUDGET, "no room for the stream decode buffer");
+  }
   // the staging ring takes what is left
   c->ring_bytes = (c->ar.cap - c->ar.used - 4096) / 4096 * 4096;
   c->ring = (uint8_t*)c->ar.alloc(c->ring_bytes, 4096);
   if (!c->ring || c->ring_bytes < max_group) return fail(c, SS_ERR_BUDGET, "no room for the staging ring");
   // pinned host store for offloaded layers (device layout)
-  c->host_bytes = size_t(c->L - nr) * layer_bf16;
+  c->host_bytes = host_store_bytes(c, nr);
   if (ext_host) {
     if (ext_bytes < c->host_bytes) return fail(c, SS_ERR_BUDGET, "shared host store smaller than ss_host_store_bytes");
     if (c->host_bytes && !host_register(ext_host, c->host_bytes))
@@ -1355,7 +1439,7 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
     for (int l = nr; l < c->L; ++l)
       for (int g = 0; g < 4; ++g) {
         c->lw[l].host_off[g] = off;
-        off += bf16_bytes(c->gN[g], c->gK[g]);
+        off += group_store_bytes(c, g);
       }
   }
   if (hw) {
@@ -1392,10 +1476,7 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
         uint8_t* dst = w.resident ? w.bf16[g] : c->ring;
         ss_status s = fill_group_from_host(c, h, g, dst, w.resident ? reinterpret_cast<uint16_t*>(c->ring) : staging);
         if (s != SS_OK) return s;
-        if (!w.resident) {
-          CK(cudaMemcpyAsync(c->host + w.host_off[g], c->ring, bf16_bytes(c->gN[g], c->gK[g]), cudaMemcpyDeviceToHost, c->cs));
-          CK(cudaStreamSynchronize(c->cs));
-        }
+        if (!w.resident && (s = store_group(c, l, g)) != SS_OK) return s;
       }
     }
   } else {
@@ -1442,8 +1523,17 @@ ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
   for (int l = c->n_resident; l < c->L; ++l)
     for (int g = 0; g < 4; ++g) {
       const LayerW& w = c->lw[l];
-      CK(cudaMemcpyAsync(c->ring, c->host + w.host_off[g], bf16_bytes(c->gN[g], c->gK[g]), cudaMemcpyHostToDevice, c->cs));
-      launch_quantize(c->ring, w.q4[g], c->gN[g], c->gK[g], c->sub_bits, c->cs);
+      const int64_t n = int64_t(c->gN[g]) * c->gK[g];
+      const uint8_t* src = c->ring;   // the target's tiled bf16 (decoded from the host store's blob)
+      if (w.zmode[g] < 0) {
+        CK(cudaMemcpyAsync(c->ring, c->host + w.host_off[g], size_t(n) * 2, cudaMemcpyHostToDevice, c->cs));
+      } else {
+        uint8_t* blob = c->ring + (size_t(n) * 2 + 4095) / 4096 * 4096;
+        CK(cudaMemcpyAsync(blob, c->host + w.host_off[g], w.host_used[g], cudaMemcpyHostToDevice, c->cs));
+        if (w.zmode[g] == 1) launch_zdecode(blob, reinterpret_cast<uint16_t*>(c->ring), n, c->cs);
+        else src = blob + w.host_a0[g];
+      }
+      launch_quantize(src, w.q4[g], c->gN[g], c->gK[g], c->sub_bits, c->cs);
       CK(cudaStreamSynchronize(c->cs));
     }
   ss_status s = check_launch(c, "quantize");
@@ -1797,7 +1887,7 @@ namespace {
 struct CoopBlob {
   uint32_t magic, version;
   int32_t pid, device;
-  uint64_t ring_off, flags_off, ring_bytes, n_items, host_bytes;
+  uint64_t ring_off, flags_off, ring_bytes, n_items, host_bytes, cycle_bytes;
   uint64_t ring_ptr, flags_ptr;
   cudaIpcMemHandle_t ipc;
 };
@@ -1828,6 +1918,7 @@ ss_status ss_coop_export(ss_ctx* c, ss_coop_handle* out) {
   b.ring_bytes = c->ring_bytes;
   b.n_items = c->cycle.size();
   b.host_bytes = c->host_bytes;
+  for (auto& lg : c->cycle) b.cycle_bytes += c->lw[lg.first].host_used[lg.second];
   b.ring_ptr = uint64_t(reinterpret_cast<uintptr_t>(c->ring));
   b.flags_ptr = uint64_t(reinterpret_cast<uintptr_t>(c->flags));
   CK(cudaIpcGetMemHandle(&b.ipc, c->ar.base));
@@ -1845,11 +1936,19 @@ ss_status ss_coop_enable(ss_ctx* c, int32_t rank, int32_t world, const ss_coop_h
   if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "coop_enable inside a step");
   if (c->next_consume % int64_t(c->cycle.size()) != 0) return fail(c, SS_ERR_STRUCTURE, "coop_enable: mid-pass");
   std::vector<CoopBlob> bl(world);
+  for (int h = 0; h < world; ++h) std::memcpy(&bl[h], &all[h], sizeof(CoopBlob));
   for (int h = 0; h < world; ++h) {
-    std::memcpy(&bl[h], &all[h], sizeof(CoopBlob));
     if (bl[h].magic != kCoopMagic || bl[h].version != 1) return fail(c, SS_ERR_INVALID, "coop_enable: bad handle");
-    if (bl[h].ring_bytes != c->ring_bytes || bl[h].n_items != c->cycle.size() || bl[h].host_bytes != c->host_bytes)
-      return fail(c, SS_ERR_INVALID, "coop_enable: ranks differ in model, placement or ring size");
+    if (bl[h].ring_bytes != c->ring_bytes || bl[h].n_items != c->cycle.size() || bl[h].host_bytes != c->host_bytes ||
+        bl[h].cycle_bytes != bl[rank].cycle_bytes) {
+      char msg[320];
+      std::snprintf(msg, sizeof msg,
+                    "coop_enable: rank %d differs in model, placement or ring (ring %llu/%llu items %llu/%zu host %llu/%zu "
+                    "cycle %llu/%llu)", h, (unsigned long long)bl[h].ring_bytes, (unsigned long long)c->ring_bytes,
+                    (unsigned long long)bl[h].n_items, c->cycle.size(), (unsigned long long)bl[h].host_bytes, c->host_bytes,
+                    (unsigned long long)bl[h].cycle_bytes, (unsigned long long)bl[rank].cycle_bytes);
+      return fail(c, SS_ERR_INVALID, msg);
+    }
   }
   if (bl[rank].ring_ptr != uint64_t(reinterpret_cast<uintptr_t>(c->ring)))
     return fail(c, SS_ERR_INVALID, "coop_enable: handle `rank` is not this context's");
@@ -1953,7 +2052,8 @@ ss_status ss_debug_read_group(ss_ctx* c, int32_t layer, int32_t group, uint16_t*
   std::vector<uint8_t> tmp;
   if (!w.resident) {
     tmp.resize(bf16_bytes(N, K));
-    std::memcpy(tmp.data(), c->host + w.host_off[group], tmp.size());
+    if (w.zmode[group] < 0) std::memcpy(tmp.data(), c->host + w.host_off[group], tmp.size());
+    else zdecode_host(c->host + w.host_off[group], reinterpret_cast<uint16_t*>(tmp.data()));   // the K7 codec's blob
   } else {
     tmp.resize(bf16_bytes(N, K));
     CK(cudaMemcpyAsync(tmp.data(), src, tmp.size(), cudaMemcpyDeviceToHost, c->cs));
@@ -1963,6 +2063,37 @@ ss_status ss_debug_read_group(ss_ctx* c, int32_t layer, int32_t group, uint16_t*
     for (int64_t k = 0; k < K; ++k)
       std::memcpy(out + n * K + k, tmp.data() + bf16_tiled_offset(n, k, K), 2);
   return SS_OK;
+}
+
+ss_status ss_debug_decode_group(ss_ctx* c, int32_t layer, int32_t group, uint16_t* out, int32_t* out_mode,
+                                uint64_t* out_stream_bytes) {
+  GUARD(c);
+  if (c->state < ST_LOADED || layer < 0 || layer >= c->L || group < 0 || group > 3 || !out || c->lw[layer].resident)
+    return fail(c, SS_ERR_INVALID, "decode_group args (an offloaded group)");
+  const LayerW& w = c->lw[layer];
+  const int N = c->gN[group], K = c->gK[group];
+  const int64_t n = int64_t(N) * K;
+  ss_status s = drain_stream(c);
+  if (s != SS_OK) return s;
+  if (c->ring && !c->inflight.empty()) return fail(c, SS_ERR_STRUCTURE, "decode_group: ring in use by streaming");
+  // the blob as streamed (H2D into the ring), decoded by the GPU kernel the verify uses
+  uint8_t* blob = c->ring + (size_t(n) * 2 + 4095) / 4096 * 4096;
+  const uint16_t* tiles = reinterpret_cast<const uint16_t*>(c->ring);
+  if (w.zmode[group] < 0) {
+    CK(cudaMemcpyAsync(c->ring, c->host + w.host_off[group], size_t(n) * 2, cudaMemcpyHostToDevice, c->cs));
+  } else {
+    CK(cudaMemcpyAsync(blob, c->host + w.host_off[group], w.host_used[group], cudaMemcpyHostToDevice, c->cs));
+    if (w.zmode[group] == 1) launch_zdecode(blob, reinterpret_cast<uint16_t*>(c->ring), n, c->cs);
+    else tiles = reinterpret_cast<const uint16_t*>(blob + w.host_a0[group]);
+  }
+  std::vector<uint8_t> tmp(size_t(n) * 2);
+  CK(cudaMemcpyAsync(tmp.data(), tiles, tmp.size(), cudaMemcpyDeviceToHost, c->cs));
+  CK(cudaStreamSynchronize(c->cs));
+  for (int64_t r = 0; r < N; ++r)
+    for (int64_t k = 0; k < K; ++k) std::memcpy(out + r * K + k, tmp.data() + bf16_tiled_offset(r, k, K), 2);
+  if (out_mode) *out_mode = w.zmode[group];
+  if (out_stream_bytes) *out_stream_bytes = w.host_used[group];
+  return check_launch(c, "decode_group");
 }
 
 ss_status ss_debug_get_substitute(ss_ctx* c, int32_t layer, int32_t group, uint8_t* codes, uint16_t* s, uint16_t* z) {

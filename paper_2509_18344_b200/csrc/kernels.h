@@ -110,6 +110,24 @@ struct GemmParams {
 void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st, int variant = 0);
 int gemm_tc_split(int N, int K, int sms);
 
+// K7 stream codec (zstream.cu): lossless exponent-coded bf16 blobs of the streamed layers
+constexpr int kZChunk = 16384;                 // weights per chunk (one bf16 tile-chunk)
+constexpr uint32_t kZMagic = 0x315A5353u;      // "SSZ1"
+struct ZTable {
+  uint8_t exp[8];                              // code -> exponent; code 7 = exception
+};
+struct ZHeader {                               // at the start of every blob (64 bytes)
+  uint32_t magic, mode, nchunks, nexc;         // mode 0: raw bf16 at a0; 1: coded
+  ZTable table;
+  uint64_t n, a0, b0, e0, used;                // weights; plane A, planes B, exceptions offsets; bytes to stream
+};
+static_assert(sizeof(ZHeader) == 64, "ZHeader");
+size_t zhdr_bytes(int64_t n);
+size_t zblob_cap(int64_t n);
+cudaError_t zencode(const uint16_t* x, int64_t n, uint8_t* blob, void* scratch, cudaStream_t st, ZHeader* out);
+void launch_zdecode(const uint8_t* blob, uint16_t* out, int64_t n, cudaStream_t st);
+void zdecode_host(const uint8_t* blob, uint16_t* out);
+
 // generator / quantizer / readback
 void launch_gen_natural(uint16_t* dst, uint64_t key, uint64_t count, float c32, int gain, cudaStream_t st,
                         uint64_t first = 0);   // elements [first, first + count) of the tensor

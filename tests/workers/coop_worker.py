@@ -15,7 +15,7 @@ from paper_2509_18344_b200.binding import SubSpec  # noqa: E402
 
 SEED = 0x5EED
 D, K, T, STEPS = 4, 6, 0.2, 6
-CAP = int(os.environ.get("COOP_CAP", str(96 << 20)))   # ring (~37 MB) below one pass (45 MB): it wraps
+CAP = int(os.environ.get("COOP_CAP", str(112 << 20)))   # ring ~39 MB ~ 1.2 coded passes: it wraps every pass
 
 
 def decode(ss, prompt, rank, world, coop):
