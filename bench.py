@@ -48,6 +48,8 @@ def args_():
                     help="request slots per GPU sharing one weight stream (SURVEY 8(f) NEXT-2); 1 = the paper's batch 1")
     ap.add_argument("--sub-bits", type=int, default=4, choices=[4, 2],
                     help="substitute code bits (4 = the paper's setting, P:278; 2 = NEXT-3, P:343)")
+    ap.add_argument("--quant", default="rtn", choices=["rtn", "hqq"],
+                    help="substitute quantizer: min/max RTN or HQQ's half-quadratic zero (NEXT-3, R28)")
     ap.add_argument("--embed-gpu", action="store_true",
                     help="embedding GPU-resident in the arena (PAPER.md:534) instead of mapped host memory (R24)")
     ap.add_argument("--no-async", action="store_true",
@@ -135,14 +137,15 @@ class OracleSample:
     too).  Every per-layer and per-vocabulary cost of a step is L x the slice's, so the step time is
     L x the measured sample step; tau is the slice model's own acceptance (measured, not borrowed)."""
 
-    def __init__(self, cfg, depth, topk, temp, bits=4):
+    def __init__(self, cfg, depth, topk, temp, bits=4, quant="rtn"):
         from oracle.decode import Session
         self.L = cfg.n_layers
         self.vs = max(128, (cfg.vocab // self.L) // 128 * 128)
         self.cfg1 = cfg.with_(name=cfg.name + "-slice", n_layers=1, vocab=self.vs)
         self.depth, self.topk, self.temp, self.bits = depth, topk, temp, bits
         t0 = time.time()
-        self.sess = Session(self.cfg1, SEED, n_resident=0, bits=bits, mode="bf16-fp32", max_nodes=max(1 + topk * depth, 256))
+        self.sess = Session(self.cfg1, SEED, n_resident=0, bits=bits, mode="bf16-fp32", max_nodes=max(1 + topk * depth, 256),
+                            quant=quant)
         self.prompt = [int(t) % self.vs for t in mtbench_prompt(SEED, 0, cfg.vocab)]
         self.root = self.sess.prefill(self.prompt)
         self.setup = time.time() - t0
@@ -171,7 +174,7 @@ def run_reference(a):
     if rank != 0:
         return
     cfg = PRESETS[a.config]
-    sample = OracleSample(cfg, a.depth, a.topk, a.temp, bits=a.sub_bits)
+    sample = OracleSample(cfg, a.depth, a.topk, a.temp, bits=a.sub_bits, quant=a.quant)
     times, toks = [], []
     for i in range(a.warmup + a.steps):
         s, n = sample.step_seconds()
@@ -208,7 +211,7 @@ def ngram_repetition(tokens, n=4):
 def workload_config(a, cfg):
     batch = "" if a.batch == 1 else f", {a.batch} requests per GPU sharing one weight stream (NEXT-2)"
     return {"workload": f"{cfg.name} SubSpec step, {a.cap_gib:g} GiB cap, n_resident={a.n_resident}, "
-                        f"{a.sub_bits}-bit g64 substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt{batch}",
+                        f"{a.sub_bits}-bit g64 {a.quant.upper()} substitutes, D={a.depth} k={a.topk} T={a.temp}, MT-Bench-shaped prompt{batch}",
             "model_shape": cfg.name, "vram_cap_gib": a.cap_gib, "n_resident": a.n_resident, "depth": a.depth,
             "top_k": a.topk, "sharpen_t": a.temp, "batch": a.batch, "max_context": cfg.max_context,
             "l2": "inputs larger than L2 (>= 4.76 GB of draft weights per draft pass; 13 GB streamed per verify)",
@@ -324,7 +327,7 @@ def run_ours(a):
     if a.sub_bits != 4:
         ss.set_substitute_bits(a.sub_bits)
     shm = load_weights_for_job(ss, dist, local, a.n_resident)
-    ss.build_substitutes(a.sub_bits, 64)
+    ss.build_substitutes(a.sub_bits, 64, method=a.quant)
     if Bq == 1:
         ss.prefill(request_for_rank(rank, cfg.vocab))
         step = lambda: [ss.step(D, k, T)]                     # noqa: E731
@@ -555,7 +558,7 @@ def run_ours(a):
     }
     if rank == 0:
         if world == 1 and not a.no_cpu_baseline:
-            sample = OracleSample(cfg, D, k, T, bits=a.sub_bits)
+            sample = OracleSample(cfg, D, k, T, bits=a.sub_bits, quant=a.quant)
             ts, ns = [], []
             for _ in range(2):
                 s_, n_ = sample.step_seconds()

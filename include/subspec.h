@@ -109,8 +109,14 @@ typedef struct {
 } ss_options;
 void ss_default_options(ss_options* out);
 
-/* Substitute quantization: bits = 4, group_size = 64 are supported. */
-typedef struct { int32_t bits, group_size; } ss_quant_spec;
+/* Substitute quantization ("quantized to 4 bits with a group size 64 using HQQ"):
+ * bits = 4 (or 2, see ss_set_substitute_bits), group_size = 64.  method: SS_QUANT_RTN (0, min/max
+ * round-to-nearest, SPEC.md:125 — HQQ's initialisation, reading R1) or SS_QUANT_HQQ (1, the same scale
+ * with HQQ's half-quadratic zero refinement: l_0.7 objective, beta0 = 10, kappa = 1.01, per 64-group
+ * early stop keeping the zero of the lowest mean |x - x_hat|, fp64; reading R28 in DESIGN.md,
+ * oracle/quant.py).  hqq_iters: maximum iterations (0 = 20, HQQ's default); ignored for RTN. */
+enum { SS_QUANT_RTN = 0, SS_QUANT_HQQ = 1 };
+typedef struct { int32_t bits, group_size, method, hqq_iters; } ss_quant_spec;
 
 /* Draft tree parameters: depth D, top-k, sharpening temperature. */
 typedef struct { int32_t depth, top_k; float sharpen_t; } ss_draft_params;
@@ -200,7 +206,8 @@ ss_status ss_load_weights_synthetic_shared(ss_ctx* ctx, uint64_t seed, int32_t n
                                            size_t host_bytes, int32_t fill);
 
 /* Build the 4-bit (or, after ss_set_substitute_bits(2), 2-bit) group-64 substitute of every offloaded layer: stream it host->device through
- * the staging ring and quantize on the device (K1).  Norms/biases are shared. */
+ * the staging ring and quantize on the device (K1) with q->method.  Norms/biases are
+ * shared.  Errors: INVALID (bits/group/method/hqq_iters), STRUCTURE (before load), CUDA. */
 ss_status ss_build_substitutes(ss_ctx* ctx, const ss_quant_spec* q);
 
 /* Start a new session (committed length 0) and prefill `prompt` (n tokens, host) through the

@@ -27,7 +27,7 @@ class Session:
 
     def __init__(self, cfg: ModelConfig, seed: int, n_resident: int = 0, bits: int = 4,
                  group: int = 64, mode: str = "exact", max_nodes: int | None = None,
-                 target: TargetWeights | None = None, dlayers=None):
+                 target: TargetWeights | None = None, dlayers=None, quant: str = "rtn"):
         """mode: "exact" (fp64), "bf16" (fp64 + the GPU's bf16 rounding points) or "bf16-fp32" (the
         rounding points with fp32 weights and node-batched fp32 matrix products: full-width shapes)."""
         self.cfg, self.mode = cfg, mode
@@ -35,7 +35,7 @@ class Session:
         self.target = target if target is not None else TargetWeights(cfg, seed, dtype=wdt)
         self.tlayers = self.target.layers
         # dlayers: a draft view built once and shared by several sessions (batched requests)
-        self.dlayers = dlayers if dlayers is not None else draft_layers(self.target, n_resident, bits, group)
+        self.dlayers = dlayers if dlayers is not None else draft_layers(self.target, n_resident, bits, group, method=quant)
         self.kv = KVCache(cfg, max_nodes or 512)
         self.n_forward_nodes = 0
 

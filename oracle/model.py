@@ -81,7 +81,7 @@ class TargetWeights:
                 setattr(self, name, gen(tid, shape, kind, sigma))
 
 
-def draft_layers(target: TargetWeights, n_resident: int, bits=4, group=64, block_rows=2048):
+def draft_layers(target: TargetWeights, n_resident: int, bits=4, group=64, block_rows=2048, method="rtn"):
     """Draft model view (SPEC.md:214-222 build_draft_view):
     layers [0, n_resident) are Shared (the target's own dict); the rest are
     Substitute: every linear matrix replaced by its dequantized low-bit copy,
@@ -99,7 +99,7 @@ def draft_layers(target: TargetWeights, n_resident: int, bits=4, group=64, block
                 q = np.empty(w.shape, dtype=dt)
 
                 def block(r0, w=w, q=q):   # groups lie inside rows: row blocks are independent
-                    blk = substitute_matrix(np.asarray(w[r0:r0 + block_rows], dtype=np.float64), bits, group)
+                    blk = substitute_matrix(np.asarray(w[r0:r0 + block_rows], dtype=np.float64), bits, group, method)
                     q[r0:r0 + block_rows] = blk
                     if dt != np.float64:   # code*s + z must be exact in the storage type
                         assert np.array_equal(q[r0:r0 + block_rows].astype(np.float64), blk), "substitute not exact in fp32"

@@ -49,7 +49,10 @@ class LimitsC(ctypes.Structure):
 
 
 class QuantSpecC(ctypes.Structure):
-    _fields_ = [("bits", c_int32), ("group_size", c_int32)]
+    _fields_ = [("bits", c_int32), ("group_size", c_int32), ("method", c_int32), ("hqq_iters", c_int32)]
+
+
+QUANT_METHODS = {"rtn": 0, "hqq": 1}
 
 
 class DraftParamsC(ctypes.Structure):
@@ -254,8 +257,9 @@ class SubSpec:
         self._check(self.lib.ss_load_weights_synthetic_shared(self.ctx, c_uint64(seed), n_resident,
                                                                c_void_p(store_addr), store_bytes, 1 if fill else 0))
 
-    def build_substitutes(self, bits=4, group=64):
-        self._check(self.lib.ss_build_substitutes(self.ctx, ctypes.byref(QuantSpecC(bits, group))))
+    def build_substitutes(self, bits=4, group=64, method="rtn", hqq_iters=0):
+        m = QUANT_METHODS[method] if isinstance(method, str) else int(method)
+        self._check(self.lib.ss_build_substitutes(self.ctx, ctypes.byref(QuantSpecC(bits, group, m, hqq_iters))))
 
     def prefill(self, prompt, chunk=256):
         p = np.ascontiguousarray(prompt, dtype=np.int32)

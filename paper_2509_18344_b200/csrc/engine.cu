@@ -1517,6 +1517,9 @@ ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
   GUARD(c);
   if (!q || (q->bits != 4 && q->bits != 2) || q->group_size != 64)
     return fail(c, SS_ERR_INVALID, "substitutes are 4- or 2-bit with group 64");
+  if ((q->method != SS_QUANT_RTN && q->method != SS_QUANT_HQQ) || q->hqq_iters < 0 || q->hqq_iters > 1000)
+    return fail(c, SS_ERR_INVALID, "quantizer method is SS_QUANT_RTN or SS_QUANT_HQQ, hqq_iters in [0, 1000]");
+  const int hqq_iters = q->method == SS_QUANT_HQQ ? (q->hqq_iters ? q->hqq_iters : 20) : 0;
   if (q->bits != c->sub_bits)
     return fail(c, SS_ERR_INVALID, "quant bits differ from the layout sized at load (ss_set_substitute_bits)");
   if (c->state != ST_LOADED) return fail(c, SS_ERR_STRUCTURE, "build_substitutes before load_weights");
@@ -1533,7 +1536,7 @@ ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
         if (w.zmode[g] == 1) launch_zdecode(blob, reinterpret_cast<uint16_t*>(c->ring), n, c->cs);
         else src = blob + w.host_a0[g];
       }
-      launch_quantize(src, w.q4[g], c->gN[g], c->gK[g], c->sub_bits, c->cs);
+      launch_quantize(src, w.q4[g], c->gN[g], c->gK[g], c->sub_bits, hqq_iters, c->cs);
       CK(cudaStreamSynchronize(c->cs));
     }
   ss_status s = check_launch(c, "quantize");

@@ -87,12 +87,57 @@ void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float
 // ---------------------------------------------------------------------------
 // K1: RTN min/max group-64 quantizer, bf16 tiled -> Q4 (or Q2) tiled (layouts in
 // common.cuh).  One thread per (row, 64-group) of a tile-chunk (256 threads per chunk):
-//   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / (2^BITS - 1)) ; z = m
+//   s = (M == m) ? 1 : RNE_bf16(fp32(M - m) / (2^BITS - 1)) ; z = m   (HQQ: z = RNE_bf16(refined zero))
 //   code = clamp(rint_even(fp32(x - z) / s), 0, 2^BITS - 1)       (IEEE div.rn; built without fast-math)
 // ---------------------------------------------------------------------------
+// HQQ zero refinement (reading R28; oracle/quant.py hqq_refine_zero): the
+// min/max scale is kept, the zero is refined by half-quadratic splitting of min_z ||x - W_r(z)||_0.7,
+//   code = clamp(rint((x - z)/s)), e = x - (code*s + z), err = mean|e|  (stop once err stops falling,
+//   keep the zero of the lowest err), W_e = sign(e)*max(|e| - |e|^(p-1)/beta, 0),
+//   z <- mean(x - W_e - code*s), beta *= kappa,
+// in fp64 with index-order sums, per 64-group (one thread).  Explicit _rn intrinsics: no contraction
+// (code*s is exact, so a contracted form would round identically, but the sums must not reassociate).
+constexpr double kHqqP = 0.7, kHqqBeta0 = 10.0, kHqqKappa = 1.01;
+template <int BITS>
+SS_DEV double hqq_refine_zero(const float (&x)[64], double s, double z0, int iters) {
+  const double qmax = double((1 << BITS) - 1), pm1 = kHqqP - 1.0;
+  double z = z0, best_z = z0, best_err = __longlong_as_double(0x7FF0000000000000ll), beta = kHqqBeta0;
+  for (int it = 0; it < iters; ++it) {
+    double err = 0.0;
+    for (int i = 0; i < 64; ++i) {
+      const double c = fmin(fmax(rint(__ddiv_rn(__dsub_rn(double(x[i]), z), s)), 0.0), qmax);
+      err = __dadd_rn(err, fabs(__dsub_rn(double(x[i]), __dadd_rn(__dmul_rn(c, s), z))));
+    }
+    err = __dmul_rn(err, 1.0 / 64.0);
+    if (!(err < best_err)) break;
+    best_err = err;
+    best_z = z;
+    double acc = 0.0;
+    for (int i = 0; i < 64; ++i) {
+      const double xi = double(x[i]);
+      const double c = fmin(fmax(rint(__ddiv_rn(__dsub_rn(xi, z), s)), 0.0), qmax);
+      const double cs = __dmul_rn(c, s);
+      const double e = __dsub_rn(xi, __dadd_rn(cs, z));
+      const double a = fabs(e);
+      const double t = __dsub_rn(a, __ddiv_rn(pow(a, pm1), beta));
+      const double we = t > 0.0 ? copysign(t, e) : 0.0;
+      acc = __dadd_rn(acc, __dsub_rn(__dsub_rn(xi, we), cs));
+    }
+    z = __dmul_rn(acc, 1.0 / 64.0);
+    beta = __dmul_rn(beta, kHqqKappa);
+  }
+  return best_z;
+}
+// fp64 -> bf16 bits, round to nearest even, in one step (normal range)
+SS_DEV uint16_t f64_to_bf16_rne(double v) {
+  const unsigned long long u = __double_as_longlong(v);
+  const unsigned long long r = (u + ((1ull << 44) - 1) + ((u >> 45) & 1ull)) & ~((1ull << 45) - 1);
+  return f2bf(float(__longlong_as_double(r)));   // exact: r has 8 significant bits
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                                                         int64_t n_tc) {
+                                                         int64_t n_tc, int hqq_iters) {
   constexpr float kLevels = float((1 << BITS) - 1);
   constexpr int kTile = BITS == 2 ? kQ2TileBytes : kQ4TileBytes, kCode = BITS == 2 ? kQ2CodeBytes : kQ4CodeBytes;
   const int row = threadIdx.x & 127, G = threadIdx.x >> 7;
@@ -117,7 +162,8 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restri
       mx = fmaxf(mx, x[i]);
     }
     const float sc = (mx == mn) ? 1.0f : __uint_as_float(uint32_t(f2bf(__fdiv_rn(__fsub_rn(mx, mn), kLevels))) << 16);
-    const float z = mn;
+    float z = mn;
+    if (hqq_iters > 0) z = __uint_as_float(uint32_t(f64_to_bf16_rne(hqq_refine_zero<BITS>(x, sc, mn, hqq_iters))) << 16);
     // codes in A-fragment order (common.cuh): lane t4 of this row's 8-row group takes the k with
     // (k % 16) / 2 % 4 == t4; word h of lane t4 holds k-steps 2h, 2h+1
     const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
@@ -147,13 +193,14 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restri
   }
 }
 
-void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, cudaStream_t st) {
+void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, int hqq_iters,
+                     cudaStream_t st) {
   int64_t n_tc = (N / 128) * (K / 128);
   int blocks = int(n_tc < 148 * 8 ? n_tc : 148 * 8);
   if (bits == 2)
-    quantize_q_kernel<2><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc);
+    quantize_q_kernel<2><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc, hqq_iters);
   else
-    quantize_q_kernel<4><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc);
+    quantize_q_kernel<4><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc, hqq_iters);
 }
 
 // ---- debug readbacks --------------------------------------------------------

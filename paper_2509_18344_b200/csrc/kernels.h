@@ -135,7 +135,8 @@ void launch_gen_tiled(uint8_t* dst, uint64_t key, int64_t rows, int64_t K, float
                       cudaStream_t st);
 void launch_tile_from_natural(uint8_t* dst, const uint16_t* src, int64_t rows, int64_t K, int map, int64_t row_off,
                               cudaStream_t st);
-void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, cudaStream_t st);
+void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, int64_t K, int bits, int hqq_iters,
+                     cudaStream_t st);
 void launch_q4_to_canonical(const uint8_t* q4, uint8_t* codes, uint16_t* s, uint16_t* z, int64_t N, int64_t K,
                             cudaStream_t st);
 void launch_tiled_to_natural(const uint8_t* t, uint16_t* out, int64_t N, int64_t K, cudaStream_t st);

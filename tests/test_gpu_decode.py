@@ -27,11 +27,11 @@ pytestmark = pytest.mark.gpu
 SEED = 0x5EED
 
 
-def _gpu(cfg, n_resident, D, k, cap=512 << 20, max_chunk=256):
+def _gpu(cfg, n_resident, D, k, cap=512 << 20, max_chunk=256, quant="rtn"):
     from paper_2509_18344_b200.binding import SubSpec
     ss = SubSpec(cfg, cap, max_depth=D, max_top_k=k, max_chunk=max_chunk)
     ss.load_synthetic(SEED, n_resident=n_resident)
-    ss.build_substitutes(4, 64)
+    ss.build_substitutes(4, 64, method=quant)
     return ss
 
 
@@ -56,12 +56,13 @@ def _check_selection(tree_tok, tree_par, tree_score, gpu_logits, D, k, T):
     return flags
 
 
-@pytest.mark.parametrize("cfg,n_res,D,k", [(TINY, 1, 4, 6), (SMALL, 1, 4, 6), (SMALL, 0, 3, 4)],
-                         ids=["tiny-D4k6", "small-D4k6", "small-allsub-D3k4"])
-def test_lockstep(cuda_required, cfg, n_res, D, k):
+@pytest.mark.parametrize("cfg,n_res,D,k,quant", [(TINY, 1, 4, 6, "rtn"), (SMALL, 1, 4, 6, "rtn"),
+                                                 (SMALL, 0, 3, 4, "rtn"), (SMALL, 0, 4, 6, "hqq")],
+                         ids=["tiny-D4k6", "small-D4k6", "small-allsub-D3k4", "small-allsub-hqq-D4k6"])
+def test_lockstep(cuda_required, cfg, n_res, D, k, quant):
     T = 0.2
-    ss = _gpu(cfg, n_res, D, k)
-    ors = Session(cfg, SEED, n_resident=n_res, mode="bf16", max_nodes=max(256, 1 + k * D))
+    ss = _gpu(cfg, n_res, D, k, quant=quant)
+    ors = Session(cfg, SEED, n_resident=n_res, mode="bf16", max_nodes=max(256, 1 + k * D), quant=quant)
     prompt = mtbench_prompt(SEED, 1, cfg.vocab, 40)
     first = ss.prefill(prompt)
     o_first = ors.prefill(prompt)

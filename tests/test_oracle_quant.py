@@ -121,3 +121,90 @@ def test_fewer_bits_more_error():
     e2 = np.abs(substitute_matrix(x, 2) - x).mean()
     e4 = np.abs(substitute_matrix(x, 4) - x).mean()
     assert e2 > 3 * e4
+
+
+# ---- HQQ refinement (NEXT-3, reading R28) ----------------------------------------------------
+from oracle.quant import hqq_shrink, hqq_step, hqq_refine_zero, HQQ_P
+
+
+def test_hqq_shrink_p1_is_soft_threshold_prox():
+    # p = 1: W_e must be the proximal point argmin_w 1/2 (w - e)^2 + |w| / beta, found by brute force
+    beta = 10.0
+    grid = np.linspace(-1.0, 1.0, 400001)
+    for e in [-0.7, -0.1, -0.05, 0.0, 0.03, 0.1, 0.2, 0.55]:
+        obj = 0.5 * (grid - e) ** 2 + np.abs(grid) / beta
+        w_bf = grid[np.argmin(obj)]
+        assert abs(hqq_shrink(np.array([e]), beta, p=1.0)[0] - w_bf) <= 1e-5
+
+
+def test_hqq_shrink_p07_threshold_and_shrinkage():
+    # |e| - |e|^(p-1)/beta <= 0  <=>  |e| <= beta^(-1/(2-p)): zero inside, sign-preserving shrink outside
+    beta = 10.0
+    thr = beta ** (-1.0 / (2.0 - HQQ_P))
+    e = np.array([-thr * 1.001, -thr * 0.999, thr * 0.999, thr * 1.001, 3 * thr, -5 * thr])
+    we = hqq_shrink(e, beta)
+    assert we[1] == 0 and we[2] == 0
+    assert we[0] < 0 < we[3] and np.all(np.abs(we) <= np.abs(e))
+    assert np.all(np.sign(we[[0, 3, 4, 5]]) == np.sign(e[[0, 3, 4, 5]]))
+
+
+def test_hqq_zero_update_minimises_the_quadratic():
+    # z_next = argmin_z sum (x - W_e - code*s - z)^2 for the step's own code and W_e (scipy minimiser)
+    from scipy.optimize import minimize_scalar
+    x = _bf16_random((3, 64), 0.02, 11)
+    codes, s, z = quantize(x)
+    for g in range(3):
+        _, zn, code, we = hqq_step(x[g:g + 1], s[g:g + 1, 0], z[g:g + 1, 0], 10.0)
+        f = lambda t: float(np.sum((x[g] - we[0] - code[0] * s[g, 0] - t) ** 2))
+        r = minimize_scalar(f, bracket=(z[g, 0] - 0.01, z[g, 0] + 0.01), tol=1e-14)
+        assert abs(zn[0] - r.x) <= 1e-9 * max(1.0, abs(r.x))
+        # err is the mean absolute reconstruction error of the CURRENT zero, via the dequantiser
+        err, _, _, _ = hqq_step(x[g:g + 1], s[g:g + 1, 0], z[g:g + 1, 0], 10.0)
+        assert np.isclose(err[0], np.mean(np.abs(dequantize(codes[g:g + 1], s[g:g + 1], z[g:g + 1]) - x[g])),
+                          rtol=1e-12)
+
+
+def test_hqq_on_grid_group_is_fixed_point():
+    # x exactly on z + c*s with c spanning 0..15: RTN is exact, HQQ keeps z and the codes
+    rng = np.random.default_rng(5)
+    c = rng.integers(0, 16, size=(4, 64))
+    c[:, 0], c[:, 1] = 0, 15
+    s, z = 0.00390625, -0.03125
+    x = c * s + z
+    for bits in (4,):
+        cr, sr, zr = quantize(x, bits, 64, "rtn")
+        ch, sh, zh = quantize(x, bits, 64, "hqq")
+        assert np.array_equal(cr, ch) and np.array_equal(zr, zh) and np.array_equal(sr, sh)
+        assert np.array_equal(dequantize(ch, sh, zh), x)
+
+
+def test_hqq_constant_group_and_iters_limits():
+    x = np.full((2, 64), 0.25)
+    assert np.array_equal(quantize(x, 4, 64, "hqq")[2], quantize(x, 4, 64, "rtn")[2])
+    y = _bf16_random((8, 256), 0.03, 12)
+    # one iteration only evaluates the RTN zero: identical to RTN
+    for a, b in zip(quantize(y, 4, 64, "hqq", hqq_iters=1), quantize(y, 4, 64, "rtn")):
+        assert np.array_equal(a, b)
+
+
+def test_hqq_error_trace_and_improvement():
+    # the kept zero has the lowest mean |x - W_r| of the visited iterates (<= RTN's), and over many
+    # Gaussian groups HQQ lowers the reconstruction error vs RTN in l1 and in HQQ's own l_0.7 (the
+    # method's published purpose)
+    x = _bf16_random((256, 1024), 0.02, 13)
+    codes, s, z = quantize(x)
+    xg = x.reshape(256, 16, 64)
+    zb, errs = hqq_refine_zero(xg, s, z, trace=True)
+    E = np.stack(errs)
+    first = E[0]
+    assert np.allclose(first, np.mean(np.abs(dequantize(codes, s, z) - x).reshape(256, 16, 64), axis=2), rtol=1e-12)
+    assert len(errs) > 2
+    best = np.min(E, axis=0)
+    assert np.all(best <= first)
+    assert np.mean(best < first) > 0.5                        # most groups improve
+    ch, sh, zh = quantize(x, 4, 64, "hqq")
+    assert np.array_equal(sh, s)                               # HQQ keeps the scale
+    r, h = dequantize(codes, s, z) - x, dequantize(ch, sh, zh) - x
+    assert np.mean(np.abs(h)) < 0.98 * np.mean(np.abs(r))
+    assert np.mean(np.abs(h) ** HQQ_P) < 0.99 * np.mean(np.abs(r) ** HQQ_P)
+    assert codes.max() <= 15 and ch.max() <= 15
