@@ -46,7 +46,7 @@ def args_():
     ap.add_argument("--temp", type=float, default=0.2)
     ap.add_argument("--batch", type=int, default=1,
                     help="request slots per GPU sharing one weight stream (SURVEY 8(f) NEXT-2); 1 = the paper's batch 1")
-    ap.add_argument("--sub-bits", type=int, default=4, choices=[4, 2],
+    ap.add_argument("--sub-bits", type=int, default=4, choices=[4, 3, 2],
                     help="substitute code bits (4 = the paper's setting, P:278; 2 = NEXT-3, P:343)")
     ap.add_argument("--quant", default="rtn", choices=["rtn", "hqq"],
                     help="substitute quantizer: min/max RTN or HQQ's half-quadratic zero (NEXT-3, R28)")

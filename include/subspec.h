@@ -110,7 +110,7 @@ typedef struct {
 void ss_default_options(ss_options* out);
 
 /* Substitute quantization ("quantized to 4 bits with a group size 64 using HQQ"):
- * bits = 4 (or 2, see ss_set_substitute_bits), group_size = 64.  method: SS_QUANT_RTN (0, min/max
+ * bits = 4 (or 3 / 2, see ss_set_substitute_bits), group_size = 64.  method: SS_QUANT_RTN (0, min/max
  * round-to-nearest, SPEC.md:125 — HQQ's initialisation, reading R1) or SS_QUANT_HQQ (1, the same scale
  * with HQQ's half-quadratic zero refinement: l_0.7 objective, beta0 = 10, kappa = 1.01, per 64-group
  * early stop keeping the zero of the lowest mean |x - x_hat|, fp64; reading R28 in DESIGN.md,
@@ -183,11 +183,11 @@ ss_status ss_load_weights(ss_ctx* ctx, const ss_host_weights* w, int32_t n_resid
 ss_status ss_load_weights_synthetic(ss_ctx* ctx, uint64_t seed, int32_t n_resident);
 
 /* Code width of the substitutes this context will build: 4 (default; "4 bits with a
- * group size 64") or 2 (the paper's "more aggressive ... 2-bit" direction,
- * PAPER.md:343; same min/max RTN rule with 2^bits - 1 levels).  Fixes the substitutes' layout and
- * footprint (2-bit: 0.3125 B/weight vs 0.5625), so it is only valid before loading weights; the
- * arena bytes it frees go to the streaming ring.  ss_build_substitutes must then pass the same bits.
- * Errors: STRUCTURE (after load), INVALID (bits not 2 or 4). */
+ * group size 64"), 3 or 2 (the paper's "more aggressive" 2/3-bit direction,
+ * PAPER.md:343; the same quantizer with 2^bits - 1 levels).  Fixes the substitutes' layout and
+ * footprint (3-bit: 0.4375 B/weight, 2-bit: 0.3125, vs 0.5625), so it is only valid before loading
+ * weights; the arena bytes it frees go to the streaming ring.  ss_build_substitutes must then pass
+ * the same bits.  Errors: STRUCTURE (after load), INVALID (bits not 2, 3 or 4). */
 ss_status ss_set_substitute_bits(ss_ctx* ctx, int32_t bits);
 
 /* Bytes of the offloaded layers' host store for an explicit n_resident >= 0 (bf16, device layout).
@@ -205,7 +205,7 @@ ss_status ss_host_store_bytes(ss_ctx* ctx, int32_t n_resident, size_t* out_bytes
 ss_status ss_load_weights_synthetic_shared(ss_ctx* ctx, uint64_t seed, int32_t n_resident, void* host_store,
                                            size_t host_bytes, int32_t fill);
 
-/* Build the 4-bit (or, after ss_set_substitute_bits(2), 2-bit) group-64 substitute of every offloaded layer: stream it host->device through
+/* Build the 4-bit (or, after ss_set_substitute_bits(3 / 2), 3- / 2-bit) group-64 substitute of every offloaded layer: stream it host->device through
  * the staging ring and quantize on the device (K1) with q->method.  Norms/biases are
  * shared.  Errors: INVALID (bits/group/method/hqq_iters), STRUCTURE (before load), CUDA. */
 ss_status ss_build_substitutes(ss_ctx* ctx, const ss_quant_spec* q);

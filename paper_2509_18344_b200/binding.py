@@ -204,7 +204,7 @@ class SubSpec:
 
     # ---- the method ---------------------------------------------------------------------
     def set_substitute_bits(self, bits):
-        """Substitute code width (4 or 2); before load_weights (sizes the substitutes' layout)."""
+        """Substitute code width (4, 3 or 2); before load_weights (sizes the substitutes' layout)."""
         self._check(self.lib.ss_set_substitute_bits(self.ctx, bits))
 
     def load_weights(self, weights, n_resident=0):

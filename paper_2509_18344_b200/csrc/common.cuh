@@ -63,8 +63,15 @@ SS_HD uint64_t q4_meta_offset(int64_t n, int64_t k, int64_t K) {     // bytes; 4
 // is a pair; meta as Q4 at kQ2CodeBytes + G * 512 + row * 4.
 constexpr int kQ2CodeBytes = 4096;  // 128 x 128 x 2 bit
 constexpr int kQ2TileBytes = kQ2CodeBytes + kQ4MetaBytes;   // 5120
-SS_HD int qtile_bytes(int bits) { return bits == 2 ? kQ2TileBytes : kQ4TileBytes; }
-SS_HD int qcode_bytes(int bits) { return bits == 2 ? kQ2CodeBytes : kQ4CodeBytes; }
+// Q3 (NEXT-3, 3-bit substitutes): the low two bits of every code in the Q2 layout
+// (4096 B), then a plane of the high bits: per (w, G, lane) one 32-bit word at 4096 +
+// ((w * 2 + G) * 32 + lane) * 4 whose bit d * 16 + h * 8 + p is the high bit of pair p's code d of
+// row g + 8h, so (word >> (8h + p - 2)) & 0x00040004 (a left shift for 8h + p < 2) puts the pair's
+// high bits at bf16 mantissa bit 2; meta as Q4 at kQ3CodeBytes + G * 512 + row * 4.
+constexpr int kQ3CodeBytes = 6144;  // 128 x 128 x 3 bit
+constexpr int kQ3TileBytes = kQ3CodeBytes + kQ4MetaBytes;   // 7168
+SS_HD int qtile_bytes(int bits) { return bits == 2 ? kQ2TileBytes : (bits == 3 ? kQ3TileBytes : kQ4TileBytes); }
+SS_HD int qcode_bytes(int bits) { return bits == 2 ? kQ2CodeBytes : (bits == 3 ? kQ3CodeBytes : kQ4CodeBytes); }
 SS_HD void q2_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int* shift) {
   const int row = int(n & 127), kk = int(k & 127);
   const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
@@ -77,6 +84,25 @@ SS_HD void q2_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* byte_off, int*
 }
 SS_HD uint64_t q2_meta_offset(int64_t n, int64_t k, int64_t K) {
   return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ2TileBytes + kQ2CodeBytes +
+         uint64_t(((k & 127) >> 6) * 512 + (n & 127) * 4);
+}
+// Q3: low two bits at (*lo_off, *lo_shift) (the Q2 position inside the Q3 tile), high bit at
+// (*hi_off, *hi_bit)
+SS_HD void q3_code_pos(int64_t n, int64_t k, int64_t K, uint64_t* lo_off, int* lo_shift, uint64_t* hi_off,
+                       int* hi_bit) {
+  const int row = int(n & 127), kk = int(k & 127);
+  const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
+  const int G = kk >> 6, kl = kk & 63, k4 = kl >> 4, r16 = kl & 15;
+  const int t4 = (r16 & 7) >> 1, e = r16 >> 3, d = r16 & 1;
+  const int lane = g * 4 + t4, p = 2 * k4 + e, bit = d * 16 + 2 * p, hb = d * 16 + h * 8 + p;
+  const uint64_t base = uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ3TileBytes;
+  *lo_off = base + uint64_t(((w * 2 + G) * 32 + lane) * 8 + h * 4 + (bit >> 3));
+  *lo_shift = bit & 7;
+  *hi_off = base + kQ2CodeBytes + uint64_t(((w * 2 + G) * 32 + lane) * 4 + (hb >> 3));
+  *hi_bit = hb & 7;
+}
+SS_HD uint64_t q3_meta_offset(int64_t n, int64_t k, int64_t K) {
+  return uint64_t((n >> 7) * (K >> 7) + (k >> 7)) * kQ3TileBytes + kQ3CodeBytes +
          uint64_t(((k & 127) >> 6) * 512 + (n & 127) * 4);
 }
 
@@ -115,7 +141,11 @@ SS_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
+#if SS_MBAR_NOHINT
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+#endif
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(done)
       : "r"(addr), "r"(parity)
@@ -137,6 +167,11 @@ SS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 SS_DEV uint32_t lop3_and_or(uint32_t x, uint32_t magic) {
   uint32_t d;
   asm("lop3.b32 %0, %1, 0x000F000F, %2, 0xEA;" : "=r"(d) : "r"(x), "r"(magic));
+  return d;
+}
+SS_DEV uint32_t lop3_and_or_hi(uint32_t x, uint32_t pair) {   // 3-bit codes: (x & 0x00040004) | pair
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 0x00040004, %2, 0xEA;" : "=r"(d) : "r"(x), "r"(pair));
   return d;
 }
 SS_DEV uint32_t lop3_and_or2(uint32_t x, uint32_t magic) {   // 2-bit codes: (x & 0x00030003) | magic

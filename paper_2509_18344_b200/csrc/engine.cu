@@ -12,6 +12,7 @@
 #include <vector>
 #include <unistd.h>
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys/ncu timelines (no link dependency)
 
 #include "subspec.h"
 #include "common.cuh"
@@ -935,6 +936,23 @@ bool valid_cfg(const ss_model_config* m, const ss_limits* l) {
   return true;
 }
 
+// NVTX range over one phase of the step (host side; nsys shows the kernels it enqueues beneath it)
+struct NvtxRange {
+  explicit NvtxRange(const char* name, uint32_t argb) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.colorType = NVTX_COLOR_ARGB;
+    a.color = argb;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxRangePushEx(&a);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 #define GUARD(c)                                                                 \
   do {                                                                           \
     if (!(c)) return SS_ERR_INVALID;                                             \
@@ -1326,7 +1344,7 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
 ss_status ss_set_substitute_bits(ss_ctx* c, int32_t bits) {
   GUARD(c);
   if (c->state != ST_CREATED) return fail(c, SS_ERR_STRUCTURE, "set_substitute_bits: only before load_weights");
-  if (bits != 4 && bits != 2) return fail(c, SS_ERR_INVALID, "set_substitute_bits: 4 or 2");
+  if (bits != 4 && bits != 3 && bits != 2) return fail(c, SS_ERR_INVALID, "set_substitute_bits: 4, 3 or 2");
   c->sub_bits = bits;
   return SS_OK;
 }
@@ -1514,9 +1532,10 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
 }
 
 ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
+  NvtxRange nvtx_range("ss.build_substitutes", 0xFFF39C12u);
   GUARD(c);
-  if (!q || (q->bits != 4 && q->bits != 2) || q->group_size != 64)
-    return fail(c, SS_ERR_INVALID, "substitutes are 4- or 2-bit with group 64");
+  if (!q || (q->bits != 4 && q->bits != 3 && q->bits != 2) || q->group_size != 64)
+    return fail(c, SS_ERR_INVALID, "substitutes are 4-, 3- or 2-bit with group 64");
   if ((q->method != SS_QUANT_RTN && q->method != SS_QUANT_HQQ) || q->hqq_iters < 0 || q->hqq_iters > 1000)
     return fail(c, SS_ERR_INVALID, "quantizer method is SS_QUANT_RTN or SS_QUANT_HQQ, hqq_iters in [0, 1000]");
   const int hqq_iters = q->method == SS_QUANT_HQQ ? (q->hqq_iters ? q->hqq_iters : 20) : 0;
@@ -1549,6 +1568,7 @@ ss_status ss_build_substitutes(ss_ctx* c, const ss_quant_spec* q) {
 
 static ss_status prefill_slot_impl(ss_ctx* c, int slot, const int32_t* prompt, int32_t n, int32_t chunk,
                                    int32_t* out_first) {
+  NvtxRange nvtx_range("ss.prefill", 0xFF8E44ADu);
   if (c->state < ST_READY) return fail(c, SS_ERR_STRUCTURE, "prefill before build_substitutes");
   if (c->state == ST_DRAFTED || c->state == ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "prefill inside a step");
   if (slot < 0 || slot >= c->B) return fail(c, SS_ERR_INVALID, "prefill: slot outside the active batch");
@@ -1618,6 +1638,7 @@ ss_status ss_set_batch(ss_ctx* c, int32_t n_req) {
 }
 
 static ss_status draft_impl(ss_ctx* c, int32_t root_token, const ss_draft_params* p) {
+  NvtxRange nvtx_range("ss.draft_tree", 0xFF2E86C1u);
   if (!p || p->top_k < 1 || p->top_k > c->lim.max_top_k || p->depth < 0 || p->depth > c->lim.max_depth ||
       !(p->sharpen_t > 0.f) || !std::isfinite(p->sharpen_t))
     return fail(c, SS_ERR_INVALID, "draft params");
@@ -1677,6 +1698,7 @@ ss_status ss_draft_tree(ss_ctx* c, int32_t root_token, const ss_draft_params* p,
 }
 
 static ss_status verify_impl(ss_ctx* c) {
+  NvtxRange nvtx_range("ss.verify_tree", 0xFFC0392Bu);
   if (c->state != ST_DRAFTED) return fail(c, SS_ERR_STRUCTURE, "verify_tree before draft_tree");
   ss_status s = do_verify(c);
   if (s != SS_OK) return s;
@@ -1698,6 +1720,7 @@ ss_status ss_verify_tree(ss_ctx* c, int32_t* opt_argmax, float* opt_gap) {
 
 // out_tokens/opt_path: [B][stride] (stride >= D_eff + 1), out_n: [B]
 static ss_status accept_impl(ss_ctx* c, int32_t* out_tokens, int32_t* out_n, int32_t* opt_path, int stride) {
+  NvtxRange nvtx_range("ss.accept_and_commit", 0xFF27AE60u);
   if (c->state != ST_VERIFIED) return fail(c, SS_ERR_STRUCTURE, "accept before verify");
   ss_status s = do_accept(c, false);
   if (s != SS_OK) return s;
@@ -2104,7 +2127,7 @@ ss_status ss_debug_get_substitute(ss_ctx* c, int32_t layer, int32_t group, uint8
   if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || c->lw[layer].resident)
     return fail(c, SS_ERR_INVALID, "get_substitute: not an offloaded layer (or substitutes not built)");
   const int N = c->gN[group], K = c->gK[group];
-  const bool q2 = c->sub_bits == 2;
+  const bool q2 = c->sub_bits == 2, q3 = c->sub_bits == 3;
   std::vector<uint8_t> q(sub_bytes(N, K, c->sub_bits));
   CK(cudaMemcpyAsync(q.data(), c->lw[layer].q4[group], q.size(), cudaMemcpyDeviceToHost, c->cs));
   CK(cudaStreamSynchronize(c->cs));
@@ -2112,12 +2135,19 @@ ss_status ss_debug_get_substitute(ss_ctx* c, int32_t layer, int32_t group, uint8
     for (int64_t k = 0; k < K; ++k) {
       uint64_t off;
       int sh;
-      if (q2) q2_code_pos(n, k, K, &off, &sh);
-      else q4_code_pos(n, k, K, &off, &sh);
-      if (codes) codes[n * K + k] = (q[off] >> sh) & (q2 ? 3 : 15);
+      if (q3) {
+        uint64_t hoff;
+        int hbit;
+        q3_code_pos(n, k, K, &off, &sh, &hoff, &hbit);
+        if (codes) codes[n * K + k] = uint8_t(((q[off] >> sh) & 3) | (((q[hoff] >> hbit) & 1) << 2));
+      } else {
+        if (q2) q2_code_pos(n, k, K, &off, &sh);
+        else q4_code_pos(n, k, K, &off, &sh);
+        if (codes) codes[n * K + k] = (q[off] >> sh) & (q2 ? 3 : 15);
+      }
       if ((k & 63) == 0) {
         uint32_t m;
-        std::memcpy(&m, q.data() + (q2 ? q2_meta_offset(n, k, K) : q4_meta_offset(n, k, K)), 4);
+        std::memcpy(&m, q.data() + (q2 ? q2_meta_offset(n, k, K) : (q3 ? q3_meta_offset(n, k, K) : q4_meta_offset(n, k, K))), 4);
         if (s) s[n * (K / 64) + k / 64] = uint16_t(m & 0xFFFF);
         if (z) z[n * (K / 64) + k / 64] = uint16_t(m >> 16);
       }

@@ -30,20 +30,29 @@ __global__ void __launch_bounds__(256) rmsnorm_f32_kernel(const int* tokens, int
   for (int i = threadIdx.x; i < H; i += 256) h[int64_t(m) * H + i] = xr[i] * r * bf2f(gain[i]);
 }
 
-// ---- K2f / K6f: Y[M x N] = X[M x K] * W^T, W tiled bf16 (fmt 0) or a 4-/2-bit substitute (fmt 4 / 2:
+// ---- K2f / K6f: Y[M x N] = X[M x K] * W^T, W tiled bf16 (fmt 0) or a 4-/3-/2-bit substitute (fmt 4 / 3 / 2:
 // W_hat = code * s + z, exact in fp32).  Block: 128 output columns x 8 rows; X tiles staged in smem.
 __device__ __forceinline__ float wval(const uint8_t* W, int fmt, int64_t n, int64_t k, int64_t K) {
   if (fmt == 0) return bf2f(*reinterpret_cast<const uint16_t*>(W + bf16_tiled_offset(n, k, K)));
   uint64_t off, moff;
   int sh;
-  if (fmt == 2) {
-    q2_code_pos(n, k, K, &off, &sh);
-    moff = q2_meta_offset(n, k, K);
+  uint32_t code;
+  if (fmt == 3) {
+    uint64_t hoff;
+    int hbit;
+    q3_code_pos(n, k, K, &off, &sh, &hoff, &hbit);
+    moff = q3_meta_offset(n, k, K);
+    code = ((W[off] >> sh) & 3u) | (((W[hoff] >> hbit) & 1u) << 2);
   } else {
-    q4_code_pos(n, k, K, &off, &sh);
-    moff = q4_meta_offset(n, k, K);
+    if (fmt == 2) {
+      q2_code_pos(n, k, K, &off, &sh);
+      moff = q2_meta_offset(n, k, K);
+    } else {
+      q4_code_pos(n, k, K, &off, &sh);
+      moff = q4_meta_offset(n, k, K);
+    }
+    code = (W[off] >> sh) & (fmt == 2 ? 3u : 15u);
   }
-  const uint32_t code = (W[off] >> sh) & (fmt == 2 ? 3u : 15u);
   const uint32_t m = *reinterpret_cast<const uint32_t*>(W + moff);
   return fmaf(float(code), __uint_as_float(m << 16), __uint_as_float(m & 0xFFFF0000u));   // exact
 }

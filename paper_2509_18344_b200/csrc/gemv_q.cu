@@ -44,18 +44,21 @@ namespace ss {
 #ifndef SS_K2_RING_KB
 #define SS_K2_RING_KB 88      // ring budget per CTA (Q4; Q2 uses 72)
 #endif
+#ifndef SS_K2_CPS
+#define SS_K2_CPS 2           // tile-chunks per ring stage
+#endif
 #ifndef SS_K2_UMULHI
 #define SS_K2_UMULHI 0        // 1: shifts by 8/12 as IMAD.HI (fma pipe) instead of SHF (alu pipe)
 #endif
 constexpr int kGemvQConsumerWarps = 8;
 constexpr int kGemvQThreads = (kGemvQConsumerWarps + 1) * 32;
 
-// NT: token groups of the activation layout; QB: code bits (4 or 2); NTC: token groups the MMAs read
+// NT: token groups of the activation layout; QB: code bits (4, 3 or 2); NTC: token groups the MMAs read
 template <int NT, int QB, int NTC>
 struct GemvQCfg {
-  static constexpr int kCPS = 2;                                  // tile-chunks per pipeline stage
-  static constexpr int kWBytes = QB == 2 ? kQ2TileBytes : kQ4TileBytes;
-  static constexpr int kCodeBytes = QB == 2 ? kQ2CodeBytes : kQ4CodeBytes;
+  static constexpr int kCPS = SS_K2_CPS;                          // tile-chunks per pipeline stage
+  static constexpr int kWBytes = QB == 2 ? kQ2TileBytes : (QB == 3 ? kQ3TileBytes : kQ4TileBytes);
+  static constexpr int kCodeBytes = QB == 2 ? kQ2CodeBytes : (QB == 3 ? kQ3CodeBytes : kQ4CodeBytes);
   static constexpr int kXGroups = SS_K2_XTRIM ? NTC : NT;         // token groups staged per chunk
   static constexpr int kXBytes = kXGroups * kXChunkBytesPerNT;
   static constexpr int kSBytes = 2 * NT * 8 * 4;                  // group sums of x: [2 groups][Mpad] fp32
@@ -87,9 +90,11 @@ SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int w
 #pragma unroll
     for (int G = 0; G < 2; ++G) {
       uint4 cw;
-      if constexpr (QB == 2) {   // [row g word][row g+8 word]
+      uint32_t hw = 0u;          // Q3: the lane's high-bit word
+      if constexpr (QB == 2 || QB == 3) {   // [row g word][row g+8 word]
         const uint2 c2 = *reinterpret_cast<const uint2*>(wst + ((warp * 2 + G) * 32 + lane) * 8);
         cw = make_uint4(c2.x, 0u, c2.y, 0u);
+        if constexpr (QB == 3) hw = *reinterpret_cast<const uint32_t*>(wst + kQ2CodeBytes + ((warp * 2 + G) * 32 + lane) * 4);
       } else {                   // [row g: word0, word1][row g+8: word0, word1]
         cw = *reinterpret_cast<const uint4*>(wst + ((warp * 2 + G) * 32 + lane) * 16);
       }
@@ -109,11 +114,18 @@ SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int w
 #pragma unroll
       for (int k4 = 0; k4 < 4; ++k4) {
         uint32_t a0, a1, a2, a3;
-        if constexpr (QB == 2) {   // pairs 2 k4 (a0/a1) and 2 k4 + 1 (a2/a3) at bit 2p
+        if constexpr (QB == 2 || QB == 3) {   // pairs 2 k4 (a0/a1) and 2 k4 + 1 (a2/a3) at bit 2p
           a0 = lop3_and_or2(cw.x >> (4 * k4), kMagic);
           a1 = lop3_and_or2(cw.z >> (4 * k4), kMagic);
           a2 = lop3_and_or2(cw.x >> (4 * k4 + 2), kMagic);
           a3 = lop3_and_or2(cw.z >> (4 * k4 + 2), kMagic);
+          if constexpr (QB == 3) {   // high bits of pair p of row g + 8h: (hw >> (8h + p - 2)) & 0x00040004
+            auto hb = [&](int sh) { return sh >= 0 ? hw >> sh : hw << (-sh); };
+            a0 = lop3_and_or_hi(hb(2 * k4 - 2), a0);
+            a1 = lop3_and_or_hi(hb(8 + 2 * k4 - 2), a1);
+            a2 = lop3_and_or_hi(hb(2 * k4 - 1), a2);
+            a3 = lop3_and_or_hi(hb(8 + 2 * k4 - 1), a3);
+          }
         } else {
           const uint32_t wg = (k4 < 2) ? cw.x : cw.y, wg8 = (k4 < 2) ? cw.z : cw.w;
           const int pp = 2 * (k4 & 1);
@@ -465,7 +477,8 @@ static int ensure_attrs_q() {
   if (it != stages_of.end()) return it->second;
   // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
   // down to ~68 KB of whole stages)
-  const int budget = SS_K2_MINB == 2 ? (QB == 2 ? 72 : SS_K2_RING_KB) * 1024 : (220 * 1024) / SS_K2_MINB - C::smem_for(0);
+  const int budget = SS_K2_MINB == 2 ? (QB == 2 ? 72 : (QB == 3 ? 80 : SS_K2_RING_KB)) * 1024
+                                    : (220 * 1024) / SS_K2_MINB - C::smem_for(0);
   int st = budget / C::kStageBytes;
   if (st < 2) st = 2;
   if (st > C::kMaxStages) st = C::kMaxStages;
@@ -532,6 +545,7 @@ static ClusterPlanQ cluster_plan_q(int N, int K, int sms, int hint = 0) {
 bool gemv_q_tiles_all_resident(int NT, int N, int K, int sms, int bits) {
   if (N / 128 > 2 * sms) return false;
   if (bits == 2) return NT <= 2 ? cluster_plan_q<2, 1, 2>(N, K, sms).all_resident : cluster_plan_q<4, 4, 2>(N, K, sms).all_resident;
+  if (bits == 3) return NT <= 2 ? cluster_plan_q<2, 1, 3>(N, K, sms).all_resident : cluster_plan_q<4, 4, 3>(N, K, sms).all_resident;
   return NT <= 2 ? cluster_plan_q<2, 1, 4>(N, K, sms).all_resident : cluster_plan_q<4, 4, 4>(N, K, sms).all_resident;
 }
 
@@ -582,6 +596,9 @@ void launch_gemv_q(const GemvParams& p, int sms, bool pdl, cudaStream_t st) {
   if (p.qbits == 2) {
     if (p.NT <= 2) ntc == 1 ? launch_mode_q<2, 1, 2>(p, sms, pdl, st) : launch_mode_q<2, 2, 2>(p, sms, pdl, st);
     else launch_mode_q<4, 4, 2>(p, sms, pdl, st);
+  } else if (p.qbits == 3) {
+    if (p.NT <= 2) ntc == 1 ? launch_mode_q<2, 1, 3>(p, sms, pdl, st) : launch_mode_q<2, 2, 3>(p, sms, pdl, st);
+    else launch_mode_q<4, 4, 3>(p, sms, pdl, st);
   } else {
     if (p.NT <= 2) ntc == 1 ? launch_mode_q<2, 1, 4>(p, sms, pdl, st) : launch_mode_q<2, 2, 4>(p, sms, pdl, st);
     else launch_mode_q<4, 4, 4>(p, sms, pdl, st);

@@ -139,7 +139,8 @@ template <int BITS>
 __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                                          int64_t n_tc, int hqq_iters) {
   constexpr float kLevels = float((1 << BITS) - 1);
-  constexpr int kTile = BITS == 2 ? kQ2TileBytes : kQ4TileBytes, kCode = BITS == 2 ? kQ2CodeBytes : kQ4CodeBytes;
+  constexpr int kTile = BITS == 2 ? kQ2TileBytes : (BITS == 3 ? kQ3TileBytes : kQ4TileBytes);
+  constexpr int kCode = BITS == 2 ? kQ2CodeBytes : (BITS == 3 ? kQ3CodeBytes : kQ4CodeBytes);
   const int row = threadIdx.x & 127, G = threadIdx.x >> 7;
   for (int64_t tc = blockIdx.x; tc < n_tc; tc += gridDim.x) {
     const uint8_t* s_tile = src + tc * kBF16TileBytes;
@@ -168,8 +169,9 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restri
     // (k % 16) / 2 % 4 == t4; word h of lane t4 holds k-steps 2h, 2h+1
     const int w = row >> 4, h = (row & 15) >> 3, g = row & 7;
     uint32_t words[4][2];
+    uint32_t hib[4][2];   // Q3 high-bit bytes of this row: [t4][d]
 #pragma unroll
-    for (int t = 0; t < 4; ++t) words[t][0] = words[t][1] = 0u;
+    for (int t = 0; t < 4; ++t) words[t][0] = words[t][1] = hib[t][0] = hib[t][1] = 0u;
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       const float t = __fdiv_rn(__fsub_rn(x[i], z), sc);
@@ -177,6 +179,9 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restri
       const int k4 = i >> 4, r16 = i & 15, t4 = (r16 & 7) >> 1, e = r16 >> 3, d = r16 & 1;
       if constexpr (BITS == 2) {
         words[t4][0] |= r << (d * 16 + 2 * (2 * k4 + e));
+      } else if constexpr (BITS == 3) {
+        words[t4][0] |= (r & 3u) << (d * 16 + 2 * (2 * k4 + e));
+        hib[t4][d] |= (r >> 2) << (2 * k4 + e);
       } else {
         words[t4][k4 >> 1] |= r << (d * 16 + 4 * (2 * (k4 & 1) + e));
       }
@@ -184,10 +189,15 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(const uint8_t* __restri
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int lane = g * 4 + t;
-      if constexpr (BITS == 2)
+      if constexpr (BITS == 2 || BITS == 3)
         *reinterpret_cast<uint32_t*>(d_tile + ((w * 2 + G) * 32 + lane) * 8 + h * 4) = words[t][0];
       else
         *reinterpret_cast<uint2*>(d_tile + ((w * 2 + G) * 32 + lane) * 16 + h * 8) = make_uint2(words[t][0], words[t][1]);
+      if constexpr (BITS == 3) {   // this row owns bytes h (d = 0) and 2 + h (d = 1) of the lane's high word
+        uint8_t* hw = d_tile + kQ2CodeBytes + ((w * 2 + G) * 32 + lane) * 4;
+        hw[h] = uint8_t(hib[t][0]);
+        hw[2 + h] = uint8_t(hib[t][1]);
+      }
     }
     *reinterpret_cast<uint32_t*>(d_tile + kCode + G * 512 + row * 4) = uint32_t(f2bf(sc)) | (uint32_t(f2bf(z)) << 16);
   }
@@ -199,6 +209,8 @@ void launch_quantize(const uint8_t* src_bf16_tiled, uint8_t* dst_q, int64_t N, i
   int blocks = int(n_tc < 148 * 8 ? n_tc : 148 * 8);
   if (bits == 2)
     quantize_q_kernel<2><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc, hqq_iters);
+  else if (bits == 3)
+    quantize_q_kernel<3><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc, hqq_iters);
   else
     quantize_q_kernel<4><<<blocks, 256, 0, st>>>(src_bf16_tiled, dst_q, n_tc, hqq_iters);
 }

@@ -114,13 +114,36 @@ def test_error_bound_2bit():
     assert codes.max() == 3 and codes.min() == 0
 
 
+def test_ramp_3bit_closed_form():
+    # NEXT-3 3-bit: ramp 0..63, s = 63/7 = 9 exactly, z = 0; x/9 never lands on a .5
+    # tie for integer x, so code = (2x + 9) // 18 and the largest error is 4 (x = 4: code 0)
+    x = np.arange(64, dtype=np.float64)[None, :]
+    codes, s, z = quantize(x, 3, 64)
+    assert s[0, 0] == 9.0 and z[0, 0] == 0.0
+    want = (2 * np.arange(64) + 9) // 18
+    assert codes[0].tolist() == want.tolist() and codes.max() == 7
+    xh = dequantize(codes, s, z)
+    assert np.array_equal(xh[0], 9.0 * want) and np.abs(xh - x).max() == 4.0
+
+
+def test_error_bound_3bit():
+    x = _bf16_random((64, 512), 0.05, 17)
+    codes, s, z = quantize(x, 3)
+    xh = dequantize(codes, s, z)
+    S = np.repeat(s, 64, axis=1)
+    top = np.repeat(z + 7 * s, 64, axis=1)
+    assert np.all((np.abs(xh - x) <= S / 2 * (1 + 2**-20)) | ((codes == 7) & (x >= top)))
+    assert codes.max() == 7 and codes.min() == 0
+
+
 def test_fewer_bits_more_error():
     # SPEC.md "monotone fidelity": mean abs error non-increasing in bits (2 -> 4 roughly / 5 here:
     # the step shrinks from range/3 to range/15)
     x = _bf16_random((32, 256), 0.05, 15)
     e2 = np.abs(substitute_matrix(x, 2) - x).mean()
+    e3 = np.abs(substitute_matrix(x, 3) - x).mean()
     e4 = np.abs(substitute_matrix(x, 4) - x).mean()
-    assert e2 > 3 * e4
+    assert e2 > 3 * e4 and e2 > 1.5 * e3 > 1.5 * 1.5 * e4
 
 
 # ---- HQQ refinement (NEXT-3, reading R28) ----------------------------------------------------
