@@ -109,6 +109,7 @@ _FUNCS = {
     "ss_debug_set_knob": [c_void_p, c_int32, c_int32],
     "ss_debug_trace_pass": [c_void_p, c_int32, c_void_p, c_int32, P(c_int32)],
     "ss_debug_cta_trace": [c_void_p, c_int32, c_int32, c_void_p, c_int32, P(c_int32)],
+    "ss_debug_step_timeline": [c_void_p, P(DraftParamsC), c_void_p, c_int32, P(c_int32), c_void_p],
 }
 EXPORTED = list(_FUNCS) + ["ss_last_error", "ss_destroy", "ss_default_options"]
 
@@ -471,6 +472,15 @@ class SubSpec:
         n = c_int32()
         self._check(self.lib.ss_debug_trace_pass(self.ctx, M, _ptr(out), cap, ctypes.byref(n)))
         return out[: n.value * 16].reshape(n.value, 16)
+
+    def debug_step_timeline(self, depth, top_k, sharpen_t, cap=1024):
+        """One step with events around each streamed group: (rows [n, 8], phases [3]); see subspec.h."""
+        out = np.zeros(cap * 8, np.float64)
+        ph = np.zeros(3, np.float64)
+        n = c_int32()
+        self._check(self.lib.ss_debug_step_timeline(self.ctx, ctypes.byref(DraftParamsC(depth, top_k, sharpen_t)),
+                                                    _ptr(out), cap, ctypes.byref(n), _ptr(ph)))
+        return out[:n.value * 8].reshape(-1, 8), ph
 
     def debug_cta_trace(self, M, launch, cap=1024):
         out = np.zeros(cap * 5, np.int64)

@@ -141,11 +141,7 @@ SS_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-#if SS_MBAR_NOHINT
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-#else
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
-#endif
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(done)
       : "r"(addr), "r"(parity)

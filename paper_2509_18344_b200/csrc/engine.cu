@@ -1,6 +1,7 @@
 // libsubspec engine: context, capped arena, placement, pinned host store, K7 layer streaming,
 // draft loop (CUDA graph + PDL), verification, acceptance, and the C-ABI (include/subspec.h).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -123,6 +124,7 @@ struct ss_ctx {
   size_t gv_part_floats = 0;
   // attention scratch
   float* at_o = nullptr;        // debug output scratch (ss_debug_matmul / ss_debug_time_matmul)
+  void* dbg_mem = nullptr;      // at_o (+ logits outside fp32 mode): debug-only, outside the arena
   size_t at_o_floats = 0;
   // topk scratch
   float *tk_max = nullptr, *tk_sum = nullptr, *tk_val = nullptr;
@@ -139,6 +141,10 @@ struct ss_ctx {
   size_t ring_bytes = 0, ring_head = 0;
   std::deque<StreamItem> inflight;
   int64_t next_issue = 0, next_consume = 0;
+  // ss_debug_step_timeline: extra timing events per streamed item while on (seq -> copy start/end on
+  // the copy stream, compute start (after the copy wait) / end (ring release) on the compute stream)
+  bool tl_on = false;
+  std::map<int64_t, std::array<cudaEvent_t, 4>> tl_ev;
   std::vector<std::pair<int, int>> cycle;
   std::vector<cudaEvent_t> ev_copied, ev_consumed, ev_t0, ev_t1;
   std::vector<bool> ev_pending;
@@ -158,7 +164,9 @@ struct ss_ctx {
   int k2_self_pf = 0;         // K2: L2-prefetch each CTA's own weight range (ss_debug_set_knob 0; measured slower)
   int k6_variant = 0;         // K6 kernel variant (ss_debug_set_knob 2; launch_gemm; A/B only)
   bool zcomp = false;         // ss_options.compress_stream (bf16 mode): the host store holds coded blobs
-  uint16_t* dbuf = nullptr;   // decoded bf16 of the group being verified (one group; K6 reads it)
+  uint16_t* dbuf = nullptr;   // decoded bf16 row tiles of the group being verified (K6 reads them)
+  size_t dbuf_bytes = 0;      // decode buffer: >= one row tile of every group; a group decodes and
+                              // runs K6 in row blocks of <= dbuf_bytes (the rest of the cap feeds the ring)
   // NEXT-1 cooperative streaming (ss_coop_*): rank r of `coop_world` copies slice r of every streamed
   // group from its host store and pushes it into every peer's ring at the same offset; flags[h] =
   // "rank h's slice of item seq landed here" (= seq + 1), flags[kCoopMax + h] = "rank h consumed
@@ -267,6 +275,17 @@ bool load_driver_fns() {
   } while (0)
 static size_t coop_slice_lo(size_t B, int h, int G) { return h >= G ? B : (B * size_t(h) / size_t(G)) & ~size_t(4095); }
 
+static void tl_record(ss_ctx* c, int64_t seq, int k, cudaStream_t st) {
+  auto it = c->tl_ev.find(seq);
+  if (it == c->tl_ev.end()) it = c->tl_ev.emplace(seq, std::array<cudaEvent_t, 4>{}).first;
+  if (!it->second[k] && cudaEventCreate(&it->second[k]) != cudaSuccess) {
+    cudaGetLastError();
+    it->second[k] = nullptr;
+    return;
+  }
+  cudaEventRecord(it->second[k], st);
+}
+
 ss_status pump(ss_ctx* c) {
   if (c->cycle.empty()) return SS_OK;
   const int n_items = int(c->cycle.size());
@@ -309,6 +328,7 @@ ss_status pump(ss_ctx* c) {
     if (c->serial_stream && c->last_consumed_ev >= 0) CK(cudaStreamWaitEvent(c->xs, c->ev_consumed[c->last_consumed_ev], 0));
     for (size_t k = dead.size(); k-- > 0;) c->inflight.erase(c->inflight.begin() + dead[k]);
     CK(cudaEventRecord(c->ev_t0[ev], c->xs));
+    if (c->tl_on) tl_record(c, seq, 0, c->xs);
     if (c->coop_world > 1) {
       // NEXT-1: the items that occupied [off, off + B) before must have been consumed by every peer
       int64_t need = 0;
@@ -341,6 +361,7 @@ ss_status pump(ss_ctx* c) {
       c->st.stream_raw_bytes += double(bf16_bytes(c->gN[g], c->gK[g]));
     }
     CK(cudaEventRecord(c->ev_t1[ev], c->xs));
+    if (c->tl_on) tl_record(c, seq, 1, c->xs);
     CK(cudaEventRecord(c->ev_copied[ev], c->xs));
     c->ev_pending[ev] = true;
     c->timing_queue.push_back(ev);
@@ -380,11 +401,13 @@ ss_status consume_begin(ss_ctx* c, int l, int g, const uint8_t** w, int* ev_out)
           CKD(g_wait32((CUstream)c->cs, (CUdeviceptr)(c->flags + h), cuuint32_t(seq + 1), CU_STREAM_WAIT_VALUE_GEQ));
       *w = c->ring + it.off;
       *ev_out = it.ev;
+      if (c->tl_on) tl_record(c, seq, 2, c->cs);
       return SS_OK;
     }
   return fail(c, SS_ERR_BUDGET, "staging ring cannot hold the next layer group");
 }
 ss_status consume_end(ss_ctx* c, int ev) {
+  if (c->tl_on) tl_record(c, c->next_consume, 3, c->cs);
   CK(cudaEventRecord(c->ev_consumed[ev], c->cs));
   for (int h = 0; h < c->coop_world && c->coop_world > 1; ++h)   // tell every peer: item consumed here
     if (h != c->coop_rank)
@@ -482,15 +505,29 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
   ss_status s = consume_begin(c, l, g, &wp, &ev);
   if (s != SS_OK) return s;
   if (w.zmode[g] == 1) {
-    // K7 codec: decode the streamed blob into the group's bf16 tiles, release the ring region, then K6
-    launch_zdecode(wp, c->dbuf, int64_t(N) * K, c->cs);
-    c->launches++;
-    if ((s = check_launch(c, "zdecode")) != SS_OK) return s;
-    if ((s = consume_end(c, ev)) != SS_OK) return s;
-    p.W = reinterpret_cast<const uint8_t*>(c->dbuf);
-    launch_gemm(p, false, c->cs, c->k6_variant);
-    c->launches++;
-    return check_launch(c, "gemm");
+    // K7 codec: decode the streamed blob into bf16 row tiles and run K6 on them, in row blocks of at
+    // most dbuf_bytes (a row block is a contiguous chunk range of the blob); the ring region is released
+    // after the last block's decode.  Every block keeps the whole matrix's K-split plan (split_n), so
+    // the products are bitwise those of one launch over the matrix.
+    const int nC = K / 128, tiles = N / 128;
+    const int per_max = std::max<int>(1, int(c->dbuf_bytes / (size_t(nC) * kBF16TileBytes)));
+    const int parts = (tiles + per_max - 1) / per_max, per = (tiles + parts - 1) / parts;
+    for (int t0 = 0; t0 < tiles; t0 += per) {
+      const int nt = std::min(per, tiles - t0);
+      launch_zdecode_range(wp, c->dbuf, t0 * nC, nt * nC, c->cs);
+      c->launches++;
+      if ((s = check_launch(c, "zdecode")) != SS_OK) return s;
+      if (t0 + nt == tiles && (s = consume_end(c, ev)) != SS_OK) return s;
+      GemmParams q = p;
+      q.W = reinterpret_cast<const uint8_t*>(c->dbuf);
+      q.N = nt * 128;
+      q.tile0 = t0;
+      q.split_n = N;
+      launch_gemm(q, false, c->cs, c->k6_variant);
+      c->launches++;
+      if ((s = check_launch(c, "gemm")) != SS_OK) return s;
+    }
+    return SS_OK;
   }
   p.W = wp + w.host_a0[g];
   launch_gemm(p, false, c->cs, c->k6_variant);   // follows a cross-stream event wait: plain serialisation
@@ -1105,7 +1142,10 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
   c->hxs = (float*)chk(A(size_t(c->mpad_max) * (fx_cols / 64) * 4));
   c->attnxs = (float*)chk(A(size_t(c->mpad_max) * (c->qd / 64) * 4));
   c->actxs = (float*)chk(A(size_t(c->mpad_max) * (c->F / 64) * 4));
-  c->logits = (float*)chk(A(size_t(32) * c->V * 4));
+  // draft logits [32 x V]: written only by the fp32 parity mode and the debug entry points (the bf16
+  // draft keeps per-tile top-k statistics instead); outside fp32 mode they live in a debug buffer
+  // allocated on first debug use, outside the VRAM cap
+  if (c->f32) c->logits = (float*)chk(A(size_t(32) * c->V * 4));
   c->tracebuf = (unsigned long long*)chk(A(size_t(512) * kTraceEvents * 8));
   c->sumsq = (float*)chk(A(size_t(c->H / 128) * 32 * 4));
   c->norm_ctr = (unsigned long long*)chk(A(256));   // 24 monotonic counters (3 x 2 formats x NT 1..4), zeroed below
@@ -1128,7 +1168,7 @@ ss_status ss_create(const ss_model_config* cfg, const ss_limits* lim, const ss_o
     // matrix group, or 32 rows of logits
     const size_t mpad_one = size_t(std::max(32, ((c->max_nodes + 127) / 128) * 128));
     c->at_o_floats = std::max(mpad_one * std::max({c->gN[0], c->gN[1], c->gN[2], c->gN[3]}), size_t(32) * c->V);
-    c->at_o = (float*)chk(A(c->at_o_floats * 4));
+    // allocated on first debug use (ensure_debug_bufs), outside the VRAM cap: not a product buffer
   }
   {   // top-k statistics: [32 rows][blocks] of the two-stage kernels (296) or of the head's vocab tiles
     const size_t nb = std::max<size_t>(296, size_t(c->V / 128));
@@ -1399,14 +1439,19 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
   c->seed = seed;
   const size_t layer_bf16 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += bf16_bytes(c->gN[g], c->gK[g]); return s; }();
   const size_t layer_q4 = [&] { size_t s = 0; for (int g = 0; g < 4; ++g) s += sub_bytes(c->gN[g], c->gK[g], c->sub_bits); return s; }();
-  size_t max_group = 0;
-  for (int g = 0; g < 4; ++g) max_group = std::max(max_group, bf16_bytes(c->gN[g], c->gK[g]));
+  size_t max_group = 0, max_tile_row = 0;
+  for (int g = 0; g < 4; ++g) {
+    max_group = std::max(max_group, bf16_bytes(c->gN[g], c->gK[g]));
+    max_tile_row = std::max(max_tile_row, size_t(c->gK[g] / 128) * kBF16TileBytes);
+  }
+  // K7 codec decode buffer: 64 MiB (the small groups fit whole; gate_up / down decode in row blocks)
+  c->dbuf_bytes = std::min(max_group, std::max(size_t(64) << 20, max_tile_row));
   const size_t avail = c->ar.cap - c->ar.used - 4096 * 8;
   auto need = [&](int nr) {
     const int off = c->L - nr;
     // offloaded layers: a ring of >= two groups (+ codec scratch) and, with the codec, the decode buffer
     return size_t(nr) * layer_bf16 + size_t(off) * layer_q4 +
-           (off > 0 ? 2 * max_group + (c->zcomp ? max_group + (8u << 20) : 0) : max_group);
+           (off > 0 ? 2 * max_group + (c->zcomp ? c->dbuf_bytes + (8u << 20) : 0) : max_group);
   };
   int nr = n_resident;
   if (nr < 0) {
@@ -1427,7 +1472,7 @@ static ss_status load_impl(ss_ctx* c, const ss_host_weights* hw, uint64_t seed, 
     }
   }
   if (c->zcomp && nr < c->L) {
-    c->dbuf = (uint16_t*)c->ar.alloc(max_group, 4096);
+    c->dbuf = (uint16_t*)c->ar.alloc(c->dbuf_bytes, 4096);
     if (!c->dbuf) return fail(c, SS_ERR_BUDGET, "no room for the stream decode buffer");
   }
   // the staging ring takes what is left
@@ -1891,6 +1936,7 @@ void ss_destroy(ss_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  if (c->dbg_mem) cudaFree(c->dbg_mem);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   for (auto e : c->ev_copied) cudaEventDestroy(e);
   for (auto e : c->ev_consumed) cudaEventDestroy(e);
@@ -2155,8 +2201,25 @@ ss_status ss_debug_get_substitute(ss_ctx* c, int32_t layer, int32_t group, uint8
   return SS_OK;
 }
 
+// debug scratch (ss_debug_* only): allocated once, outside the arena, so the product path's VRAM cap
+// holds no test-only buffer
+static ss_status ensure_debug_bufs(ss_ctx* c) {
+  if (c->dbg_mem) return SS_OK;
+  const size_t lg = c->logits ? 0 : size_t(32) * c->V * 4;
+  const size_t ao = (c->at_o_floats * 4 + 255) / 256 * 256;
+  if (cudaMalloc(&c->dbg_mem, ao + lg) != cudaSuccess) {
+    cudaGetLastError();
+    c->dbg_mem = nullptr;
+    return fail(c, SS_ERR_BUDGET, "debug scratch: device allocation failed");
+  }
+  c->at_o = reinterpret_cast<float*>(c->dbg_mem);
+  if (!c->logits) c->logits = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(c->dbg_mem) + ao);
+  return SS_OK;
+}
+
 ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group, const uint16_t* x, int32_t M, float* y) {
   GUARD(c);
+  if (ensure_debug_bufs(c) != SS_OK) return SS_ERR_BUDGET;
   if (c->state < ST_READY || layer < 0 || layer >= c->L || group < 0 || group > 3 || !x || !y || M < 1)
     return fail(c, SS_ERR_INVALID, "debug_matmul args");
   if (which == 0 && M > 32) return fail(c, SS_ERR_INVALID, "draft GEMV: M <= 32");
@@ -2225,6 +2288,7 @@ ss_status ss_debug_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group
 ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
                                float* out_ms) {
   GUARD(c);
+  if (ensure_debug_bufs(c) != SS_OK) return SS_ERR_BUDGET;
   // layer >= 0: that layer only; layer == -1: every layer in turn (weights stream from HBM, not L2).
   // group 0..3: that matrix group; -1: the bf16 head; -2: the four groups of each layer in pass order.
   // which 0: the draft GEMV (K2 / bf16 head), M <= 32; which 1: the target GEMM (K6) on resident
@@ -2321,6 +2385,7 @@ ss_status ss_debug_set_knob(ss_ctx* c, int32_t knob, int32_t value) {
 
 ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, float* out_ms) {
   GUARD(c);
+  if (ensure_debug_bufs(c) != SS_OK) return SS_ERR_BUDGET;
   if (c->state != ST_SESSION || M < 1 || M > std::min(32, c->max_nodes - 1) || iters < 1 || !out_ms)
     return fail(c, SS_ERR_INVALID, "time_pass args");
   // draft forward of M frontier nodes (slots 1..M, children of the root), repeated; tree metadata
@@ -2361,6 +2426,7 @@ ss_status ss_debug_time_pass(ss_ctx* c, int32_t M, int32_t iters, int32_t skip, 
 
 ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, int32_t* out_n) {
   GUARD(c);
+  if (ensure_debug_bufs(c) != SS_OK) return SS_ERR_BUDGET;
   if (c->state != ST_SESSION || !out || cap < 1 || !out_n) return fail(c, SS_ERR_INVALID, "trace_pass args");
   // run one draft pass with %globaltimer events recorded in every dequant-GEMV launch
   float ms = 0.f;
@@ -2391,8 +2457,73 @@ ss_status ss_debug_trace_pass(ss_ctx* c, int32_t M, int64_t* out, int32_t cap, i
   return SS_OK;
 }
 
+ss_status ss_debug_step_timeline(ss_ctx* c, const ss_draft_params* dp, double* out, int32_t cap, int32_t* out_n,
+                                 double* out_phases) {
+  GUARD(c);
+  if (!dp || !out || cap < 1 || !out_n || !out_phases) return fail(c, SS_ERR_INVALID, "step_timeline args");
+  if (c->state != ST_SESSION || c->B != 1) return fail(c, SS_ERR_STRUCTURE, "step_timeline: one-request session");
+  cudaEvent_t ev0, ev_d, ev_v, ev_a;
+  for (cudaEvent_t* e : {&ev0, &ev_d, &ev_v, &ev_a}) CK(cudaEventCreate(e));
+  for (auto& kv : c->tl_ev)
+    for (cudaEvent_t e : kv.second)
+      if (e) cudaEventDestroy(e);
+  c->tl_ev.clear();
+  const int64_t seq0 = c->next_consume;
+  c->tl_on = true;
+  CK(cudaEventRecord(ev0, c->cs));
+  ss_status s = draft_impl(c, -1, dp);
+  if (s == SS_OK) {
+    CK(cudaEventRecord(ev_d, c->cs));
+    s = verify_impl(c);
+  }
+  if (s == SS_OK) {
+    CK(cudaEventRecord(ev_v, c->cs));
+    int32_t toks[1024], n = 0;
+    s = accept_impl(c, toks, &n, nullptr, c->cur_deff + 1);
+  }
+  c->tl_on = false;
+  if (s != SS_OK) return s;
+  CK(cudaEventRecord(ev_a, c->cs));
+  CK(cudaDeviceSynchronize());
+  auto ms = [&](cudaEvent_t e) {
+    float t = 0.f;
+    if (!e || cudaEventElapsedTime(&t, ev0, e) != cudaSuccess) {
+      cudaGetLastError();
+      return -1e9;
+    }
+    return double(t);
+  };
+  out_phases[0] = ms(ev_d);
+  out_phases[1] = ms(ev_v);
+  out_phases[2] = ms(ev_a);
+  // rows: seq - seq0, layer, group, bytes, copy start, copy end, compute start, ring release (ms from the
+  // step start; copies of this verify's first groups were issued during the previous step: negative)
+  int k = 0;
+  const int n_items = int(c->cycle.size());
+  for (auto& kv : c->tl_ev) {
+    if (k >= cap) break;
+    const int64_t seq = kv.first;
+    const auto lg = c->cycle[size_t(seq % n_items)];
+    double* r = out + size_t(k) * 8;
+    r[0] = double(seq - seq0);
+    r[1] = lg.first;
+    r[2] = lg.second;
+    r[3] = double(c->lw[lg.first].host_used[lg.second]);
+    for (int j = 0; j < 4; ++j) r[4 + j] = kv.second[j] ? ms(kv.second[j]) : -1e9;
+    ++k;
+  }
+  *out_n = k;
+  for (auto& kv : c->tl_ev)
+    for (cudaEvent_t e : kv.second)
+      if (e) cudaEventDestroy(e);
+  c->tl_ev.clear();
+  for (cudaEvent_t e : {ev0, ev_d, ev_v, ev_a}) cudaEventDestroy(e);
+  return SS_OK;
+}
+
 ss_status ss_debug_cta_trace(ss_ctx* c, int32_t M, int32_t launch, int64_t* out, int32_t cap, int32_t* out_n) {
   GUARD(c);
+  if (ensure_debug_bufs(c) != SS_OK) return SS_ERR_BUDGET;
   if (c->state != ST_SESSION || !out || cap < 1 || !out_n || launch < 0) return fail(c, SS_ERR_INVALID, "cta_trace args");
   float ms = 0.f;
   ss_status s = ss_debug_time_pass(c, M, 1, 0, &ms);   // frontier set-up + warm-up
@@ -2435,6 +2566,7 @@ static ss_status read_fragx(ss_ctx* c, const uint16_t* buf, int rows, int cols, 
 ss_status ss_debug_forward(ss_ctx* c, int32_t which, const int32_t* tokens, const int32_t* parents, int32_t n,
                            float* out_logits, float* opt_hidden) {
   GUARD(c);
+  if (ensure_debug_bufs(c) != SS_OK) return SS_ERR_BUDGET;
   if (c->state != ST_SESSION && c->state != ST_DRAFTED)
     return fail(c, SS_ERR_STRUCTURE, "debug_forward needs a session (or a drafted tree)");
   if (!tokens || !parents || n < 1 || n > c->max_nodes || !out_logits) return fail(c, SS_ERR_INVALID, "debug_forward args");

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(const GemmParams 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGemmStages * kGemmStageBytes);
   uint64_t* empty = full + kGemmStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x, tt = blockIdx.y;
+  const int r = p.tile0 + int(blockIdx.x), tt = blockIdx.y;   // r: the matrix's row tile (epilogue)
   const int nC = p.K >> 7;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGemmStages; ++s) {
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(const GemmParams 
     fence_barrier_init();
   }
   __syncthreads();
-  const uint8_t* wbase = p.W + int64_t(r) * nC * kBF16TileBytes;
+  const uint8_t* wbase = p.W + int64_t(r - p.tile0) * nC * kBF16TileBytes;
   if (warp == kGemmConsumerWarps) {
     if (lane == 0) {
       const int pre = nC < kGemmStages ? nC : kGemmStages;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kTcThreads, kFull ? 1 : 2) gemm_tc_kernel(cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t S = cluster_nrank(), q = cluster_rank();
-  const int tt = blockIdx.y, r = blockIdx.z;
+  const int tt = blockIdx.y, r = p.tile0 + int(blockIdx.z);   // r: the matrix's row tile (epilogue)
   const int nC = p.K >> 7, nU = p.K / C::kUnitK;
   const int h0 = int(int64_t(q) * nU / S), h1 = int(int64_t(q + 1) * nU / S), nh = h1 - h0;
   if (threadIdx.x == 0) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kTcThreads, kFull ? 1 : 2) gemm_tc_kernel(cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint8_t* wtile = p.W + int64_t(r) * nC * kBF16TileBytes;
+  const uint8_t* wtile = p.W + int64_t(r - p.tile0) * nC * kBF16TileBytes;
   const uint8_t* xbase = reinterpret_cast<const uint8_t*>(p.X);
   // kFull: unit h = chunk h; weights 32 KB at chunk h of the row tile, activations 32 KB at
   // (h * NT + tt * 16) * 2 KB.  Half-chunks: row group g's 8 cores of half h % 2 are 1 KB at
@@ -322,7 +322,7 @@ void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st, int variant) {
     cudaLaunchKernelEx(&cfg, gemm_kernel, p);
     return;
   }
-  const int S = gemm_tc_split(p.N, p.K, sms_of[dev & 63]);
+  const int S = gemm_tc_split(p.split_n > 0 ? p.split_n : p.N, p.K, sms_of[dev & 63]);   // the whole matrix's plan
   cfg.gridDim = dim3(S, (p.NT * 8) / 128, p.N / 128);
   cfg.blockDim = dim3(kTcThreads);
   const bool fullc = variant != 2;   // whole-chunk stages unless the half-chunk A/B variant

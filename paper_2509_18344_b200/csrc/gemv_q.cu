@@ -34,33 +34,16 @@
 
 namespace ss {
 
-// experiment knobs (build-time; the defaults are the measured best)
-#ifndef SS_K2_MINB
-#define SS_K2_MINB 2          // resident CTAs per SM the kernel is compiled and planned for
-#endif
-#ifndef SS_K2_XTRIM
-#define SS_K2_XTRIM 0         // 1: stage only the token groups the MMAs read (NTC of NT)
-#endif
-#ifndef SS_K2_RING_KB
-#define SS_K2_RING_KB 88      // ring budget per CTA (Q4; Q2 uses 72)
-#endif
-#ifndef SS_K2_CPS
-#define SS_K2_CPS 2           // tile-chunks per ring stage
-#endif
-#ifndef SS_K2_UMULHI
-#define SS_K2_UMULHI 0        // 1: shifts by 8/12 as IMAD.HI (fma pipe) instead of SHF (alu pipe)
-#endif
 constexpr int kGemvQConsumerWarps = 8;
 constexpr int kGemvQThreads = (kGemvQConsumerWarps + 1) * 32;
 
 // NT: token groups of the activation layout; QB: code bits (4, 3 or 2); NTC: token groups the MMAs read
 template <int NT, int QB, int NTC>
 struct GemvQCfg {
-  static constexpr int kCPS = SS_K2_CPS;                          // tile-chunks per pipeline stage
+  static constexpr int kCPS = 2;                                  // tile-chunks per pipeline stage
   static constexpr int kWBytes = QB == 2 ? kQ2TileBytes : (QB == 3 ? kQ3TileBytes : kQ4TileBytes);
   static constexpr int kCodeBytes = QB == 2 ? kQ2CodeBytes : (QB == 3 ? kQ3CodeBytes : kQ4CodeBytes);
-  static constexpr int kXGroups = SS_K2_XTRIM ? NTC : NT;         // token groups staged per chunk
-  static constexpr int kXBytes = kXGroups * kXChunkBytesPerNT;
+  static constexpr int kXBytes = NT * kXChunkBytesPerNT;
   static constexpr int kSBytes = 2 * NT * 8 * 4;                  // group sums of x: [2 groups][Mpad] fp32
   static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
   static constexpr int kMaxStages = 16;
@@ -75,15 +58,15 @@ struct GemvQCfg {
 
 // One pipeline stage (nch tile-chunks of codes + the matching activation chunks + group sums)
 // accumulated into this warp's 16 rows x 8 NTC tokens.
-template <int NT, int NTC, int QB>
-SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int warp, int lane) {
+template <int NT, int NTC, int QB, int NCH>
+SS_DEV void consume_n(const uint8_t* stage, int ci0, float (&acc)[NTC][4], int warp, int lane) {
   using C = GemvQCfg<NT, QB, NTC>;
   const int g = lane >> 2, t4 = lane & 3;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
   const int lq = lane >> 3, lr = lane & 7;   // ldmatrix: lane supplies row lr of core matrix lq
 #pragma unroll
-  for (int ci = 0; ci < C::kCPS; ++ci) {
-    if (ci >= nch) break;
+  for (int cc = 0; cc < NCH; ++cc) {
+    const int ci = ci0 + cc;
     const uint8_t* wst = stage + ci * C::kWBytes;
     const uint32_t xst = smem_u32(stage + C::kCPS * C::kWBytes + ci * C::kXBytes);
     const float* xsum = reinterpret_cast<const float*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes);
@@ -107,7 +90,8 @@ SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int w
         ldsm_x4(b[j][0], b[j][1], b[j][2], b[j][3], xst + core_off(j, 8 * G + lq, lr, 0));
         ldsm_x4(b[j][4], b[j][5], b[j][6], b[j][7], xst + core_off(j, 8 * G + 4 + lq, lr, 0));
       }
-      // one accumulator chain per token tile (the 8 consumer warps x 2 CTAs hide the MMA latency)
+      // one accumulator chain per token tile (the 8 consumer warps x 2 CTAs hide the MMA latency; two
+      // chains per group measured slower)
       float cg[NTC][4];
 #pragma unroll
       for (int j = 0; j < NTC; ++j) cg[j][0] = cg[j][1] = cg[j][2] = cg[j][3] = 0.f;
@@ -129,15 +113,10 @@ SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int w
         } else {
           const uint32_t wg = (k4 < 2) ? cw.x : cw.y, wg8 = (k4 < 2) ? cw.z : cw.w;
           const int pp = 2 * (k4 & 1);
-#if SS_K2_UMULHI
-          auto shr = [](uint32_t v, int sh) { return sh >= 8 ? __umulhi(v, 1u << (32 - sh)) : v >> sh; };
-#else
-          auto shr = [](uint32_t v, int sh) { return v >> sh; };
-#endif
-          a0 = lop3_and_or(shr(wg, 4 * pp), kMagic);
-          a1 = lop3_and_or(shr(wg8, 4 * pp), kMagic);
-          a2 = lop3_and_or(shr(wg, 4 * pp + 4), kMagic);
-          a3 = lop3_and_or(shr(wg8, 4 * pp + 4), kMagic);
+          a0 = lop3_and_or(wg >> (4 * pp), kMagic);
+          a1 = lop3_and_or(wg8 >> (4 * pp), kMagic);
+          a2 = lop3_and_or(wg >> (4 * pp + 4), kMagic);
+          a3 = lop3_and_or(wg8 >> (4 * pp + 4), kMagic);
         }
 #pragma unroll
         for (int j = 0; j < NTC; ++j) mma_bf16_16816(cg[j], a0, a1, a2, a3, b[j][2 * k4], b[j][2 * k4 + 1]);
@@ -158,6 +137,15 @@ SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int w
   }
 }
 
+// a full two-chunk stage is one straight-line body (the scheduler interleaves both chunks' loads and
+// MMA chains: -0.4% per draft pass vs a loop with an early exit); a short last stage takes one chunk
+template <int NT, int NTC, int QB>
+SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int warp, int lane) {
+  static_assert(GemvQCfg<NT, QB, NTC>::kCPS == 2, "two tile-chunks per stage");
+  if (nch == 2) consume_n<NT, NTC, QB, 2>(stage, 0, acc, warp, lane);
+  else consume_n<NT, NTC, QB, 1>(stage, 0, acc, warp, lane);
+}
+
 static int gemv_grid_for(int N, int K, int grid) {
   const int64_t T = int64_t(N / 128) * (K / 128);
   return int(T < grid ? T : grid);   // every Stream-K CTA gets >= 1 tile-chunk
@@ -170,7 +158,7 @@ static int current_device() {
 // split factor of the cluster mode: ~per_sm CTAs per SM (hint, default 2), <= 8 (portable), <= chunks
 static int gemv_q_split(int N, int K, int sms, int hint) {
   const int tiles = N / 128, nC = K / 128;
-  const int per_sm = hint > 0 ? hint : SS_K2_MINB;
+  const int per_sm = hint > 0 ? hint : 2;
   int S = (per_sm * sms) / tiles;
   if (S < 1) S = 1;
   if (S > 8) S = 8;
@@ -193,7 +181,7 @@ SS_DEV void stash_q(float (&acc)[NTC][4], float* dst, int warp, int lane) {
 
 
 template <int NT, int NTC, bool kCluster, int QB>
-__global__ void __launch_bounds__(kGemvQThreads, SS_K2_MINB) gemv_q_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(kGemvQThreads, 2) gemv_q_kernel(const GemvParams p) {
   constexpr int CW = kGemvQConsumerWarps;
   using C = GemvQCfg<NT, QB, NTC>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -252,12 +240,7 @@ __global__ void __launch_bounds__(kGemvQThreads, SS_K2_MINB) gemv_q_kernel(const
       };
       auto issue_x = [&](int st, const Work& ww, int n) {
         uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
-        if (C::kXGroups == NT) {
-          bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
-        } else {   // the first NTC token groups of each chunk
-          for (int i = 0; i < n; ++i)
-            bulk_g2s(base + i * C::kXBytes, p.X + int64_t(ww.c + i) * NT * 1024, uint32_t(C::kXBytes), &full[st]);
-        }
+        bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
         bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * NT * 8, uint32_t(n) * C::kSBytes, &full[st]);
       };
       // weights do not depend on the previous kernel: issue before the grid-dependency wait
@@ -477,8 +460,7 @@ static int ensure_attrs_q() {
   if (it != stages_of.end()) return it->second;
   // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
   // down to ~68 KB of whole stages)
-  const int budget = SS_K2_MINB == 2 ? (QB == 2 ? 72 : (QB == 3 ? 80 : SS_K2_RING_KB)) * 1024
-                                    : (220 * 1024) / SS_K2_MINB - C::smem_for(0);
+  const int budget = (QB == 2 ? 72 : (QB == 3 ? 80 : 88)) * 1024;
   int st = budget / C::kStageBytes;
   if (st < 2) st = 2;
   if (st > C::kMaxStages) st = C::kMaxStages;
@@ -507,7 +489,7 @@ static ClusterPlanQ cluster_plan_q(int N, int K, int sms, int hint = 0) {
   if (it != cache.end()) return it->second;
   using C = GemvQCfg<NT, QB, NTC>;
   const int tiles = N / 128;
-  const int per_sm = hint > 0 ? hint : SS_K2_MINB;
+  const int per_sm = hint > 0 ? hint : 2;
   const int S0 = gemv_q_split(N, K, sms, hint);
   ClusterPlanQ plan{S0, 0, false};
   for (int S = S0; S >= 1; --S) {

@@ -101,10 +101,13 @@ void launch_gemv_q(const GemvParams& p, int sms, bool pdl, cudaStream_t st);   /
 bool gemv_q_tiles_all_resident(int NT, int N, int K, int sms, int bits);
 
 struct GemmParams {
-  const uint8_t* W;              // tiled BF16 weights [N x K]
+  const uint8_t* W;              // tiled BF16 weights [N x K] (row tiles [tile0, tile0 + N/128) of the matrix)
   const uint16_t* X;             // FragX [Mpad x K], Mpad % 128 == 0
-  int N, K, NT;                  // NT = Mpad/8
+  int N, K, NT;                  // NT = Mpad/8; N = rows of this launch
   EpiParams epi;
+  int tile0;                     // first row tile of the matrix this launch covers (epilogue row index)
+  int split_n;                   // rows of the whole matrix (K-split plan; 0 = N): a matrix launched in
+                                 // row blocks keeps its reduction order (batch invariance)
 };
 // variant: 0 tcgen05 whole-chunk stages (default), 1 legacy mma.sync, 2 tcgen05 half-chunk stages
 void launch_gemm(const GemmParams& p, bool pdl, cudaStream_t st, int variant = 0);
@@ -126,6 +129,7 @@ size_t zhdr_bytes(int64_t n);
 size_t zblob_cap(int64_t n);
 cudaError_t zencode(const uint16_t* x, int64_t n, uint8_t* blob, void* scratch, cudaStream_t st, ZHeader* out);
 void launch_zdecode(const uint8_t* blob, uint16_t* out, int64_t n, cudaStream_t st);
+void launch_zdecode_range(const uint8_t* blob, uint16_t* out, int chunk0, int nchunks, cudaStream_t st);
 void zdecode_host(const uint8_t* blob, uint16_t* out);
 
 // generator / quantizer / readback

@@ -109,12 +109,12 @@ __global__ void __launch_bounds__(256) zencode_kernel(const uint16_t* x, ZTable 
   }
 }
 
-__global__ void __launch_bounds__(256) zdecode_kernel(const uint8_t* blob, uint16_t* out) {
+__global__ void __launch_bounds__(256) zdecode_kernel(const uint8_t* blob, uint16_t* out, int chunk0) {
   __shared__ uint8_t table[8];
   __shared__ unsigned wsum[8];
   const ZHeader& hd = *reinterpret_cast<const ZHeader*>(blob);
   if (threadIdx.x < 8) table[threadIdx.x] = hd.table.exp[threadIdx.x];
-  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = chunk0 + int(blockIdx.x), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* pa = blob + hd.a0 + int64_t(c) * kZChunk;
   const uint4* a4 = reinterpret_cast<const uint4*>(pa + tid * 64);
   uint4 av[4];
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) zdecode_kernel(const uint8_t* blob, uint1
   for (int w = 0; w < warp; ++w) base += wsum[w];
   const unsigned* exc_off = reinterpret_cast<const unsigned*>(blob + sizeof(ZHeader));
   const uint8_t* ex = blob + hd.e0 + exc_off[c] + base;
-  uint16_t* oc = out + int64_t(c) * kZChunk + tid * 64;
+  uint16_t* oc = out + int64_t(c - chunk0) * kZChunk + tid * 64;   // out holds chunks [chunk0, ...)
   const uint32_t* aw = reinterpret_cast<const uint32_t*>(av);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {   // 8 weights -> one 16-byte store
@@ -223,7 +223,10 @@ cudaError_t zencode(const uint16_t* x, int64_t n, uint8_t* blob, void* scratch, 
 }
 
 void launch_zdecode(const uint8_t* blob, uint16_t* out, int64_t n, cudaStream_t st) {
-  zdecode_kernel<<<dim3(unsigned(n / kZChunk)), 256, 0, st>>>(blob, out);
+  zdecode_kernel<<<dim3(unsigned(n / kZChunk)), 256, 0, st>>>(blob, out, 0);
+}
+void launch_zdecode_range(const uint8_t* blob, uint16_t* out, int chunk0, int nchunks, cudaStream_t st) {
+  zdecode_kernel<<<dim3(unsigned(nchunks)), 256, 0, st>>>(blob, out, chunk0);
 }
 
 // CPU decoder of a host-resident blob (debug read-back; the same format as zdecode_kernel)

@@ -21,6 +21,11 @@ for spec in "gate_up 60" "qkv 4" "down 116"; do
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 \
   -o gpurun_out/head_$T python tools/prof_gemv.py 6 >> gpurun_out/ncu_k2_$T.log 2>&1
+# K3 tree attention inside a draft pass (the 200th attention launch of tools/pass_time.py)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_node_kernel -s 200 -c 1 \
+  -o gpurun_out/attn_$T python tools/pass_time.py 6 >> gpurun_out/ncu_k2_$T.log 2>&1
+# copy/compute overlap of one step (events around every streamed group)
+timeout 600 python tools/step_timeline.py gpurun_out/step_timeline_$T.json > gpurun_out/step_timeline_$T.log 2>&1
 # K6 (tcgen05 verify GEMM) at M = 289 on a resident Qwen2.5-7B-width layer: gate_up and the head
 # (launch order in tools/prof_k6.py with K6_ITERS=1: qkv 0-1, o 2-3, gate_up 4-5, down 6-7, head 8-9)
 for spec in "gate_up 4" "head 8"; do

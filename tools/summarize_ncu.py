@@ -39,12 +39,16 @@ want = ["Kernel Name", "Grid Size", "Block Size", "launch__cluster_dim_x", "gpu_
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second",
-        "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"]
+        "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
 traffic = {}
 for name, rep in (("gate_up (N=37888, K=3584, M=6)", f"k2_gate_up_{tag}.ncu-rep"), ("qkv (N=4608, K=3584, M=6)", f"k2_qkv_{tag}.ncu-rep"),
                   ("down (N=3584, K=18944, M=6)", f"k2_down_{tag}.ncu-rep"),
                   ("2-bit gate_up (N=37888, K=3584, M=6; NEXT-3)", f"k2q2_gate_up_{tag}.ncu-rep"),
                   ("tcgen05 bf16 head (N=152064, K=3584, M=6)", f"head_{tag}.ncu-rep"),
+                  ("K3 tree attention in a draft pass (M=6 nodes, 4 kv heads)", f"attn_{tag}.ncu-rep"),
                   ("K6 tcgen05 verify GEMM gate_up (N=37888, K=3584, M=289)", f"k6_gate_up_{tag}.ncu-rep"),
                   ("K6 tcgen05 verify head + argmax (N=152064, K=3584, M=289)", f"k6_head_{tag}.ncu-rep")):
     path = os.path.join(src, rep)
@@ -65,6 +69,25 @@ for name, rep in (("gate_up (N=37888, K=3584, M=6)", f"k2_gate_up_{tag}.ncu-rep"
                 pass
     stalls.sort(reverse=True)
     out.append("\nTop warp-stall samples: " + ", ".join(f"{n} {s}" for s, n in [(s, n) for n, s in stalls[:6]]) + "\n")
+    # SASS lines with the most stall samples (source page)
+    src_csv = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                             capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(src_csv)))
+    hi = next((i for i, rr in enumerate(srows) if "Address" in rr and "Source" in rr), None)
+    if hi is not None:
+        sh = srows[hi]
+        ia, isr = sh.index("Source"), sh.index("Warp Stall Sampling (All Samples)")
+
+        def fnum(x):
+            try:
+                return float(x)
+            except ValueError:
+                return 0.0
+        body = srows[hi + 1:]
+        tot_s = sum(fnum(rr[isr]) for rr in body if len(rr) > isr)
+        top = sorted((rr for rr in body if len(rr) > isr), key=lambda rr: -fnum(rr[isr]))[:5]
+        out.append(f"Top SASS lines by stall samples (of {tot_s:.0f}): " +
+                   "; ".join(f"`{rr[ia].strip()[:48]}` {fnum(rr[isr]):.0f}" for rr in top) + "\n")
     rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
     wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
