@@ -360,11 +360,11 @@ ss_status ss_debug_time_pass(ss_ctx* ctx, int32_t M, int32_t iters, int32_t skip
  * 5 flush, 6 kernel end, 7 loop end max, 8 cluster reduction done, 9-12 residual / norm barrier /
  * norm scale / epilogue done; unused events 0); *out_n = number of launches traced (<= cap, <= 512). */
 ss_status ss_debug_trace_pass(ss_ctx* ctx, int32_t M, int64_t* out, int32_t cap, int32_t* out_n);
-/* One SubSpec step (draft + verify + accept, one request) with CUDA events around every streamed
- * layer group (A4 / K7, App. E): out[8*i .. 8*i+7] = (item - first item consumed by
- * this step, layer, group, host bytes, copy start, copy end, compute start, ring release) in ms from
- * the step start (copies issued during the previous step are negative; -1e9 = not recorded in this
- * window); out_phases[0..2] = draft end, verify end, accept end.  *out_n = rows (<= cap). */
+/* Two SubSpec steps (draft + verify + accept, one request) with CUDA events around every streamed
+ * layer group (A4 / K7, App. E); the second is reported: out[8*i .. 8*i+7] = (item -
+ * first item consumed by the reported step, layer, group, host bytes, copy start, copy end, compute
+ * start, ring release) in ms from that step's start (negative: during the lead-in step; -1e9 = not in
+ * the window); out_phases[0..2] = draft end, verify end, accept end.  *out_n = rows (<= cap). */
 ss_status ss_debug_step_timeline(ss_ctx* ctx, const ss_draft_params* p, double* out, int32_t cap, int32_t* out_n,
                                  double* out_phases);
 /* One draft pass (non-fused) with a per-CTA trace of its `launch`-th dequant-GEMV launch (0 = layer

@@ -2468,10 +2468,21 @@ ss_status ss_debug_step_timeline(ss_ctx* c, const ss_draft_params* dp, double* o
     for (cudaEvent_t e : kv.second)
       if (e) cudaEventDestroy(e);
   c->tl_ev.clear();
-  const int64_t seq0 = c->next_consume;
   c->tl_on = true;
+  ss_status s = SS_OK;
+  {   // a lead-in step with the events on: the copies that refill the ring during the measured step's
+      // draft are issued while the lead-in step's verify releases ring regions
+    int32_t toks[1024], n = 0;
+    if ((s = draft_impl(c, -1, dp)) == SS_OK && (s = verify_impl(c)) == SS_OK)
+      s = accept_impl(c, toks, &n, nullptr, c->cur_deff + 1);
+    if (s != SS_OK) {
+      c->tl_on = false;
+      return s;
+    }
+  }
+  const int64_t seq0 = c->next_consume;
   CK(cudaEventRecord(ev0, c->cs));
-  ss_status s = draft_impl(c, -1, dp);
+  s = draft_impl(c, -1, dp);
   if (s == SS_OK) {
     CK(cudaEventRecord(ev_d, c->cs));
     s = verify_impl(c);
@@ -2503,6 +2514,7 @@ ss_status ss_debug_step_timeline(ss_ctx* c, const ss_draft_params* dp, double* o
   for (auto& kv : c->tl_ev) {
     if (k >= cap) break;
     const int64_t seq = kv.first;
+    if (seq < seq0 - n_items) continue;   // consumed by the lead-in step's verify
     const auto lg = c->cycle[size_t(seq % n_items)];
     double* r = out + size_t(k) * 8;
     r[0] = double(seq - seq0);

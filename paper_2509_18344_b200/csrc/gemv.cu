@@ -1,24 +1,21 @@
-// K2 — fused dequant-GEMV/GEMM for the draft (M = frontier tokens <= 32).
-// Y[M x N] = X[M x K] * W_hat^T with W_hat = code*s + z per 64-group
-// ("highly optimized low-bit GEMM kernels"; 4 bit / group 64, PAPER.md:278;
-// reading R3 in DESIGN.md: the affine dequantisation is applied exactly, in fp32).
+// The draft's bf16 GEMV on the 5th-generation tensor cores (tcgen05): the head (N = vocab, with the
+// EPI_TOPK epilogue of K5: per vocab tile max, sum exp((l - max)/T) and top-k, so draft logits never
+// reach HBM) and the GPU-resident layers of a planner placement.
+// Y[M x N] = X[M x K] * W^T for M = frontier tokens <= 32.
 //
-// B200 design (DESIGN.md "K2"):
-//  * weights are tile-chunk contiguous (128 rows x 128 k, 9 KB for Q4): a CTA streams its work
-//    with cp.async.bulk (TMA engine) into an S-stage shared-memory ring guarded by mbarriers; the
-//    weight part of the first stages is issued BEFORE griddepcontrol.wait (PDL), overlapping the
-//    previous kernel's tail;
-//  * 8 consumer warps turn 4-bit codes into exact bf16 (128 + code) with ONE lop3 per pair and
-//    feed them straight into mma.m16n8k16 as the 16-row A operand (tokens are N = 8..32); every
-//    k-step stays inside one 64-group, the producers of X publish its 64-group sums, and
-//    y += s*sum((128+c)x) + (z - 128 s)*sum(x) applies the group scale/zero in fp32;
-//  * narrow matrices (qkv, o, down) use cluster split-K: the S CTAs of a cluster split a row
-//    tile's K and rank 0 reduces their partial tiles through distributed shared memory, in rank
-//    order, then runs the fused epilogue (bias+RoPE+KV write / residual / SiLU*mul / logits);
-//    persistent clusters loop over row tiles so that at most one CTA per SM is used and the next
-//    kernel can co-reside and prefetch;
-//  * the tall bf16 head uses Stream-K (equal contiguous ranges of the tile-chunk space per
-//    persistent CTA) with a fixed-order fixup by the last-arriving CTA.
+// B200 design (DESIGN.md §7):
+//  * weights are 128-row x 128-k tile-chunks in the core-matrix layout (common.cuh) -- directly the A
+//    operand of tcgen05.mma (SWIZZLE_NONE descriptors, LBO 128 B, SBO 2048 B); the activations, in the
+//    same layout, are the B operand (N = 8..32 tokens).  Warp 0 streams stages with cp.async.bulk
+//    (TMA) into an mbarrier ring, issuing the weight part of the first stages before
+//    griddepcontrol.wait (PDL); warp 1's elected lane issues the MMAs into TMEM accumulators (two
+//    slots, so a tile's MMAs overlap the previous tile's read-out); worker warps read TMEM with
+//    tcgen05.ld and run the fused epilogues;
+//  * narrow matrices use cluster split-K with a push-based DSMEM reduction in rank order; the tall
+//    head uses Stream-K with a fixed-order fixup by the last-arriving CTA.
+// The WF = 4 / 2 template branches are the tcgen05 dequant-GEMV measured against the mma.sync K2 in
+// DESIGN.md §7 (converter warps dequantise codes into TMEM, per-64-group TMEM accumulators); no
+// launcher instantiates them -- the product K2 is gemv_q.cu.
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "gemv_core.cuh"

@@ -36,6 +36,8 @@ summary = {
                        "verify": busy(t_draft, t_verify) / max(t_verify - t_draft, 1e-9)},
     "groups_consumed": int(cons.sum()),
     "groups_copied_before_verify": int(((ce < t_draft) & cons & ok).sum()),
+    "bytes_copied_during_draft": float(sum(b * max(0.0, min(e, t_draft) - max(st, 0.0)) / max(e - st, 1e-9)
+                                          for b, st, e in zip(rows[ok, 3], cs[ok], ce[ok]))),
     "compute_ms_per_group_mean": float(np.mean(ke[cons] - ks[cons])) if cons.any() else None,
     "stream_bytes_step": float(rows[cons, 3].sum()),
     "verify_waiting_on_copies_ms": float(sum(max(0.0, s - max(prev, t_draft)) for s, prev in
