@@ -65,6 +65,7 @@ def args_():
                          "group over its host link and pushes it to the peers over NVLink (ss_coop_*)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ar", action="store_true", help="skip the offloading AR baseline line (SURVEY §8(d))")
     return ap.parse_args()
 
 
@@ -502,6 +503,37 @@ def run_ours(a):
             best = min(best, x0.elapsed_time(x1))
     link_gbs = (1 << 30) / (best * 1e-3) / 1e9
     del hbuf, dbuf
+    # ---- offloading AR baseline ("None"): the same engine with D = 0 (one token per
+    # target pass, nothing drafted) at the planner's maximum residency under the same cap; speedup =
+    # SubSpec tokens/s / AR tokens/s, context for the paper's 9.15x ----
+    ar = None
+    if not a.no_ar and world == 1 and Bq == 1:
+        ar_ss = SubSpec(cfg, int(a.cap_gib * GIB), device=dev, max_depth=D, max_top_k=max(k, 6), max_chunk=256,
+                        embed_on_host=0 if a.embed_gpu else 1, compress_stream=0 if a.no_compress else 1)
+        if a.sub_bits != 4:
+            ar_ss.set_substitute_bits(a.sub_bits)
+        ar_ss.load_synthetic(SEED, -1)
+        ar_ss.build_substitutes(a.sub_bits, 64, method=a.quant)
+        ar_ss.prefill(prompt0)
+        for _ in range(a.warmup):
+            ar_ss.step(0, 1, T)
+        cs2 = ar_ss.compute_stream
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(cs2)
+        ar_toks = [t for _ in range(a.steps) for t in ar_ss.step(0, 1, T)]
+        rf = torch.cuda.Event()
+        rf.record(ar_ss.copy_stream)
+        cs2.wait_event(rf)
+        f1.record(cs2)
+        torch.cuda.synchronize()
+        ar_ms = f0.elapsed_time(f1)
+        ar_st = ar_ss.stats()
+        ar = {"tokens_per_s": len(ar_toks) / (ar_ms / 1e3), "ms_per_token": ar_ms / len(ar_toks),
+              "n_resident": ar_st["n_resident"], "tokens": len(ar_toks),
+              "note": "D = 0 through the same engine, planner-max residency, same cap and codec (SURVEY §8(d) AR "
+                      "baseline, P:536); speedup = value / tokens_per_s (tau of random weights, not trained ones)"}
+        ar_ss.close()
     # ---- aggregate over ranks ----
     tmax, tot_tokens = aggregate_ranks(dist, ms, emitted, dist_device(local))
     value = tot_tokens / (tmax / 1e3)
@@ -555,6 +587,7 @@ def run_ours(a):
                    "n_resident": st["n_resident"]},
         "gpu_launches": int(st["gpu_launches"]),
         "clocks": ck, "e2e": e2e, "prompt_sweep": sweep, "setup_s": t_setup,
+        "ar_baseline": ar, "speedup_vs_ar": (value / ar["tokens_per_s"]) if ar else None,
     }
     if rank == 0:
         if world == 1 and not a.no_cpu_baseline:

@@ -2514,7 +2514,7 @@ ss_status ss_debug_step_timeline(ss_ctx* c, const ss_draft_params* dp, double* o
   for (auto& kv : c->tl_ev) {
     if (k >= cap) break;
     const int64_t seq = kv.first;
-    if (seq < seq0 - n_items) continue;   // consumed by the lead-in step's verify
+    if (seq < seq0) continue;   // consumed by the lead-in step's verify
     const auto lg = c->cycle[size_t(seq % n_items)];
     double* r = out + size_t(k) * 8;
     r[0] = double(seq - seq0);

@@ -11,7 +11,7 @@ timeout 900 python bench.py > gpurun_out/bench_$T.jsonl 2> gpurun_out/bench_$T.e
 tail -1 gpurun_out/bench_$T.jsonl | cut -c1-400
 # launch list of exactly the timed steps (bench brackets them with cudaProfilerStart/Stop)
 SS_PROFILE_TIMED=1 timeout 1800 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_$T.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --prompts 0 \
+  --log-file gpurun_out/launches_$T.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-ar --prompts 0 \
   > gpurun_out/ncu_launch_$T.log 2>&1
 # full captures at M = 6 (see tools/prof_gemv.py for the launch order)
 for spec in "gate_up 60" "qkv 4" "down 116"; do
