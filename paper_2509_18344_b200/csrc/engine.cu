@@ -474,10 +474,8 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     p.max_seg = gemv_max_segments(N, K, gemv_streamk_grid(!w.resident, N, K, c->gv_grid));
     p.epi = epi;
     if (c->l2_prefetch) next_weights(c, l, g, &p.pf, &p.pf_bytes);
-    // qkv substitutes: plan one CTA per SM.  Its whole per-CTA weight range (9.3 MB / 144 CTAs =
-    // 64 KB at Qwen-7B) then sits in the ring before the grid-dependency wait, and the CTAs find
-    // free slots next to the previous layer's down GEMV (2 CTAs on ~84 SMs), so they are resident
-    // and prefetched early (measured: pass 2082 -> 2013 us; o and down are slower at 1 CTA/SM).
+    // qkv substitutes: planned at one CTA per SM (the 16-warp K2 plans one CTA per SM for every group;
+    // the hint matters for the 8-warp build, SS_K2_CW = 8, whose default is two per SM)
     p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
     p.self_pf = c->k2_self_pf;
     p.dbg = c->k2_dbg;

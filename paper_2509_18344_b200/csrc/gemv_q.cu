@@ -34,13 +34,28 @@
 
 namespace ss {
 
-constexpr int kGemvQConsumerWarps = 8;
+// Consumer warps per CTA.  16 (default): one CTA per SM, two warp groups, each warp two chunks of a
+// four-chunk stage, a 220 KB ring (4 stages); measured per draft pass at Qwen2.5-7B, M = 6: 1976 us vs
+// 2073 us for 8 warps at two CTAs per SM (88 KB rings), 2032 us for 24 warps (72 registers),
+// 1999 us for 16 warps with 2-3 stages (tools/k2_variants.sh)
+#ifndef SS_K2_CW
+#define SS_K2_CW 16
+#endif
+#ifndef SS_K2_WCH
+#define SS_K2_WCH 2           // tile-chunks per consumer warp per stage
+#endif
+#ifndef SS_K2_RING1_KB
+#define SS_K2_RING1_KB 220    // shared-memory budget of the one-CTA-per-SM variants
+#endif
+constexpr int kGemvQConsumerWarps = SS_K2_CW;
 constexpr int kGemvQThreads = (kGemvQConsumerWarps + 1) * 32;
+constexpr int kGemvQGroups = kGemvQConsumerWarps / 8;   // warp groups: group q takes stage chunks q*WCH..
+constexpr int kGemvQCtasPerSm = kGemvQGroups == 1 ? 2 : 1;
 
 // NT: token groups of the activation layout; QB: code bits (4, 3 or 2); NTC: token groups the MMAs read
 template <int NT, int QB, int NTC>
 struct GemvQCfg {
-  static constexpr int kCPS = 2;                                  // tile-chunks per pipeline stage
+  static constexpr int kCPS = kGemvQGroups * SS_K2_WCH;           // tile-chunks per pipeline stage
   static constexpr int kWBytes = QB == 2 ? kQ2TileBytes : (QB == 3 ? kQ3TileBytes : kQ4TileBytes);
   static constexpr int kCodeBytes = QB == 2 ? kQ2CodeBytes : (QB == 3 ? kQ3CodeBytes : kQ4CodeBytes);
   static constexpr int kXBytes = NT * kXChunkBytesPerNT;
@@ -51,8 +66,10 @@ struct GemvQCfg {
   static constexpr int kXPreTokens = 8;
   static constexpr int kXPreFloats = kXPreTokens * kTileRows;
   static constexpr int kStagingFloats = (NT * 8 + kGemvMaxCluster - 1) * kTileRows;
+  static constexpr int kGPartFloats = kGemvQGroups > 1 ? kGemvQGroups * kTileFloats : 0;   // per-group partial tiles
   static constexpr int smem_for(int S) {
-    return S * kStageBytes + kTileFloats * 4 + kStagingFloats * 4 + 2 * kMaxStages * 8 + 64 + 512 + kXPreFloats * 4;
+    return S * kStageBytes + kTileFloats * 4 + kStagingFloats * 4 + 2 * kMaxStages * 8 + 64 + 512 + kXPreFloats * 4 +
+           kGPartFloats * 4;
   }
 };
 
@@ -90,7 +107,7 @@ SS_DEV void consume_n(const uint8_t* stage, int ci0, float (&acc)[NTC][4], int w
         ldsm_x4(b[j][0], b[j][1], b[j][2], b[j][3], xst + core_off(j, 8 * G + lq, lr, 0));
         ldsm_x4(b[j][4], b[j][5], b[j][6], b[j][7], xst + core_off(j, 8 * G + 4 + lq, lr, 0));
       }
-      // one accumulator chain per token tile (the 8 consumer warps x 2 CTAs hide the MMA latency; two
+      // one accumulator chain per token tile (16 consumer warps per SM hide the MMA latency; two
       // chains per group measured slower)
       float cg[NTC][4];
 #pragma unroll
@@ -137,13 +154,19 @@ SS_DEV void consume_n(const uint8_t* stage, int ci0, float (&acc)[NTC][4], int w
   }
 }
 
-// a full two-chunk stage is one straight-line body (the scheduler interleaves both chunks' loads and
-// MMA chains: -0.4% per draft pass vs a loop with an early exit); a short last stage takes one chunk
+// warp w consumes chunks [q*WCH, q*WCH + WCH) of a stage (q = w / 8, its warp group) for row block
+// w % 8; two chunks are one straight-line body (the scheduler interleaves both chunks' loads and MMA
+// chains: -0.4% per draft pass vs a loop with an early exit); a short last stage takes fewer
 template <int NT, int NTC, int QB>
 SS_DEV void consume_q(const uint8_t* stage, int nch, float (&acc)[NTC][4], int warp, int lane) {
-  static_assert(GemvQCfg<NT, QB, NTC>::kCPS == 2, "two tile-chunks per stage");
-  if (nch == 2) consume_n<NT, NTC, QB, 2>(stage, 0, acc, warp, lane);
-  else consume_n<NT, NTC, QB, 1>(stage, 0, acc, warp, lane);
+  const int c0 = (warp >> 3) * SS_K2_WCH, rb = warp & 7;
+  const int n = nch - c0 < SS_K2_WCH ? nch - c0 : SS_K2_WCH;
+  if constexpr (SS_K2_WCH == 2) {
+    if (n == 2) consume_n<NT, NTC, QB, 2>(stage, c0, acc, rb, lane);
+    else if (n == 1) consume_n<NT, NTC, QB, 1>(stage, c0, acc, rb, lane);
+  } else {
+    if (n >= 1) consume_n<NT, NTC, QB, 1>(stage, c0, acc, rb, lane);
+  }
 }
 
 static int gemv_grid_for(int N, int K, int grid) {
@@ -158,7 +181,7 @@ static int current_device() {
 // split factor of the cluster mode: ~per_sm CTAs per SM (hint, default 2), <= 8 (portable), <= chunks
 static int gemv_q_split(int N, int K, int sms, int hint) {
   const int tiles = N / 128, nC = K / 128;
-  const int per_sm = hint > 0 ? hint : 2;
+  const int per_sm = hint > 0 ? hint : kGemvQCtasPerSm;
   int S = (per_sm * sms) / tiles;
   if (S < 1) S = 1;
   if (S > 8) S = 8;
@@ -167,21 +190,43 @@ static int gemv_q_split(int N, int K, int sms, int hint) {
 }
 
 // accumulators -> [128 x Mpad] fp32 tile (row-major in n), then clear
+// (token_major: [Mpad][128], the cluster reduction's layout).  With several warp groups each group
+// writes its own partial tile to gpart and the copies are summed into dst in group order
+// (deterministic); the caller's next named barrier orders dst for the other threads.
 template <int NT, int NTC>
-SS_DEV void stash_q(float (&acc)[NTC][4], float* dst, int warp, int lane) {
-  const int g = lane >> 2, t4 = lane & 3, Mpad = NT * 8;
+SS_DEV void stash_q(float (&acc)[NTC][4], float* dst, int warp, int lane, bool token_major, float* gpart, int tid,
+                    int nthr) {
+  const int g = lane >> 2, t4 = lane & 3, Mpad = NT * 8, rb = warp & 7;
+  float* out = kGemvQGroups > 1 ? gpart + (warp >> 3) * (kTileRows * Mpad) : dst;
 #pragma unroll
   for (int j = 0; j < NTC; ++j) {
-    const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
-    *reinterpret_cast<float2*>(dst + n0 * Mpad + m) = make_float2(acc[j][0], acc[j][1]);
-    *reinterpret_cast<float2*>(dst + (n0 + 8) * Mpad + m) = make_float2(acc[j][2], acc[j][3]);
+    const int n0 = rb * 16 + g, m = j * 8 + 2 * t4;
+    if (token_major) {
+      out[m * kTileRows + n0] = acc[j][0];
+      out[(m + 1) * kTileRows + n0] = acc[j][1];
+      out[m * kTileRows + n0 + 8] = acc[j][2];
+      out[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
+    } else {
+      *reinterpret_cast<float2*>(out + n0 * Mpad + m) = make_float2(acc[j][0], acc[j][1]);
+      *reinterpret_cast<float2*>(out + (n0 + 8) * Mpad + m) = make_float2(acc[j][2], acc[j][3]);
+    }
     acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  }
+  if constexpr (kGemvQGroups > 1) {
+    named_bar(1, nthr);
+    constexpr int kTF = kTileRows * NT * 8;
+    for (int e = tid; e < kTF; e += nthr) {
+      float v = gpart[e];
+#pragma unroll
+      for (int q = 1; q < kGemvQGroups; ++q) v += gpart[q * kTF + e];
+      dst[e] = v;
+    }
   }
 }
 
 
 template <int NT, int NTC, bool kCluster, int QB>
-__global__ void __launch_bounds__(kGemvQThreads, 2) gemv_q_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(kGemvQThreads, kGemvQCtasPerSm) gemv_q_kernel(const GemvParams p) {
   constexpr int CW = kGemvQConsumerWarps;
   using C = GemvQCfg<NT, QB, NTC>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -304,7 +349,8 @@ __global__ void __launch_bounds__(kGemvQThreads, 2) gemv_q_kernel(const GemvPara
 #pragma unroll
   for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
-  auto stash = [&](float* dst) { stash_q<NT, NTC>(acc, dst, warp, lane); };   // [128][Mpad] partial tile
+  float* gpart = xpre + C::kXPreFloats;   // per-warp-group partial tiles (several warp groups only)
+  auto stash = [&](float* dst) { stash_q<NT, NTC>(acc, dst, warp, lane, false, gpart, threadIdx.x, nthr); };   // [128][Mpad]
 
   uint32_t xph = 0;   // phase of xbar
   auto flush = [&](int r, int c_first, int c_last, bool last) {
@@ -336,15 +382,7 @@ __global__ void __launch_bounds__(kGemvQThreads, 2) gemv_q_kernel(const GemvPara
         for (int m = 0; m < nvalid; ++m)
           bulk_g2s(xpre + m * kTileRows, p.epi.x + int64_t(mlo + m) * p.epi.ldx + int64_t(r) * kTileRows, kTileRows * 4, xbar);
       }
-#pragma unroll
-      for (int j = 0; j < NTC; ++j) {   // token-major [Mpad][128] partial tile
-        const int n0 = warp * 16 + g, m = j * 8 + 2 * t4;
-        otile[m * kTileRows + n0] = acc[j][0];
-        otile[(m + 1) * kTileRows + n0] = acc[j][1];
-        otile[m * kTileRows + n0 + 8] = acc[j][2];
-        otile[(m + 1) * kTileRows + n0 + 8] = acc[j][3];
-        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-      }
+      stash_q<NT, NTC>(acc, otile, warp, lane, true, gpart, threadIdx.x, nthr);   // token-major [Mpad][128]
       named_bar(1, nthr);
       for (int i = threadIdx.x; i < Mpad * (kTileRows / 4); i += nthr) {
         const int m = i / (kTileRows / 4), n4 = (i % (kTileRows / 4)) * 4;
@@ -458,9 +496,10 @@ static int ensure_attrs_q() {
   const int dev = current_device();
   auto it = stages_of.find(dev);
   if (it != stages_of.end()) return it->second;
-  // Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
+  // (two-CTA-per-SM builds, SS_K2_CW = 8) Q2 stages are smaller: a 72 KB budget keeps two CTAs per SM (the Q4/bf16 rings round 88 KB
   // down to ~68 KB of whole stages)
-  const int budget = (QB == 2 ? 72 : (QB == 3 ? 80 : 88)) * 1024;
+  const int budget = kGemvQCtasPerSm == 2 ? (QB == 2 ? 72 : (QB == 3 ? 80 : 88)) * 1024
+                                           : SS_K2_RING1_KB * 1024 - C::smem_for(0);
   int st = budget / C::kStageBytes;
   if (st < 2) st = 2;
   if (st > C::kMaxStages) st = C::kMaxStages;
@@ -489,7 +528,7 @@ static ClusterPlanQ cluster_plan_q(int N, int K, int sms, int hint = 0) {
   if (it != cache.end()) return it->second;
   using C = GemvQCfg<NT, QB, NTC>;
   const int tiles = N / 128;
-  const int per_sm = hint > 0 ? hint : 2;
+  const int per_sm = hint > 0 ? hint : kGemvQCtasPerSm;
   const int S0 = gemv_q_split(N, K, sms, hint);
   ClusterPlanQ plan{S0, 0, false};
   for (int S = S0; S >= 1; --S) {
