@@ -13,7 +13,7 @@ import json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-steps = ["--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--prompts", "0"]
+steps = ["--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-ar", "--prompts", "0"]
 variants = [
     ("full (D=48, k=6, T=0.2, async)", {}, []),
     ("async transfer off", {}, ["--no-async"]),
