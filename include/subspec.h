@@ -347,9 +347,9 @@ ss_status ss_debug_decode_group(ss_ctx* ctx, int32_t layer, int32_t group, uint1
 ss_status ss_debug_time_matmul(ss_ctx* ctx, int32_t which, int32_t layer, int32_t group, int32_t M, int32_t iters,
                                float* out_ms);
 
-/* Debug A/B switches of the kernels (tests and tools only): knob 0 = K2 L2 self-prefetch of each
- * CTA's weight range (0 default, 1 on); knob 1 = K2 debug bits; knob 2 = the K6 kernel variant
- * (0 default: tcgen05 with whole-chunk stages; 1: legacy mma.sync; 2: tcgen05 with half-chunk stages).  Captured draft graphs are dropped.  Errors: INVALID (unknown knob). */
+/* Debug A/B switch of the kernels (tests and tools only): knob 2 = the K6 kernel variant (0 default:
+ * tcgen05 with whole-chunk stages; 1: legacy mma.sync; 2: tcgen05 with half-chunk stages).  Captured
+ * draft graphs are dropped.  Errors: INVALID (unknown knob or value). */
 ss_status ss_debug_set_knob(ss_ctx* ctx, int32_t knob, int32_t value);
 /* Time the draft forward of M frontier nodes (one draft pass incl. head, no top-k): average device ms
  * over `iters` eager launches.  skip: bit mask of kernel classes left out (1 attention, 2 RMSNorm,

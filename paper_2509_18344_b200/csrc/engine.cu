@@ -160,8 +160,6 @@ struct ss_ctx {
   int last_consumed_ev = -1;
   cudaEvent_t ev_root = nullptr;
   bool fuse_norm = true;
-  int k2_dbg = 0;             // K2 debug A/B bits (ss_debug_set_knob 1)
-  int k2_self_pf = 0;         // K2: L2-prefetch each CTA's own weight range (ss_debug_set_knob 0; measured slower)
   int k6_variant = 0;         // K6 kernel variant (ss_debug_set_knob 2; launch_gemm; A/B only)
   bool zcomp = false;         // ss_options.compress_stream (bf16 mode): the host store holds coded blobs
   uint16_t* dbuf = nullptr;   // decoded bf16 row tiles of the group being verified (K6 reads them)
@@ -477,8 +475,6 @@ ss_status matmul(ss_ctx* c, bool target, int l, int g, const uint16_t* X, int M,
     // qkv substitutes: planned at one CTA per SM (the 16-warp K2 plans one CTA per SM for every group;
     // the hint matters for the 8-warp build, SS_K2_CW = 8, whose default is two per SM)
     p.ctas_per_sm = (g == 0 && !w.resident) ? 1 : 0;
-    p.self_pf = c->k2_self_pf;
-    p.dbg = c->k2_dbg;
     p.qbits = c->sub_bits;
     if (g_trace && g_trace_n < g_trace_cap) p.trace = g_trace + kTraceEvents * (g_trace_n++);
     if (g_cta_trace && g_gemv_n++ == g_cta_launch) p.cta_trace = g_cta_trace;
@@ -2345,8 +2341,6 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
     p.epi = base_epi(c, M);
     p.epi.kind = EPI_STORE;
     p.ctas_per_sm = (!head && g == 0 && !w.resident) ? 1 : 0;   // the draft pass's plan (matmul)
-    p.self_pf = c->k2_self_pf;
-    p.dbg = c->k2_dbg;
     p.qbits = c->sub_bits;
     p.epi.out = c->at_o;
     p.epi.ldo = N;
@@ -2369,8 +2363,6 @@ ss_status ss_debug_time_matmul(ss_ctx* c, int32_t which, int32_t layer, int32_t 
 ss_status ss_debug_set_knob(ss_ctx* c, int32_t knob, int32_t value) {
   GUARD(c);
   switch (knob) {
-    case 0: c->k2_self_pf = value; break;
-    case 1: c->k2_dbg = value; break;
     case 2: c->k6_variant = value; break;
     default: return fail(c, SS_ERR_INVALID, "unknown knob");
   }

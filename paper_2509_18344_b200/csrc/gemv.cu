@@ -61,10 +61,8 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
   uint8_t* metabuf = reinterpret_cast<uint8_t*>(staging + C::kStagingFloats);
   uint64_t* full = reinterpret_cast<uint64_t*>(metabuf + C::kMetaBytes);
   uint64_t* empty = full + C::kMaxStages;
-  uint64_t* go = empty + C::kMaxStages;        // Q: chunk slot ready (A written, D slot free)
-  uint64_t* a_empty = go + 4;                  // Q: A slot free (MMAs done)
-  uint64_t* d_full = a_empty + 4;              // accumulator ready
-  uint64_t* d_empty = d_full + 4;              // bf16: tile accumulator consumed
+  uint64_t* d_full = empty + C::kMaxStages;    // tile accumulator ready (two TMEM slots)
+  uint64_t* d_empty = d_full + 2;              // tile accumulator consumed
   uint64_t* xbar = d_empty + 2;                // residual-row prefetch
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 1);
   int* flag = reinterpret_cast<int*>(xbar + 2);
@@ -90,13 +88,9 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::kQ ? 8 + Sh::kMmaWarps : 1);   // Q: every MMA warp's commit + 8 convert warps
+      mbar_init(&empty[s], 1);   // the MMA warp's commit
     }
-    for (int j = 0; j < 4; ++j) {
-      mbar_init(&go[j], 12);        // 8 convert warps (A halves) + 4 accumulate warps (D slot released)
-      mbar_init(&a_empty[j], C::kQ ? 2 : 1);   // Q: one commit per MMA warp (one per 64-group)
-      mbar_init(&d_full[j], C::kQ ? 2 : 1);
-    }
+    for (int j = 0; j < 2; ++j) mbar_init(&d_full[j], 1);
     for (int j = 0; j < 2; ++j) mbar_init(&d_empty[j], 4);
     mbar_init(xbar, 1);
     fence_barrier_init();
@@ -147,8 +141,6 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
       auto issue_x = [&](int st, const Work& ww, int n) {
         uint8_t* base = ring + st * C::kStageBytes + C::kCPS * C::kWBytes;
         bulk_g2s(base, p.X + int64_t(ww.c) * NT * 1024, uint32_t(n) * C::kXBytes, &full[st]);
-        if constexpr (C::kQ)
-          bulk_g2s(base + C::kCPS * C::kXBytes, p.XS + int64_t(ww.c) * 2 * kN, uint32_t(n) * C::kSBytes, &full[st]);
       };
       // L2 prefetch of the next matrix (independent of every activation): this CTA's slice
       if (p.pf && p.pf_bytes > 0) {
@@ -185,19 +177,15 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
     return;
   }
 
-  if (warp == 1 || warp >= 14) {
-    // ------------------------------ MMA issuers (whole warps, one elected lane issues) --------------
-    // substitutes: MMA warp m = (warp 1 -> 0, warp 14 + i -> 1 + i) issues the MMAs of 64-group m % 2 of
-    // the tile-chunks with cc % (kMmaWarps / 2) == m / 2 (independent accumulators; each warp commits
-    // its own MMAs, two commits per chunk); bf16: warp 1 alone
-    const int mw = warp == 1 ? 0 : warp - 13;
-    const int Gm = mw & 1, par = mw >> 1;
-    constexpr int kPar = Sh::kMmaWarps / 2;
+  if (warp == 1) {
+    // ------------------------------ MMA issuer (one elected lane issues) --------------------------
+    // per stage: 8 MMAs (M = 128 rows, N = tokens, K = 16) into the tile's TMEM slot tc % 2; the
+    // stage is released by a commit to its "empty" barrier, the tile's accumulator by one to d_full
     Work w = make_work<kCluster>(p.N, p.K, crank, csize);
     constexpr uint32_t idesc = umma_idesc_bf16(kN);
     int s = 0;
     uint32_t ph = 0;
-    uint32_t cc = 0, tc = 0;   // chunk counter (Q: slot cc % 4, parity cc / 4 % 2); tile counter (bf16)
+    uint32_t tc = 0;   // tile counter
     const uint32_t ring0 = smem_u32(ring);
     while (w.left > 0) {
       const int cur_r = w.r;
@@ -205,47 +193,25 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
       do {
         const int nch = w.take(C::kCPS);
         mbar_wait(&full[s], ph);
-        if (Gm == 0) gtr(int(cc), 11);
+        gtr(int(tc), 11);
         tc_fence_after();
         const uint32_t sb = ring0 + s * C::kStageBytes;
         const uint64_t xdesc = umma_desc(sb + C::kCPS * C::kWBytes, 128, 2048);   // B: token groups at 2048 B
         w.next(nC, nch);
         const bool last = w.left == 0 || w.r != cur_r;
-        if constexpr (C::kQ) {
-          for (int ci = 0; ci < nch; ++ci) {
-            const uint32_t j = cc & 3;
-            if (kPar > 1 && int(cc % kPar) != par) {
-              ++cc;
-              continue;
-            }
-            mbar_wait(&go[j], (cc >> 2) & 1);   // A of this chunk written and accumulator slot j free
-            if (Gm == 0) gtr(int(cc), 3); else gtr(int(cc), 4);
-            tc_fence_after();
-            const uint32_t acol = tbase + C::kACol0 + j * 64, dcol = tbase + j * C::kDCols;
-            const uint64_t xd = xdesc + uint64_t(ci * (C::kXBytes >> 4));
+        const uint32_t j = tc & 1;
+        if (first) {
+          mbar_wait(&d_empty[j], ((tc >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        const uint64_t wdesc = umma_desc(sb, 128, 2048);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)   // K = 16 per MMA: 8 A columns, +256 B of B (16 in desc units)
-              umma_ts_w(dcol + Gm * kN, acol + Gm * 32 + kk * 8, xd + uint64_t(Gm * 64 + kk * 16), idesc, kk > 0);
-            umma_commit_w(&a_empty[j]);
-            umma_commit_w(&d_full[j]);
-            if (Gm == 0) gtr(int(cc), 5); else gtr(int(cc), 13);
-            ++cc;
-          }
-        } else {
-          const uint32_t j = tc & 1;
-          if (first) {
-            mbar_wait(&d_empty[j], ((tc >> 1) & 1) ^ 1);
-            tc_fence_after();
-          }
-          const uint64_t wdesc = umma_desc(sb, 128, 2048);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_ss_w(tbase + j * C::kDCols, wdesc + uint64_t(kk * 16), xdesc + uint64_t(kk * 16), idesc,
-                      (first && kk == 0) ? 0u : 1u);
-          if (last) {
-            umma_commit_w(&d_full[j]);
-            ++tc;
-          }
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ss_w(tbase + j * C::kDCols, wdesc + uint64_t(kk * 16), xdesc + uint64_t(kk * 16), idesc,
+                    (first && kk == 0) ? 0u : 1u);
+        if (last) {
+          umma_commit_w(&d_full[j]);
+          ++tc;
         }
         umma_commit_w(&empty[s]);
         first = false;
@@ -271,8 +237,7 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
   const int q = warp & 3;                       // TMEM lane quadrant of this warp
   const int row = 32 * q + lane;                // weight row of the tile owned in TMEM
   const uint32_t tl = tbase + (uint32_t(32 * q) << 16);
-  const bool is_acc = warp >= 10;               // accumulate warps 10..13; convert warps 2..9
-  const int Gc = (warp - 2) >> 2;               // convert warps: 64-group of every chunk
+  const bool is_acc = warp >= 10;               // TMEM readers 10..13 (one lane quadrant each); 2..9 epilogue only
 
   uint32_t xph = 0;   // phase of xbar
   // --- split-K reduction + epilogue of tile r from otile (worker threads only) ---
@@ -368,14 +333,8 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
   const int64_t n_items = w.left;
   int s = 0;
   uint32_t ph = 0;
-  uint32_t cc = 0, tc = 0;
+  uint32_t tc = 0;
   const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128): 128 + code is exact in bf16
-  uint32_t* meta_s = reinterpret_cast<uint32_t*>(metabuf);                            // [8][2][128]
-  float* xs_s = reinterpret_cast<float*>(metabuf + C::kMetaSlots * 2 * kTileRows * 4);   // [8][2][N]
-  if (C::kQ && is_acc && lane == 0)
-    for (int j = 0; j < 4; ++j) mbar_arrive(&go[j]);   // every accumulator slot starts free
-  bool cpend = false;   // convert warps: a TMEM store whose "go" arrival is pending
-  uint32_t cj = 0;
   while (w.left > 0) {
     const int cur_r = w.r, c_first = w.c;
     int c_last = w.c;
@@ -392,165 +351,34 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
       }
       w.next(nC, nch);
       const bool last_of_tile = w.left == 0 || w.r != cur_r;
-      if constexpr (C::kQ) {
-        if (!is_acc) {
-          // ---- convert: this row's 64 codes of group Gc -> exact bf16 (128 + code) pairs -> TMEM ----
-          // Software-pipelined: the TMEM store of chunk c completes while chunk c + 1 is converted, and
-          // only then does this warp report chunk c's A half (the "go" barrier).
-          if (warp == 2 && lane == 0) gtr(int(cc), 12);
-          mbar_wait(&full[s], ph);
-          if (warp == 2 && lane == 0) gtr(int(cc), 10);
-          for (int ci = 0; ci < nch; ++ci) {
-            const uint8_t* wst = stage + ci * C::kWBytes;
-            uint32_t v[32];
-            if constexpr (WF == 4) {
-              const uint4 c0 = *reinterpret_cast<const uint4*>(wst + Gc * 4096 + row * 16);
-              const uint4 c1 = *reinterpret_cast<const uint4*>(wst + Gc * 4096 + 2048 + row * 16);
-              const uint32_t wd[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-              if (p.dbg & 1) {   // debug A/B: no conversion work (results wrong)
+      if (is_acc && last_of_tile) {   // the tile's accumulator, K reduced by the MMAs
+        const uint32_t j = tc & 1;
+        mbar_wait(&d_full[j], (tc >> 1) & 1);
+        tc_fence_after();
+        uint32_t d[MV];
+        if constexpr (MV == 8) {
+          uint32_t d8[8];
+          tmem_ld8(tl + j * C::kDCols, d8);
 #pragma unroll
-                for (int jj = 0; jj < 32; ++jj) v[jj] = wd[jj & 7];
-              } else {
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-                for (int pp = 0; pp < 4; ++pp) v[4 * jj + pp] = lop3_and_or(wd[jj] >> (4 * pp), kMagic);
-              }
-            } else {
-              const uint4 c0 = *reinterpret_cast<const uint4*>(wst + Gc * 2048 + row * 16);
-              const uint32_t wd[4] = {c0.x, c0.y, c0.z, c0.w};
-#pragma unroll
-              for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-                for (int pp = 0; pp < 8; ++pp) v[8 * jj + pp] = lop3_and_or2(wd[jj] >> (2 * pp), kMagic);
-            }
-            const uint32_t meta = *reinterpret_cast<const uint32_t*>(wst + C::kCodeBytes + Gc * 512 + row * 4);
-            float4 xsv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (q == 0 && lane < kN / 4)
-              xsv = reinterpret_cast<const float4*>(stage + C::kCPS * (C::kWBytes + C::kXBytes) + ci * C::kSBytes + Gc * kN * 4)[lane];
-            if (cpend) {   // the previous chunk's TMEM store has had this conversion's time to land
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&go[cj]);
-              if (warp == 2 && lane == 0) gtr(int(cc) - 1, 2);
-              cpend = false;
-            }
-            const uint32_t j = cc & 3;
-            if (warp == 2 && lane == 0) gtr(int(cc), 0);
-            mbar_wait(&a_empty[j], ((cc >> 2) & 1) ^ 1);
-            if (warp == 2 && lane == 0) gtr(int(cc), 1);
-            tc_fence_after();
-            tmem_st32(tl + C::kACol0 + j * 64 + Gc * 32, v);
-            // scale/zero and this group's activation sums -> side buffer slot cc % 8 (the stage can then be
-            // refilled as soon as the codes are converted).  Slot cc % 8 was last read by the accumulate
-            // step of chunk cc - 8, which precedes its release of accumulator slot j, which the MMAs of
-            // chunk cc - 4 waited for, which the a_empty wait above waited for.
-            const uint32_t k8 = cc & 7;
-            meta_s[(k8 * 2 + Gc) * kTileRows + row] = meta;
-            if (q == 0 && lane < kN / 4) reinterpret_cast<float4*>(xs_s + (k8 * 2 + Gc) * kN)[lane] = xsv;
-            cj = j;
-            cpend = true;
-            ++cc;
-            if (p.dbg & 2) {   // debug A/B: no software pipelining
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&go[cj]);
-              cpend = false;
-            }
-          }
-          if (last_of_tile && cpend) {   // the accumulate warps need the tile's last chunk before the flush
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&go[cj]);
-            cpend = false;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
+          for (int t = 0; t < 8; ++t) d[t] = d8[t];
         } else {
-          // ---- accumulate: y += s * acc + (z - 128 s) * sum(x) per 64-group (exact affine, fp32; R3) ----
-          for (int ci = 0; ci < nch; ++ci) {
-            const uint32_t j = cc & 3, k8 = cc & 7;
-            mbar_wait(&d_full[j], (cc >> 2) & 1);   // implies the side-buffer slot is written (via go)
-            if (warp == 10 && lane == 0) gtr(int(cc), 6);
-            tc_fence_after();
-            uint32_t m[2];
-            float4 xv[2][MV / 4];
 #pragma unroll
-            for (int G = 0; G < 2; ++G) {
-              m[G] = meta_s[(k8 * 2 + G) * kTileRows + row];
+          for (int h = 0; h < MV / 16; ++h) {
+            uint32_t d16[16];
+            tmem_ld16(tl + j * C::kDCols + h * 16, d16);
 #pragma unroll
-              for (int t4 = 0; t4 < MV / 4; ++t4) xv[G][t4] = reinterpret_cast<const float4*>(xs_s + (k8 * 2 + G) * kN)[t4];
-            }
-            uint32_t d[2][MV];
-#pragma unroll
-            for (int G = 0; G < 2; ++G) {
-              if constexpr (MV == 8) {
-                uint32_t d8[8];
-                tmem_ld8(tl + j * C::kDCols + G * kN, d8);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) d[G][t] = d8[t];
-              } else {
-#pragma unroll
-                for (int h = 0; h < MV / 16; ++h) {
-                  uint32_t d16[16];
-                  tmem_ld16(tl + j * C::kDCols + G * kN + h * 16, d16);
-#pragma unroll
-                  for (int t = 0; t < 16; ++t) d[G][16 * h + t] = d16[t];
-                }
-              }
-            }
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&go[j]);   // accumulator slot j free for the chunk four ahead
-            if (warp == 10 && lane == 0) gtr(int(cc), 7);
-#pragma unroll
-            for (int G = 0; G < 2; ++G) {
-              const float sc = __uint_as_float(m[G] << 16);
-              const float zz = fmaf(-128.0f, sc, __uint_as_float(m[G] & 0xFFFF0000u));   // z - 128 s, exact
-#pragma unroll
-              for (int t4 = 0; t4 < MV / 4; ++t4) {
-                y[4 * t4 + 0] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 0]), fmaf(zz, xv[G][t4].x, y[4 * t4 + 0]));
-                y[4 * t4 + 1] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 1]), fmaf(zz, xv[G][t4].y, y[4 * t4 + 1]));
-                y[4 * t4 + 2] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 2]), fmaf(zz, xv[G][t4].z, y[4 * t4 + 2]));
-                y[4 * t4 + 3] = fmaf(sc, __uint_as_float(d[G][4 * t4 + 3]), fmaf(zz, xv[G][t4].w, y[4 * t4 + 3]));
-              }
-            }
-            ++cc;
+            for (int t = 0; t < 16; ++t) d[16 * h + t] = d16[t];
           }
         }
-      } else {
-        if (is_acc && last_of_tile) {   // bf16: the tile's accumulator, K reduced by the MMAs
-          const uint32_t j = tc & 1;
-          mbar_wait(&d_full[j], (tc >> 1) & 1);
-          tc_fence_after();
-          uint32_t d[MV];
-          if constexpr (MV == 8) {
-            uint32_t d8[8];
-            tmem_ld8(tl + j * C::kDCols, d8);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[j]);
 #pragma unroll
-            for (int t = 0; t < 8; ++t) d[t] = d8[t];
-          } else {
-#pragma unroll
-            for (int h = 0; h < MV / 16; ++h) {
-              uint32_t d16[16];
-              tmem_ld16(tl + j * C::kDCols + h * 16, d16);
-#pragma unroll
-              for (int t = 0; t < 16; ++t) d[16 * h + t] = d16[t];
-            }
-          }
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[j]);
-#pragma unroll
-          for (int t = 0; t < MV; ++t) y[t] = __uint_as_float(d[t]);
-        }
-        if (last_of_tile) ++tc;
+        for (int t = 0; t < MV; ++t) y[t] = __uint_as_float(d[t]);
       }
+      if (last_of_tile) ++tc;
+    
       if (++s == kStages) {
         s = 0;
         ph ^= 1;

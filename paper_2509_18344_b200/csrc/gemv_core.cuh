@@ -1,63 +1,56 @@
-// K2 building blocks of the dequant-GEMV kernel (gemv.cu): pipeline geometry, work lists, and the
-// per-stage tensor-core consumer (see gemv.cu's header for the design).
+// Shared building blocks of the draft GEMVs (gemv_q.cu: K2 on substitutes; gemv.cu: the tcgen05 bf16
+// GEMV): pipeline geometry, work lists (cluster tiles / Stream-K), cluster and trace helpers.
 #pragma once
 #include "common.cuh"
 
 namespace ss {
 
-// Warp roles of the tcgen05 K2 kernel (gemv.cu), one CTA per SM: 0 producer (TMA), 1 MMA issuer +
-// TMEM owner, 2..9 convert (quadrant w % 4, 64-group (w - 2) / 4 of every tile-chunk: 4-/2-bit codes ->
-// bf16 A operand in TMEM), 10..13 accumulate (quadrant w % 4: per-group TMEM accumulators -> fp32
-// rows), 14.. further MMA issuers.  Substitutes use 2 (MV = 32) or 4 MMA warps: warp (G, parity)
-// issues the MMAs of 64-group G of the tile-chunks of that parity (MMA issue from one thread is ~13
-// instructions per tcgen05.mma and shares its sub-partition with three busy warps).  Warps 2..13
-// (384 threads) run the split-K reduction and epilogue.
+// The tcgen05 bf16 GEMV of gemv.cu (the head, resident layers), one CTA per SM: warp 0 producer
+// (TMA), warp 1 MMA issuer + TMEM owner, warps 2..13 workers (10..13 read the TMEM accumulators, one
+// lane quadrant each; all 12 run the split-K reduction and the epilogue).
 template <int WF, int MV>
 struct GemvShape {
-  static constexpr int kMmaWarps = WF == 16 ? 1 : (MV <= 16 ? 4 : 2);
-  static constexpr int kWarps = 14 + (kMmaWarps > 1 ? kMmaWarps - 1 : 0);
+  static_assert(WF == 16, "the tcgen05 GEMV is the bf16 path (substitutes: gemv_q.cu)");
+  static constexpr int kMmaWarps = 1;
+  static constexpr int kWarps = 14;
   static constexpr int kThreads = kWarps * 32;
-  static constexpr int kMaxReg = kWarps > 16 ? 96 : 128;   // <= 5 warps x 96 x 32 per sub-partition
+  static constexpr int kMaxReg = 128;   // <= 4 warps x 128 x 32 per sub-partition
 };
-constexpr int kGemvMaxThreads = 17 * 32;
 constexpr int kGemvWorkers = 384;        // warps 2..13
+constexpr int kGemvMaxThreads = 14 * 32; // block of the bf16 GEMV (occupancy proxy)
 constexpr int kGemvMaxCluster = 8;       // largest (portable) cluster the split factor may use
 constexpr int kGemvSmemBudget = 227 * 1024;
 
-// WF: weight format, 16 = bf16 (A from shared memory), 4 / 2 = group-64 substitutes (A dequantised
-// into TMEM).  NT: token groups of 8 (MMA N = 8 NT: 16 or 32).
+// NT: token groups of 8 (MMA N = 8 NT: 16 or 32).  A stage is one 32 KB bf16 tile-chunk plus the
+// matching activation chunk; TMEM holds two tile accumulators of N columns (512 columns allocated:
+// the CTA is alone on its SM).
 template <int WF, int NT>
 struct GemvCfg {
-  static constexpr bool kQ = WF != 16;
-  static constexpr int kCPS = kQ ? 2 : 1;                       // tile-chunks per pipeline stage
-  static constexpr int kWBytes = WF == 16 ? kBF16TileBytes : (WF == 2 ? kQ2TileBytes : kQ4TileBytes);
-  static constexpr int kCodeBytes = WF == 2 ? kQ2CodeBytes : kQ4CodeBytes;
+  static_assert(WF == 16, "bf16 only");
+  static constexpr int kCPS = 1;                                // tile-chunks per pipeline stage
+  static constexpr int kWBytes = kBF16TileBytes;
   static constexpr int kXBytes = NT * kXChunkBytesPerNT;
   static constexpr int kN = NT * 8;                             // MMA N (tokens, padded)
-  static constexpr int kSBytes = kQ ? 2 * kN * 4 : 0;           // group sums of x: [2 groups][N] fp32
+  static constexpr int kSBytes = 0;
   static constexpr int kStageBytes = kCPS * (kWBytes + kXBytes + kSBytes);
   static constexpr int kMaxStages = 16;
-  // TMEM (all 512 columns): Q: 4 chunk slots of accumulators (2 groups x N columns) then 4 A slots of
-  // 64 columns (128 k as bf16 pairs); bf16: 2 tile slots of N columns
-  static constexpr int kSlots = kQ ? 4 : 2;
-  static constexpr int kDCols = kQ ? 2 * kN : kN;
-  static constexpr int kACol0 = kSlots * kDCols;
+  static constexpr int kSlots = 2;
+  static constexpr int kDCols = kN;
   static constexpr int kTmemCols = 512;
-  static constexpr int kMetaSlots = 8;                          // scale/zero + group-sum side buffer
-  static constexpr int kMetaBytes = kQ ? kMetaSlots * (2 * kTileRows * 4 + 2 * kN * 4) : 0;
+  static constexpr int kMetaBytes = 0;
   static constexpr int kTileFloats = kTileRows * kN;
   static constexpr int kXPreTokens = 8;
   static constexpr int kXPreFloats = kXPreTokens * kTileRows;
   // cluster reduction staging: [S][ceil(N/S)][128] fp32 partial columns pushed by the ranks
   static constexpr int kStagingFloats = (kN + kGemvMaxCluster - 1) * kTileRows;
-  static constexpr int kBars = 2 * kMaxStages + 3 * 4 + 2 + 2;   // full, empty, go, a_empty, d_full, d_empty, xbar
+  static constexpr int kBars = 2 * kMaxStages + 2 + 2 + 2;     // full, empty, d_full, d_empty, xbar
   static constexpr int kFixed = kTileFloats * 4 + kStagingFloats * 4 + kMetaBytes + kBars * 8 + 64 + 512 + kXPreFloats * 4;
   static constexpr int smem_for(int S) { return S * kStageBytes + kFixed; }
   static constexpr int stages() {
     const int s = (kGemvSmemBudget - kFixed - 1024) / kStageBytes;
     return s > kMaxStages ? kMaxStages : (s < 2 ? 2 : s);
   }
-  static_assert(kACol0 + (kQ ? kSlots * 64 : 0) <= kTmemCols, "TMEM columns");
+  static_assert(kSlots * kDCols <= kTmemCols, "TMEM columns");
 };
 SS_HD int64_t owner_of(int64_t t, int64_t T, int G) { return ((t + 1) * G - 1) / T; }
 

@@ -87,8 +87,6 @@ struct GemvParams {
   unsigned long long* cta_trace; // optional per-CTA trace [grid][5]: smid, entry, first data, loop end, end
   unsigned long long* gtrace;    // optional per-group clock64 events of CTA 0 [64][8] (debug)
   int ctas_per_sm;               // cluster plan: resident CTAs per SM to plan for (0 = default 2)
-  int self_pf;                   // substitutes: L2-prefetch this CTA's whole weight range at entry
-  int dbg;                       // debug A/B bits (ss_debug_set_knob 1)
   int qbits;                     // code bits of a quantised matrix: 4 (0 = 4) or 2 (NEXT-3)
   EpiParams epi;
 };

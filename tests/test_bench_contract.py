@@ -28,3 +28,13 @@ def test_reference_arm_2bit_workload():
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert "2-bit" in line["config"]["workload"] and "2-bit substitute" in line["cpu_baseline"]["sample"]
+
+
+def test_reference_arm_3bit_hqq_workload():
+    # --sub-bits 3 --quant hqq (NEXT-3): the oracle sample builds a 3-bit HQQ substitute and says so
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "tiny",
+                        "--steps", "1", "--warmup", "0", "--depth", "4", "--sub-bits", "3", "--quant", "hqq"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert "3-bit g64 HQQ" in line["config"]["workload"] and "3-bit substitute" in line["cpu_baseline"]["sample"]
