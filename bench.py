@@ -486,9 +486,21 @@ def run_ours(a):
     n_res = cfg.n_layers - n_off
     pass_bytes = n_off * sum(k2_bytes(N, K, M, a.sub_bits) for N, K in groups) + \
         n_res * sum(2 * N * K for N, K in groups) + cfg.vocab * cfg.hidden * 2
+    k3 = None
     if Bq == 1:
         t_pass = ss.debug_time_pass(M, 5, 0)
         draft_pass = {"us": t_pass * 1e3, "weight_bytes": pass_bytes, "gbs": pass_bytes / (t_pass * 1e-3) / 1e9}
+        # K3 tree attention inside the pass: its share by leaving it out (attribution only),
+        # and the K/V bytes it must read: each frontier node's P prefix keys + its (<= 2) tree keys, K and
+        # V, per kv head and layer (the per-(kv head, node) kernel reads the prefix once per node)
+        t_noattn = ss.debug_time_pass(M, 5, 1)
+        P = ss.stats()["committed_len"]
+        kv_key = 2 * cfg.head_dim * 2 * cfg.n_kv_heads                     # bytes per key per layer
+        k3_bytes = cfg.n_layers * M * (P + 2) * kv_key
+        us = (t_pass - t_noattn) * 1e3
+        k3 = {"us_per_pass": us, "us_per_layer": us / cfg.n_layers, "kv_bytes_per_pass": k3_bytes,
+              "gbs": k3_bytes / (us * 1e-6) / 1e9 if us > 0 else None, "prefix_len": P, "bound": "latency",
+              "note": "pass time with vs without the attention launches (debug_time_pass skip mask 1)"}
     # host link measured in the same run: pinned H2D 1 GiB on the copy stream, best of 5
     hbuf = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
     dbuf = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -571,7 +583,7 @@ def run_ours(a):
                      "traffic": traffic, "traffic_launch": "gate_up (ncu --set full, profiles/k2_traffic.json)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      "per_group": per_group, "in_pass": k2_in_pass, "head_bf16_gemv_gbs": head_gbs,
-                     "draft_pass": draft_pass},
+                     "draft_pass": draft_pass, "k3_attention": k3},
         "streaming": {"mode": f"cooperative over {world} ranks (NEXT-1)" if coop else "per rank",
                       "peer_bytes_per_step": st["peer_bytes"] / a.steps,
                       "codec": "off (plain bf16)" if a.no_compress else "lossless exponent-coded bf16 (K7 codec)",
