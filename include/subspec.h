@@ -303,6 +303,10 @@ const char* ss_last_error(ss_ctx* ctx);
 void ss_destroy(ss_ctx* ctx);
 
 /* ---- debug / parity entry points (tests only) ------------------------------------------- */
+/* The matmul / forward / pass-timing entry points write device outputs into a debug scratch buffer
+ * allocated (cudaMalloc) on their first use, outside the context's arena: it is not a product
+ * allocation and does not count against the emulated VRAM cap.  Errors: BUDGET if it cannot be
+ * allocated. */
 /* Device generator for one tensor id (natural row-major bf16 bits) -> host out[rows*cols]. */
 ss_status ss_debug_gen_tensor(ss_ctx* ctx, uint64_t seed, int32_t tid, int64_t rows, int64_t cols,
                               int32_t kind /*0 mat, 1 gain, 2 bias*/, double sigma, uint16_t* out);
