@@ -219,7 +219,6 @@ ss_status check_launch(ss_ctx* c, const char* what) {
   return SS_OK;
 }
 
-size_t q4_bytes(int N, int K) { return size_t(N / 128) * (K / 128) * kQ4TileBytes; }
 size_t sub_bytes(int N, int K, int bits) { return size_t(N / 128) * (K / 128) * size_t(qtile_bytes(bits)); }
 size_t bf16_bytes(int N, int K) { return size_t(N) * K * 2; }
 
@@ -431,7 +430,7 @@ int g_skip = 0;
 unsigned long long* g_trace = nullptr;   // device buffer [launch][kTraceEvents] for ss_debug_trace_pass
 int g_trace_n = 0, g_trace_cap = 0;
 unsigned long long* g_cta_trace = nullptr;   // per-CTA trace of GEMV launch number g_cta_launch
-int g_cta_launch = -1, g_gemv_n = 0, g_cta_grid = 0;
+int g_cta_launch = -1, g_gemv_n = 0;
 enum { SKIP_ATTN = 1, SKIP_NORM = 2, SKIP_GEMV = 4, SKIP_HEAD = 8 };
 
 // the draft's weight stream in pass order: qkv, o, gate_up, down of each layer, then the head

@@ -334,7 +334,6 @@ __global__ void __maxnreg__((GemvShape<WF, MV>::kMaxReg)) gemv_kernel(const Gemv
   int s = 0;
   uint32_t ph = 0;
   uint32_t tc = 0;
-  const uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128): 128 + code is exact in bf16
   while (w.left > 0) {
     const int cur_r = w.r, c_first = w.c;
     int c_last = w.c;

@@ -343,7 +343,6 @@ __global__ void __launch_bounds__(kGemvQThreads, kGemvQCtasPerSm) gemv_q_kernel(
   // ------------------------------ consumers --------------------------------
   griddep_wait();
   if (threadIdx.x == 0) SS_TRACE_CTA0(2);
-  const int g = lane >> 2, t4 = lane & 3;
   const int nthr = CW * 32;
   float acc[NTC][4];
 #pragma unroll

@@ -234,7 +234,7 @@ SS_DEV bool sel_before(float s, int t, int m, float s2, int t2, int m2) {
   return s > s2 || (s == s2 && (t < t2 || (t == t2 && m < m2)));
 }
 __global__ void __launch_bounds__(512) topk_select_kernel(const TopkParams p) {
-  extern __shared__ __align__(16) uint8_t sm[];
+  extern __shared__ __align__(128) uint8_t sm[];
   const int B = p.blocks_per_row;
   float* sel_s = reinterpret_cast<float*>(sm);      // [k]
   int* sel_t = reinterpret_cast<int*>(sel_s + 32);  // [k] token
