@@ -15,7 +15,7 @@ import torch
 
 from synth.configs import TINY, SMALL
 from synth.prompts import mtbench_prompt, uniform_prompt
-from oracle.model import TargetWeights
+from oracle.model import draft_layers, TargetWeights
 from oracle.tree import Tree
 from oracle.decode import Session, ar_generate, sd_generate
 
@@ -166,3 +166,20 @@ def test_capacity_clamp_keeps_losslessness(tiny_target):
     with pytest.raises(ValueError):
         s2 = Session(cfg, SEED, target=tw, max_nodes=256)
         s2.prefill(list(range(65)))
+
+
+def test_sd_lossless_many_prompts(tiny_target):
+    """O.8 at breadth (>= 200 prompts, D <= 48): for 200 MT-Bench-shaped prompts, SubSpec's
+    greedy output equals plain greedy AR ("lossless"), over trees from D = 48, k = 6 (the
+    paper's setting) down to a chain, in the GPU's bf16-emulation mode."""
+    combos = [(48, 6), (16, 2), (4, 6), (1, 1), (8, 3), (24, 4), (2, 2), (4, 6), (12, 1), (6, 6),
+              (32, 2), (16, 2), (4, 6), (1, 1), (8, 3), (24, 4), (2, 2), (4, 6), (12, 1), (6, 6)]
+    views = {nr: draft_layers(tiny_target, nr) for nr in (0, 1)}   # the draft views, built once
+    for p in range(200):
+        prompt = mtbench_prompt(SEED, 2000 + p, TINY.vocab, 24 + (p * 7) % 40)
+        ar, _ = ar_generate(TINY, prompt, 8, session=Session(TINY, SEED, target=tiny_target, mode="bf16"))
+        D, k = combos[p % len(combos)]
+        sd, taus, _ = sd_generate(TINY, prompt, 8, D, k, 0.2, session=Session(
+            TINY, SEED, target=tiny_target, dlayers=views[p % 2], mode="bf16", max_nodes=max(256, 1 + k * D)))
+        assert sd == ar, (p, D, k)
+        assert all(1 <= t <= D + 1 for t in taus)
